@@ -1,0 +1,151 @@
+/*
+ * vfpi.h — C ABI of the B200-native V-FPI contact solver (libvfpi.so).
+ *
+ * Drop-in boundary for the reference's hot path
+ *   condsim.solver.solve_vfpi(aug, cfg, warm, w_cached=None, project_override=None)
+ *   (/root/reference/pkg/src/condsim/solver.py:345-461)
+ * and for the per-iteration subsystems it drives (see each entry point).
+ *
+ * Plain C: pointers and sizes only, fp64 values, int32 indices. All entry
+ * points except vfpi_solve_device/vfpi_wait take HOST pointers, copy to the
+ * device, compute with the sm_100a kernels, copy back and return when done.
+ * A handle is one CUDA stream plus its device workspace; it is not
+ * thread-safe — use one handle per calling thread (the reference calls
+ * solve_vfpi concurrently from a ThreadPoolExecutor, harness.py:762-767).
+ * There is no CPU fallback: without a usable CUDA device every call returns
+ * VFPI_CUDA_ERROR.
+ */
+#ifndef VFPI_H
+#define VFPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes (errors.py:8-40 taxonomy) */
+#define VFPI_OK 0
+#define VFPI_DIVERGED 1          /* DivergenceError: non-finite iterate, trace valid (solver.py:424-427) */
+#define VFPI_INVALID_MATRIX 2    /* InvalidMatrixError: zero row norm (solver.py:220-221) */
+#define VFPI_TIE_VIOLATION 3     /* InvalidMatrixError: broken tie group (solver.py:256-259) */
+#define VFPI_DIM_MISMATCH 4      /* DimensionMismatchError (sparse.py:100-101) */
+#define VFPI_CUDA_ERROR 5
+#define VFPI_UNSUPPORTED 6       /* e.g. two contacts sharing a node column */
+#define VFPI_BAD_ARGUMENT 7
+
+/* SolverConfig.operator (solver.py:33) */
+#define VFPI_OP_STRICT 0
+#define VFPI_OP_PROXIMAL 1
+#define VFPI_OP_STRICT_ANISOTROPIC 2
+/* SolverConfig.step_strategy (solver.py:34) */
+#define VFPI_STEP_FROBENIUS 0
+#define VFPI_STEP_BB1 1
+#define VFPI_STEP_BB2 2
+#define VFPI_STEP_BB_ALTERNATING 3
+#define VFPI_STEP_FIXED_ALPHA 4
+
+typedef struct vfpi_handle vfpi_handle;
+
+/* One augmented system = contacts.AugmentedDynamics (contacts.py:118-128). */
+typedef struct vfpi_system {
+  int64_t n;               /* aug.n: augmented velocity dimension */
+  int64_t n_c;             /* number of nodalized contacts */
+  int64_t nnz;             /* stored entries of aug.a (CSC, both triangles) */
+  const int32_t* indptr;   /* [n+1] SparseSymmetric.indptr  (sparse.py:30-37) */
+  const int32_t* indices;  /* [nnz] SparseSymmetric.indices (row of each entry) */
+  const double* data;      /* [nnz] SparseSymmetric.data */
+  const double* b;         /* [n]   aug.b */
+  const int32_t* col_i;    /* [n_c] aug.col_i: first velocity offset of node i */
+  const int32_t* col_j;    /* [n_c] aug.col_j: node j offset, -1 for S contacts */
+  const double* frames;    /* [n_c*9] aug.frames, row-major rows (n, t1, t2) */
+  const double* mu;        /* [n_c] Contact.mu */
+  const double* mu2;       /* [n_c] Contact.mu2 (mu when None, solver.py:340) */
+  const double* phi;       /* [n_c] Contact.phi_n */
+} vfpi_system;
+
+/* SolverConfig (solver.py:50-62). fixed_alpha = NaN means None. */
+typedef struct vfpi_config {
+  int32_t op;
+  int32_t step_strategy;
+  int32_t max_iters;
+  int32_t chebyshev;
+  int32_t cheby_start;
+  int32_t reserved;
+  double residual_tol;
+  double under_relax;
+  double omega;
+  double fixed_alpha;
+  double consistency_factor;
+} vfpi_config;
+
+/* Outputs of one solve (the (v, lam, SolverReport) triple, solver.py:65-74). */
+typedef struct vfpi_result {
+  double* v;               /* [n] out: v_hat */
+  double* lam;             /* [n_c*3] out: contact-frame impulses */
+  double* residual_trace;  /* [max(max_iters,1)] out: theta per iteration */
+  double* scc;             /* [n_c] out or NULL: SolverReport.scc_residuals */
+  double* w;               /* [n] out or NULL: the step matrix used */
+  int32_t iterations;
+  int32_t converged;
+  int32_t diverged;
+  int32_t status;          /* return code of the solve */
+  double consistency;      /* ||A v - b - J_c^T lam|| */
+  double setup_ms;         /* device time of W/gamma/layout setup */
+  double loop_ms;          /* device time of the iteration kernel */
+} vfpi_result;
+
+int vfpi_create(int device, vfpi_handle** out);
+void vfpi_destroy(vfpi_handle* h);
+const char* vfpi_last_error(const vfpi_handle* h);
+int vfpi_version(void);
+
+/* solve_vfpi (solver.py:345-461). warm: [n]. w_cached: [n] or NULL
+ * (solver.py:349, 370-371). Host pointers; synchronous. Returns VFPI_OK,
+ * VFPI_DIVERGED (res->residual_trace[0..iterations) valid), or an error. */
+int vfpi_solve(vfpi_handle* h, const vfpi_system* sys, const vfpi_config* cfg,
+               const double* warm, const double* w_cached, vfpi_result* res);
+
+/* Same solve with every pointer in sys/warm/w_cached/res already in device
+ * memory; enqueued on `stream` (cudaStream_t, NULL = the handle's stream)
+ * without a host synchronisation. vfpi_wait() synchronises and fills the
+ * scalar fields of res (iterations, converged, ...). */
+int vfpi_solve_device(vfpi_handle* h, const vfpi_system* sys, const vfpi_config* cfg,
+                      const double* warm, const double* w_cached, vfpi_result* res, void* stream);
+int vfpi_wait(vfpi_handle* h, vfpi_result* res);
+
+/* Number of kernels this library launched on the handle since creation. */
+int64_t vfpi_launch_count(const vfpi_handle* h);
+
+/* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */
+void* vfpi_host_alloc(int64_t bytes);
+void vfpi_host_free(void* p);
+
+/* ---- per-subsystem entry points (host pointers, synchronous) ---------- */
+/* spmv (sparse.py:97-102): y = A x over the CSC arrays of sys */
+int vfpi_spmv(vfpi_handle* h, const vfpi_system* sys, const double* x, double* y);
+/* row_norms_sq (sparse.py:105-108) and SparseSymmetric.diagonal (:67-68) */
+int vfpi_row_norms_sq(vfpi_handle* h, const vfpi_system* sys, double* out);
+int vfpi_diagonal(vfpi_handle* h, const vfpi_system* sys, double* out);
+/* step_matrix_frobenius (solver.py:216-229); tie groups from sys contacts */
+int vfpi_step_matrix_frobenius(vfpi_handle* h, const vfpi_system* sys, int pair_tie, double* w);
+/* surrogate_gamma (solver.py:244-253) */
+int vfpi_surrogate_gamma(vfpi_handle* h, const vfpi_system* sys, const double* w, double omega, double* gamma);
+/* apply_jc (contacts.py:402-411): eta [n_c*3] */
+int vfpi_apply_jc(vfpi_handle* h, const vfpi_system* sys, const double* v, double* eta);
+/* apply_jc_t (contacts.py:414-423): out [n] */
+int vfpi_apply_jc_t(vfpi_handle* h, const vfpi_system* sys, const double* lam, double* out);
+/* contact_solve_oneshot (solver.py:262-281): lam [n_c*3] */
+int vfpi_contact_solve_oneshot(vfpi_handle* h, int64_t n_c, const double* gamma, const double* eta,
+                               const double* phi, const double* mu, const double* mu2, int op, double* lam);
+/* scc_residual (solver.py:304-334) */
+int vfpi_scc_residual(vfpi_handle* h, int64_t n_c, const double* vc, const double* lam,
+                      const double* phi, const double* mu, double* out);
+/* inverse_contact (solver.py:468-475) */
+int vfpi_inverse_contact(vfpi_handle* h, const vfpi_system* sys, const double* v, double omega, int op,
+                         double* lam);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VFPI_H */

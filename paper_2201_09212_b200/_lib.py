@@ -1,0 +1,153 @@
+"""ctypes binding of libvfpi.so (include/vfpi.h). Fails loudly if the
+library or a CUDA device is missing — there is no CPU fallback."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvfpi.so")
+
+OK, DIVERGED, INVALID_MATRIX, TIE_VIOLATION, DIM_MISMATCH, CUDA_ERROR, UNSUPPORTED, BAD_ARGUMENT = range(8)
+OPERATORS = {"strict": 0, "proximal": 1, "strict-anisotropic": 2}
+STRATEGIES = {"frobenius": 0, "bb1": 1, "bb2": 2, "bb-alternating": 3, "fixed-alpha": 4}
+
+_i32p = C.POINTER(C.c_int32)
+_f64p = C.POINTER(C.c_double)
+
+
+class VfpiSystem(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("n_c", C.c_int64), ("nnz", C.c_int64),
+        ("indptr", _i32p), ("indices", _i32p), ("data", _f64p), ("b", _f64p),
+        ("col_i", _i32p), ("col_j", _i32p), ("frames", _f64p),
+        ("mu", _f64p), ("mu2", _f64p), ("phi", _f64p),
+    ]
+
+
+class VfpiConfig(C.Structure):
+    _fields_ = [
+        ("op", C.c_int32), ("step_strategy", C.c_int32), ("max_iters", C.c_int32),
+        ("chebyshev", C.c_int32), ("cheby_start", C.c_int32), ("reserved", C.c_int32),
+        ("residual_tol", C.c_double), ("under_relax", C.c_double), ("omega", C.c_double),
+        ("fixed_alpha", C.c_double), ("consistency_factor", C.c_double),
+    ]
+
+
+class VfpiResult(C.Structure):
+    _fields_ = [
+        ("v", _f64p), ("lam", _f64p), ("residual_trace", _f64p), ("scc", _f64p), ("w", _f64p),
+        ("iterations", C.c_int32), ("converged", C.c_int32), ("diverged", C.c_int32), ("status", C.c_int32),
+        ("consistency", C.c_double), ("setup_ms", C.c_double), ("loop_ms", C.c_double),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """Load libvfpi.so (raise if absent: the product has no CPU path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is not built; run `python -m paper_2201_09212_b200.build` "
+                    "(the V-FPI solver has no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            H = C.c_void_p
+            sysp, cfgp, resp = C.POINTER(VfpiSystem), C.POINTER(VfpiConfig), C.POINTER(VfpiResult)
+            sig = {
+                "vfpi_create": (C.c_int, [C.c_int, C.POINTER(H)]),
+                "vfpi_destroy": (None, [H]),
+                "vfpi_last_error": (C.c_char_p, [H]),
+                "vfpi_version": (C.c_int, []),
+                "vfpi_solve": (C.c_int, [H, sysp, cfgp, _f64p, _f64p, resp]),
+                "vfpi_solve_device": (C.c_int, [H, sysp, cfgp, _f64p, _f64p, resp, C.c_void_p]),
+                "vfpi_wait": (C.c_int, [H, resp]),
+                "vfpi_launch_count": (C.c_int64, [H]),
+                "vfpi_host_alloc": (C.c_void_p, [C.c_int64]),
+                "vfpi_host_free": (None, [C.c_void_p]),
+                "vfpi_spmv": (C.c_int, [H, sysp, _f64p, _f64p]),
+                "vfpi_row_norms_sq": (C.c_int, [H, sysp, _f64p]),
+                "vfpi_diagonal": (C.c_int, [H, sysp, _f64p]),
+                "vfpi_step_matrix_frobenius": (C.c_int, [H, sysp, C.c_int, _f64p]),
+                "vfpi_surrogate_gamma": (C.c_int, [H, sysp, _f64p, C.c_double, _f64p]),
+                "vfpi_apply_jc": (C.c_int, [H, sysp, _f64p, _f64p]),
+                "vfpi_apply_jc_t": (C.c_int, [H, sysp, _f64p, _f64p]),
+                "vfpi_contact_solve_oneshot": (C.c_int, [H, C.c_int64, _f64p, _f64p, _f64p, _f64p, _f64p, C.c_int,
+                                                         _f64p]),
+                "vfpi_scc_residual": (C.c_int, [H, C.c_int64, _f64p, _f64p, _f64p, _f64p, _f64p]),
+                "vfpi_inverse_contact": (C.c_int, [H, sysp, _f64p, C.c_double, C.c_int, _f64p]),
+            }
+            for name, (res, args) in sig.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def ptr(a, typ=_f64p):
+    if a is None:
+        return None
+    return a.ctypes.data_as(typ)
+
+
+class Handle:
+    """One device stream + workspace (vfpi_handle). One per thread."""
+
+    def __init__(self, device: int = 0):
+        self.L = lib()
+        h = C.c_void_p()
+        rc = self.L.vfpi_create(int(device), C.byref(h))
+        if rc != OK:
+            raise RuntimeError(f"vfpi_create(device={device}) failed with code {rc}: no usable CUDA device")
+        self.h = h
+        self.device = device
+
+    def error(self) -> str:
+        msg = self.L.vfpi_last_error(self.h)
+        return msg.decode() if msg else ""
+
+    def launches(self) -> int:
+        return int(self.L.vfpi_launch_count(self.h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.L.vfpi_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def handle(device: int | None = None) -> Handle:
+    """Thread-local handle for ``device`` (default: current torch device or 0)."""
+    if device is None:
+        device = int(os.environ.get("VFPI_DEVICE", "0"))
+    hs = getattr(_tls, "handles", None)
+    if hs is None:
+        hs = _tls.handles = {}
+    h = hs.get(device)
+    if h is None:
+        h = hs[device] = Handle(device)
+    return h
+
+
+def as_i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=np.int32)
+
+
+def as_f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=np.float64)

@@ -1,0 +1,581 @@
+// C-ABI (include/vfpi.h): handles, host<->device staging, solve orchestration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vfpi_internal.cuh"
+
+using vfpi::Workspace;
+
+struct vfpi_handle {
+  Workspace ws;
+  std::string err;
+  int64_t launches = 0;
+  // last solve (device path) bookkeeping for vfpi_wait
+  int pending = 0;
+  int max_iters = 0;
+  int* h_flags = nullptr;  // pinned
+};
+
+namespace {
+
+#define CK(x)                                                     \
+  do {                                                            \
+    cudaError_t e_ = (x);                                         \
+    if (e_ != cudaSuccess) {                                      \
+      h->err = std::string(#x) + ": " + cudaGetErrorString(e_);   \
+      return VFPI_CUDA_ERROR;                                     \
+    }                                                             \
+  } while (0)
+
+template <class T>
+T* P(Workspace::Buf& b) { return reinterpret_cast<T*>(b.p); }
+
+int choose_blocks(const vfpi_system& s, int num_sms) {
+  // ~6K stored entries per CTA keeps every SM busy for large systems while
+  // small systems use few CTAs (the grid barrier cost grows with G).
+  const int64_t by_nnz = (s.nnz + 6143) / 6144;
+  const int64_t by_rows = (s.n + 255) / 256;
+  int64_t g = std::max<int64_t>(1, std::min(by_nnz, by_rows * 4));
+  g = std::min<int64_t>(g, 2 * (int64_t)num_sms);
+  return (int)g;
+}
+
+int upload(vfpi_handle* h, Workspace::Buf& b, const void* src, size_t bytes) {
+  if (bytes == 0) return VFPI_OK;
+  CK(vfpi::ensure(b, bytes));
+  CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, h->ws.stream));
+  return VFPI_OK;
+}
+
+// host-side validation common to all entry points (sizes only; the device
+// checks column ranges and overlaps)
+int check_system(vfpi_handle* h, const vfpi_system* s) {
+  if (!s) { h->err = "null system"; return VFPI_BAD_ARGUMENT; }
+  if (s->n < 0 || s->n_c < 0 || s->nnz < 0 || s->n > (int64_t)1 << 30 || s->nnz > ((int64_t)1 << 31) - 1) {
+    h->err = "system sizes out of range";
+    return VFPI_BAD_ARGUMENT;
+  }
+  return VFPI_OK;
+}
+
+// copy a host system into the handle's device input buffers
+int stage_system(vfpi_handle* h, const vfpi_system* s, vfpi_system* d) {
+  Workspace& ws = h->ws;
+  const size_t n = (size_t)s->n, nc = (size_t)s->n_c, nnz = (size_t)s->nnz;
+  int rc;
+  if ((rc = upload(h, ws.b_indptr, s->indptr, 4 * (n + 1)))) return rc;
+  if ((rc = upload(h, ws.b_indices, s->indices, 4 * nnz))) return rc;
+  if ((rc = upload(h, ws.b_data, s->data, 8 * nnz))) return rc;
+  if (s->b && (rc = upload(h, ws.b_b, s->b, 8 * n))) return rc;
+  if (nc) {
+    if ((rc = upload(h, ws.b_ci, s->col_i, 4 * nc))) return rc;
+    if ((rc = upload(h, ws.b_cj, s->col_j, 4 * nc))) return rc;
+    if ((rc = upload(h, ws.b_frames, s->frames, 72 * nc))) return rc;
+    if (s->mu && (rc = upload(h, ws.b_mu, s->mu, 8 * nc))) return rc;
+    if (s->mu2 && (rc = upload(h, ws.b_mu2, s->mu2, 8 * nc))) return rc;
+    if (s->phi && (rc = upload(h, ws.b_phi, s->phi, 8 * nc))) return rc;
+  }
+  *d = *s;
+  d->indptr = P<int32_t>(ws.b_indptr);
+  d->indices = P<int32_t>(ws.b_indices);
+  d->data = P<double>(ws.b_data);
+  d->b = P<double>(ws.b_b);
+  d->col_i = P<int32_t>(ws.b_ci);
+  d->col_j = P<int32_t>(ws.b_cj);
+  d->frames = P<double>(ws.b_frames);
+  d->mu = P<double>(ws.b_mu);
+  d->mu2 = P<double>(ws.b_mu2);
+  d->phi = P<double>(ws.b_phi);
+  return VFPI_OK;
+}
+
+int flags_to_code(vfpi_handle* h, int flags) {
+  if (flags & 2) { h->err = "contact column index out of range"; return VFPI_BAD_ARGUMENT; }
+  if (flags & 1) { h->err = "two contacts share a node column"; return VFPI_UNSUPPORTED; }
+  if (flags & 4) { h->err = "zero row norm in step-matrix computation"; return VFPI_INVALID_MATRIX; }
+  if (flags & 8) { h->err = "step matrix violates the per-node tie groups"; return VFPI_TIE_VIOLATION; }
+  return VFPI_OK;
+}
+
+// layout for the per-op entry points (CSR order, no contact partition needed)
+int op_layout(vfpi_handle* h, const vfpi_system& d, bool with_contacts) {
+  vfpi_system dd = d;
+  if (!with_contacts) dd.n_c = 0;
+  vfpi::SetupSummary* hs = h->ws.h_summary;
+  int rc = vfpi::setup_layout(h->ws, dd, 1, h->ws.stream, hs, h->err, h->launches);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vfpi_version(void) { return 1; }
+
+int vfpi_create(int device, vfpi_handle** out) {
+  if (!out) return VFPI_BAD_ARGUMENT;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0 || device < 0 || device >= count)
+    return VFPI_CUDA_ERROR;
+  if (cudaSetDevice(device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  vfpi_handle* h = new vfpi_handle();
+  h->ws.device = device;
+  cudaDeviceGetAttribute(&h->ws.num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&h->ws.stream, cudaStreamNonBlocking) != cudaSuccess) { delete h; return VFPI_CUDA_ERROR; }
+  for (auto& e : h->ws.ev) cudaEventCreate(&e);
+  cudaMallocHost(&h->ws.h_summary, sizeof(vfpi::SetupSummary));
+  cudaMallocHost(&h->ws.h_status, sizeof(vfpi::SolveStatus));
+  cudaMallocHost(&h->h_flags, 16);
+  *out = h;
+  return VFPI_OK;
+}
+
+void vfpi_destroy(vfpi_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->ws.device);
+  cudaStreamSynchronize(h->ws.stream);
+  Workspace::Buf* bufs[] = {&h->ws.b_indptr, &h->ws.b_indices, &h->ws.b_data, &h->ws.b_b, &h->ws.b_ci,
+                            &h->ws.b_cj, &h->ws.b_frames, &h->ws.b_mu, &h->ws.b_mu2, &h->ws.b_phi,
+                            &h->ws.b_warm, &h->ws.b_wc, &h->ws.b_out_v, &h->ws.b_out_lam, &h->ws.b_trace,
+                            &h->ws.b_scc, &h->ws.b_w_out, &h->ws.diag, &h->ws.rns, &h->ws.w, &h->ws.gamma,
+                            &h->ws.w_mean, &h->ws.rowcnt, &h->ws.row_ptr, &h->ws.keys, &h->ws.keys_sorted,
+                            &h->ws.vals, &h->ws.perm, &h->ws.colof, &h->ws.mark, &h->ws.ucost, &h->ws.cpos,
+                            &h->ws.urows, &h->ws.rpos, &h->ws.ucont, &h->ws.kpos, &h->ws.blk_row, &h->ws.blk_ct,
+                            &h->ws.blk_slice, &h->ws.row_list, &h->ws.row_slot, &h->ws.cont_list,
+                            &h->ws.slice_w, &h->ws.slice_off, &h->ws.sell_val, &h->ws.sell_col, &h->ws.vbuf,
+                            &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
+                            &h->ws.cub_tmp, &h->ws.x, &h->ws.y};
+  for (auto* b : bufs)
+    if (b->p) cudaFree(b->p);
+  for (auto& e : h->ws.ev)
+    if (e) cudaEventDestroy(e);
+  if (h->ws.stream) cudaStreamDestroy(h->ws.stream);
+  if (h->ws.h_summary) cudaFreeHost(h->ws.h_summary);
+  if (h->ws.h_status) cudaFreeHost(h->ws.h_status);
+  if (h->h_flags) cudaFreeHost(h->h_flags);
+  delete h;
+}
+
+const char* vfpi_last_error(const vfpi_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int64_t vfpi_launch_count(const vfpi_handle* h) { return h ? h->launches : 0; }
+
+void* vfpi_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, (size_t)std::max<int64_t>(bytes, 8)) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void vfpi_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* cfg, const double* warm,
+                      const double* w_cached, vfpi_result* res, void* stream_) {
+  if (!h || !cfg || !res || !warm) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, d);
+  if (rc) return rc;
+  if (cfg->op < 0 || cfg->op > 2 || cfg->step_strategy < 0 || cfg->step_strategy > 4 || cfg->max_iters < 0) {
+    h->err = "bad solver config";
+    return VFPI_BAD_ARGUMENT;
+  }
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  Workspace& ws = h->ws;
+  cudaStream_t st = stream_ ? (cudaStream_t)stream_ : ws.stream;
+  const int n = (int)d->n, n_c = (int)d->n_c;
+  const bool cheb = cfg->chebyshev != 0;
+  const bool bb = cfg->step_strategy >= VFPI_STEP_BB1 && cfg->step_strategy <= VFPI_STEP_BB_ALTERNATING;
+
+  CK(cudaEventRecord(ws.ev[0], st));
+  int G = choose_blocks(*d, ws.num_sms);
+  vfpi::SetupSummary* hs = ws.h_summary;
+  int smem = 0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches);
+    if (rc) return rc;
+    smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
+    const int bps = vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem);
+    if (bps <= 0) { h->err = "iteration kernel does not fit on an SM"; return VFPI_UNSUPPORTED; }
+    if (G <= bps * ws.num_sms) break;
+    G = bps * ws.num_sms;
+  }
+  rc = vfpi::setup_step_matrix(ws, *d, *cfg, w_cached, st, h->err, h->launches);
+  if (rc) return rc;
+
+  const int tr = std::max(cfg->max_iters, 1);
+  CK(vfpi::ensure(ws.vbuf, 3 * 8 * (size_t)std::max(n, 1)));
+  CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)std::max(n_c, 1)));
+  CK(vfpi::ensure(ws.partials, 2 * 8 * (size_t)G * vfpi::kPartialStride));
+  CK(vfpi::ensure(ws.status, sizeof(vfpi::SolveStatus)));
+  double* vb = P<double>(ws.vbuf);
+  double* lb = P<double>(ws.lambuf);
+  if (n > 0) {
+    CK(cudaMemcpyAsync(vb, warm, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(vb + 2 * (size_t)n, warm, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaMemsetAsync(lb, 0, 2 * 24 * (size_t)std::max(n_c, 1), st));
+  CK(cudaMemsetAsync(ws.status.p, 0, sizeof(vfpi::SolveStatus), st));
+  CK(cudaEventRecord(ws.ev[1], st));
+
+  vfpi::IterParams p{};
+  p.n = n;
+  p.n_c = n_c;
+  p.G = G;
+  p.row_list = P<int>(ws.row_list);
+  p.row_slot = P<int>(ws.row_slot);
+  p.blk_row = P<int>(ws.blk_row);
+  p.blk_slice = P<int>(ws.blk_slice);
+  p.blk_ct = P<int>(ws.blk_ct);
+  p.slice_off = P<int64_t>(ws.slice_off);
+  p.sell_val = P<double>(ws.sell_val);
+  p.sell_col = P<int>(ws.sell_col);
+  p.cont_list = P<int>(ws.cont_list);
+  p.b = d->b;
+  p.w = P<double>(ws.w);
+  p.gamma = P<double>(ws.gamma);
+  p.col_i = d->col_i;
+  p.col_j = d->col_j;
+  p.frames = d->frames;
+  p.mu = d->mu;
+  p.mu2 = d->mu2;
+  p.phi = d->phi;
+  p.w_mean = P<double>(ws.w_mean);
+  p.vbuf0 = vb;
+  p.vbuf1 = vb + (size_t)n;
+  p.vbuf2 = vb + 2 * (size_t)n;
+  p.lam0 = lb;
+  p.lam1 = lb + 3 * (size_t)std::max(n_c, 1);
+  p.partials = P<double>(ws.partials);
+  p.trace = res->residual_trace;
+  p.status = P<vfpi::SolveStatus>(ws.status);
+  p.out_v = res->v;
+  p.out_lam = res->lam;
+  p.max_iters = cfg->max_iters;
+  p.cheby_start = cfg->cheby_start;
+  p.step = cfg->step_strategy;
+  p.tol = cfg->residual_tol;
+  p.under_relax = cfg->under_relax;
+  p.omega = cfg->omega;
+  p.cfactor = cfg->consistency_factor;
+  (void)tr;
+  rc = vfpi::launch_iterate(p, cfg->op, cheb, bb, smem, st, h->err);
+  if (rc) return rc;
+  ++h->launches;
+  CK(cudaEventRecord(ws.ev[2], st));
+  if (res->scc && n_c > 0) {
+    rc = vfpi::launch_scc_final(p, res->scc, st);
+    if (rc) { h->err = "scc kernel launch failed"; return rc; }
+    ++h->launches;
+  }
+  if (res->w && n > 0) CK(cudaMemcpyAsync(res->w, ws.w.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(ws.h_status, ws.status.p, sizeof(vfpi::SolveStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->h_flags, ws.flags.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(ws.ev[3], st));
+  h->pending = 1;
+  h->max_iters = cfg->max_iters;
+  return VFPI_OK;
+}
+
+int vfpi_wait(vfpi_handle* h, vfpi_result* res) {
+  if (!h || !res) return VFPI_BAD_ARGUMENT;
+  if (!h->pending) { h->err = "no solve pending"; return VFPI_BAD_ARGUMENT; }
+  cudaSetDevice(h->ws.device);
+  h->pending = 0;
+  CK(cudaEventSynchronize(h->ws.ev[3]));
+  const vfpi::SolveStatus& s = *h->ws.h_status;
+  res->iterations = s.iterations;
+  res->converged = s.converged;
+  res->diverged = s.diverged;
+  res->consistency = s.consistency;
+  float a = 0.f, b = 0.f;
+  cudaEventElapsedTime(&a, h->ws.ev[0], h->ws.ev[1]);
+  cudaEventElapsedTime(&b, h->ws.ev[1], h->ws.ev[2]);
+  res->setup_ms = a;
+  res->loop_ms = b;
+  int rc = flags_to_code(h, *h->h_flags);
+  if (!rc && s.diverged) {
+    h->err = "non-finite iterate in V-FPI";
+    rc = VFPI_DIVERGED;
+  }
+  res->status = rc;
+  return rc;
+}
+
+int vfpi_solve(vfpi_handle* h, const vfpi_system* s, const vfpi_config* cfg, const double* warm,
+               const double* w_cached, vfpi_result* res) {
+  if (!h || !cfg || !res || !warm) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  Workspace& ws = h->ws;
+  vfpi_system d;
+  if ((rc = stage_system(h, s, &d))) return rc;
+  const size_t n = (size_t)s->n, nc = (size_t)s->n_c;
+  if ((rc = upload(h, ws.b_warm, warm, 8 * n))) return rc;
+  CK(vfpi::ensure(ws.b_warm, 8 * n));
+  const double* dwc = nullptr;
+  if (w_cached) {
+    if ((rc = upload(h, ws.b_wc, w_cached, 8 * n))) return rc;
+    dwc = P<double>(ws.b_wc);
+  }
+  const size_t tr = (size_t)std::max(cfg->max_iters, 1);
+  CK(vfpi::ensure(ws.b_out_v, 8 * std::max<size_t>(n, 1)));
+  CK(vfpi::ensure(ws.b_out_lam, 24 * std::max<size_t>(nc, 1)));
+  CK(vfpi::ensure(ws.b_trace, 8 * tr));
+  CK(vfpi::ensure(ws.b_scc, 8 * std::max<size_t>(nc, 1)));
+  CK(vfpi::ensure(ws.b_w_out, 8 * std::max<size_t>(n, 1)));
+  vfpi_result dres = *res;
+  dres.v = P<double>(ws.b_out_v);
+  dres.lam = P<double>(ws.b_out_lam);
+  dres.residual_trace = P<double>(ws.b_trace);
+  dres.scc = res->scc ? P<double>(ws.b_scc) : nullptr;
+  dres.w = res->w ? P<double>(ws.b_w_out) : nullptr;
+  rc = vfpi_solve_device(h, &d, cfg, P<double>(ws.b_warm), dwc, &dres, ws.stream);
+  if (rc) {
+    cudaStreamSynchronize(ws.stream);
+    return rc;
+  }
+  if (n) CK(cudaMemcpyAsync(res->v, dres.v, 8 * n, cudaMemcpyDeviceToHost, ws.stream));
+  if (nc) CK(cudaMemcpyAsync(res->lam, dres.lam, 24 * nc, cudaMemcpyDeviceToHost, ws.stream));
+  if (res->residual_trace && cfg->max_iters > 0)
+    CK(cudaMemcpyAsync(res->residual_trace, dres.residual_trace, 8 * (size_t)cfg->max_iters, cudaMemcpyDeviceToHost,
+                       ws.stream));
+  if (res->scc && nc) CK(cudaMemcpyAsync(res->scc, dres.scc, 8 * nc, cudaMemcpyDeviceToHost, ws.stream));
+  if (res->w && n) CK(cudaMemcpyAsync(res->w, dres.w, 8 * n, cudaMemcpyDeviceToHost, ws.stream));
+  // the copies above are ordered after ev[3] on the same stream
+  CK(cudaStreamSynchronize(ws.stream));
+  rc = vfpi_wait(h, &dres);
+  res->iterations = dres.iterations;
+  res->converged = dres.converged;
+  res->diverged = dres.diverged;
+  res->consistency = dres.consistency;
+  res->setup_ms = dres.setup_ms;
+  res->loop_ms = dres.loop_ms;
+  res->status = rc;
+  return rc;
+}
+
+// ---- per-subsystem entry points -------------------------------------------
+
+int vfpi_spmv(vfpi_handle* h, const vfpi_system* s, const double* x, double* y) {
+  if (!h || !x || !y) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  cudaSetDevice(h->ws.device);
+  Workspace& ws = h->ws;
+  vfpi_system d, s0 = *s;
+  s0.n_c = 0;
+  if ((rc = stage_system(h, &s0, &d))) return rc;
+  const size_t n = (size_t)s->n;
+  if ((rc = upload(h, ws.x, x, 8 * n))) return rc;
+  CK(vfpi::ensure(ws.y, 8 * std::max<size_t>(n, 1)));
+  if ((rc = op_layout(h, d, false))) return rc;
+  vfpi::launch_spmv_csr_rows((int64_t)n, P<int64_t>(ws.row_ptr), P<int>(ws.perm), P<int>(ws.colof), d.data,
+                             P<double>(ws.x), P<double>(ws.y), ws.stream);
+  ++h->launches;
+  CK(cudaGetLastError());
+  if (n) CK(cudaMemcpyAsync(y, ws.y.p, 8 * n, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaStreamSynchronize(ws.stream));
+  return VFPI_OK;
+}
+
+static int stats_op(vfpi_handle* h, const vfpi_system* s, double* out, bool rns) {
+  if (!h || !out) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  cudaSetDevice(h->ws.device);
+  vfpi_system d, s0 = *s;
+  s0.n_c = 0;
+  if ((rc = stage_system(h, &s0, &d))) return rc;
+  if ((rc = op_layout(h, d, false))) return rc;
+  const size_t n = (size_t)s->n;
+  if (n) CK(cudaMemcpyAsync(out, rns ? h->ws.rns.p : h->ws.diag.p, 8 * n, cudaMemcpyDeviceToHost, h->ws.stream));
+  CK(cudaStreamSynchronize(h->ws.stream));
+  return VFPI_OK;
+}
+
+int vfpi_row_norms_sq(vfpi_handle* h, const vfpi_system* s, double* out) { return stats_op(h, s, out, true); }
+int vfpi_diagonal(vfpi_handle* h, const vfpi_system* s, double* out) { return stats_op(h, s, out, false); }
+
+int vfpi_step_matrix_frobenius(vfpi_handle* h, const vfpi_system* s, int pair_tie, double* w) {
+  if (!h || !w) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  cudaSetDevice(h->ws.device);
+  vfpi_system d;
+  if ((rc = stage_system(h, s, &d))) return rc;
+  if ((rc = op_layout(h, d, true))) return rc;
+  vfpi_config cfg{};
+  cfg.op = pair_tie ? VFPI_OP_PROXIMAL : VFPI_OP_STRICT;
+  cfg.step_strategy = VFPI_STEP_FROBENIUS;
+  if ((rc = vfpi::setup_step_matrix(h->ws, d, cfg, nullptr, h->ws.stream, h->err, h->launches))) return rc;
+  const size_t n = (size_t)s->n;
+  if (n) CK(cudaMemcpyAsync(w, h->ws.w.p, 8 * n, cudaMemcpyDeviceToHost, h->ws.stream));
+  CK(cudaMemcpyAsync(h->h_flags, h->ws.flags.p, 4, cudaMemcpyDeviceToHost, h->ws.stream));
+  CK(cudaStreamSynchronize(h->ws.stream));
+  return flags_to_code(h, *h->h_flags);
+}
+
+int vfpi_surrogate_gamma(vfpi_handle* h, const vfpi_system* s, const double* w, double omega, double* gamma) {
+  if (!h || !w || !gamma) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  cudaSetDevice(h->ws.device);
+  vfpi_system d;
+  if ((rc = stage_system(h, s, &d))) return rc;
+  if ((rc = upload(h, h->ws.b_wc, w, 8 * (size_t)s->n))) return rc;
+  vfpi_config cfg{};
+  cfg.op = VFPI_OP_STRICT;
+  cfg.step_strategy = VFPI_STEP_FROBENIUS;
+  cfg.omega = omega;
+  CK(vfpi::ensure(h->ws.flags, 16));
+  CK(cudaMemsetAsync(h->ws.flags.p, 0, 16, h->ws.stream));
+  if ((rc = vfpi::setup_step_matrix(h->ws, d, cfg, P<double>(h->ws.b_wc), h->ws.stream, h->err, h->launches)))
+    return rc;
+  const size_t nc = (size_t)s->n_c;
+  if (nc) CK(cudaMemcpyAsync(gamma, h->ws.gamma.p, 8 * nc, cudaMemcpyDeviceToHost, h->ws.stream));
+  CK(cudaMemcpyAsync(h->h_flags, h->ws.flags.p, 4, cudaMemcpyDeviceToHost, h->ws.stream));
+  CK(cudaStreamSynchronize(h->ws.stream));
+  return flags_to_code(h, *h->h_flags);
+}
+
+int vfpi_apply_jc(vfpi_handle* h, const vfpi_system* s, const double* v, double* eta) {
+  if (!h || !v || !eta) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  cudaSetDevice(h->ws.device);
+  Workspace& ws = h->ws;
+  const size_t n = (size_t)s->n, nc = (size_t)s->n_c;
+  if ((rc = upload(h, ws.b_ci, s->col_i, 4 * nc))) return rc;
+  if ((rc = upload(h, ws.b_cj, s->col_j, 4 * nc))) return rc;
+  if ((rc = upload(h, ws.b_frames, s->frames, 72 * nc))) return rc;
+  if ((rc = upload(h, ws.x, v, 8 * n))) return rc;
+  CK(vfpi::ensure(ws.y, 24 * std::max<size_t>(nc, 1)));
+  vfpi::launch_apply_jc((int64_t)nc, P<int>(ws.b_ci), P<int>(ws.b_cj), P<double>(ws.b_frames), P<double>(ws.x),
+                        P<double>(ws.y), ws.stream);
+  ++h->launches;
+  CK(cudaGetLastError());
+  if (nc) CK(cudaMemcpyAsync(eta, ws.y.p, 24 * nc, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaStreamSynchronize(ws.stream));
+  return VFPI_OK;
+}
+
+int vfpi_apply_jc_t(vfpi_handle* h, const vfpi_system* s, const double* lam, double* out) {
+  if (!h || !lam || !out) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  cudaSetDevice(h->ws.device);
+  Workspace& ws = h->ws;
+  const size_t n = (size_t)s->n, nc = (size_t)s->n_c;
+  // column overlap decides between the parallel scatter and the ordered one
+  bool overlap = false;
+  {
+    std::vector<unsigned char> used(n + 3, 0);
+    for (size_t m = 0; m < nc && !overlap; ++m) {
+      const int cols[2] = {s->col_i[m], s->col_j[m]};
+      for (int c : cols) {
+        if (c < 0) continue;
+        if ((size_t)c + 3 > n) { h->err = "contact column out of range"; return VFPI_BAD_ARGUMENT; }
+        for (int t = 0; t < 3; ++t) {
+          if (used[c + t]) overlap = true;
+          used[c + t] = 1;
+        }
+      }
+    }
+  }
+  if ((rc = upload(h, ws.b_ci, s->col_i, 4 * nc))) return rc;
+  if ((rc = upload(h, ws.b_cj, s->col_j, 4 * nc))) return rc;
+  if ((rc = upload(h, ws.b_frames, s->frames, 72 * nc))) return rc;
+  if ((rc = upload(h, ws.x, lam, 24 * nc))) return rc;
+  CK(vfpi::ensure(ws.y, 8 * std::max<size_t>(n, 1)));
+  vfpi::launch_apply_jc_t((int64_t)n, (int64_t)nc, P<int>(ws.b_ci), P<int>(ws.b_cj), P<double>(ws.b_frames),
+                          P<double>(ws.x), P<double>(ws.y), overlap, ws.stream);
+  ++h->launches;
+  CK(cudaGetLastError());
+  if (n) CK(cudaMemcpyAsync(out, ws.y.p, 8 * n, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaStreamSynchronize(ws.stream));
+  return VFPI_OK;
+}
+
+int vfpi_contact_solve_oneshot(vfpi_handle* h, int64_t n_c, const double* gamma, const double* eta,
+                               const double* phi, const double* mu, const double* mu2, int op, double* lam) {
+  if (!h || n_c < 0 || op < 0 || op > 2) return VFPI_BAD_ARGUMENT;
+  if (n_c == 0) return VFPI_OK;
+  cudaSetDevice(h->ws.device);
+  Workspace& ws = h->ws;
+  const size_t nc = (size_t)n_c;
+  int rc;
+  if ((rc = upload(h, ws.gamma, gamma, 8 * nc))) return rc;
+  if ((rc = upload(h, ws.x, eta, 24 * nc))) return rc;
+  if ((rc = upload(h, ws.b_phi, phi, 8 * nc))) return rc;
+  if ((rc = upload(h, ws.b_mu, mu, 8 * nc))) return rc;
+  if ((rc = upload(h, ws.b_mu2, mu2 ? mu2 : mu, 8 * nc))) return rc;
+  CK(vfpi::ensure(ws.y, 24 * nc));
+  vfpi::launch_oneshot(n_c, P<double>(ws.gamma), P<double>(ws.x), P<double>(ws.b_phi), P<double>(ws.b_mu),
+                       P<double>(ws.b_mu2), op, P<double>(ws.y), ws.stream);
+  ++h->launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(lam, ws.y.p, 24 * nc, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaStreamSynchronize(ws.stream));
+  return VFPI_OK;
+}
+
+int vfpi_scc_residual(vfpi_handle* h, int64_t n_c, const double* vc, const double* lam, const double* phi,
+                      const double* mu, double* out) {
+  if (!h || n_c < 0) return VFPI_BAD_ARGUMENT;
+  if (n_c == 0) return VFPI_OK;
+  cudaSetDevice(h->ws.device);
+  Workspace& ws = h->ws;
+  const size_t nc = (size_t)n_c;
+  int rc;
+  if ((rc = upload(h, ws.x, vc, 24 * nc))) return rc;
+  if ((rc = upload(h, ws.b_out_lam, lam, 24 * nc))) return rc;
+  if ((rc = upload(h, ws.b_phi, phi, 8 * nc))) return rc;
+  if ((rc = upload(h, ws.b_mu, mu, 8 * nc))) return rc;
+  CK(vfpi::ensure(ws.y, 8 * nc));
+  vfpi::launch_scc(n_c, P<double>(ws.x), P<double>(ws.b_out_lam), P<double>(ws.b_phi), P<double>(ws.b_mu),
+                   P<double>(ws.y), ws.stream);
+  ++h->launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, ws.y.p, 8 * nc, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaStreamSynchronize(ws.stream));
+  return VFPI_OK;
+}
+
+int vfpi_inverse_contact(vfpi_handle* h, const vfpi_system* s, const double* v, double omega, int op, double* lam) {
+  if (!h || !v || !lam || op < 0 || op > 2) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  cudaSetDevice(h->ws.device);
+  Workspace& ws = h->ws;
+  const size_t n = (size_t)s->n, nc = (size_t)s->n_c;
+  if (nc == 0) return VFPI_OK;
+  if ((rc = upload(h, ws.b_ci, s->col_i, 4 * nc))) return rc;
+  if ((rc = upload(h, ws.b_cj, s->col_j, 4 * nc))) return rc;
+  if ((rc = upload(h, ws.b_frames, s->frames, 72 * nc))) return rc;
+  if ((rc = upload(h, ws.b_phi, s->phi, 8 * nc))) return rc;
+  if ((rc = upload(h, ws.b_mu, s->mu, 8 * nc))) return rc;
+  if ((rc = upload(h, ws.b_mu2, s->mu2 ? s->mu2 : s->mu, 8 * nc))) return rc;
+  if ((rc = upload(h, ws.x, v, 8 * n))) return rc;
+  CK(vfpi::ensure(ws.y, 24 * nc));
+  CK(vfpi::ensure(ws.gamma, 8 * nc));
+  CK(vfpi::ensure(ws.b_out_lam, 24 * nc));
+  vfpi::launch_const_fill(P<double>(ws.gamma), omega, (int64_t)nc, ws.stream);
+  vfpi::launch_apply_jc((int64_t)nc, P<int>(ws.b_ci), P<int>(ws.b_cj), P<double>(ws.b_frames), P<double>(ws.x),
+                        P<double>(ws.y), ws.stream);
+  vfpi::launch_oneshot((int64_t)nc, P<double>(ws.gamma), P<double>(ws.y), P<double>(ws.b_phi), P<double>(ws.b_mu),
+                       P<double>(ws.b_mu2), op, P<double>(ws.b_out_lam), ws.stream);
+  h->launches += 3;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(lam, ws.b_out_lam.p, 24 * nc, cudaMemcpyDeviceToHost, ws.stream));
+  CK(cudaStreamSynchronize(ws.stream));
+  return VFPI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,543 @@
+// Per-solve setup on the device: CSC -> row-sorted numeric entries, contact-
+// aware CTA partition, SELL-32 packing, Frobenius step matrix and gamma.
+//
+// Reference semantics:
+//   SparseSymmetric.diagonal     sparse.py:67-68
+//   row_norms_sq                 sparse.py:105-108 (reduceat over pruned squares)
+//   step_matrix_frobenius        solver.py:216-229 (tie groups solver.py:182-213)
+//   surrogate_gamma / _check_tie solver.py:244-259
+//   fixed-alpha default          solver.py:367-369
+#include <cub/cub.cuh>
+#include <climits>
+
+#include "vfpi_internal.cuh"
+#include "vfpi_math.cuh"
+
+namespace vfpi {
+
+namespace {
+
+constexpr int kRowCost = 2;      // per-row overhead in the partition cost model
+constexpr int kContactCost = 24; // per-contact work in the partition cost model
+
+#define VFPI_CK(x)                                                     \
+  do {                                                                 \
+    cudaError_t e_ = (x);                                              \
+    if (e_ != cudaSuccess) {                                           \
+      err = std::string(#x) + ": " + cudaGetErrorString(e_);           \
+      return VFPI_CUDA_ERROR;                                          \
+    }                                                                  \
+  } while (0)
+
+inline int nblk(int64_t n, int t = 256) { return (int)((n + t - 1) / t); }
+
+// ---------------------------------------------------------------------------
+// column statistics: diagonal, squared norms, numeric row counts, sort keys
+// ---------------------------------------------------------------------------
+struct PrunedSquares {
+  const double* data;
+  int e0, e1;
+  mutable int cur_e;
+  mutable int64_t cur_k;
+  __device__ double operator()(int64_t k) const {
+    if (k < cur_k) { cur_k = -1; cur_e = e0 - 1; }
+    while (cur_k < k) {
+      ++cur_e;
+      const double d = data[cur_e];
+      if (dmul(d, d) != 0.0) ++cur_k;
+    }
+    const double d = data[cur_e];
+    return dmul(d, d);
+  }
+};
+
+__global__ void k_colstats(int n, const int* __restrict__ indptr, const int* __restrict__ indices,
+                           const double* __restrict__ data, double* __restrict__ diag, double* __restrict__ rns,
+                           int* __restrict__ rowcnt, int* __restrict__ keys, int* __restrict__ colof) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int e0 = indptr[j], e1 = indptr[j + 1];
+  double dg = 0.0;
+  int64_t npr = 0;
+  for (int e = e0; e < e1; ++e) {
+    const int i = indices[e];
+    const double d = data[e];
+    if (i == j) dg = dadd(dg, d);
+    if (dmul(d, d) != 0.0) ++npr;
+    const bool num = (d != 0.0);
+    keys[e] = num ? i : n;
+    colof[e] = j;
+    if (num) atomicAdd(&rowcnt[i], 1);
+  }
+  diag[j] = dg;
+  double r = 0.0;
+  if (npr > 0) {
+    PrunedSquares g{data, e0, e1, e0 - 1, -1};
+    const double first = g(0);
+    r = (npr == 1) ? first : dadd(first, np_pairwise(g, 1, npr - 1));
+  }
+  rns[j] = r;
+}
+
+__global__ void k_mark(int n, int n_c, const int* __restrict__ ci, const int* __restrict__ cj, int* mark,
+                       int* flags) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n_c) return;
+  const int i = ci[m], j = cj[m];
+  if (i < 0 || i > n - 3 || j < -1 || (j >= 0 && j > n - 3)) { atomicOr(flags, 2); return; }
+  for (int t = 0; t < 3; ++t)
+    if (atomicCAS(&mark[i + t], -1, m) != -1) atomicOr(flags, 1);
+  if (j >= 0)
+    for (int t = 0; t < 3; ++t)
+      if (atomicCAS(&mark[j + t], -1, m) != -1) atomicOr(flags, 1);
+}
+
+// unit = one free row, or all (3 or 6) rows of one contact, anchored at col_i
+__global__ void k_units(int n, const int* __restrict__ mark, const int* __restrict__ ci, const int* __restrict__ cj,
+                        const int* __restrict__ rowcnt, int64_t* ucost, int* urows, int* ucont) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int m = mark[r];
+  int64_t cost = 0;
+  int rows = 0, ct = 0;
+  if (m < 0) {
+    cost = rowcnt[r] + kRowCost;
+    rows = 1;
+  } else if (r == ci[m]) {
+    const int i = ci[m], j = cj[m];
+    ct = 1;
+    rows = (j >= 0) ? 6 : 3;
+    cost = kContactCost;
+    for (int t = 0; t < 3; ++t) cost += rowcnt[i + t] + kRowCost;
+    if (j >= 0)
+      for (int t = 0; t < 3; ++t) cost += rowcnt[j + t] + kRowCost;
+  }
+  ucost[r] = cost;
+  urows[r] = rows;
+  ucont[r] = ct;
+}
+
+__global__ void k_blocks(int n, int G, const int64_t* __restrict__ ucost, const int64_t* __restrict__ cpos,
+                         const int* __restrict__ urows, const int* __restrict__ rpos, const int* __restrict__ kpos,
+                         int* blk_row, int* blk_ct) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || urows[r] == 0) return;
+  const int64_t total = cpos[n - 1] + ucost[n - 1];
+  int64_t b = total > 0 ? (cpos[r] * (int64_t)G) / total : 0;
+  if (b > G - 1) b = G - 1;
+  atomicMin(&blk_row[b], rpos[r]);
+  atomicMin(&blk_ct[b], kpos[r]);
+}
+
+__global__ void k_blocks_fix(int n, int n_c, int G, int* blk_row, int* blk_ct, int* blk_slice, SetupSummary* sum) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  blk_row[G] = n;
+  blk_ct[G] = n_c;
+  for (int b = G - 1; b >= 0; --b) {
+    if (blk_row[b] == INT_MAX) blk_row[b] = blk_row[b + 1];
+    if (blk_ct[b] == INT_MAX) blk_ct[b] = blk_ct[b + 1];
+  }
+  blk_row[0] = 0;
+  blk_ct[0] = 0;
+  int s = 0, mx = 0;
+  for (int b = 0; b < G; ++b) {
+    blk_slice[b] = s;
+    s += (blk_row[b + 1] - blk_row[b] + 31) / 32;
+    const int c = blk_ct[b + 1] - blk_ct[b];
+    mx = c > mx ? c : mx;
+  }
+  blk_slice[G] = s;
+  sum->n_slices = s;
+  sum->max_ct_per_blk = mx;
+}
+
+__device__ __forceinline__ int owner(const int* __restrict__ starts, int G, int p) {
+  // largest b with starts[b] <= p (starts has G+1 monotone entries)
+  int lo = 0, hi = G;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (starts[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_fill(int n, int G, const int* __restrict__ mark, const int* __restrict__ ci,
+                       const int* __restrict__ cj, const int* __restrict__ urows, const int* __restrict__ rpos,
+                       const int* __restrict__ kpos, const int* __restrict__ blk_row, const int* __restrict__ blk_ct,
+                       int* row_list, int* row_slot, int* cont_list) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || urows[r] == 0) return;
+  const int p = rpos[r];
+  const int m = mark[r];
+  if (m < 0) {
+    row_list[p] = r;
+    row_slot[p] = -1;
+    return;
+  }
+  const int b = owner(blk_row, G, p);
+  const int k = kpos[r];
+  const int loc = (k - blk_ct[b]) * kSlotsPerContact;
+  cont_list[k] = m;
+  const int i = ci[m], j = cj[m];
+  for (int t = 0; t < 3; ++t) {
+    row_list[p + t] = i + t;
+    row_slot[p + t] = loc + t;
+  }
+  if (j >= 0)
+    for (int t = 0; t < 3; ++t) {
+      row_list[p + 3 + t] = j + t;
+      row_slot[p + 3 + t] = loc + 3 + t;
+    }
+}
+
+__global__ void k_slice_width(int S_max, int G, const SetupSummary* __restrict__ sum,
+                              const int* __restrict__ blk_slice, const int* __restrict__ blk_row,
+                              const int* __restrict__ row_list, const int* __restrict__ rowcnt, int64_t* width) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > S_max) return;
+  const int S = sum->n_slices;
+  if (s >= S) { width[s] = 0; return; }
+  const int b = owner(blk_slice, G, s);
+  const int p0 = blk_row[b] + (s - blk_slice[b]) * 32;
+  const int p1 = min(p0 + 32, blk_row[b + 1]);
+  int W = 0;
+  for (int p = p0; p < p1; ++p) W = max(W, rowcnt[row_list[p]]);
+  width[s] = 32 * (int64_t)W;
+}
+
+__global__ void k_summary(int n, const int64_t* row_ptr, const int64_t* slice_off, const int* flags,
+                          SetupSummary* sum) {
+  sum->nnz_num = row_ptr[n];
+  sum->sell_elems = slice_off[sum->n_slices];
+  sum->flags = *flags;
+}
+
+__global__ void k_iota(int64_t n, int* v) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < n) v[e] = (int)e;
+}
+
+// one warp per slice: lane k-th entry of its row at off + k*32 + lane
+__global__ void k_pack(int S, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_row,
+                       const int* __restrict__ row_list, const int* __restrict__ rowcnt,
+                       const int64_t* __restrict__ row_ptr, const int* __restrict__ perm,
+                       const int* __restrict__ colof, const double* __restrict__ data,
+                       const int64_t* __restrict__ slice_off, double* __restrict__ sv, int* __restrict__ sc) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= S) return;
+  const int b = owner(blk_slice, G, s);
+  const int p = blk_row[b] + (s - blk_slice[b]) * 32 + lane;
+  const bool valid = p < blk_row[b + 1];
+  const int row = valid ? row_list[p] : 0;
+  const int len = valid ? rowcnt[row] : 0;
+  const int64_t base = valid ? row_ptr[row] : 0;
+  const int64_t off = slice_off[s];
+  const int W = (int)((slice_off[s + 1] - off) >> 5);
+  for (int k = 0; k < W; ++k) {
+    const int64_t dst = off + (int64_t)k * 32 + lane;
+    if (k < len) {
+      const int e = perm[base + k];
+      sv[dst] = data[e];
+      sc[dst] = colof[e];
+    } else {
+      sv[dst] = 0.0;
+      sc[dst] = -1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// step matrix W and surrogate Delassus gamma
+// ---------------------------------------------------------------------------
+__global__ void k_w_frob(int n, const double* __restrict__ diag, const double* __restrict__ rns, double* w,
+                         int* flags) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  if (rns[r] <= 0.0) atomicOr(flags, 4);
+  w[r] = ddiv(diag[r], rns[r]);
+}
+
+// tie groups: strict ties each contacted node's triple; proximal also merges
+// the two nodes of a D contact (solver.py:182-213, 366). Groups are disjoint
+// because contact columns do not overlap (checked in k_mark).
+__global__ void k_tie(int n_c, int pair_tie, const int* __restrict__ ci, const int* __restrict__ cj,
+                      const double* __restrict__ diag, const double* __restrict__ rns, double* w) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n_c) return;
+  const int i = ci[m], j = cj[m];
+  if (pair_tie && j >= 0) {
+    double sd = 0.0, sr = 0.0;
+    for (int t = 0; t < 3; ++t) { sd = dadd(sd, diag[i + t]); sr = dadd(sr, rns[i + t]); }
+    for (int t = 0; t < 3; ++t) { sd = dadd(sd, diag[j + t]); sr = dadd(sr, rns[j + t]); }
+    const double v = ddiv(sd, sr);
+    for (int t = 0; t < 3; ++t) { w[i + t] = v; w[j + t] = v; }
+    return;
+  }
+  {
+    double sd = 0.0, sr = 0.0;
+    for (int t = 0; t < 3; ++t) { sd = dadd(sd, diag[i + t]); sr = dadd(sr, rns[i + t]); }
+    const double v = ddiv(sd, sr);
+    for (int t = 0; t < 3; ++t) w[i + t] = v;
+  }
+  if (j >= 0) {
+    double sd = 0.0, sr = 0.0;
+    for (int t = 0; t < 3; ++t) { sd = dadd(sd, diag[j + t]); sr = dadd(sr, rns[j + t]); }
+    const double v = ddiv(sd, sr);
+    for (int t = 0; t < 3; ++t) w[j + t] = v;
+  }
+}
+
+__global__ void k_gamma(int n_c, const int* __restrict__ ci, const int* __restrict__ cj, const double* __restrict__ w,
+                        double omega, double* gamma, int* flags) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n_c) return;
+  const int i = ci[m], j = cj[m];
+  double g = w[i];
+  if (!(w[i] == w[i + 1] && w[i] == w[i + 2])) atomicOr(flags, 8);
+  if (j >= 0) {
+    if (!(w[j] == w[j + 1] && w[j] == w[j + 2])) atomicOr(flags, 8);
+    g = dadd(g, w[j]);
+  }
+  gamma[m] = dadd(g, omega);
+}
+
+// single-CTA deterministic reductions: max|diag| (NaN-propagating) and mean(w)
+__global__ void k_absmax_alpha(int n, const double* __restrict__ diag, double* w_alpha_out) {
+  __shared__ double sm[256];
+  double mx = -INFINITY;
+  bool nan = false;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    const double a = fabs(diag[r]);
+    if (isnan(a)) nan = true;
+    mx = a > mx ? a : mx;
+  }
+  sm[threadIdx.x] = nan ? NAN : mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = -INFINITY;
+    for (int t = 0; t < blockDim.x; ++t) m = np_max(sm[t], m);
+    *w_alpha_out = ddiv(1.0, m);
+  }
+}
+
+__global__ void k_fill_alpha(int n, const double* __restrict__ alpha, double* w) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) w[r] = *alpha;
+}
+
+__global__ void k_mean(int n, const double* __restrict__ w, double* out) {
+  __shared__ double sm[256];
+  double s = 0.0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) s = dadd(s, w[r]);
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < blockDim.x; ++k) t = dadd(t, sm[k]);
+    *out = n > 0 ? ddiv(t, (double)n) : 0.0;
+  }
+}
+
+__global__ void k_fill_int(int* p, int v, int64_t n) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < n) p[e] = v;
+}
+
+}  // namespace
+
+cudaError_t ensure(Workspace::Buf& b, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  if (b.cap >= bytes) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  const size_t want = bytes + bytes / 4;
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e == cudaSuccess) b.cap = want;
+  return e;
+}
+
+template <class T>
+static T* P(Workspace::Buf& b) { return reinterpret_cast<T*>(b.p); }
+
+static int end_bit_for(int64_t v) {
+  int b = 1;
+  while (b < 31 && (int64_t(1) << b) <= v) ++b;
+  return b;
+}
+
+// Phase 1: column statistics, contact marks, partition into G CTAs, slice
+// widths. Ends with ONE host read of the summary (sizes + flags).
+int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, SetupSummary* hs, std::string& err,
+                 int64_t& launches) {
+  const int n = (int)s.n, n_c = (int)s.n_c;
+  const int64_t nnz = s.nnz;
+  VFPI_CK(ensure(ws.diag, 8 * (size_t)n));
+  VFPI_CK(ensure(ws.rns, 8 * (size_t)n));
+  VFPI_CK(ensure(ws.rowcnt, 4 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.row_ptr, 8 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.keys, 4 * (size_t)nnz));
+  VFPI_CK(ensure(ws.colof, 4 * (size_t)nnz));
+  VFPI_CK(ensure(ws.mark, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.ucost, 8 * (size_t)n));
+  VFPI_CK(ensure(ws.cpos, 8 * (size_t)n));
+  VFPI_CK(ensure(ws.urows, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.rpos, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.ucont, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.kpos, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.blk_row, 4 * (size_t)(G + 1)));
+  VFPI_CK(ensure(ws.blk_ct, 4 * (size_t)(G + 1)));
+  VFPI_CK(ensure(ws.blk_slice, 4 * (size_t)(G + 1)));
+  VFPI_CK(ensure(ws.row_list, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.row_slot, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.cont_list, 4 * (size_t)n_c));
+  VFPI_CK(ensure(ws.flags, 16));
+  VFPI_CK(ensure(ws.summary, sizeof(SetupSummary)));
+  const int S_max = (n + 31) / 32 + G;  // each CTA rounds its row count up once
+  VFPI_CK(ensure(ws.slice_w, 8 * (size_t)(S_max + 1)));
+  VFPI_CK(ensure(ws.slice_off, 8 * (size_t)(S_max + 1)));
+
+  size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t1, P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr), n + 1, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), n, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t3, P<int>(ws.urows), P<int>(ws.rpos), n, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t4, P<int64_t>(ws.slice_w), P<int64_t>(ws.slice_off), S_max + 1, st);
+  VFPI_CK(ensure(ws.cub_tmp, std::max(std::max(t1, t2), std::max(t3, t4))));
+  size_t tb = ws.cub_tmp.cap;
+
+  VFPI_CK(cudaMemsetAsync(ws.rowcnt.p, 0, 4 * (size_t)(n + 1), st));
+  VFPI_CK(cudaMemsetAsync(ws.mark.p, 0xff, 4 * (size_t)n, st));
+  VFPI_CK(cudaMemsetAsync(ws.flags.p, 0, 16, st));
+  VFPI_CK(cudaMemsetAsync(ws.summary.p, 0, sizeof(SetupSummary), st));
+  k_fill_int<<<nblk(G + 1), 256, 0, st>>>(P<int>(ws.blk_row), INT_MAX, G + 1);
+  k_fill_int<<<nblk(G + 1), 256, 0, st>>>(P<int>(ws.blk_ct), INT_MAX, G + 1);
+  launches += 2;
+  if (n > 0) {
+    k_colstats<<<nblk(n), 256, 0, st>>>(n, s.indptr, s.indices, s.data, P<double>(ws.diag), P<double>(ws.rns),
+                                        P<int>(ws.rowcnt), P<int>(ws.keys), P<int>(ws.colof));
+    ++launches;
+  }
+  if (n_c > 0) {
+    k_mark<<<nblk(n_c), 256, 0, st>>>(n, n_c, s.col_i, s.col_j, P<int>(ws.mark), P<int>(ws.flags));
+    ++launches;
+  }
+  VFPI_CK(cudaGetLastError());
+  VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr), n + 1, st));
+  ++launches;
+  if (n > 0) {
+    k_units<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.rowcnt), P<int64_t>(ws.ucost),
+                                     P<int>(ws.urows), P<int>(ws.ucont));
+    VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), n, st));
+    VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.urows), P<int>(ws.rpos), n, st));
+    VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ucont), P<int>(ws.kpos), n, st));
+    k_blocks<<<nblk(n), 256, 0, st>>>(n, G, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), P<int>(ws.urows),
+                                      P<int>(ws.rpos), P<int>(ws.kpos), P<int>(ws.blk_row), P<int>(ws.blk_ct));
+    launches += 5;
+  }
+  k_blocks_fix<<<1, 1, 0, st>>>(n, n_c, G, P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_slice),
+                                P<SetupSummary>(ws.summary));
+  ++launches;
+  if (n > 0) {
+    k_fill<<<nblk(n), 256, 0, st>>>(n, G, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.urows), P<int>(ws.rpos),
+                                    P<int>(ws.kpos), P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.row_list),
+                                    P<int>(ws.row_slot), P<int>(ws.cont_list));
+    ++launches;
+  }
+  VFPI_CK(cudaGetLastError());
+  // slice count is data dependent but bounded by S_max; slices past the real
+  // count get width 0, so one scan over S_max+1 entries suffices.
+  k_slice_width<<<nblk(S_max + 1), 256, 0, st>>>(S_max, G, P<SetupSummary>(ws.summary), P<int>(ws.blk_slice),
+                                                 P<int>(ws.blk_row), P<int>(ws.row_list), P<int>(ws.rowcnt),
+                                                 P<int64_t>(ws.slice_w));
+  VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.slice_w), P<int64_t>(ws.slice_off),
+                                        S_max + 1, st));
+  k_summary<<<1, 1, 0, st>>>(n, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int>(ws.flags),
+                             P<SetupSummary>(ws.summary));
+  launches += 3;
+  VFPI_CK(cudaGetLastError());
+  VFPI_CK(cudaMemcpyAsync(hs, ws.summary.p, sizeof(SetupSummary), cudaMemcpyDeviceToHost, st));
+  VFPI_CK(cudaStreamSynchronize(st));
+  const int S = hs->n_slices;
+  if (hs->flags & 2) { err = "contact column index out of range"; return VFPI_BAD_ARGUMENT; }
+  if (hs->flags & 1) {
+    err = "two contacts share a node column (nodalization guarantees one contact per node, contacts.py:242-268)";
+    return VFPI_UNSUPPORTED;
+  }
+
+  // Phase 2: stable radix sort of CSC entries by row -> per-row increasing
+  // column order (scipy's accumulation order), then SELL-32 packing.
+  VFPI_CK(ensure(ws.vals, 4 * (size_t)nnz));
+  VFPI_CK(ensure(ws.perm, 4 * (size_t)nnz));
+  VFPI_CK(ensure(ws.keys_sorted, 4 * (size_t)nnz));
+  VFPI_CK(ensure(ws.sell_val, 8 * (size_t)hs->sell_elems));
+  VFPI_CK(ensure(ws.sell_col, 4 * (size_t)hs->sell_elems));
+  if (nnz > 0) {
+    const int eb = end_bit_for(n);
+    size_t ts = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, ts, P<int>(ws.keys), P<int>(ws.keys_sorted), P<int>(ws.vals),
+                                    P<int>(ws.perm), (int)nnz, 0, eb, st);
+    VFPI_CK(ensure(ws.cub_tmp, ts));
+    tb = ws.cub_tmp.cap;
+    k_iota<<<nblk(nnz), 256, 0, st>>>(nnz, P<int>(ws.vals));
+    VFPI_CK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.keys), P<int>(ws.keys_sorted),
+                                            P<int>(ws.vals), P<int>(ws.perm), (int)nnz, 0, eb, st));
+    launches += 4;  // iota + onesweep passes (approximate count for the sort)
+  }
+  if (S > 0) {
+    k_pack<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row), P<int>(ws.row_list),
+                                                  P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr), P<int>(ws.perm),
+                                                  P<int>(ws.colof), s.data, P<int64_t>(ws.slice_off),
+                                                  P<double>(ws.sell_val), P<int>(ws.sell_col));
+    ++launches;
+  }
+  VFPI_CK(cudaGetLastError());
+  return VFPI_OK;
+}
+
+// W (frobenius / fixed-alpha / cached) and gamma; flags reported through ws.flags
+int setup_step_matrix(Workspace& ws, const vfpi_system& s, const vfpi_config& cfg, const double* d_w_cached,
+                      cudaStream_t st, std::string& err, int64_t& launches) {
+  const int n = (int)s.n, n_c = (int)s.n_c;
+  VFPI_CK(ensure(ws.w, 8 * (size_t)n));
+  VFPI_CK(ensure(ws.gamma, 8 * (size_t)n_c));
+  VFPI_CK(ensure(ws.w_mean, 16));
+  double* w = P<double>(ws.w);
+  if (cfg.step_strategy == VFPI_STEP_FIXED_ALPHA) {
+    if (std::isnan(cfg.fixed_alpha)) {
+      k_absmax_alpha<<<1, 256, 0, st>>>(n, P<double>(ws.diag), P<double>(ws.w_mean) + 1);
+      ++launches;
+    } else {
+      VFPI_CK(cudaMemcpyAsync(P<double>(ws.w_mean) + 1, &cfg.fixed_alpha, 8, cudaMemcpyHostToDevice, st));
+    }
+    if (n > 0) {
+      k_fill_alpha<<<nblk(n), 256, 0, st>>>(n, P<double>(ws.w_mean) + 1, w);
+      ++launches;
+    }
+  } else if (d_w_cached != nullptr) {
+    VFPI_CK(cudaMemcpyAsync(w, d_w_cached, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    if (n > 0) {
+      k_w_frob<<<nblk(n), 256, 0, st>>>(n, P<double>(ws.diag), P<double>(ws.rns), w, P<int>(ws.flags));
+      ++launches;
+    }
+    if (n_c > 0) {
+      k_tie<<<nblk(n_c), 256, 0, st>>>(n_c, cfg.op == VFPI_OP_PROXIMAL ? 1 : 0, s.col_i, s.col_j,
+                                       P<double>(ws.diag), P<double>(ws.rns), w);
+      ++launches;
+    }
+  }
+  if (n_c > 0) {
+    k_gamma<<<nblk(n_c), 256, 0, st>>>(n_c, s.col_i, s.col_j, w, cfg.omega, P<double>(ws.gamma), P<int>(ws.flags));
+    ++launches;
+  }
+  const bool bb = cfg.step_strategy >= VFPI_STEP_BB1 && cfg.step_strategy <= VFPI_STEP_BB_ALTERNATING;
+  if (bb) {
+    k_mean<<<1, 256, 0, st>>>(n, w, P<double>(ws.w_mean));
+    ++launches;
+  }
+  VFPI_CK(cudaGetLastError());
+  return VFPI_OK;
+}
+
+}  // namespace vfpi

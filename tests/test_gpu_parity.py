@@ -1,0 +1,103 @@
+"""CUDA path (through the C-ABI) vs the reference's own outputs and the oracle.
+
+Parity bar (BASELINE.json north_star): identical iteration counts and
+converged/diverged outcomes, velocities and impulses within 1e-9 relative in
+fp64. Where no decision depends on OpenBLAS-ordered dot products (plain
+Frobenius / fixed-alpha iterations), the GPU result is additionally required
+to be BIT-identical to the reference.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from golden_cases import load, names
+from gpu_util import config, packed, relerr
+
+pytestmark = pytest.mark.gpu
+
+CASES = names()
+TOL = 1e-9
+
+
+def _solve(d):
+    from paper_2201_09212_b200.solver import solve_packed
+
+    return solve_packed(packed(d), config(d), d["warm"], d.get("w_cached"))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_solve_matches_reference(name):
+    from paper_2201_09212_b200.errors import DivergenceError
+
+    d = load(name)
+    if d["out_diverged"]:
+        with pytest.raises(DivergenceError) as exc:
+            _solve(d)
+        tr = np.asarray(exc.value.residual_trace)
+        assert len(tr) == int(d["out_iterations"])
+        fin = np.isfinite(d["out_trace"])
+        assert np.allclose(tr[fin], d["out_trace"][fin], rtol=1e-6)
+        return
+    v, lam, rep = _solve(d)
+    assert rep.iterations == int(d["out_iterations"]), (rep.iterations, int(d["out_iterations"]))
+    assert rep.converged == bool(d["out_converged"])
+    assert relerr(v, d["out_v"]) <= TOL
+    if lam.size:
+        assert relerr(lam, d["out_lam"]) <= TOL
+    assert len(rep.residual_trace) == rep.iterations
+    assert np.allclose(rep.residual_trace, d["out_trace"], rtol=1e-6, atol=1e-300, equal_nan=True)
+    c_ref = float(d["out_consistency"])
+    if np.isfinite(c_ref):
+        assert abs(rep.consistency - c_ref) <= 1e-6 * max(abs(c_ref), 1e-12)
+    if lam.size:
+        assert np.allclose(rep.scc_residuals, d["out_scc"], rtol=1e-6, atol=1e-12, equal_nan=True)
+
+
+BITWISE = [c for c in CASES
+           if not load(c)["cfg"]["chebyshev"] and load(c)["cfg"]["step_strategy"] in ("frobenius", "fixed-alpha")
+           and load(c)["cfg"]["operator"] != "strict-anisotropic" and not load(c)["out_diverged"]]
+
+
+@pytest.mark.parametrize("name", BITWISE)
+def test_plain_iteration_bit_identical(name):
+    d = load(name)
+    v, lam, rep = _solve(d)
+    assert rep.iterations == int(d["out_iterations"])
+    assert np.array_equal(v, d["out_v"])
+    assert np.array_equal(lam.ravel(), d["out_lam"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_per_op_entry_points(name):
+    from paper_2201_09212_b200 import contacts as GC
+    from paper_2201_09212_b200 import solver as GS
+    from paper_2201_09212_b200 import sparse as GP
+    from paper_2201_09212_b200.system import SparseSymmetric
+
+    d = load(name)
+    ps = packed(d)
+    a = SparseSymmetric(int(d["n"]), d["indptr"], d["indices"], d["data"])
+    x = d["op_x"]
+    assert np.array_equal(GP.spmv(a, x), d["op_spmv"])  # bit-exact to scipy
+    assert np.array_equal(GP.row_norms_sq(a), d["op_rns"])
+    assert np.array_equal(GP.diagonal(a), d["op_diag"])
+    if "op_w_strict" in d:
+        assert np.array_equal(GS.step_matrix_frobenius(a, ps, False).w, d["op_w_strict"])
+        assert np.array_equal(GS.step_matrix_frobenius(a, ps, True).w, d["op_w_prox"])
+    if ps.n_c == 0:
+        return
+    op = d["cfg"]["operator"]
+    w = GS.step_matrix_frobenius(a, ps, op == "proximal")
+    gam = GS.surrogate_gamma(w, ps, d["cfg"]["omega"])
+    assert np.array_equal(gam.gamma, d["op_gamma"])
+    assert np.array_equal(GC.apply_jc(ps, x).ravel(), d["op_jc"])
+    assert np.array_equal(GC.apply_jc_t(ps, d["op_lam"]), d["op_jct"])
+    eta = d["op_eta"].reshape(-1, 3)
+    for o in ("strict", "proximal"):
+        got = GS.contact_solve_oneshot(gam, eta, ps.phi, ps.mu, o, ps.mu2).ravel()
+        assert np.array_equal(got, d["op_oneshot_" + o], equal_nan=True), o
+    got = GS.contact_solve_oneshot(gam, eta, ps.phi, ps.mu, "strict-anisotropic", ps.mu2).ravel()
+    assert np.allclose(got, d["op_oneshot_strict_anisotropic"], rtol=1e-9, atol=1e-12, equal_nan=True)
+    assert np.array_equal(GS.inverse_contact(ps, x, 1e-3).ravel(), d["op_inverse"])
