@@ -188,7 +188,8 @@ def run_ours(args):
     ds = DeviceSystem(ps, local)
     warm = torch.zeros(ps.n, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(local)
+    stream = torch.cuda.Stream(local)  # the solve and the timing events share this stream
+    torch.cuda.set_stream(stream)
     h = _lib.handle(local)
 
     def one_step():
@@ -199,6 +200,7 @@ def run_ours(args):
         flush.fill_(1.0)
         one_step()
         ds.finish()
+    layout = h.last_layout()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -315,7 +317,10 @@ def run_ours(args):
                    "operator": "strict", "step_strategy": "frobenius", "chebyshev": False, "tol": TOL,
                    "max_iters": MAX_ITERS, "iterations_per_step": mean_iters,
                    "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}"},
-        "roofline": {"bound": "hbm", "kernel": "k_iterate (persistent V-FPI iteration kernel)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k_iterate_res (persistent, partition resident in shared memory)" if layout["resident"]
+                                else "k_iterate (persistent, SELL-32 streamed from global memory)"),
+                     "ctas": layout["ctas"],
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_iter": b_iter, "kernel_ms_per_launch": loop_max,

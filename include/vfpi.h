@@ -116,6 +116,17 @@ int vfpi_wait(vfpi_handle* h, vfpi_result* res);
 
 /* Number of kernels this library launched on the handle since creation. */
 int64_t vfpi_launch_count(const vfpi_handle* h);
+/* Layout chosen by the last solve: shared-memory resident kernel (1) or the
+ * streaming SELL-32 kernel (0), and the number of CTAs. */
+int vfpi_last_layout(const vfpi_handle* h, int* resident, int* ctas);
+/* Kernel selection for later solves on h: 0 auto (resident when the largest
+ * CTA partition fits in shared memory), 1 force resident, 2 force streaming. */
+int vfpi_set_kernel(vfpi_handle* h, int mode);
+/* Tuning aid: when iter0 > 0, later resident solves record per-CTA phase
+ * timestamps of iterations iter0..iter0+3 ([G][4][8] int64: clock64 at
+ * phase starts 0..5, globaltimer at 7); vfpi_get_profile copies them out. */
+int vfpi_set_profile(vfpi_handle* h, int iter0);
+int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */
 void* vfpi_host_alloc(int64_t bytes);

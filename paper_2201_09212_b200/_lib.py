@@ -73,6 +73,10 @@ def lib() -> C.CDLL:
                 "vfpi_solve_device": (C.c_int, [H, sysp, cfgp, _f64p, _f64p, resp, C.c_void_p]),
                 "vfpi_wait": (C.c_int, [H, resp]),
                 "vfpi_launch_count": (C.c_int64, [H]),
+                "vfpi_last_layout": (C.c_int, [H, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+                "vfpi_set_kernel": (C.c_int, [H, C.c_int]),
+                "vfpi_set_profile": (C.c_int, [H, C.c_int]),
+                "vfpi_get_profile": (C.c_int, [H, C.POINTER(C.c_longlong), C.c_int64]),
                 "vfpi_host_alloc": (C.c_void_p, [C.c_int64]),
                 "vfpi_host_free": (None, [C.c_void_p]),
                 "vfpi_spmv": (C.c_int, [H, sysp, _f64p, _f64p]),
@@ -119,6 +123,16 @@ class Handle:
 
     def launches(self) -> int:
         return int(self.L.vfpi_launch_count(self.h))
+
+    def set_kernel(self, mode: str):
+        """'auto' | 'resident' | 'streaming' for later solves on this handle."""
+        code = {"auto": 0, "resident": 1, "streaming": 2}[mode]
+        self.L.vfpi_set_kernel(self.h, code)
+
+    def last_layout(self):
+        r, g = C.c_int(), C.c_int()
+        self.L.vfpi_last_layout(self.h, C.byref(r), C.byref(g))
+        return {"resident": bool(r.value), "ctas": int(g.value)}
 
     def __del__(self):
         try:

@@ -4,12 +4,31 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
 #include "vfpi_internal.cuh"
 
 using vfpi::Workspace;
+
+cudaError_t vfpi::ensure_max_dynamic_smem(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, fn})) return cudaSuccess;
+  cudaFuncAttributes a{};
+  cudaError_t e = cudaFuncGetAttributes(&a, fn);
+  if (e != cudaSuccess) return e;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+  if (e == cudaSuccess) done.insert({dev, fn});
+  return e;
+}
 
 struct vfpi_handle {
   Workspace ws;
@@ -18,6 +37,10 @@ struct vfpi_handle {
   // last solve (device path) bookkeeping for vfpi_wait
   int pending = 0;
   int max_iters = 0;
+  int last_resident = 0;
+  int kernel_mode = 0;  // 0 auto, 1 force shared-memory resident, 2 force streaming
+  int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
+  int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
 
@@ -35,14 +58,18 @@ namespace {
 template <class T>
 T* P(Workspace::Buf& b) { return reinterpret_cast<T*>(b.p); }
 
+// CTAs for the global-memory (streaming) kernel: a multiple of the SM count
+// so every SM carries the same share of the cost-balanced partition.
 int choose_blocks(const vfpi_system& s, int num_sms) {
-  // ~6K stored entries per CTA keeps every SM busy for large systems while
-  // small systems use few CTAs (the grid barrier cost grows with G).
-  const int64_t by_nnz = (s.nnz + 6143) / 6144;
-  const int64_t by_rows = (s.n + 255) / 256;
-  int64_t g = std::max<int64_t>(1, std::min(by_nnz, by_rows * 4));
-  g = std::min<int64_t>(g, 2 * (int64_t)num_sms);
-  return (int)g;
+  const int64_t by_nnz = (s.nnz + 4095) / 4096;
+  if (by_nnz < num_sms) return (int)std::max<int64_t>(1, by_nnz);
+  return by_nnz >= 2 * num_sms ? 2 * num_sms : num_sms;
+}
+
+// CTAs for the shared-memory-resident kernel: one per SM at most.
+int choose_blocks_resident(const vfpi_system& s, int num_sms) {
+  const int64_t by_nnz = (s.nnz + 2047) / 2048;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(by_nnz, num_sms));
 }
 
 int upload(vfpi_handle* h, Workspace::Buf& b, const void* src, size_t bytes) {
@@ -108,7 +135,8 @@ int op_layout(vfpi_handle* h, const vfpi_system& d, bool with_contacts) {
   if (!with_contacts) dd.n_c = 0;
   vfpi::SetupSummary* hs = h->ws.h_summary;
   int rc = vfpi::setup_layout(h->ws, dd, 1, h->ws.stream, hs, h->err, h->launches);
-  return rc;
+  if (rc) return rc;
+  return vfpi::setup_pack(h->ws, dd, 1, true, *hs, h->ws.stream, h->err, h->launches);
 }
 
 }  // namespace
@@ -127,6 +155,7 @@ int vfpi_create(int device, vfpi_handle** out) {
   vfpi_handle* h = new vfpi_handle();
   h->ws.device = device;
   cudaDeviceGetAttribute(&h->ws.num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&h->ws.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (cudaStreamCreateWithFlags(&h->ws.stream, cudaStreamNonBlocking) != cudaSuccess) { delete h; return VFPI_CUDA_ERROR; }
   for (auto& e : h->ws.ev) cudaEventCreate(&e);
   cudaMallocHost(&h->ws.h_summary, sizeof(vfpi::SetupSummary));
@@ -148,9 +177,10 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.vals, &h->ws.perm, &h->ws.colof, &h->ws.mark, &h->ws.ucost, &h->ws.cpos,
                             &h->ws.urows, &h->ws.rpos, &h->ws.ucont, &h->ws.kpos, &h->ws.blk_row, &h->ws.blk_ct,
                             &h->ws.blk_slice, &h->ws.row_list, &h->ws.row_slot, &h->ws.cont_list,
-                            &h->ws.slice_w, &h->ws.slice_off, &h->ws.sell_val, &h->ws.sell_col, &h->ws.vbuf,
+                            &h->ws.slice_w, &h->ws.slice_off, &h->ws.sell_val, &h->ws.sell_col, &h->ws.pos_len, &h->ws.pos_ptr,
+                            &h->ws.pk_val, &h->ws.pk_col, &h->ws.bar_flags, &h->ws.vbuf,
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
-                            &h->ws.cub_tmp, &h->ws.x, &h->ws.y};
+                            &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
   for (auto* b : bufs)
     if (b->p) cudaFree(b->p);
   for (auto& e : h->ws.ev)
@@ -165,6 +195,35 @@ void vfpi_destroy(vfpi_handle* h) {
 const char* vfpi_last_error(const vfpi_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 int64_t vfpi_launch_count(const vfpi_handle* h) { return h ? h->launches : 0; }
+
+int vfpi_set_profile(vfpi_handle* h, int iter0) {
+  if (!h || iter0 < 0) return VFPI_BAD_ARGUMENT;
+  h->prof_iter0 = iter0;
+  return VFPI_OK;
+}
+
+int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count) {
+  if (!h || !out) return VFPI_BAD_ARGUMENT;
+  const int64_t cnt = std::min<int64_t>(max_count, 32 * (int64_t)h->last_G);
+  if (!h->ws.prof.p || cnt <= 0) return VFPI_BAD_ARGUMENT;
+  cudaSetDevice(h->ws.device);
+  CK(cudaStreamSynchronize(h->ws.stream));
+  CK(cudaMemcpy(out, h->ws.prof.p, sizeof(long long) * (size_t)cnt, cudaMemcpyDeviceToHost));
+  return VFPI_OK;
+}
+
+int vfpi_set_kernel(vfpi_handle* h, int mode) {
+  if (!h || mode < 0 || mode > 2) return VFPI_BAD_ARGUMENT;
+  h->kernel_mode = mode;
+  return VFPI_OK;
+}
+
+int vfpi_last_layout(const vfpi_handle* h, int* resident, int* ctas) {
+  if (!h) return VFPI_BAD_ARGUMENT;
+  if (resident) *resident = h->last_resident;
+  if (ctas) *ctas = h->last_G;
+  return VFPI_OK;
+}
 
 void* vfpi_host_alloc(int64_t bytes) {
   void* p = nullptr;
@@ -193,18 +252,30 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   const bool bb = cfg->step_strategy >= VFPI_STEP_BB1 && cfg->step_strategy <= VFPI_STEP_BB_ALTERNATING;
 
   CK(cudaEventRecord(ws.ev[0], st));
-  int G = choose_blocks(*d, ws.num_sms);
   vfpi::SetupSummary* hs = ws.h_summary;
+  // first choice: the whole partition of every CTA resident in shared memory
+  int G = choose_blocks_resident(*d, ws.num_sms);
+  rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches);
+  if (rc) return rc;
+  const size_t smem_res = (size_t)hs->max_res_bytes;
+  const bool fits = hs->max_ent_per_blk < (1 << 24) && smem_res + 2048 <= (size_t)ws.max_smem_optin;
+  if (h->kernel_mode == 1 && !fits) { h->err = "partition does not fit in shared memory"; return VFPI_UNSUPPORTED; }
+  const bool resident = fits && h->kernel_mode != 2;
   int smem = 0;
-  for (int attempt = 0; attempt < 4; ++attempt) {
-    rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches);
-    if (rc) return rc;
-    smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
-    const int bps = vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem);
-    if (bps <= 0) { h->err = "iteration kernel does not fit on an SM"; return VFPI_UNSUPPORTED; }
-    if (G <= bps * ws.num_sms) break;
-    G = bps * ws.num_sms;
+  if (!resident) {
+    G = choose_blocks(*d, ws.num_sms);
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches);
+      if (rc) return rc;
+      smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
+      const int bps = vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem);
+      if (bps <= 0) { h->err = "iteration kernel does not fit on an SM"; return VFPI_UNSUPPORTED; }
+      if (G <= bps * ws.num_sms) break;
+      G = bps * ws.num_sms;
+    }
   }
+  rc = vfpi::setup_pack(ws, *d, G, resident, *hs, st, h->err, h->launches);
+  if (rc) return rc;
   rc = vfpi::setup_step_matrix(ws, *d, *cfg, w_cached, st, h->err, h->launches);
   if (rc) return rc;
 
@@ -213,6 +284,8 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)std::max(n_c, 1)));
   CK(vfpi::ensure(ws.partials, 2 * 8 * (size_t)G * vfpi::kPartialStride));
   CK(vfpi::ensure(ws.status, sizeof(vfpi::SolveStatus)));
+  CK(vfpi::ensure(ws.bar_flags, 4 * (size_t)G));
+  CK(cudaMemsetAsync(ws.bar_flags.p, 0, 4 * (size_t)G, st));
   double* vb = P<double>(ws.vbuf);
   double* lb = P<double>(ws.lambuf);
   if (n > 0) {
@@ -235,6 +308,18 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.slice_off = P<int64_t>(ws.slice_off);
   p.sell_val = P<double>(ws.sell_val);
   p.sell_col = P<int>(ws.sell_col);
+  p.pos_ptr = P<int64_t>(ws.pos_ptr);
+  p.pk_val = P<double>(ws.pk_val);
+  p.pk_col = P<int>(ws.pk_col);
+  p.bar_flags = P<int>(ws.bar_flags);
+  p.prof = nullptr;
+  p.prof_iter0 = 0;
+  if (h->prof_iter0 > 0) {
+    CK(vfpi::ensure(ws.prof, sizeof(long long) * 32 * (size_t)G));
+    CK(cudaMemsetAsync(ws.prof.p, 0, sizeof(long long) * 32 * (size_t)G, st));
+    p.prof = P<long long>(ws.prof);
+    p.prof_iter0 = h->prof_iter0;
+  }
   p.cont_list = P<int>(ws.cont_list);
   p.b = d->b;
   p.w = P<double>(ws.w);
@@ -264,8 +349,11 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.omega = cfg->omega;
   p.cfactor = cfg->consistency_factor;
   (void)tr;
-  rc = vfpi::launch_iterate(p, cfg->op, cheb, bb, smem, st, h->err);
+  rc = resident ? vfpi::launch_iterate_resident(p, cfg->op, cheb, bb, smem_res, st, h->err)
+                : vfpi::launch_iterate(p, cfg->op, cheb, bb, smem, st, h->err);
   if (rc) return rc;
+  h->last_resident = resident ? 1 : 0;
+  h->last_G = G;
   ++h->launches;
   CK(cudaEventRecord(ws.ev[2], st));
   if (res->scc && n_c > 0) {

@@ -13,14 +13,44 @@ constexpr int kThreads = 256;      // threads per CTA of the iteration kernel
 constexpr int kSlotsPerContact = 6;  // rows of a contact unit (3 for S, 6 for D)
 constexpr int kPartialStride = 8;  // doubles per CTA per parity in the partials ring
 
+// Shared-memory layout of one CTA of the resident iteration kernel.
+struct ResLayout {
+  size_t o_sv, o_prod, o_sc, o_rp, o_row, o_slot, o_b, o_w, o_cm, o_fr, o_par, o_vs, o_jt, o_lam, total;
+  __host__ __device__ ResLayout(int64_t E, int R, int C) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+      const size_t r = o;
+      o += (bytes + 15) & ~size_t(15);
+      return r;
+    };
+    o_sv = take(8 * (size_t)E);
+    o_prod = take(8 * (size_t)E);
+    o_sc = take(4 * (size_t)E);
+    o_rp = take(4 * (size_t)(R + 1));
+    o_row = take(4 * (size_t)R);
+    o_slot = take(4 * (size_t)R);
+    o_b = take(8 * (size_t)R);
+    o_w = take(8 * (size_t)R);
+    o_cm = take(4 * (size_t)C);
+    o_fr = take(72 * (size_t)C);
+    o_par = take(32 * (size_t)C);
+    o_vs = take(48 * (size_t)C);
+    o_jt = take(48 * (size_t)C);
+    o_lam = take(48 * (size_t)C);
+    total = o;
+  }
+};
+
 // Device-side summary written at the end of layout setup (one D2H read).
 struct SetupSummary {
-  int64_t nnz_num;       // numeric (non-zero) entries of A
-  int64_t sell_elems;    // padded SELL-32 element count
+  int64_t nnz_num;          // numeric (non-zero) entries of A
+  int64_t sell_elems;       // padded SELL-32 element count
+  int64_t max_ent_per_blk;  // numeric entries of the largest CTA partition
+  int64_t max_res_bytes;    // largest per-CTA ResLayout footprint
   int32_t n_slices;
   int32_t max_ct_per_blk;
-  int32_t flags;         // bit0 overlap, bit1 bad column index
-  int32_t pad;
+  int32_t max_rows_per_blk;
+  int32_t flags;            // bit0 overlap, bit1 bad column index
 };
 
 // Device-side status written by the iteration kernel.
@@ -46,6 +76,12 @@ struct IterParams {
   const int64_t* slice_off; // [S+1] element offset of every SELL-32 slice
   const double* sell_val;   // [sell_elems]
   const int* sell_col;      // [sell_elems], -1 = padding
+  const int64_t* pos_ptr;   // [n+1] entry offset of every row-list position (resident kernel)
+  const double* pk_val;     // [nnz_num] entries in row-list order (resident kernel)
+  const int* pk_col;
+  int* bar_flags;           // [G] epoch flags of the flag barrier
+  long long* prof;          // optional [G][4][8] phase timestamps (NULL = off)
+  int prof_iter0;           // first of the 4 profiled iterations
   const int* cont_list;     // [n_c] contact ids in partition order
   // system
   const double* b;
@@ -77,9 +113,14 @@ struct IterParams {
 // ---- setup (vfpi_setup.cu) -------------------------------------------------
 struct Workspace;  // device buffers owned by a handle
 
-// Layout + step-matrix setup on the handle stream. Returns VFPI_* code.
+// Layout setup on the stream: statistics, contact-aware CTA partition and
+// sizes (ends with one host read of the summary). Returns VFPI_* code.
 int setup_layout(Workspace& ws, const vfpi_system& dsys, int G, cudaStream_t st, SetupSummary* host_summary,
                  std::string& err, int64_t& launches);
+// Row-sorted entries packed for the chosen iteration kernel:
+// resident = CTA-contiguous CSR (pos_ptr/pk_val/pk_col), else SELL-32.
+int setup_pack(Workspace& ws, const vfpi_system& dsys, int G, bool resident, const SetupSummary& hs,
+               cudaStream_t st, std::string& err, int64_t& launches);
 int setup_step_matrix(Workspace& ws, const vfpi_system& dsys, const vfpi_config& cfg, const double* d_w_cached,
                       cudaStream_t st, std::string& err, int64_t& launches);
 
@@ -87,6 +128,10 @@ int setup_step_matrix(Workspace& ws, const vfpi_system& dsys, const vfpi_config&
 int launch_iterate(const IterParams& p, int op, bool cheb, bool bb, int smem_bytes, cudaStream_t st,
                    std::string& err);
 int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes);
+// shared-memory resident variant (whole CTA partition of A on chip)
+int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, size_t smem_bytes, cudaStream_t st,
+                            std::string& err);
+constexpr int kResThreads = 512;
 int launch_scc_final(const IterParams& p, double* scc, cudaStream_t st);
 
 // ---- per-op kernels (vfpi_ops.cu) -----------------------------------------
@@ -114,16 +159,22 @@ struct Workspace {
   Buf rowcnt, row_ptr, keys, keys_sorted, vals, perm, colof, mark;
   Buf ucost, cpos, urows, rpos, ucont, kpos;
   Buf blk_row, blk_ct, blk_slice, row_list, row_slot, cont_list;
-  Buf slice_w, slice_off, sell_val, sell_col;
+  Buf slice_w, slice_off, sell_val, sell_col, pos_len, pos_ptr, pk_val, pk_col, bar_flags;
   Buf vbuf, lambuf, partials, status, summary, flags, cub_tmp;
   Buf x, y;  // scratch for per-op entry points
+  Buf prof;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   SetupSummary* h_summary = nullptr;  // pinned
   SolveStatus* h_status = nullptr;    // pinned
   int num_sms = 148;
+  int max_smem_optin = 232448;
 };
 
 cudaError_t ensure(Workspace::Buf& b, size_t bytes);
+// Raise a kernel's dynamic shared-memory limit to the device maximum, once per
+// kernel, under a lock (the attribute is process-wide; concurrent solves on
+// several threads must never shrink it under each other).
+cudaError_t ensure_max_dynamic_smem(const void* fn);
 
 }  // namespace vfpi

@@ -1,0 +1,445 @@
+// V-FPI iteration, shared-memory-resident variant (the configs[1] path).
+//
+// Same algorithm and decision pipeline as vfpi_solve.cu (reference loop
+// solver.py:388-446), but each CTA (one per SM) keeps its whole partition on
+// chip for the lifetime of the launch:
+//   * its rows' numeric entries (values + columns, CTA-contiguous CSR),
+//     b, w, the contact frames and parameters, lam (both parities), J_c^T lam
+//     and v* of contact rows -> only the x-gathers of the SpMV and the
+//     v_next stores touch L2 per iteration;
+//   * the SpMV is split in two passes so the gathers are fully parallel while
+//     the row sums keep scipy's sequential order bit for bit:
+//       pass A  prod[e] = a[e] * x[col[e]]   (all entries, 8 gathers in flight / thread)
+//       pass B  acc(row) = (((0 + prod[k0]) + prod[k0+1]) + ...)   (one thread per row)
+//   * the grid barrier is a flag barrier fused with the deterministic
+//     residual reduction: every CTA publishes (theta^2, force^2, #nonfinite)
+//     and an epoch flag; every CTA waits for all flags and sums the G partials
+//     in the same fixed order, so decisions are identical everywhere.
+#include "vfpi_internal.cuh"
+#include "vfpi_math.cuh"
+
+namespace vfpi {
+
+namespace {
+
+__device__ __forceinline__ int ld_flag(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs of the grid reach this point; partial sums of iteration `epoch` are
+// published in part[b*kPartialStride + off .. +2] before the flag
+__device__ __forceinline__ void flag_barrier(int* flags, int G, int epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(epoch) : "memory");
+  }
+  if (threadIdx.x < 32) {
+    for (int g = threadIdx.x; g < G; g += 32) {
+      const long long t0 = clock64();
+      while (ld_flag(flags + g) < epoch) {
+        if (clock64() - t0 > (1ll << 36)) __trap();  // ~30 s: never in a healthy run
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cta_reduce3(double a, double b, double c, double* sm_warp, double* sm_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = dadd(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = dadd(b, __shfl_xor_sync(0xffffffffu, b, o));
+    c = dadd(c, __shfl_xor_sync(0xffffffffu, c, o));
+  }
+  if (lane == 0) {
+    sm_warp[3 * warp + 0] = a;
+    sm_warp[3 * warp + 1] = b;
+    sm_warp[3 * warp + 2] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0, z = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      x = dadd(x, sm_warp[3 * w + 0]);
+      y = dadd(y, sm_warp[3 * w + 1]);
+      z = dadd(z, sm_warp[3 * w + 2]);
+    }
+    sm_out[0] = x;
+    sm_out[1] = y;
+    sm_out[2] = z;
+  }
+}
+
+// publish this CTA's three partials, barrier, reduce all G in fixed order
+__device__ __forceinline__ void grid_reduce3(double a, double b, double c, double* part, int off, int* flags, int G,
+                                             int epoch, double* sm_warp, double* sm_tot) {
+  cta_reduce3(a, b, c, sm_warp, sm_tot);
+  if (threadIdx.x == 0) {
+    double* q = part + (size_t)blockIdx.x * kPartialStride + off;
+    q[0] = sm_tot[0];
+    q[1] = sm_tot[1];
+    q[2] = sm_tot[2];
+  }
+  flag_barrier(flags, G, epoch);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double x = 0.0, y = 0.0, z = 0.0;
+    for (int g = lane; g < G; g += 32) {
+      const double* q = part + (size_t)g * kPartialStride + off;
+      x = dadd(x, __ldcg(q + 0));
+      y = dadd(y, __ldcg(q + 1));
+      z = dadd(z, __ldcg(q + 2));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      x = dadd(x, __shfl_xor_sync(0xffffffffu, x, o));
+      y = dadd(y, __shfl_xor_sync(0xffffffffu, y, o));
+      z = dadd(z, __shfl_xor_sync(0xffffffffu, z, o));
+    }
+    if (lane == 0) {
+      sm_tot[0] = x;
+      sm_tot[1] = y;
+      sm_tot[2] = z;
+    }
+  }
+  __syncthreads();
+}
+
+// pass A: prod[e] = a[e] * x(col[e]) over the CTA's entries, 8 independent gathers per thread in flight
+template <class X>
+__device__ __forceinline__ void products(const double* __restrict__ sv, const int* __restrict__ sc,
+                                         double* __restrict__ prod, int E, X x) {
+  const int T = blockDim.x;
+  for (int base = threadIdx.x; base < E; base += 8 * T) {
+    int c[8];
+    double a[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * T;
+      c[u] = i < E ? sc[i] : -1;
+      a[u] = i < E ? sv[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? x(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * T;
+      if (i < E) prod[i] = dmul(a[u], xv[u]);
+    }
+  }
+}
+
+template <int OP, bool CHEB, bool BB, bool HASC>
+__global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double sm_warp[3 * (kResThreads / 32)];
+  __shared__ double sm_tot[4];
+  const int b = blockIdx.x, G = p.G, T = blockDim.x, tid = threadIdx.x;
+  const int p0 = p.blk_row[b], p1 = p.blk_row[b + 1], R = p1 - p0;
+  const int64_t e0 = p.pos_ptr[p0];
+  const int E = (int)(p.pos_ptr[p1] - e0);
+  const int c0 = p.blk_ct[b], c1 = p.blk_ct[b + 1], C = c1 - c0;
+  const ResLayout Lo(E, R, C);  // this CTA's own footprint (launch size = max over CTAs)
+  double* sv = reinterpret_cast<double*>(smraw + Lo.o_sv);
+  double* prod = reinterpret_cast<double*>(smraw + Lo.o_prod);
+  int* sc = reinterpret_cast<int*>(smraw + Lo.o_sc);
+  int* rp = reinterpret_cast<int*>(smraw + Lo.o_rp);
+  int* rw = reinterpret_cast<int*>(smraw + Lo.o_row);
+  int* sl = reinterpret_cast<int*>(smraw + Lo.o_slot);
+  double* bs = reinterpret_cast<double*>(smraw + Lo.o_b);
+  double* ws = reinterpret_cast<double*>(smraw + Lo.o_w);
+  int* cm = reinterpret_cast<int*>(smraw + Lo.o_cm);
+  double* cfr = reinterpret_cast<double*>(smraw + Lo.o_fr);
+  double* cpar = reinterpret_cast<double*>(smraw + Lo.o_par);  // mu, mu2, phi, gamma
+  double* vs_s = reinterpret_cast<double*>(smraw + Lo.o_vs);
+  double* jt_s = reinterpret_cast<double*>(smraw + Lo.o_jt);
+  double* lam_s = reinterpret_cast<double*>(smraw + Lo.o_lam);  // [2][3C]
+
+
+  // ---- stage the partition on chip (once per launch) --------------------
+  for (int i = tid; i < E; i += T) {
+    sv[i] = __ldg(p.pk_val + e0 + i);
+    sc[i] = __ldg(p.pk_col + e0 + i);
+  }
+  for (int q = tid; q < R; q += T) {
+    const int row = __ldg(p.row_list + p0 + q);
+    rp[q] = (int)(__ldg(p.pos_ptr + p0 + q) - e0);
+    rw[q] = row;
+    sl[q] = HASC ? __ldg(p.row_slot + p0 + q) : -1;
+    bs[q] = __ldg(p.b + row);
+    ws[q] = __ldg(p.w + row);
+  }
+  if (tid == 0) rp[R] = E;
+  for (int k = tid; k < C; k += T) {
+    const int m = __ldg(p.cont_list + c0 + k);
+    cm[k] = m;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) cfr[9 * k + t] = __ldg(p.frames + 9 * (size_t)m + t);
+    cpar[4 * k + 0] = __ldg(p.mu + m);
+    cpar[4 * k + 1] = __ldg(p.mu2 + m);
+    cpar[4 * k + 2] = __ldg(p.phi + m);
+    cpar[4 * k + 3] = __ldg(p.gamma + m);
+  }
+  for (int t = tid; t < 6 * C; t += T) {
+    jt_s[t] = 0.0;
+    lam_s[t] = 0.0;
+  }
+  __syncthreads();
+
+  double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
+  const double u = p.under_relax;
+  const double omu = dsub(1.0, u);
+  double rho = 0.0, nu = 1.0, theta_prev = 0.0;
+  double alpha_prev = BB ? *p.w_mean : 0.0;
+  double alpha = 0.0;
+  bool pending = false;
+  int final_buf = 0, final_lam = 0, iters = 0, conv = 0, div = 0;
+  double consistency = NAN;
+  int epoch = 0;
+
+  for (int l = 1;; ++l) {
+    const bool check_only = (l == p.max_iters + 1);
+    const bool profl = p.prof != nullptr && l >= p.prof_iter0 && l < p.prof_iter0 + 4;
+    auto stamp = [&](int k) {  // phase timestamps for tuning (off unless p.prof is set)
+      if (profl) {
+        __syncthreads();
+        if (tid == 0) {
+          long long g;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+          p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 8 + k] = k == 7 ? g : clock64();
+        }
+      }
+    };
+    stamp(0);
+    const double* vcur = vb[(l - 1) % 3];   // written by other CTAs: coherent loads only
+    const double* vprev = vb[(l + 1) % 3];  // v^(l-2)
+    double* vnext = vb[l % 3];
+    double* lam_out = lam_s + (l & 1) * 3 * C;
+    double* part = p.partials + (size_t)(l & 1) * G * kPartialStride;
+
+    // ---- Barzilai-Borwein scalar step (solver.py:389-400) ----------------
+    bool use_alpha = false;
+    if (BB && l >= 2 && !check_only) {
+      products(sv, sc, prod, E, [&](int c) { return dsub(vcur[c], vprev[c]); });
+      __syncthreads();
+      double sz = 0.0, ss = 0.0, zz = 0.0;
+      for (int q = tid; q < R; q += T) {
+        double z = 0.0;
+        for (int k = rp[q]; k < rp[q + 1]; ++k) z = dadd(z, prod[k]);
+        const int row = rw[q];
+        const double s = dsub(vcur[row], vprev[row]);
+        sz = dadd(sz, dmul(s, z));
+        ss = dadd(ss, dmul(s, s));
+        zz = dadd(zz, dmul(z, z));
+      }
+      grid_reduce3(sz, ss, zz, part, 4, p.bar_flags, G, ++epoch, sm_warp, sm_tot);
+      const double tsz = sm_tot[0], tss = sm_tot[1], tzz = sm_tot[2];
+      const bool bb1 = (p.step == VFPI_STEP_BB1) || (p.step == VFPI_STEP_BB_ALTERNATING && (l % 2 == 0));
+      if (tsz <= 0.0) alpha = alpha_prev;
+      else alpha = bb1 ? ddiv(tss, tsz) : ddiv(tsz, tzz);
+      alpha_prev = alpha;
+      use_alpha = true;
+      __syncthreads();  // prod is reused below
+    }
+
+    if (CHEB && !check_only) {  // solver.py:284-290, :417
+      if (l < p.cheby_start) nu = 1.0;
+      else if (l == p.cheby_start) nu = ddiv(2.0, dsub(2.0, dmul(rho, rho)));
+      else nu = ddiv(4.0, dsub(4.0, dmul(dmul(rho, rho), nu)));
+    }
+
+    double th = 0.0, fr = 0.0, nf = 0.0;
+    auto finish_row = [&](int row, double vnew, double vc) {
+      double vn = vnew;
+      if (CHEB) {
+        const double vss = dadd(dmul(u, vnew), dmul(omu, vc));
+        if (l > 1) {
+          const double vp = vprev[row];
+          vn = dadd(dmul(nu, dsub(vss, vp)), vp);
+        } else {
+          vn = vss;
+        }
+      }
+      const double d = dsub(vn, vc);
+      th = dadd(th, dmul(d, d));
+      if (!isfinite(vn)) nf = dadd(nf, 1.0);
+      vnext[row] = vn;
+    };
+
+    // ---- (1) surrogate-dynamics sweep: pass A gathers, pass B ordered sums --
+    stamp(1);
+    products(sv, sc, prod, E, [&](int c) { return vcur[c]; });
+    __syncthreads();
+    stamp(2);
+    for (int q = tid; q < R; q += T) {
+      double acc = 0.0;
+      const int k1 = rp[q + 1];
+      for (int k = rp[q]; k < k1; ++k) acc = dadd(acc, prod[k]);
+      const int row = rw[q];
+      const int slot = sl[q];
+      const double r = dsub(acc, bs[q]);
+      const double f = (slot >= 0) ? dsub(r, jt_s[slot]) : dsub(r, 0.0);  // solver.py:437-439
+      fr = dadd(fr, dmul(f, f));
+      if (!check_only) {
+        const double wr = use_alpha ? alpha : ws[q];
+        const double vc = vcur[row];
+        const double vstar = dsub(vc, dmul(wr, r));
+        if (slot >= 0) {
+          vs_s[slot] = vstar;
+        } else {
+          finish_row(row, HASC ? dadd(vstar, dmul(wr, 0.0)) : vstar, vc);
+        }
+      }
+    }
+
+    // ---- (2)(3)(2') contacts out of shared memory ------------------------
+    stamp(3);
+    if (HASC && !check_only) {
+      __syncthreads();
+      for (int k = tid; k < C; k += T) {
+        const int m = cm[k];
+        const int loc = k * kSlotsPerContact;
+        const int ci = __ldg(p.col_i + m), cj = __ldg(p.col_j + m);
+        const double* R9 = cfr + 9 * k;
+        double vi[3], vj[3] = {0.0, 0.0, 0.0}, rel[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) vi[t] = vs_s[loc + t];
+        if (cj >= 0) {
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            vj[t] = vs_s[loc + 3 + t];
+            rel[t] = dsub(vi[t], vj[t]);
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 3; ++t) rel[t] = vi[t];
+        }
+        double Rr[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) Rr[t] = R9[t];
+        double eta[3], lam[3], world[3];
+        frame_apply(Rr, rel, eta);
+        double g;
+        if (use_alpha) g = (cj >= 0) ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
+        else g = cpar[4 * k + 3];
+        trial_impulse(eta, cpar[4 * k + 2], g, lam);
+        project(OP, lam, cpar[4 * k + 0], cpar[4 * k + 1]);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) lam_out[3 * k + t] = lam[t];
+        frame_apply_t(Rr, lam, world);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int row = ci + t;
+          const double oi = dadd(0.0, world[t]);
+          jt_s[loc + t] = oi;
+          const double wr = use_alpha ? alpha : __ldg(p.w + row);
+          finish_row(row, dadd(vi[t], dmul(wr, oi)), vcur[row]);
+        }
+        if (cj >= 0) {
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int row = cj + t;
+            const double oj = dsub(0.0, world[t]);
+            jt_s[loc + 3 + t] = oj;
+            const double wr = use_alpha ? alpha : __ldg(p.w + row);
+            finish_row(row, dadd(vj[t], dmul(wr, oj)), vcur[row]);
+          }
+        }
+      }
+    }
+
+    // ---- (4) residual reduction + grid-wide decision --------------------
+    stamp(4);
+    stamp(7);
+    grid_reduce3(th, fr, nf, part, 0, p.bar_flags, G, ++epoch, sm_warp, sm_tot);
+    stamp(5);
+    const double theta = dsqrt(sm_tot[0]);
+    const double fres = dsqrt(sm_tot[1]);
+    const bool nonfinite = sm_tot[2] > 0.0;
+    if (pending) {
+      consistency = fres;
+      if (fres <= dmul(p.cfactor, p.tol)) {
+        iters = l - 1; conv = 1;
+        final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
+        break;
+      }
+    }
+    if (check_only) {
+      iters = p.max_iters;
+      consistency = fres;
+      final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
+      break;
+    }
+    if (b == 0 && tid == 0) p.trace[l - 1] = theta;
+    if (nonfinite) {
+      iters = l; div = 1;
+      final_buf = l % 3; final_lam = l & 1;
+      break;
+    }
+    pending = theta < p.tol;
+    if (CHEB) rho = (theta_prev <= 0.0) ? rho : py_min(ddiv(theta, theta_prev), 1.0);
+    theta_prev = theta;
+  }
+
+  const double* vfin = vb[final_buf];
+  for (int q = tid; q < R; q += T) p.out_v[rw[q]] = vfin[rw[q]];
+  const double* lfin = lam_s + final_lam * 3 * C;
+  for (int k = tid; k < C; k += T) {
+    const int m = cm[k];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) p.out_lam[3 * (size_t)m + t] = lfin[3 * k + t];
+  }
+  if (b == 0 && tid == 0) {
+    p.status->iterations = iters;
+    p.status->converged = conv;
+    p.status->diverged = div;
+    p.status->final_vbuf = final_buf;
+    p.status->consistency = consistency;
+  }
+}
+
+using KernelFn = void (*)(IterParams);
+
+template <int OP>
+KernelFn pick3(bool cheb, bool bb, bool hasc) {
+  if (cheb) {
+    if (bb) return hasc ? k_iterate_res<OP, true, true, true> : k_iterate_res<OP, true, true, false>;
+    return hasc ? k_iterate_res<OP, true, false, true> : k_iterate_res<OP, true, false, false>;
+  }
+  if (bb) return hasc ? k_iterate_res<OP, false, true, true> : k_iterate_res<OP, false, true, false>;
+  return hasc ? k_iterate_res<OP, false, false, true> : k_iterate_res<OP, false, false, false>;
+}
+
+KernelFn pick(int op, bool cheb, bool bb, bool hasc) {
+  if (op == OP_PROXIMAL) return pick3<OP_PROXIMAL>(cheb, bb, hasc);
+  if (op == OP_ANISO) return pick3<OP_ANISO>(cheb, bb, hasc);
+  return pick3<OP_STRICT>(cheb, bb, hasc);
+}
+
+}  // namespace
+
+
+int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, size_t smem_bytes, cudaStream_t st,
+                            std::string& err) {
+  KernelFn f = pick(op, cheb, bb, p.n_c > 0);
+  cudaError_t e = ensure_max_dynamic_smem((const void*)f);
+  if (e != cudaSuccess) { err = std::string("smem attribute: ") + cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
+  int nb = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kResThreads, smem_bytes);
+  if (e != cudaSuccess || nb < 1) { err = "resident kernel does not fit on an SM"; return VFPI_UNSUPPORTED; }
+  IterParams local = p;
+  void* args[] = {&local};
+  e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kResThreads), args, smem_bytes, st);
+  if (e != cudaSuccess) {
+    err = std::string("cooperative launch (resident): ") + cudaGetErrorString(e);
+    return VFPI_CUDA_ERROR;
+  }
+  return VFPI_OK;
+}
+
+}  // namespace vfpi

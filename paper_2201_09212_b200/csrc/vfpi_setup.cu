@@ -17,8 +17,12 @@ namespace vfpi {
 
 namespace {
 
-constexpr int kRowCost = 2;      // per-row overhead in the partition cost model
-constexpr int kContactCost = 24; // per-contact work in the partition cost model
+// Partition cost model, in bytes of per-CTA state (the resident kernel's
+// shared-memory footprint, which also tracks per-iteration work): 20 B per
+// numeric entry (value, column, product), 28 B per row, 252 B per contact.
+constexpr int kEntryCost = 20;
+constexpr int kRowCost = 28;
+constexpr int kContactCost = 252;
 
 #define VFPI_CK(x)                                                     \
   do {                                                                 \
@@ -101,16 +105,16 @@ __global__ void k_units(int n, const int* __restrict__ mark, const int* __restri
   int64_t cost = 0;
   int rows = 0, ct = 0;
   if (m < 0) {
-    cost = rowcnt[r] + kRowCost;
+    cost = (int64_t)kEntryCost * rowcnt[r] + kRowCost;
     rows = 1;
   } else if (r == ci[m]) {
     const int i = ci[m], j = cj[m];
     ct = 1;
     rows = (j >= 0) ? 6 : 3;
     cost = kContactCost;
-    for (int t = 0; t < 3; ++t) cost += rowcnt[i + t] + kRowCost;
+    for (int t = 0; t < 3; ++t) cost += (int64_t)kEntryCost * rowcnt[i + t] + kRowCost;
     if (j >= 0)
-      for (int t = 0; t < 3; ++t) cost += rowcnt[j + t] + kRowCost;
+      for (int t = 0; t < 3; ++t) cost += (int64_t)kEntryCost * rowcnt[j + t] + kRowCost;
   }
   ucost[r] = cost;
   urows[r] = rows;
@@ -205,11 +209,48 @@ __global__ void k_slice_width(int S_max, int G, const SetupSummary* __restrict__
   width[s] = 32 * (int64_t)W;
 }
 
-__global__ void k_summary(int n, const int64_t* row_ptr, const int64_t* slice_off, const int* flags,
+__global__ void k_poslen(int n, const int* __restrict__ row_list, const int* __restrict__ rowcnt, int64_t* len) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > n) return;
+  len[p] = (p < n) ? rowcnt[row_list[p]] : 0;
+}
+
+__global__ void k_summary(int n, int G, const int64_t* row_ptr, const int64_t* slice_off,
+                          const int64_t* pos_ptr, const int* blk_row, const int* blk_ct, const int* flags,
                           SetupSummary* sum) {
   sum->nnz_num = row_ptr[n];
   sum->sell_elems = slice_off[sum->n_slices];
   sum->flags = *flags;
+  int64_t me = 0, mb = 0;
+  int mr = 0;
+  for (int b = 0; b < G; ++b) {
+    const int64_t e = pos_ptr[blk_row[b + 1]] - pos_ptr[blk_row[b]];
+    const int r = blk_row[b + 1] - blk_row[b];
+    const int64_t by = (int64_t)ResLayout(e, r, blk_ct[b + 1] - blk_ct[b]).total;
+    me = e > me ? e : me;
+    mr = r > mr ? r : mr;
+    mb = by > mb ? by : mb;
+  }
+  sum->max_ent_per_blk = me;
+  sum->max_rows_per_blk = mr;
+  sum->max_res_bytes = mb;
+}
+
+// CTA-contiguous CSR: the entries of row-list position p at pos_ptr[p]..
+__global__ void k_pack_csr(int n, const int* __restrict__ row_list, const int* __restrict__ rowcnt,
+                           const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ pos_ptr,
+                           const int* __restrict__ perm, const int* __restrict__ colof,
+                           const double* __restrict__ data, double* __restrict__ pv, int* __restrict__ pc) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int row = row_list[p];
+  const int len = rowcnt[row];
+  const int64_t src = row_ptr[row], dst = pos_ptr[p];
+  for (int k = 0; k < len; ++k) {
+    const int e = perm[src + k];
+    pv[dst + k] = data[e];
+    pc[dst + k] = colof[e];
+  }
 }
 
 __global__ void k_iota(int64_t n, int* v) {
@@ -397,13 +438,17 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   const int S_max = (n + 31) / 32 + G;  // each CTA rounds its row count up once
   VFPI_CK(ensure(ws.slice_w, 8 * (size_t)(S_max + 1)));
   VFPI_CK(ensure(ws.slice_off, 8 * (size_t)(S_max + 1)));
+  VFPI_CK(ensure(ws.pos_len, 8 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.pos_ptr, 8 * (size_t)(n + 1)));
 
   size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t1, P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr), n + 1, st);
   cub::DeviceScan::ExclusiveSum(nullptr, t2, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), n, st);
   cub::DeviceScan::ExclusiveSum(nullptr, t3, P<int>(ws.urows), P<int>(ws.rpos), n, st);
   cub::DeviceScan::ExclusiveSum(nullptr, t4, P<int64_t>(ws.slice_w), P<int64_t>(ws.slice_off), S_max + 1, st);
-  VFPI_CK(ensure(ws.cub_tmp, std::max(std::max(t1, t2), std::max(t3, t4))));
+  size_t t5 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t5, P<int64_t>(ws.pos_len), P<int64_t>(ws.pos_ptr), n + 1, st);
+  VFPI_CK(ensure(ws.cub_tmp, std::max(std::max(std::max(t1, t2), std::max(t3, t4)), t5)));
   size_t tb = ws.cub_tmp.cap;
 
   VFPI_CK(cudaMemsetAsync(ws.rowcnt.p, 0, 4 * (size_t)(n + 1), st));
@@ -452,8 +497,12 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
                                                  P<int64_t>(ws.slice_w));
   VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.slice_w), P<int64_t>(ws.slice_off),
                                         S_max + 1, st));
-  k_summary<<<1, 1, 0, st>>>(n, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int>(ws.flags),
-                             P<SetupSummary>(ws.summary));
+  k_poslen<<<nblk(n + 1), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.pos_len));
+  VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.pos_len), P<int64_t>(ws.pos_ptr), n + 1,
+                                        st));
+  k_summary<<<1, 1, 0, st>>>(n, G, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int64_t>(ws.pos_ptr),
+                             P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.flags), P<SetupSummary>(ws.summary));
+  launches += 3;
   launches += 3;
   VFPI_CK(cudaGetLastError());
   VFPI_CK(cudaMemcpyAsync(hs, ws.summary.p, sizeof(SetupSummary), cudaMemcpyDeviceToHost, st));
@@ -465,31 +514,52 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
     return VFPI_UNSUPPORTED;
   }
 
-  // Phase 2: stable radix sort of CSC entries by row -> per-row increasing
-  // column order (scipy's accumulation order), then SELL-32 packing.
+  return VFPI_OK;
+}
+
+// Phase 2: stable radix sort of CSC entries by row -> per-row increasing
+// column order (scipy's accumulation order), then packing for the kernel.
+int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const SetupSummary& hs, cudaStream_t st,
+               std::string& err, int64_t& launches) {
+  const int n = (int)s.n;
+  const int64_t nnz = s.nnz;
+  const int S = hs.n_slices;
   VFPI_CK(ensure(ws.vals, 4 * (size_t)nnz));
   VFPI_CK(ensure(ws.perm, 4 * (size_t)nnz));
   VFPI_CK(ensure(ws.keys_sorted, 4 * (size_t)nnz));
-  VFPI_CK(ensure(ws.sell_val, 8 * (size_t)hs->sell_elems));
-  VFPI_CK(ensure(ws.sell_col, 4 * (size_t)hs->sell_elems));
   if (nnz > 0) {
     const int eb = end_bit_for(n);
     size_t ts = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, ts, P<int>(ws.keys), P<int>(ws.keys_sorted), P<int>(ws.vals),
                                     P<int>(ws.perm), (int)nnz, 0, eb, st);
     VFPI_CK(ensure(ws.cub_tmp, ts));
-    tb = ws.cub_tmp.cap;
+    size_t tb = ws.cub_tmp.cap;
     k_iota<<<nblk(nnz), 256, 0, st>>>(nnz, P<int>(ws.vals));
     VFPI_CK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.keys), P<int>(ws.keys_sorted),
                                             P<int>(ws.vals), P<int>(ws.perm), (int)nnz, 0, eb, st));
-    launches += 4;  // iota + onesweep passes (approximate count for the sort)
+    launches += 3 + (eb + 7) / 8;  // iota, histogram, exclusive-sum, one onesweep pass per 8 key bits
   }
-  if (S > 0) {
-    k_pack<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row), P<int>(ws.row_list),
-                                                  P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr), P<int>(ws.perm),
-                                                  P<int>(ws.colof), s.data, P<int64_t>(ws.slice_off),
-                                                  P<double>(ws.sell_val), P<int>(ws.sell_col));
-    ++launches;
+  (void)G;
+  if (resident) {
+    VFPI_CK(ensure(ws.pk_val, 8 * (size_t)hs.nnz_num));
+    VFPI_CK(ensure(ws.pk_col, 4 * (size_t)hs.nnz_num));
+    if (n > 0) {
+      k_pack_csr<<<nblk(n, 128), 128, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr),
+                                          P<int64_t>(ws.pos_ptr), P<int>(ws.perm), P<int>(ws.colof), s.data,
+                                          P<double>(ws.pk_val), P<int>(ws.pk_col));
+      ++launches;
+    }
+  } else {
+    VFPI_CK(ensure(ws.sell_val, 8 * (size_t)hs.sell_elems));
+    VFPI_CK(ensure(ws.sell_col, 4 * (size_t)hs.sell_elems));
+    if (S > 0) {
+      k_pack<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row),
+                                                    P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr),
+                                                    P<int>(ws.perm), P<int>(ws.colof), s.data,
+                                                    P<int64_t>(ws.slice_off), P<double>(ws.sell_val),
+                                                    P<int>(ws.sell_col));
+      ++launches;
+    }
   }
   VFPI_CK(cudaGetLastError());
   return VFPI_OK;

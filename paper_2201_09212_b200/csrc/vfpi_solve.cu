@@ -400,8 +400,7 @@ KernelFn pick(int op, bool cheb, bool bb, bool hasc) {
 
 int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes) {
   KernelFn f = pick(op, cheb, bb, true);
-  if (smem_bytes > 48 * 1024)
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (ensure_max_dynamic_smem((const void*)f) != cudaSuccess) return 0;
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, smem_bytes) != cudaSuccess) return 0;
   return nb;
@@ -410,8 +409,8 @@ int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes) {
 int launch_iterate(const IterParams& p, int op, bool cheb, bool bb, int smem_bytes, cudaStream_t st,
                    std::string& err) {
   KernelFn f = pick(op, cheb, bb, p.n_c > 0);
-  if (smem_bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  {
+    cudaError_t e = ensure_max_dynamic_smem((const void*)f);
     if (e != cudaSuccess) { err = cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
   }
   IterParams local = p;

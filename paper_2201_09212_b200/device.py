@@ -61,8 +61,10 @@ class DeviceSystem:
         res.v, res.lam, res.residual_trace = _dptr(self.v, f64), _dptr(self.lam, f64), _dptr(self.trace, f64)
         res.scc, res.w = _dptr(self.scc, f64), None
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        code = h.L.vfpi_solve_device(h.h, self.sysc, _c_config(cfg), _dptr(warm, f64), None, res,
-                                     C.c_void_p(st.cuda_stream))
+        # torch's default stream is the legacy NULL stream; the C-ABI reads NULL
+        # as "the handle's own stream", so pass cudaStreamLegacy explicitly
+        sp = st.cuda_stream if st.cuda_stream else 1
+        code = h.L.vfpi_solve_device(h.h, self.sysc, _c_config(cfg), _dptr(warm, f64), None, res, C.c_void_p(sp))
         _raise_for(code, h)
         self._res = res
         return res

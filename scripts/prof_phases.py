@@ -1,0 +1,36 @@
+"""Per-CTA phase timing of the resident iteration kernel on configs[1] (tuning aid)."""
+import ctypes as C
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from paper_2201_09212_b200 import _lib  # noqa: E402
+from paper_2201_09212_b200.scenes import rigid_contact_system  # noqa: E402
+from paper_2201_09212_b200.solver import SolverConfig, solve_packed  # noqa: E402
+
+nb = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+nc = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+ps = rigid_contact_system(nb, nc, 2201)
+h = _lib.handle(0)
+cfg = SolverConfig(residual_tol=1e-8, max_iters=1000)
+solve_packed(ps, cfg, np.zeros(ps.n))
+v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
+print("layout", h.last_layout(), "loop_ms", rep.timings["loop_s"] * 1e3, "setup_ms", rep.timings["setup_s"] * 1e3)
+h.L.vfpi_set_profile(h.h, 500)
+solve_packed(ps, cfg, np.zeros(ps.n))
+G = h.last_layout()["ctas"]
+buf = (C.c_longlong * (32 * G))()
+h.L.vfpi_get_profile(h.h, buf, 32 * G)
+a = np.frombuffer(buf, dtype=np.int64).reshape(G, 4, 8)
+names = ["bb/cheb", "products", "pass B", "contacts", "reduce+barrier"]
+for k, nm in enumerate(names):
+    d = a[:, :, k + 1] - a[:, :, k] if k < 4 else a[:, :, 5] - a[:, :, 4]
+    print(f"{nm:16s} cycles mean {d.mean():9.0f}  max {d.max():9.0f}  min {d.min():9.0f}")
+tot = a[:, :, 5] - a[:, :, 0]
+print(f"{'iteration':16s} cycles mean {tot.mean():9.0f}  max {tot.max():9.0f}")
+work = a[:, :, 4] - a[:, :, 0]
+print("work (pre-barrier) per CTA: mean", work.mean(), "max", work.max(), "argmax cta", int(work.mean(1).argmax()))
+arr = a[:, :, 7]
+print("arrival skew (globaltimer ns) per iteration:", (arr.max(0) - arr.min(0)).tolist())
+h.L.vfpi_set_profile(h.h, 0)

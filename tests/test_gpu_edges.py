@@ -145,16 +145,25 @@ def test_concurrent_threads_independent_handles():
         assert np.array_equal(o, ref)
 
 
-def test_config1_full_size_matches_oracle_prefix():
+@pytest.mark.parametrize("mode", ["auto", "streaming"])
+def test_config1_full_size_matches_oracle_prefix(mode):
     """configs[1] at full size (122,880 DOF, 16,384 contacts): the first 40
     iterations bit-match the CPU oracle (plain V-FPI, no OpenBLAS-ordered
-    decision involved)."""
+    decision involved), on both iteration kernels."""
     from oracle import vfpi_oracle as O
+    from paper_2201_09212_b200 import _lib
     from paper_2201_09212_b200.solver import SolverConfig, solve_packed
 
     ps = _rigid(4096, 16384, seed=2201)
     cfg = SolverConfig(residual_tol=1e-8, max_iters=40)
-    v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
+    h = _lib.handle()
+    h.set_kernel(mode)
+    try:
+        v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
+        layout = h.last_layout()
+    finally:
+        h.set_kernel("auto")
+    assert layout["resident"] == (mode == "auto")  # configs[1] fits on chip: the resident kernel is the default
     s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64), ps.col_j.astype(np.int64),
                  ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
     vo, lo, ro = O.solve(s, O.Config(residual_tol=1e-8, max_iters=40), np.zeros(ps.n))

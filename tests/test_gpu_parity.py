@@ -21,26 +21,36 @@ CASES = names()
 TOL = 1e-9
 
 
-def _solve(d):
+def _solve(d, mode="auto"):
+    from paper_2201_09212_b200 import _lib
     from paper_2201_09212_b200.solver import solve_packed
 
-    return solve_packed(packed(d), config(d), d["warm"], d.get("w_cached"))
+    h = _lib.handle()
+    h.set_kernel(mode)
+    try:
+        return solve_packed(packed(d), config(d), d["warm"], d.get("w_cached"))
+    finally:
+        h.set_kernel("auto")
 
 
+MODES = ["resident", "streaming"]
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", CASES)
-def test_solve_matches_reference(name):
+def test_solve_matches_reference(name, mode):
     from paper_2201_09212_b200.errors import DivergenceError
 
     d = load(name)
     if d["out_diverged"]:
         with pytest.raises(DivergenceError) as exc:
-            _solve(d)
+            _solve(d, mode)
         tr = np.asarray(exc.value.residual_trace)
         assert len(tr) == int(d["out_iterations"])
         fin = np.isfinite(d["out_trace"])
         assert np.allclose(tr[fin], d["out_trace"][fin], rtol=1e-6)
         return
-    v, lam, rep = _solve(d)
+    v, lam, rep = _solve(d, mode)
     assert rep.iterations == int(d["out_iterations"]), (rep.iterations, int(d["out_iterations"]))
     assert rep.converged == bool(d["out_converged"])
     assert relerr(v, d["out_v"]) <= TOL
@@ -60,10 +70,11 @@ BITWISE = [c for c in CASES
            and load(c)["cfg"]["operator"] != "strict-anisotropic" and not load(c)["out_diverged"]]
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", BITWISE)
-def test_plain_iteration_bit_identical(name):
+def test_plain_iteration_bit_identical(name, mode):
     d = load(name)
-    v, lam, rep = _solve(d)
+    v, lam, rep = _solve(d, mode)
     assert rep.iterations == int(d["out_iterations"])
     assert np.array_equal(v, d["out_v"])
     assert np.array_equal(lam.ravel(), d["out_lam"])
