@@ -178,7 +178,9 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.urows, &h->ws.rpos, &h->ws.ucont, &h->ws.kpos, &h->ws.blk_row, &h->ws.blk_ct,
                             &h->ws.blk_slice, &h->ws.row_list, &h->ws.row_slot, &h->ws.cont_list,
                             &h->ws.slice_w, &h->ws.slice_off, &h->ws.sell_val, &h->ws.sell_col, &h->ws.pos_len, &h->ws.pos_ptr,
-                            &h->ws.pk_val, &h->ws.pk_col, &h->ws.bar_flags, &h->ws.vbuf,
+                            &h->ws.pk_val, &h->ws.pk_col, &h->ws.bar_flags, &h->ws.ucr, &h->ws.ufr,
+                            &h->ws.cposc, &h->ws.cposf, &h->ws.blk_first, &h->ws.blk_cr, &h->ws.cont_q,
+                            &h->ws.ps_col, &h->ws.ps_src, &h->ws.seg_beg, &h->ws.seg_end, &h->ws.rowpos, &h->ws.vbuf,
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
                             &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
   for (auto* b : bufs)
@@ -258,7 +260,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches);
   if (rc) return rc;
   const size_t smem_res = (size_t)hs->max_res_bytes;
-  const bool fits = hs->max_ent_per_blk < (1 << 24) && smem_res + 2048 <= (size_t)ws.max_smem_optin;
+  const bool fits = hs->max_ent_per_blk < (1 << 24) && smem_res + 2048 <= (size_t)ws.max_smem_optin && G <= 256;
   if (h->kernel_mode == 1 && !fits) { h->err = "partition does not fit in shared memory"; return VFPI_UNSUPPORTED; }
   const bool resident = fits && h->kernel_mode != 2;
   int smem = 0;
@@ -311,6 +313,11 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.pos_ptr = P<int64_t>(ws.pos_ptr);
   p.pk_val = P<double>(ws.pk_val);
   p.pk_col = P<int>(ws.pk_col);
+  p.ps_col = P<int>(ws.ps_col);
+  p.ps_src = P<int>(ws.ps_src);
+  p.blk_cr = P<int>(ws.blk_cr);
+  p.cont_q = P<int>(ws.cont_q);
+  p.rowpos = P<int>(ws.rowpos);
   p.bar_flags = P<int>(ws.bar_flags);
   p.prof = nullptr;
   p.prof_iter0 = 0;

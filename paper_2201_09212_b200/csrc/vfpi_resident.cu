@@ -15,6 +15,8 @@
 //     residual reduction: every CTA publishes (theta^2, force^2, #nonfinite)
 //     and an epoch flag; every CTA waits for all flags and sums the G partials
 //     in the same fixed order, so decisions are identical everywhere.
+#include <climits>
+
 #include "vfpi_internal.cuh"
 #include "vfpi_math.cuh"
 
@@ -22,32 +24,19 @@ namespace vfpi {
 
 namespace {
 
-__device__ __forceinline__ int ld_flag(const int* p) {
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-// all CTAs of the grid reach this point; partial sums of iteration `epoch` are
-// published in part[b*kPartialStride + off .. +2] before the flag
-__device__ __forceinline__ void flag_barrier(int* flags, int G, int epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(epoch) : "memory");
-  }
-  if (threadIdx.x < 32) {
-    for (int g = threadIdx.x; g < G; g += 32) {
-      const long long t0 = clock64();
-      while (ld_flag(flags + g) < epoch) {
-        if (clock64() - t0 > (1ll << 36)) __trap();  // ~30 s: never in a healthy run
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// fixed-order CTA sum of three doubles -> sm_out[0..2] (visible after the trailing barrier)
 __device__ __forceinline__ void cta_reduce3(double a, double b, double c, double* sm_warp, double* sm_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
@@ -62,38 +51,70 @@ __device__ __forceinline__ void cta_reduce3(double a, double b, double c, double
     sm_warp[3 * warp + 2] = c;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double x = 0.0, y = 0.0, z = 0.0;
-    for (int w = 0; w < nw; ++w) {
-      x = dadd(x, sm_warp[3 * w + 0]);
-      y = dadd(y, sm_warp[3 * w + 1]);
-      z = dadd(z, sm_warp[3 * w + 2]);
+  if (warp == 0) {
+    double x = lane < nw ? sm_warp[3 * lane + 0] : 0.0;
+    double y = lane < nw ? sm_warp[3 * lane + 1] : 0.0;
+    double z = lane < nw ? sm_warp[3 * lane + 2] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      x = dadd(x, __shfl_xor_sync(0xffffffffu, x, o));
+      y = dadd(y, __shfl_xor_sync(0xffffffffu, y, o));
+      z = dadd(z, __shfl_xor_sync(0xffffffffu, z, o));
     }
-    sm_out[0] = x;
-    sm_out[1] = y;
-    sm_out[2] = z;
+    if (lane == 0) {
+      sm_out[0] = x;
+      sm_out[1] = y;
+      sm_out[2] = z;
+    }
   }
 }
 
-// publish this CTA's three partials, barrier, reduce all G in fixed order
-__device__ __forceinline__ void grid_reduce3(double a, double b, double c, double* part, int off, int* flags, int G,
-                                             int epoch, double* sm_warp, double* sm_tot) {
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier fused with the deterministic reduction of three partial sums.
+// Arrive: thread 0 stores the CTA's partials, then one release reduction on a
+// monotonic counter (target epoch*G: no reset between barriers). Wait: thread
+// 0 spins with acquire loads on that single word. Collect: warp 0 reads the G
+// partials (<= 8 independent loads per lane) and reduces them in a fixed order
+// that is identical in every CTA, so every CTA gets bit-identical totals.
+constexpr int kMaxPartialsPerLane = 8;  // G <= 256
+
+__device__ __forceinline__ void grid_reduce3(double a, double b, double c, double* part, int off, unsigned* counter,
+                                             int G, int epoch, double* sm_warp, double* sm_tot) {
   cta_reduce3(a, b, c, sm_warp, sm_tot);
   if (threadIdx.x == 0) {
     double* q = part + (size_t)blockIdx.x * kPartialStride + off;
     q[0] = sm_tot[0];
     q[1] = sm_tot[1];
     q[2] = sm_tot[2];
+    red_release_add(counter, 1u);
+    const unsigned target = (unsigned)epoch * (unsigned)G;
+    const long long t0 = clock64();
+    while (ld_acquire_u32(counter) < target) {
+      if (clock64() - t0 > (1ll << 36)) __trap();  // ~30 s: never in a healthy run
+    }
   }
-  flag_barrier(flags, G, epoch);
+  __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double x = 0.0, y = 0.0, z = 0.0;
-    for (int g = lane; g < G; g += 32) {
-      const double* q = part + (size_t)g * kPartialStride + off;
-      x = dadd(x, __ldcg(q + 0));
-      y = dadd(y, __ldcg(q + 1));
-      z = dadd(z, __ldcg(q + 2));
+#pragma unroll
+    for (int k = 0; k < kMaxPartialsPerLane; ++k) {
+      const int g = lane + 32 * k;
+      if (g < G) {
+        const double* q = part + (size_t)g * kPartialStride + off;
+        x = dadd(x, __ldcg(q + 0));
+        y = dadd(y, __ldcg(q + 1));
+        z = dadd(z, __ldcg(q + 2));
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -110,28 +131,40 @@ __device__ __forceinline__ void grid_reduce3(double a, double b, double c, doubl
   __syncthreads();
 }
 
-// pass A: prod[e] = a[e] * x(col[e]) over the CTA's entries, 8 independent gathers per thread in flight
+// pass A: prod[dst[i]] = a[i] * x(col[i]) over the CTA's column-sorted entries
+// (neighbouring lanes gather neighbouring columns), UN gathers per thread in flight
 template <class X>
 __device__ __forceinline__ void products(const double* __restrict__ sv, const int* __restrict__ sc,
-                                         double* __restrict__ prod, int E, X x) {
+                                         const int* __restrict__ sd, double* __restrict__ prod, int E, X x) {
+  constexpr int UN = 8;
   const int T = blockDim.x;
-  for (int base = threadIdx.x; base < E; base += 8 * T) {
-    int c[8];
-    double a[8], xv[8];
+  for (int base = threadIdx.x; base < E; base += UN * T) {
+    int c[UN];
+    double xv[UN];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < UN; ++u) {
       const int i = base + u * T;
-      c[u] = i < E ? sc[i] : -1;
-      a[u] = i < E ? sv[i] : 0.0;
+      c[u] = i < E ? sc[i] : INT_MIN;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? x(c[u]) : 0.0;
+    for (int u = 0; u < UN; ++u) xv[u] = c[u] != INT_MIN ? x(c[u]) : 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < UN; ++u) {
       const int i = base + u * T;
-      if (i < E) prod[i] = dmul(a[u], xv[u]);
+      if (i < E) prod[sd[i]] = dmul(sv[i], xv[u]);
     }
   }
+}
+
+// pass B: sequential (scipy-order) sum of one row's products, loads batched by 4
+__device__ __forceinline__ double row_sum(const double* __restrict__ prod, int k, int k1) {
+  double acc = 0.0;
+  for (; k + 4 <= k1; k += 4) {
+    const double t0 = prod[k], t1 = prod[k + 1], t2 = prod[k + 2], t3 = prod[k + 3];
+    acc = dadd(dadd(dadd(dadd(acc, t0), t1), t2), t3);
+  }
+  for (; k < k1; ++k) acc = dadd(acc, prod[k]);
+  return acc;
 }
 
 template <int OP, bool CHEB, bool BB, bool HASC>
@@ -144,40 +177,47 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   const int64_t e0 = p.pos_ptr[p0];
   const int E = (int)(p.pos_ptr[p1] - e0);
   const int c0 = p.blk_ct[b], c1 = p.blk_ct[b + 1], C = c1 - c0;
-  const ResLayout Lo(E, R, C);  // this CTA's own footprint (launch size = max over CTAs)
+  const int CR = HASC ? p.blk_cr[b] : 0;  // rows [0, CR) belong to the CTA's contacts
+  const ResLayout Lo(E, R, C, CR);        // this CTA's own footprint (launch size = max over CTAs)
   double* sv = reinterpret_cast<double*>(smraw + Lo.o_sv);
   double* prod = reinterpret_cast<double*>(smraw + Lo.o_prod);
   int* sc = reinterpret_cast<int*>(smraw + Lo.o_sc);
+  int* sd = reinterpret_cast<int*>(smraw + Lo.o_sd);
   int* rp = reinterpret_cast<int*>(smraw + Lo.o_rp);
   int* rw = reinterpret_cast<int*>(smraw + Lo.o_row);
-  int* sl = reinterpret_cast<int*>(smraw + Lo.o_slot);
   double* bs = reinterpret_cast<double*>(smraw + Lo.o_b);
   double* ws = reinterpret_cast<double*>(smraw + Lo.o_w);
+  double* vown = reinterpret_cast<double*>(smraw + Lo.o_v0);   // own rows of v^(l-1)
+  double* vown2 = reinterpret_cast<double*>(smraw + Lo.o_v1);  // own rows of v^(l)
   int* cm = reinterpret_cast<int*>(smraw + Lo.o_cm);
+  int* cq = reinterpret_cast<int*>(smraw + Lo.o_cq);
   double* cfr = reinterpret_cast<double*>(smraw + Lo.o_fr);
   double* cpar = reinterpret_cast<double*>(smraw + Lo.o_par);  // mu, mu2, phi, gamma
-  double* vs_s = reinterpret_cast<double*>(smraw + Lo.o_vs);
-  double* jt_s = reinterpret_cast<double*>(smraw + Lo.o_jt);
-  double* lam_s = reinterpret_cast<double*>(smraw + Lo.o_lam);  // [2][3C]
-
+  double* lam_s = reinterpret_cast<double*>(smraw + Lo.o_lam); // [2][3C]
+  double* vs_s = reinterpret_cast<double*>(smraw + Lo.o_vs);   // [CR]
+  double* jt_s = reinterpret_cast<double*>(smraw + Lo.o_jt);   // [CR]
 
   // ---- stage the partition on chip (once per launch) --------------------
   for (int i = tid; i < E; i += T) {
-    sv[i] = __ldg(p.pk_val + e0 + i);
-    sc[i] = __ldg(p.pk_col + e0 + i);
+    const int src = __ldg(p.ps_src + e0 + i);
+    const int c = __ldg(p.ps_col + e0 + i);
+    sc[i] = c;
+    sd[i] = (int)(src - e0);
+    sv[i] = __ldg(p.pk_val + src);
   }
   for (int q = tid; q < R; q += T) {
     const int row = __ldg(p.row_list + p0 + q);
     rp[q] = (int)(__ldg(p.pos_ptr + p0 + q) - e0);
     rw[q] = row;
-    sl[q] = HASC ? __ldg(p.row_slot + p0 + q) : -1;
     bs[q] = __ldg(p.b + row);
     ws[q] = __ldg(p.w + row);
+    vown[q] = p.vbuf0[row];
   }
   if (tid == 0) rp[R] = E;
   for (int k = tid; k < C; k += T) {
     const int m = __ldg(p.cont_list + c0 + k);
     cm[k] = m;
+    cq[k] = __ldg(p.cont_q + c0 + k);
 #pragma unroll
     for (int t = 0; t < 9; ++t) cfr[9 * k + t] = __ldg(p.frames + 9 * (size_t)m + t);
     cpar[4 * k + 0] = __ldg(p.mu + m);
@@ -185,11 +225,14 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     cpar[4 * k + 2] = __ldg(p.phi + m);
     cpar[4 * k + 3] = __ldg(p.gamma + m);
   }
-  for (int t = tid; t < 6 * C; t += T) {
-    jt_s[t] = 0.0;
-    lam_s[t] = 0.0;
-  }
+  for (int t = tid; t < 6 * C; t += T) lam_s[t] = 0.0;
+  for (int t = tid; t < CR; t += T) jt_s[t] = 0.0;
   __syncthreads();
+
+  // warps [0, WC) run the contact one-shots while warps [WC, nw) finish the free rows
+  const int nw = T >> 5, warp = tid >> 5;
+  int WC = (C + 31) >> 5;
+  if (C > 0) WC = (R > CR) ? (WC > nw - 1 ? nw - 1 : WC) : nw;
 
   double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
   const double u = p.under_relax;
@@ -225,26 +268,25 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     // ---- Barzilai-Borwein scalar step (solver.py:389-400) ----------------
     bool use_alpha = false;
     if (BB && l >= 2 && !check_only) {
-      products(sv, sc, prod, E, [&](int c) { return dsub(vcur[c], vprev[c]); });
+      products(sv, sc, sd, prod, E, [&](int c) { return dsub(vcur[c], vprev[c]); });
       __syncthreads();
       double sz = 0.0, ss = 0.0, zz = 0.0;
       for (int q = tid; q < R; q += T) {
-        double z = 0.0;
-        for (int k = rp[q]; k < rp[q + 1]; ++k) z = dadd(z, prod[k]);
+        const double z = row_sum(prod, rp[q], rp[q + 1]);
         const int row = rw[q];
-        const double s = dsub(vcur[row], vprev[row]);
+        const double s = dsub(vown[q], vprev[row]);
         sz = dadd(sz, dmul(s, z));
         ss = dadd(ss, dmul(s, s));
         zz = dadd(zz, dmul(z, z));
       }
-      grid_reduce3(sz, ss, zz, part, 4, p.bar_flags, G, ++epoch, sm_warp, sm_tot);
+      grid_reduce3(sz, ss, zz, part, 4, reinterpret_cast<unsigned*>(p.bar_flags), G, ++epoch, sm_warp, sm_tot);
       const double tsz = sm_tot[0], tss = sm_tot[1], tzz = sm_tot[2];
       const bool bb1 = (p.step == VFPI_STEP_BB1) || (p.step == VFPI_STEP_BB_ALTERNATING && (l % 2 == 0));
       if (tsz <= 0.0) alpha = alpha_prev;
       else alpha = bb1 ? ddiv(tss, tsz) : ddiv(tsz, tzz);
       alpha_prev = alpha;
       use_alpha = true;
-      __syncthreads();  // prod is reused below
+      __syncthreads();  // prod and sm_tot are reused below
     }
 
     if (CHEB && !check_only) {  // solver.py:284-290, :417
@@ -254,7 +296,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     }
 
     double th = 0.0, fr = 0.0, nf = 0.0;
-    auto finish_row = [&](int row, double vnew, double vc) {
+    // v_new -> (Chebyshev) -> v_next of own row q; theta / finiteness partials
+    auto finish_row = [&](int q, double vnew) {
+      const double vc = vown[q];
+      const int row = rw[q];
       double vn = vnew;
       if (CHEB) {
         const double vss = dadd(dmul(u, vnew), dmul(omu, vc));
@@ -269,86 +314,88 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       th = dadd(th, dmul(d, d));
       if (!isfinite(vn)) nf = dadd(nf, 1.0);
       vnext[row] = vn;
+      vown2[q] = vn;
+    };
+    // r = A v - b of own row q; force residual of the previous iterate (solver.py:437-439)
+    auto residual = [&](int q) {
+      const double r = dsub(row_sum(prod, rp[q], rp[q + 1]), bs[q]);
+      const double f = (q < CR) ? dsub(r, jt_s[q]) : dsub(r, 0.0);
+      fr = dadd(fr, dmul(f, f));
+      return r;
     };
 
     // ---- (1) surrogate-dynamics sweep: pass A gathers, pass B ordered sums --
     stamp(1);
-    products(sv, sc, prod, E, [&](int c) { return vcur[c]; });
+    products(sv, sc, sd, prod, E, [&](int c) { return vcur[c]; });
     __syncthreads();
     stamp(2);
-    for (int q = tid; q < R; q += T) {
-      double acc = 0.0;
-      const int k1 = rp[q + 1];
-      for (int k = rp[q]; k < k1; ++k) acc = dadd(acc, prod[k]);
-      const int row = rw[q];
-      const int slot = sl[q];
-      const double r = dsub(acc, bs[q]);
-      const double f = (slot >= 0) ? dsub(r, jt_s[slot]) : dsub(r, 0.0);  // solver.py:437-439
-      fr = dadd(fr, dmul(f, f));
-      if (!check_only) {
-        const double wr = use_alpha ? alpha : ws[q];
-        const double vc = vcur[row];
-        const double vstar = dsub(vc, dmul(wr, r));
-        if (slot >= 0) {
-          vs_s[slot] = vstar;
-        } else {
-          finish_row(row, HASC ? dadd(vstar, dmul(wr, 0.0)) : vstar, vc);
+    // contact rows first: their v* feeds the contact one-shots
+    for (int q = tid; q < CR; q += T) {
+      const double r = residual(q);
+      if (!check_only) vs_s[q] = dsub(vown[q], dmul(use_alpha ? alpha : ws[q], r));
+    }
+    __syncthreads();
+    stamp(3);
+
+    if (warp < WC) {
+      // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter ------
+      if (HASC && !check_only) {
+        for (int k = tid; k < C; k += WC * 32) {
+          const int qb = cq[k];
+          const int cj = __ldg(p.col_j + cm[k]);
+          double vi[3], vj[3] = {0.0, 0.0, 0.0}, rel[3];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) vi[t] = vs_s[qb + t];
+          if (cj >= 0) {
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              vj[t] = vs_s[qb + 3 + t];
+              rel[t] = dsub(vi[t], vj[t]);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < 3; ++t) rel[t] = vi[t];
+          }
+          double Rr[9];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) Rr[t] = cfr[9 * k + t];
+          double eta[3], lam[3], world[3];
+          frame_apply(Rr, rel, eta);
+          double g;
+          if (use_alpha) g = (cj >= 0) ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
+          else g = cpar[4 * k + 3];
+          trial_impulse(eta, cpar[4 * k + 2], g, lam);
+          project(OP, lam, cpar[4 * k + 0], cpar[4 * k + 1]);
+#pragma unroll
+          for (int t = 0; t < 3; ++t) lam_out[3 * k + t] = lam[t];
+          frame_apply_t(Rr, lam, world);
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const double oi = dadd(0.0, world[t]);  // np.add.at onto zeros
+            jt_s[qb + t] = oi;
+            finish_row(qb + t, dadd(vi[t], dmul(use_alpha ? alpha : ws[qb + t], oi)));
+          }
+          if (cj >= 0) {
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              const double oj = dsub(0.0, world[t]);  // np.subtract.at onto zeros
+              jt_s[qb + 3 + t] = oj;
+              finish_row(qb + 3 + t, dadd(vj[t], dmul(use_alpha ? alpha : ws[qb + 3 + t], oj)));
+            }
+          }
         }
       }
     }
-
-    // ---- (2)(3)(2') contacts out of shared memory ------------------------
-    stamp(3);
-    if (HASC && !check_only) {
-      __syncthreads();
-      for (int k = tid; k < C; k += T) {
-        const int m = cm[k];
-        const int loc = k * kSlotsPerContact;
-        const int ci = __ldg(p.col_i + m), cj = __ldg(p.col_j + m);
-        const double* R9 = cfr + 9 * k;
-        double vi[3], vj[3] = {0.0, 0.0, 0.0}, rel[3];
-#pragma unroll
-        for (int t = 0; t < 3; ++t) vi[t] = vs_s[loc + t];
-        if (cj >= 0) {
-#pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            vj[t] = vs_s[loc + 3 + t];
-            rel[t] = dsub(vi[t], vj[t]);
-          }
-        } else {
-#pragma unroll
-          for (int t = 0; t < 3; ++t) rel[t] = vi[t];
-        }
-        double Rr[9];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) Rr[t] = R9[t];
-        double eta[3], lam[3], world[3];
-        frame_apply(Rr, rel, eta);
-        double g;
-        if (use_alpha) g = (cj >= 0) ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
-        else g = cpar[4 * k + 3];
-        trial_impulse(eta, cpar[4 * k + 2], g, lam);
-        project(OP, lam, cpar[4 * k + 0], cpar[4 * k + 1]);
-#pragma unroll
-        for (int t = 0; t < 3; ++t) lam_out[3 * k + t] = lam[t];
-        frame_apply_t(Rr, lam, world);
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const int row = ci + t;
-          const double oi = dadd(0.0, world[t]);
-          jt_s[loc + t] = oi;
-          const double wr = use_alpha ? alpha : __ldg(p.w + row);
-          finish_row(row, dadd(vi[t], dmul(wr, oi)), vcur[row]);
-        }
-        if (cj >= 0) {
-#pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            const int row = cj + t;
-            const double oj = dsub(0.0, world[t]);
-            jt_s[loc + 3 + t] = oj;
-            const double wr = use_alpha ? alpha : __ldg(p.w + row);
-            finish_row(row, dadd(vj[t], dmul(wr, oj)), vcur[row]);
-          }
+    if (warp >= WC || WC == nw) {
+      // ---- free rows: v_new = v* (+ w * 0 when contacts exist) ------------
+      const int t0 = (WC == nw) ? tid : tid - WC * 32;
+      const int TT = (WC == nw) ? T : T - WC * 32;
+      for (int q = CR + t0; q < R; q += TT) {
+        const double r = residual(q);
+        if (!check_only) {
+          const double wr = use_alpha ? alpha : ws[q];
+          const double vstar = dsub(vown[q], dmul(wr, r));
+          finish_row(q, HASC ? dadd(vstar, dmul(wr, 0.0)) : vstar);
         }
       }
     }
@@ -356,7 +403,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     // ---- (4) residual reduction + grid-wide decision --------------------
     stamp(4);
     stamp(7);
-    grid_reduce3(th, fr, nf, part, 0, p.bar_flags, G, ++epoch, sm_warp, sm_tot);
+    grid_reduce3(th, fr, nf, part, 0, reinterpret_cast<unsigned*>(p.bar_flags), G, ++epoch, sm_warp, sm_tot);
     stamp(5);
     const double theta = dsqrt(sm_tot[0]);
     const double fres = dsqrt(sm_tot[1]);
@@ -384,6 +431,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     pending = theta < p.tol;
     if (CHEB) rho = (theta_prev <= 0.0) ? rho : py_min(ddiv(theta, theta_prev), 1.0);
     theta_prev = theta;
+    double* tmp = vown;  // own rows of v^(l) become the current iterate
+    vown = vown2;
+    vown2 = tmp;
   }
 
   const double* vfin = vb[final_buf];

@@ -18,11 +18,12 @@ namespace vfpi {
 namespace {
 
 // Partition cost model, in bytes of per-CTA state (the resident kernel's
-// shared-memory footprint, which also tracks per-iteration work): 20 B per
-// numeric entry (value, column, product), 28 B per row, 252 B per contact.
-constexpr int kEntryCost = 20;
-constexpr int kRowCost = 28;
-constexpr int kContactCost = 252;
+// shared-memory footprint, which also tracks per-iteration work): 24 B per
+// numeric entry (value, column, destination, product), 40 B per row, 256 B
+// per contact.
+constexpr int kEntryCost = 24;
+constexpr int kRowCost = 40;
+constexpr int kContactCost = 256;
 
 #define VFPI_CK(x)                                                     \
   do {                                                                 \
@@ -98,7 +99,7 @@ __global__ void k_mark(int n, int n_c, const int* __restrict__ ci, const int* __
 
 // unit = one free row, or all (3 or 6) rows of one contact, anchored at col_i
 __global__ void k_units(int n, const int* __restrict__ mark, const int* __restrict__ ci, const int* __restrict__ cj,
-                        const int* __restrict__ rowcnt, int64_t* ucost, int* urows, int* ucont) {
+                        const int* __restrict__ rowcnt, int64_t* ucost, int* urows, int* ucont, int* ucr, int* ufr) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int m = mark[r];
@@ -119,11 +120,14 @@ __global__ void k_units(int n, const int* __restrict__ mark, const int* __restri
   ucost[r] = cost;
   urows[r] = rows;
   ucont[r] = ct;
+  ucr[r] = ct ? rows : 0;          // rows of a contact unit
+  ufr[r] = (rows == 1 && !ct) ? 1 : 0;  // a free row
+  if (r == n - 1) { ucr[n] = 0; ufr[n] = 0; }
 }
 
 __global__ void k_blocks(int n, int G, const int64_t* __restrict__ ucost, const int64_t* __restrict__ cpos,
                          const int* __restrict__ urows, const int* __restrict__ rpos, const int* __restrict__ kpos,
-                         int* blk_row, int* blk_ct) {
+                         int* blk_row, int* blk_ct, int* blk_first) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n || urows[r] == 0) return;
   const int64_t total = cpos[n - 1] + ucost[n - 1];
@@ -131,18 +135,25 @@ __global__ void k_blocks(int n, int G, const int64_t* __restrict__ ucost, const 
   if (b > G - 1) b = G - 1;
   atomicMin(&blk_row[b], rpos[r]);
   atomicMin(&blk_ct[b], kpos[r]);
+  atomicMin(&blk_first[b], r);
 }
 
-__global__ void k_blocks_fix(int n, int n_c, int G, int* blk_row, int* blk_ct, int* blk_slice, SetupSummary* sum) {
+__global__ void k_blocks_fix(int n, int n_c, int G, int* blk_row, int* blk_ct, int* blk_slice, int* blk_first,
+                             int* blk_cr, const int* __restrict__ cposc, SetupSummary* sum) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   blk_row[G] = n;
   blk_ct[G] = n_c;
+  blk_first[G] = n;
   for (int b = G - 1; b >= 0; --b) {
     if (blk_row[b] == INT_MAX) blk_row[b] = blk_row[b + 1];
     if (blk_ct[b] == INT_MAX) blk_ct[b] = blk_ct[b + 1];
+    if (blk_first[b] == INT_MAX) blk_first[b] = blk_first[b + 1];
   }
   blk_row[0] = 0;
   blk_ct[0] = 0;
+  blk_first[0] = 0;
+  for (int b = 0; b < G; ++b) blk_cr[b] = cposc[blk_first[b + 1]] - cposc[blk_first[b]];
+  blk_cr[G] = 0;
   int s = 0, mx = 0;
   for (int b = 0; b < G; ++b) {
     blk_slice[b] = s;
@@ -165,23 +176,31 @@ __device__ __forceinline__ int owner(const int* __restrict__ starts, int G, int 
   return lo;
 }
 
+// Row list: within every CTA range, the rows of its contact units come first
+// (unit order), then its free rows (natural order). cont_q = local position
+// of each contact's first row.
 __global__ void k_fill(int n, int G, const int* __restrict__ mark, const int* __restrict__ ci,
                        const int* __restrict__ cj, const int* __restrict__ urows, const int* __restrict__ rpos,
-                       const int* __restrict__ kpos, const int* __restrict__ blk_row, const int* __restrict__ blk_ct,
-                       int* row_list, int* row_slot, int* cont_list) {
+                       const int* __restrict__ kpos, const int* __restrict__ cposc, const int* __restrict__ cposf,
+                       const int* __restrict__ blk_row, const int* __restrict__ blk_ct,
+                       const int* __restrict__ blk_first, const int* __restrict__ blk_cr, int* row_list, int* row_slot,
+                       int* cont_list, int* cont_q) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n || urows[r] == 0) return;
-  const int p = rpos[r];
+  const int b = owner(blk_row, G, rpos[r]);
+  const int f = blk_first[b];
   const int m = mark[r];
   if (m < 0) {
+    const int p = blk_row[b] + blk_cr[b] + (cposf[r] - cposf[f]);
     row_list[p] = r;
     row_slot[p] = -1;
     return;
   }
-  const int b = owner(blk_row, G, p);
+  const int p = blk_row[b] + (cposc[r] - cposc[f]);
   const int k = kpos[r];
   const int loc = (k - blk_ct[b]) * kSlotsPerContact;
   cont_list[k] = m;
+  cont_q[k] = p - blk_row[b];
   const int i = ci[m], j = cj[m];
   for (int t = 0; t < 3; ++t) {
     row_list[p + t] = i + t;
@@ -216,8 +235,8 @@ __global__ void k_poslen(int n, const int* __restrict__ row_list, const int* __r
 }
 
 __global__ void k_summary(int n, int G, const int64_t* row_ptr, const int64_t* slice_off,
-                          const int64_t* pos_ptr, const int* blk_row, const int* blk_ct, const int* flags,
-                          SetupSummary* sum) {
+                          const int64_t* pos_ptr, const int* blk_row, const int* blk_ct, const int* blk_cr,
+                          const int* flags, SetupSummary* sum) {
   sum->nnz_num = row_ptr[n];
   sum->sell_elems = slice_off[sum->n_slices];
   sum->flags = *flags;
@@ -226,7 +245,7 @@ __global__ void k_summary(int n, int G, const int64_t* row_ptr, const int64_t* s
   for (int b = 0; b < G; ++b) {
     const int64_t e = pos_ptr[blk_row[b + 1]] - pos_ptr[blk_row[b]];
     const int r = blk_row[b + 1] - blk_row[b];
-    const int64_t by = (int64_t)ResLayout(e, r, blk_ct[b + 1] - blk_ct[b]).total;
+    const int64_t by = (int64_t)ResLayout(e, r, blk_ct[b + 1] - blk_ct[b], blk_cr[b]).total;
     me = e > me ? e : me;
     mr = r > mr ? r : mr;
     mb = by > mb ? by : mb;
@@ -234,6 +253,19 @@ __global__ void k_summary(int n, int G, const int64_t* row_ptr, const int64_t* s
   sum->max_ent_per_blk = me;
   sum->max_rows_per_blk = mr;
   sum->max_res_bytes = mb;
+}
+
+__global__ void k_rowpos(int n, const int* __restrict__ row_list, int* __restrict__ rowpos) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) rowpos[row_list[q]] = q;
+}
+
+__global__ void k_segments(int G, const int64_t* __restrict__ pos_ptr, const int* __restrict__ blk_row, int* beg,
+                           int* end) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= G) return;
+  beg[b] = (int)pos_ptr[blk_row[b]];
+  end[b] = (int)pos_ptr[blk_row[b + 1]];
 }
 
 // CTA-contiguous CSR: the entries of row-list position p at pos_ptr[p]..
@@ -427,6 +459,13 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   VFPI_CK(ensure(ws.rpos, 4 * (size_t)n));
   VFPI_CK(ensure(ws.ucont, 4 * (size_t)n));
   VFPI_CK(ensure(ws.kpos, 4 * (size_t)n));
+  VFPI_CK(ensure(ws.ucr, 4 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.ufr, 4 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.cposc, 4 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.cposf, 4 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.blk_first, 4 * (size_t)(G + 1)));
+  VFPI_CK(ensure(ws.blk_cr, 4 * (size_t)(G + 1)));
+  VFPI_CK(ensure(ws.cont_q, 4 * (size_t)std::max(n_c, 1)));
   VFPI_CK(ensure(ws.blk_row, 4 * (size_t)(G + 1)));
   VFPI_CK(ensure(ws.blk_ct, 4 * (size_t)(G + 1)));
   VFPI_CK(ensure(ws.blk_slice, 4 * (size_t)(G + 1)));
@@ -444,7 +483,7 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t1, P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr), n + 1, st);
   cub::DeviceScan::ExclusiveSum(nullptr, t2, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), n, st);
-  cub::DeviceScan::ExclusiveSum(nullptr, t3, P<int>(ws.urows), P<int>(ws.rpos), n, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t3, P<int>(ws.urows), P<int>(ws.rpos), n + 1, st);
   cub::DeviceScan::ExclusiveSum(nullptr, t4, P<int64_t>(ws.slice_w), P<int64_t>(ws.slice_off), S_max + 1, st);
   size_t t5 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t5, P<int64_t>(ws.pos_len), P<int64_t>(ws.pos_ptr), n + 1, st);
@@ -457,7 +496,8 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   VFPI_CK(cudaMemsetAsync(ws.summary.p, 0, sizeof(SetupSummary), st));
   k_fill_int<<<nblk(G + 1), 256, 0, st>>>(P<int>(ws.blk_row), INT_MAX, G + 1);
   k_fill_int<<<nblk(G + 1), 256, 0, st>>>(P<int>(ws.blk_ct), INT_MAX, G + 1);
-  launches += 2;
+  k_fill_int<<<nblk(G + 1), 256, 0, st>>>(P<int>(ws.blk_first), INT_MAX, G + 1);
+  launches += 3;
   if (n > 0) {
     k_colstats<<<nblk(n), 256, 0, st>>>(n, s.indptr, s.indices, s.data, P<double>(ws.diag), P<double>(ws.rns),
                                         P<int>(ws.rowcnt), P<int>(ws.keys), P<int>(ws.colof));
@@ -472,21 +512,28 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   ++launches;
   if (n > 0) {
     k_units<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.rowcnt), P<int64_t>(ws.ucost),
-                                     P<int>(ws.urows), P<int>(ws.ucont));
+                                     P<int>(ws.urows), P<int>(ws.ucont), P<int>(ws.ucr), P<int>(ws.ufr));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), n, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.urows), P<int>(ws.rpos), n, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ucont), P<int>(ws.kpos), n, st));
+    VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ucr), P<int>(ws.cposc), n + 1, st));
+    VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ufr), P<int>(ws.cposf), n + 1, st));
     k_blocks<<<nblk(n), 256, 0, st>>>(n, G, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), P<int>(ws.urows),
-                                      P<int>(ws.rpos), P<int>(ws.kpos), P<int>(ws.blk_row), P<int>(ws.blk_ct));
-    launches += 5;
+                                      P<int>(ws.rpos), P<int>(ws.kpos), P<int>(ws.blk_row), P<int>(ws.blk_ct),
+                                      P<int>(ws.blk_first));
+    launches += 7;
+  } else {
+    VFPI_CK(cudaMemsetAsync(ws.cposc.p, 0, 4, st));
   }
   k_blocks_fix<<<1, 1, 0, st>>>(n, n_c, G, P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_slice),
+                                P<int>(ws.blk_first), P<int>(ws.blk_cr), P<int>(ws.cposc),
                                 P<SetupSummary>(ws.summary));
   ++launches;
   if (n > 0) {
     k_fill<<<nblk(n), 256, 0, st>>>(n, G, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.urows), P<int>(ws.rpos),
-                                    P<int>(ws.kpos), P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.row_list),
-                                    P<int>(ws.row_slot), P<int>(ws.cont_list));
+                                    P<int>(ws.kpos), P<int>(ws.cposc), P<int>(ws.cposf), P<int>(ws.blk_row),
+                                    P<int>(ws.blk_ct), P<int>(ws.blk_first), P<int>(ws.blk_cr), P<int>(ws.row_list),
+                                    P<int>(ws.row_slot), P<int>(ws.cont_list), P<int>(ws.cont_q));
     ++launches;
   }
   VFPI_CK(cudaGetLastError());
@@ -501,7 +548,8 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.pos_len), P<int64_t>(ws.pos_ptr), n + 1,
                                         st));
   k_summary<<<1, 1, 0, st>>>(n, G, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int64_t>(ws.pos_ptr),
-                             P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.flags), P<SetupSummary>(ws.summary));
+                             P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr), P<int>(ws.flags),
+                             P<SetupSummary>(ws.summary));
   launches += 3;
   launches += 3;
   VFPI_CK(cudaGetLastError());
@@ -541,13 +589,39 @@ int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const 
   }
   (void)G;
   if (resident) {
-    VFPI_CK(ensure(ws.pk_val, 8 * (size_t)hs.nnz_num));
-    VFPI_CK(ensure(ws.pk_col, 4 * (size_t)hs.nnz_num));
+    const int64_t nn = hs.nnz_num;
+    VFPI_CK(ensure(ws.pk_val, 8 * (size_t)nn));
+    VFPI_CK(ensure(ws.pk_col, 4 * (size_t)nn));
+    VFPI_CK(ensure(ws.ps_col, 4 * (size_t)nn));
+    VFPI_CK(ensure(ws.ps_src, 4 * (size_t)nn));
+    VFPI_CK(ensure(ws.seg_beg, 4 * (size_t)G));
+    VFPI_CK(ensure(ws.seg_end, 4 * (size_t)G));
     if (n > 0) {
       k_pack_csr<<<nblk(n, 128), 128, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr),
-                                          P<int64_t>(ws.pos_ptr), P<int>(ws.perm), P<int>(ws.colof), s.data,
-                                          P<double>(ws.pk_val), P<int>(ws.pk_col));
+                                               P<int64_t>(ws.pos_ptr), P<int>(ws.perm), P<int>(ws.colof), s.data,
+                                               P<double>(ws.pk_val), P<int>(ws.pk_col));
       ++launches;
+    }
+    VFPI_CK(ensure(ws.rowpos, 4 * (size_t)std::max(n, 1)));
+    if (n > 0) {
+      k_rowpos<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowpos));
+      ++launches;
+    }
+    if (nn > 0) {
+      // per CTA, entries re-ordered by column so the gathers of a warp hit few
+      // cache lines; ps_src remembers each entry's row-ordered slot
+      k_segments<<<nblk(G), 256, 0, st>>>(G, P<int64_t>(ws.pos_ptr), P<int>(ws.blk_row), P<int>(ws.seg_beg),
+                                          P<int>(ws.seg_end));
+      k_iota<<<nblk(nn), 256, 0, st>>>(nn, P<int>(ws.vals));
+      size_t ts = 0;
+      cub::DeviceSegmentedSort::SortPairs(nullptr, ts, P<int>(ws.pk_col), P<int>(ws.ps_col), P<int>(ws.vals),
+                                          P<int>(ws.ps_src), (int)nn, G, P<int>(ws.seg_beg), P<int>(ws.seg_end), st);
+      VFPI_CK(ensure(ws.cub_tmp, ts));
+      size_t tb = ws.cub_tmp.cap;
+      VFPI_CK(cub::DeviceSegmentedSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.pk_col), P<int>(ws.ps_col),
+                                                  P<int>(ws.vals), P<int>(ws.ps_src), (int)nn, G, P<int>(ws.seg_beg),
+                                                  P<int>(ws.seg_end), st));
+      launches += 4;
     }
   } else {
     VFPI_CK(ensure(ws.sell_val, 8 * (size_t)hs.sell_elems));
