@@ -86,6 +86,7 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 // partials (<= 8 independent loads per lane) and reduces them in a fixed order
 // that is identical in every CTA, so every CTA gets bit-identical totals.
 constexpr int kMaxPartialsPerLane = 8;  // G <= 256
+constexpr int kLPC = 4;                 // lanes per contact in the one-shot phase
 
 __device__ __forceinline__ void grid_reduce3(double a, double b, double c, double* part, int off, unsigned* counter,
                                              int G, int epoch, double* sm_warp, double* sm_tot) {
@@ -172,7 +173,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double sm_warp[3 * (kResThreads / 32)];
   __shared__ double sm_tot[4];
+  __shared__ unsigned long long sm_role_end[2];
   const int b = blockIdx.x, G = p.G, T = blockDim.x, tid = threadIdx.x;
+  if (tid < 2) sm_role_end[tid] = 0;
   const int p0 = p.blk_row[b], p1 = p.blk_row[b + 1], R = p1 - p0;
   const int64_t e0 = p.pos_ptr[p0];
   const int E = (int)(p.pos_ptr[p1] - e0);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   for (int k = tid; k < C; k += T) {
     const int m = __ldg(p.cont_list + c0 + k);
     cm[k] = m;
-    cq[k] = __ldg(p.cont_q + c0 + k);
+    cq[k] = __ldg(p.cont_q + c0 + k) | (__ldg(p.col_j + m) >= 0 ? (1 << 30) : 0);
 #pragma unroll
     for (int t = 0; t < 9; ++t) cfr[9 * k + t] = __ldg(p.frames + 9 * (size_t)m + t);
     cpar[4 * k + 0] = __ldg(p.mu + m);
@@ -231,8 +234,25 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
 
   // warps [0, WC) run the contact one-shots while warps [WC, nw) finish the free rows
   const int nw = T >> 5, warp = tid >> 5;
-  int WC = (C + 31) >> 5;
-  if (C > 0) WC = (R > CR) ? (WC > nw - 1 ? nw - 1 : WC) : nw;
+  // split the warps between the contact quads (kLPC lanes per contact) and the
+  // free rows so both finish together: cost ~ rounds x per-round latency
+  int WC = 0;
+  if (C > 0) {
+    const int FR = R - CR;
+    if (FR == 0) {
+      WC = nw;
+    } else {
+      const int efree = E - rp[CR];
+      const long long kf = 8LL * (efree / FR + 1) + 200;  // cycles per free-row round
+      long long best = LLONG_MAX;
+      for (int w = 1; w < nw; ++w) {
+        const long long tc = (long long)((C + (32 / kLPC) * w - 1) / ((32 / kLPC) * w)) * 1000;
+        const long long tf = (long long)((FR + 32 * (nw - w) - 1) / (32 * (nw - w))) * kf;
+        const long long c2 = tc > tf ? tc : tf;
+        if (c2 < best) { best = c2; WC = w; }
+      }
+    }
+  }
 
   double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
   const double u = p.under_relax;
@@ -325,7 +345,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     };
 
     // ---- (1) surrogate-dynamics sweep: pass A gathers, pass B ordered sums --
-    stamp(1);
     products(sv, sc, sd, prod, E, [&](int c) { return vcur[c]; });
     __syncthreads();
     stamp(2);
@@ -339,53 +358,60 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
 
     if (warp < WC) {
       // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter ------
+      // kLPC lanes per contact: lane a < 3 owns frame row / component a; the
+      // projection needs all three components and is evaluated redundantly.
       if (HASC && !check_only) {
-        for (int k = tid; k < C; k += WC * 32) {
-          const int qb = cq[k];
-          const int cj = __ldg(p.col_j + cm[k]);
-          double vi[3], vj[3] = {0.0, 0.0, 0.0}, rel[3];
-#pragma unroll
-          for (int t = 0; t < 3; ++t) vi[t] = vs_s[qb + t];
-          if (cj >= 0) {
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-              vj[t] = vs_s[qb + 3 + t];
-              rel[t] = dsub(vi[t], vj[t]);
-            }
-          } else {
-#pragma unroll
-            for (int t = 0; t < 3; ++t) rel[t] = vi[t];
-          }
-          double Rr[9];
-#pragma unroll
-          for (int t = 0; t < 9; ++t) Rr[t] = cfr[9 * k + t];
-          double eta[3], lam[3], world[3];
-          frame_apply(Rr, rel, eta);
-          double g;
-          if (use_alpha) g = (cj >= 0) ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
-          else g = cpar[4 * k + 3];
-          trial_impulse(eta, cpar[4 * k + 2], g, lam);
-          project(OP, lam, cpar[4 * k + 0], cpar[4 * k + 1]);
-#pragma unroll
-          for (int t = 0; t < 3; ++t) lam_out[3 * k + t] = lam[t];
-          frame_apply_t(Rr, lam, world);
+        const int lane = tid & 31;
+        const int a = (lane & (kLPC - 1)) < 3 ? (lane & (kLPC - 1)) : 2;
+        const bool owner = (lane & (kLPC - 1)) < 3;
+        const int qbase = lane & ~(kLPC - 1);  // first lane of this contact's group
+        for (int k0 = warp * (32 / kLPC); k0 < C; k0 += WC * (32 / kLPC)) {
+          const int k = k0 + lane / kLPC;
+          const bool act = k < C;
+          const int kk = act ? k : k0;
+          const int code = cq[kk];
+          const int qb = code & 0x3fffffff;
+          const bool dj = (code >> 30) & 1;
+          const double* R9 = cfr + 9 * kk;
+          double rel[3], vi_a, vj_a = 0.0;
 #pragma unroll
           for (int t = 0; t < 3; ++t) {
-            const double oi = dadd(0.0, world[t]);  // np.add.at onto zeros
-            jt_s[qb + t] = oi;
-            finish_row(qb + t, dadd(vi[t], dmul(use_alpha ? alpha : ws[qb + t], oi)));
+            const double xi = vs_s[qb + t];
+            rel[t] = dj ? dsub(xi, vs_s[qb + 3 + t]) : xi;
           }
-          if (cj >= 0) {
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-              const double oj = dsub(0.0, world[t]);  // np.subtract.at onto zeros
-              jt_s[qb + 3 + t] = oj;
-              finish_row(qb + 3 + t, dadd(vj[t], dmul(use_alpha ? alpha : ws[qb + 3 + t], oj)));
+          vi_a = vs_s[qb + a];
+          if (dj) vj_a = vs_s[qb + 3 + a];
+          // eta_a = R[a,:] rel  ((p0+p2)+p1, einsum order) ; lam*_a
+          const double eta_a = dadd(dadd(dmul(R9[3 * a + 0], rel[0]), dmul(R9[3 * a + 2], rel[2])),
+                                    dmul(R9[3 * a + 1], rel[1]));
+          double g;
+          if (use_alpha) g = dj ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
+          else g = cpar[4 * kk + 3];
+          const double ls_a = ddiv(-dadd(eta_a, a == 0 ? cpar[4 * kk + 2] : 0.0), g);
+          double lam[3];
+          lam[0] = __shfl_sync(0xffffffffu, ls_a, qbase + 0);
+          lam[1] = __shfl_sync(0xffffffffu, ls_a, qbase + 1);
+          lam[2] = __shfl_sync(0xffffffffu, ls_a, qbase + 2);
+          if (act) {
+            project(OP, lam, cpar[4 * kk + 0], cpar[4 * kk + 1]);
+            if (owner) {
+              lam_out[3 * k + a] = lam[a];
+              // world_a = R[:,a] . lam  ((p0+p1)+p2)
+              const double wa = dadd(dadd(dmul(R9[a], lam[0]), dmul(R9[3 + a], lam[1])), dmul(R9[6 + a], lam[2]));
+              const double oi = dadd(0.0, wa);  // np.add.at onto zeros
+              jt_s[qb + a] = oi;
+              finish_row(qb + a, dadd(vi_a, dmul(use_alpha ? alpha : ws[qb + a], oi)));
+              if (dj) {
+                const double oj = dsub(0.0, wa);  // np.subtract.at onto zeros
+                jt_s[qb + 3 + a] = oj;
+                finish_row(qb + 3 + a, dadd(vj_a, dmul(use_alpha ? alpha : ws[qb + 3 + a], oj)));
+              }
             }
           }
         }
       }
     }
+    if (profl && (tid & 31) == 0 && warp < WC) atomicMax(&sm_role_end[0], (unsigned long long)clock64());
     if (warp >= WC || WC == nw) {
       // ---- free rows: v_new = v* (+ w * 0 when contacts exist) ------------
       const int t0 = (WC == nw) ? tid : tid - WC * 32;
@@ -400,8 +426,15 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       }
     }
 
+    if (profl && (tid & 31) == 0 && (warp >= WC || WC == nw)) atomicMax(&sm_role_end[1], (unsigned long long)clock64());
     // ---- (4) residual reduction + grid-wide decision --------------------
     stamp(4);
+    if (profl && tid == 0) {
+      p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 8 + 6] = (long long)sm_role_end[0];
+      p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 8 + 1] = (long long)sm_role_end[1];
+      sm_role_end[0] = 0;
+      sm_role_end[1] = 0;
+    }
     stamp(7);
     grid_reduce3(th, fr, nf, part, 0, reinterpret_cast<unsigned*>(p.bar_flags), G, ++epoch, sm_warp, sm_tot);
     stamp(5);

@@ -138,32 +138,68 @@ __global__ void k_blocks(int n, int G, const int64_t* __restrict__ ucost, const 
   atomicMin(&blk_first[b], r);
 }
 
-__global__ void k_blocks_fix(int n, int n_c, int G, int* blk_row, int* blk_ct, int* blk_slice, int* blk_first,
-                             int* blk_cr, const int* __restrict__ cposc, SetupSummary* sum) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  blk_row[G] = n;
-  blk_ct[G] = n_c;
-  blk_first[G] = n;
-  for (int b = G - 1; b >= 0; --b) {
-    if (blk_row[b] == INT_MAX) blk_row[b] = blk_row[b + 1];
-    if (blk_ct[b] == INT_MAX) blk_ct[b] = blk_ct[b + 1];
-    if (blk_first[b] == INT_MAX) blk_first[b] = blk_first[b + 1];
+// one CTA of kFixThreads threads, G <= kFixThreads: fill empty CTA ranges with
+// the next non-empty start (suffix minimum), slice prefix, contact-row counts
+constexpr int kFixThreads = 1024;
+
+__global__ void __launch_bounds__(kFixThreads) k_blocks_fix(int n, int n_c, int G, int* blk_row, int* blk_ct,
+                                                             int* blk_slice, int* blk_first, int* blk_cr,
+                                                             const int* __restrict__ cposc, SetupSummary* sum) {
+  __shared__ int s_row[kFixThreads + 1], s_ct[kFixThreads + 1], s_first[kFixThreads + 1], s_x[kFixThreads];
+  const int b = threadIdx.x;
+  s_row[b] = (b < G) ? blk_row[b] : n;
+  s_ct[b] = (b < G) ? blk_ct[b] : n_c;
+  s_first[b] = (b < G) ? blk_first[b] : n;
+  if (b == 0) { s_row[kFixThreads] = n; s_ct[kFixThreads] = n_c; s_first[kFixThreads] = n; }
+  __syncthreads();
+  // suffix minimum (Hillis-Steele, log2 steps); INT_MAX marks empty ranges
+  for (int o = 1; o < kFixThreads; o <<= 1) {
+    const int r = (b + o <= kFixThreads) ? s_row[b + o] : n;
+    const int c = (b + o <= kFixThreads) ? s_ct[b + o] : n_c;
+    const int f = (b + o <= kFixThreads) ? s_first[b + o] : n;
+    __syncthreads();
+    s_row[b] = min(s_row[b], r);
+    s_ct[b] = min(s_ct[b], c);
+    s_first[b] = min(s_first[b], f);
+    __syncthreads();
   }
-  blk_row[0] = 0;
-  blk_ct[0] = 0;
-  blk_first[0] = 0;
-  for (int b = 0; b < G; ++b) blk_cr[b] = cposc[blk_first[b + 1]] - cposc[blk_first[b]];
-  blk_cr[G] = 0;
-  int s = 0, mx = 0;
-  for (int b = 0; b < G; ++b) {
-    blk_slice[b] = s;
-    s += (blk_row[b + 1] - blk_row[b] + 31) / 32;
-    const int c = blk_ct[b + 1] - blk_ct[b];
-    mx = c > mx ? c : mx;
+  if (b == 0) { s_row[0] = 0; s_ct[0] = 0; s_first[0] = 0; }
+  __syncthreads();
+  const int nsl = (b < G) ? (s_row[b + 1] - s_row[b] + 31) / 32 : 0;
+  const int nct = (b < G) ? (s_ct[b + 1] - s_ct[b]) : 0;
+  // inclusive prefix of slice counts
+  s_x[b] = nsl;
+  __syncthreads();
+  for (int o = 1; o < kFixThreads; o <<= 1) {
+    const int t = (b >= o) ? s_x[b - o] : 0;
+    __syncthreads();
+    s_x[b] += t;
+    __syncthreads();
   }
-  blk_slice[G] = s;
-  sum->n_slices = s;
-  sum->max_ct_per_blk = mx;
+  if (b < G) {
+    blk_row[b] = s_row[b];
+    blk_ct[b] = s_ct[b];
+    blk_first[b] = s_first[b];
+    blk_slice[b] = s_x[b] - nsl;
+    blk_cr[b] = cposc[s_first[b + 1]] - cposc[s_first[b]];
+  }
+  if (b == 0) {
+    blk_row[G] = n;
+    blk_ct[G] = n_c;
+    blk_first[G] = n;
+    blk_slice[G] = s_x[kFixThreads - 1];
+    blk_cr[G] = 0;
+    sum->n_slices = s_x[kFixThreads - 1];
+  }
+  // max contacts per CTA
+  __syncthreads();
+  s_x[b] = nct;
+  __syncthreads();
+  for (int o = kFixThreads / 2; o > 0; o >>= 1) {
+    if (b < o) s_x[b] = max(s_x[b], s_x[b + o]);
+    __syncthreads();
+  }
+  if (b == 0) sum->max_ct_per_blk = s_x[0];
 }
 
 __device__ __forceinline__ int owner(const int* __restrict__ starts, int G, int p) {
@@ -234,25 +270,40 @@ __global__ void k_poslen(int n, const int* __restrict__ row_list, const int* __r
   len[p] = (p < n) ? rowcnt[row_list[p]] : 0;
 }
 
-__global__ void k_summary(int n, int G, const int64_t* row_ptr, const int64_t* slice_off,
-                          const int64_t* pos_ptr, const int* blk_row, const int* blk_ct, const int* blk_cr,
-                          const int* flags, SetupSummary* sum) {
-  sum->nnz_num = row_ptr[n];
-  sum->sell_elems = slice_off[sum->n_slices];
-  sum->flags = *flags;
-  int64_t me = 0, mb = 0;
-  int mr = 0;
-  for (int b = 0; b < G; ++b) {
-    const int64_t e = pos_ptr[blk_row[b + 1]] - pos_ptr[blk_row[b]];
-    const int r = blk_row[b + 1] - blk_row[b];
-    const int64_t by = (int64_t)ResLayout(e, r, blk_ct[b + 1] - blk_ct[b], blk_cr[b]).total;
-    me = e > me ? e : me;
-    mr = r > mr ? r : mr;
-    mb = by > mb ? by : mb;
+__global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int64_t* row_ptr,
+                                                          const int64_t* slice_off, const int64_t* pos_ptr,
+                                                          const int* blk_row, const int* blk_ct, const int* blk_cr,
+                                                          const int* flags, SetupSummary* sum) {
+  __shared__ long long s_e[kFixThreads], s_b[kFixThreads];
+  __shared__ int s_r[kFixThreads];
+  const int b = threadIdx.x;
+  long long e = 0, by = 0;
+  int r = 0;
+  if (b < G) {
+    e = pos_ptr[blk_row[b + 1]] - pos_ptr[blk_row[b]];
+    r = blk_row[b + 1] - blk_row[b];
+    by = (long long)ResLayout(e, r, blk_ct[b + 1] - blk_ct[b], blk_cr[b]).total;
   }
-  sum->max_ent_per_blk = me;
-  sum->max_rows_per_blk = mr;
-  sum->max_res_bytes = mb;
+  s_e[b] = e;
+  s_b[b] = by;
+  s_r[b] = r;
+  __syncthreads();
+  for (int o = kFixThreads / 2; o > 0; o >>= 1) {
+    if (b < o) {
+      s_e[b] = max(s_e[b], s_e[b + o]);
+      s_b[b] = max(s_b[b], s_b[b + o]);
+      s_r[b] = max(s_r[b], s_r[b + o]);
+    }
+    __syncthreads();
+  }
+  if (b == 0) {
+    sum->nnz_num = row_ptr[n];
+    sum->sell_elems = slice_off[sum->n_slices];
+    sum->flags = *flags;
+    sum->max_ent_per_blk = s_e[0];
+    sum->max_rows_per_blk = s_r[0];
+    sum->max_res_bytes = s_b[0];
+  }
 }
 
 __global__ void k_rowpos(int n, const int* __restrict__ row_list, int* __restrict__ rowpos) {
@@ -525,7 +576,7 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   } else {
     VFPI_CK(cudaMemsetAsync(ws.cposc.p, 0, 4, st));
   }
-  k_blocks_fix<<<1, 1, 0, st>>>(n, n_c, G, P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_slice),
+  k_blocks_fix<<<1, kFixThreads, 0, st>>>(n, n_c, G, P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_slice),
                                 P<int>(ws.blk_first), P<int>(ws.blk_cr), P<int>(ws.cposc),
                                 P<SetupSummary>(ws.summary));
   ++launches;
@@ -547,7 +598,7 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   k_poslen<<<nblk(n + 1), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.pos_len));
   VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.pos_len), P<int64_t>(ws.pos_ptr), n + 1,
                                         st));
-  k_summary<<<1, 1, 0, st>>>(n, G, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int64_t>(ws.pos_ptr),
+  k_summary<<<1, kFixThreads, 0, st>>>(n, G, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int64_t>(ws.pos_ptr),
                              P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr), P<int>(ws.flags),
                              P<SetupSummary>(ws.summary));
   launches += 3;

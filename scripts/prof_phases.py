@@ -23,10 +23,14 @@ G = h.last_layout()["ctas"]
 buf = (C.c_longlong * (32 * G))()
 h.L.vfpi_get_profile(h.h, buf, 32 * G)
 a = np.frombuffer(buf, dtype=np.int64).reshape(G, 4, 8)
-names = ["bb/cheb", "products", "pass B", "contacts", "reduce+barrier"]
-for k, nm in enumerate(names):
-    d = a[:, :, k + 1] - a[:, :, k] if k < 4 else a[:, :, 5] - a[:, :, 4]
-    print(f"{nm:16s} cycles mean {d.mean():9.0f}  max {d.max():9.0f}  min {d.min():9.0f}")
+def show(nm, d):
+    print(f"{nm:22s} cycles mean {d.mean():9.0f}  max {d.max():9.0f}  min {d.min():9.0f}")
+show("products", a[:, :, 2] - a[:, :, 0])
+show("pass B contact rows", a[:, :, 3] - a[:, :, 2])
+show("contact warps", np.where(a[:, :, 6] > 0, a[:, :, 6] - a[:, :, 3], 0))
+show("free-row warps", np.where(a[:, :, 1] > 0, a[:, :, 1] - a[:, :, 3], 0))
+show("role phase (sync)", a[:, :, 4] - a[:, :, 3])
+show("reduce+barrier", a[:, :, 5] - a[:, :, 4])
 tot = a[:, :, 5] - a[:, :, 0]
 print(f"{'iteration':16s} cycles mean {tot.mean():9.0f}  max {tot.max():9.0f}")
 work = a[:, :, 4] - a[:, :, 0]
