@@ -127,6 +127,8 @@ int vfpi_set_kernel(vfpi_handle* h, int mode);
  * phase starts 0..5, globaltimer at 7); vfpi_get_profile copies them out. */
 int vfpi_set_profile(vfpi_handle* h, int iter0);
 int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
+/* Tuning knobs (key 0: force the resident kernel's contact-warp count, 0 = auto). */
+int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */
 void* vfpi_host_alloc(int64_t bytes);

@@ -76,6 +76,7 @@ def lib() -> C.CDLL:
                 "vfpi_last_layout": (C.c_int, [H, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
                 "vfpi_set_kernel": (C.c_int, [H, C.c_int]),
                 "vfpi_set_profile": (C.c_int, [H, C.c_int]),
+                "vfpi_set_tuning": (C.c_int, [H, C.c_int, C.c_int]),
                 "vfpi_get_profile": (C.c_int, [H, C.POINTER(C.c_longlong), C.c_int64]),
                 "vfpi_host_alloc": (C.c_void_p, [C.c_int64]),
                 "vfpi_host_free": (None, [C.c_void_p]),

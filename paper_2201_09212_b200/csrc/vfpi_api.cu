@@ -40,6 +40,7 @@ struct vfpi_handle {
   int last_resident = 0;
   int kernel_mode = 0;  // 0 auto, 1 force shared-memory resident, 2 force streaming
   int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
+  int tune_wc = 0;      // >0: force the contact-warp count of the resident kernel
   int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
@@ -180,7 +181,9 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.slice_w, &h->ws.slice_off, &h->ws.sell_val, &h->ws.sell_col, &h->ws.pos_len, &h->ws.pos_ptr,
                             &h->ws.pk_val, &h->ws.pk_col, &h->ws.bar_flags, &h->ws.ucr, &h->ws.ufr,
                             &h->ws.cposc, &h->ws.cposf, &h->ws.blk_first, &h->ws.blk_cr, &h->ws.cont_q,
-                            &h->ws.ps_col, &h->ws.ps_src, &h->ws.seg_beg, &h->ws.seg_end, &h->ws.rowpos, &h->ws.vbuf,
+                            &h->ws.ps_col, &h->ws.ps_src, &h->ws.seg_beg, &h->ws.seg_end, &h->ws.rowpos, &h->ws.sec_key,
+                            &h->ws.sec_skey, &h->ws.sec_idx, &h->ws.sec_sidx, &h->ws.sec_flag, &h->ws.sec_upos,
+                            &h->ws.sell_map, &h->ws.secs, &h->ws.sec_ptr, &h->ws.vbuf,
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
                             &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
   for (auto* b : bufs)
@@ -197,6 +200,12 @@ void vfpi_destroy(vfpi_handle* h) {
 const char* vfpi_last_error(const vfpi_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 int64_t vfpi_launch_count(const vfpi_handle* h) { return h ? h->launches : 0; }
+
+int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
+  if (!h) return VFPI_BAD_ARGUMENT;
+  if (key == 0) { h->tune_wc = value; return VFPI_OK; }
+  return VFPI_BAD_ARGUMENT;
+}
 
 int vfpi_set_profile(vfpi_handle* h, int iter0) {
   if (!h || iter0 < 0) return VFPI_BAD_ARGUMENT;
@@ -262,7 +271,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   const size_t smem_res = (size_t)hs->max_res_bytes;
   const bool fits = hs->max_ent_per_blk < (1 << 24) && smem_res + 2048 <= (size_t)ws.max_smem_optin && G <= 256;
   if (h->kernel_mode == 1 && !fits) { h->err = "partition does not fit in shared memory"; return VFPI_UNSUPPORTED; }
-  const bool resident = fits && h->kernel_mode != 2;
+  bool resident = fits && h->kernel_mode != 2;
   int smem = 0;
   if (!resident) {
     G = choose_blocks(*d, ws.num_sms);
@@ -278,11 +287,27 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   }
   rc = vfpi::setup_pack(ws, *d, G, resident, *hs, st, h->err, h->launches);
   if (rc) return rc;
+  size_t smem_res_full = 0;
+  if (resident) {
+    // second read: the staged-sector count is known only after packing
+    CK(cudaMemcpyAsync(hs, ws.summary.p, sizeof(vfpi::SetupSummary), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    smem_res_full = (size_t)hs->max_res_bytes;
+    if (smem_res_full + 2048 > (size_t)ws.max_smem_optin) {
+      if (h->kernel_mode == 1) { h->err = "partition does not fit in shared memory"; return VFPI_UNSUPPORTED; }
+      resident = false;  // SELL-32 slices are packed for both kernels: stream instead
+      smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
+    }
+  }
   rc = vfpi::setup_step_matrix(ws, *d, *cfg, w_cached, st, h->err, h->launches);
   if (rc) return rc;
 
   const int tr = std::max(cfg->max_iters, 1);
-  CK(vfpi::ensure(ws.vbuf, 3 * 8 * (size_t)std::max(n, 1)));
+  // v ring: each buffer 32-byte aligned with 4 spare doubles, because the
+  // resident kernel stages whole 32-byte sectors
+  const size_t npad = (((size_t)std::max(n, 1) + 3) / 4) * 4 + 4;
+  CK(vfpi::ensure(ws.vbuf, 3 * 8 * npad));
+  CK(cudaMemsetAsync(ws.vbuf.p, 0, 3 * 8 * npad, st));
   CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)std::max(n_c, 1)));
   CK(vfpi::ensure(ws.partials, 2 * 8 * (size_t)G * vfpi::kPartialStride));
   CK(vfpi::ensure(ws.status, sizeof(vfpi::SolveStatus)));
@@ -292,7 +317,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   double* lb = P<double>(ws.lambuf);
   if (n > 0) {
     CK(cudaMemcpyAsync(vb, warm, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(vb + 2 * (size_t)n, warm, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(vb + 2 * npad, warm, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
   }
   CK(cudaMemsetAsync(lb, 0, 2 * 24 * (size_t)std::max(n_c, 1), st));
   CK(cudaMemsetAsync(ws.status.p, 0, sizeof(vfpi::SolveStatus), st));
@@ -311,16 +336,15 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.sell_val = P<double>(ws.sell_val);
   p.sell_col = P<int>(ws.sell_col);
   p.pos_ptr = P<int64_t>(ws.pos_ptr);
-  p.pk_val = P<double>(ws.pk_val);
-  p.pk_col = P<int>(ws.pk_col);
-  p.ps_col = P<int>(ws.ps_col);
-  p.ps_src = P<int>(ws.ps_src);
+  p.sell_map = P<unsigned>(ws.sell_map);
+  p.secs = P<unsigned>(ws.secs);
+  p.sec_ptr = P<int>(ws.sec_ptr);
   p.blk_cr = P<int>(ws.blk_cr);
   p.cont_q = P<int>(ws.cont_q);
-  p.rowpos = P<int>(ws.rowpos);
   p.bar_flags = P<int>(ws.bar_flags);
   p.prof = nullptr;
   p.prof_iter0 = 0;
+  p.tune_wc = h->tune_wc;
   if (h->prof_iter0 > 0) {
     CK(vfpi::ensure(ws.prof, sizeof(long long) * 32 * (size_t)G));
     CK(cudaMemsetAsync(ws.prof.p, 0, sizeof(long long) * 32 * (size_t)G, st));
@@ -339,8 +363,8 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.phi = d->phi;
   p.w_mean = P<double>(ws.w_mean);
   p.vbuf0 = vb;
-  p.vbuf1 = vb + (size_t)n;
-  p.vbuf2 = vb + 2 * (size_t)n;
+  p.vbuf1 = vb + npad;
+  p.vbuf2 = vb + 2 * npad;
   p.lam0 = lb;
   p.lam1 = lb + 3 * (size_t)std::max(n_c, 1);
   p.partials = P<double>(ws.partials);
@@ -356,7 +380,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.omega = cfg->omega;
   p.cfactor = cfg->consistency_factor;
   (void)tr;
-  rc = resident ? vfpi::launch_iterate_resident(p, cfg->op, cheb, bb, smem_res, st, h->err)
+  rc = resident ? vfpi::launch_iterate_resident(p, cfg->op, cheb, bb, smem_res_full, st, h->err)
                 : vfpi::launch_iterate(p, cfg->op, cheb, bb, smem, st, h->err);
   if (rc) return rc;
   h->last_resident = resident ? 1 : 0;

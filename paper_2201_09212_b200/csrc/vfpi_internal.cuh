@@ -13,23 +13,26 @@ constexpr int kThreads = 256;      // threads per CTA of the iteration kernel
 constexpr int kSlotsPerContact = 6;  // rows of a contact unit (3 for S, 6 for D)
 constexpr int kPartialStride = 8;  // doubles per CTA per parity in the partials ring
 
-// Shared-memory layout of one CTA of the resident iteration kernel:
-// E numeric entries, R rows (the first CR of them belong to its C contacts).
+// Shared-memory layout of one CTA of the resident iteration kernel: EP SELL-32
+// elements (values + gather map) of its R rows (the first CR belong to its C
+// contacts) and NS staged 32-byte sectors of remote v.
 struct ResLayout {
-  size_t o_sv, o_prod, o_sc, o_sd, o_rp, o_row, o_b, o_w, o_v0, o_v1, o_cm, o_cq, o_fr, o_par, o_lam, o_vs, o_jt,
-      total;
-  __host__ __device__ ResLayout(int64_t E, int R, int C, int CR) {
+  size_t o_sv, o_map, o_xs, o_sec, o_sb, o_len, o_row, o_b, o_w, o_v0, o_v1, o_cm, o_cq, o_fr, o_par, o_lam, o_vs,
+      o_jt, total;
+  __host__ __device__ ResLayout(int64_t EP, int R, int C, int CR, int NS) {
     size_t o = 0;
     auto take = [&](size_t bytes) {
       const size_t r = o;
       o += (bytes + 15) & ~size_t(15);
       return r;
     };
-    o_sv = take(8 * (size_t)E);    // values, column-sorted
-    o_prod = take(8 * (size_t)E);  // products, row-ordered
-    o_sc = take(4 * (size_t)E);    // columns, sorted
-    o_sd = take(4 * (size_t)E);    // row-ordered slot of each sorted entry
-    o_rp = take(4 * (size_t)(R + 1));
+    const int NSL = (R + 31) / 32;
+    o_sv = take(8 * (size_t)EP);
+    o_map = take(4 * (size_t)EP);
+    o_xs = take(32 * (size_t)NS);
+    o_sec = take(4 * (size_t)NS);
+    o_sb = take(4 * (size_t)(NSL + 1));
+    o_len = take(4 * (size_t)R);
     o_row = take(4 * (size_t)R);
     o_b = take(8 * (size_t)R);
     o_w = take(8 * (size_t)R);
@@ -82,15 +85,14 @@ struct IterParams {
   const double* sell_val;   // [sell_elems]
   const int* sell_col;      // [sell_elems], -1 = padding
   const int64_t* pos_ptr;   // [n+1] entry offset of every row-list position (resident kernel)
-  const double* pk_val;     // [nnz_num] entries in row-list order (resident kernel)
-  const int* pk_col;
-  const int* ps_col;        // [nnz_num] per-CTA column-sorted columns (resident kernel)
-  const int* ps_src;        // [nnz_num] their row-ordered global entry index
+  const unsigned* sell_map; // [sell_elems] gather map of every SELL element (resident kernel)
+  const unsigned* secs;     // [sum NS] 32-byte sectors of v each CTA stages per iteration
+  const int* sec_ptr;       // [G+1] per-CTA range in secs
   const int* blk_cr;        // [G+1] contact rows at the head of every CTA range
   const int* cont_q;        // [n_c] local row position of each contact's first row
-  const int* rowpos;        // [n] row-list position of every row
   int* bar_flags;           // [G] epoch flags of the flag barrier
   long long* prof;          // optional [G][4][8] phase timestamps (NULL = off)
+  int tune_wc;              // > 0: force the number of contact warps (tuning aid)
   int prof_iter0;           // first of the 4 profiled iterations
   const int* cont_list;     // [n_c] contact ids in partition order
   // system
@@ -171,6 +173,7 @@ struct Workspace {
   Buf blk_row, blk_ct, blk_slice, row_list, row_slot, cont_list;
   Buf slice_w, slice_off, sell_val, sell_col, pos_len, pos_ptr, pk_val, pk_col, bar_flags;
   Buf ucr, ufr, cposc, cposf, blk_first, blk_cr, cont_q, ps_col, ps_src, seg_beg, seg_end, rowpos;
+  Buf sec_key, sec_skey, sec_idx, sec_sidx, sec_flag, sec_upos, sell_map, secs, sec_ptr;
   Buf vbuf, lambuf, partials, status, summary, flags, cub_tmp;
   Buf x, y;  // scratch for per-op entry points
   Buf prof;

@@ -1,20 +1,21 @@
 // V-FPI iteration, shared-memory-resident variant (the configs[1] path).
 //
-// Same algorithm and decision pipeline as vfpi_solve.cu (reference loop
-// solver.py:388-446), but each CTA (one per SM) keeps its whole partition on
-// chip for the lifetime of the launch:
-//   * its rows' numeric entries (values + columns, CTA-contiguous CSR),
-//     b, w, the contact frames and parameters, lam (both parities), J_c^T lam
-//     and v* of contact rows -> only the x-gathers of the SpMV and the
-//     v_next stores touch L2 per iteration;
-//   * the SpMV is split in two passes so the gathers are fully parallel while
-//     the row sums keep scipy's sequential order bit for bit:
-//       pass A  prod[e] = a[e] * x[col[e]]   (all entries, 8 gathers in flight / thread)
-//       pass B  acc(row) = (((0 + prod[k0]) + prod[k0+1]) + ...)   (one thread per row)
-//   * the grid barrier is a flag barrier fused with the deterministic
-//     residual reduction: every CTA publishes (theta^2, force^2, #nonfinite)
-//     and an epoch flag; every CTA waits for all flags and sums the G partials
-//     in the same fixed order, so decisions are identical everywhere.
+// Same algorithm as vfpi_solve.cu (reference loop solver.py:388-446), but each
+// CTA (one per SM) keeps its whole partition on chip for the lifetime of the
+// launch: its rows' SELL-32 entries, b, w, its own rows of v, the contact
+// frames / parameters, lam (both parities), J_c^T lam and v* of contact rows.
+// Per iteration only two things cross L2:
+//   * phase 1 stages, as whole 32-byte sectors, the entries of v^(l-1) the CTA
+//     reads from other CTAs' rows (the sector list is fixed per solve, so the
+//     ~5 scattered 8-byte gathers per entry become ~1 coalesced 32-byte load
+//     per distinct sector, all in flight at once);
+//   * v_next of its own rows is stored for the other CTAs.
+// Row sums then run out of shared memory in scipy's sequential order (bit for
+// bit), contacts run as lane quads beside the free rows, and one release
+// reduction on a monotonic counter is the grid barrier. The residual partials
+// of iteration l are reduced (in the same fixed order by every CTA) while the
+// sectors of iteration l+1 are in flight, and the convergence decision for l
+// is taken at the top of l+1.
 #include <climits>
 
 #include "vfpi_internal.cuh"
@@ -24,19 +25,29 @@ namespace vfpi {
 
 namespace {
 
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+constexpr unsigned kOwn = 0x80000000u;
+constexpr int kLPC = 4;                 // lanes per contact in the one-shot phase
+constexpr int kMaxPartialsPerLane = 8;  // G <= 256
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// one 32-byte sector of v in a single 256-bit load (coherent: plain ld.global)
+__device__ __forceinline__ double4 ld_sector(const double* p) {
+  double4 r;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p)
+               : "memory");
+  return r;
+}
 
-// fixed-order CTA sum of three doubles -> sm_out[0..2] (visible after the trailing barrier)
+// fixed-order CTA sum of three doubles -> sm_out[0..2] (visible after the next barrier)
 __device__ __forceinline__ void cta_reduce3(double a, double b, double c, double* sm_warp, double* sm_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
@@ -69,28 +80,10 @@ __device__ __forceinline__ void cta_reduce3(double a, double b, double c, double
   }
 }
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Grid barrier fused with the deterministic reduction of three partial sums.
-// Arrive: thread 0 stores the CTA's partials, then one release reduction on a
-// monotonic counter (target epoch*G: no reset between barriers). Wait: thread
-// 0 spins with acquire loads on that single word. Collect: warp 0 reads the G
-// partials (<= 8 independent loads per lane) and reduces them in a fixed order
-// that is identical in every CTA, so every CTA gets bit-identical totals.
-constexpr int kMaxPartialsPerLane = 8;  // G <= 256
-constexpr int kLPC = 4;                 // lanes per contact in the one-shot phase
-
-__device__ __forceinline__ void grid_reduce3(double a, double b, double c, double* part, int off, unsigned* counter,
-                                             int G, int epoch, double* sm_warp, double* sm_tot) {
-  cta_reduce3(a, b, c, sm_warp, sm_tot);
+// Arrive (publish this CTA's partials, release-add the counter) and wait until
+// all G CTAs arrived at `epoch` (counter target epoch*G, never reset).
+__device__ __forceinline__ void grid_arrive_wait(const double* sm_tot, double* part, int off, unsigned* counter,
+                                                 int G, int epoch) {
   if (threadIdx.x == 0) {
     double* q = part + (size_t)blockIdx.x * kPartialStride + off;
     q[0] = sm_tot[0];
@@ -104,67 +97,58 @@ __device__ __forceinline__ void grid_reduce3(double a, double b, double c, doubl
     }
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double x = 0.0, y = 0.0, z = 0.0;
-#pragma unroll
-    for (int k = 0; k < kMaxPartialsPerLane; ++k) {
-      const int g = lane + 32 * k;
-      if (g < G) {
-        const double* q = part + (size_t)g * kPartialStride + off;
-        x = dadd(x, __ldcg(q + 0));
-        y = dadd(y, __ldcg(q + 1));
-        z = dadd(z, __ldcg(q + 2));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      x = dadd(x, __shfl_xor_sync(0xffffffffu, x, o));
-      y = dadd(y, __shfl_xor_sync(0xffffffffu, y, o));
-      z = dadd(z, __shfl_xor_sync(0xffffffffu, z, o));
-    }
-    if (lane == 0) {
-      sm_tot[0] = x;
-      sm_tot[1] = y;
-      sm_tot[2] = z;
-    }
-  }
-  __syncthreads();
 }
 
-// pass A: prod[dst[i]] = a[i] * x(col[i]) over the CTA's column-sorted entries
-// (neighbouring lanes gather neighbouring columns), UN gathers per thread in flight
-template <class X>
-__device__ __forceinline__ void products(const double* __restrict__ sv, const int* __restrict__ sc,
-                                         const int* __restrict__ sd, double* __restrict__ prod, int E, X x) {
-  constexpr int UN = 8;
-  const int T = blockDim.x;
-  for (int base = threadIdx.x; base < E; base += UN * T) {
-    int c[UN];
-    double xv[UN];
+// warp 0: fixed-order sum of the G published partials -> sm_tot[0..2]
+__device__ __forceinline__ void warp0_collect(const double* part, int off, int G, double* sm_tot) {
+  const int lane = threadIdx.x & 31;
+  double x = 0.0, y = 0.0, z = 0.0;
 #pragma unroll
-    for (int u = 0; u < UN; ++u) {
-      const int i = base + u * T;
-      c[u] = i < E ? sc[i] : INT_MIN;
+  for (int k = 0; k < kMaxPartialsPerLane; ++k) {
+    const int g = lane + 32 * k;
+    if (g < G) {
+      const double* q = part + (size_t)g * kPartialStride + off;
+      x = dadd(x, __ldcg(q + 0));
+      y = dadd(y, __ldcg(q + 1));
+      z = dadd(z, __ldcg(q + 2));
     }
+  }
 #pragma unroll
-    for (int u = 0; u < UN; ++u) xv[u] = c[u] != INT_MIN ? x(c[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < UN; ++u) {
-      const int i = base + u * T;
-      if (i < E) prod[sd[i]] = dmul(sv[i], xv[u]);
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    x = dadd(x, __shfl_xor_sync(0xffffffffu, x, o));
+    y = dadd(y, __shfl_xor_sync(0xffffffffu, y, o));
+    z = dadd(z, __shfl_xor_sync(0xffffffffu, z, o));
+  }
+  if (lane == 0) {
+    sm_tot[0] = x;
+    sm_tot[1] = y;
+    sm_tot[2] = z;
   }
 }
 
-// pass B: sequential (scipy-order) sum of one row's products, loads batched by 4
-__device__ __forceinline__ double row_sum(const double* __restrict__ prod, int k, int k1) {
+// sequential (scipy-order) dot of one row with x: SELL element i = base + 32k,
+// x from the staged sectors or from the CTA's own rows
+__device__ __forceinline__ double row_dot(const double* __restrict__ sv, const unsigned* __restrict__ mp, int base,
+                                          int len, const double* __restrict__ xs, const double* __restrict__ vown) {
   double acc = 0.0;
-  for (; k + 4 <= k1; k += 4) {
-    const double t0 = prod[k], t1 = prod[k + 1], t2 = prod[k + 2], t3 = prod[k + 3];
-    acc = dadd(dadd(dadd(dadd(acc, t0), t1), t2), t3);
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    double a[4], x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = base + 32 * (k + u);
+      const unsigned m = mp[i];
+      a[u] = sv[i];
+      x[u] = (m & kOwn) ? vown[m & ~kOwn] : xs[m];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = dadd(acc, dmul(a[u], x[u]));
   }
-  for (; k < k1; ++k) acc = dadd(acc, prod[k]);
+  for (; k < len; ++k) {
+    const int i = base + 32 * k;
+    const unsigned m = mp[i];
+    acc = dadd(acc, dmul(sv[i], (m & kOwn) ? vown[m & ~kOwn] : xs[m]));
+  }
   return acc;
 }
 
@@ -175,18 +159,23 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   __shared__ double sm_tot[4];
   __shared__ unsigned long long sm_role_end[2];
   const int b = blockIdx.x, G = p.G, T = blockDim.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = T >> 5;
   if (tid < 2) sm_role_end[tid] = 0;
   const int p0 = p.blk_row[b], p1 = p.blk_row[b + 1], R = p1 - p0;
-  const int64_t e0 = p.pos_ptr[p0];
-  const int E = (int)(p.pos_ptr[p1] - e0);
+  const int s0 = p.blk_slice[b], s1 = p.blk_slice[b + 1];
+  const int64_t ep0 = p.slice_off[s0];
+  const int EP = (int)(p.slice_off[s1] - ep0);
   const int c0 = p.blk_ct[b], c1 = p.blk_ct[b + 1], C = c1 - c0;
   const int CR = HASC ? p.blk_cr[b] : 0;  // rows [0, CR) belong to the CTA's contacts
-  const ResLayout Lo(E, R, C, CR);        // this CTA's own footprint (launch size = max over CTAs)
+  const int sec0 = p.sec_ptr[b];
+  const int NS = p.sec_ptr[b + 1] - sec0;
+  const ResLayout Lo(EP, R, C, CR, NS);  // this CTA's own footprint (launch size = max over CTAs)
   double* sv = reinterpret_cast<double*>(smraw + Lo.o_sv);
-  double* prod = reinterpret_cast<double*>(smraw + Lo.o_prod);
-  int* sc = reinterpret_cast<int*>(smraw + Lo.o_sc);
-  int* sd = reinterpret_cast<int*>(smraw + Lo.o_sd);
-  int* rp = reinterpret_cast<int*>(smraw + Lo.o_rp);
+  unsigned* mp = reinterpret_cast<unsigned*>(smraw + Lo.o_map);
+  double* xs = reinterpret_cast<double*>(smraw + Lo.o_xs);
+  unsigned* sec = reinterpret_cast<unsigned*>(smraw + Lo.o_sec);
+  int* sb = reinterpret_cast<int*>(smraw + Lo.o_sb);
+  int* rlen = reinterpret_cast<int*>(smraw + Lo.o_len);
   int* rw = reinterpret_cast<int*>(smraw + Lo.o_row);
   double* bs = reinterpret_cast<double*>(smraw + Lo.o_b);
   double* ws = reinterpret_cast<double*>(smraw + Lo.o_w);
@@ -199,24 +188,23 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   double* lam_s = reinterpret_cast<double*>(smraw + Lo.o_lam); // [2][3C]
   double* vs_s = reinterpret_cast<double*>(smraw + Lo.o_vs);   // [CR]
   double* jt_s = reinterpret_cast<double*>(smraw + Lo.o_jt);   // [CR]
+  unsigned* counter = reinterpret_cast<unsigned*>(p.bar_flags);
 
   // ---- stage the partition on chip (once per launch) --------------------
-  for (int i = tid; i < E; i += T) {
-    const int src = __ldg(p.ps_src + e0 + i);
-    const int c = __ldg(p.ps_col + e0 + i);
-    sc[i] = c;
-    sd[i] = (int)(src - e0);
-    sv[i] = __ldg(p.pk_val + src);
+  for (int i = tid; i < EP; i += T) {
+    sv[i] = __ldg(p.sell_val + ep0 + i);
+    mp[i] = __ldg(p.sell_map + ep0 + i);
   }
+  for (int j = tid; j < NS; j += T) sec[j] = __ldg(p.secs + sec0 + j);
+  for (int s = tid; s <= s1 - s0; s += T) sb[s] = (int)(__ldg(p.slice_off + s0 + s) - ep0);
   for (int q = tid; q < R; q += T) {
     const int row = __ldg(p.row_list + p0 + q);
-    rp[q] = (int)(__ldg(p.pos_ptr + p0 + q) - e0);
+    rlen[q] = (int)(__ldg(p.pos_ptr + p0 + q + 1) - __ldg(p.pos_ptr + p0 + q));
     rw[q] = row;
     bs[q] = __ldg(p.b + row);
     ws[q] = __ldg(p.w + row);
     vown[q] = p.vbuf0[row];
   }
-  if (tid == 0) rp[R] = E;
   for (int k = tid; k < C; k += T) {
     const int m = __ldg(p.cont_list + c0 + k);
     cm[k] = m;
@@ -232,21 +220,21 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   for (int t = tid; t < CR; t += T) jt_s[t] = 0.0;
   __syncthreads();
 
-  // warps [0, WC) run the contact one-shots while warps [WC, nw) finish the free rows
-  const int nw = T >> 5, warp = tid >> 5;
-  // split the warps between the contact quads (kLPC lanes per contact) and the
-  // free rows so both finish together: cost ~ rounds x per-round latency
+  // split the warps: [0, WC) sweep the contact rows and run the contact quads,
+  // [WC, nw) sweep the free rows; estimated cost = rounds x per-round latency
   int WC = 0;
   if (C > 0) {
     const int FR = R - CR;
     if (FR == 0) {
       WC = nw;
     } else {
-      const int efree = E - rp[CR];
-      const long long kf = 8LL * (efree / FR + 1) + 200;  // cycles per free-row round
+      int maxlen = 0;
+      for (int q = CR; q < R; ++q) maxlen = rlen[q] > maxlen ? rlen[q] : maxlen;
+      const long long kf = 22LL * maxlen + 400;  // cycles per free-row round
       long long best = LLONG_MAX;
       for (int w = 1; w < nw; ++w) {
-        const long long tc = (long long)((C + (32 / kLPC) * w - 1) / ((32 / kLPC) * w)) * 1000;
+        const long long tc = (long long)((CR + 32 * w - 1) / (32 * w)) * 500 +
+                             (long long)((C + (32 / kLPC) * w - 1) / ((32 / kLPC) * w)) * 2500;
         const long long tf = (long long)((FR + 32 * (nw - w) - 1) / (32 * (nw - w))) * kf;
         const long long c2 = tc > tf ? tc : tf;
         if (c2 < best) { best = c2; WC = w; }
@@ -254,6 +242,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     }
   }
 
+  if (C > 0 && WC < nw && p.tune_wc > 0) WC = p.tune_wc < nw ? p.tune_wc : nw - 1;
   double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
   const double u = p.under_relax;
   const double omu = dsub(1.0, u);
@@ -283,30 +272,83 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     const double* vprev = vb[(l + 1) % 3];  // v^(l-2)
     double* vnext = vb[l % 3];
     double* lam_out = lam_s + (l & 1) * 3 * C;
+
+    // ---- phase 1: stage the remote sectors of v^(l-1); reduce partials of l-1
+    {
+      double4* dst = reinterpret_cast<double4*>(xs);
+      for (int j = tid; j < NS; j += T) dst[j] = ld_sector(vcur + 4 * (size_t)sec[j]);
+      if (l > 1 && warp == 0)
+        warp0_collect(p.partials + (size_t)((l - 1) & 1) * G * kPartialStride, 0, G, sm_tot);
+    }
+    __syncthreads();
+    stamp(2);
+
+    // ---- decision for iteration l-1 (solver.py:422-446) -------------------
+    if (l > 1) {
+      const int lp = l - 1;
+      const double theta = dsqrt(sm_tot[0]);   // theta_{l-1}
+      const double fres = dsqrt(sm_tot[1]);    // ||A v^(l-2) - b - J_c^T lam^(l-2)||
+      const bool nonfinite = sm_tot[2] > 0.0;
+      if (pending) {
+        consistency = fres;
+        if (fres <= dmul(p.cfactor, p.tol)) {
+          iters = lp - 1; conv = 1;
+          final_buf = (lp - 1) % 3; final_lam = (lp - 1) & 1;
+          break;
+        }
+      }
+      if (lp == p.max_iters + 1) {
+        iters = p.max_iters;
+        consistency = fres;
+        final_buf = (lp - 1) % 3; final_lam = (lp - 1) & 1;
+        break;
+      }
+      if (b == 0 && tid == 0) p.trace[lp - 1] = theta;
+      if (nonfinite) {
+        iters = lp; div = 1;
+        final_buf = lp % 3; final_lam = lp & 1;
+        break;
+      }
+      pending = theta < p.tol;
+      if (CHEB) rho = (theta_prev <= 0.0) ? rho : py_min(ddiv(theta, theta_prev), 1.0);
+      theta_prev = theta;
+      double* tmp = vown;  // own rows of v^(l-1) become the current iterate
+      vown = vown2;
+      vown2 = tmp;
+    }
     double* part = p.partials + (size_t)(l & 1) * G * kPartialStride;
 
     // ---- Barzilai-Borwein scalar step (solver.py:389-400) ----------------
     bool use_alpha = false;
     if (BB && l >= 2 && !check_only) {
-      products(sv, sc, sd, prod, E, [&](int c) { return dsub(vcur[c], vprev[c]); });
-      __syncthreads();
       double sz = 0.0, ss = 0.0, zz = 0.0;
       for (int q = tid; q < R; q += T) {
-        const double z = row_sum(prod, rp[q], rp[q + 1]);
-        const int row = rw[q];
-        const double s = dsub(vown[q], vprev[row]);
+        // z = A s with s = v - v_prev gathered from global (BB is not a hot configuration)
+        const int base = sb[q >> 5] + (q & 31);
+        double z = 0.0;
+        for (int k = 0; k < rlen[q]; ++k) {
+          const int i = base + 32 * k;
+          const unsigned m = mp[i];
+          const int g = (m & kOwn) ? rw[m & ~kOwn] : (int)(4u * sec[m >> 2] + (m & 3u));
+          z = dadd(z, dmul(sv[i], dsub(vcur[g], vprev[g])));
+        }
+        const double s = dsub(vown[q], vprev[rw[q]]);
         sz = dadd(sz, dmul(s, z));
         ss = dadd(ss, dmul(s, s));
         zz = dadd(zz, dmul(z, z));
       }
-      grid_reduce3(sz, ss, zz, part, 4, reinterpret_cast<unsigned*>(p.bar_flags), G, ++epoch, sm_warp, sm_tot);
+      cta_reduce3(sz, ss, zz, sm_warp, sm_tot);
+      __syncthreads();
+      grid_arrive_wait(sm_tot, part, 4, counter, G, ++epoch);
+      if (warp == 0) warp0_collect(part, 4, G, sm_tot);
+      __syncthreads();
       const double tsz = sm_tot[0], tss = sm_tot[1], tzz = sm_tot[2];
       const bool bb1 = (p.step == VFPI_STEP_BB1) || (p.step == VFPI_STEP_BB_ALTERNATING && (l % 2 == 0));
       if (tsz <= 0.0) alpha = alpha_prev;
       else alpha = bb1 ? ddiv(tss, tsz) : ddiv(tsz, tzz);
       alpha_prev = alpha;
       use_alpha = true;
-      __syncthreads();  // prod and sm_tot are reused below
+      __syncthreads();  // sm_tot is reused below
     }
 
     if (CHEB && !check_only) {  // solver.py:284-290, :417
@@ -324,8 +366,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       if (CHEB) {
         const double vss = dadd(dmul(u, vnew), dmul(omu, vc));
         if (l > 1) {
-          const double vp = vprev[row];
-          vn = dadd(dmul(nu, dsub(vss, vp)), vp);
+          const double vpv = vprev[row];
+          vn = dadd(dmul(nu, dsub(vss, vpv)), vpv);
         } else {
           vn = vss;
         }
@@ -338,33 +380,30 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     };
     // r = A v - b of own row q; force residual of the previous iterate (solver.py:437-439)
     auto residual = [&](int q) {
-      const double r = dsub(row_sum(prod, rp[q], rp[q + 1]), bs[q]);
+      const double r = dsub(row_dot(sv, mp, sb[q >> 5] + (q & 31), rlen[q], xs, vown), bs[q]);
       const double f = (q < CR) ? dsub(r, jt_s[q]) : dsub(r, 0.0);
       fr = dadd(fr, dmul(f, f));
       return r;
     };
 
-    // ---- (1) surrogate-dynamics sweep: pass A gathers, pass B ordered sums --
-    products(sv, sc, sd, prod, E, [&](int c) { return vcur[c]; });
-    __syncthreads();
-    stamp(2);
-    // contact rows first: their v* feeds the contact one-shots
-    for (int q = tid; q < CR; q += T) {
-      const double r = residual(q);
-      if (!check_only) vs_s[q] = dsub(vown[q], dmul(use_alpha ? alpha : ws[q], r));
-    }
-    __syncthreads();
+    // ---- (1)-(3): contact warps sweep the contact rows then run the one-shots;
+    // the free-row warps sweep their rows concurrently -----------------------
     stamp(3);
-
     if (warp < WC) {
+      // (1) surrogate-dynamics sweep of the contact rows
+      for (int q = tid; q < CR; q += WC * 32) {
+        const double r = residual(q);
+        if (!check_only) vs_s[q] = dsub(vown[q], dmul(use_alpha ? alpha : ws[q], r));
+      }
+      if (WC == nw) __syncthreads();
+      else asm volatile("bar.sync 1, %0;" ::"r"(WC * 32) : "memory");
       // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter ------
       // kLPC lanes per contact: lane a < 3 owns frame row / component a; the
       // projection needs all three components and is evaluated redundantly.
       if (HASC && !check_only) {
-        const int lane = tid & 31;
         const int a = (lane & (kLPC - 1)) < 3 ? (lane & (kLPC - 1)) : 2;
         const bool owner = (lane & (kLPC - 1)) < 3;
-        const int qbase = lane & ~(kLPC - 1);  // first lane of this contact's group
+        const int qbase = lane & ~(kLPC - 1);
         for (int k0 = warp * (32 / kLPC); k0 < C; k0 += WC * (32 / kLPC)) {
           const int k = k0 + lane / kLPC;
           const bool act = k < C;
@@ -373,15 +412,14 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
           const int qb = code & 0x3fffffff;
           const bool dj = (code >> 30) & 1;
           const double* R9 = cfr + 9 * kk;
-          double rel[3], vi_a, vj_a = 0.0;
+          double rel[3];
 #pragma unroll
           for (int t = 0; t < 3; ++t) {
             const double xi = vs_s[qb + t];
             rel[t] = dj ? dsub(xi, vs_s[qb + 3 + t]) : xi;
           }
-          vi_a = vs_s[qb + a];
-          if (dj) vj_a = vs_s[qb + 3 + a];
-          // eta_a = R[a,:] rel  ((p0+p2)+p1, einsum order) ; lam*_a
+          const double vi_a = vs_s[qb + a];
+          const double vj_a = dj ? vs_s[qb + 3 + a] : 0.0;
           const double eta_a = dadd(dadd(dmul(R9[3 * a + 0], rel[0]), dmul(R9[3 * a + 2], rel[2])),
                                     dmul(R9[3 * a + 1], rel[1]));
           double g;
@@ -396,7 +434,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
             project(OP, lam, cpar[4 * kk + 0], cpar[4 * kk + 1]);
             if (owner) {
               lam_out[3 * k + a] = lam[a];
-              // world_a = R[:,a] . lam  ((p0+p1)+p2)
               const double wa = dadd(dadd(dmul(R9[a], lam[0]), dmul(R9[3 + a], lam[1])), dmul(R9[6 + a], lam[2]));
               const double oi = dadd(0.0, wa);  // np.add.at onto zeros
               jt_s[qb + a] = oi;
@@ -410,8 +447,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
           }
         }
       }
+      if (profl && lane == 0) atomicMax(&sm_role_end[0], (unsigned long long)clock64());
     }
-    if (profl && (tid & 31) == 0 && warp < WC) atomicMax(&sm_role_end[0], (unsigned long long)clock64());
     if (warp >= WC || WC == nw) {
       // ---- free rows: v_new = v* (+ w * 0 when contacts exist) ------------
       const int t0 = (WC == nw) ? tid : tid - WC * 32;
@@ -424,10 +461,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
           finish_row(q, HASC ? dadd(vstar, dmul(wr, 0.0)) : vstar);
         }
       }
+      if (profl && lane == 0) atomicMax(&sm_role_end[1], (unsigned long long)clock64());
     }
 
-    if (profl && (tid & 31) == 0 && (warp >= WC || WC == nw)) atomicMax(&sm_role_end[1], (unsigned long long)clock64());
-    // ---- (4) residual reduction + grid-wide decision --------------------
+    // ---- (4) residual partials + grid barrier (reduction at the top of l+1)
     stamp(4);
     if (profl && tid == 0) {
       p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 8 + 6] = (long long)sm_role_end[0];
@@ -436,37 +473,33 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       sm_role_end[1] = 0;
     }
     stamp(7);
-    grid_reduce3(th, fr, nf, part, 0, reinterpret_cast<unsigned*>(p.bar_flags), G, ++epoch, sm_warp, sm_tot);
-    stamp(5);
-    const double theta = dsqrt(sm_tot[0]);
-    const double fres = dsqrt(sm_tot[1]);
-    const bool nonfinite = sm_tot[2] > 0.0;
-    if (pending) {
-      consistency = fres;
-      if (fres <= dmul(p.cfactor, p.tol)) {
-        iters = l - 1; conv = 1;
-        final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
-        break;
+    {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        th = dadd(th, __shfl_xor_sync(0xffffffffu, th, o));
+        fr = dadd(fr, __shfl_xor_sync(0xffffffffu, fr, o));
+        nf = dadd(nf, __shfl_xor_sync(0xffffffffu, nf, o));
+      }
+      if (lane == 0) {
+        sm_warp[3 * warp + 0] = th;
+        sm_warp[3 * warp + 1] = fr;
+        sm_warp[3 * warp + 2] = nf;
+      }
+      __syncthreads();
+      if (tid == 0) {  // fixed warp order
+        double x = 0.0, y = 0.0, z = 0.0;
+        for (int w2 = 0; w2 < nw; ++w2) {
+          x = dadd(x, sm_warp[3 * w2 + 0]);
+          y = dadd(y, sm_warp[3 * w2 + 1]);
+          z = dadd(z, sm_warp[3 * w2 + 2]);
+        }
+        sm_tot[0] = x;
+        sm_tot[1] = y;
+        sm_tot[2] = z;
       }
     }
-    if (check_only) {
-      iters = p.max_iters;
-      consistency = fres;
-      final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
-      break;
-    }
-    if (b == 0 && tid == 0) p.trace[l - 1] = theta;
-    if (nonfinite) {
-      iters = l; div = 1;
-      final_buf = l % 3; final_lam = l & 1;
-      break;
-    }
-    pending = theta < p.tol;
-    if (CHEB) rho = (theta_prev <= 0.0) ? rho : py_min(ddiv(theta, theta_prev), 1.0);
-    theta_prev = theta;
-    double* tmp = vown;  // own rows of v^(l) become the current iterate
-    vown = vown2;
-    vown2 = tmp;
+    grid_arrive_wait(sm_tot, part, 0, counter, G, ++epoch);
+    stamp(5);
   }
 
   const double* vfin = vb[final_buf];

@@ -273,7 +273,7 @@ __global__ void k_poslen(int n, const int* __restrict__ row_list, const int* __r
 __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int64_t* row_ptr,
                                                           const int64_t* slice_off, const int64_t* pos_ptr,
                                                           const int* blk_row, const int* blk_ct, const int* blk_cr,
-                                                          const int* flags, SetupSummary* sum) {
+                                                          const int* blk_slice, const int* flags, SetupSummary* sum) {
   __shared__ long long s_e[kFixThreads], s_b[kFixThreads];
   __shared__ int s_r[kFixThreads];
   const int b = threadIdx.x;
@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int
   if (b < G) {
     e = pos_ptr[blk_row[b + 1]] - pos_ptr[blk_row[b]];
     r = blk_row[b + 1] - blk_row[b];
-    by = (long long)ResLayout(e, r, blk_ct[b + 1] - blk_ct[b], blk_cr[b]).total;
+    const int64_t ep = slice_off[blk_slice[b + 1]] - slice_off[blk_slice[b]];
+    by = (long long)ResLayout(ep, r, blk_ct[b + 1] - blk_ct[b], blk_cr[b], 0).total;
   }
   s_e[b] = e;
   s_b[b] = by;
@@ -311,29 +312,110 @@ __global__ void k_rowpos(int n, const int* __restrict__ row_list, int* __restric
   if (q < n) rowpos[row_list[q]] = q;
 }
 
-__global__ void k_segments(int G, const int64_t* __restrict__ pos_ptr, const int* __restrict__ blk_row, int* beg,
-                           int* end) {
+// ---- gather plan of the resident kernel -------------------------------------
+// Every CTA stages, once per iteration, the 32-byte sectors of v its SELL
+// entries read from other CTAs' rows; columns that are its own rows read the
+// on-chip copy. sell_map[i] encodes where entry i's x comes from:
+//   0x80000000 | q  -> own row q (local position),  else 4*slot + (col & 3).
+constexpr unsigned kOwnBit = 0x80000000u;
+constexpr unsigned kNoSector = 0xFFFFFFFFu;
+
+__global__ void k_sell_segments(int G, const int64_t* __restrict__ slice_off, const int* __restrict__ blk_slice,
+                                int* beg, int* end) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= G) return;
-  beg[b] = (int)pos_ptr[blk_row[b]];
-  end[b] = (int)pos_ptr[blk_row[b + 1]];
+  beg[b] = (int)slice_off[blk_slice[b]];
+  end[b] = (int)slice_off[blk_slice[b + 1]];
 }
 
-// CTA-contiguous CSR: the entries of row-list position p at pos_ptr[p]..
-__global__ void k_pack_csr(int n, const int* __restrict__ row_list, const int* __restrict__ rowcnt,
-                           const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ pos_ptr,
-                           const int* __restrict__ perm, const int* __restrict__ colof,
-                           const double* __restrict__ data, double* __restrict__ pv, int* __restrict__ pc) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const int row = row_list[p];
-  const int len = rowcnt[row];
-  const int64_t src = row_ptr[row], dst = pos_ptr[p];
-  for (int k = 0; k < len; ++k) {
-    const int e = perm[src + k];
-    pv[dst + k] = data[e];
-    pc[dst + k] = colof[e];
+// warp per slice: sector key of every SELL element (kNoSector for padding/own)
+__global__ void k_sec_keys(int S, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_row,
+                           const int64_t* __restrict__ slice_off, const int* __restrict__ sell_col,
+                           const int* __restrict__ rowpos, unsigned* __restrict__ key, int* __restrict__ idx,
+                           unsigned* __restrict__ map) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= S) return;
+  const int b = owner(blk_slice, G, s);
+  const int p0 = blk_row[b], p1 = blk_row[b + 1];
+  const int64_t off = slice_off[s];
+  const int W = (int)((slice_off[s + 1] - off) >> 5);
+  for (int k = 0; k < W; ++k) {
+    const int64_t i = off + (int64_t)k * 32 + lane;
+    const int c = sell_col[i];
+    unsigned kk = kNoSector;
+    if (c >= 0) {
+      const int pc = rowpos[c];
+      if (pc >= p0 && pc < p1) map[i] = kOwnBit | (unsigned)(pc - p0);
+      else kk = (unsigned)c >> 2;
+    } else {
+      map[i] = 0u;
+    }
+    key[i] = kk;
+    idx[i] = (int)i;
   }
+}
+
+// first element of every run of equal sector keys inside a CTA segment
+__global__ void k_sec_flags(int64_t N, int G, const int* __restrict__ seg_beg, const unsigned* __restrict__ skey,
+                            int* __restrict__ flag) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const unsigned k = skey[j];
+  int f = 0;
+  if (k != kNoSector) {
+    int lo = 0, hi = G;  // segment containing j (largest b with seg_beg[b] <= j)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (seg_beg[mid] <= j) lo = mid; else hi = mid;
+    }
+    f = (j == seg_beg[lo] || skey[j - 1] != k) ? 1 : 0;
+  }
+  flag[j] = f;
+}
+
+__global__ void k_sec_emit(int64_t N, int G, const int* __restrict__ seg_beg, const unsigned* __restrict__ skey,
+                           const int* __restrict__ sidx, const int* __restrict__ flag, const int* __restrict__ upos,
+                           const int* __restrict__ sell_col, unsigned* __restrict__ secs, unsigned* __restrict__ map) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const unsigned k = skey[j];
+  if (k == kNoSector) return;
+  int lo = 0, hi = G;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (seg_beg[mid] <= j) lo = mid; else hi = mid;
+  }
+  const int u = upos[j] + flag[j] - 1;          // global unique id of this sector
+  const int base = upos[seg_beg[lo]];           // first unique id of the CTA
+  if (flag[j]) secs[u] = k;
+  const int i = sidx[j];
+  map[i] = 4u * (unsigned)(u - base) + ((unsigned)sell_col[i] & 3u);
+}
+
+__global__ void __launch_bounds__(1024) k_summary2(int G, int64_t NSELL, const int* __restrict__ seg_beg,
+                                                   const int* __restrict__ seg_end, const int* __restrict__ upos,
+                                                   const int* __restrict__ flag, const int* __restrict__ blk_row,
+                                                   const int* __restrict__ blk_ct, const int* __restrict__ blk_cr,
+                                                   int* __restrict__ sec_ptr, SetupSummary* sum) {
+  __shared__ long long s_b[1024];
+  const int b = threadIdx.x;
+  long long by = 0;
+  if (b < G) {
+    const int u0 = upos[seg_beg[b]];
+    const int u1 = (seg_end[b] < NSELL) ? upos[seg_end[b]] : upos[NSELL - 1] + flag[NSELL - 1];
+    sec_ptr[b] = u0;
+    if (b == G - 1) sec_ptr[G] = u1;
+    const int R = blk_row[b + 1] - blk_row[b];
+    by = (long long)ResLayout(seg_end[b] - seg_beg[b], R, blk_ct[b + 1] - blk_ct[b], blk_cr[b], u1 - u0).total;
+  }
+  s_b[b] = by;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (b < o) s_b[b] = max(s_b[b], s_b[b + o]);
+    __syncthreads();
+  }
+  if (b == 0) sum->max_res_bytes = s_b[0];
 }
 
 __global__ void k_iota(int64_t n, int* v) {
@@ -599,8 +681,8 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.pos_len), P<int64_t>(ws.pos_ptr), n + 1,
                                         st));
   k_summary<<<1, kFixThreads, 0, st>>>(n, G, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int64_t>(ws.pos_ptr),
-                             P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr), P<int>(ws.flags),
-                             P<SetupSummary>(ws.summary));
+                             P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr), P<int>(ws.blk_slice),
+                             P<int>(ws.flags), P<SetupSummary>(ws.summary));
   launches += 3;
   launches += 3;
   VFPI_CK(cudaGetLastError());
@@ -638,52 +720,62 @@ int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const 
                                             P<int>(ws.vals), P<int>(ws.perm), (int)nnz, 0, eb, st));
     launches += 3 + (eb + 7) / 8;  // iota, histogram, exclusive-sum, one onesweep pass per 8 key bits
   }
-  (void)G;
+  VFPI_CK(ensure(ws.sell_val, 8 * (size_t)std::max<int64_t>(hs.sell_elems, 1)));
+  VFPI_CK(ensure(ws.sell_col, 4 * (size_t)std::max<int64_t>(hs.sell_elems, 1)));
+  if (S > 0) {
+    k_pack<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row),
+                                                  P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr),
+                                                  P<int>(ws.perm), P<int>(ws.colof), s.data,
+                                                  P<int64_t>(ws.slice_off), P<double>(ws.sell_val),
+                                                  P<int>(ws.sell_col));
+    ++launches;
+  }
   if (resident) {
-    const int64_t nn = hs.nnz_num;
-    VFPI_CK(ensure(ws.pk_val, 8 * (size_t)nn));
-    VFPI_CK(ensure(ws.pk_col, 4 * (size_t)nn));
-    VFPI_CK(ensure(ws.ps_col, 4 * (size_t)nn));
-    VFPI_CK(ensure(ws.ps_src, 4 * (size_t)nn));
+    const int64_t NS = hs.sell_elems;
+    VFPI_CK(ensure(ws.rowpos, 4 * (size_t)std::max(n, 1)));
+    VFPI_CK(ensure(ws.sec_key, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.sec_skey, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.sec_idx, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.sec_sidx, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.sec_flag, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.sec_upos, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.sell_map, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.secs, 4 * (size_t)std::max<int64_t>(NS, 1)));
+    VFPI_CK(ensure(ws.sec_ptr, 4 * (size_t)(G + 1)));
     VFPI_CK(ensure(ws.seg_beg, 4 * (size_t)G));
     VFPI_CK(ensure(ws.seg_end, 4 * (size_t)G));
-    if (n > 0) {
-      k_pack_csr<<<nblk(n, 128), 128, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr),
-                                               P<int64_t>(ws.pos_ptr), P<int>(ws.perm), P<int>(ws.colof), s.data,
-                                               P<double>(ws.pk_val), P<int>(ws.pk_col));
-      ++launches;
-    }
-    VFPI_CK(ensure(ws.rowpos, 4 * (size_t)std::max(n, 1)));
     if (n > 0) {
       k_rowpos<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowpos));
       ++launches;
     }
-    if (nn > 0) {
-      // per CTA, entries re-ordered by column so the gathers of a warp hit few
-      // cache lines; ps_src remembers each entry's row-ordered slot
-      k_segments<<<nblk(G), 256, 0, st>>>(G, P<int64_t>(ws.pos_ptr), P<int>(ws.blk_row), P<int>(ws.seg_beg),
-                                          P<int>(ws.seg_end));
-      k_iota<<<nblk(nn), 256, 0, st>>>(nn, P<int>(ws.vals));
-      size_t ts = 0;
-      cub::DeviceSegmentedSort::SortPairs(nullptr, ts, P<int>(ws.pk_col), P<int>(ws.ps_col), P<int>(ws.vals),
-                                          P<int>(ws.ps_src), (int)nn, G, P<int>(ws.seg_beg), P<int>(ws.seg_end), st);
-      VFPI_CK(ensure(ws.cub_tmp, ts));
+    VFPI_CK(cudaMemsetAsync(ws.sec_ptr.p, 0, 4 * (size_t)(G + 1), st));
+    if (NS > 0) {
+      k_sell_segments<<<nblk(G), 256, 0, st>>>(G, P<int64_t>(ws.slice_off), P<int>(ws.blk_slice), P<int>(ws.seg_beg),
+                                               P<int>(ws.seg_end));
+      k_sec_keys<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row),
+                                                        P<int64_t>(ws.slice_off), P<int>(ws.sell_col),
+                                                        P<int>(ws.rowpos), P<unsigned>(ws.sec_key), P<int>(ws.sec_idx),
+                                                        P<unsigned>(ws.sell_map));
+      size_t ts = 0, tsc = 0;
+      cub::DeviceSegmentedSort::SortPairs(nullptr, ts, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey),
+                                          P<int>(ws.sec_idx), P<int>(ws.sec_sidx), (int)NS, G, P<int>(ws.seg_beg),
+                                          P<int>(ws.seg_end), st);
+      cub::DeviceScan::ExclusiveSum(nullptr, tsc, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)NS, st);
+      VFPI_CK(ensure(ws.cub_tmp, std::max(ts, tsc)));
       size_t tb = ws.cub_tmp.cap;
-      VFPI_CK(cub::DeviceSegmentedSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.pk_col), P<int>(ws.ps_col),
-                                                  P<int>(ws.vals), P<int>(ws.ps_src), (int)nn, G, P<int>(ws.seg_beg),
-                                                  P<int>(ws.seg_end), st));
-      launches += 4;
-    }
-  } else {
-    VFPI_CK(ensure(ws.sell_val, 8 * (size_t)hs.sell_elems));
-    VFPI_CK(ensure(ws.sell_col, 4 * (size_t)hs.sell_elems));
-    if (S > 0) {
-      k_pack<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row),
-                                                    P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr),
-                                                    P<int>(ws.perm), P<int>(ws.colof), s.data,
-                                                    P<int64_t>(ws.slice_off), P<double>(ws.sell_val),
-                                                    P<int>(ws.sell_col));
-      ++launches;
+      VFPI_CK(cub::DeviceSegmentedSort::SortPairs(ws.cub_tmp.p, tb, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey),
+                                                  P<int>(ws.sec_idx), P<int>(ws.sec_sidx), (int)NS, G,
+                                                  P<int>(ws.seg_beg), P<int>(ws.seg_end), st));
+      k_sec_flags<<<nblk(NS), 256, 0, st>>>(NS, G, P<int>(ws.seg_beg), P<unsigned>(ws.sec_skey), P<int>(ws.sec_flag));
+      VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)NS,
+                                            st));
+      k_sec_emit<<<nblk(NS), 256, 0, st>>>(NS, G, P<int>(ws.seg_beg), P<unsigned>(ws.sec_skey), P<int>(ws.sec_sidx),
+                                           P<int>(ws.sec_flag), P<int>(ws.sec_upos), P<int>(ws.sell_col),
+                                           P<unsigned>(ws.secs), P<unsigned>(ws.sell_map));
+      k_summary2<<<1, 1024, 0, st>>>(G, NS, P<int>(ws.seg_beg), P<int>(ws.seg_end), P<int>(ws.sec_upos),
+                                     P<int>(ws.sec_flag), P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr),
+                                     P<int>(ws.sec_ptr), P<SetupSummary>(ws.summary));
+      launches += 10;
     }
   }
   VFPI_CK(cudaGetLastError());

@@ -38,3 +38,8 @@ print("work (pre-barrier) per CTA: mean", work.mean(), "max", work.max(), "argma
 arr = a[:, :, 7]
 print("arrival skew (globaltimer ns) per iteration:", (arr.max(0) - arr.min(0)).tolist())
 h.L.vfpi_set_profile(h.h, 0)
+for wc in (2, 4, 6, 8, 10, 12, 14):
+    h.L.vfpi_set_tuning(h.h, 0, wc)
+    v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
+    print(f"WC={wc:2d} loop_ms {rep.timings['loop_s'] * 1e3:.3f}")
+h.L.vfpi_set_tuning(h.h, 0, 0)
