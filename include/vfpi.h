@@ -127,7 +127,9 @@ int vfpi_set_kernel(vfpi_handle* h, int mode);
  * phase starts 0..5, globaltimer at 7); vfpi_get_profile copies them out. */
 int vfpi_set_profile(vfpi_handle* h, int iter0);
 int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
-/* Tuning knobs (key 0: force the resident kernel's contact-warp count, 0 = auto). */
+/* Tuning knobs. key 0: force the resident kernel's contact-warp count (0 = auto);
+ * key 1: order units by their smallest referenced column (default 0 = row order);
+ * key 2: sort each CTA's free rows by decreasing length (default 1). */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

@@ -41,6 +41,7 @@ struct vfpi_handle {
   int kernel_mode = 0;  // 0 auto, 1 force shared-memory resident, 2 force streaming
   int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
   int tune_wc = 0;      // >0: force the contact-warp count of the resident kernel
+  vfpi::LayoutOptions layout_opt;
   int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
@@ -183,7 +184,8 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.cposc, &h->ws.cposf, &h->ws.blk_first, &h->ws.blk_cr, &h->ws.cont_q,
                             &h->ws.ps_col, &h->ws.ps_src, &h->ws.seg_beg, &h->ws.seg_end, &h->ws.rowpos, &h->ws.sec_key,
                             &h->ws.sec_skey, &h->ws.sec_idx, &h->ws.sec_sidx, &h->ws.sec_flag, &h->ws.sec_upos,
-                            &h->ws.sell_map, &h->ws.secs, &h->ws.sec_ptr, &h->ws.vbuf,
+                            &h->ws.sell_map, &h->ws.secs, &h->ws.sec_ptr, &h->ws.rowmin, &h->ws.ukey, &h->ws.ukey_s,
+                            &h->ws.uval, &h->ws.uorder, &h->ws.row_list2, &h->ws.row_slot2, &h->ws.vbuf,
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
                             &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
   for (auto* b : bufs)
@@ -204,6 +206,8 @@ int64_t vfpi_launch_count(const vfpi_handle* h) { return h ? h->launches : 0; }
 int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (!h) return VFPI_BAD_ARGUMENT;
   if (key == 0) { h->tune_wc = value; return VFPI_OK; }
+  if (key == 1) { h->layout_opt.anchor_order = value != 0; return VFPI_OK; }
+  if (key == 2) { h->layout_opt.length_sort = value != 0; return VFPI_OK; }
   return VFPI_BAD_ARGUMENT;
 }
 
@@ -266,7 +270,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   vfpi::SetupSummary* hs = ws.h_summary;
   // first choice: the whole partition of every CTA resident in shared memory
   int G = choose_blocks_resident(*d, ws.num_sms);
-  rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches);
+  rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches, h->layout_opt);
   if (rc) return rc;
   const size_t smem_res = (size_t)hs->max_res_bytes;
   const bool fits = hs->max_ent_per_blk < (1 << 24) && smem_res + 2048 <= (size_t)ws.max_smem_optin && G <= 256;
@@ -276,7 +280,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   if (!resident) {
     G = choose_blocks(*d, ws.num_sms);
     for (int attempt = 0; attempt < 4; ++attempt) {
-      rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches);
+      rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches, h->layout_opt);
       if (rc) return rc;
       smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
       const int bps = vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem);
@@ -287,18 +291,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   }
   rc = vfpi::setup_pack(ws, *d, G, resident, *hs, st, h->err, h->launches);
   if (rc) return rc;
-  size_t smem_res_full = 0;
-  if (resident) {
-    // second read: the staged-sector count is known only after packing
-    CK(cudaMemcpyAsync(hs, ws.summary.p, sizeof(vfpi::SetupSummary), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    smem_res_full = (size_t)hs->max_res_bytes;
-    if (smem_res_full + 2048 > (size_t)ws.max_smem_optin) {
-      if (h->kernel_mode == 1) { h->err = "partition does not fit in shared memory"; return VFPI_UNSUPPORTED; }
-      resident = false;  // SELL-32 slices are packed for both kernels: stream instead
-      smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
-    }
-  }
+  const size_t smem_res_full = smem_res;
   rc = vfpi::setup_step_matrix(ws, *d, *cfg, w_cached, st, h->err, h->launches);
   if (rc) return rc;
 

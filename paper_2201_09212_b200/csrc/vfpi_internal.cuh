@@ -127,8 +127,12 @@ struct Workspace;  // device buffers owned by a handle
 
 // Layout setup on the stream: statistics, contact-aware CTA partition and
 // sizes (ends with one host read of the summary). Returns VFPI_* code.
+struct LayoutOptions {
+  bool anchor_order = false;  // order units by their smallest referenced column
+  bool length_sort = true;    // free rows of a CTA by decreasing length
+};
 int setup_layout(Workspace& ws, const vfpi_system& dsys, int G, cudaStream_t st, SetupSummary* host_summary,
-                 std::string& err, int64_t& launches);
+                 std::string& err, int64_t& launches, const LayoutOptions& opt = LayoutOptions());
 // Row-sorted entries packed for the chosen iteration kernel:
 // resident = CTA-contiguous CSR (pos_ptr/pk_val/pk_col), else SELL-32.
 int setup_pack(Workspace& ws, const vfpi_system& dsys, int G, bool resident, const SetupSummary& hs,
@@ -174,6 +178,7 @@ struct Workspace {
   Buf slice_w, slice_off, sell_val, sell_col, pos_len, pos_ptr, pk_val, pk_col, bar_flags;
   Buf ucr, ufr, cposc, cposf, blk_first, blk_cr, cont_q, ps_col, ps_src, seg_beg, seg_end, rowpos;
   Buf sec_key, sec_skey, sec_idx, sec_sidx, sec_flag, sec_upos, sell_map, secs, sec_ptr;
+  Buf rowmin, ukey, ukey_s, uval, uorder, row_list2, row_slot2;
   Buf vbuf, lambuf, partials, status, summary, flags, cub_tmp;
   Buf x, y;  // scratch for per-op entry points
   Buf prof;
@@ -183,6 +188,7 @@ struct Workspace {
   SolveStatus* h_status = nullptr;    // pinned
   int num_sms = 148;
   int max_smem_optin = 232448;
+  bool unit_order_is_sorted = false;
 };
 
 cudaError_t ensure(Workspace::Buf& b, size_t bytes);

@@ -58,7 +58,8 @@ struct PrunedSquares {
 
 __global__ void k_colstats(int n, const int* __restrict__ indptr, const int* __restrict__ indices,
                            const double* __restrict__ data, double* __restrict__ diag, double* __restrict__ rns,
-                           int* __restrict__ rowcnt, int* __restrict__ keys, int* __restrict__ colof) {
+                           int* __restrict__ rowcnt, int* __restrict__ keys, int* __restrict__ colof,
+                           int* __restrict__ rowmin) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int e0 = indptr[j], e1 = indptr[j + 1];
@@ -72,7 +73,10 @@ __global__ void k_colstats(int n, const int* __restrict__ indptr, const int* __r
     const bool num = (d != 0.0);
     keys[e] = num ? i : n;
     colof[e] = j;
-    if (num) atomicAdd(&rowcnt[i], 1);
+    if (num) {
+      atomicAdd(&rowcnt[i], 1);
+      atomicMin(&rowmin[i], j);
+    }
   }
   diag[j] = dg;
   double r = 0.0;
@@ -97,32 +101,64 @@ __global__ void k_mark(int n, int n_c, const int* __restrict__ ci, const int* __
       if (atomicCAS(&mark[j + t], -1, m) != -1) atomicOr(flags, 1);
 }
 
-// unit = one free row, or all (3 or 6) rows of one contact, anchored at col_i
-__global__ void k_units(int n, const int* __restrict__ mark, const int* __restrict__ ci, const int* __restrict__ cj,
-                        const int* __restrict__ rowcnt, int64_t* ucost, int* urows, int* ucont, int* ucr, int* ufr) {
+// unit = one free row, or all (3 or 6) rows of one contact, anchored at col_i.
+// Units are ordered by their anchor = the smallest column any of their rows
+// touches (stable in row order): a unit then sits next to the rows it couples
+// to (a rigid body's virtual nodes next to the body, FEM rows stay banded), so
+// a CTA range reads few remote sectors of v.
+__global__ void k_unit_keys(int n, const int* __restrict__ mark, const int* __restrict__ ci,
+                            const int* __restrict__ cj, const int* __restrict__ rowmin, int* __restrict__ key,
+                            int* __restrict__ val, int anchor) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int m = mark[r];
-  int64_t cost = 0;
-  int rows = 0, ct = 0;
+  int k = INT_MAX;
   if (m < 0) {
-    cost = (int64_t)kEntryCost * rowcnt[r] + kRowCost;
-    rows = 1;
+    k = min(r, rowmin[r]);
   } else if (r == ci[m]) {
     const int i = ci[m], j = cj[m];
-    ct = 1;
-    rows = (j >= 0) ? 6 : 3;
-    cost = kContactCost;
-    for (int t = 0; t < 3; ++t) cost += (int64_t)kEntryCost * rowcnt[i + t] + kRowCost;
-    if (j >= 0)
-      for (int t = 0; t < 3; ++t) cost += (int64_t)kEntryCost * rowcnt[j + t] + kRowCost;
+    k = i;
+    for (int t = 0; t < 3; ++t) k = min(k, rowmin[i + t]);
+    if (j >= 0) {
+      k = min(k, j);
+      for (int t = 0; t < 3; ++t) k = min(k, rowmin[j + t]);
+    }
   }
-  ucost[r] = cost;
-  urows[r] = rows;
-  ucont[r] = ct;
-  ucr[r] = ct ? rows : 0;          // rows of a contact unit
-  ufr[r] = (rows == 1 && !ct) ? 1 : 0;  // a free row
-  if (r == n - 1) { ucr[n] = 0; ufr[n] = 0; }
+  key[r] = (k == INT_MAX || anchor) ? k : r;  // natural order: the start row itself
+  val[r] = r;
+}
+
+// per sorted unit t (anchor order): cost / rows / contact indicators
+__global__ void k_units(int n, const int* __restrict__ skey, const int* __restrict__ U, const int* __restrict__ mark,
+                        const int* __restrict__ ci, const int* __restrict__ cj, const int* __restrict__ rowcnt,
+                        int64_t* ucost, int* urows, int* ucont, int* ucr, int* ufr) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > n) return;
+  int64_t cost = 0;
+  int rows = 0, ct = 0;
+  if (t < n && skey[t] != INT_MAX) {
+    const int r = U[t];
+    const int m = mark[r];
+    if (m < 0) {
+      cost = (int64_t)kEntryCost * rowcnt[r] + kRowCost;
+      rows = 1;
+    } else {
+      const int i = ci[m], j = cj[m];
+      ct = 1;
+      rows = (j >= 0) ? 6 : 3;
+      cost = kContactCost;
+      for (int q = 0; q < 3; ++q) cost += (int64_t)kEntryCost * rowcnt[i + q] + kRowCost;
+      if (j >= 0)
+        for (int q = 0; q < 3; ++q) cost += (int64_t)kEntryCost * rowcnt[j + q] + kRowCost;
+    }
+  }
+  if (t < n) {
+    ucost[t] = cost;
+    urows[t] = rows;
+    ucont[t] = ct;
+  }
+  ucr[t] = ct ? rows : 0;                // rows of a contact unit
+  ufr[t] = (rows == 1 && !ct) ? 1 : 0;   // a free row
 }
 
 __global__ void k_blocks(int n, int G, const int64_t* __restrict__ ucost, const int64_t* __restrict__ cpos,
@@ -135,7 +171,7 @@ __global__ void k_blocks(int n, int G, const int64_t* __restrict__ ucost, const 
   if (b > G - 1) b = G - 1;
   atomicMin(&blk_row[b], rpos[r]);
   atomicMin(&blk_ct[b], kpos[r]);
-  atomicMin(&blk_first[b], r);
+  atomicMin(&blk_first[b], r);  // r is the sorted unit index t here
 }
 
 // one CTA of kFixThreads threads, G <= kFixThreads: fill empty CTA ranges with
@@ -213,40 +249,64 @@ __device__ __forceinline__ int owner(const int* __restrict__ starts, int G, int 
 }
 
 // Row list: within every CTA range, the rows of its contact units come first
-// (unit order), then its free rows (natural order). cont_q = local position
-// of each contact's first row.
-__global__ void k_fill(int n, int G, const int* __restrict__ mark, const int* __restrict__ ci,
-                       const int* __restrict__ cj, const int* __restrict__ urows, const int* __restrict__ rpos,
-                       const int* __restrict__ kpos, const int* __restrict__ cposc, const int* __restrict__ cposf,
-                       const int* __restrict__ blk_row, const int* __restrict__ blk_ct,
+// (unit order), then its free rows (unit order). cont_q = local position of
+// each contact's first row. t = sorted unit index, U[t] = its start row.
+__global__ void k_fill(int n, int G, const int* __restrict__ U, const int* __restrict__ mark,
+                       const int* __restrict__ ci, const int* __restrict__ cj, const int* __restrict__ urows,
+                       const int* __restrict__ rpos, const int* __restrict__ kpos, const int* __restrict__ cposc,
+                       const int* __restrict__ cposf, const int* __restrict__ blk_row, const int* __restrict__ blk_ct,
                        const int* __restrict__ blk_first, const int* __restrict__ blk_cr, int* row_list, int* row_slot,
                        int* cont_list, int* cont_q) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n || urows[r] == 0) return;
-  const int b = owner(blk_row, G, rpos[r]);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n || urows[t] == 0) return;
+  const int r = U[t];
+  const int b = owner(blk_row, G, rpos[t]);
   const int f = blk_first[b];
   const int m = mark[r];
   if (m < 0) {
-    const int p = blk_row[b] + blk_cr[b] + (cposf[r] - cposf[f]);
+    const int p = blk_row[b] + blk_cr[b] + (cposf[t] - cposf[f]);
     row_list[p] = r;
     row_slot[p] = -1;
     return;
   }
-  const int p = blk_row[b] + (cposc[r] - cposc[f]);
-  const int k = kpos[r];
+  const int p = blk_row[b] + (cposc[t] - cposc[f]);
+  const int k = kpos[t];
   const int loc = (k - blk_ct[b]) * kSlotsPerContact;
   cont_list[k] = m;
   cont_q[k] = p - blk_row[b];
   const int i = ci[m], j = cj[m];
-  for (int t = 0; t < 3; ++t) {
-    row_list[p + t] = i + t;
-    row_slot[p + t] = loc + t;
+  for (int q = 0; q < 3; ++q) {
+    row_list[p + q] = i + q;
+    row_slot[p + q] = loc + q;
   }
   if (j >= 0)
-    for (int t = 0; t < 3; ++t) {
-      row_list[p + 3 + t] = j + t;
-      row_slot[p + 3 + t] = loc + 3 + t;
+    for (int q = 0; q < 3; ++q) {
+      row_list[p + 3 + q] = j + q;
+      row_slot[p + 3 + q] = loc + 3 + q;
     }
+}
+
+// Within every CTA, free rows are re-ordered by decreasing length (contact
+// rows stay first and in place): SELL-32 slices then group rows of equal
+// length, so padding and warp divergence of the row sums stay small.
+__global__ void k_row_keys(int n, int G, const int* __restrict__ row_list, const int* __restrict__ row_slot,
+                           const int* __restrict__ rowcnt, const int* __restrict__ blk_row, int* __restrict__ key,
+                           int* __restrict__ val) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int b = owner(blk_row, G, p);
+  const int len = min(rowcnt[row_list[p]], 255);
+  key[p] = (b << 9) | (row_slot[p] < 0 ? (256 | (255 - len)) : 0);
+  val[p] = p;
+}
+
+__global__ void k_row_permute(int n, const int* __restrict__ perm, const int* __restrict__ row_list,
+                              const int* __restrict__ row_slot, int* __restrict__ row_list2,
+                              int* __restrict__ row_slot2) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  row_list2[p] = row_list[perm[p]];
+  row_slot2[p] = row_slot[perm[p]];
 }
 
 __global__ void k_slice_width(int S_max, int G, const SetupSummary* __restrict__ sum,
@@ -273,7 +333,8 @@ __global__ void k_poslen(int n, const int* __restrict__ row_list, const int* __r
 __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int64_t* row_ptr,
                                                           const int64_t* slice_off, const int64_t* pos_ptr,
                                                           const int* blk_row, const int* blk_ct, const int* blk_cr,
-                                                          const int* blk_slice, const int* flags, SetupSummary* sum) {
+                                                          const int* blk_slice, const int* sec_ptr, const int* flags,
+                                                          SetupSummary* sum) {
   __shared__ long long s_e[kFixThreads], s_b[kFixThreads];
   __shared__ int s_r[kFixThreads];
   const int b = threadIdx.x;
@@ -283,7 +344,7 @@ __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int
     e = pos_ptr[blk_row[b + 1]] - pos_ptr[blk_row[b]];
     r = blk_row[b + 1] - blk_row[b];
     const int64_t ep = slice_off[blk_slice[b + 1]] - slice_off[blk_slice[b]];
-    by = (long long)ResLayout(ep, r, blk_ct[b + 1] - blk_ct[b], blk_cr[b], 0).total;
+    by = (long long)ResLayout(ep, r, blk_ct[b + 1] - blk_ct[b], blk_cr[b], sec_ptr[b + 1] - sec_ptr[b]).total;
   }
   s_e[b] = e;
   s_b[b] = by;
@@ -307,115 +368,100 @@ __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int
   }
 }
 
+// ---- gather plan of the resident kernel -------------------------------------
+// Every CTA stages, once per iteration, the 32-byte sectors of v its entries
+// read from other CTAs' rows; columns that are its own rows read the on-chip
+// copy. Built in phase 1 from the CSC entries (so the shared-memory size is
+// known at the single host read): key = (cta << 24) | sector, radix sorted,
+// first-of-run flags -> block-major unique sector list secs + per-CTA ranges.
+// sell_map[i] (phase 2) encodes where SELL element i's x comes from:
+//   0x80000000 | q  -> own row q (local position),  else 4*slot + (col & 3).
+constexpr unsigned kOwnBit = 0x80000000u;
+constexpr unsigned kNoSector = 0xFFFFFFFFu;
+
 __global__ void k_rowpos(int n, const int* __restrict__ row_list, int* __restrict__ rowpos) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) rowpos[row_list[q]] = q;
 }
 
-// ---- gather plan of the resident kernel -------------------------------------
-// Every CTA stages, once per iteration, the 32-byte sectors of v its SELL
-// entries read from other CTAs' rows; columns that are its own rows read the
-// on-chip copy. sell_map[i] encodes where entry i's x comes from:
-//   0x80000000 | q  -> own row q (local position),  else 4*slot + (col & 3).
-constexpr unsigned kOwnBit = 0x80000000u;
-constexpr unsigned kNoSector = 0xFFFFFFFFu;
-
-__global__ void k_sell_segments(int G, const int64_t* __restrict__ slice_off, const int* __restrict__ blk_slice,
-                                int* beg, int* end) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= G) return;
-  beg[b] = (int)slice_off[blk_slice[b]];
-  end[b] = (int)slice_off[blk_slice[b + 1]];
+// per CSC entry (thread per column): sector key of a numeric entry whose row's
+// CTA does not own its column
+__global__ void k_sec_keys(int n, int G, const int* __restrict__ indptr, const int* __restrict__ indices,
+                           const double* __restrict__ data, const int* __restrict__ rowpos,
+                           const int* __restrict__ blk_row, unsigned* __restrict__ key) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int pj = rowpos[j];
+  for (int e = indptr[j]; e < indptr[j + 1]; ++e) {
+    unsigned k = kNoSector;
+    if (data[e] != 0.0) {
+      const int b = owner(blk_row, G, rowpos[indices[e]]);
+      if (pj < blk_row[b] || pj >= blk_row[b + 1]) k = ((unsigned)b << 24) | ((unsigned)j >> 2);
+    }
+    key[e] = k;
+  }
 }
 
-// warp per slice: sector key of every SELL element (kNoSector for padding/own)
-__global__ void k_sec_keys(int S, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_row,
+__global__ void k_sec_flags(int64_t N, const unsigned* __restrict__ skey, int* __restrict__ flag) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const unsigned k = skey[j];
+  flag[j] = (k != kNoSector && (j == 0 || skey[j - 1] != k)) ? 1 : 0;
+}
+
+// unique sector list (sector ids) and the first unique index of every CTA
+__global__ void k_sec_emit(int64_t N, const unsigned* __restrict__ skey, const int* __restrict__ flag,
+                           const int* __restrict__ upos, unsigned* __restrict__ secs, int* __restrict__ sec_ptr) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= N || !flag[j]) return;
+  const unsigned k = skey[j];
+  secs[upos[j]] = k & 0xFFFFFFu;
+  const int b = (int)(k >> 24);
+  if (j == 0 || (skey[j - 1] >> 24) != (unsigned)b || skey[j - 1] == kNoSector) sec_ptr[b] = upos[j];
+}
+
+// CTAs without remote sectors inherit the next start; sec_ptr[G] = total
+__global__ void k_sec_ptr_fix(int G, int64_t N, const int* __restrict__ flag, const int* __restrict__ upos,
+                              int* __restrict__ sec_ptr) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  sec_ptr[G] = N > 0 ? upos[N - 1] + flag[N - 1] : 0;
+  for (int b = G - 1; b >= 0; --b)
+    if (sec_ptr[b] < 0) sec_ptr[b] = sec_ptr[b + 1];
+}
+
+// warp per slice: gather map of every SELL element
+__global__ void k_sell_map(int S, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_row,
                            const int64_t* __restrict__ slice_off, const int* __restrict__ sell_col,
-                           const int* __restrict__ rowpos, unsigned* __restrict__ key, int* __restrict__ idx,
-                           unsigned* __restrict__ map) {
+                           const int* __restrict__ rowpos, const unsigned* __restrict__ secs,
+                           const int* __restrict__ sec_ptr, unsigned* __restrict__ map) {
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= S) return;
   const int b = owner(blk_slice, G, s);
   const int p0 = blk_row[b], p1 = blk_row[b + 1];
+  const int u0 = sec_ptr[b], u1 = sec_ptr[b + 1];
   const int64_t off = slice_off[s];
   const int W = (int)((slice_off[s + 1] - off) >> 5);
   for (int k = 0; k < W; ++k) {
     const int64_t i = off + (int64_t)k * 32 + lane;
     const int c = sell_col[i];
-    unsigned kk = kNoSector;
+    unsigned m = 0u;
     if (c >= 0) {
       const int pc = rowpos[c];
-      if (pc >= p0 && pc < p1) map[i] = kOwnBit | (unsigned)(pc - p0);
-      else kk = (unsigned)c >> 2;
-    } else {
-      map[i] = 0u;
+      if (pc >= p0 && pc < p1) {
+        m = kOwnBit | (unsigned)(pc - p0);
+      } else {
+        const unsigned sec = (unsigned)c >> 2;
+        int lo = u0, hi = u1;  // first unique sector >= sec
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (secs[mid] < sec) lo = mid + 1; else hi = mid;
+        }
+        m = 4u * (unsigned)(lo - u0) + ((unsigned)c & 3u);
+      }
     }
-    key[i] = kk;
-    idx[i] = (int)i;
+    map[i] = m;
   }
-}
-
-// first element of every run of equal sector keys inside a CTA segment
-__global__ void k_sec_flags(int64_t N, int G, const int* __restrict__ seg_beg, const unsigned* __restrict__ skey,
-                            int* __restrict__ flag) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= N) return;
-  const unsigned k = skey[j];
-  int f = 0;
-  if (k != kNoSector) {
-    int lo = 0, hi = G;  // segment containing j (largest b with seg_beg[b] <= j)
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (seg_beg[mid] <= j) lo = mid; else hi = mid;
-    }
-    f = (j == seg_beg[lo] || skey[j - 1] != k) ? 1 : 0;
-  }
-  flag[j] = f;
-}
-
-__global__ void k_sec_emit(int64_t N, int G, const int* __restrict__ seg_beg, const unsigned* __restrict__ skey,
-                           const int* __restrict__ sidx, const int* __restrict__ flag, const int* __restrict__ upos,
-                           const int* __restrict__ sell_col, unsigned* __restrict__ secs, unsigned* __restrict__ map) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= N) return;
-  const unsigned k = skey[j];
-  if (k == kNoSector) return;
-  int lo = 0, hi = G;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (seg_beg[mid] <= j) lo = mid; else hi = mid;
-  }
-  const int u = upos[j] + flag[j] - 1;          // global unique id of this sector
-  const int base = upos[seg_beg[lo]];           // first unique id of the CTA
-  if (flag[j]) secs[u] = k;
-  const int i = sidx[j];
-  map[i] = 4u * (unsigned)(u - base) + ((unsigned)sell_col[i] & 3u);
-}
-
-__global__ void __launch_bounds__(1024) k_summary2(int G, int64_t NSELL, const int* __restrict__ seg_beg,
-                                                   const int* __restrict__ seg_end, const int* __restrict__ upos,
-                                                   const int* __restrict__ flag, const int* __restrict__ blk_row,
-                                                   const int* __restrict__ blk_ct, const int* __restrict__ blk_cr,
-                                                   int* __restrict__ sec_ptr, SetupSummary* sum) {
-  __shared__ long long s_b[1024];
-  const int b = threadIdx.x;
-  long long by = 0;
-  if (b < G) {
-    const int u0 = upos[seg_beg[b]];
-    const int u1 = (seg_end[b] < NSELL) ? upos[seg_end[b]] : upos[NSELL - 1] + flag[NSELL - 1];
-    sec_ptr[b] = u0;
-    if (b == G - 1) sec_ptr[G] = u1;
-    const int R = blk_row[b + 1] - blk_row[b];
-    by = (long long)ResLayout(seg_end[b] - seg_beg[b], R, blk_ct[b + 1] - blk_ct[b], blk_cr[b], u1 - u0).total;
-  }
-  s_b[b] = by;
-  __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
-    if (b < o) s_b[b] = max(s_b[b], s_b[b + o]);
-    __syncthreads();
-  }
-  if (b == 0) sum->max_res_bytes = s_b[0];
 }
 
 __global__ void k_iota(int64_t n, int* v) {
@@ -576,7 +622,7 @@ static int end_bit_for(int64_t v) {
 // Phase 1: column statistics, contact marks, partition into G CTAs, slice
 // widths. Ends with ONE host read of the summary (sizes + flags).
 int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, SetupSummary* hs, std::string& err,
-                 int64_t& launches) {
+                 int64_t& launches, const LayoutOptions& opt) {
   const int n = (int)s.n, n_c = (int)s.n_c;
   const int64_t nnz = s.nnz;
   VFPI_CK(ensure(ws.diag, 8 * (size_t)n));
@@ -593,6 +639,11 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   VFPI_CK(ensure(ws.ucont, 4 * (size_t)n));
   VFPI_CK(ensure(ws.kpos, 4 * (size_t)n));
   VFPI_CK(ensure(ws.ucr, 4 * (size_t)(n + 1)));
+  VFPI_CK(ensure(ws.rowmin, 4 * (size_t)std::max(n, 1)));
+  VFPI_CK(ensure(ws.ukey, 4 * (size_t)std::max(n, 1)));
+  VFPI_CK(ensure(ws.ukey_s, 4 * (size_t)std::max(n, 1)));
+  VFPI_CK(ensure(ws.uval, 4 * (size_t)std::max(n, 1)));
+  VFPI_CK(ensure(ws.uorder, 4 * (size_t)std::max(n, 1)));
   VFPI_CK(ensure(ws.ufr, 4 * (size_t)(n + 1)));
   VFPI_CK(ensure(ws.cposc, 4 * (size_t)(n + 1)));
   VFPI_CK(ensure(ws.cposf, 4 * (size_t)(n + 1)));
@@ -624,6 +675,7 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   size_t tb = ws.cub_tmp.cap;
 
   VFPI_CK(cudaMemsetAsync(ws.rowcnt.p, 0, 4 * (size_t)(n + 1), st));
+  VFPI_CK(cudaMemsetAsync(ws.rowmin.p, 0x7f, 4 * (size_t)std::max(n, 1), st));  // ~INT_MAX
   VFPI_CK(cudaMemsetAsync(ws.mark.p, 0xff, 4 * (size_t)n, st));
   VFPI_CK(cudaMemsetAsync(ws.flags.p, 0, 16, st));
   VFPI_CK(cudaMemsetAsync(ws.summary.p, 0, sizeof(SetupSummary), st));
@@ -633,7 +685,7 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   launches += 3;
   if (n > 0) {
     k_colstats<<<nblk(n), 256, 0, st>>>(n, s.indptr, s.indices, s.data, P<double>(ws.diag), P<double>(ws.rns),
-                                        P<int>(ws.rowcnt), P<int>(ws.keys), P<int>(ws.colof));
+                                        P<int>(ws.rowcnt), P<int>(ws.keys), P<int>(ws.colof), P<int>(ws.rowmin));
     ++launches;
   }
   if (n_c > 0) {
@@ -644,8 +696,27 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.rowcnt), P<int64_t>(ws.row_ptr), n + 1, st));
   ++launches;
   if (n > 0) {
-    k_units<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.rowcnt), P<int64_t>(ws.ucost),
-                                     P<int>(ws.urows), P<int>(ws.ucont), P<int>(ws.ucr), P<int>(ws.ufr));
+    k_unit_keys<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.rowmin), P<int>(ws.ukey),
+                                         P<int>(ws.uval), opt.anchor_order ? 1 : 0);
+    // natural order: keys are already the start rows (non-starts = INT_MAX stay
+    // interleaved as empty units), so only the anchor order needs a sort
+    int* skey = P<int>(ws.ukey);
+    int* uord = P<int>(ws.uval);
+    if (opt.anchor_order) {
+      size_t tu = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tu, P<int>(ws.ukey), P<int>(ws.ukey_s), P<int>(ws.uval),
+                                      P<int>(ws.uorder), n, 0, 32, st);
+      VFPI_CK(ensure(ws.cub_tmp, tu));
+      tb = ws.cub_tmp.cap;
+      VFPI_CK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.ukey), P<int>(ws.ukey_s), P<int>(ws.uval),
+                                              P<int>(ws.uorder), n, 0, 32, st));
+      skey = P<int>(ws.ukey_s);
+      uord = P<int>(ws.uorder);
+    }
+    ws.unit_order_is_sorted = opt.anchor_order;
+    k_units<<<nblk(n + 1), 256, 0, st>>>(n, skey, uord, P<int>(ws.mark), s.col_i, s.col_j,
+                                         P<int>(ws.rowcnt), P<int64_t>(ws.ucost), P<int>(ws.urows), P<int>(ws.ucont),
+                                         P<int>(ws.ucr), P<int>(ws.ufr));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), n, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.urows), P<int>(ws.rpos), n, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ucont), P<int>(ws.kpos), n, st));
@@ -663,13 +734,34 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
                                 P<SetupSummary>(ws.summary));
   ++launches;
   if (n > 0) {
-    k_fill<<<nblk(n), 256, 0, st>>>(n, G, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.urows), P<int>(ws.rpos),
+    k_fill<<<nblk(n), 256, 0, st>>>(n, G, opt.anchor_order ? P<int>(ws.uorder) : P<int>(ws.uval), P<int>(ws.mark),
+                                    s.col_i, s.col_j, P<int>(ws.urows),
+                                    P<int>(ws.rpos),
                                     P<int>(ws.kpos), P<int>(ws.cposc), P<int>(ws.cposf), P<int>(ws.blk_row),
                                     P<int>(ws.blk_ct), P<int>(ws.blk_first), P<int>(ws.blk_cr), P<int>(ws.row_list),
                                     P<int>(ws.row_slot), P<int>(ws.cont_list), P<int>(ws.cont_q));
     ++launches;
   }
   VFPI_CK(cudaGetLastError());
+  if (opt.length_sort && n > 0 && G <= 4096) {
+    VFPI_CK(ensure(ws.row_list2, 4 * (size_t)n));
+    VFPI_CK(ensure(ws.row_slot2, 4 * (size_t)n));
+    k_row_keys<<<nblk(n), 256, 0, st>>>(n, G, P<int>(ws.row_list), P<int>(ws.row_slot), P<int>(ws.rowcnt),
+                                        P<int>(ws.blk_row), P<int>(ws.ukey), P<int>(ws.uval));
+    size_t tr = 0;
+    const int eb = end_bit_for((int64_t)G << 9);
+    cub::DeviceRadixSort::SortPairs(nullptr, tr, P<int>(ws.ukey), P<int>(ws.ukey_s), P<int>(ws.uval),
+                                    P<int>(ws.uorder), n, 0, eb, st);
+    VFPI_CK(ensure(ws.cub_tmp, tr));
+    tb = ws.cub_tmp.cap;
+    VFPI_CK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.ukey), P<int>(ws.ukey_s), P<int>(ws.uval),
+                                            P<int>(ws.uorder), n, 0, eb, st));
+    k_row_permute<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.uorder), P<int>(ws.row_list), P<int>(ws.row_slot),
+                                           P<int>(ws.row_list2), P<int>(ws.row_slot2));
+    std::swap(ws.row_list, ws.row_list2);
+    std::swap(ws.row_slot, ws.row_slot2);
+    launches += 2 + 2 + (eb + 7) / 8;
+  }
   // slice count is data dependent but bounded by S_max; slices past the real
   // count get width 0, so one scan over S_max+1 entries suffices.
   k_slice_width<<<nblk(S_max + 1), 256, 0, st>>>(S_max, G, P<SetupSummary>(ws.summary), P<int>(ws.blk_slice),
@@ -680,9 +772,39 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   k_poslen<<<nblk(n + 1), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowcnt), P<int64_t>(ws.pos_len));
   VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.pos_len), P<int64_t>(ws.pos_ptr), n + 1,
                                         st));
+  // gather plan of the resident kernel (remote 32-byte sectors per CTA)
+  VFPI_CK(ensure(ws.rowpos, 4 * (size_t)std::max(n, 1)));
+  VFPI_CK(ensure(ws.sec_key, 4 * (size_t)std::max<int64_t>(nnz, 1)));
+  VFPI_CK(ensure(ws.sec_skey, 4 * (size_t)std::max<int64_t>(nnz, 1)));
+  VFPI_CK(ensure(ws.sec_flag, 4 * (size_t)std::max<int64_t>(nnz, 1)));
+  VFPI_CK(ensure(ws.sec_upos, 4 * (size_t)std::max<int64_t>(nnz, 1)));
+  VFPI_CK(ensure(ws.secs, 4 * (size_t)std::max<int64_t>(nnz, 1)));
+  VFPI_CK(ensure(ws.sec_ptr, 4 * (size_t)(G + 1)));
+  VFPI_CK(cudaMemsetAsync(ws.sec_ptr.p, 0xff, 4 * (size_t)(G + 1), st));
+  if (n > 0 && nnz > 0 && G <= 256 && n < (1 << 26)) {
+    k_rowpos<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowpos));
+    k_sec_keys<<<nblk(n), 256, 0, st>>>(n, G, s.indptr, s.indices, s.data, P<int>(ws.rowpos), P<int>(ws.blk_row),
+                                        P<unsigned>(ws.sec_key));
+    size_t tk = 0, tsc = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tk, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey), (int)nnz, 0, 32,
+                                   st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tsc, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)nnz, st);
+    VFPI_CK(ensure(ws.cub_tmp, std::max(tk, tsc)));
+    tb = ws.cub_tmp.cap;
+    VFPI_CK(cub::DeviceRadixSort::SortKeys(ws.cub_tmp.p, tb, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey),
+                                           (int)nnz, 0, 32, st));
+    k_sec_flags<<<nblk(nnz), 256, 0, st>>>(nnz, P<unsigned>(ws.sec_skey), P<int>(ws.sec_flag));
+    VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)nnz, st));
+    k_sec_emit<<<nblk(nnz), 256, 0, st>>>(nnz, P<unsigned>(ws.sec_skey), P<int>(ws.sec_flag), P<int>(ws.sec_upos),
+                                          P<unsigned>(ws.secs), P<int>(ws.sec_ptr));
+    k_sec_ptr_fix<<<1, 1, 0, st>>>(G, nnz, P<int>(ws.sec_flag), P<int>(ws.sec_upos), P<int>(ws.sec_ptr));
+    launches += 12;
+  } else {
+    VFPI_CK(cudaMemsetAsync(ws.sec_ptr.p, 0, 4 * (size_t)(G + 1), st));
+  }
   k_summary<<<1, kFixThreads, 0, st>>>(n, G, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int64_t>(ws.pos_ptr),
                              P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr), P<int>(ws.blk_slice),
-                             P<int>(ws.flags), P<SetupSummary>(ws.summary));
+                             P<int>(ws.sec_ptr), P<int>(ws.flags), P<SetupSummary>(ws.summary));
   launches += 3;
   launches += 3;
   VFPI_CK(cudaGetLastError());
@@ -731,51 +853,13 @@ int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const 
     ++launches;
   }
   if (resident) {
-    const int64_t NS = hs.sell_elems;
-    VFPI_CK(ensure(ws.rowpos, 4 * (size_t)std::max(n, 1)));
-    VFPI_CK(ensure(ws.sec_key, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.sec_skey, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.sec_idx, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.sec_sidx, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.sec_flag, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.sec_upos, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.sell_map, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.secs, 4 * (size_t)std::max<int64_t>(NS, 1)));
-    VFPI_CK(ensure(ws.sec_ptr, 4 * (size_t)(G + 1)));
-    VFPI_CK(ensure(ws.seg_beg, 4 * (size_t)G));
-    VFPI_CK(ensure(ws.seg_end, 4 * (size_t)G));
-    if (n > 0) {
-      k_rowpos<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowpos));
-      ++launches;
-    }
-    VFPI_CK(cudaMemsetAsync(ws.sec_ptr.p, 0, 4 * (size_t)(G + 1), st));
-    if (NS > 0) {
-      k_sell_segments<<<nblk(G), 256, 0, st>>>(G, P<int64_t>(ws.slice_off), P<int>(ws.blk_slice), P<int>(ws.seg_beg),
-                                               P<int>(ws.seg_end));
-      k_sec_keys<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row),
-                                                        P<int64_t>(ws.slice_off), P<int>(ws.sell_col),
-                                                        P<int>(ws.rowpos), P<unsigned>(ws.sec_key), P<int>(ws.sec_idx),
+    VFPI_CK(ensure(ws.sell_map, 4 * (size_t)std::max<int64_t>(hs.sell_elems, 1)));
+    if (S > 0) {
+      k_sell_map<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row),
+                                                        P<int64_t>(ws.slice_off), P<int>(ws.sell_col), P<int>(ws.rowpos),
+                                                        P<unsigned>(ws.secs), P<int>(ws.sec_ptr),
                                                         P<unsigned>(ws.sell_map));
-      size_t ts = 0, tsc = 0;
-      cub::DeviceSegmentedSort::SortPairs(nullptr, ts, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey),
-                                          P<int>(ws.sec_idx), P<int>(ws.sec_sidx), (int)NS, G, P<int>(ws.seg_beg),
-                                          P<int>(ws.seg_end), st);
-      cub::DeviceScan::ExclusiveSum(nullptr, tsc, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)NS, st);
-      VFPI_CK(ensure(ws.cub_tmp, std::max(ts, tsc)));
-      size_t tb = ws.cub_tmp.cap;
-      VFPI_CK(cub::DeviceSegmentedSort::SortPairs(ws.cub_tmp.p, tb, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey),
-                                                  P<int>(ws.sec_idx), P<int>(ws.sec_sidx), (int)NS, G,
-                                                  P<int>(ws.seg_beg), P<int>(ws.seg_end), st));
-      k_sec_flags<<<nblk(NS), 256, 0, st>>>(NS, G, P<int>(ws.seg_beg), P<unsigned>(ws.sec_skey), P<int>(ws.sec_flag));
-      VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)NS,
-                                            st));
-      k_sec_emit<<<nblk(NS), 256, 0, st>>>(NS, G, P<int>(ws.seg_beg), P<unsigned>(ws.sec_skey), P<int>(ws.sec_sidx),
-                                           P<int>(ws.sec_flag), P<int>(ws.sec_upos), P<int>(ws.sell_col),
-                                           P<unsigned>(ws.secs), P<unsigned>(ws.sell_map));
-      k_summary2<<<1, 1024, 0, st>>>(G, NS, P<int>(ws.seg_beg), P<int>(ws.seg_end), P<int>(ws.sec_upos),
-                                     P<int>(ws.sec_flag), P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr),
-                                     P<int>(ws.sec_ptr), P<SetupSummary>(ws.summary));
-      launches += 10;
+      ++launches;
     }
   }
   VFPI_CK(cudaGetLastError());

@@ -107,6 +107,46 @@ __global__ void fp64_lat(double* io, long long* out, int n) {
   if (threadIdx.x == 0) { out[0] = (t1 - t0) / n; out[1] = (t2 - t1) / n; out[2] = (t3 - t2) / n; out[3] = (t4 - t3) / n; }
 }
 
+// SELL row dots out of shared memory: 512 threads, rows of `len` entries,
+// x gathered at random smem offsets (like xs / vown in the resident kernel)
+__global__ void rowdot_bench(int len, int nx, long long* out, double* sink) {
+  extern __shared__ double smd[];
+  double* sv = smd;                          // [len*512]
+  unsigned* mp = (unsigned*)(sv + len * 512);  // [len*512]
+  double* xs = (double*)(mp + len * 512 + (len * 512) % 2);
+  const int T = blockDim.x, tid = threadIdx.x;
+  unsigned seed = 12345u + tid;
+  for (int i = tid; i < len * 512; i += T) {
+    seed = seed * 1664525u + 1013904223u;
+    sv[i] = 1.0 + (i & 7);
+    mp[i] = seed % nx;
+  }
+  for (int i = tid; i < nx; i += T) xs[i] = 0.5 * i;
+  __syncthreads();
+  double acc = 0.0;
+  long long t0 = clock64();
+  for (int rep = 0; rep < 16; ++rep) {
+    const int base = tid;
+    int k = 0;
+    for (; k + 4 <= len; k += 4) {
+      double a[4], x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + 512 * (k + u);
+        a[u] = sv[i];
+        x[u] = xs[mp[i]];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(a[u], x[u]));
+    }
+    for (; k < len; ++k) acc = __dadd_rn(acc, __dmul_rn(sv[base + 512 * k], xs[mp[base + 512 * k]]));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  sink[tid] = acc;
+  if (tid == 0) out[0] = (t1 - t0) / 16;
+}
+
 __global__ void chase(const unsigned* next, int steps, long long* out) {
   unsigned i = 0;
   long long t0 = clock64();
@@ -184,6 +224,18 @@ int main() {
     fp64_lat<<<1, 32>>>(io, d_out, 4096);
     cudaMemcpy(h.data(), d_out, 32, cudaMemcpyDeviceToHost);
     printf("fp64 dependent latency: DADD %lld, DMUL %lld, DDIV %lld, DSQRT(+DADD) %lld cycles\n", h[0], h[1], h[2], h[3]);
+  }
+  for (int len : {4, 16, 45}) {
+    double* sink;
+    cudaMalloc(&sink, 512 * 8);
+    const int nx = 3000;
+    const size_t smb = (size_t)len * 512 * 12 + 16 + nx * 8;
+    cudaFuncSetAttribute((void*)rowdot_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+    rowdot_bench<<<1, 512, smb>>>(len, nx, d_out, sink);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h.data(), d_out, 8, cudaMemcpyDeviceToHost);
+    printf("row dot from smem, 512 rows x %d entries: %lld cycles (%s)\n", len, h[0], cudaGetErrorString(cudaGetLastError()));
+    cudaFree(sink);
   }
   // (b) barrier only
   unsigned* d_ctr;
