@@ -185,7 +185,7 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.ps_col, &h->ws.ps_src, &h->ws.seg_beg, &h->ws.seg_end, &h->ws.rowpos, &h->ws.sec_key,
                             &h->ws.sec_skey, &h->ws.sec_idx, &h->ws.sec_sidx, &h->ws.sec_flag, &h->ws.sec_upos,
                             &h->ws.sell_map, &h->ws.secs, &h->ws.sec_ptr, &h->ws.rowmin, &h->ws.ukey, &h->ws.ukey_s,
-                            &h->ws.uval, &h->ws.uorder, &h->ws.row_list2, &h->ws.row_slot2, &h->ws.vbuf,
+                            &h->ws.uval, &h->ws.uorder, &h->ws.row_list2, &h->ws.row_slot2, &h->ws.rowblk, &h->ws.vbuf,
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
                             &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
   for (auto* b : bufs)

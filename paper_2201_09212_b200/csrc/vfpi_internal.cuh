@@ -178,7 +178,7 @@ struct Workspace {
   Buf slice_w, slice_off, sell_val, sell_col, pos_len, pos_ptr, pk_val, pk_col, bar_flags;
   Buf ucr, ufr, cposc, cposf, blk_first, blk_cr, cont_q, ps_col, ps_src, seg_beg, seg_end, rowpos;
   Buf sec_key, sec_skey, sec_idx, sec_sidx, sec_flag, sec_upos, sell_map, secs, sec_ptr;
-  Buf rowmin, ukey, ukey_s, uval, uorder, row_list2, row_slot2;
+  Buf rowmin, ukey, ukey_s, uval, uorder, row_list2, row_slot2, rowblk;
   Buf vbuf, lambuf, partials, status, summary, flags, cub_tmp;
   Buf x, y;  // scratch for per-op entry points
   Buf prof;

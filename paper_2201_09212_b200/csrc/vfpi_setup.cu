@@ -161,17 +161,29 @@ __global__ void k_units(int n, const int* __restrict__ skey, const int* __restri
   ufr[t] = (rows == 1 && !ct) ? 1 : 0;   // a free row
 }
 
+// CTA b starts at the unit whose cost range contains the first cost position
+// of block b (blk_of(c) = floor(c*G/total)): that unit writes the starts of
+// every CTA it opens (no atomics; a unit spanning several boundaries leaves the
+// earlier ones empty).
 __global__ void k_blocks(int n, int G, const int64_t* __restrict__ ucost, const int64_t* __restrict__ cpos,
                          const int* __restrict__ urows, const int* __restrict__ rpos, const int* __restrict__ kpos,
                          int* blk_row, int* blk_ct, int* blk_first) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n || urows[r] == 0) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n || urows[t] == 0) return;
   const int64_t total = cpos[n - 1] + ucost[n - 1];
-  int64_t b = total > 0 ? (cpos[r] * (int64_t)G) / total : 0;
-  if (b > G - 1) b = G - 1;
-  atomicMin(&blk_row[b], rpos[r]);
-  atomicMin(&blk_ct[b], kpos[r]);
-  atomicMin(&blk_first[b], r);  // r is the sorted unit index t here
+  if (total <= 0) return;
+  auto blk_of = [&](int64_t c) -> int64_t {  // block of cost position c (floor, c >= 0)
+    const int64_t b = (c * (int64_t)G) / total;
+    return b > G - 1 ? G - 1 : b;
+  };
+  // blocks whose first cost position lies inside this unit's cost range
+  const int64_t hi = blk_of(cpos[t] + ucost[t] - 1);
+  const int64_t lo = (cpos[t] == 0) ? -1 : blk_of(cpos[t] - 1);
+  for (int64_t b = lo + 1; b <= hi; ++b) {
+    blk_row[b] = rpos[t];
+    blk_ct[b] = kpos[t];
+    blk_first[b] = t;
+  }
 }
 
 // one CTA of kFixThreads threads, G <= kFixThreads: fill empty CTA ranges with
@@ -379,24 +391,28 @@ __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int
 constexpr unsigned kOwnBit = 0x80000000u;
 constexpr unsigned kNoSector = 0xFFFFFFFFu;
 
-__global__ void k_rowpos(int n, const int* __restrict__ row_list, int* __restrict__ rowpos) {
+__global__ void k_rowpos(int n, int G, const int* __restrict__ row_list, const int* __restrict__ blk_row,
+                         int* __restrict__ rowpos, int* __restrict__ rowblk) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) rowpos[row_list[q]] = q;
+  if (q >= n) return;
+  const int r = row_list[q];
+  rowpos[r] = q;
+  rowblk[r] = owner(blk_row, G, q);
 }
 
 // per CSC entry (thread per column): sector key of a numeric entry whose row's
 // CTA does not own its column
-__global__ void k_sec_keys(int n, int G, const int* __restrict__ indptr, const int* __restrict__ indices,
-                           const double* __restrict__ data, const int* __restrict__ rowpos,
-                           const int* __restrict__ blk_row, unsigned* __restrict__ key) {
+__global__ void k_sec_keys(int n, const int* __restrict__ indptr, const int* __restrict__ indices,
+                           const double* __restrict__ data, const int* __restrict__ rowblk,
+                           unsigned* __restrict__ key) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  const int pj = rowpos[j];
+  const int bj = rowblk[j];
   for (int e = indptr[j]; e < indptr[j + 1]; ++e) {
     unsigned k = kNoSector;
     if (data[e] != 0.0) {
-      const int b = owner(blk_row, G, rowpos[indices[e]]);
-      if (pj < blk_row[b] || pj >= blk_row[b + 1]) k = ((unsigned)b << 24) | ((unsigned)j >> 2);
+      const int b = rowblk[indices[e]];
+      if (b != bj) k = ((unsigned)b << 24) | ((unsigned)j >> 2);
     }
     key[e] = k;
   }
@@ -429,21 +445,27 @@ __global__ void k_sec_ptr_fix(int G, int64_t N, const int* __restrict__ flag, co
     if (sec_ptr[b] < 0) sec_ptr[b] = sec_ptr[b + 1];
 }
 
-// warp per slice: gather map of every SELL element
-__global__ void k_sell_map(int S, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_row,
-                           const int64_t* __restrict__ slice_off, const int* __restrict__ sell_col,
-                           const int* __restrict__ rowpos, const unsigned* __restrict__ secs,
-                           const int* __restrict__ sec_ptr, unsigned* __restrict__ map) {
-  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (s >= S) return;
-  const int b = owner(blk_slice, G, s);
+// one CTA per partition: its sector list in shared memory, gather map of every
+// SELL element of the partition (binary search on chip)
+constexpr int kMapSmemSectors = 8192;
+
+__global__ void __launch_bounds__(256) k_sell_map(int G, const int* __restrict__ blk_slice,
+                                                  const int* __restrict__ blk_row, const int64_t* __restrict__ slice_off,
+                                                  const int* __restrict__ sell_col, const int* __restrict__ rowpos,
+                                                  const unsigned* __restrict__ secs, const int* __restrict__ sec_ptr,
+                                                  unsigned* __restrict__ map) {
+  __shared__ unsigned ssec[kMapSmemSectors];
+  const int b = blockIdx.x;
   const int p0 = blk_row[b], p1 = blk_row[b + 1];
   const int u0 = sec_ptr[b], u1 = sec_ptr[b + 1];
-  const int64_t off = slice_off[s];
-  const int W = (int)((slice_off[s + 1] - off) >> 5);
-  for (int k = 0; k < W; ++k) {
-    const int64_t i = off + (int64_t)k * 32 + lane;
+  const int ns = u1 - u0;
+  const bool on_chip = ns <= kMapSmemSectors;
+  if (on_chip)
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) ssec[j] = secs[u0 + j];
+  __syncthreads();
+  const unsigned* sl = on_chip ? ssec : secs + u0;
+  const int64_t e0 = slice_off[blk_slice[b]], e1 = slice_off[blk_slice[b + 1]];
+  for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
     const int c = sell_col[i];
     unsigned m = 0u;
     if (c >= 0) {
@@ -452,12 +474,12 @@ __global__ void k_sell_map(int S, int G, const int* __restrict__ blk_slice, cons
         m = kOwnBit | (unsigned)(pc - p0);
       } else {
         const unsigned sec = (unsigned)c >> 2;
-        int lo = u0, hi = u1;  // first unique sector >= sec
+        int lo = 0, hi = ns;  // first sector >= sec
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (secs[mid] < sec) lo = mid + 1; else hi = mid;
+          if (sl[mid] < sec) lo = mid + 1; else hi = mid;
         }
-        m = 4u * (unsigned)(lo - u0) + ((unsigned)c & 3u);
+        m = 4u * (unsigned)lo + ((unsigned)c & 3u);
       }
     }
     map[i] = m;
@@ -782,9 +804,10 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   VFPI_CK(ensure(ws.sec_ptr, 4 * (size_t)(G + 1)));
   VFPI_CK(cudaMemsetAsync(ws.sec_ptr.p, 0xff, 4 * (size_t)(G + 1), st));
   if (n > 0 && nnz > 0 && G <= 256 && n < (1 << 26)) {
-    k_rowpos<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowpos));
-    k_sec_keys<<<nblk(n), 256, 0, st>>>(n, G, s.indptr, s.indices, s.data, P<int>(ws.rowpos), P<int>(ws.blk_row),
-                                        P<unsigned>(ws.sec_key));
+    VFPI_CK(ensure(ws.rowblk, 4 * (size_t)n));
+    k_rowpos<<<nblk(n), 256, 0, st>>>(n, G, P<int>(ws.row_list), P<int>(ws.blk_row), P<int>(ws.rowpos),
+                                      P<int>(ws.rowblk));
+    k_sec_keys<<<nblk(n), 256, 0, st>>>(n, s.indptr, s.indices, s.data, P<int>(ws.rowblk), P<unsigned>(ws.sec_key));
     size_t tk = 0, tsc = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tk, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey), (int)nnz, 0, 32,
                                    st);
@@ -855,10 +878,9 @@ int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const 
   if (resident) {
     VFPI_CK(ensure(ws.sell_map, 4 * (size_t)std::max<int64_t>(hs.sell_elems, 1)));
     if (S > 0) {
-      k_sell_map<<<nblk((int64_t)S * 32), 256, 0, st>>>(S, G, P<int>(ws.blk_slice), P<int>(ws.blk_row),
-                                                        P<int64_t>(ws.slice_off), P<int>(ws.sell_col), P<int>(ws.rowpos),
-                                                        P<unsigned>(ws.secs), P<int>(ws.sec_ptr),
-                                                        P<unsigned>(ws.sell_map));
+      k_sell_map<<<G, 256, 0, st>>>(G, P<int>(ws.blk_slice), P<int>(ws.blk_row), P<int64_t>(ws.slice_off),
+                                    P<int>(ws.sell_col), P<int>(ws.rowpos), P<unsigned>(ws.secs), P<int>(ws.sec_ptr),
+                                    P<unsigned>(ws.sell_map));
       ++launches;
     }
   }
