@@ -114,6 +114,34 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* sys, const vfpi_config*
                       const double* warm, const double* w_cached, vfpi_result* res, void* stream);
 int vfpi_wait(vfpi_handle* h, vfpi_result* res);
 
+/* Per-scene outputs of a scene batch. Arrays are concatenated in scene order:
+ * v [sum n_s], lam [3 * sum n_c_s], scc [sum n_c_s] (or NULL), residual_trace
+ * [num_scenes * max(max_iters,1)] (row s = scene s), and one entry per scene in
+ * iterations / converged / diverged / consistency. */
+typedef struct vfpi_scene_result {
+  double* v;
+  double* lam;
+  double* residual_trace;
+  double* scc;
+  int32_t* iterations;
+  int32_t* converged;
+  int32_t* diverged;
+  double* consistency;
+  double setup_ms;
+  double loop_ms;
+} vfpi_scene_result;
+
+/* A batch of independent systems (e.g. configs[2]'s 1024 FEM scenes), solved
+ * concurrently with one CTA per scene, each with its own iteration count,
+ * convergence test and divergence flag (solve_vfpi semantics per scene).
+ * sys holds the block-diagonal concatenation (host pointers); scene_row_ptr
+ * [num_scenes+1] and scene_ct_ptr [num_scenes+1] delimit each scene's rows
+ * and contacts (contacts grouped by scene, never coupling two scenes).
+ * num_scenes <= 1024 per call. A diverged scene does not fail the call. */
+int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* sys, int32_t num_scenes, const int32_t* scene_row_ptr,
+                      const int32_t* scene_ct_ptr, const vfpi_config* cfg, const double* warm,
+                      const double* w_cached, vfpi_scene_result* res);
+
 /* Number of kernels this library launched on the handle since creation. */
 int64_t vfpi_launch_count(const vfpi_handle* h);
 /* Layout chosen by the last solve: shared-memory resident kernel (1) or the

@@ -185,7 +185,8 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.ps_col, &h->ws.ps_src, &h->ws.seg_beg, &h->ws.seg_end, &h->ws.rowpos, &h->ws.sec_key,
                             &h->ws.sec_skey, &h->ws.sec_idx, &h->ws.sec_sidx, &h->ws.sec_flag, &h->ws.sec_upos,
                             &h->ws.sell_map, &h->ws.secs, &h->ws.sec_ptr, &h->ws.rowmin, &h->ws.ukey, &h->ws.ukey_s,
-                            &h->ws.uval, &h->ws.uorder, &h->ws.row_list2, &h->ws.row_slot2, &h->ws.rowblk, &h->ws.vbuf,
+                            &h->ws.uval, &h->ws.uorder, &h->ws.row_list2, &h->ws.row_slot2, &h->ws.rowblk,
+                            &h->ws.scene_rows, &h->ws.scene_cts, &h->ws.vbuf,
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
                             &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
   for (auto* b : bufs)
@@ -338,6 +339,9 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.prof = nullptr;
   p.prof_iter0 = 0;
   p.tune_wc = h->tune_wc;
+  p.diag = P<double>(ws.diag);
+  p.fixed_alpha_default = 0;
+  p.trace_stride = 0;
   if (h->prof_iter0 > 0) {
     CK(vfpi::ensure(ws.prof, sizeof(long long) * 32 * (size_t)G));
     CK(cudaMemsetAsync(ws.prof.p, 0, sizeof(long long) * 32 * (size_t)G, st));
@@ -471,6 +475,154 @@ int vfpi_solve(vfpi_handle* h, const vfpi_system* s, const vfpi_config* cfg, con
   res->loop_ms = dres.loop_ms;
   res->status = rc;
   return rc;
+}
+
+int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* s, int32_t S, const int32_t* scene_row_ptr,
+                      const int32_t* scene_ct_ptr, const vfpi_config* cfg, const double* warm,
+                      const double* w_cached, vfpi_scene_result* res) {
+  if (!h || !cfg || !res || !warm || !scene_row_ptr || !scene_ct_ptr || S < 1 || S > 1024) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  if (scene_row_ptr[0] != 0 || scene_row_ptr[S] != s->n || scene_ct_ptr[0] != 0 || scene_ct_ptr[S] != s->n_c) {
+    h->err = "scene pointers do not cover the system";
+    return VFPI_BAD_ARGUMENT;
+  }
+  for (int k = 0; k < S; ++k)
+    if (scene_row_ptr[k + 1] < scene_row_ptr[k] || scene_ct_ptr[k + 1] < scene_ct_ptr[k]) {
+      h->err = "scene pointers must be non-decreasing";
+      return VFPI_BAD_ARGUMENT;
+    }
+  if (cfg->op < 0 || cfg->op > 2 || cfg->step_strategy < 0 || cfg->step_strategy > 4 || cfg->max_iters < 0) {
+    h->err = "bad solver config";
+    return VFPI_BAD_ARGUMENT;
+  }
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  Workspace& ws = h->ws;
+  cudaStream_t st = ws.stream;
+  const int n = (int)s->n, n_c = (int)s->n_c;
+  const bool cheb = cfg->chebyshev != 0;
+  const bool bb = cfg->step_strategy >= VFPI_STEP_BB1 && cfg->step_strategy <= VFPI_STEP_BB_ALTERNATING;
+  vfpi_system d;
+  if ((rc = stage_system(h, s, &d))) return rc;
+  if ((rc = upload(h, ws.b_warm, warm, 8 * (size_t)n))) return rc;
+  CK(vfpi::ensure(ws.b_warm, 8 * (size_t)std::max(n, 1)));
+  const double* dwc = nullptr;
+  if (w_cached) {
+    if ((rc = upload(h, ws.b_wc, w_cached, 8 * (size_t)n))) return rc;
+    dwc = P<double>(ws.b_wc);
+  }
+  if ((rc = upload(h, ws.scene_rows, scene_row_ptr, 4 * (size_t)(S + 1)))) return rc;
+  if ((rc = upload(h, ws.scene_cts, scene_ct_ptr, 4 * (size_t)(S + 1)))) return rc;
+  CK(cudaEventRecord(ws.ev[0], st));
+  vfpi::LayoutOptions opt;
+  opt.anchor_order = false;
+  opt.length_sort = h->layout_opt.length_sort;
+  opt.scene_row_ptr = P<int>(ws.scene_rows);
+  opt.scene_ct_ptr = P<int>(ws.scene_cts);
+  vfpi::SetupSummary* hs = ws.h_summary;
+  const int G = S;
+  rc = vfpi::setup_layout(ws, d, G, st, hs, h->err, h->launches, opt);
+  if (rc) return rc;
+  rc = vfpi::setup_pack(ws, d, G, false, *hs, st, h->err, h->launches);
+  if (rc) return rc;
+  rc = vfpi::setup_step_matrix(ws, d, *cfg, dwc, st, h->err, h->launches);
+  if (rc) return rc;
+  const int smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
+  if (vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem) <= 0) {
+    h->err = "a scene has too many contacts for one CTA";
+    return VFPI_UNSUPPORTED;
+  }
+  const size_t tr = (size_t)std::max(cfg->max_iters, 1);
+  const size_t npad = (((size_t)std::max(n, 1) + 3) / 4) * 4 + 4;
+  CK(vfpi::ensure(ws.vbuf, 3 * 8 * npad));
+  CK(cudaMemsetAsync(ws.vbuf.p, 0, 3 * 8 * npad, st));
+  CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)std::max(n_c, 1)));
+  CK(vfpi::ensure(ws.status, sizeof(vfpi::SolveStatus) * (size_t)S));
+  CK(vfpi::ensure(ws.b_out_v, 8 * (size_t)std::max(n, 1)));
+  CK(vfpi::ensure(ws.b_out_lam, 24 * (size_t)std::max(n_c, 1)));
+  CK(vfpi::ensure(ws.b_trace, 8 * tr * (size_t)S));
+  CK(vfpi::ensure(ws.b_scc, 8 * (size_t)std::max(n_c, 1)));
+  double* vb = P<double>(ws.vbuf);
+  double* lb = P<double>(ws.lambuf);
+  if (n > 0) {
+    CK(cudaMemcpyAsync(vb, ws.b_warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(vb + 2 * npad, ws.b_warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaMemsetAsync(lb, 0, 2 * 24 * (size_t)std::max(n_c, 1), st));
+  CK(cudaMemsetAsync(ws.status.p, 0, sizeof(vfpi::SolveStatus) * (size_t)S, st));
+  CK(cudaEventRecord(ws.ev[1], st));
+  vfpi::IterParams p{};
+  p.n = n;
+  p.n_c = n_c;
+  p.G = G;
+  p.row_list = P<int>(ws.row_list);
+  p.row_slot = P<int>(ws.row_slot);
+  p.blk_row = P<int>(ws.blk_row);
+  p.blk_slice = P<int>(ws.blk_slice);
+  p.blk_ct = P<int>(ws.blk_ct);
+  p.slice_off = P<int64_t>(ws.slice_off);
+  p.sell_val = P<double>(ws.sell_val);
+  p.sell_col = P<int>(ws.sell_col);
+  p.cont_list = P<int>(ws.cont_list);
+  p.b = d.b;
+  p.w = P<double>(ws.w);
+  p.gamma = P<double>(ws.gamma);
+  p.col_i = d.col_i;
+  p.col_j = d.col_j;
+  p.frames = d.frames;
+  p.mu = d.mu;
+  p.mu2 = d.mu2;
+  p.phi = d.phi;
+  p.w_mean = P<double>(ws.w_mean);
+  p.diag = P<double>(ws.diag);
+  p.fixed_alpha_default = (cfg->step_strategy == VFPI_STEP_FIXED_ALPHA && std::isnan(cfg->fixed_alpha)) ? 1 : 0;
+  p.vbuf0 = vb;
+  p.vbuf1 = vb + npad;
+  p.vbuf2 = vb + 2 * npad;
+  p.lam0 = lb;
+  p.lam1 = lb + 3 * (size_t)std::max(n_c, 1);
+  p.trace = P<double>(ws.b_trace);
+  p.trace_stride = tr;
+  p.status = P<vfpi::SolveStatus>(ws.status);
+  p.out_v = P<double>(ws.b_out_v);
+  p.out_lam = P<double>(ws.b_out_lam);
+  p.max_iters = cfg->max_iters;
+  p.cheby_start = cfg->cheby_start;
+  p.step = cfg->step_strategy;
+  p.tol = cfg->residual_tol;
+  p.under_relax = cfg->under_relax;
+  p.omega = cfg->omega;
+  p.cfactor = cfg->consistency_factor;
+  rc = vfpi::launch_iterate_scenes(p, cfg->op, cheb, bb, smem, st, h->err);
+  if (rc) return rc;
+  ++h->launches;
+  CK(cudaEventRecord(ws.ev[2], st));
+  if (res->scc && n_c > 0) {
+    rc = vfpi::launch_scc_final(p, P<double>(ws.b_scc), st);
+    if (rc) { h->err = "scc kernel launch failed"; return rc; }
+    ++h->launches;
+  }
+  std::vector<vfpi::SolveStatus> stat((size_t)S);
+  CK(cudaMemcpyAsync(stat.data(), ws.status.p, sizeof(vfpi::SolveStatus) * (size_t)S, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->h_flags, ws.flags.p, 4, cudaMemcpyDeviceToHost, st));
+  if (n) CK(cudaMemcpyAsync(res->v, ws.b_out_v.p, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  if (n_c) CK(cudaMemcpyAsync(res->lam, ws.b_out_lam.p, 24 * (size_t)n_c, cudaMemcpyDeviceToHost, st));
+  if (res->residual_trace && cfg->max_iters > 0)
+    CK(cudaMemcpyAsync(res->residual_trace, ws.b_trace.p, 8 * tr * (size_t)S, cudaMemcpyDeviceToHost, st));
+  if (res->scc && n_c) CK(cudaMemcpyAsync(res->scc, ws.b_scc.p, 8 * (size_t)n_c, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int k = 0; k < S; ++k) {
+    if (res->iterations) res->iterations[k] = stat[k].iterations;
+    if (res->converged) res->converged[k] = stat[k].converged;
+    if (res->diverged) res->diverged[k] = stat[k].diverged;
+    if (res->consistency) res->consistency[k] = stat[k].consistency;
+  }
+  float a = 0.f, b2 = 0.f;
+  cudaEventElapsedTime(&a, ws.ev[0], ws.ev[1]);
+  cudaEventElapsedTime(&b2, ws.ev[1], ws.ev[2]);
+  res->setup_ms = a;
+  res->loop_ms = b2;
+  return flags_to_code(h, *h->h_flags);
 }
 
 // ---- per-subsystem entry points -------------------------------------------

@@ -93,6 +93,9 @@ struct IterParams {
   int* bar_flags;           // [G] epoch flags of the flag barrier
   long long* prof;          // optional [G][4][8] phase timestamps (NULL = off)
   int tune_wc;              // > 0: force the number of contact warps (tuning aid)
+  const double* diag;       // [n] diagonal of A (per-scene fixed-alpha default)
+  int fixed_alpha_default;  // fixed-alpha strategy with fixed_alpha = None
+  size_t trace_stride;      // scene batches: residual_trace row stride per scene
   int prof_iter0;           // first of the 4 profiled iterations
   const int* cont_list;     // [n_c] contact ids in partition order
   // system
@@ -130,6 +133,10 @@ struct Workspace;  // device buffers owned by a handle
 struct LayoutOptions {
   bool anchor_order = false;  // order units by their smallest referenced column
   bool length_sort = true;    // free rows of a CTA by decreasing length
+  // scene batches: CTA b = scene b (device arrays, G+1 entries each); contacts
+  // must be grouped by scene and never couple two scenes
+  const int* scene_row_ptr = nullptr;
+  const int* scene_ct_ptr = nullptr;
 };
 int setup_layout(Workspace& ws, const vfpi_system& dsys, int G, cudaStream_t st, SetupSummary* host_summary,
                  std::string& err, int64_t& launches, const LayoutOptions& opt = LayoutOptions());
@@ -149,6 +156,9 @@ int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, siz
                             std::string& err);
 constexpr int kResThreads = 512;
 int launch_scc_final(const IterParams& p, double* scc, cudaStream_t st);
+// independent scenes, one CTA each (layout with one CTA range per scene)
+int launch_iterate_scenes(const IterParams& p, int op, bool cheb, bool bb, int smem_bytes, cudaStream_t st,
+                          std::string& err);
 
 // ---- per-op kernels (vfpi_ops.cu) -----------------------------------------
 void launch_apply_jc(int64_t n_c, const int* ci, const int* cj, const double* fr, const double* v, double* eta,
@@ -178,7 +188,7 @@ struct Workspace {
   Buf slice_w, slice_off, sell_val, sell_col, pos_len, pos_ptr, pk_val, pk_col, bar_flags;
   Buf ucr, ufr, cposc, cposf, blk_first, blk_cr, cont_q, ps_col, ps_src, seg_beg, seg_end, rowpos;
   Buf sec_key, sec_skey, sec_idx, sec_sidx, sec_flag, sec_upos, sell_map, secs, sec_ptr;
-  Buf rowmin, ukey, ukey_s, uval, uorder, row_list2, row_slot2, rowblk;
+  Buf rowmin, ukey, ukey_s, uval, uorder, row_list2, row_slot2, rowblk, scene_rows, scene_cts;
   Buf vbuf, lambuf, partials, status, summary, flags, cub_tmp;
   Buf x, y;  // scratch for per-op entry points
   Buf prof;

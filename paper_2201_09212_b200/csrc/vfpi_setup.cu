@@ -647,6 +647,8 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
                  int64_t& launches, const LayoutOptions& opt) {
   const int n = (int)s.n, n_c = (int)s.n_c;
   const int64_t nnz = s.nnz;
+  if (G > 1024) { err = "more than 1024 CTA ranges per layout"; return VFPI_BAD_ARGUMENT; }
+  if (opt.scene_row_ptr && opt.anchor_order) { err = "scene batches use the natural unit order"; return VFPI_BAD_ARGUMENT; }
   VFPI_CK(ensure(ws.diag, 8 * (size_t)n));
   VFPI_CK(ensure(ws.rns, 8 * (size_t)n));
   VFPI_CK(ensure(ws.rowcnt, 4 * (size_t)(n + 1)));
@@ -744,9 +746,17 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ucont), P<int>(ws.kpos), n, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ucr), P<int>(ws.cposc), n + 1, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ufr), P<int>(ws.cposf), n + 1, st));
-    k_blocks<<<nblk(n), 256, 0, st>>>(n, G, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), P<int>(ws.urows),
-                                      P<int>(ws.rpos), P<int>(ws.kpos), P<int>(ws.blk_row), P<int>(ws.blk_ct),
-                                      P<int>(ws.blk_first));
+    if (opt.scene_row_ptr) {
+      // scene batch: CTA b = scene b; in natural unit order the rows of earlier
+      // scenes precede every unit of scene b, so its start is scene_row_ptr[b]
+      VFPI_CK(cudaMemcpyAsync(ws.blk_row.p, opt.scene_row_ptr, 4 * (size_t)(G + 1), cudaMemcpyDeviceToDevice, st));
+      VFPI_CK(cudaMemcpyAsync(ws.blk_ct.p, opt.scene_ct_ptr, 4 * (size_t)(G + 1), cudaMemcpyDeviceToDevice, st));
+      VFPI_CK(cudaMemcpyAsync(ws.blk_first.p, opt.scene_row_ptr, 4 * (size_t)(G + 1), cudaMemcpyDeviceToDevice, st));
+    } else {
+      k_blocks<<<nblk(n), 256, 0, st>>>(n, G, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), P<int>(ws.urows),
+                                        P<int>(ws.rpos), P<int>(ws.kpos), P<int>(ws.blk_row), P<int>(ws.blk_ct),
+                                        P<int>(ws.blk_first));
+    }
     launches += 7;
   } else {
     VFPI_CK(cudaMemsetAsync(ws.cposc.p, 0, 4, st));

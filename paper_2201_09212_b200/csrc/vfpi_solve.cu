@@ -121,12 +121,15 @@ __device__ __forceinline__ double sell_row(const double* __restrict__ sv, const 
   return acc;
 }
 
-template <int OP, bool CHEB, bool BB, bool HASC>
+// SC = false: one system over a cooperative grid (grid barrier per iteration).
+// SC = true : a batch of independent scenes, one CTA per scene (CTA b owns
+//             scene b's rows and contacts); every CTA runs its own iteration
+//             loop, reductions and termination with CTA barriers only.
+template <int OP, bool CHEB, bool BB, bool HASC, bool SC>
 __global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
   extern __shared__ double smem[];
   __shared__ double sm_warp[3 * (kThreads / 32)];
   __shared__ double sm_tot[4];
-  cg::grid_group grid = cg::this_grid();
 
   const int b = blockIdx.x;
   const int G = p.G;
@@ -146,8 +149,48 @@ __global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
   const double u = p.under_relax;
   const double omu = dsub(1.0, u);
   double rho = 0.0, nu = 1.0, theta_prev = 0.0;
-  double alpha_prev = BB ? *p.w_mean : 0.0;
+  double alpha_prev = (BB && !SC) ? *p.w_mean : 0.0;
   double alpha = 0.0;
+  bool fixed_scene_alpha = false;  // SC: fixed-alpha default 1/max|diag| of this scene
+  if constexpr (SC) {
+    // per-scene quantities the single-system setup computes globally:
+    // BB fallback alpha = mean(w) (solver.py:381), fixed-alpha default (:368)
+    double sw = 0.0, mx = -INFINITY, nanf = 0.0;
+    for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
+      const int row = __ldg(p.row_list + pos);
+      sw = dadd(sw, __ldg(p.w + row));
+      const double a = fabs(__ldg(p.diag + row));
+      if (isnan(a)) nanf = 1.0;
+      mx = a > mx ? a : mx;
+    }
+    // max |diag| over the scene: warp shuffles then warps in fixed order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = t > mx ? t : mx;
+    }
+    cta_reduce3(sw, 0.0, nanf, sm_warp, sm_tot);
+    const double wsum = sm_tot[0], anynan = sm_tot[2];
+    __syncthreads();
+    if (lane == 0) sm_warp[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = -INFINITY;
+      for (int w2 = 0; w2 < nwarps; ++w2) m = sm_warp[w2] > m ? sm_warp[w2] : m;
+      sm_tot[3] = m;
+    }
+    __syncthreads();
+    const double dmax = anynan > 0.0 ? NAN : sm_tot[3];
+    const int nrows = p1 - p0;
+    if (BB) alpha_prev = nrows > 0 ? ddiv(wsum, (double)nrows) : 0.0;
+    if (p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
+      fixed_scene_alpha = true;
+      alpha = ddiv(1.0, dmax);
+    }
+    __syncthreads();
+  }
+  double* trace = SC ? p.trace + (size_t)b * p.trace_stride : p.trace;
+  SolveStatus* status = SC ? p.status + b : p.status;
   bool pending = false;       // theta_{l-1} < tol: consistency check due
   int final_buf = 0, final_lam = 0, iters = 0, conv = 0, div = 0;
   double consistency = NAN;
@@ -163,7 +206,7 @@ __global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
     double* part = p.partials + (size_t)(l & 1) * G * kPartialStride;
 
     // ---- Barzilai-Borwein scalar step (solver.py:389-400) ----------------
-    bool use_alpha = false;
+    bool use_alpha = fixed_scene_alpha;
     if (BB && l >= 2 && !check_only) {
       double sz = 0.0, ss = 0.0, zz = 0.0;
       for (int s = s0 + warp; s < s1; s += nwarps) {
@@ -181,13 +224,15 @@ __global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
         }
       }
       cta_reduce3(sz, ss, zz, sm_warp, sm_tot);
-      if (threadIdx.x == 0) {
-        part[(size_t)b * kPartialStride + 4] = sm_tot[0];
-        part[(size_t)b * kPartialStride + 5] = sm_tot[1];
-        part[(size_t)b * kPartialStride + 6] = sm_tot[2];
+      if constexpr (!SC) {
+        if (threadIdx.x == 0) {
+          part[(size_t)b * kPartialStride + 4] = sm_tot[0];
+          part[(size_t)b * kPartialStride + 5] = sm_tot[1];
+          part[(size_t)b * kPartialStride + 6] = sm_tot[2];
+        }
+        cg::this_grid().sync();
+        grid_totals(part, G, 4, sm_tot);
       }
-      grid.sync();
-      grid_totals(part, G, 4, sm_tot);
       const double tsz = sm_tot[0], tss = sm_tot[1], tzz = sm_tot[2];
       const bool bb1 = (p.step == VFPI_STEP_BB1) || (p.step == VFPI_STEP_BB_ALTERNATING && (l % 2 == 0));
       if (tsz <= 0.0) alpha = alpha_prev;
@@ -304,13 +349,15 @@ __global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
 
     // ---- (4) residual reduction + grid-wide decision --------------------
     cta_reduce3(th, fr, nf, sm_warp, sm_tot);
-    if (threadIdx.x == 0) {
-      part[(size_t)b * kPartialStride + 0] = sm_tot[0];
-      part[(size_t)b * kPartialStride + 1] = sm_tot[1];
-      part[(size_t)b * kPartialStride + 2] = sm_tot[2];
+    if constexpr (!SC) {
+      if (threadIdx.x == 0) {
+        part[(size_t)b * kPartialStride + 0] = sm_tot[0];
+        part[(size_t)b * kPartialStride + 1] = sm_tot[1];
+        part[(size_t)b * kPartialStride + 2] = sm_tot[2];
+      }
+      cg::this_grid().sync();
+      grid_totals(part, G, 0, sm_tot);
     }
-    grid.sync();
-    grid_totals(part, G, 0, sm_tot);
     const double theta = dsqrt(sm_tot[0]);
     const double fres = dsqrt(sm_tot[1]);  // ||A v^(l-1) - b - J_c^T lam^(l-1)||
     const bool nonfinite = sm_tot[2] > 0.0;
@@ -329,7 +376,7 @@ __global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
       final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
       break;
     }
-    if (b == 0 && threadIdx.x == 0) p.trace[l - 1] = theta;
+    if ((SC || b == 0) && threadIdx.x == 0) trace[l - 1] = theta;
     if (nonfinite) {  // DivergenceError (solver.py:424-427)
       iters = l; div = 1;
       final_buf = l % 3; final_lam = l & 1;
@@ -354,12 +401,12 @@ __global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
 #pragma unroll
     for (int t = 0; t < 3; ++t) p.out_lam[3 * (size_t)m + t] = lfin[3 * (size_t)m + t];
   }
-  if (b == 0 && threadIdx.x == 0) {
-    p.status->iterations = iters;
-    p.status->converged = conv;
-    p.status->diverged = div;
-    p.status->final_vbuf = final_buf;
-    p.status->consistency = consistency;
+  if ((SC || b == 0) && threadIdx.x == 0) {
+    status->iterations = iters;
+    status->converged = conv;
+    status->diverged = div;
+    status->final_vbuf = final_buf;
+    status->consistency = consistency;
   }
 }
 
@@ -380,20 +427,25 @@ __global__ void k_scc_final(int n_c, const int* __restrict__ ci, const int* __re
 
 using KernelFn = void (*)(IterParams);
 
-template <int OP>
+template <int OP, bool SC>
 KernelFn pick3(bool cheb, bool bb, bool hasc) {
   if (cheb) {
-    if (bb) return hasc ? k_iterate<OP, true, true, true> : k_iterate<OP, true, true, false>;
-    return hasc ? k_iterate<OP, true, false, true> : k_iterate<OP, true, false, false>;
+    if (bb) return hasc ? k_iterate<OP, true, true, true, SC> : k_iterate<OP, true, true, false, SC>;
+    return hasc ? k_iterate<OP, true, false, true, SC> : k_iterate<OP, true, false, false, SC>;
   }
-  if (bb) return hasc ? k_iterate<OP, false, true, true> : k_iterate<OP, false, true, false>;
-  return hasc ? k_iterate<OP, false, false, true> : k_iterate<OP, false, false, false>;
+  if (bb) return hasc ? k_iterate<OP, false, true, true, SC> : k_iterate<OP, false, true, false, SC>;
+  return hasc ? k_iterate<OP, false, false, true, SC> : k_iterate<OP, false, false, false, SC>;
 }
 
-KernelFn pick(int op, bool cheb, bool bb, bool hasc) {
-  if (op == OP_PROXIMAL) return pick3<OP_PROXIMAL>(cheb, bb, hasc);
-  if (op == OP_ANISO) return pick3<OP_ANISO>(cheb, bb, hasc);
-  return pick3<OP_STRICT>(cheb, bb, hasc);
+KernelFn pick(int op, bool cheb, bool bb, bool hasc, bool sc = false) {
+  if (sc) {
+    if (op == OP_PROXIMAL) return pick3<OP_PROXIMAL, true>(cheb, bb, hasc);
+    if (op == OP_ANISO) return pick3<OP_ANISO, true>(cheb, bb, hasc);
+    return pick3<OP_STRICT, true>(cheb, bb, hasc);
+  }
+  if (op == OP_PROXIMAL) return pick3<OP_PROXIMAL, false>(cheb, bb, hasc);
+  if (op == OP_ANISO) return pick3<OP_ANISO, false>(cheb, bb, hasc);
+  return pick3<OP_STRICT, false>(cheb, bb, hasc);
 }
 
 }  // namespace
@@ -418,6 +470,20 @@ int launch_iterate(const IterParams& p, int op, bool cheb, bool bb, int smem_byt
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kThreads), args, smem_bytes, st);
   if (e != cudaSuccess) {
     err = std::string("cooperative launch: ") + cudaGetErrorString(e);
+    return VFPI_CUDA_ERROR;
+  }
+  return VFPI_OK;
+}
+
+int launch_iterate_scenes(const IterParams& p, int op, bool cheb, bool bb, int smem_bytes, cudaStream_t st,
+                          std::string& err) {
+  KernelFn f = pick(op, cheb, bb, p.n_c > 0, true);
+  cudaError_t e = ensure_max_dynamic_smem((const void*)f);
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
+  f<<<p.G, kThreads, smem_bytes, st>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("scene-batch launch: ") + cudaGetErrorString(e);
     return VFPI_CUDA_ERROR;
   }
   return VFPI_OK;
