@@ -87,3 +87,124 @@ def rigid_contact_system(n_bodies: int = 4096, n_contacts: int = 16384, seed: in
     col_i = n_o + 6 * np.arange(n_contacts)
     col_j = col_i + 3
     return make_packed(n_o + 3 * n_v, a.indptr, a.indices, a.data, b, col_i, col_j, frames, mus, mus, phi)
+
+
+# ---------------------------------------------------------------------------
+# configs[0] / configs[2]: linear-tet FEM cube dropped on the plane z = 0
+# ---------------------------------------------------------------------------
+# The reference has no FEM; this is the linear small-strain
+# assembly the SURVEY probe describes (Appendix C): 5 tets per hex with
+# alternating parity, K_e = V B^T C B, lumped mass rho V / 4 per tet node,
+# A = (2/dt) M + (dt/2) K, b = (2/dt) M v - K (x - X) + m g (Eq. 10 with the
+# elastic potential). Node-plane contacts follow the reference's
+# detect_contacts (contacts.py:159-200, NodeProxy radius 0, margin 1e-4) and
+# nodalize (contacts.py:271-321): one S-contact per node below the margin,
+# frame contact_frame(+z), phi = -(beta/dt) depth (+ restitution).
+
+_EVEN = ((0, 1, 2, 4), (1, 3, 2, 7), (1, 4, 5, 7), (2, 4, 6, 7), (1, 2, 4, 7))
+_ODD = ((1, 0, 3, 5), (0, 2, 3, 6), (0, 4, 5, 6), (3, 5, 6, 7), (0, 3, 5, 6))
+
+
+def _tets(nx: int):
+    tets = []
+    idx = lambda i, j, k: i + nx * (j + nx * k)  # noqa: E731
+    for k in range(nx - 1):
+        for j in range(nx - 1):
+            for i in range(nx - 1):
+                c = [idx(i + (v & 1), j + ((v >> 1) & 1), k + ((v >> 2) & 1)) for v in range(8)]
+                for t in (_EVEN if (i + j + k) % 2 == 0 else _ODD):
+                    tets.append([c[a] for a in t])
+    return np.array(tets, dtype=np.int64)
+
+
+def _elasticity(E, nu):
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    C = np.zeros((6, 6))
+    C[:3, :3] = lam
+    C[np.arange(3), np.arange(3)] += 2 * mu
+    C[np.arange(3, 6), np.arange(3, 6)] = mu
+    return C
+
+
+class FemCube:
+    """One deformable cube (configs[0] defaults; configs[2] varies E, drop, yaw)."""
+
+    def __init__(self, nx=10, side=0.1, E=1e5, nu=0.3, rho=1000.0, drop=0.05, yaw=0.0, dt=1e-3, mu=0.5,
+                 gravity=-9.81, margin=1e-4, beta_err=0.2, e_rest=0.0, rest_threshold=0.01):
+        self.nx, self.dt, self.mu = nx, dt, mu
+        self.margin, self.beta, self.e_rest, self.thr = margin, beta_err, e_rest, rest_threshold
+        h = side / (nx - 1)
+        g = np.arange(nx) * h - side / 2
+        z, y, x = np.meshgrid(g, g, g, indexing="ij")
+        X = np.stack([x.ravel(), y.ravel(), z.ravel() + side / 2], axis=1)
+        cy, sy = np.cos(yaw), np.sin(yaw)
+        X = X @ np.array([[cy, -sy, 0.0], [sy, cy, 0.0], [0.0, 0.0, 1.0]]).T
+        X[:, 2] += drop
+        self.X = X
+        self.x = X.copy()
+        self.v = np.zeros_like(X)
+        tets = _tets(nx)
+        C = _elasticity(E, nu)
+        nn = X.shape[0]
+        # all tets at once: D = [P1-P0, P2-P0, P3-P0] (columns), grad lambda_1..3 = rows of D^-1
+        P = X[tets]                                   # (T, 4, 3)
+        D = np.stack([P[:, 1] - P[:, 0], P[:, 2] - P[:, 0], P[:, 3] - P[:, 0]], axis=2)
+        V = np.abs(np.linalg.det(D)) / 6.0
+        Gi = np.linalg.inv(D)                         # (T, 3, 3)
+        grads = np.concatenate([-Gi.sum(axis=1, keepdims=True), Gi], axis=1)  # (T, 4, 3)
+        T = tets.shape[0]
+        B = np.zeros((T, 6, 12))
+        for a in range(4):
+            gx, gy, gz = grads[:, a, 0], grads[:, a, 1], grads[:, a, 2]
+            c0 = 3 * a
+            B[:, 0, c0], B[:, 1, c0 + 1], B[:, 2, c0 + 2] = gx, gy, gz
+            B[:, 3, c0], B[:, 3, c0 + 1] = gy, gx
+            B[:, 4, c0 + 1], B[:, 4, c0 + 2] = gz, gy
+            B[:, 5, c0], B[:, 5, c0 + 2] = gz, gx
+        Ke = V[:, None, None] * np.einsum("tji,jk,tkl->til", B, C, B)
+        dof = (3 * tets[:, :, None] + np.arange(3)).reshape(T, 12)
+        rows = [np.broadcast_to(dof[:, :, None], (T, 12, 12)).ravel()]
+        cols = [np.broadcast_to(dof[:, None, :], (T, 12, 12)).ravel()]
+        vals = [Ke.ravel()]
+        mass = np.zeros(nn)
+        np.add.at(mass, tets.ravel(), np.repeat(rho * V / 4.0, 4))
+        n = 3 * nn
+        K = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n)).tocsc()
+        K.sum_duplicates()
+        self.K = K
+        self.m = np.repeat(mass, 3)
+        self.gravity = np.zeros(n)
+        self.gravity[2::3] = gravity
+        A = sp.diags((2.0 / dt) * self.m, format="csc") + (dt / 2.0) * K
+        A = sp.csc_matrix(A)
+        A.sum_duplicates()
+        A.sort_indices()
+        self.A = A
+        self.n = n
+
+    def contacts(self):
+        """Node-plane contacts of the current configuration (reference detect + nodalize)."""
+        z = self.x[:, 2]
+        nodes = np.nonzero(z < self.margin)[0]
+        depth = np.maximum(0.0, -z[nodes])
+        phi = -(self.beta / self.dt) * depth
+        vn = self.v[nodes, 2]
+        rest = np.abs(vn) > self.thr
+        phi = np.where(rest, phi + self.e_rest * np.minimum(0.0, vn), phi)
+        frame = contact_frame(np.array([0.0, 0.0, 1.0]))
+        return nodes, phi, depth, frame
+
+    def system(self) -> PackedSystem:
+        b = (2.0 / self.dt) * self.m * self.v.ravel() - self.K @ (self.x - self.X).ravel() + self.m * self.gravity
+        nodes, phi, depth, frame = self.contacts()
+        n_c = nodes.shape[0]
+        mu = np.full(n_c, self.mu)
+        return make_packed(self.n, self.A.indptr, self.A.indices, self.A.data, b, 3 * nodes,
+                           np.full(n_c, -1), np.tile(frame.ravel(), n_c), mu, mu, phi)
+
+    def advance(self, v_hat):
+        """Midpoint integration (dynamics.py:237-255 for particles)."""
+        vh = np.asarray(v_hat)[: self.n].reshape(-1, 3)
+        self.x = self.x + self.dt * vh
+        self.v = 2.0 * vh - self.v

@@ -294,8 +294,48 @@ def rigid_pile_case(n_bodies=256, n_contacts=1024, seed=2201, k_v=1e5):
     return aug
 
 
+def fem_cases():
+    """configs[0]-shaped FEM cubes (the repo's own linear-tet assembly — the
+    reference has none), stepped with the reference solve_vfpi; the contacts
+    of the saved steps come from the reference detect_contacts / nodalize /
+    augment_dynamics on the same state, so they pin FemCube.contacts()."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from condsim.contacts import Geometry, NodeProxy, Plane, StabilizationParams
+    from paper_2201_09212_b200.scenes import FemCube
+
+    out = []
+    for tag, kw, picks in (("fem6", dict(nx=6, drop=0.01), (45, 47, 60)),
+                           ("fem10", dict(nx=10), (101, 104))):
+        cube = FemCube(**kw)
+        nn = cube.n // 3
+        bodies = [Body("particle3", float(cube.m[3 * k]), 3 * k, 3 * k) for k in range(nn)]
+        geom = Geometry(planes=[Plane(np.zeros(3), np.array([0.0, 0.0, 1.0]))],
+                        node_proxies=[NodeProxy(k, 3 * k, 0.0) for k in range(nn)])
+        a_o = SparseSymmetric.from_scipy(cube.A)
+        prev = None
+        for step in range(max(picks) + 1):
+            ps = cube.system()
+            state = SystemState(cube.x.ravel().copy(), cube.v.ravel().copy(), step, cube.dt)
+            raw = detect_contacts(state, bodies, geom)
+            nodal = nodalize(raw, state, bodies, 1e5, 0.5, None, StabilizationParams(dt=cube.dt))
+            aug = augment_dynamics(a_o, ps.b.copy(), nodal)
+            warm = np.zeros(aug.n) if prev is None else prev
+            cfg = SolverConfig(residual_tol=1e-8, max_iters=500, chebyshev=(tag == "fem6"))
+            if step in picks and aug.contacts.contacts:
+                case = f"{tag}_s{step}"
+                save_case(case, aug, cfg, warm, seed=step,
+                          extra=dict(fem_x=cube.x.copy(), fem_v=cube.v.copy(),
+                                     fem_kw=json.dumps(kw)))
+                out.append(case)
+            v, lam, rep = solve_vfpi(aug, cfg, warm)
+            cube.advance(v)
+            prev = v
+    return out
+
+
 def main():
-    names = random_cases()
+    names = fem_cases()
+    names += random_cases()
     names += scenario_cases()
     aug = rigid_pile_case()
     save_case("rigid_pile_256", aug, SolverConfig(residual_tol=1e-8, max_iters=300), np.zeros(aug.n), seed=5)

@@ -25,3 +25,26 @@ def test_rigid_system_structure_at_config1_scale():
     assert np.all(ps.col_j == ps.col_i + 3)
     assert int(np.count_nonzero(ps.data)) == 786420  # SURVEY §8 sizing table
     assert ps.nnz == 1376244
+
+
+def test_fem_cube_system_matches_reference_contact_pipeline():
+    """FemCube's A, b and node-plane contacts equal what the reference's
+    detect_contacts / nodalize / augment_dynamics built for the same state
+    (golden fem*_s*: the FEM assembly itself has no reference and is the
+    repo's own; the contact pipeline and the solve are pinned)."""
+    import json
+
+    from golden_cases import names
+
+    from paper_2201_09212_b200.scenes import FemCube
+
+    cases = [c for c in names() if c.startswith("fem")]
+    assert len(cases) >= 3
+    for c in cases:
+        d = load(c)
+        cube = FemCube(**json.loads(str(d["fem_kw"])))
+        cube.x = d["fem_x"].copy()
+        cube.v = d["fem_v"].copy()
+        ps = cube.system()
+        for k in ("indptr", "indices", "data", "b", "col_i", "col_j", "frames", "mu", "phi"):
+            assert np.array_equal(getattr(ps, k), d[k]), (c, k)
