@@ -10,7 +10,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvfpi.so")
+LIB_PATH = os.environ.get("VFPI_LIB") or os.path.join(HERE, "libvfpi.so")
 
 OK, DIVERGED, INVALID_MATRIX, TIE_VIOLATION, DIM_MISMATCH, CUDA_ERROR, UNSUPPORTED, BAD_ARGUMENT = range(8)
 OPERATORS = {"strict": 0, "proximal": 1, "strict-anisotropic": 2}

@@ -93,25 +93,33 @@ __device__ __forceinline__ void grid_totals(const double* __restrict__ part, int
 
 // sequential SELL-32 row sum of one slice: acc = sum_k val[k] * x(col[k]),
 // in increasing column order, FMA-free, starting from 0 (sparse.py:97-102).
+#ifndef VFPI_SELL_UNROLL
+#define VFPI_SELL_UNROLL 8
+#endif
+#ifndef VFPI_SC_MIN_BLOCKS
+#define VFPI_SC_MIN_BLOCKS 4
+#endif
+
 template <class X>
 __device__ __forceinline__ double sell_row(const double* __restrict__ sv, const int* __restrict__ sc, int64_t off,
                                            int W, int lane, X x) {
+  constexpr int U = VFPI_SELL_UNROLL;
   double acc = 0.0;
   const double* vp = sv + off + lane;
   const int* cp = sc + off + lane;
   int k = 0;
-  for (; k + 4 <= W; k += 4) {
-    int c[4];
-    double a[4], xv[4];
+  for (; k + U <= W; k += U) {
+    int c[U];
+    double a[U], xv[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       c[u] = __ldg(cp + 32 * (k + u));
       a[u] = __ldg(vp + 32 * (k + u));
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xv[u] = c[u] >= 0 ? x(c[u]) : 0.0;
+    for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? x(c[u]) : 0.0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
       if (c[u] >= 0) acc = dadd(acc, dmul(a[u], xv[u]));
   }
   for (; k < W; ++k) {
@@ -126,7 +134,7 @@ __device__ __forceinline__ double sell_row(const double* __restrict__ sv, const 
 //             scene b's rows and contacts); every CTA runs its own iteration
 //             loop, reductions and termination with CTA barriers only.
 template <int OP, bool CHEB, bool BB, bool HASC, bool SC>
-__global__ void __launch_bounds__(kThreads) k_iterate(IterParams p) {
+__global__ void __launch_bounds__(kThreads, SC ? VFPI_SC_MIN_BLOCKS : 1) k_iterate(IterParams p) {
   extern __shared__ double smem[];
   __shared__ double sm_warp[3 * (kThreads / 32)];
   __shared__ double sm_tot[4];
