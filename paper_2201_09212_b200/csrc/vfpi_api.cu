@@ -209,6 +209,9 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (key == 0) { h->tune_wc = value; return VFPI_OK; }
   if (key == 1) { h->layout_opt.anchor_order = value != 0; return VFPI_OK; }
   if (key == 2) { h->layout_opt.length_sort = value != 0; return VFPI_OK; }
+  if (key == 3 && value > 0) { h->layout_opt.entry_cost = value; return VFPI_OK; }
+  if (key == 4 && value > 0) { h->layout_opt.row_cost = value; return VFPI_OK; }
+  if (key == 5 && value >= 0) { h->layout_opt.contact_cost = value; return VFPI_OK; }
   return VFPI_BAD_ARGUMENT;
 }
 
@@ -220,7 +223,7 @@ int vfpi_set_profile(vfpi_handle* h, int iter0) {
 
 int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count) {
   if (!h || !out) return VFPI_BAD_ARGUMENT;
-  const int64_t cnt = std::min<int64_t>(max_count, 32 * (int64_t)h->last_G);
+  const int64_t cnt = std::min<int64_t>(max_count, 64 * (int64_t)h->last_G);
   if (!h->ws.prof.p || cnt <= 0) return VFPI_BAD_ARGUMENT;
   cudaSetDevice(h->ws.device);
   CK(cudaStreamSynchronize(h->ws.stream));
@@ -343,8 +346,8 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.fixed_alpha_default = 0;
   p.trace_stride = 0;
   if (h->prof_iter0 > 0) {
-    CK(vfpi::ensure(ws.prof, sizeof(long long) * 32 * (size_t)G));
-    CK(cudaMemsetAsync(ws.prof.p, 0, sizeof(long long) * 32 * (size_t)G, st));
+    CK(vfpi::ensure(ws.prof, sizeof(long long) * 64 * (size_t)G));
+    CK(cudaMemsetAsync(ws.prof.p, 0, sizeof(long long) * 64 * (size_t)G, st));
     p.prof = P<long long>(ws.prof);
     p.prof_iter0 = h->prof_iter0;
   }

@@ -89,7 +89,7 @@ struct IterParams {
   const unsigned* secs;     // [sum NS] 32-byte sectors of v each CTA stages per iteration
   const int* sec_ptr;       // [G+1] per-CTA range in secs
   const int* blk_cr;        // [G+1] contact rows at the head of every CTA range
-  const int* cont_q;        // [n_c] local row position of each contact's first row
+  const int* cont_q;        // [n_c] rank of a two-sided contact among its CTA's (row a of side j: 3C + a*CD + rank)
   int* bar_flags;           // [G] epoch flags of the flag barrier
   long long* prof;          // optional [G][4][8] phase timestamps (NULL = off)
   int tune_wc;              // > 0: force the number of contact warps (tuning aid)
@@ -133,6 +133,7 @@ struct Workspace;  // device buffers owned by a handle
 struct LayoutOptions {
   bool anchor_order = false;  // order units by their smallest referenced column
   bool length_sort = true;    // free rows of a CTA by decreasing length
+  int entry_cost = 24, row_cost = 40, contact_cost = 256;  // partition cost model
   // scene batches: CTA b = scene b (device arrays, G+1 entries each); contacts
   // must be grouped by scene and never couple two scenes
   const int* scene_row_ptr = nullptr;

@@ -26,7 +26,6 @@ namespace vfpi {
 namespace {
 
 constexpr unsigned kOwn = 0x80000000u;
-constexpr int kLPC = 4;                 // lanes per contact in the one-shot phase
 constexpr int kMaxPartialsPerLane = 8;  // G <= 256
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -100,17 +99,25 @@ __device__ __forceinline__ void grid_arrive_wait(const double* sm_tot, double* p
 }
 
 // warp 0: fixed-order sum of the G published partials -> sm_tot[0..2]
-__device__ __forceinline__ void warp0_collect(const double* part, int off, int G, double* sm_tot) {
+// (roots: sm_tot[0..1] = square roots, the residual norms of the decision)
+__device__ __forceinline__ void warp0_collect(const double* part, int off, int G, double* sm_tot, bool roots) {
   const int lane = threadIdx.x & 31;
+  double px[kMaxPartialsPerLane], py[kMaxPartialsPerLane], pz[kMaxPartialsPerLane];
+#pragma unroll
+  for (int k = 0; k < kMaxPartialsPerLane; ++k) {  // all loads in flight first
+    const int g = lane + 32 * k;
+    const double* q = part + (size_t)g * kPartialStride + off;
+    px[k] = g < G ? __ldcg(q + 0) : 0.0;
+    py[k] = g < G ? __ldcg(q + 1) : 0.0;
+    pz[k] = g < G ? __ldcg(q + 2) : 0.0;
+  }
   double x = 0.0, y = 0.0, z = 0.0;
 #pragma unroll
   for (int k = 0; k < kMaxPartialsPerLane; ++k) {
-    const int g = lane + 32 * k;
-    if (g < G) {
-      const double* q = part + (size_t)g * kPartialStride + off;
-      x = dadd(x, __ldcg(q + 0));
-      y = dadd(y, __ldcg(q + 1));
-      z = dadd(z, __ldcg(q + 2));
+    if (lane + 32 * k < G) {
+      x = dadd(x, px[k]);
+      y = dadd(y, py[k]);
+      z = dadd(z, pz[k]);
     }
   }
 #pragma unroll
@@ -120,10 +127,19 @@ __device__ __forceinline__ void warp0_collect(const double* part, int off, int G
     z = dadd(z, __shfl_xor_sync(0xffffffffu, z, o));
   }
   if (lane == 0) {
-    sm_tot[0] = x;
-    sm_tot[1] = y;
+    sm_tot[0] = roots ? dsqrt(x) : x;
+    sm_tot[1] = roots ? dsqrt(y) : y;
     sm_tot[2] = z;
   }
+}
+
+// x of one SELL element -- the on-chip copy of an own row or a staged sector
+// value -- as a pointer select and one shared load (no branch, so the gathers
+// of an unrolled row sum are all in flight together)
+__device__ __forceinline__ double gather_x(unsigned m, const double* __restrict__ xs,
+                                           const double* __restrict__ vown) {
+  const double* src = (m & kOwn) ? vown : xs;
+  return src[m & ~kOwn];
 }
 
 // sequential (scipy-order) dot of one row with x: SELL element i = base + 32k,
@@ -139,7 +155,7 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const u
       const int i = base + 32 * (k + u);
       const unsigned m = mp[i];
       a[u] = sv[i];
-      x[u] = (m & kOwn) ? vown[m & ~kOwn] : xs[m];
+      x[u] = gather_x(m, xs, vown);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc = dadd(acc, dmul(a[u], x[u]));
@@ -147,9 +163,47 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const u
   for (; k < len; ++k) {
     const int i = base + 32 * k;
     const unsigned m = mp[i];
-    acc = dadd(acc, dmul(sv[i], (m & kOwn) ? vown[m & ~kOwn] : xs[m]));
+    acc = dadd(acc, dmul(sv[i], gather_x(m, xs, vown)));
   }
   return acc;
+}
+
+// three independent row sums at once (one contact side), each in scipy order
+__device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const unsigned* __restrict__ mp,
+                                         const int* __restrict__ sb, const int* __restrict__ rlen,
+                                         const double* __restrict__ xs, const double* __restrict__ vown, int q0,
+                                         int q1, int q2, double* out) {
+  const int qq[3] = {q0, q1, q2};
+  int base[3], len[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    base[a] = sb[qq[a] >> 5] + (qq[a] & 31);
+    len[a] = rlen[qq[a]];
+  }
+  const int L = max(len[0], max(len[1], len[2]));
+  double acc[3] = {0.0, 0.0, 0.0};
+  // branch-free: every lane loads (a row past its end re-reads its last
+  // element) and only adds while k < len, so the three chains interleave
+  for (int k = 0; k < L; k += 2) {
+    double pr[2][3];
+    bool ok[2][3];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int kk = k + u;
+        ok[u][a] = kk < len[a];
+        const int i = base[a] + 32 * (ok[u][a] ? kk : 0);
+        const unsigned m = mp[i];
+        pr[u][a] = dmul(sv[i], gather_x(m, xs, vown));
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) acc[a] = ok[u][a] ? dadd(acc[a], pr[u][a]) : acc[a];
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) out[a] = acc[a];
 }
 
 template <int OP, bool CHEB, bool BB, bool HASC>
@@ -157,10 +211,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double sm_warp[3 * (kResThreads / 32)];
   __shared__ double sm_tot[4];
-  __shared__ unsigned long long sm_role_end[2];
+  __shared__ unsigned long long sm_role_end[8];
   const int b = blockIdx.x, G = p.G, T = blockDim.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, nw = T >> 5;
-  if (tid < 2) sm_role_end[tid] = 0;
+  if (tid < 8) sm_role_end[tid] = 0;
   const int p0 = p.blk_row[b], p1 = p.blk_row[b + 1], R = p1 - p0;
   const int s0 = p.blk_slice[b], s1 = p.blk_slice[b + 1];
   const int64_t ep0 = p.slice_off[s0];
@@ -186,7 +240,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   double* cfr = reinterpret_cast<double*>(smraw + Lo.o_fr);
   double* cpar = reinterpret_cast<double*>(smraw + Lo.o_par);  // mu, mu2, phi, gamma
   double* lam_s = reinterpret_cast<double*>(smraw + Lo.o_lam); // [2][3C]
-  double* vs_s = reinterpret_cast<double*>(smraw + Lo.o_vs);   // [CR]
   double* jt_s = reinterpret_cast<double*>(smraw + Lo.o_jt);   // [CR]
   unsigned* counter = reinterpret_cast<unsigned*>(p.bar_flags);
 
@@ -220,28 +273,14 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   for (int t = tid; t < CR; t += T) jt_s[t] = 0.0;
   __syncthreads();
 
-  // split the warps: [0, WC) sweep the contact rows and run the contact quads,
-  // [WC, nw) sweep the free rows; estimated cost = rounds x per-round latency
+  // split the warps: [0, WC) run one contact per lane (its rows, the one-shot
+  // projection and the scatter), [WC, nw) sweep the free rows
   int WC = 0;
   if (C > 0) {
-    const int FR = R - CR;
-    if (FR == 0) {
-      WC = nw;
-    } else {
-      int maxlen = 0;
-      for (int q = CR; q < R; ++q) maxlen = rlen[q] > maxlen ? rlen[q] : maxlen;
-      const long long kf = 22LL * maxlen + 400;  // cycles per free-row round
-      long long best = LLONG_MAX;
-      for (int w = 1; w < nw; ++w) {
-        const long long tc = (long long)((CR + 32 * w - 1) / (32 * w)) * 500 +
-                             (long long)((C + (32 / kLPC) * w - 1) / ((32 / kLPC) * w)) * 2500;
-        const long long tf = (long long)((FR + 32 * (nw - w) - 1) / (32 * (nw - w))) * kf;
-        const long long c2 = tc > tf ? tc : tf;
-        if (c2 < best) { best = c2; WC = w; }
-      }
-    }
+    WC = (C + 31) / 32;
+    if (WC > nw - 1 && R > CR) WC = nw - 1;
+    if (WC > nw) WC = nw;
   }
-
   if (C > 0 && WC < nw && p.tune_wc > 0) WC = p.tune_wc < nw ? p.tune_wc : nw - 1;
   double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
   const double u = p.under_relax;
@@ -263,7 +302,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         if (tid == 0) {
           long long g;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-          p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 8 + k] = k == 7 ? g : clock64();
+          p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 16 + k] = k == 7 ? g : clock64();
         }
       }
     };
@@ -275,10 +314,23 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
 
     // ---- phase 1: stage the remote sectors of v^(l-1); reduce partials of l-1
     {
+      // warps 1.. stage (up to four sectors per thread in flight before the
+      // first smem store); warp 0 reduces the partials and takes the roots
       double4* dst = reinterpret_cast<double4*>(xs);
-      for (int j = tid; j < NS; j += T) dst[j] = ld_sector(vcur + 4 * (size_t)sec[j]);
-      if (l > 1 && warp == 0)
-        warp0_collect(p.partials + (size_t)((l - 1) & 1) * G * kPartialStride, 0, G, sm_tot);
+      const int TS = T - 32;
+      if (warp > 0) {
+        for (int j0 = tid - 32; j0 < NS; j0 += 4 * TS) {
+          double4 r[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j0 + u * TS < NS) r[u] = ld_sector(vcur + 4 * (size_t)sec[j0 + u * TS]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j0 + u * TS < NS) dst[j0 + u * TS] = r[u];
+        }
+      } else if (l > 1) {
+        warp0_collect(p.partials + (size_t)((l - 1) & 1) * G * kPartialStride, 0, G, sm_tot, true);
+      }
     }
     __syncthreads();
     stamp(2);
@@ -286,8 +338,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     // ---- decision for iteration l-1 (solver.py:422-446) -------------------
     if (l > 1) {
       const int lp = l - 1;
-      const double theta = dsqrt(sm_tot[0]);   // theta_{l-1}
-      const double fres = dsqrt(sm_tot[1]);    // ||A v^(l-2) - b - J_c^T lam^(l-2)||
+      const double theta = sm_tot[0];  // theta_{l-1} (square roots taken by warp 0)
+      const double fres = sm_tot[1];   // ||A v^(l-2) - b - J_c^T lam^(l-2)||
       const bool nonfinite = sm_tot[2] > 0.0;
       if (pending) {
         consistency = fres;
@@ -340,7 +392,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       cta_reduce3(sz, ss, zz, sm_warp, sm_tot);
       __syncthreads();
       grid_arrive_wait(sm_tot, part, 4, counter, G, ++epoch);
-      if (warp == 0) warp0_collect(part, 4, G, sm_tot);
+      if (warp == 0) warp0_collect(part, 4, G, sm_tot, false);
       __syncthreads();
       const double tsz = sm_tot[0], tss = sm_tot[1], tzz = sm_tot[2];
       const bool bb1 = (p.step == VFPI_STEP_BB1) || (p.step == VFPI_STEP_BB_ALTERNATING && (l % 2 == 0));
@@ -386,66 +438,72 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       return r;
     };
 
-    // ---- (1)-(3): contact warps sweep the contact rows then run the one-shots;
-    // the free-row warps sweep their rows concurrently -----------------------
+    // ---- (1)-(3): contact lanes -- sweep of the contact's rows, one-shot
+    // projection, scatter -- beside the free-row warps ----------------------
     stamp(3);
     if (warp < WC) {
-      // (1) surrogate-dynamics sweep of the contact rows
-      for (int q = tid; q < CR; q += WC * 32) {
-        const double r = residual(q);
-        if (!check_only) vs_s[q] = dsub(vown[q], dmul(use_alpha ? alpha : ws[q], r));
-      }
-      if (WC == nw) __syncthreads();
-      else asm volatile("bar.sync 1, %0;" ::"r"(WC * 32) : "memory");
-      // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter ------
-      // kLPC lanes per contact: lane a < 3 owns frame row / component a; the
-      // projection needs all three components and is evaluated redundantly.
-      if (HASC && !check_only) {
-        const int a = (lane & (kLPC - 1)) < 3 ? (lane & (kLPC - 1)) : 2;
-        const bool owner = (lane & (kLPC - 1)) < 3;
-        const int qbase = lane & ~(kLPC - 1);
-        for (int k0 = warp * (32 / kLPC); k0 < C; k0 += WC * (32 / kLPC)) {
-          const int k = k0 + lane / kLPC;
-          const bool act = k < C;
-          const int kk = act ? k : k0;
-          const int code = cq[kk];
-          const int qb = code & 0x3fffffff;
-          const bool dj = (code >> 30) & 1;
-          const double* R9 = cfr + 9 * kk;
-          double rel[3];
+      const int CD = CR / 3 - C;  // two-sided contacts of the CTA
+      for (int k = tid; k < C; k += WC * 32) {
+        const int code = cq[k];
+        const bool dj = (code >> 30) & 1;
+        const int kd = code & 0x3fffffff;
+        int qs[6];
+        qs[0] = k;
+        qs[1] = C + k;
+        qs[2] = 2 * C + k;
+        qs[3] = 3 * C + kd;
+        qs[4] = qs[3] + CD;
+        qs[5] = qs[4] + CD;
+        // (1) surrogate-dynamics sweep of the contact's rows (3 chains at a time)
+        double vsr[6];
 #pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            const double xi = vs_s[qb + t];
-            rel[t] = dj ? dsub(xi, vs_s[qb + 3 + t]) : xi;
-          }
-          const double vi_a = vs_s[qb + a];
-          const double vj_a = dj ? vs_s[qb + 3 + a] : 0.0;
-          const double eta_a = dadd(dadd(dmul(R9[3 * a + 0], rel[0]), dmul(R9[3 * a + 2], rel[2])),
-                                    dmul(R9[3 * a + 1], rel[1]));
-          double g;
-          if (use_alpha) g = dj ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
-          else g = cpar[4 * kk + 3];
-          const double ls_a = ddiv(-dadd(eta_a, a == 0 ? cpar[4 * kk + 2] : 0.0), g);
-          double lam[3];
-          lam[0] = __shfl_sync(0xffffffffu, ls_a, qbase + 0);
-          lam[1] = __shfl_sync(0xffffffffu, ls_a, qbase + 1);
-          lam[2] = __shfl_sync(0xffffffffu, ls_a, qbase + 2);
-          if (act) {
-            project(OP, lam, cpar[4 * kk + 0], cpar[4 * kk + 1]);
-            if (owner) {
-              lam_out[3 * k + a] = lam[a];
-              const double wa = dadd(dadd(dmul(R9[a], lam[0]), dmul(R9[3 + a], lam[1])), dmul(R9[6 + a], lam[2]));
-              const double oi = dadd(0.0, wa);  // np.add.at onto zeros
-              jt_s[qb + a] = oi;
-              finish_row(qb + a, dadd(vi_a, dmul(use_alpha ? alpha : ws[qb + a], oi)));
-              if (dj) {
-                const double oj = dsub(0.0, wa);  // np.subtract.at onto zeros
-                jt_s[qb + 3 + a] = oj;
-                finish_row(qb + 3 + a, dadd(vj_a, dmul(use_alpha ? alpha : ws[qb + 3 + a], oj)));
-              }
-            }
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !dj) break;
+          double dot[3];
+          row_dot3(sv, mp, sb, rlen, xs, vown, qs[3 * h], qs[3 * h + 1], qs[3 * h + 2], dot);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const int q = qs[3 * h + a];
+            const double r = dsub(dot[a], bs[q]);
+            const double f = dsub(r, jt_s[q]);
+            fr = dadd(fr, dmul(f, f));
+            vsr[3 * h + a] = dsub(vown[q], dmul(use_alpha ? alpha : ws[q], r));
           }
         }
+        if (profl) { __syncwarp(__activemask()); if ((tid & 31) == __ffs(__activemask()) - 1) atomicMax(&sm_role_end[2], (unsigned long long)clock64()); }
+        if (!HASC || check_only) continue;
+        // (2) gather + (3) one-shot projection (solver.py:262-281)
+        const double* R9 = cfr + 9 * k;
+        double rel[3], eta[3], lam[3], wv[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) rel[t] = dj ? dsub(vsr[t], vsr[3 + t]) : vsr[t];
+        frame_apply(R9, rel, eta);
+        double g;
+        if (use_alpha) g = dj ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
+        else g = cpar[4 * k + 3];
+        trial_impulse(eta, cpar[4 * k + 2], g, lam);
+        project(OP, lam, cpar[4 * k + 0], cpar[4 * k + 1]);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) lam_out[3 * k + t] = lam[t];
+        // (2') scatter J_c^T lam and v_new = v* + w J_c^T lam
+        frame_apply_t(R9, lam, wv);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const int q = qs[a];
+          const double oi = dadd(0.0, wv[a]);  // np.add.at onto zeros
+          jt_s[q] = oi;
+          finish_row(q, dadd(vsr[a], dmul(use_alpha ? alpha : ws[q], oi)));
+        }
+        if (dj) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const int q = qs[3 + a];
+            const double oj = dsub(0.0, wv[a]);  // np.subtract.at onto zeros
+            jt_s[q] = oj;
+            finish_row(q, dadd(vsr[3 + a], dmul(use_alpha ? alpha : ws[q], oj)));
+          }
+        }
+        if (profl) { __syncwarp(__activemask()); if ((tid & 31) == __ffs(__activemask()) - 1) atomicMax(&sm_role_end[4], (unsigned long long)clock64()); }
       }
       if (profl && lane == 0) atomicMax(&sm_role_end[0], (unsigned long long)clock64());
     }
@@ -467,10 +525,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     // ---- (4) residual partials + grid barrier (reduction at the top of l+1)
     stamp(4);
     if (profl && tid == 0) {
-      p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 8 + 6] = (long long)sm_role_end[0];
-      p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 8 + 1] = (long long)sm_role_end[1];
-      sm_role_end[0] = 0;
-      sm_role_end[1] = 0;
+      p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 16 + 6] = (long long)sm_role_end[0];
+      p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 16 + 1] = (long long)sm_role_end[1];
+      for (int t = 2; t < 5; ++t) p.prof[((size_t)b * 4 + (l - p.prof_iter0)) * 16 + 6 + t] = (long long)sm_role_end[t];
+      for (int t = 0; t < 8; ++t) sm_role_end[t] = 0;
     }
     stamp(7);
     {

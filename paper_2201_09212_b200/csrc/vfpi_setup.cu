@@ -21,9 +21,7 @@ namespace {
 // shared-memory footprint, which also tracks per-iteration work): 24 B per
 // numeric entry (value, column, destination, product), 40 B per row, 256 B
 // per contact.
-constexpr int kEntryCost = 24;
-constexpr int kRowCost = 40;
-constexpr int kContactCost = 256;
+// (defaults in LayoutOptions: entry 24, row 40, contact 256)
 
 #define VFPI_CK(x)                                                     \
   do {                                                                 \
@@ -131,7 +129,8 @@ __global__ void k_unit_keys(int n, const int* __restrict__ mark, const int* __re
 // per sorted unit t (anchor order): cost / rows / contact indicators
 __global__ void k_units(int n, const int* __restrict__ skey, const int* __restrict__ U, const int* __restrict__ mark,
                         const int* __restrict__ ci, const int* __restrict__ cj, const int* __restrict__ rowcnt,
-                        int64_t* ucost, int* urows, int* ucont, int* ucr, int* ufr) {
+                        int64_t* ucost, int* urows, int* ucont, int* ucr, int* ufr, int kEntryCost, int kRowCost,
+                        int kContactCost) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > n) return;
   int64_t cost = 0;
@@ -260,9 +259,9 @@ __device__ __forceinline__ int owner(const int* __restrict__ starts, int G, int 
   return lo;
 }
 
-// Row list: within every CTA range, the rows of its contact units come first
-// (unit order), then its free rows (unit order). cont_q = local position of
-// each contact's first row. t = sorted unit index, U[t] = its start row.
+// Row list: within every CTA range, the rows of its contact units come first,
+// then its free rows (unit order). cont_q = rank of a two-sided contact among
+// the CTA's two-sided contacts. t = sorted unit index, U[t] = its start row.
 __global__ void k_fill(int n, int G, const int* __restrict__ U, const int* __restrict__ mark,
                        const int* __restrict__ ci, const int* __restrict__ cj, const int* __restrict__ urows,
                        const int* __restrict__ rpos, const int* __restrict__ kpos, const int* __restrict__ cposc,
@@ -281,20 +280,29 @@ __global__ void k_fill(int n, int G, const int* __restrict__ U, const int* __res
     row_slot[p] = -1;
     return;
   }
-  const int p = blk_row[b] + (cposc[t] - cposc[f]);
+  // contact rows are component-major: row a of side i of local contact kl at
+  // a*C + kl, row a of side j at 3C + a*CD + kd (kd = rank among the CTA's
+  // two-sided contacts), so lane kl of the resident kernel reads its rows
+  // from consecutive SELL lanes
   const int k = kpos[t];
-  const int loc = (k - blk_ct[b]) * kSlotsPerContact;
+  const int kl = k - blk_ct[b];
+  const int Cb = blk_ct[b + 1] - blk_ct[b];
+  const int CDb = blk_cr[b] / 3 - Cb;
+  const int kd = (cposc[t] - cposc[f]) / 3 - kl;
+  const int loc = kl * kSlotsPerContact;
   cont_list[k] = m;
-  cont_q[k] = p - blk_row[b];
+  cont_q[k] = kd;
   const int i = ci[m], j = cj[m];
   for (int q = 0; q < 3; ++q) {
-    row_list[p + q] = i + q;
-    row_slot[p + q] = loc + q;
+    const int p = blk_row[b] + q * Cb + kl;
+    row_list[p] = i + q;
+    row_slot[p] = loc + q;
   }
   if (j >= 0)
     for (int q = 0; q < 3; ++q) {
-      row_list[p + 3 + q] = j + q;
-      row_slot[p + 3 + q] = loc + 3 + q;
+      const int p = blk_row[b] + 3 * Cb + q * CDb + kd;
+      row_list[p] = j + q;
+      row_slot[p] = loc + 3 + q;
     }
 }
 
@@ -740,7 +748,8 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
     ws.unit_order_is_sorted = opt.anchor_order;
     k_units<<<nblk(n + 1), 256, 0, st>>>(n, skey, uord, P<int>(ws.mark), s.col_i, s.col_j,
                                          P<int>(ws.rowcnt), P<int64_t>(ws.ucost), P<int>(ws.urows), P<int>(ws.ucont),
-                                         P<int>(ws.ucr), P<int>(ws.ufr));
+                                         P<int>(ws.ucr), P<int>(ws.ufr), opt.entry_cost, opt.row_cost,
+                                         opt.contact_cost);
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.ucost), P<int64_t>(ws.cpos), n, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.urows), P<int>(ws.rpos), n, st));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.ucont), P<int>(ws.kpos), n, st));

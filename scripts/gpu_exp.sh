@@ -1,4 +1,3 @@
 python -m paper_2201_09212_b200.build
-timeout 900 python -m pytest tests -m gpu -q -x --tb=short -p no:cacheprovider 2>&1 | tail -2
-timeout 300 python scripts/exp_variants.py 2>&1 | tail -5
-timeout 300 python scripts/bench_scenes_kernel.py --reps 2 2>&1 | tail -1
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -1
+timeout 300 python scripts/prof_phases.py 2>&1 | grep -v WC

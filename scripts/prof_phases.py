@@ -22,9 +22,9 @@ print("layout", h.last_layout(), "loop_ms", rep.timings["loop_s"] * 1e3, "setup_
 h.L.vfpi_set_profile(h.h, 500)
 solve_packed(ps, cfg, np.zeros(ps.n))
 G = h.last_layout()["ctas"]
-buf = (C.c_longlong * (32 * G))()
-h.L.vfpi_get_profile(h.h, buf, 32 * G)
-a = np.frombuffer(buf, dtype=np.int64).reshape(G, 4, 8)
+buf = (C.c_longlong * (64 * G))()
+h.L.vfpi_get_profile(h.h, buf, 64 * G)
+a = np.frombuffer(buf, dtype=np.int64).reshape(G, 4, 16)
 def show(nm, d):
     print(f"{nm:22s} cycles mean {d.mean():9.0f}  max {d.max():9.0f}  min {d.min():9.0f}")
 show("products", a[:, :, 2] - a[:, :, 0])
@@ -37,6 +37,12 @@ tot = a[:, :, 5] - a[:, :, 0]
 print(f"{'iteration':16s} cycles mean {tot.mean():9.0f}  max {tot.max():9.0f}")
 work = a[:, :, 4] - a[:, :, 0]
 print("work (pre-barrier) per CTA: mean", work.mean(), "max", work.max(), "argmax cta", int(work.mean(1).argmax()))
+for b_ in (0, 20, 40, 55, 60, 61, 62, 63, 64, 80, 100, 147):
+    r = a[b_].mean(0)
+    print(f"cta {b_:3d}: stage {r[2]-r[0]:6.0f} passB {r[3]-r[2]:6.0f} role {r[4]-r[3]:6.0f} "
+          f"cw {r[6]-r[3] if r[6] > 0 else 0:6.0f} fw {r[1]-r[3] if r[1] > 0 else 0:6.0f} red+bar {r[5]-r[4]:6.0f}"
+          + (f" | sweep {r[8]-r[3]:6.0f} oneshot {r[10]-r[8]:6.0f}"
+             if r[8] > 0 else ""))
 arr = a[:, :, 7]
 print("arrival skew (globaltimer ns) per iteration:", (arr.max(0) - arr.min(0)).tolist())
 h.L.vfpi_set_profile(h.h, 0)
