@@ -156,9 +156,9 @@ int vfpi_set_kernel(vfpi_handle* h, int mode);
 int vfpi_set_profile(vfpi_handle* h, int iter0);
 int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
 /* Tuning knobs. key 0: force the resident kernel's contact-warp count (0 = auto);
- * key 1: order units by their smallest referenced column (default 0 = row order);
+ * key 1: order units by their smallest referenced column (default 1; 0 = row order);
  * key 2: sort each CTA's free rows by decreasing length (default 1);
- * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 256). */
+ * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0). */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

@@ -131,9 +131,9 @@ struct Workspace;  // device buffers owned by a handle
 // Layout setup on the stream: statistics, contact-aware CTA partition and
 // sizes (ends with one host read of the summary). Returns VFPI_* code.
 struct LayoutOptions {
-  bool anchor_order = false;  // order units by their smallest referenced column
+  bool anchor_order = true;   // order units by their smallest referenced column
   bool length_sort = true;    // free rows of a CTA by decreasing length
-  int entry_cost = 24, row_cost = 40, contact_cost = 256;  // partition cost model
+  int entry_cost = 24, row_cost = 40, contact_cost = 0;  // partition cost model
   // scene batches: CTA b = scene b (device arrays, G+1 entries each); contacts
   // must be grouped by scene and never couple two scenes
   const int* scene_row_ptr = nullptr;

@@ -15,6 +15,10 @@ if "--nocontacts" in sys.argv:
     from paper_2201_09212_b200.system import make_packed
     ps = make_packed(ps.n, ps.indptr, ps.indices, ps.data, ps.b, [], [], [], [])
 h = _lib.handle(0)
+for a in sys.argv[1:]:  # key=value tuning knobs, e.g. 1=1 5=0 (anchor order, contact cost)
+    if "=" in a:
+        k_, v_ = a.split("=")
+        h.L.vfpi_set_tuning(h.h, int(k_), int(v_))
 cfg = SolverConfig(residual_tol=0.0, max_iters=1000)
 solve_packed(ps, cfg, np.zeros(ps.n))
 v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
