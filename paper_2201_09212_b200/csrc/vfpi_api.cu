@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -30,8 +31,18 @@ cudaError_t vfpi::ensure_max_dynamic_smem(const void* fn) {
   return e;
 }
 
+// A captured setup phase: replayed as one graph launch when the next solve has
+// the same shapes, input pointers, options and workspace allocations (key).
+struct SetupGraph {
+  std::vector<uint64_t> key, last_key;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+};
+
 struct vfpi_handle {
   Workspace ws;
+  SetupGraph graph_layout, graph_pack;
+  int use_graphs = 1;
   std::string err;
   int64_t launches = 0;
   // last solve (device path) bookkeeping for vfpi_wait
@@ -72,6 +83,58 @@ int choose_blocks(const vfpi_system& s, int num_sms) {
 int choose_blocks_resident(const vfpi_system& s, int num_sms) {
   const int64_t by_nnz = (s.nnz + 2047) / 2048;
   return (int)std::max<int64_t>(1, std::min<int64_t>(by_nnz, num_sms));
+}
+
+// Run a setup phase: eagerly the first time a key is seen (this is where the
+// workspace grows), captured into a graph the second time, replayed after.
+template <class F>
+int run_setup_phase(vfpi_handle* h, SetupGraph& g, std::vector<uint64_t> key, cudaStream_t st, F&& body) {
+  const bool capturable = h->use_graphs && st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread;
+  key.push_back(vfpi::alloc_generation());
+  key.push_back((uint64_t)(uintptr_t)st);
+  if (!capturable) return body();
+  if (g.exec && g.key == key) {
+    CK(cudaGraphLaunch(g.exec, st));
+    h->launches += g.launches;
+    return VFPI_OK;
+  }
+  if (g.last_key != key) {
+    g.last_key = key;
+    return body();
+  }
+  const int64_t l0 = h->launches;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  const int rc = body();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(st, &graph);
+  if (rc != VFPI_OK || e != cudaSuccess || vfpi::alloc_generation() != key[key.size() - 2]) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    g.last_key.clear();
+    h->launches = l0;
+    return rc != VFPI_OK ? rc : body();  // capture not possible: run eagerly
+  }
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g.exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    g.exec = nullptr;
+    g.last_key.clear();
+    h->launches = l0;
+    return body();
+  }
+  g.key = key;
+  g.launches = h->launches - l0;
+  CK(cudaGraphLaunch(g.exec, st));
+  return VFPI_OK;
+}
+
+std::vector<uint64_t> system_key(const vfpi_system& d, int G) {
+  return {(uint64_t)d.n, (uint64_t)d.n_c, (uint64_t)d.nnz, (uint64_t)G, (uint64_t)(uintptr_t)d.indptr,
+          (uint64_t)(uintptr_t)d.indices, (uint64_t)(uintptr_t)d.data, (uint64_t)(uintptr_t)d.b,
+          (uint64_t)(uintptr_t)d.col_i, (uint64_t)(uintptr_t)d.col_j, (uint64_t)(uintptr_t)d.frames,
+          (uint64_t)(uintptr_t)d.mu, (uint64_t)(uintptr_t)d.mu2, (uint64_t)(uintptr_t)d.phi};
 }
 
 int upload(vfpi_handle* h, Workspace::Buf& b, const void* src, size_t bytes) {
@@ -193,6 +256,8 @@ void vfpi_destroy(vfpi_handle* h) {
     if (b->p) cudaFree(b->p);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
+  for (SetupGraph* g : {&h->graph_layout, &h->graph_pack})
+    if (g->exec) cudaGraphExecDestroy(g->exec);
   if (h->ws.stream) cudaStreamDestroy(h->ws.stream);
   if (h->ws.h_summary) cudaFreeHost(h->ws.h_summary);
   if (h->ws.h_status) cudaFreeHost(h->ws.h_status);
@@ -274,8 +339,19 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   vfpi::SetupSummary* hs = ws.h_summary;
   // first choice: the whole partition of every CTA resident in shared memory
   int G = choose_blocks_resident(*d, ws.num_sms);
-  rc = vfpi::setup_layout(ws, *d, G, st, hs, h->err, h->launches, h->layout_opt);
-  if (rc) return rc;
+  {
+    std::vector<uint64_t> key = system_key(*d, G);
+    const vfpi::LayoutOptions& o = h->layout_opt;
+    for (uint64_t x : {(uint64_t)o.anchor_order, (uint64_t)o.length_sort, (uint64_t)o.entry_cost,
+                       (uint64_t)o.row_cost, (uint64_t)o.contact_cost})
+      key.push_back(x);
+    rc = run_setup_phase(h, h->graph_layout, key, st, [&] {
+      return vfpi::setup_layout_async(ws, *d, G, st, h->err, h->launches, h->layout_opt);
+    });
+    if (rc) return rc;
+    rc = vfpi::setup_layout_finish(ws, st, hs, h->err);
+    if (rc) return rc;
+  }
   const size_t smem_res = (size_t)hs->max_res_bytes;
   const bool fits = hs->max_ent_per_blk < (1 << 24) && smem_res + 2048 <= (size_t)ws.max_smem_optin && G <= 256;
   if (h->kernel_mode == 1 && !fits) { h->err = "partition does not fit in shared memory"; return VFPI_UNSUPPORTED; }
@@ -293,7 +369,16 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
       G = bps * ws.num_sms;
     }
   }
-  rc = vfpi::setup_pack(ws, *d, G, resident, *hs, st, h->err, h->launches);
+  if (resident) {
+    std::vector<uint64_t> key = system_key(*d, G);
+    for (uint64_t x : {(uint64_t)hs->n_slices, (uint64_t)hs->sell_elems, (uint64_t)hs->nnz_num})
+      key.push_back(x);
+    rc = run_setup_phase(h, h->graph_pack, key, st, [&] {
+      return vfpi::setup_pack(ws, *d, G, true, *hs, st, h->err, h->launches);
+    });
+  } else {
+    rc = vfpi::setup_pack(ws, *d, G, false, *hs, st, h->err, h->launches);
+  }
   if (rc) return rc;
   const size_t smem_res_full = smem_res;
   rc = vfpi::setup_step_matrix(ws, *d, *cfg, w_cached, st, h->err, h->launches);

@@ -139,8 +139,18 @@ struct LayoutOptions {
   const int* scene_row_ptr = nullptr;
   const int* scene_ct_ptr = nullptr;
 };
-int setup_layout(Workspace& ws, const vfpi_system& dsys, int G, cudaStream_t st, SetupSummary* host_summary,
-                 std::string& err, int64_t& launches, const LayoutOptions& opt = LayoutOptions());
+// setup_layout = setup_layout_async (kernels only, capturable into a graph) +
+// setup_layout_finish (the one host read of the summary, input checks)
+int setup_layout_async(Workspace& ws, const vfpi_system& dsys, int G, cudaStream_t st, std::string& err,
+                       int64_t& launches, const LayoutOptions& opt);
+int setup_layout_finish(Workspace& ws, cudaStream_t st, SetupSummary* host_summary, std::string& err);
+inline int setup_layout(Workspace& ws, const vfpi_system& dsys, int G, cudaStream_t st, SetupSummary* host_summary,
+                        std::string& err, int64_t& launches, const LayoutOptions& opt = LayoutOptions()) {
+  const int rc = setup_layout_async(ws, dsys, G, st, err, launches, opt);
+  return rc ? rc : setup_layout_finish(ws, st, host_summary, err);
+}
+// generation counter of workspace (re)allocations (captured setup graphs key on it)
+uint64_t alloc_generation();
 // Row-sorted entries packed for the chosen iteration kernel:
 // resident = CTA-contiguous CSR (pos_ptr/pk_val/pk_col), else SELL-32.
 int setup_pack(Workspace& ws, const vfpi_system& dsys, int G, bool resident, const SetupSummary& hs,

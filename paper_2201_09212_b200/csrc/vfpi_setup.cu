@@ -8,6 +8,7 @@
 //   surrogate_gamma / _check_tie solver.py:244-259
 //   fixed-alpha default          solver.py:367-369
 #include <cub/cub.cuh>
+#include <atomic>
 #include <climits>
 
 #include "vfpi_internal.cuh"
@@ -628,9 +629,14 @@ __global__ void k_fill_int(int* p, int v, int64_t n) {
 
 }  // namespace
 
+static std::atomic<uint64_t> g_alloc_gen{0};
+
+uint64_t alloc_generation() { return g_alloc_gen.load(); }
+
 cudaError_t ensure(Workspace::Buf& b, size_t bytes) {
   if (bytes == 0) bytes = 8;
   if (b.cap >= bytes) return cudaSuccess;
+  g_alloc_gen.fetch_add(1);  // invalidates captured setup graphs
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.cap = 0;
@@ -651,7 +657,7 @@ static int end_bit_for(int64_t v) {
 
 // Phase 1: column statistics, contact marks, partition into G CTAs, slice
 // widths. Ends with ONE host read of the summary (sizes + flags).
-int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, SetupSummary* hs, std::string& err,
+int setup_layout_async(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, std::string& err,
                  int64_t& launches, const LayoutOptions& opt) {
   const int n = (int)s.n, n_c = (int)s.n_c;
   const int64_t nnz = s.nnz;
@@ -774,20 +780,27 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
                                 P<int>(ws.blk_first), P<int>(ws.blk_cr), P<int>(ws.cposc),
                                 P<SetupSummary>(ws.summary));
   ++launches;
+  // with the length sort, k_fill writes a scratch list that the permutation
+  // copies into row_list (fixed buffer roles: replayable as a captured graph)
+  const bool lsort = opt.length_sort && n > 0 && G <= 4096;
+  if (lsort) {
+    VFPI_CK(ensure(ws.row_list2, 4 * (size_t)n));
+    VFPI_CK(ensure(ws.row_slot2, 4 * (size_t)n));
+  }
+  int* fill_list = lsort ? P<int>(ws.row_list2) : P<int>(ws.row_list);
+  int* fill_slot = lsort ? P<int>(ws.row_slot2) : P<int>(ws.row_slot);
   if (n > 0) {
     k_fill<<<nblk(n), 256, 0, st>>>(n, G, opt.anchor_order ? P<int>(ws.uorder) : P<int>(ws.uval), P<int>(ws.mark),
                                     s.col_i, s.col_j, P<int>(ws.urows),
                                     P<int>(ws.rpos),
                                     P<int>(ws.kpos), P<int>(ws.cposc), P<int>(ws.cposf), P<int>(ws.blk_row),
-                                    P<int>(ws.blk_ct), P<int>(ws.blk_first), P<int>(ws.blk_cr), P<int>(ws.row_list),
-                                    P<int>(ws.row_slot), P<int>(ws.cont_list), P<int>(ws.cont_q));
+                                    P<int>(ws.blk_ct), P<int>(ws.blk_first), P<int>(ws.blk_cr), fill_list,
+                                    fill_slot, P<int>(ws.cont_list), P<int>(ws.cont_q));
     ++launches;
   }
   VFPI_CK(cudaGetLastError());
-  if (opt.length_sort && n > 0 && G <= 4096) {
-    VFPI_CK(ensure(ws.row_list2, 4 * (size_t)n));
-    VFPI_CK(ensure(ws.row_slot2, 4 * (size_t)n));
-    k_row_keys<<<nblk(n), 256, 0, st>>>(n, G, P<int>(ws.row_list), P<int>(ws.row_slot), P<int>(ws.rowcnt),
+  if (lsort) {
+    k_row_keys<<<nblk(n), 256, 0, st>>>(n, G, fill_list, fill_slot, P<int>(ws.rowcnt),
                                         P<int>(ws.blk_row), P<int>(ws.ukey), P<int>(ws.uval));
     size_t tr = 0;
     const int eb = end_bit_for((int64_t)G << 9);
@@ -797,10 +810,8 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
     tb = ws.cub_tmp.cap;
     VFPI_CK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.ukey), P<int>(ws.ukey_s), P<int>(ws.uval),
                                             P<int>(ws.uorder), n, 0, eb, st));
-    k_row_permute<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.uorder), P<int>(ws.row_list), P<int>(ws.row_slot),
-                                           P<int>(ws.row_list2), P<int>(ws.row_slot2));
-    std::swap(ws.row_list, ws.row_list2);
-    std::swap(ws.row_slot, ws.row_slot2);
+    k_row_permute<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.uorder), fill_list, fill_slot, P<int>(ws.row_list),
+                                           P<int>(ws.row_slot));
     launches += 2 + 2 + (eb + 7) / 8;
   }
   // slice count is data dependent but bounded by S_max; slices past the real
@@ -847,12 +858,14 @@ int setup_layout(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, Se
   k_summary<<<1, kFixThreads, 0, st>>>(n, G, P<int64_t>(ws.row_ptr), P<int64_t>(ws.slice_off), P<int64_t>(ws.pos_ptr),
                              P<int>(ws.blk_row), P<int>(ws.blk_ct), P<int>(ws.blk_cr), P<int>(ws.blk_slice),
                              P<int>(ws.sec_ptr), P<int>(ws.flags), P<SetupSummary>(ws.summary));
-  launches += 3;
-  launches += 3;
+  launches += 6;
   VFPI_CK(cudaGetLastError());
+  return VFPI_OK;
+}
+
+int setup_layout_finish(Workspace& ws, cudaStream_t st, SetupSummary* hs, std::string& err) {
   VFPI_CK(cudaMemcpyAsync(hs, ws.summary.p, sizeof(SetupSummary), cudaMemcpyDeviceToHost, st));
   VFPI_CK(cudaStreamSynchronize(st));
-  const int S = hs->n_slices;
   if (hs->flags & 2) { err = "contact column index out of range"; return VFPI_BAD_ARGUMENT; }
   if (hs->flags & 1) {
     err = "two contacts share a node column (nodalization guarantees one contact per node, contacts.py:242-268)";
