@@ -123,7 +123,7 @@ __global__ void k_unit_keys(int n, const int* __restrict__ mark, const int* __re
       for (int t = 0; t < 3; ++t) k = min(k, rowmin[j + t]);
     }
   }
-  key[r] = (k == INT_MAX || anchor) ? k : r;  // natural order: the start row itself
+  key[r] = (k == INT_MAX) ? n : (anchor ? k : r);  // non-start rows: n; natural order: the start row itself
   val[r] = r;
 }
 
@@ -136,7 +136,7 @@ __global__ void k_units(int n, const int* __restrict__ skey, const int* __restri
   if (t > n) return;
   int64_t cost = 0;
   int rows = 0, ct = 0;
-  if (t < n && skey[t] != INT_MAX) {
+  if (t < n && skey[t] < n) {
     const int r = U[t];
     const int m = mark[r];
     if (m < 0) {
@@ -330,19 +330,24 @@ __global__ void k_row_permute(int n, const int* __restrict__ perm, const int* __
   row_slot2[p] = row_slot[perm[p]];
 }
 
+// warp per slice: width = longest row of its (up to) 32 rows
 __global__ void k_slice_width(int S_max, int G, const SetupSummary* __restrict__ sum,
                               const int* __restrict__ blk_slice, const int* __restrict__ blk_row,
                               const int* __restrict__ row_list, const int* __restrict__ rowcnt, int64_t* width) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (s > S_max) return;
   const int S = sum->n_slices;
-  if (s >= S) { width[s] = 0; return; }
+  if (s >= S) {
+    if (lane == 0) width[s] = 0;
+    return;
+  }
   const int b = owner(blk_slice, G, s);
-  const int p0 = blk_row[b] + (s - blk_slice[b]) * 32;
-  const int p1 = min(p0 + 32, blk_row[b + 1]);
-  int W = 0;
-  for (int p = p0; p < p1; ++p) W = max(W, rowcnt[row_list[p]]);
-  width[s] = 32 * (int64_t)W;
+  const int p = blk_row[b] + (s - blk_slice[b]) * 32 + lane;
+  int W = p < blk_row[b + 1] ? rowcnt[row_list[p]] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) W = max(W, __shfl_xor_sync(0xffffffffu, W, o));
+  if (lane == 0) width[s] = 32 * (int64_t)W;
 }
 
 __global__ void k_poslen(int n, const int* __restrict__ row_list, const int* __restrict__ rowcnt, int64_t* len) {
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int
 // Every CTA stages, once per iteration, the 32-byte sectors of v its entries
 // read from other CTAs' rows; columns that are its own rows read the on-chip
 // copy. Built in phase 1 from the CSC entries (so the shared-memory size is
-// known at the single host read): key = (cta << 24) | sector, radix sorted,
+// known at the single host read): key = (cta << SB) | sector, radix sorted,
 // first-of-run flags -> block-major unique sector list secs + per-CTA ranges.
 // sell_map[i] (phase 2) encodes where SELL element i's x comes from:
 //   0x80000000 | q  -> own row q (local position),  else 4*slot + (col & 3).
@@ -413,7 +418,7 @@ __global__ void k_rowpos(int n, int G, const int* __restrict__ row_list, const i
 // CTA does not own its column
 __global__ void k_sec_keys(int n, const int* __restrict__ indptr, const int* __restrict__ indices,
                            const double* __restrict__ data, const int* __restrict__ rowblk,
-                           unsigned* __restrict__ key) {
+                           unsigned* __restrict__ key, int SB) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int bj = rowblk[j];
@@ -421,7 +426,7 @@ __global__ void k_sec_keys(int n, const int* __restrict__ indptr, const int* __r
     unsigned k = kNoSector;
     if (data[e] != 0.0) {
       const int b = rowblk[indices[e]];
-      if (b != bj) k = ((unsigned)b << 24) | ((unsigned)j >> 2);
+      if (b != bj) k = ((unsigned)b << SB) | ((unsigned)j >> 2);
     }
     key[e] = k;
   }
@@ -436,29 +441,41 @@ __global__ void k_sec_flags(int64_t N, const unsigned* __restrict__ skey, int* _
 
 // unique sector list (sector ids) and the first unique index of every CTA
 __global__ void k_sec_emit(int64_t N, const unsigned* __restrict__ skey, const int* __restrict__ flag,
-                           const int* __restrict__ upos, unsigned* __restrict__ secs, int* __restrict__ sec_ptr) {
+                           const int* __restrict__ upos, unsigned* __restrict__ secs, int* __restrict__ sec_ptr, int SB) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= N || !flag[j]) return;
   const unsigned k = skey[j];
-  secs[upos[j]] = k & 0xFFFFFFu;
-  const int b = (int)(k >> 24);
-  if (j == 0 || (skey[j - 1] >> 24) != (unsigned)b || skey[j - 1] == kNoSector) sec_ptr[b] = upos[j];
+  secs[upos[j]] = k & ((1u << SB) - 1u);
+  const int b = (int)(k >> SB);
+  if (j == 0 || (skey[j - 1] >> SB) != (unsigned)b || skey[j - 1] == kNoSector) sec_ptr[b] = upos[j];
 }
 
 // CTAs without remote sectors inherit the next start; sec_ptr[G] = total
-__global__ void k_sec_ptr_fix(int G, int64_t N, const int* __restrict__ flag, const int* __restrict__ upos,
-                              int* __restrict__ sec_ptr) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  sec_ptr[G] = N > 0 ? upos[N - 1] + flag[N - 1] : 0;
-  for (int b = G - 1; b >= 0; --b)
-    if (sec_ptr[b] < 0) sec_ptr[b] = sec_ptr[b + 1];
+// (one CTA, G < blockDim.x: suffix minimum)
+__global__ void __launch_bounds__(1024) k_sec_ptr_fix(int G, int64_t N, const int* __restrict__ flag,
+                                                      const int* __restrict__ upos, int* __restrict__ sec_ptr) {
+  __shared__ int sp[1025];
+  const int b = threadIdx.x;
+  const int total = N > 0 ? upos[N - 1] + flag[N - 1] : 0;
+  if (b <= G) {
+    const int v = (b == G) ? total : sec_ptr[b];
+    sp[b] = v < 0 ? INT_MAX : v;
+  }
+  __syncthreads();
+  for (int o = 1; o <= G; o <<= 1) {
+    const int v = (b <= G) ? ((b + o <= G) ? min(sp[b], sp[b + o]) : sp[b]) : 0;
+    __syncthreads();
+    if (b <= G) sp[b] = v;
+    __syncthreads();
+  }
+  if (b <= G) sec_ptr[b] = sp[b];
 }
 
 // one CTA per partition: its sector list in shared memory, gather map of every
 // SELL element of the partition (binary search on chip)
 constexpr int kMapSmemSectors = 8192;
 
-__global__ void __launch_bounds__(256) k_sell_map(int G, const int* __restrict__ blk_slice,
+__global__ void __launch_bounds__(1024) k_sell_map(int G, const int* __restrict__ blk_slice,
                                                   const int* __restrict__ blk_row, const int64_t* __restrict__ slice_off,
                                                   const int* __restrict__ sell_col, const int* __restrict__ rowpos,
                                                   const unsigned* __restrict__ secs, const int* __restrict__ sec_ptr,
@@ -736,18 +753,18 @@ int setup_layout_async(Workspace& ws, const vfpi_system& s, int G, cudaStream_t 
   if (n > 0) {
     k_unit_keys<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.mark), s.col_i, s.col_j, P<int>(ws.rowmin), P<int>(ws.ukey),
                                          P<int>(ws.uval), opt.anchor_order ? 1 : 0);
-    // natural order: keys are already the start rows (non-starts = INT_MAX stay
+    // natural order: keys are already the start rows (non-starts = n stay
     // interleaved as empty units), so only the anchor order needs a sort
     int* skey = P<int>(ws.ukey);
     int* uord = P<int>(ws.uval);
     if (opt.anchor_order) {
       size_t tu = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tu, P<int>(ws.ukey), P<int>(ws.ukey_s), P<int>(ws.uval),
-                                      P<int>(ws.uorder), n, 0, 32, st);
+                                      P<int>(ws.uorder), n, 0, end_bit_for(n), st);
       VFPI_CK(ensure(ws.cub_tmp, tu));
       tb = ws.cub_tmp.cap;
       VFPI_CK(cub::DeviceRadixSort::SortPairs(ws.cub_tmp.p, tb, P<int>(ws.ukey), P<int>(ws.ukey_s), P<int>(ws.uval),
-                                              P<int>(ws.uorder), n, 0, 32, st));
+                                              P<int>(ws.uorder), n, 0, end_bit_for(n), st));
       skey = P<int>(ws.ukey_s);
       uord = P<int>(ws.uorder);
     }
@@ -816,7 +833,7 @@ int setup_layout_async(Workspace& ws, const vfpi_system& s, int G, cudaStream_t 
   }
   // slice count is data dependent but bounded by S_max; slices past the real
   // count get width 0, so one scan over S_max+1 entries suffices.
-  k_slice_width<<<nblk(S_max + 1), 256, 0, st>>>(S_max, G, P<SetupSummary>(ws.summary), P<int>(ws.blk_slice),
+  k_slice_width<<<nblk((int64_t)(S_max + 1) * 32), 256, 0, st>>>(S_max, G, P<SetupSummary>(ws.summary), P<int>(ws.blk_slice),
                                                  P<int>(ws.blk_row), P<int>(ws.row_list), P<int>(ws.rowcnt),
                                                  P<int64_t>(ws.slice_w));
   VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int64_t>(ws.slice_w), P<int64_t>(ws.slice_off),
@@ -837,20 +854,26 @@ int setup_layout_async(Workspace& ws, const vfpi_system& s, int G, cudaStream_t 
     VFPI_CK(ensure(ws.rowblk, 4 * (size_t)n));
     k_rowpos<<<nblk(n), 256, 0, st>>>(n, G, P<int>(ws.row_list), P<int>(ws.blk_row), P<int>(ws.rowpos),
                                       P<int>(ws.rowblk));
-    k_sec_keys<<<nblk(n), 256, 0, st>>>(n, s.indptr, s.indices, s.data, P<int>(ws.rowblk), P<unsigned>(ws.sec_key));
+    // key bits: CTA above the sector id; every real key stays below the
+    // all-ones kNoSector (both fields strictly below their maxima)
+    int SB = end_bit_for((n - 1) / 4 + 1);
+    int KB = SB + end_bit_for(G);
+    if (KB > 32) { SB = 24; KB = 32; }
+    k_sec_keys<<<nblk(n), 256, 0, st>>>(n, s.indptr, s.indices, s.data, P<int>(ws.rowblk), P<unsigned>(ws.sec_key),
+                                        SB);
     size_t tk = 0, tsc = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tk, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey), (int)nnz, 0, 32,
+    cub::DeviceRadixSort::SortKeys(nullptr, tk, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey), (int)nnz, 0, KB,
                                    st);
     cub::DeviceScan::ExclusiveSum(nullptr, tsc, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)nnz, st);
     VFPI_CK(ensure(ws.cub_tmp, std::max(tk, tsc)));
     tb = ws.cub_tmp.cap;
     VFPI_CK(cub::DeviceRadixSort::SortKeys(ws.cub_tmp.p, tb, P<unsigned>(ws.sec_key), P<unsigned>(ws.sec_skey),
-                                           (int)nnz, 0, 32, st));
+                                           (int)nnz, 0, KB, st));
     k_sec_flags<<<nblk(nnz), 256, 0, st>>>(nnz, P<unsigned>(ws.sec_skey), P<int>(ws.sec_flag));
     VFPI_CK(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.p, tb, P<int>(ws.sec_flag), P<int>(ws.sec_upos), (int)nnz, st));
     k_sec_emit<<<nblk(nnz), 256, 0, st>>>(nnz, P<unsigned>(ws.sec_skey), P<int>(ws.sec_flag), P<int>(ws.sec_upos),
-                                          P<unsigned>(ws.secs), P<int>(ws.sec_ptr));
-    k_sec_ptr_fix<<<1, 1, 0, st>>>(G, nnz, P<int>(ws.sec_flag), P<int>(ws.sec_upos), P<int>(ws.sec_ptr));
+                                          P<unsigned>(ws.secs), P<int>(ws.sec_ptr), SB);
+    k_sec_ptr_fix<<<1, 1024, 0, st>>>(G, nnz, P<int>(ws.sec_flag), P<int>(ws.sec_upos), P<int>(ws.sec_ptr));
     launches += 12;
   } else {
     VFPI_CK(cudaMemsetAsync(ws.sec_ptr.p, 0, 4 * (size_t)(G + 1), st));
@@ -910,7 +933,7 @@ int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const 
   if (resident) {
     VFPI_CK(ensure(ws.sell_map, 4 * (size_t)std::max<int64_t>(hs.sell_elems, 1)));
     if (S > 0) {
-      k_sell_map<<<G, 256, 0, st>>>(G, P<int>(ws.blk_slice), P<int>(ws.blk_row), P<int64_t>(ws.slice_off),
+      k_sell_map<<<G, 1024, 0, st>>>(G, P<int>(ws.blk_slice), P<int>(ws.blk_row), P<int64_t>(ws.slice_off),
                                     P<int>(ws.sell_col), P<int>(ws.rowpos), P<unsigned>(ws.secs), P<int>(ws.sec_ptr),
                                     P<unsigned>(ws.sell_map));
       ++launches;
