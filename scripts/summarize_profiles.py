@@ -64,7 +64,7 @@ traffic = {
     "dram_bytes_write_per_launch": int(wr),
     "dram_bytes_per_launch": int(rd + wr),
     "duration_us": float(m["gpu__time_duration.sum"].replace(",", "")) * {
-        "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u.get("gpu__time_duration.sum"), 1.0),
+        "nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(u.get("gpu__time_duration.sum"), 1.0),
     "note": "after the L2 flush the partition is read once from HBM into shared memory; the iterations then run "
             "from SMEM/L2",
 }
