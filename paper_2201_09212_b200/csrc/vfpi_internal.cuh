@@ -15,7 +15,8 @@ constexpr int kPartialStride = 8;  // doubles per CTA per parity in the partials
 
 // Shared-memory layout of one CTA of the resident iteration kernel: EP SELL-32
 // elements (values + gather map) of its R rows (the first CR belong to its C
-// contacts) and NS staged 32-byte sectors of remote v.
+// contacts) and NS staged 32-byte sectors of remote v, followed directly by the
+// CTA's own rows of v^(l-1): one x array, indexed by the gather map.
 struct ResLayout {
   size_t o_sv, o_map, o_xs, o_sec, o_sb, o_len, o_row, o_b, o_w, o_v0, o_v1, o_cm, o_cq, o_fr, o_par, o_lam, o_vs,
       o_jt, total;
@@ -29,14 +30,14 @@ struct ResLayout {
     const int NSL = (R + 31) / 32;
     o_sv = take(8 * (size_t)EP);
     o_map = take(4 * (size_t)EP);
-    o_xs = take(32 * (size_t)NS);
+    o_xs = take(32 * (size_t)NS + 8 * (size_t)R);  // staged sectors, then own rows of v^(l-1)
+    o_v0 = o_xs + 32 * (size_t)NS;
     o_sec = take(4 * (size_t)NS);
     o_sb = take(4 * (size_t)(NSL + 1));
     o_len = take(4 * (size_t)R);
     o_row = take(4 * (size_t)R);
     o_b = take(8 * (size_t)R);
     o_w = take(8 * (size_t)R);
-    o_v0 = take(8 * (size_t)R);    // own rows of v^(l-1)
     o_v1 = take(8 * (size_t)R);    // own rows of v^(l)
     o_cm = take(4 * (size_t)C);
     o_cq = take(4 * (size_t)C);

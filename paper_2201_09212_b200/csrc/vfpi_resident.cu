@@ -25,7 +25,6 @@ namespace vfpi {
 
 namespace {
 
-constexpr unsigned kOwn = 0x80000000u;
 constexpr int kMaxPartialsPerLane = 8;  // G <= 256
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -36,14 +35,6 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// one 32-byte sector of v in a single 256-bit load (coherent: plain ld.global)
-__device__ __forceinline__ double4 ld_sector(const double* p) {
-  double4 r;
-  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p)
-               : "memory");
-  return r;
 }
 
 // fixed-order CTA sum of three doubles -> sm_out[0..2] (visible after the next barrier)
@@ -133,19 +124,10 @@ __device__ __forceinline__ void warp0_collect(const double* part, int off, int G
   }
 }
 
-// x of one SELL element -- the on-chip copy of an own row or a staged sector
-// value -- as a pointer select and one shared load (no branch, so the gathers
-// of an unrolled row sum are all in flight together)
-__device__ __forceinline__ double gather_x(unsigned m, const double* __restrict__ xs,
-                                           const double* __restrict__ vown) {
-  const double* src = (m & kOwn) ? vown : xs;
-  return src[m & ~kOwn];
-}
-
 // sequential (scipy-order) dot of one row with x: SELL element i = base + 32k,
 // x from the staged sectors or from the CTA's own rows
 __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const unsigned* __restrict__ mp, int base,
-                                          int len, const double* __restrict__ xs, const double* __restrict__ vown) {
+                                          int len, const double* __restrict__ xs) {
   double acc = 0.0;
   int k = 0;
   for (; k + 4 <= len; k += 4) {
@@ -155,7 +137,7 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const u
       const int i = base + 32 * (k + u);
       const unsigned m = mp[i];
       a[u] = sv[i];
-      x[u] = gather_x(m, xs, vown);
+      x[u] = xs[m];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc = dadd(acc, dmul(a[u], x[u]));
@@ -163,7 +145,7 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const u
   for (; k < len; ++k) {
     const int i = base + 32 * k;
     const unsigned m = mp[i];
-    acc = dadd(acc, dmul(sv[i], gather_x(m, xs, vown)));
+    acc = dadd(acc, dmul(sv[i], xs[m]));
   }
   return acc;
 }
@@ -171,8 +153,7 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const u
 // three independent row sums at once (one contact side), each in scipy order
 __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const unsigned* __restrict__ mp,
                                          const int* __restrict__ sb, const int* __restrict__ rlen,
-                                         const double* __restrict__ xs, const double* __restrict__ vown, int q0,
-                                         int q1, int q2, double* out) {
+                                         const double* __restrict__ xs, int q0, int q1, int q2, double* out) {
   const int qq[3] = {q0, q1, q2};
   int base[3], len[3];
 #pragma unroll
@@ -195,7 +176,7 @@ __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const un
         ok[u][a] = kk < len[a];
         const int i = base[a] + 32 * (ok[u][a] ? kk : 0);
         const unsigned m = mp[i];
-        pr[u][a] = dmul(sv[i], gather_x(m, xs, vown));
+        pr[u][a] = dmul(sv[i], xs[m]);
       }
 #pragma unroll
     for (int u = 0; u < 2; ++u)
@@ -206,7 +187,9 @@ __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const un
   for (int a = 0; a < 3; ++a) out[a] = acc[a];
 }
 
-template <int OP, bool CHEB, bool BB, bool HASC>
+// PROF: phase timestamps (tuning aid, scripts/prof_phases.py); compiled only
+// into the configs[1] instantiation so the production kernels carry no checks
+template <int OP, bool CHEB, bool BB, bool HASC, bool PROF = false>
 __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double sm_warp[3 * (kResThreads / 32)];
@@ -233,7 +216,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   int* rw = reinterpret_cast<int*>(smraw + Lo.o_row);
   double* bs = reinterpret_cast<double*>(smraw + Lo.o_b);
   double* ws = reinterpret_cast<double*>(smraw + Lo.o_w);
-  double* vown = reinterpret_cast<double*>(smraw + Lo.o_v0);   // own rows of v^(l-1)
+  double* vown = reinterpret_cast<double*>(smraw + Lo.o_v0);   // own rows of v^(l-1) (= xs + 4 NS)
   double* vown2 = reinterpret_cast<double*>(smraw + Lo.o_v1);  // own rows of v^(l)
   int* cm = reinterpret_cast<int*>(smraw + Lo.o_cm);
   int* cq = reinterpret_cast<int*>(smraw + Lo.o_cq);
@@ -295,7 +278,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
 
   for (int l = 1;; ++l) {
     const bool check_only = (l == p.max_iters + 1);
-    const bool profl = p.prof != nullptr && l >= p.prof_iter0 && l < p.prof_iter0 + 4;
+    const bool profl = PROF && p.prof != nullptr && l >= p.prof_iter0 && l < p.prof_iter0 + 4;
     auto stamp = [&](int k) {  // phase timestamps for tuning (off unless p.prof is set)
       if (profl) {
         __syncthreads();
@@ -314,20 +297,22 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
 
     // ---- phase 1: stage the remote sectors of v^(l-1); reduce partials of l-1
     {
-      // warps 1.. stage (up to four sectors per thread in flight before the
-      // first smem store); warp 0 reduces the partials and takes the roots
-      double4* dst = reinterpret_cast<double4*>(xs);
+      // warps 1.. stage with asynchronous global->shared copies (two 16-byte
+      // cp.async per sector, no register round trip); warp 0 reduces the
+      // partials and takes the roots meanwhile
       const int TS = T - 32;
       if (warp > 0) {
-        for (int j0 = tid - 32; j0 < NS; j0 += 4 * TS) {
-          double4 r[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (j0 + u * TS < NS) r[u] = ld_sector(vcur + 4 * (size_t)sec[j0 + u * TS]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (j0 + u * TS < NS) dst[j0 + u * TS] = r[u];
+        const unsigned xs_sh = (unsigned)__cvta_generic_to_shared(xs);
+        for (int j = tid - 32; j < NS; j += TS) {
+          const double* src = vcur + 4 * (size_t)sec[j];
+          const unsigned d = xs_sh + 32u * (unsigned)j;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u), "l"(src + 2) : "memory");
         }
+        // own rows of v^(l-1) (written last iteration) join the x array
+        if (l > 1)
+          for (int q = tid - 32; q < R; q += TS) vown[q] = vown2[q];
+        asm volatile("cp.async.wait_all;" ::: "memory");
       } else if (l > 1) {
         warp0_collect(p.partials + (size_t)((l - 1) & 1) * G * kPartialStride, 0, G, sm_tot, true);
       }
@@ -364,9 +349,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       pending = theta < p.tol;
       if (CHEB) rho = (theta_prev <= 0.0) ? rho : py_min(ddiv(theta, theta_prev), 1.0);
       theta_prev = theta;
-      double* tmp = vown;  // own rows of v^(l-1) become the current iterate
-      vown = vown2;
-      vown2 = tmp;
     }
     double* part = p.partials + (size_t)(l & 1) * G * kPartialStride;
 
@@ -381,7 +363,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         for (int k = 0; k < rlen[q]; ++k) {
           const int i = base + 32 * k;
           const unsigned m = mp[i];
-          const int g = (m & kOwn) ? rw[m & ~kOwn] : (int)(4u * sec[m >> 2] + (m & 3u));
+          const int g = (m >= 4u * (unsigned)NS) ? rw[m - 4u * (unsigned)NS] : (int)(4u * sec[m >> 2] + (m & 3u));
           z = dadd(z, dmul(sv[i], dsub(vcur[g], vprev[g])));
         }
         const double s = dsub(vown[q], vprev[rw[q]]);
@@ -432,7 +414,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     };
     // r = A v - b of own row q; force residual of the previous iterate (solver.py:437-439)
     auto residual = [&](int q) {
-      const double r = dsub(row_dot(sv, mp, sb[q >> 5] + (q & 31), rlen[q], xs, vown), bs[q]);
+      const double r = dsub(row_dot(sv, mp, sb[q >> 5] + (q & 31), rlen[q], xs), bs[q]);
       const double f = (q < CR) ? dsub(r, jt_s[q]) : dsub(r, 0.0);
       fr = dadd(fr, dmul(f, f));
       return r;
@@ -460,7 +442,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && !dj) break;
           double dot[3];
-          row_dot3(sv, mp, sb, rlen, xs, vown, qs[3 * h], qs[3 * h + 1], qs[3 * h + 2], dot);
+          row_dot3(sv, mp, sb, rlen, xs, qs[3 * h], qs[3 * h + 1], qs[3 * h + 2], dot);
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             const int q = qs[3 * h + a];
@@ -601,6 +583,8 @@ KernelFn pick(int op, bool cheb, bool bb, bool hasc) {
 int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, size_t smem_bytes, cudaStream_t st,
                             std::string& err) {
   KernelFn f = pick(op, cheb, bb, p.n_c > 0);
+  if (p.prof != nullptr && op == OP_STRICT && !cheb && !bb && p.n_c > 0)
+    f = k_iterate_res<OP_STRICT, false, false, true, true>;
   cudaError_t e = ensure_max_dynamic_smem((const void*)f);
   if (e != cudaSuccess) { err = std::string("smem attribute: ") + cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
   int nb = 0;

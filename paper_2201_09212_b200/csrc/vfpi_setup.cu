@@ -400,9 +400,8 @@ __global__ void __launch_bounds__(kFixThreads) k_summary(int n, int G, const int
 // copy. Built in phase 1 from the CSC entries (so the shared-memory size is
 // known at the single host read): key = (cta << SB) | sector, radix sorted,
 // first-of-run flags -> block-major unique sector list secs + per-CTA ranges.
-// sell_map[i] (phase 2) encodes where SELL element i's x comes from:
-//   0x80000000 | q  -> own row q (local position),  else 4*slot + (col & 3).
-constexpr unsigned kOwnBit = 0x80000000u;
+// sell_map[i] (phase 2) is the index of SELL element i's x in the CTA's x
+// array: 4*slot + (col & 3) for a staged sector, 4*NS + q for own row q.
 constexpr unsigned kNoSector = 0xFFFFFFFFu;
 
 __global__ void k_rowpos(int n, int G, const int* __restrict__ row_list, const int* __restrict__ blk_row,
@@ -497,7 +496,7 @@ __global__ void __launch_bounds__(1024) k_sell_map(int G, const int* __restrict_
     if (c >= 0) {
       const int pc = rowpos[c];
       if (pc >= p0 && pc < p1) {
-        m = kOwnBit | (unsigned)(pc - p0);
+        m = 4u * (unsigned)ns + (unsigned)(pc - p0);  // own rows follow the staged sectors
       } else {
         const unsigned sec = (unsigned)c >> 2;
         int lo = 0, hi = ns;  // first sector >= sec
