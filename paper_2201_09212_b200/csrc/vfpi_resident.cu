@@ -425,14 +425,17 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     stamp(3);
     if (warp < WC) {
       const int CD = CR / 3 - C;  // two-sided contacts of the CTA
-      for (int k = tid; k < C; k += WC * 32) {
-        const int code = cq[k];
+      for (int k0 = warp * 32; k0 < C; k0 += WC * 32) {  // warp-uniform trip count
+        const int k = k0 + lane;
+        const bool act = k < C;
+        const int kc = act ? k : 0;
+        const int code = cq[kc];
         const bool dj = (code >> 30) & 1;
         const int kd = code & 0x3fffffff;
         int qs[6];
-        qs[0] = k;
-        qs[1] = C + k;
-        qs[2] = 2 * C + k;
+        qs[0] = kc;
+        qs[1] = C + kc;
+        qs[2] = 2 * C + kc;
         qs[3] = 3 * C + kd;
         qs[4] = qs[3] + CD;
         qs[5] = qs[4] + CD;
@@ -448,12 +451,15 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
             const int q = qs[3 * h + a];
             const double r = dsub(dot[a], bs[q]);
             const double f = dsub(r, jt_s[q]);
-            fr = dadd(fr, dmul(f, f));
+            if (act) fr = dadd(fr, dmul(f, f));
             vsr[3 * h + a] = dsub(vown[q], dmul(use_alpha ? alpha : ws[q], r));
           }
         }
-        if (profl) { __syncwarp(__activemask()); if ((tid & 31) == __ffs(__activemask()) - 1) atomicMax(&sm_role_end[2], (unsigned long long)clock64()); }
-        if (!HASC || check_only) continue;
+        // the free-row warps start once every contact's rows are swept (they
+        // would otherwise take the issue slots the contact lanes' chains need)
+        if (k0 == warp * 32 && WC < nw) asm volatile("bar.arrive 2, %0;" ::"r"(T) : "memory");
+        if (profl) { __syncwarp(); if (lane == 0) atomicMax(&sm_role_end[2], (unsigned long long)clock64()); }
+        if (!act || !HASC || check_only) continue;
         // (2) gather + (3) one-shot projection (solver.py:262-281)
         const double* R9 = cfr + 9 * k;
         double rel[3], eta[3], lam[3], wv[3];
@@ -489,6 +495,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       }
       if (profl && lane == 0) atomicMax(&sm_role_end[0], (unsigned long long)clock64());
     }
+    if (warp >= WC && WC > 0 && WC < nw) asm volatile("bar.sync 2, %0;" ::"r"(T) : "memory");
     if (warp >= WC || WC == nw) {
       // ---- free rows: v_new = v* (+ w * 0 when contacts exist) ------------
       const int t0 = (WC == nw) ? tid : tid - WC * 32;
