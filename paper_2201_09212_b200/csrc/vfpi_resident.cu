@@ -165,11 +165,11 @@ __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const un
   double acc[3] = {0.0, 0.0, 0.0};
   // branch-free: every lane loads (a row past its end re-reads its last
   // element) and only adds while k < len, so the three chains interleave
-  for (int k = 0; k < L; k += 2) {
-    double pr[2][3];
-    bool ok[2][3];
+  for (int k = 0; k < L; k += 4) {  // 12 independent loads per step (rows of <= 4 entries: one step)
+    double pr[4][3];
+    bool ok[4][3];
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const int kk = k + u;
@@ -179,7 +179,7 @@ __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const un
         pr[u][a] = dmul(sv[i], xs[m]);
       }
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int a = 0; a < 3; ++a) acc[a] = ok[u][a] ? dadd(acc[a], pr[u][a]) : acc[a];
   }
@@ -533,16 +533,21 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         sm_warp[3 * warp + 2] = nf;
       }
       __syncthreads();
-      if (tid == 0) {  // fixed warp order
-        double x = 0.0, y = 0.0, z = 0.0;
-        for (int w2 = 0; w2 < nw; ++w2) {
-          x = dadd(x, sm_warp[3 * w2 + 0]);
-          y = dadd(y, sm_warp[3 * w2 + 1]);
-          z = dadd(z, sm_warp[3 * w2 + 2]);
+      if (warp == 0) {  // fixed-order tree over the warps' partials
+        double x = lane < nw ? sm_warp[3 * lane + 0] : 0.0;
+        double y = lane < nw ? sm_warp[3 * lane + 1] : 0.0;
+        double z = lane < nw ? sm_warp[3 * lane + 2] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          x = dadd(x, __shfl_xor_sync(0xffffffffu, x, o));
+          y = dadd(y, __shfl_xor_sync(0xffffffffu, y, o));
+          z = dadd(z, __shfl_xor_sync(0xffffffffu, z, o));
         }
-        sm_tot[0] = x;
-        sm_tot[1] = y;
-        sm_tot[2] = z;
+        if (lane == 0) {
+          sm_tot[0] = x;
+          sm_tot[1] = y;
+          sm_tot[2] = z;
+        }
       }
     }
     grid_arrive_wait(sm_tot, part, 0, counter, G, ++epoch);
