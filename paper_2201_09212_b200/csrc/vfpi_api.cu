@@ -76,6 +76,7 @@ T* P(Workspace::Buf& b) { return reinterpret_cast<T*>(b.p); }
 int choose_blocks(const vfpi_system& s, int num_sms) {
   const int64_t by_nnz = (s.nnz + 4095) / 4096;
   if (by_nnz < num_sms) return (int)std::max<int64_t>(1, by_nnz);
+  if (by_nnz >= 4 * num_sms) return 4 * num_sms;  // HBM streaming wants several CTAs per SM
   return by_nnz >= 2 * num_sms ? 2 * num_sms : num_sms;
 }
 

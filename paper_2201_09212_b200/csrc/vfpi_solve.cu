@@ -70,11 +70,23 @@ __device__ __forceinline__ void grid_totals(const double* __restrict__ part, int
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     double a = 0.0, b = 0.0, c = 0.0;
-    for (int g = lane; g < G; g += 32) {
-      const double* q = part + (size_t)g * kPartialStride + off;
-      a = dadd(a, __ldcg(q + 0));
-      b = dadd(b, __ldcg(q + 1));
-      c = dadd(c, __ldcg(q + 2));
+    for (int g0 = lane; g0 < G; g0 += 32 * 4) {  // four partials per lane in flight
+      double x[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int g = g0 + 32 * u;
+        const double* q = part + (size_t)g * kPartialStride + off;
+        x[u][0] = g < G ? __ldcg(q + 0) : 0.0;
+        x[u][1] = g < G ? __ldcg(q + 1) : 0.0;
+        x[u][2] = g < G ? __ldcg(q + 2) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (g0 + 32 * u < G) {
+          a = dadd(a, x[u][0]);
+          b = dadd(b, x[u][1]);
+          c = dadd(c, x[u][2]);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -134,7 +146,7 @@ __device__ __forceinline__ double sell_row(const double* __restrict__ sv, const 
 //             scene b's rows and contacts); every CTA runs its own iteration
 //             loop, reductions and termination with CTA barriers only.
 template <int OP, bool CHEB, bool BB, bool HASC, bool SC>
-__global__ void __launch_bounds__(kThreads, SC ? VFPI_SC_MIN_BLOCKS : 1) k_iterate(IterParams p) {
+__global__ void __launch_bounds__(kThreads, VFPI_SC_MIN_BLOCKS) k_iterate(IterParams p) {
   extern __shared__ double smem[];
   __shared__ double sm_warp[3 * (kThreads / 32)];
   __shared__ double sm_tot[4];

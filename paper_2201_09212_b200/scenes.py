@@ -208,3 +208,64 @@ class FemCube:
         vh = np.asarray(v_hat)[: self.n].reshape(-1, 3)
         self.x = self.x + self.dt * vh
         self.v = 2.0 * vh - self.v
+
+
+# ---------------------------------------------------------------------------
+# configs[3]: 64^3-node linear-tet block pressed onto a heightfield
+# ---------------------------------------------------------------------------
+# The reference has no heightfield detector (parity of the
+# detection is unpinned; the solve itself is pinned like every other system).
+# Parameters BASELINE leaves open are fixed here and recorded by the bench:
+# side 0.1 m (cfg0's), E 1e6, nu 0.35, rho 1000, mu 0.4, dt 1e-3,
+# heightfield z = 0.005 sin(40x) sin(40y), "pressed" = the bottom face conformed
+# to the heightfield 0.1 mm deep, the layers above relaxing linearly to the flat
+# rest shape, plus a 50 N downward load spread over the top face.
+
+def _heightfield(x, y):
+    return 0.005 * np.sin(40.0 * x) * np.sin(40.0 * y)
+
+
+def _heightfield_normal(x, y):
+    hx = 0.2 * np.cos(40.0 * x) * np.sin(40.0 * y)
+    hy = 0.2 * np.sin(40.0 * x) * np.cos(40.0 * y)
+    n = np.stack([-hx, -hy, np.ones_like(hx)], axis=-1)
+    return n / np.linalg.norm(n, axis=-1, keepdims=True)
+
+
+class HeightfieldBlock(FemCube):
+    """configs[3] (nx=64); small nx for parity tests."""
+
+    def __init__(self, nx=64, side=0.1, E=1e6, nu=0.35, rho=1000.0, dt=1e-3, mu=0.4, press=50.0,
+                 depth=1e-4, margin=1e-4, beta_err=0.2):
+        super().__init__(nx=nx, side=side, E=E, nu=nu, rho=rho, drop=0.0, dt=dt, mu=mu, margin=margin,
+                         beta_err=beta_err)
+        X = self.X
+        k = np.round((X[:, 2] - X[:, 2].min()) / (side / (nx - 1))).astype(int)  # layer index
+        bottom = _heightfield(X[:, 0], X[:, 1]) - depth
+        frac = 1.0 - k / (nx - 1)
+        self.x = X.copy()
+        self.x[:, 2] = X[:, 2] + frac * bottom
+        self.v = np.zeros_like(X)
+        top = k == nx - 1
+        self.f_ext = np.zeros(self.n)
+        self.f_ext[3 * np.nonzero(top)[0] + 2] = -press / max(int(top.sum()), 1)
+
+    def contacts(self):
+        """Nodes within the margin of the heightfield: S-contacts along its normal."""
+        x, y, z = self.x[:, 0], self.x[:, 1], self.x[:, 2]
+        h = _heightfield(x, y)
+        nodes = np.nonzero(z < h + self.margin)[0]
+        depth = np.maximum(0.0, h[nodes] - z[nodes])
+        phi = -(self.beta / self.dt) * depth
+        normals = _heightfield_normal(x[nodes], y[nodes])
+        frames = np.stack([contact_frame(nrm) for nrm in normals]) if len(nodes) else np.zeros((0, 3, 3))
+        return nodes, phi, depth, frames
+
+    def system(self) -> PackedSystem:
+        b = ((2.0 / self.dt) * self.m * self.v.ravel() - self.K @ (self.x - self.X).ravel() + self.m * self.gravity
+             + self.f_ext)
+        nodes, phi, depth, frames = self.contacts()
+        n_c = nodes.shape[0]
+        mu = np.full(n_c, self.mu)
+        return make_packed(self.n, self.A.indptr, self.A.indices, self.A.data, b, 3 * nodes, np.full(n_c, -1),
+                           frames.reshape(-1), mu, mu, phi)

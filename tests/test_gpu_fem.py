@@ -70,3 +70,23 @@ def test_config2_scene_batch_steps_match_oracle():
     assert touched > 0
     for a, b in zip(gpu, cpu):
         assert np.linalg.norm(a.x - b.x) <= 1e-9 * np.linalg.norm(b.x)
+
+
+@pytest.mark.parametrize("cheb", [False, True])
+def test_config3_heightfield_block_matches_oracle(cheb):
+    """configs[3]-shaped system (heightfield S-contacts with per-contact frames) at
+    nx=8, through the single-system path: identical iterations, v bitwise (plain)."""
+    from paper_2201_09212_b200.scenes import HeightfieldBlock
+    from paper_2201_09212_b200.solver import SolverConfig, solve_packed
+
+    ps = HeightfieldBlock(nx=8).system()
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=500, chebyshev=cheb)
+    v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
+    vc, lc, rc = _oracle_step(ps, cfg, np.zeros(ps.n))
+    assert rep.iterations == rc.iterations and rep.converged == rc.converged
+    if cheb:
+        assert np.allclose(v, vc, rtol=1e-9, atol=1e-12)
+        assert np.allclose(lam, lc, rtol=1e-9, atol=1e-9)
+    else:
+        assert np.array_equal(v, vc)
+        assert np.array_equal(lam, lc)
