@@ -125,8 +125,8 @@ __device__ __forceinline__ double sell_row(const double* __restrict__ sv, const 
     double a[U], xv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      c[u] = __ldg(cp + 32 * (k + u));
-      a[u] = __ldg(vp + 32 * (k + u));
+      c[u] = __ldcs(cp + 32 * (k + u));  // streamed once per iteration: evict-first,
+      a[u] = __ldcs(vp + 32 * (k + u));  // so the gathered vectors stay in L2
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? x(c[u]) : 0.0;
@@ -135,8 +135,8 @@ __device__ __forceinline__ double sell_row(const double* __restrict__ sv, const 
       if (c[u] >= 0) acc = dadd(acc, dmul(a[u], xv[u]));
   }
   for (; k < W; ++k) {
-    const int c = __ldg(cp + 32 * k);
-    if (c >= 0) acc = dadd(acc, dmul(__ldg(vp + 32 * k), x(c)));
+    const int c = __ldcs(cp + 32 * k);
+    if (c >= 0) acc = dadd(acc, dmul(__ldcs(vp + 32 * k), x(c)));
   }
   return acc;
 }
