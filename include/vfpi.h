@@ -142,6 +142,38 @@ int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* sys, int32_t num_scenes
                       const int32_t* scene_ct_ptr, const vfpi_config* cfg, const double* warm,
                       const double* w_cached, vfpi_scene_result* res);
 
+/* ---- FEM scene batch stepped on the device (configs[0]/[2]) ---------------
+ * SURVEY §8(f) item 1; reference analogues harness.run (harness.py:526-619),
+ * assemble_step (dynamics.py:176-218, here the linear-FEM right-hand side
+ * b = (2/dt) M v - K (x - X) + M g), detect_contacts node-plane branch
+ * (contacts.py:159-200), stabilization_term (contacts.py:230-239) and
+ * integrate (dynamics.py:237-255). The batch keeps A (block diagonal, CSC),
+ * K (block diagonal, CSR, for b) and the state x, v on the device; each
+ * vfpi_fem_step assembles b, detects node-plane contacts (z < margin, frame
+ * `frame9` for every contact), solves all scenes with vfpi_solve_scenes
+ * semantics (warm start = the previous step's solution) and integrates.
+ * The handle is borrowed and must outlive the batch. */
+typedef struct vfpi_fem_batch vfpi_fem_batch;
+typedef struct vfpi_fem_params {
+  double dt, margin, beta_err, e_rest, rest_threshold, mu;
+} vfpi_fem_params;
+typedef struct vfpi_fem_step_stats {
+  int64_t contacts;            /* contacts of the step, all scenes */
+  int64_t contact_iterations;  /* sum over scenes of n_c(scene) * iterations(scene) */
+  int64_t iterations;          /* sum over scenes */
+  int32_t max_iterations;
+  int32_t diverged_scenes;
+  double setup_ms, loop_ms, step_ms;  /* solve setup, iteration kernel, whole step (device events) */
+} vfpi_fem_step_stats;
+int vfpi_fem_create(vfpi_handle* h, int32_t num_scenes, int32_t nodes_per_scene, const vfpi_system* a_batch,
+                    const int64_t* k_rowptr, const int32_t* k_cols, const double* k_vals, const double* mass,
+                    const double* gravity, const double* rest_x, const double* x, const double* v,
+                    const double* frame9, const vfpi_fem_params* params, vfpi_fem_batch** out);
+int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stats* stats,
+                  int32_t* iterations_per_scene /* optional [num_scenes] */);
+int vfpi_fem_state(vfpi_fem_batch* fb, double* x, double* v);
+void vfpi_fem_destroy(vfpi_fem_batch* fb);
+
 /* Number of kernels this library launched on the handle since creation. */
 int64_t vfpi_launch_count(const vfpi_handle* h);
 /* Layout chosen by the last solve: shared-memory resident kernel (1) or the

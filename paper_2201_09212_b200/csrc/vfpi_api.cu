@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "vfpi_internal.cuh"
 
 using vfpi::Workspace;
@@ -566,55 +568,33 @@ int vfpi_solve(vfpi_handle* h, const vfpi_system* s, const vfpi_config* cfg, con
   return rc;
 }
 
-int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* s, int32_t S, const int32_t* scene_row_ptr,
-                      const int32_t* scene_ct_ptr, const vfpi_config* cfg, const double* warm,
-                      const double* w_cached, vfpi_scene_result* res) {
-  if (!h || !cfg || !res || !warm || !scene_row_ptr || !scene_ct_ptr || S < 1 || S > 1024) return VFPI_BAD_ARGUMENT;
-  int rc = check_system(h, s);
-  if (rc) return rc;
-  if (scene_row_ptr[0] != 0 || scene_row_ptr[S] != s->n || scene_ct_ptr[0] != 0 || scene_ct_ptr[S] != s->n_c) {
-    h->err = "scene pointers do not cover the system";
-    return VFPI_BAD_ARGUMENT;
-  }
-  for (int k = 0; k < S; ++k)
-    if (scene_row_ptr[k + 1] < scene_row_ptr[k] || scene_ct_ptr[k + 1] < scene_ct_ptr[k]) {
-      h->err = "scene pointers must be non-decreasing";
-      return VFPI_BAD_ARGUMENT;
-    }
-  if (cfg->op < 0 || cfg->op > 2 || cfg->step_strategy < 0 || cfg->step_strategy > 4 || cfg->max_iters < 0) {
-    h->err = "bad solver config";
-    return VFPI_BAD_ARGUMENT;
-  }
-  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+}  // extern "C" (reopened below)
+
+// Scene-batch solve on device arrays (system, scene pointers, warm start and
+// outputs all on the device). Returns per-scene status in `stat` (host) after
+// one stream synchronisation.
+int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t* d_scene_rows,
+                     const int32_t* d_scene_cts, const vfpi_config* cfg, const double* d_warm, const double* d_wc,
+                     double* d_out_v, double* d_out_lam, double* d_trace, double* d_scc, vfpi::SolveStatus* h_stat,
+                     cudaStream_t st, float* setup_ms, float* loop_ms) {
   Workspace& ws = h->ws;
-  cudaStream_t st = ws.stream;
-  const int n = (int)s->n, n_c = (int)s->n_c;
+  const int n = (int)d.n, n_c = (int)d.n_c;
   const bool cheb = cfg->chebyshev != 0;
   const bool bb = cfg->step_strategy >= VFPI_STEP_BB1 && cfg->step_strategy <= VFPI_STEP_BB_ALTERNATING;
-  vfpi_system d;
-  if ((rc = stage_system(h, s, &d))) return rc;
-  if ((rc = upload(h, ws.b_warm, warm, 8 * (size_t)n))) return rc;
-  CK(vfpi::ensure(ws.b_warm, 8 * (size_t)std::max(n, 1)));
-  const double* dwc = nullptr;
-  if (w_cached) {
-    if ((rc = upload(h, ws.b_wc, w_cached, 8 * (size_t)n))) return rc;
-    dwc = P<double>(ws.b_wc);
-  }
-  if ((rc = upload(h, ws.scene_rows, scene_row_ptr, 4 * (size_t)(S + 1)))) return rc;
-  if ((rc = upload(h, ws.scene_cts, scene_ct_ptr, 4 * (size_t)(S + 1)))) return rc;
+  int rc;
   CK(cudaEventRecord(ws.ev[0], st));
   vfpi::LayoutOptions opt;
   opt.anchor_order = false;
   opt.length_sort = h->layout_opt.length_sort;
-  opt.scene_row_ptr = P<int>(ws.scene_rows);
-  opt.scene_ct_ptr = P<int>(ws.scene_cts);
+  opt.scene_row_ptr = d_scene_rows;
+  opt.scene_ct_ptr = d_scene_cts;
   vfpi::SetupSummary* hs = ws.h_summary;
   const int G = S;
   rc = vfpi::setup_layout(ws, d, G, st, hs, h->err, h->launches, opt);
   if (rc) return rc;
   rc = vfpi::setup_pack(ws, d, G, false, *hs, st, h->err, h->launches);
   if (rc) return rc;
-  rc = vfpi::setup_step_matrix(ws, d, *cfg, dwc, st, h->err, h->launches);
+  rc = vfpi::setup_step_matrix(ws, d, *cfg, d_wc, st, h->err, h->launches);
   if (rc) return rc;
   const int smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
   if (vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem) <= 0) {
@@ -627,15 +607,15 @@ int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* s, int32_t S, const int
   CK(cudaMemsetAsync(ws.vbuf.p, 0, 3 * 8 * npad, st));
   CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)std::max(n_c, 1)));
   CK(vfpi::ensure(ws.status, sizeof(vfpi::SolveStatus) * (size_t)S));
-  CK(vfpi::ensure(ws.b_out_v, 8 * (size_t)std::max(n, 1)));
-  CK(vfpi::ensure(ws.b_out_lam, 24 * (size_t)std::max(n_c, 1)));
-  CK(vfpi::ensure(ws.b_trace, 8 * tr * (size_t)S));
-  CK(vfpi::ensure(ws.b_scc, 8 * (size_t)std::max(n_c, 1)));
+  if (!d_trace) {
+    CK(vfpi::ensure(ws.b_trace, 8 * tr * (size_t)S));
+    d_trace = P<double>(ws.b_trace);
+  }
   double* vb = P<double>(ws.vbuf);
   double* lb = P<double>(ws.lambuf);
   if (n > 0) {
-    CK(cudaMemcpyAsync(vb, ws.b_warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(vb + 2 * npad, ws.b_warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(vb, d_warm, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(vb + 2 * npad, d_warm, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
   }
   CK(cudaMemsetAsync(lb, 0, 2 * 24 * (size_t)std::max(n_c, 1), st));
   CK(cudaMemsetAsync(ws.status.p, 0, sizeof(vfpi::SolveStatus) * (size_t)S, st));
@@ -670,11 +650,11 @@ int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* s, int32_t S, const int
   p.vbuf2 = vb + 2 * npad;
   p.lam0 = lb;
   p.lam1 = lb + 3 * (size_t)std::max(n_c, 1);
-  p.trace = P<double>(ws.b_trace);
+  p.trace = d_trace;
   p.trace_stride = tr;
   p.status = P<vfpi::SolveStatus>(ws.status);
-  p.out_v = P<double>(ws.b_out_v);
-  p.out_lam = P<double>(ws.b_out_lam);
+  p.out_v = d_out_v;
+  p.out_lam = d_out_lam;
   p.max_iters = cfg->max_iters;
   p.cheby_start = cfg->cheby_start;
   p.step = cfg->step_strategy;
@@ -686,14 +666,69 @@ int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* s, int32_t S, const int
   if (rc) return rc;
   ++h->launches;
   CK(cudaEventRecord(ws.ev[2], st));
-  if (res->scc && n_c > 0) {
-    rc = vfpi::launch_scc_final(p, P<double>(ws.b_scc), st);
+  if (d_scc && n_c > 0) {
+    rc = vfpi::launch_scc_final(p, d_scc, st);
     if (rc) { h->err = "scc kernel launch failed"; return rc; }
     ++h->launches;
   }
-  std::vector<vfpi::SolveStatus> stat((size_t)S);
-  CK(cudaMemcpyAsync(stat.data(), ws.status.p, sizeof(vfpi::SolveStatus) * (size_t)S, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_stat, ws.status.p, sizeof(vfpi::SolveStatus) * (size_t)S, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h->h_flags, ws.flags.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float a = 0.f, b2 = 0.f;
+  cudaEventElapsedTime(&a, ws.ev[0], ws.ev[1]);
+  cudaEventElapsedTime(&b2, ws.ev[1], ws.ev[2]);
+  if (setup_ms) *setup_ms = a;
+  if (loop_ms) *loop_ms = b2;
+  return flags_to_code(h, *h->h_flags);
+}
+
+extern "C" {
+
+int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* s, int32_t S, const int32_t* scene_row_ptr,
+                      const int32_t* scene_ct_ptr, const vfpi_config* cfg, const double* warm,
+                      const double* w_cached, vfpi_scene_result* res) {
+  if (!h || !cfg || !res || !warm || !scene_row_ptr || !scene_ct_ptr || S < 1 || S > 1024) return VFPI_BAD_ARGUMENT;
+  int rc = check_system(h, s);
+  if (rc) return rc;
+  if (scene_row_ptr[0] != 0 || scene_row_ptr[S] != s->n || scene_ct_ptr[0] != 0 || scene_ct_ptr[S] != s->n_c) {
+    h->err = "scene pointers do not cover the system";
+    return VFPI_BAD_ARGUMENT;
+  }
+  for (int k = 0; k < S; ++k)
+    if (scene_row_ptr[k + 1] < scene_row_ptr[k] || scene_ct_ptr[k + 1] < scene_ct_ptr[k]) {
+      h->err = "scene pointers must be non-decreasing";
+      return VFPI_BAD_ARGUMENT;
+    }
+  if (cfg->op < 0 || cfg->op > 2 || cfg->step_strategy < 0 || cfg->step_strategy > 4 || cfg->max_iters < 0) {
+    h->err = "bad solver config";
+    return VFPI_BAD_ARGUMENT;
+  }
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  Workspace& ws = h->ws;
+  cudaStream_t st = ws.stream;
+  const int n = (int)s->n, n_c = (int)s->n_c;
+  vfpi_system d;
+  if ((rc = stage_system(h, s, &d))) return rc;
+  if ((rc = upload(h, ws.b_warm, warm, 8 * (size_t)n))) return rc;
+  CK(vfpi::ensure(ws.b_warm, 8 * (size_t)std::max(n, 1)));
+  const double* dwc = nullptr;
+  if (w_cached) {
+    if ((rc = upload(h, ws.b_wc, w_cached, 8 * (size_t)n))) return rc;
+    dwc = P<double>(ws.b_wc);
+  }
+  if ((rc = upload(h, ws.scene_rows, scene_row_ptr, 4 * (size_t)(S + 1)))) return rc;
+  if ((rc = upload(h, ws.scene_cts, scene_ct_ptr, 4 * (size_t)(S + 1)))) return rc;
+  const size_t tr = (size_t)std::max(cfg->max_iters, 1);
+  CK(vfpi::ensure(ws.b_out_v, 8 * (size_t)std::max(n, 1)));
+  CK(vfpi::ensure(ws.b_out_lam, 24 * (size_t)std::max(n_c, 1)));
+  CK(vfpi::ensure(ws.b_trace, 8 * tr * (size_t)S));
+  CK(vfpi::ensure(ws.b_scc, 8 * (size_t)std::max(n_c, 1)));
+  std::vector<vfpi::SolveStatus> stat((size_t)S);
+  float su = 0.f, lo = 0.f;
+  rc = vfpi_scenes_core(h, d, S, P<int32_t>(ws.scene_rows), P<int32_t>(ws.scene_cts), cfg, P<double>(ws.b_warm),
+                        dwc, P<double>(ws.b_out_v), P<double>(ws.b_out_lam), P<double>(ws.b_trace),
+                        res->scc ? P<double>(ws.b_scc) : nullptr, stat.data(), st, &su, &lo);
+  if (rc) return rc;
   if (n) CK(cudaMemcpyAsync(res->v, ws.b_out_v.p, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
   if (n_c) CK(cudaMemcpyAsync(res->lam, ws.b_out_lam.p, 24 * (size_t)n_c, cudaMemcpyDeviceToHost, st));
   if (res->residual_trace && cfg->max_iters > 0)
@@ -706,12 +741,9 @@ int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* s, int32_t S, const int
     if (res->diverged) res->diverged[k] = stat[k].diverged;
     if (res->consistency) res->consistency[k] = stat[k].consistency;
   }
-  float a = 0.f, b2 = 0.f;
-  cudaEventElapsedTime(&a, ws.ev[0], ws.ev[1]);
-  cudaEventElapsedTime(&b2, ws.ev[1], ws.ev[2]);
-  res->setup_ms = a;
-  res->loop_ms = b2;
-  return flags_to_code(h, *h->h_flags);
+  res->setup_ms = su;
+  res->loop_ms = lo;
+  return VFPI_OK;
 }
 
 // ---- per-subsystem entry points -------------------------------------------
@@ -929,6 +961,190 @@ int vfpi_inverse_contact(vfpi_handle* h, const vfpi_system* s, const double* v, 
   CK(cudaMemcpyAsync(lam, ws.b_out_lam.p, 24 * nc, cudaMemcpyDeviceToHost, ws.stream));
   CK(cudaStreamSynchronize(ws.stream));
   return VFPI_OK;
+}
+
+
+// ---- FEM scene batch stepped on the device ---------------------------------
+
+}  // extern "C"
+
+struct vfpi_fem_batch {
+  vfpi_handle* h = nullptr;
+  int S = 0, Nn = 0;      // scenes, nodes per scene
+  int64_t n = 0, nodes = 0;
+  vfpi_fem_params prm{};
+  vfpi_system A{};        // device CSC of the block-diagonal A
+  Workspace::Buf a_indptr, a_indices, a_data, krp, kc, kv, m, g, X, x, v, warm, vhat, lam, b, ci, cj, frames, mu,
+      mu2, phi, flag, pos, cts, rows, frame, tmp;
+  std::vector<int32_t> h_cts;
+  std::vector<vfpi::SolveStatus> stat;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+namespace {
+
+int fem_upload(vfpi_handle* h, Workspace::Buf& b, const void* src, size_t bytes) {
+  CK(vfpi::ensure(b, std::max<size_t>(bytes, 8)));
+  if (bytes) CK(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
+  return VFPI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a, const int64_t* k_rowptr,
+                    const int32_t* k_cols, const double* k_vals, const double* mass, const double* gravity,
+                    const double* rest_x, const double* x, const double* v, const double* frame9,
+                    const vfpi_fem_params* prm, vfpi_fem_batch** out) {
+  if (!h || !a || !k_rowptr || !k_cols || !k_vals || !mass || !gravity || !rest_x || !x || !v || !frame9 || !prm ||
+      !out || S < 1 || S > 1024 || Nn < 1)
+    return VFPI_BAD_ARGUMENT;
+  if (a->n != (int64_t)S * 3 * Nn || a->n_c != 0) {
+    h->err = "A must cover num_scenes * 3 * nodes_per_scene rows and carry no contacts";
+    return VFPI_DIM_MISMATCH;
+  }
+  int rc = check_system(h, a);
+  if (rc) return rc;
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  auto* fb = new vfpi_fem_batch();
+  fb->h = h;
+  fb->S = S;
+  fb->Nn = Nn;
+  fb->n = a->n;
+  fb->nodes = (int64_t)S * Nn;
+  fb->prm = *prm;
+  const size_t n = (size_t)fb->n, nodes = (size_t)fb->nodes, nnz = (size_t)a->nnz, knnz = (size_t)k_rowptr[n];
+  auto fail = [&](int code) { vfpi_fem_destroy(fb); return code; };
+  if ((rc = fem_upload(h, fb->a_indptr, a->indptr, 4 * (n + 1))) || (rc = fem_upload(h, fb->a_indices, a->indices, 4 * nnz)) ||
+      (rc = fem_upload(h, fb->a_data, a->data, 8 * nnz)) || (rc = fem_upload(h, fb->krp, k_rowptr, 8 * (n + 1))) ||
+      (rc = fem_upload(h, fb->kc, k_cols, 4 * knnz)) || (rc = fem_upload(h, fb->kv, k_vals, 8 * knnz)) ||
+      (rc = fem_upload(h, fb->m, mass, 8 * n)) || (rc = fem_upload(h, fb->g, gravity, 8 * n)) ||
+      (rc = fem_upload(h, fb->X, rest_x, 8 * n)) || (rc = fem_upload(h, fb->x, x, 8 * n)) ||
+      (rc = fem_upload(h, fb->v, v, 8 * n)) || (rc = fem_upload(h, fb->frame, frame9, 72)))
+    return fail(rc);
+  for (Workspace::Buf* bb : {&fb->warm, &fb->vhat, &fb->b}) {
+    if (vfpi::ensure(*bb, 8 * n) != cudaSuccess) return fail(VFPI_CUDA_ERROR);
+  }
+  if (cudaMemset(fb->warm.p, 0, 8 * n) != cudaSuccess) return fail(VFPI_CUDA_ERROR);
+  // contact arrays sized for every node in contact
+  if (vfpi::ensure(fb->lam, 24 * nodes) || vfpi::ensure(fb->ci, 4 * nodes) || vfpi::ensure(fb->cj, 4 * nodes) ||
+      vfpi::ensure(fb->frames, 72 * nodes) || vfpi::ensure(fb->mu, 8 * nodes) || vfpi::ensure(fb->mu2, 8 * nodes) ||
+      vfpi::ensure(fb->phi, 8 * nodes) || vfpi::ensure(fb->flag, 4 * nodes) || vfpi::ensure(fb->pos, 4 * nodes) ||
+      vfpi::ensure(fb->cts, 4 * (size_t)(S + 1)))
+    return fail(VFPI_CUDA_ERROR);
+  std::vector<int32_t> rows((size_t)S + 1);
+  for (int k = 0; k <= S; ++k) rows[k] = k * 3 * Nn;
+  if ((rc = fem_upload(h, fb->rows, rows.data(), 4 * (size_t)(S + 1)))) return fail(rc);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)fb->flag.p, (int*)fb->pos.p, (int)nodes);
+  if (vfpi::ensure(fb->tmp, tb)) return fail(VFPI_CUDA_ERROR);
+  fb->A = *a;
+  fb->A.indptr = (const int32_t*)fb->a_indptr.p;
+  fb->A.indices = (const int32_t*)fb->a_indices.p;
+  fb->A.data = (const double*)fb->a_data.p;
+  fb->h_cts.resize((size_t)S + 1);
+  fb->stat.resize((size_t)S);
+  if (cudaEventCreate(&fb->e0) != cudaSuccess || cudaEventCreate(&fb->e1) != cudaSuccess) return fail(VFPI_CUDA_ERROR);
+  *out = fb;
+  return VFPI_OK;
+}
+
+int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stats* stats,
+                  int32_t* iterations_per_scene) {
+  if (!fb || !cfg || !stats) return VFPI_BAD_ARGUMENT;
+  vfpi_handle* h = fb->h;
+  if (cfg->op < 0 || cfg->op > 2 || cfg->step_strategy < 0 || cfg->step_strategy > 4 || cfg->max_iters < 0) {
+    h->err = "bad solver config";
+    return VFPI_BAD_ARGUMENT;
+  }
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  cudaStream_t st = h->ws.stream;
+  const vfpi_fem_params& q = fb->prm;
+  CK(cudaEventRecord(fb->e0, st));
+  // (1) right-hand side of every scene
+  vfpi::launch_fem_rhs(fb->n, P<int64_t>(fb->krp), P<int>(fb->kc), P<double>(fb->kv), P<double>(fb->x),
+                       P<double>(fb->X), P<double>(fb->v), P<double>(fb->m), P<double>(fb->g), 2.0 / q.dt,
+                       P<double>(fb->b), st);
+  // (2) node-plane contacts: flags, scene-ordered compaction, parameters
+  vfpi::launch_fem_flags(fb->nodes, P<double>(fb->x), q.margin, P<int>(fb->flag), st);
+  size_t tb = fb->tmp.cap;
+  CK(cub::DeviceScan::ExclusiveSum(fb->tmp.p, tb, P<int>(fb->flag), P<int>(fb->pos), (int)fb->nodes, st));
+  vfpi::launch_fem_scene_cts(fb->S, fb->Nn, P<int>(fb->flag), P<int>(fb->pos), P<int>(fb->cts), st);
+  vfpi::launch_fem_contacts(fb->nodes, P<int>(fb->flag), P<int>(fb->pos), P<double>(fb->x), P<double>(fb->v),
+                            P<double>(fb->frame), q.mu, -(q.beta_err / q.dt), q.e_rest, q.rest_threshold,
+                            P<int>(fb->ci), P<int>(fb->cj), P<double>(fb->frames), P<double>(fb->mu),
+                            P<double>(fb->mu2), P<double>(fb->phi), st);
+  h->launches += 6;  // rhs, flags, scan (init + pass), scene pointers, contacts
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(fb->h_cts.data(), fb->cts.p, 4 * (size_t)(fb->S + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // (3) solve every scene (vfpi_solve_scenes semantics, warm = previous solution)
+  vfpi_system d = fb->A;
+  d.n_c = fb->h_cts[fb->S];
+  d.b = P<double>(fb->b);
+  d.col_i = P<int32_t>(fb->ci);
+  d.col_j = P<int32_t>(fb->cj);
+  d.frames = P<double>(fb->frames);
+  d.mu = P<double>(fb->mu);
+  d.mu2 = P<double>(fb->mu2);
+  d.phi = P<double>(fb->phi);
+  float su = 0.f, lo = 0.f;
+  int rc = vfpi_scenes_core(h, d, fb->S, P<int32_t>(fb->rows), P<int32_t>(fb->cts), cfg, P<double>(fb->warm),
+                            nullptr, P<double>(fb->vhat), P<double>(fb->lam), nullptr, nullptr, fb->stat.data(), st,
+                            &su, &lo);
+  if (rc) return rc;
+  // (4) midpoint integration; the solution warm-starts the next step
+  vfpi::launch_fem_advance(fb->n, q.dt, P<double>(fb->vhat), P<double>(fb->x), P<double>(fb->v),
+                           P<double>(fb->warm), st);
+  ++h->launches;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(fb->e1, st));
+  CK(cudaEventSynchronize(fb->e1));
+  int64_t ci = 0, it = 0;
+  int mx = 0, dv = 0;
+  for (int k = 0; k < fb->S; ++k) {
+    const vfpi::SolveStatus& s = fb->stat[k];
+    ci += (int64_t)(fb->h_cts[k + 1] - fb->h_cts[k]) * s.iterations;
+    it += s.iterations;
+    mx = std::max(mx, s.iterations);
+    dv += s.diverged ? 1 : 0;
+    if (iterations_per_scene) iterations_per_scene[k] = s.iterations;
+  }
+  float step = 0.f;
+  cudaEventElapsedTime(&step, fb->e0, fb->e1);
+  stats->contacts = d.n_c;
+  stats->contact_iterations = ci;
+  stats->iterations = it;
+  stats->max_iterations = mx;
+  stats->diverged_scenes = dv;
+  stats->setup_ms = su;
+  stats->loop_ms = lo;
+  stats->step_ms = step;
+  return VFPI_OK;
+}
+
+int vfpi_fem_state(vfpi_fem_batch* fb, double* x, double* v) {
+  if (!fb) return VFPI_BAD_ARGUMENT;
+  vfpi_handle* h = fb->h;
+  cudaSetDevice(h->ws.device);
+  CK(cudaStreamSynchronize(h->ws.stream));
+  if (x) CK(cudaMemcpy(x, fb->x.p, 8 * (size_t)fb->n, cudaMemcpyDeviceToHost));
+  if (v) CK(cudaMemcpy(v, fb->v.p, 8 * (size_t)fb->n, cudaMemcpyDeviceToHost));
+  return VFPI_OK;
+}
+
+void vfpi_fem_destroy(vfpi_fem_batch* fb) {
+  if (!fb) return;
+  cudaSetDevice(fb->h->ws.device);
+  for (Workspace::Buf* b : {&fb->a_indptr, &fb->a_indices, &fb->a_data, &fb->krp, &fb->kc, &fb->kv, &fb->m, &fb->g,
+                            &fb->X, &fb->x, &fb->v, &fb->warm, &fb->vhat, &fb->lam, &fb->b, &fb->ci, &fb->cj,
+                            &fb->frames, &fb->mu, &fb->mu2, &fb->phi, &fb->flag, &fb->pos, &fb->cts, &fb->rows,
+                            &fb->frame, &fb->tmp})
+    if (b->p) cudaFree(b->p);
+  if (fb->e0) cudaEventDestroy(fb->e0);
+  if (fb->e1) cudaEventDestroy(fb->e1);
+  delete fb;
 }
 
 }  // extern "C"

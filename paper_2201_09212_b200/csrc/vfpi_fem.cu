@@ -1,0 +1,113 @@
+// Device step pipeline of the FEM scene batches (configs[0]/[2]; SURVEY
+// §8(f) item 1): right-hand side assembly, node-plane contact detection,
+// contact parameters and midpoint integration, so a batch steps without host
+// round trips of the state. Every expression follows the host restatement
+// (scenes.FemCube.system / contacts / advance) operation for operation, so
+// the device pipeline and the host pipeline produce identical bits.
+#include "vfpi_internal.cuh"
+#include "vfpi_math.cuh"
+
+namespace vfpi {
+
+namespace {
+
+// b = ((2/dt) m) v - K (x - X) + m g   (FemCube.system; K @ u in scipy's
+// per-row column order, FMA-free, explicit zeros included)
+__global__ void k_fem_rhs(int64_t n, const int64_t* __restrict__ krp, const int* __restrict__ kc,
+                          const double* __restrict__ kv, const double* __restrict__ x, const double* __restrict__ X,
+                          const double* __restrict__ v, const double* __restrict__ m, const double* __restrict__ g,
+                          double twodt, double* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ku = 0.0;
+  for (int64_t e = krp[i]; e < krp[i + 1]; ++e) {
+    const int j = kc[e];
+    ku = dadd(ku, dmul(kv[e], dsub(x[j], X[j])));
+  }
+  const double t1 = dmul(dmul(twodt, m[i]), v[i]);
+  b[i] = dadd(dsub(t1, ku), dmul(m[i], g[i]));
+}
+
+// node below the margin of the plane z = 0 (FemCube.contacts)
+__global__ void k_fem_flags(int64_t nodes, const double* __restrict__ x, double margin, int* __restrict__ flag) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < nodes) flag[k] = x[3 * k + 2] < margin ? 1 : 0;
+}
+
+__global__ void k_fem_contacts(int64_t nodes, const int* __restrict__ flag, const int* __restrict__ pos,
+                               const double* __restrict__ x, const double* __restrict__ v,
+                               const double* __restrict__ frame, double mu, double neg_beta_dt, double e_rest,
+                               double thr, int* __restrict__ ci, int* __restrict__ cj, double* __restrict__ frames,
+                               double* __restrict__ muv, double* __restrict__ mu2v, double* __restrict__ phi) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nodes || !flag[k]) return;
+  const int c = pos[k];
+  const double z = x[3 * k + 2];
+  const double depth = np_max(0.0, -z);        // np.maximum(0.0, -z[nodes])
+  double ph = dmul(neg_beta_dt, depth);        // -(beta / dt) * depth
+  const double vn = v[3 * k + 2];
+  if (fabs(vn) > thr) ph = dadd(ph, dmul(e_rest, np_min(0.0, vn)));  // np.where(rest, ...)
+  ci[c] = (int)(3 * k);
+  cj[c] = -1;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) frames[9 * (size_t)c + t] = frame[t];
+  muv[c] = mu;
+  mu2v[c] = mu;
+  phi[c] = ph;
+}
+
+// contacts of scene s start at the exclusive prefix of the flags at its first node
+__global__ void k_fem_scene_cts(int S, int nodes_per_scene, const int* __restrict__ flag,
+                                const int* __restrict__ pos, int* __restrict__ cts) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > S) return;
+  if (s < S) {
+    cts[s] = pos[(int64_t)s * nodes_per_scene];
+  } else {
+    const int64_t last = (int64_t)S * nodes_per_scene - 1;
+    cts[S] = pos[last] + flag[last];
+  }
+}
+
+// midpoint integration (FemCube.advance): x += dt v_hat; v = 2 v_hat - v;
+// the solution also warm-starts the next step
+__global__ void k_fem_advance(int64_t n, double dt, const double* __restrict__ vh, double* __restrict__ x,
+                              double* __restrict__ v, double* __restrict__ warm) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double h = vh[i];
+  x[i] = dadd(x[i], dmul(dt, h));
+  v[i] = dsub(dmul(2.0, h), v[i]);
+  warm[i] = h;
+}
+
+inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,
+                    const double* v, const double* m, const double* g, double twodt, double* b, cudaStream_t st) {
+  if (n > 0) k_fem_rhs<<<nb(n), 256, 0, st>>>(n, krp, kc, kv, x, X, v, m, g, twodt, b);
+}
+
+void launch_fem_flags(int64_t nodes, const double* x, double margin, int* flag, cudaStream_t st) {
+  if (nodes > 0) k_fem_flags<<<nb(nodes), 256, 0, st>>>(nodes, x, margin, flag);
+}
+
+void launch_fem_contacts(int64_t nodes, const int* flag, const int* pos, const double* x, const double* v,
+                         const double* frame, double mu, double neg_beta_dt, double e_rest, double thr, int* ci,
+                         int* cj, double* frames, double* muv, double* mu2v, double* phi, cudaStream_t st) {
+  if (nodes > 0)
+    k_fem_contacts<<<nb(nodes), 256, 0, st>>>(nodes, flag, pos, x, v, frame, mu, neg_beta_dt, e_rest, thr, ci, cj,
+                                             frames, muv, mu2v, phi);
+}
+
+void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int* pos, int* cts, cudaStream_t st) {
+  k_fem_scene_cts<<<nb(S + 1), 256, 0, st>>>(S, nodes_per_scene, flag, pos, cts);
+}
+
+void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st) {
+  if (n > 0) k_fem_advance<<<nb(n), 256, 0, st>>>(n, dt, vh, x, v, warm);
+}
+
+}  // namespace vfpi

@@ -219,4 +219,15 @@ cudaError_t ensure(Workspace::Buf& b, size_t bytes);
 // several threads must never shrink it under each other).
 cudaError_t ensure_max_dynamic_smem(const void* fn);
 
+
+// ---- FEM scene-batch step pipeline (vfpi_fem.cu) ----------------------------
+void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,
+                    const double* v, const double* m, const double* g, double twodt, double* b, cudaStream_t st);
+void launch_fem_flags(int64_t nodes, const double* x, double margin, int* flag, cudaStream_t st);
+void launch_fem_contacts(int64_t nodes, const int* flag, const int* pos, const double* x, const double* v,
+                         const double* frame, double mu, double neg_beta_dt, double e_rest, double thr, int* ci,
+                         int* cj, double* frames, double* muv, double* mu2v, double* phi, cudaStream_t st);
+void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int* pos, int* cts, cudaStream_t st);
+void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st);
+
 }  // namespace vfpi

@@ -1,0 +1,126 @@
+"""FEM scene batches stepped entirely on the device (configs[0]/[2]; SURVEY
+§8(f) item 1): ``FemBatch`` uploads the block-diagonal A and K and the state
+of a list of ``scenes.FemCube`` once; every ``step`` then assembles b, detects
+node-plane contacts, solves all scenes (``vfpi_solve_scenes`` semantics, warm
+start = previous solution) and integrates on the GPU through ``vfpi_fem_step``
+(include/vfpi.h). The host pipeline (``FemCube.system`` -> ``solve_scenes`` ->
+``FemCube.advance``) is its restatement; both give identical bits
+(tests/test_gpu_fem.py)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import VfpiConfig, as_f64, as_i32, ptr
+from .contacts import contact_frame
+from .solver import SolverConfig, _c_config, _raise_for
+from .system import make_packed
+
+
+class _Params(C.Structure):
+    _fields_ = [("dt", C.c_double), ("margin", C.c_double), ("beta_err", C.c_double), ("e_rest", C.c_double),
+                ("rest_threshold", C.c_double), ("mu", C.c_double)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("contacts", C.c_int64), ("contact_iterations", C.c_int64), ("iterations", C.c_int64),
+                ("max_iterations", C.c_int32), ("diverged_scenes", C.c_int32), ("setup_ms", C.c_double),
+                ("loop_ms", C.c_double), ("step_ms", C.c_double)]
+
+
+def _bind():
+    L = _lib.lib()
+    if not hasattr(L, "_fem_bound"):
+        i64p = C.POINTER(C.c_int64)
+        L.vfpi_fem_create.restype = C.c_int
+        L.vfpi_fem_create.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(_lib.VfpiSystem), i64p,
+                                      _lib._i32p, _lib._f64p, _lib._f64p, _lib._f64p, _lib._f64p, _lib._f64p,
+                                      _lib._f64p, _lib._f64p, C.POINTER(_Params), C.POINTER(C.c_void_p)]
+        L.vfpi_fem_step.restype = C.c_int
+        L.vfpi_fem_step.argtypes = [C.c_void_p, C.POINTER(VfpiConfig), C.POINTER(_Stats), _lib._i32p]
+        L.vfpi_fem_state.restype = C.c_int
+        L.vfpi_fem_state.argtypes = [C.c_void_p, _lib._f64p, _lib._f64p]
+        L.vfpi_fem_destroy.restype = None
+        L.vfpi_fem_destroy.argtypes = [C.c_void_p]
+        L._fem_bound = True
+    return L
+
+
+def _block_diag(mats):
+    """Compressed arrays (CSC or CSR alike) of the block-diagonal stack, entries
+    of each block kept exactly as stored (order, explicit zeros)."""
+    ptrs, idx, val = [np.zeros(1, dtype=np.int64)], [], []
+    nnz = 0
+    off = 0
+    for m in mats:
+        ptrs.append(m.indptr[1:].astype(np.int64) + nnz)
+        idx.append(m.indices.astype(np.int64) + off)
+        val.append(m.data)
+        nnz += m.nnz
+        off += m.shape[0]
+    return np.concatenate(ptrs), np.concatenate(idx), np.concatenate(val)
+
+
+class FemBatch:
+    """Device-resident batch of FemCube scenes (same node count, same dt/margin/mu)."""
+
+    def __init__(self, cubes, device=None):
+        c0 = cubes[0]
+        for c in cubes:
+            if (c.n, c.dt, c.margin, c.beta, c.e_rest, c.thr, c.mu) != (c0.n, c0.dt, c0.margin, c0.beta, c0.e_rest,
+                                                                        c0.thr, c0.mu):
+                raise ValueError("scenes of a FemBatch share node count, dt, margin and contact parameters")
+        self.S, self.n_scene = len(cubes), c0.n
+        self.h = _lib.handle(device)
+        self.L = _bind()
+        a_ptr, a_idx, a_val = _block_diag([c.A for c in cubes])
+        ks = [c.K.tocsr() for c in cubes]
+        for km in ks:
+            km.sort_indices()
+        k_ptr, k_idx, k_val = _block_diag(ks)
+        ntot = self.S * self.n_scene
+        self._a = make_packed(ntot, a_ptr, a_idx, a_val, np.zeros(ntot), [], [], [], [])
+        self._k = (np.ascontiguousarray(k_ptr, dtype=np.int64), as_i32(k_idx), as_f64(k_val))
+        cat = lambda f: as_f64(np.concatenate([np.asarray(f(c), float).ravel() for c in cubes]))  # noqa: E731
+        self._m, self._g, self._X = cat(lambda c: c.m), cat(lambda c: c.gravity), cat(lambda c: c.X)
+        x, v = cat(lambda c: c.x), cat(lambda c: c.v)
+        frame = as_f64(contact_frame(np.array([0.0, 0.0, 1.0])).ravel())
+        prm = _Params(c0.dt, c0.margin, c0.beta, c0.e_rest, c0.thr, c0.mu)
+        out = C.c_void_p()
+        i64p = C.POINTER(C.c_int64)
+        code = self.L.vfpi_fem_create(self.h.h, self.S, self.n_scene // 3, self._a.c_struct(), ptr(self._k[0], i64p),
+                                      ptr(self._k[1], _lib._i32p), ptr(self._k[2]), ptr(self._m), ptr(self._g),
+                                      ptr(self._X), ptr(x), ptr(v), ptr(frame), C.byref(prm), C.byref(out))
+        _raise_for(code, self.h)
+        self.fb = out
+
+    def step(self, cfg: SolverConfig, per_scene=False):
+        st = _Stats()
+        its = np.zeros(self.S, dtype=np.int32) if per_scene else None
+        code = self.L.vfpi_fem_step(self.fb, _c_config(cfg), C.byref(st),
+                                    ptr(its, _lib._i32p) if its is not None else None)
+        _raise_for(code, self.h)
+        out = {f: getattr(st, f) for f, _ in _Stats._fields_}
+        if its is not None:
+            out["iterations_per_scene"] = its
+        return out
+
+    def state(self):
+        x = np.empty(self.S * self.n_scene)
+        v = np.empty(self.S * self.n_scene)
+        _raise_for(self.L.vfpi_fem_state(self.fb, ptr(x), ptr(v)), self.h)
+        return x.reshape(self.S, -1, 3), v.reshape(self.S, -1, 3)
+
+    def close(self):
+        if getattr(self, "fb", None):
+            self.L.vfpi_fem_destroy(self.fb)
+            self.fb = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -90,3 +90,40 @@ def test_config3_heightfield_block_matches_oracle(cheb):
     else:
         assert np.array_equal(v, vc)
         assert np.array_equal(lam, lc)
+
+
+def test_device_fem_pipeline_matches_host_pipeline():
+    """vfpi_fem_step (b, detection, solve, integration on the device) against the
+    host pipeline (FemCube.system -> solve_scenes -> FemCube.advance): identical
+    state bits after free fall, touchdown and contact steps."""
+    from paper_2201_09212_b200.batch import solve_scenes
+    from paper_2201_09212_b200.fembatch import FemBatch
+    from paper_2201_09212_b200.scenes import FemCube
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    def make():
+        return [FemCube(nx=5, E=e, drop=d, yaw=y) for e, d, y in ((6e4, 0.004, 0.3), (1.5e5, 0.006, 1.1),
+                                                                  (1e5, 0.002, 2.0))]
+
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=200)
+    host = make()
+    dev = FemBatch(make())
+    warms = [np.zeros(c.n) for c in host]
+    saw_contacts = False
+    for step in range(45):
+        systems = [c.system() for c in host]
+        res, _ = solve_scenes(systems, cfg, warms=warms)
+        st = dev.step(cfg, per_scene=True)
+        assert st["contacts"] == sum(s.n_c for s in systems)
+        saw_contacts |= st["contacts"] > 0
+        for k, (c, r) in enumerate(zip(host, res)):
+            v, lam, rep = r
+            assert st["iterations_per_scene"][k] == rep.iterations
+            c.advance(v)
+            warms[k] = v
+        x, vel = dev.state()
+        for k, c in enumerate(host):
+            assert np.array_equal(x[k], c.x), f"step {step} scene {k}"
+            assert np.array_equal(vel[k], c.v), f"step {step} scene {k}"
+    assert saw_contacts
+    dev.close()
