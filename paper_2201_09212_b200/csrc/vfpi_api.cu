@@ -576,7 +576,10 @@ int vfpi_solve(vfpi_handle* h, const vfpi_system* s, const vfpi_config* cfg, con
 int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t* d_scene_rows,
                      const int32_t* d_scene_cts, const vfpi_config* cfg, const double* d_warm, const double* d_wc,
                      double* d_out_v, double* d_out_lam, double* d_trace, double* d_scc, vfpi::SolveStatus* h_stat,
-                     cudaStream_t st, float* setup_ms, float* loop_ms) {
+                     cudaStream_t st, float* setup_ms, float* loop_ms, int refresh_max_ct = -1) {
+  // refresh_max_ct >= 0: the workspace holds this batch's contact-free row
+  // layout (FEM pipeline); only the contact marks are rebuilt, and
+  // refresh_max_ct is the largest per-scene contact count
   Workspace& ws = h->ws;
   const int n = (int)d.n, n_c = (int)d.n_c;
   const bool cheb = cfg->chebyshev != 0;
@@ -590,13 +593,19 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
   opt.scene_ct_ptr = d_scene_cts;
   vfpi::SetupSummary* hs = ws.h_summary;
   const int G = S;
-  rc = vfpi::setup_layout(ws, d, G, st, hs, h->err, h->launches, opt);
-  if (rc) return rc;
-  rc = vfpi::setup_pack(ws, d, G, false, *hs, st, h->err, h->launches);
-  if (rc) return rc;
+  if (refresh_max_ct < 0) {
+    rc = vfpi::setup_layout(ws, d, G, st, hs, h->err, h->launches, opt);
+    if (rc) return rc;
+    rc = vfpi::setup_pack(ws, d, G, false, *hs, st, h->err, h->launches);
+    if (rc) return rc;
+  } else {
+    rc = vfpi::setup_contacts_refresh(ws, d, G, d_scene_cts, st, h->err, h->launches);
+    if (rc) return rc;
+  }
   rc = vfpi::setup_step_matrix(ws, d, *cfg, d_wc, st, h->err, h->launches);
   if (rc) return rc;
-  const int smem = 2 * vfpi::kSlotsPerContact * 8 * hs->max_ct_per_blk;
+  const int max_ct = refresh_max_ct < 0 ? hs->max_ct_per_blk : refresh_max_ct;
+  const int smem = 2 * vfpi::kSlotsPerContact * 8 * max_ct;
   if (vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem) <= 0) {
     h->err = "a scene has too many contacts for one CTA";
     return VFPI_UNSUPPORTED;
@@ -979,6 +988,8 @@ struct vfpi_fem_batch {
   std::vector<int32_t> h_cts;
   std::vector<vfpi::SolveStatus> stat;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  Workspace::Buf zero_cts;
+  uint64_t layout_epoch = ~0ull, layout_gen = ~0ull;  // the handle workspace holds our contact-free layout
 };
 
 namespace {
@@ -1036,6 +1047,8 @@ int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a,
   std::vector<int32_t> rows((size_t)S + 1);
   for (int k = 0; k <= S; ++k) rows[k] = k * 3 * Nn;
   if ((rc = fem_upload(h, fb->rows, rows.data(), 4 * (size_t)(S + 1)))) return fail(rc);
+  std::vector<int32_t> zeros((size_t)S + 1, 0);
+  if ((rc = fem_upload(h, fb->zero_cts, zeros.data(), 4 * (size_t)(S + 1)))) return fail(rc);
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)fb->flag.p, (int*)fb->pos.p, (int)nodes);
   if (vfpi::ensure(fb->tmp, tb)) return fail(VFPI_CUDA_ERROR);
@@ -1079,7 +1092,36 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(fb->h_cts.data(), fb->cts.p, 4 * (size_t)(fb->S + 1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  // (3) solve every scene (vfpi_solve_scenes semantics, warm = previous solution)
+  // (3) solve every scene (vfpi_solve_scenes semantics, warm = previous solution);
+  // A is fixed, so its row layout is built once without contacts and only the
+  // contact marks are refreshed per step (rebuilt if another solve used the workspace)
+  Workspace& ws = h->ws;
+  if (fb->layout_epoch != ws.layout_epoch || fb->layout_gen != vfpi::alloc_generation()) {
+    vfpi_system d0 = fb->A;
+    d0.n_c = 0;
+    d0.b = P<double>(fb->b);
+    d0.col_i = P<int32_t>(fb->ci);
+    d0.col_j = P<int32_t>(fb->cj);
+    d0.frames = P<double>(fb->frames);
+    d0.mu = P<double>(fb->mu);
+    d0.mu2 = P<double>(fb->mu2);
+    d0.phi = P<double>(fb->phi);
+    vfpi::LayoutOptions opt;
+    opt.anchor_order = false;
+    opt.length_sort = h->layout_opt.length_sort;
+    opt.scene_row_ptr = P<int>(fb->rows);
+    opt.scene_ct_ptr = P<int>(fb->zero_cts);
+    int rc0 = vfpi::setup_layout(ws, d0, fb->S, st, ws.h_summary, h->err, h->launches, opt);
+    if (!rc0) rc0 = vfpi::setup_pack(ws, d0, fb->S, false, *ws.h_summary, st, h->err, h->launches);
+    if (!rc0) rc0 = vfpi::setup_rowpos(ws, (int)fb->n, fb->S, st, h->err);
+    if (rc0) return rc0;
+    CK(vfpi::ensure(ws.cont_list, 4 * (size_t)fb->nodes));  // per-step refresh never grows it
+    CK(cudaStreamSynchronize(st));
+    fb->layout_epoch = ws.layout_epoch;
+    fb->layout_gen = vfpi::alloc_generation();
+  }
+  int max_ct = 0;
+  for (int k = 0; k < fb->S; ++k) max_ct = std::max(max_ct, fb->h_cts[k + 1] - fb->h_cts[k]);
   vfpi_system d = fb->A;
   d.n_c = fb->h_cts[fb->S];
   d.b = P<double>(fb->b);
@@ -1092,7 +1134,7 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   float su = 0.f, lo = 0.f;
   int rc = vfpi_scenes_core(h, d, fb->S, P<int32_t>(fb->rows), P<int32_t>(fb->cts), cfg, P<double>(fb->warm),
                             nullptr, P<double>(fb->vhat), P<double>(fb->lam), nullptr, nullptr, fb->stat.data(), st,
-                            &su, &lo);
+                            &su, &lo, max_ct);
   if (rc) return rc;
   // (4) midpoint integration; the solution warm-starts the next step
   vfpi::launch_fem_advance(fb->n, q.dt, P<double>(fb->vhat), P<double>(fb->x), P<double>(fb->v),
@@ -1140,7 +1182,7 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
   for (Workspace::Buf* b : {&fb->a_indptr, &fb->a_indices, &fb->a_data, &fb->krp, &fb->kc, &fb->kv, &fb->m, &fb->g,
                             &fb->X, &fb->x, &fb->v, &fb->warm, &fb->vhat, &fb->lam, &fb->b, &fb->ci, &fb->cj,
                             &fb->frames, &fb->mu, &fb->mu2, &fb->phi, &fb->flag, &fb->pos, &fb->cts, &fb->rows,
-                            &fb->frame, &fb->tmp})
+                            &fb->frame, &fb->tmp, &fb->zero_cts})
     if (b->p) cudaFree(b->p);
   if (fb->e0) cudaEventDestroy(fb->e0);
   if (fb->e1) cudaEventDestroy(fb->e1);

@@ -188,6 +188,7 @@ void launch_const_fill(double* p, double v, int64_t n, cudaStream_t st);
 // ---- device workspace ------------------------------------------------------
 struct Workspace {
   int device = 0;
+  uint64_t layout_epoch = 0;  // bumped by every layout/pack (cached layouts compare against it)
   std::vector<void*> owned;
   // grow-only buffers
   struct Buf { void* p = nullptr; size_t cap = 0; };
@@ -219,6 +220,14 @@ cudaError_t ensure(Workspace::Buf& b, size_t bytes);
 // several threads must never shrink it under each other).
 cudaError_t ensure_max_dynamic_smem(const void* fn);
 
+
+// Scene batches whose matrix stays fixed while contacts change (the FEM step
+// pipeline): the row layout is built once without contacts (setup_layout +
+// setup_pack with n_c = 0, then setup_rowpos); each step only re-marks the
+// contact rows (row_slot), the contact list and the CTA contact ranges.
+int setup_rowpos(Workspace& ws, int n, int G, cudaStream_t st, std::string& err);
+int setup_contacts_refresh(Workspace& ws, const vfpi_system& dsys, int G, const int* d_scene_ct_ptr, cudaStream_t st,
+                           std::string& err, int64_t& launches);
 
 // ---- FEM scene-batch step pipeline (vfpi_fem.cu) ----------------------------
 void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,

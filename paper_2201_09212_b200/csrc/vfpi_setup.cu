@@ -675,6 +675,7 @@ static int end_bit_for(int64_t v) {
 // widths. Ends with ONE host read of the summary (sizes + flags).
 int setup_layout_async(Workspace& ws, const vfpi_system& s, int G, cudaStream_t st, std::string& err,
                  int64_t& launches, const LayoutOptions& opt) {
+  ++ws.layout_epoch;
   const int n = (int)s.n, n_c = (int)s.n_c;
   const int64_t nnz = s.nnz;
   if (G > 1024) { err = "more than 1024 CTA ranges per layout"; return VFPI_BAD_ARGUMENT; }
@@ -901,6 +902,7 @@ int setup_layout_finish(Workspace& ws, cudaStream_t st, SetupSummary* hs, std::s
 // column order (scipy's accumulation order), then packing for the kernel.
 int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const SetupSummary& hs, cudaStream_t st,
                std::string& err, int64_t& launches) {
+  ++ws.layout_epoch;
   const int n = (int)s.n;
   const int64_t nnz = s.nnz;
   const int S = hs.n_slices;
@@ -981,6 +983,56 @@ int setup_step_matrix(Workspace& ws, const vfpi_system& s, const vfpi_config& cf
   const bool bb = cfg.step_strategy >= VFPI_STEP_BB1 && cfg.step_strategy <= VFPI_STEP_BB_ALTERNATING;
   if (bb) {
     k_mean<<<1, 256, 0, st>>>(n, w, P<double>(ws.w_mean));
+    ++launches;
+  }
+  VFPI_CK(cudaGetLastError());
+  return VFPI_OK;
+}
+
+
+namespace {
+
+// contact k of the CTA (scene) b whose contact range holds k: its rows get
+// slots (k - ct[b]) * 6 + q, the row order itself is unchanged
+__global__ void k_refresh_slots(int n_c, int G, const int* __restrict__ ci, const int* __restrict__ cj,
+                                const int* __restrict__ ct, const int* __restrict__ rowpos, int* __restrict__ row_slot,
+                                int* __restrict__ cont_list) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_c) return;
+  const int b = owner(ct, G, k);
+  const int loc = (k - ct[b]) * kSlotsPerContact;
+  cont_list[k] = k;
+  const int i = ci[k], j = cj[k];
+  for (int q = 0; q < 3; ++q) row_slot[rowpos[i + q]] = loc + q;
+  if (j >= 0)
+    for (int q = 0; q < 3; ++q) row_slot[rowpos[j + q]] = loc + 3 + q;
+}
+
+__global__ void k_rowpos_only(int n, const int* __restrict__ row_list, int* __restrict__ rowpos) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) rowpos[row_list[q]] = q;
+}
+
+}  // namespace
+
+int setup_rowpos(Workspace& ws, int n, int G, cudaStream_t st, std::string& err) {
+  (void)G;
+  VFPI_CK(ensure(ws.rowpos, 4 * (size_t)std::max(n, 1)));
+  if (n > 0) k_rowpos_only<<<nblk(n), 256, 0, st>>>(n, P<int>(ws.row_list), P<int>(ws.rowpos));
+  VFPI_CK(cudaGetLastError());
+  return VFPI_OK;
+}
+
+int setup_contacts_refresh(Workspace& ws, const vfpi_system& s, int G, const int* d_scene_ct_ptr, cudaStream_t st,
+                           std::string& err, int64_t& launches) {
+  const int n = (int)s.n, n_c = (int)s.n_c;
+  VFPI_CK(ensure(ws.cont_list, 4 * (size_t)std::max(n_c, 1)));
+  VFPI_CK(cudaMemsetAsync(ws.row_slot.p, 0xff, 4 * (size_t)std::max(n, 1), st));
+  VFPI_CK(cudaMemcpyAsync(ws.blk_ct.p, d_scene_ct_ptr, 4 * (size_t)(G + 1), cudaMemcpyDeviceToDevice, st));
+  VFPI_CK(cudaMemsetAsync(ws.flags.p, 0, 16, st));
+  if (n_c > 0) {
+    k_refresh_slots<<<nblk(n_c), 256, 0, st>>>(n_c, G, s.col_i, s.col_j, d_scene_ct_ptr, P<int>(ws.rowpos),
+                                                P<int>(ws.row_slot), P<int>(ws.cont_list));
     ++launches;
   }
   VFPI_CK(cudaGetLastError());
