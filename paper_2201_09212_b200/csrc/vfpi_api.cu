@@ -988,8 +988,8 @@ struct vfpi_fem_batch {
   std::vector<int32_t> h_cts;
   std::vector<vfpi::SolveStatus> stat;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  Workspace::Buf zero_cts;
-  uint64_t layout_epoch = ~0ull, layout_gen = ~0ull;  // the handle workspace holds our contact-free layout
+  Workspace::Buf zero_cts, ks_off, ks_val, ks_col;  // K in SELL-32
+  uint64_t layout_epoch = ~0ull;  // the handle workspace holds our contact-free layout
 };
 
 namespace {
@@ -1052,6 +1052,32 @@ int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a,
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)fb->flag.p, (int*)fb->pos.p, (int)nodes);
   if (vfpi::ensure(fb->tmp, tb)) return fail(VFPI_CUDA_ERROR);
+  {  // K -> SELL-32 once (coalesced right-hand-side sums)
+    const int64_t nsl = ((int64_t)n + 31) / 32;
+    if (vfpi::ensure(fb->ks_off, 8 * (size_t)(nsl + 1))) return fail(VFPI_CUDA_ERROR);
+    Workspace::Buf wbuf;
+    if (vfpi::ensure(wbuf, 8 * (size_t)(nsl + 1))) return fail(VFPI_CUDA_ERROR);
+    vfpi::launch_fem_sell_width((int64_t)n, P<int64_t>(fb->krp), P<int64_t>(wbuf), nullptr);
+    size_t t2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, P<int64_t>(wbuf), P<int64_t>(fb->ks_off), (int)(nsl + 1));
+    Workspace::Buf tb2;
+    if (vfpi::ensure(tb2, t2) ||
+        cub::DeviceScan::ExclusiveSum(tb2.p, t2, P<int64_t>(wbuf), P<int64_t>(fb->ks_off), (int)(nsl + 1))) {
+      cudaFree(wbuf.p);
+      cudaFree(tb2.p);
+      return fail(VFPI_CUDA_ERROR);
+    }
+    int64_t elems = 0;
+    cudaMemcpy(&elems, P<int64_t>(fb->ks_off) + nsl, 8, cudaMemcpyDeviceToHost);
+    cudaFree(wbuf.p);
+    cudaFree(tb2.p);
+    if (vfpi::ensure(fb->ks_val, 8 * (size_t)std::max<int64_t>(elems, 1)) ||
+        vfpi::ensure(fb->ks_col, 4 * (size_t)std::max<int64_t>(elems, 1)))
+      return fail(VFPI_CUDA_ERROR);
+    vfpi::launch_fem_sell_pack((int64_t)n, P<int64_t>(fb->krp), P<int>(fb->kc), P<double>(fb->kv),
+                               P<int64_t>(fb->ks_off), P<double>(fb->ks_val), P<int>(fb->ks_col), nullptr);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(VFPI_CUDA_ERROR);
+  }
   fb->A = *a;
   fb->A.indptr = (const int32_t*)fb->a_indptr.p;
   fb->A.indices = (const int32_t*)fb->a_indices.p;
@@ -1076,9 +1102,9 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   const vfpi_fem_params& q = fb->prm;
   CK(cudaEventRecord(fb->e0, st));
   // (1) right-hand side of every scene
-  vfpi::launch_fem_rhs(fb->n, P<int64_t>(fb->krp), P<int>(fb->kc), P<double>(fb->kv), P<double>(fb->x),
-                       P<double>(fb->X), P<double>(fb->v), P<double>(fb->m), P<double>(fb->g), 2.0 / q.dt,
-                       P<double>(fb->b), st);
+  vfpi::launch_fem_rhs_sell(fb->n, P<int64_t>(fb->ks_off), P<double>(fb->ks_val), P<int>(fb->ks_col),
+                            P<double>(fb->x), P<double>(fb->X), P<double>(fb->v), P<double>(fb->m), P<double>(fb->g),
+                            2.0 / q.dt, P<double>(fb->b), st);
   // (2) node-plane contacts: flags, scene-ordered compaction, parameters
   vfpi::launch_fem_flags(fb->nodes, P<double>(fb->x), q.margin, P<int>(fb->flag), st);
   size_t tb = fb->tmp.cap;
@@ -1096,7 +1122,9 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   // A is fixed, so its row layout is built once without contacts and only the
   // contact marks are refreshed per step (rebuilt if another solve used the workspace)
   Workspace& ws = h->ws;
-  if (fb->layout_epoch != ws.layout_epoch || fb->layout_gen != vfpi::alloc_generation()) {
+  // (layout buffers are only (re)allocated inside setup_layout/setup_pack, which
+  // bump the epoch; growth of unrelated workspace buffers leaves them intact)
+  if (fb->layout_epoch != ws.layout_epoch) {
     vfpi_system d0 = fb->A;
     d0.n_c = 0;
     d0.b = P<double>(fb->b);
@@ -1118,7 +1146,6 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
     CK(vfpi::ensure(ws.cont_list, 4 * (size_t)fb->nodes));  // per-step refresh never grows it
     CK(cudaStreamSynchronize(st));
     fb->layout_epoch = ws.layout_epoch;
-    fb->layout_gen = vfpi::alloc_generation();
   }
   int max_ct = 0;
   for (int k = 0; k < fb->S; ++k) max_ct = std::max(max_ct, fb->h_cts[k + 1] - fb->h_cts[k]);
@@ -1182,7 +1209,7 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
   for (Workspace::Buf* b : {&fb->a_indptr, &fb->a_indices, &fb->a_data, &fb->krp, &fb->kc, &fb->kv, &fb->m, &fb->g,
                             &fb->X, &fb->x, &fb->v, &fb->warm, &fb->vhat, &fb->lam, &fb->b, &fb->ci, &fb->cj,
                             &fb->frames, &fb->mu, &fb->mu2, &fb->phi, &fb->flag, &fb->pos, &fb->cts, &fb->rows,
-                            &fb->frame, &fb->tmp, &fb->zero_cts})
+                            &fb->frame, &fb->tmp, &fb->zero_cts, &fb->ks_off, &fb->ks_val, &fb->ks_col})
     if (b->p) cudaFree(b->p);
   if (fb->e0) cudaEventDestroy(fb->e0);
   if (fb->e1) cudaEventDestroy(fb->e1);

@@ -28,6 +28,52 @@ __global__ void k_fem_rhs(int64_t n, const int64_t* __restrict__ krp, const int*
   b[i] = dadd(dsub(t1, ku), dmul(m[i], g[i]));
 }
 
+// K in SELL-32 (slices of 32 consecutive rows, entry k of row r at
+// off[slice] + 32 k + (r & 31); padding column -1), so the per-row
+// sequential sums of the right-hand side read K coalesced
+__global__ void k_fem_sell_width(int64_t n, const int64_t* __restrict__ krp, int64_t* __restrict__ width) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nsl = (n + 31) / 32;
+  if (s > nsl) return;
+  if (s == nsl) { width[s] = 0; return; }
+  int64_t w = 0;
+  for (int64_t r = 32 * s; r < n && r < 32 * s + 32; ++r) w = max(w, krp[r + 1] - krp[r]);
+  width[s] = 32 * w;
+}
+
+__global__ void k_fem_sell_pack(int64_t n, const int64_t* __restrict__ krp, const int* __restrict__ kc,
+                                const double* __restrict__ kv, const int64_t* __restrict__ off,
+                                double* __restrict__ sv, int* __restrict__ sc) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t s = r >> 5, o = off[s];
+  const int W = (int)((off[s + 1] - o) >> 5);
+  const int64_t e0 = krp[r], len = krp[r + 1] - e0;
+  for (int k = 0; k < W; ++k) {
+    const int64_t dst = o + 32 * (int64_t)k + (r & 31);
+    sv[dst] = k < len ? kv[e0 + k] : 0.0;
+    sc[dst] = k < len ? kc[e0 + k] : -1;
+  }
+}
+
+__global__ void k_fem_rhs_sell(int64_t n, const int64_t* __restrict__ off, const double* __restrict__ sv,
+                               const int* __restrict__ sc, const double* __restrict__ x,
+                               const double* __restrict__ X, const double* __restrict__ v,
+                               const double* __restrict__ m, const double* __restrict__ g, double twodt,
+                               double* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t o = off[i >> 5] + (i & 31);
+  const int W = (int)((off[(i >> 5) + 1] - off[i >> 5]) >> 5);
+  double ku = 0.0;
+  for (int k = 0; k < W; ++k) {
+    const int j = __ldcs(sc + o + 32 * (int64_t)k);
+    if (j >= 0) ku = dadd(ku, dmul(__ldcs(sv + o + 32 * (int64_t)k), dsub(x[j], X[j])));
+  }
+  const double t1 = dmul(dmul(twodt, m[i]), v[i]);
+  b[i] = dadd(dsub(t1, ku), dmul(m[i], g[i]));
+}
+
 // node below the margin of the plane z = 0 (FemCube.contacts)
 __global__ void k_fem_flags(int64_t nodes, const double* __restrict__ x, double margin, int* __restrict__ flag) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -88,6 +134,21 @@ inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t);
 void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,
                     const double* v, const double* m, const double* g, double twodt, double* b, cudaStream_t st) {
   if (n > 0) k_fem_rhs<<<nb(n), 256, 0, st>>>(n, krp, kc, kv, x, X, v, m, g, twodt, b);
+}
+
+void launch_fem_sell_width(int64_t n, const int64_t* krp, int64_t* width, cudaStream_t st) {
+  k_fem_sell_width<<<nb((n + 31) / 32 + 1), 256, 0, st>>>(n, krp, width);
+}
+
+void launch_fem_sell_pack(int64_t n, const int64_t* krp, const int* kc, const double* kv, const int64_t* off,
+                          double* sv, int* sc, cudaStream_t st) {
+  if (n > 0) k_fem_sell_pack<<<nb(n), 256, 0, st>>>(n, krp, kc, kv, off, sv, sc);
+}
+
+void launch_fem_rhs_sell(int64_t n, const int64_t* off, const double* sv, const int* sc, const double* x,
+                         const double* X, const double* v, const double* m, const double* g, double twodt, double* b,
+                         cudaStream_t st) {
+  if (n > 0) k_fem_rhs_sell<<<nb(n), 256, 0, st>>>(n, off, sv, sc, x, X, v, m, g, twodt, b);
 }
 
 void launch_fem_flags(int64_t nodes, const double* x, double margin, int* flag, cudaStream_t st) {

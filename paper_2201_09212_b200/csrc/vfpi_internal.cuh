@@ -232,6 +232,12 @@ int setup_contacts_refresh(Workspace& ws, const vfpi_system& dsys, int G, const 
 // ---- FEM scene-batch step pipeline (vfpi_fem.cu) ----------------------------
 void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,
                     const double* v, const double* m, const double* g, double twodt, double* b, cudaStream_t st);
+void launch_fem_sell_width(int64_t n, const int64_t* krp, int64_t* width, cudaStream_t st);
+void launch_fem_sell_pack(int64_t n, const int64_t* krp, const int* kc, const double* kv, const int64_t* off,
+                          double* sv, int* sc, cudaStream_t st);
+void launch_fem_rhs_sell(int64_t n, const int64_t* off, const double* sv, const int* sc, const double* x,
+                         const double* X, const double* v, const double* m, const double* g, double twodt, double* b,
+                         cudaStream_t st);
 void launch_fem_flags(int64_t nodes, const double* x, double margin, int* flag, cudaStream_t st);
 void launch_fem_contacts(int64_t nodes, const int* flag, const int* pos, const double* x, const double* v,
                          const double* frame, double mu, double neg_beta_dt, double e_rest, double thr, int* ci,
