@@ -190,7 +190,8 @@ int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
 /* Tuning knobs. key 0: force the resident kernel's contact-warp count (0 = auto);
  * key 1: order units by their smallest referenced column (default 1; 0 = row order);
  * key 2: sort each CTA's free rows by decreasing length (default 1);
- * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0). */
+ * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0);
+ * key 6: resident grid barrier (0 one counter = default, 1/2 CTA pairs). */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */
@@ -220,6 +221,51 @@ int vfpi_scc_residual(vfpi_handle* h, int64_t n_c, const double* vc, const doubl
 /* inverse_contact (solver.py:468-475) */
 int vfpi_inverse_contact(vfpi_handle* h, const vfpi_system* sys, const double* v, double omega, int op,
                          double* lam);
+
+/* ---- virtual-node augmentation ------------------ */
+/* Replaces condsim.contacts.augment_dynamics (contacts.py:343-375):
+ *   A = [[A_o + k_v J_v^T J_v, -k_v J_v^T], [-k_v J_v, k_v I]]
+ * with the reference's exact scipy arithmetic and stored-entry rules
+ * (zero sums of J_v^T J_v and zero results of the top-left sum are not
+ * stored; J_v's stored entries, explicit zeros included, are kept in the
+ * off-diagonal blocks; no virtual node = A_o unchanged), so the output CSC
+ * equals SparseSymmetric.from_scipy(...) of the reference bit for bit.
+ * b of the augmented system is [b_o; 0] (the caller appends the zeros).
+ * A_o: canonical CSC (sorted rows, no duplicates), n_o x n_o.
+ * J_v: canonical CSR, n_v3 x n_o (n_v3 = 3 * NodalContactSet.n_virtual),
+ *      as nodalize builds it (contacts.py:311-320). */
+typedef struct vfpi_augment_input {
+  int64_t n_o;
+  int64_t n_v3;
+  int64_t a_nnz;
+  const int32_t* a_indptr;
+  const int32_t* a_indices;
+  const double* a_data;
+  int64_t jv_nnz;
+  const int32_t* jv_indptr;
+  const int32_t* jv_indices;
+  const double* jv_data;
+  double k_v;
+} vfpi_augment_input;
+
+typedef struct vfpi_augmented {
+  int64_t n;          /* n_o + n_v3 */
+  int64_t nnz;        /* stored entries */
+  int32_t* indptr;    /* [n+1] */
+  int32_t* indices;   /* [nnz] */
+  double* data;       /* [nnz] */
+} vfpi_augmented;
+
+/* Device pointers in; out->indptr/indices/data point at device buffers owned
+ * by the handle, valid until the next augmentation call on it or
+ * vfpi_destroy. Enqueued on `stream` (NULL = handle stream); returns after
+ * the output size is known (two small host reads). */
+int vfpi_augment_device(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augmented* out, void* stream);
+/* Host pointers in and out (synchronous). out->indptr/indices/data are
+ * caller buffers; out->nnz holds their capacity on entry (an upper bound is
+ * a_nnz + sum over J_v rows of nonzeros^2 + 2 jv_nnz + n_v3) and the stored
+ * entry count on return (VFPI_BAD_ARGUMENT if the capacity is too small). */
+int vfpi_augment(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augmented* out);
 
 #ifdef __cplusplus
 }

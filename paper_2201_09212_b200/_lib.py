@@ -46,6 +46,19 @@ class VfpiResult(C.Structure):
     ]
 
 
+class VfpiAugmentInput(C.Structure):
+    _fields_ = [
+        ("n_o", C.c_int64), ("n_v3", C.c_int64), ("a_nnz", C.c_int64),
+        ("a_indptr", _i32p), ("a_indices", _i32p), ("a_data", _f64p),
+        ("jv_nnz", C.c_int64), ("jv_indptr", _i32p), ("jv_indices", _i32p), ("jv_data", _f64p),
+        ("k_v", C.c_double),
+    ]
+
+
+class VfpiAugmented(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("indptr", _i32p), ("indices", _i32p), ("data", _f64p)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -77,6 +90,9 @@ def lib() -> C.CDLL:
                 "vfpi_set_kernel": (C.c_int, [H, C.c_int]),
                 "vfpi_set_profile": (C.c_int, [H, C.c_int]),
                 "vfpi_set_tuning": (C.c_int, [H, C.c_int, C.c_int]),
+                "vfpi_augment": (C.c_int, [H, C.POINTER(VfpiAugmentInput), C.POINTER(VfpiAugmented)]),
+                "vfpi_augment_device": (C.c_int, [H, C.POINTER(VfpiAugmentInput), C.POINTER(VfpiAugmented),
+                                                  C.c_void_p]),
                 "vfpi_get_profile": (C.c_int, [H, C.POINTER(C.c_longlong), C.c_int64]),
                 "vfpi_host_alloc": (C.c_void_p, [C.c_int64]),
                 "vfpi_host_free": (None, [C.c_void_p]),

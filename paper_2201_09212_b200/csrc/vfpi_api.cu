@@ -56,6 +56,7 @@ struct vfpi_handle {
   int tune_wc = 0;      // >0: force the contact-warp count of the resident kernel
   int bar_mode = 0;     // resident grid barrier (IterParams::bar_mode)
   vfpi::LayoutOptions layout_opt;
+  vfpi::AugmentWork aug;
   int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
@@ -230,6 +231,7 @@ int vfpi_create(int device, vfpi_handle** out) {
   cudaMallocHost(&h->ws.h_summary, sizeof(vfpi::SetupSummary));
   cudaMallocHost(&h->ws.h_status, sizeof(vfpi::SolveStatus));
   cudaMallocHost(&h->h_flags, 16);
+  cudaMallocHost(&h->aug.h_small, 2 * sizeof(int64_t));
   *out = h;
   return VFPI_OK;
 }
@@ -258,6 +260,12 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
   for (auto* b : bufs)
     if (b->p) cudaFree(b->p);
+  vfpi::AugmentWork& aw = h->aug;
+  for (Workspace::Buf* b : {&aw.pcnt, &aw.poff, &aw.pkey, &aw.pkey2, &aw.pval, &aw.pval2, &aw.head, &aw.hpos, &aw.tmp,
+                            &aw.tmp2, &aw.jrow, &aw.jcol_s, &aw.jidx, &aw.jperm, &aw.jcp, &aw.t_row, &aw.t_col,
+                            &aw.t_val, &aw.cs, &aw.ccnt, &aw.cptr, &aw.out_p, &aw.out_i, &aw.out_x})
+    if (b->p) cudaFree(b->p);
+  if (aw.h_small) cudaFreeHost(aw.h_small);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
   for (SetupGraph* g : {&h->graph_layout, &h->graph_pack})
@@ -1220,3 +1228,97 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
 }
 
 }  // extern "C"
+
+
+// ---- virtual-node augmentation ----------------------------------------------
+namespace {
+int augment_common(vfpi_handle* h, const vfpi_augment_input* in, const vfpi_augment_input& dev, cudaStream_t st,
+                   vfpi::AugmentOut& o) {
+  vfpi::AugmentIn ai;
+  ai.n_o = (int)in->n_o;
+  ai.n_v3 = (int)in->n_v3;
+  ai.a_nnz = in->a_nnz;
+  ai.jv_nnz = in->jv_nnz;
+  ai.a_indptr = dev.a_indptr;
+  ai.a_indices = dev.a_indices;
+  ai.a_data = dev.a_data;
+  ai.jv_indptr = dev.jv_indptr;
+  ai.jv_indices = dev.jv_indices;
+  ai.jv_data = dev.jv_data;
+  ai.k_v = in->k_v;
+  return vfpi::augment_device(h->aug, ai, st, o, h->err, h->launches);
+}
+bool augment_args_ok(vfpi_handle* h, const vfpi_augment_input* in) {
+  if (!in || in->n_o < 0 || in->n_v3 < 0 || in->n_v3 % 3 || in->a_nnz < 0 || in->jv_nnz < 0 ||
+      in->n_o + in->n_v3 > INT32_MAX || in->a_nnz > INT32_MAX || in->jv_nnz > INT32_MAX) {
+    h->err = "augment: bad sizes";
+    return false;
+  }
+  return true;
+}
+}  // namespace
+
+int vfpi_augment_device(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augmented* out, void* stream) {
+  if (!h || !out) return VFPI_BAD_ARGUMENT;
+  if (!augment_args_ok(h, in)) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::AugmentOut o;
+  const int rc = augment_common(h, in, *in, st, o);
+  if (rc != VFPI_OK) return rc;
+  out->n = o.n;
+  out->nnz = o.nnz;
+  out->indptr = o.indptr;
+  out->indices = o.indices;
+  out->data = o.data;
+  return VFPI_OK;
+}
+
+int vfpi_augment(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augmented* out) {
+  if (!h || !out) return VFPI_BAD_ARGUMENT;
+  if (!augment_args_ok(h, in)) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = h->ws.stream;
+  Workspace& ws = h->ws;
+  const int64_t n_o = in->n_o, rows = in->n_v3;
+  CK(vfpi::ensure(ws.b_indptr, sizeof(int) * (size_t)(n_o + 1 + rows + 1)));
+  CK(vfpi::ensure(ws.b_indices, sizeof(int) * (size_t)std::max<int64_t>(in->a_nnz + in->jv_nnz, 1)));
+  CK(vfpi::ensure(ws.b_data, sizeof(double) * (size_t)std::max<int64_t>(in->a_nnz + in->jv_nnz, 1)));
+  vfpi_augment_input dev = *in;
+  int* dp = P<int>(ws.b_indptr);
+  int* di = P<int>(ws.b_indices);
+  double* dx = P<double>(ws.b_data);
+  dev.a_indptr = dp;
+  dev.jv_indptr = dp + n_o + 1;
+  dev.a_indices = di;
+  dev.jv_indices = di + in->a_nnz;
+  dev.a_data = dx;
+  dev.jv_data = dx + in->a_nnz;
+  CK(cudaMemcpyAsync(dp, in->a_indptr, sizeof(int) * (size_t)(n_o + 1), cudaMemcpyHostToDevice, st));
+  if (rows) CK(cudaMemcpyAsync(dp + n_o + 1, in->jv_indptr, sizeof(int) * (size_t)(rows + 1), cudaMemcpyHostToDevice, st));
+  if (in->a_nnz) {
+    CK(cudaMemcpyAsync(di, in->a_indices, sizeof(int) * (size_t)in->a_nnz, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dx, in->a_data, sizeof(double) * (size_t)in->a_nnz, cudaMemcpyHostToDevice, st));
+  }
+  if (in->jv_nnz) {
+    CK(cudaMemcpyAsync(di + in->a_nnz, in->jv_indices, sizeof(int) * (size_t)in->jv_nnz, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dx + in->a_nnz, in->jv_data, sizeof(double) * (size_t)in->jv_nnz, cudaMemcpyHostToDevice, st));
+  }
+  vfpi::AugmentOut o;
+  const int rc = augment_common(h, in, dev, st, o);
+  if (rc != VFPI_OK) return rc;
+  if (o.nnz > out->nnz) {
+    h->err = "augment: output capacity too small (need " + std::to_string(o.nnz) + ")";
+    out->nnz = o.nnz;
+    return VFPI_BAD_ARGUMENT;
+  }
+  CK(cudaMemcpyAsync(out->indptr, o.indptr, sizeof(int) * (size_t)(o.n + 1), cudaMemcpyDeviceToHost, st));
+  if (o.nnz) {
+    CK(cudaMemcpyAsync(out->indices, o.indices, sizeof(int) * (size_t)o.nnz, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out->data, o.data, sizeof(double) * (size_t)o.nnz, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  out->n = o.n;
+  out->nnz = o.nnz;
+  return VFPI_OK;
+}

@@ -230,6 +230,34 @@ int setup_rowpos(Workspace& ws, int n, int G, cudaStream_t st, std::string& err)
 int setup_contacts_refresh(Workspace& ws, const vfpi_system& dsys, int G, const int* d_scene_ct_ptr, cudaStream_t st,
                            std::string& err, int64_t& launches);
 
+// ---- virtual-node augmentation (vfpi_augment.cu) ----------------------------
+struct AugmentIn {
+  int n_o = 0, n_v3 = 0;  // original dimension, rows of J_v (3 per virtual node)
+  int64_t a_nnz = 0, jv_nnz = 0;
+  const int* a_indptr = nullptr;   // CSC of A_o (device), canonical
+  const int* a_indices = nullptr;
+  const double* a_data = nullptr;
+  const int* jv_indptr = nullptr;  // CSR of J_v (device), canonical
+  const int* jv_indices = nullptr;
+  const double* jv_data = nullptr;
+  double k_v = 0.0;
+};
+struct AugmentOut {
+  int n = 0;
+  int64_t nnz = 0;
+  int* indptr = nullptr;  // device, owned by the AugmentWork
+  int* indices = nullptr;
+  double* data = nullptr;
+};
+struct AugmentWork {
+  Workspace::Buf pcnt, poff, pkey, pkey2, pval, pval2, head, hpos, tmp, tmp2;
+  Workspace::Buf jrow, jcol_s, jidx, jperm, jcp, t_row, t_col, t_val, cs, ccnt, cptr;
+  Workspace::Buf out_p, out_i, out_x;
+  int64_t* h_small = nullptr;  // pinned [2]
+};
+int augment_device(AugmentWork& w, const AugmentIn& in, cudaStream_t st, AugmentOut& out, std::string& err,
+                   int64_t& launches);
+
 // ---- FEM scene-batch step pipeline (vfpi_fem.cu) ----------------------------
 void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,
                     const double* v, const double* m, const double* g, double twodt, double* b, cudaStream_t st);

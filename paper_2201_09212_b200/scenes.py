@@ -31,8 +31,33 @@ def _quat_to_rot(q):
 
 
 def rigid_contact_system(n_bodies: int = 4096, n_contacts: int = 16384, seed: int = 2201, k_v: float = 1e5,
-                         dt: float = 1e-3, beta_err: float = 0.2) -> PackedSystem:
-    """configs[1]: 4096 rigid bodies, 16384 D-contacts (defaults)."""
+                         dt: float = 1e-3, beta_err: float = 0.2, augment: str = "host") -> PackedSystem:
+    """configs[1]: 4096 rigid bodies, 16384 D-contacts (defaults).
+
+    ``augment="host"`` forms the augmented matrix with the reference's scipy
+    expression (the fixture path), ``"device"`` with ``vfpi_augment`` on the
+    GPU (bit-identical, ``tests/test_gpu_augment.py``)."""
+    p = rigid_contact_parts(n_bodies, n_contacts, seed, k_v, dt, beta_err)
+    if augment == "device":
+        from .augment import augment_arrays
+
+        ip, ix, dx = augment_arrays(p["n_o"], p["a_o"].indptr, p["a_o"].indices, p["a_o"].data, p["jv"], k_v)
+    else:
+        a_o, jv = p["a_o"], p["jv"]
+        top_left = a_o + k_v * (jv.T @ jv)
+        nv3 = jv.shape[0]
+        a = sp.bmat([[top_left, -k_v * jv.T], [-k_v * jv, k_v * sp.identity(nv3, format="csr")]], format="csc")
+        a = sp.csc_matrix(a)
+        a.sum_duplicates()
+        ip, ix, dx = a.indptr, a.indices, a.data
+    b = np.concatenate([p["b_o"], np.zeros(p["jv"].shape[0])])
+    return make_packed(p["n_o"] + p["jv"].shape[0], ip, ix, dx, b, p["col_i"], p["col_j"], p["frames"], p["mu"],
+                       p["mu"], p["phi"])
+
+
+def rigid_contact_parts(n_bodies: int = 4096, n_contacts: int = 16384, seed: int = 2201, k_v: float = 1e5,
+                        dt: float = 1e-3, beta_err: float = 0.2) -> dict:
+    """configs[1] before augmentation: A_o (CSC), b_o, J_v (CSR, nodalize's), contacts."""
     rng = np.random.default_rng(seed)
     mass = rng.uniform(0.5, 2.0, n_bodies)
     inert = rng.uniform(0.01, 0.1, (n_bodies, 3))
@@ -78,15 +103,8 @@ def rigid_contact_system(n_bodies: int = 4096, n_contacts: int = 16384, seed: in
     for m in range(n_contacts):
         frames[m] = contact_frame(normals[m])
     phi = np.full(n_contacts, -(beta_err / dt) * 0.0)  # depth 0, bodies at rest
-
-    top_left = a_o + k_v * (jv.T @ jv)
-    a = sp.bmat([[top_left, -k_v * jv.T], [-k_v * jv, k_v * sp.identity(3 * n_v, format="csr")]], format="csc")
-    a = sp.csc_matrix(a)
-    a.sum_duplicates()
-    b = np.concatenate([b_o, np.zeros(3 * n_v)])
     col_i = n_o + 6 * np.arange(n_contacts)
-    col_j = col_i + 3
-    return make_packed(n_o + 3 * n_v, a.indptr, a.indices, a.data, b, col_i, col_j, frames, mus, mus, phi)
+    return dict(n_o=n_o, a_o=a_o, b_o=b_o, jv=jv, col_i=col_i, col_j=col_i + 3, frames=frames, mu=mus, phi=phi)
 
 
 # ---------------------------------------------------------------------------

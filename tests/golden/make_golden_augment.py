@@ -1,0 +1,138 @@
+"""Golden vectors of the virtual-node augmentation, from the REFERENCE.
+
+Run in the build container only (the reference does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden_augment.py
+
+Every case calls the reference's ``augment_dynamics`` (``contacts.py:343-375``)
+and stores its input (A_o CSC arrays, b_o, J_v CSR arrays, k_v) and output
+(the augmented CSC arrays and b):
+
+* ``aug_rigid``: rigid bodies through the reference ``nodalize``
+  (``contacts.py:271-321``, ``_slot_and_jv`` rigid sides: J_v blocks
+  ``[I, -[r]x]``), including pairs of virtual nodes on one body with opposite
+  levers (exact cancellations in J_vᵀJ_v) and explicit zeros stored in A_o;
+* ``aug_face``: two FEM blocks with barycentric face-side virtual nodes
+  (blocks ``w_k I`` on three nodes; some ``w_k`` exactly 0) and identity
+  virtual nodes (a node's second contact, ``contacts.py:249-255``), J_v built
+  the way ``nodalize`` builds it (COO of every block entry -> CSR);
+* ``aug_none``: no virtual node (A_o returned unchanged, explicit zeros kept).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import scipy.sparse as sp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from condsim.contacts import NodalContactSet, RawContact, augment_dynamics, nodalize  # noqa: E402
+from condsim.dynamics import Body, SystemState, _quat_to_rot  # noqa: E402
+from condsim.sparse import SparseSymmetric  # noqa: E402
+
+
+def save(name, a_o, b_o, jv, k_v, aug):
+    jv = sp.csr_matrix(jv) if jv is not None else sp.csr_matrix((0, a_o.dim))
+    np.savez_compressed(
+        os.path.join(HERE, name + ".npz"), n_o=np.int64(a_o.dim), a_indptr=a_o.indptr.astype(np.int32),
+        a_indices=a_o.indices.astype(np.int32), a_data=a_o.data, b_o=b_o, jv_rows=np.int64(jv.shape[0]),
+        jv_indptr=jv.indptr.astype(np.int32), jv_indices=jv.indices.astype(np.int32), jv_data=jv.data,
+        k_v=np.float64(k_v), out_indptr=aug.a.indptr.astype(np.int32), out_indices=aug.a.indices.astype(np.int32),
+        out_data=aug.a.data, out_b=aug.b)
+    print(name, "n", aug.n, "nnz", aug.a.data.shape[0], "zeros", int((aug.a.data == 0).sum()))
+
+
+def rigid_case(rng, n_bodies=48, n_contacts=160, k_v=1e5):
+    bodies, q, rows, cols, vals = [], [], [], [], []
+    for k in range(n_bodies):
+        m = rng.uniform(0.5, 2.0)
+        inert = rng.uniform(0.01, 0.1, 3)
+        quat = rng.standard_normal(4)
+        quat /= np.linalg.norm(quat)
+        bodies.append(Body("rigid6", float(m), 7 * k, 6 * k, np.diag(inert)))
+        q += [np.zeros(3), quat]
+        rot = _quat_to_rot(quat)
+        for off, blk in ((6 * k, m * np.eye(3)), (6 * k + 3, rot @ np.diag(inert) @ rot.T)):
+            ii, jj = np.meshgrid(range(off, off + 3), range(off, off + 3), indexing="ij")
+            rows.append(ii.ravel())
+            cols.append(jj.ravel())
+            vals.append(blk.ravel())
+        # explicit zeros between the translational and rotational blocks of some bodies
+        if k % 3 == 0:
+            rows.append(np.array([6 * k, 6 * k + 3]))
+            cols.append(np.array([6 * k + 3, 6 * k]))
+            vals.append(np.zeros(2))
+    n_o = 6 * n_bodies
+    a_o = SparseSymmetric.from_scipy(sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows),
+                                                                          np.concatenate(cols))),
+                                                   shape=(n_o, n_o)).tocsc())
+    b_o = rng.standard_normal(n_o)
+    state = SystemState(np.concatenate(q), np.zeros(n_o), 0, 1e-3)
+    raw = []
+    for m in range(n_contacts):
+        i, j = rng.choice(n_bodies - 2, 2, replace=False)
+        lever = rng.uniform(-0.1, 0.1, 3)
+        raw.append(RawContact(point=lever, normal=rng.standard_normal(3), depth=0.0,
+                              first=("rigid", int(i), m), second=("rigid", int(j), m)))
+        if m % 10 == 0:  # mirrored lever on the same bodies: J_v^T J_v cross terms cancel exactly
+            raw.append(RawContact(point=-lever, normal=rng.standard_normal(3), depth=0.0,
+                                  first=("rigid", int(i), m + 100000), second=("rigid", int(j), m + 100000)))
+    if n_contacts:  # the last two bodies: only a mirrored pair -> exact zero sums in J_v^T J_v
+        lever = np.array([0.0625, -0.03125, 0.0])
+        for s, k in ((1.0, 0), (-1.0, 1)):
+            raw.append(RawContact(point=s * lever, normal=np.array([0.0, 0.0, 1.0]), depth=0.0,
+                                  first=("rigid", n_bodies - 2, -1 - k), second=("rigid", n_bodies - 1, -1 - k)))
+    nodal = nodalize(raw, state, bodies, k_v, 0.5)
+    return a_o, b_o, nodal
+
+
+def face_case(rng, k_v=1e5):
+    from paper_2201_09212_b200.scenes import FemCube
+
+    blocks = [FemCube(nx=4).A, FemCube(nx=4, E=2e5).A]
+    a = sp.block_diag(blocks, format="csc")
+    a_o = SparseSymmetric.from_scipy(a)
+    n_o = a_o.dim
+    nn = n_o // 3
+    b_o = rng.standard_normal(n_o)
+    jv_rows = []
+    nv = 0
+    for f in range(40):  # face-side virtual nodes: w0 I, w1 I, w2 I on three nodes
+        nodes = rng.choice(nn, 3, replace=False)
+        w = rng.dirichlet(np.ones(3))
+        if f % 7 == 0:
+            w = np.array([0.25, 0.75, 0.0])
+        for node, wk in zip(nodes, w):
+            jv_rows.append((nv, 3 * int(node), wk * np.eye(3)))
+        nv += 1
+    for node in rng.choice(nn, 12, replace=False):  # identity virtual nodes
+        jv_rows.append((nv, 3 * int(node), np.eye(3)))
+        nv += 1
+    r, c, v = [], [], []
+    for virt, off, block in jv_rows:  # contacts.py:311-320
+        for rr in range(3):
+            for cc in range(block.shape[1]):
+                r.append(3 * virt + rr)
+                c.append(off + cc)
+                v.append(block[rr, cc])
+    jv = sp.csr_matrix((v, (r, c)), shape=(3 * nv, n_o))
+    return a_o, b_o, NodalContactSet([], nv, jv, k_v)
+
+
+def main():
+    rng = np.random.default_rng(91)
+    a_o, b_o, nodal = rigid_case(rng)
+    save("aug_rigid", a_o, b_o, nodal.jv, nodal.k_v, augment_dynamics(a_o, b_o, nodal))
+    a_o, b_o, nodal = face_case(rng)
+    save("aug_face", a_o, b_o, nodal.jv, nodal.k_v, augment_dynamics(a_o, b_o, nodal))
+    a_o2, b_o2, _ = rigid_case(rng, n_bodies=6, n_contacts=0)
+    save("aug_none", a_o2, b_o2, None, 1e5, augment_dynamics(a_o2, b_o2, NodalContactSet([], 0, None, 1e5)))
+
+
+if __name__ == "__main__":
+    main()

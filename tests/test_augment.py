@@ -1,0 +1,99 @@
+"""Virtual-node augmentation (reference
+``augment_dynamics``, contacts.py:343-375).
+
+CPU: the oracle restatement against golden vectors produced by the reference
+itself (``tests/golden/make_golden_augment.py``). GPU (``-m gpu``): the device
+augmentation (``vfpi_augment``) against the same goldens and against the
+reference's scipy expression at configs[1] size — bit for bit, pattern and
+values."""
+
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import vfpi_oracle as O
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CASES = ["aug_rigid", "aug_face", "aug_none"]
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLD, name + ".npz")))
+
+
+def jv_of(d):
+    return sp.csr_matrix((d["jv_data"], d["jv_indices"], d["jv_indptr"]), shape=(int(d["jv_rows"]), int(d["n_o"])))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_augment_matches_reference(name):
+    d = load(name)
+    p, i, x, b = O.augment(int(d["n_o"]), d["a_indptr"], d["a_indices"], d["a_data"], d["b_o"], jv_of(d),
+                           float(d["k_v"]))
+    assert np.array_equal(p, d["out_indptr"])
+    assert np.array_equal(i, d["out_indices"])
+    assert np.array_equal(x, d["out_data"])
+    assert np.array_equal(b, d["out_b"])
+
+
+def test_golden_cases_exercise_the_stored_entry_rules():
+    r = load("aug_rigid")
+    # explicit zeros of A_o vanish in the top-left sum, J_v's zeros stay in the off-diagonal blocks
+    assert (r["a_data"] == 0).any()
+    n_o = int(r["n_o"])
+    top = sp.csc_matrix((r["out_data"], r["out_indices"], r["out_indptr"]))[:n_o, :n_o]
+    assert not (top.data == 0).any()
+    assert (r["out_data"] == 0).any()
+    # exact cancellations in J_v^T J_v: fewer top-left entries than the union of the patterns
+    jv = jv_of(r)
+    pat = jv.copy()
+    pat.data = (pat.data != 0).astype(float)
+    assert (jv.T @ jv).nnz < (pat.T @ pat).nnz
+    f = load("aug_face")
+    assert (f["jv_data"] == 0).any() and int(f["jv_rows"]) > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_device_augment_matches_reference(name):
+    from paper_2201_09212_b200.augment import augment_arrays
+
+    d = load(name)
+    p, i, x = augment_arrays(int(d["n_o"]), d["a_indptr"], d["a_indices"], d["a_data"], jv_of(d), float(d["k_v"]))
+    assert np.array_equal(p, d["out_indptr"])
+    assert np.array_equal(i, d["out_indices"])
+    assert np.array_equal(x, d["out_data"])
+
+
+@pytest.mark.gpu
+def test_device_augment_dynamics_api():
+    from paper_2201_09212_b200.augment import augment_dynamics
+    from paper_2201_09212_b200.errors import DimensionMismatchError
+    from paper_2201_09212_b200.system import Contact, NodalContactSet, SparseSymmetric
+
+    d = load("aug_face")
+    n_o = int(d["n_o"])
+    a_o = SparseSymmetric(n_o, d["a_indptr"], d["a_indices"], d["a_data"])
+    nv = int(d["jv_rows"]) // 3
+    frame = np.eye(3)
+    cs = [Contact("D", ("orig", 0), frame, 0.5, 0.0, slot_j=("virt", 1)), Contact("S", ("virt", 2), frame, 0.5, 0.0)]
+    aug = augment_dynamics(a_o, d["b_o"], NodalContactSet(cs, nv, jv_of(d), float(d["k_v"])))
+    assert aug.n == n_o + 3 * nv and aug.n_orig == n_o
+    assert np.array_equal(aug.a.data, d["out_data"]) and np.array_equal(aug.b, d["out_b"])
+    assert list(aug.col_i) == [0, n_o + 6] and list(aug.col_j) == [n_o + 3, -1]
+    with pytest.raises(DimensionMismatchError):
+        augment_dynamics(a_o, d["b_o"][:-1], NodalContactSet(cs, nv, jv_of(d), 1e5))
+
+
+@pytest.mark.gpu
+def test_device_augment_configs1_size():
+    """Full configs[1] (4096 bodies, 32768 virtual nodes): device == scipy."""
+    from paper_2201_09212_b200.scenes import rigid_contact_system
+
+    host = rigid_contact_system()
+    dev = rigid_contact_system(augment="device")
+    assert np.array_equal(host.indptr, dev.indptr)
+    assert np.array_equal(host.indices, dev.indices)
+    assert np.array_equal(host.data, dev.data)
