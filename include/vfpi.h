@@ -267,6 +267,23 @@ int vfpi_augment_device(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augme
  * entry count on return (VFPI_BAD_ARGUMENT if the capacity is too small). */
 int vfpi_augment(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augmented* out);
 
+/* ---- step-pipeline primitives (device pointers, enqueued on `stream`) -- */
+/* b = (2/dt) m v - K (x - X) + m g: the elastic right-hand side of the FEM
+ * scenes (Eq. 10 with e = u; the reference's assemble_step analogue,
+ * dynamics.py:176-218), K in CSR (int64 row pointers), rows summed in
+ * increasing column order like scipy's matvec. */
+int vfpi_fem_rhs_device(vfpi_handle* h, int64_t n, const int64_t* k_indptr, const int32_t* k_indices,
+                        const double* k_data, const double* x, const double* X, const double* v, const double* m,
+                        const double* g, double dt, double* b, void* stream);
+/* y = J x, J in CSR (scipy csr_matvec order): the warm start's virtual-node
+ * extension v0[n_o:] = J_v v0[:n_o] (harness._warm_velocity, harness.py:502-512). */
+int vfpi_csr_matvec_device(vfpi_handle* h, int64_t rows, const int32_t* indptr, const int32_t* indices,
+                           const double* data, const double* x, double* y, void* stream);
+/* midpoint integration of the original coordinates (dynamics.py:237-255):
+ * x += dt v_hat; v = 2 v_hat - v. */
+int vfpi_advance_device(vfpi_handle* h, int64_t n, double dt, const double* v_hat, double* x, double* v,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

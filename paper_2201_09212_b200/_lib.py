@@ -94,6 +94,13 @@ def lib() -> C.CDLL:
                 "vfpi_augment_device": (C.c_int, [H, C.POINTER(VfpiAugmentInput), C.POINTER(VfpiAugmented),
                                                   C.c_void_p]),
                 "vfpi_get_profile": (C.c_int, [H, C.POINTER(C.c_longlong), C.c_int64]),
+                "vfpi_fem_rhs_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                                  C.c_void_p, C.c_void_p]),
+                "vfpi_csr_matvec_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                     C.c_void_p, C.c_void_p]),
+                "vfpi_advance_device": (C.c_int, [H, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                  C.c_void_p]),
                 "vfpi_host_alloc": (C.c_void_p, [C.c_int64]),
                 "vfpi_host_free": (None, [C.c_void_p]),
                 "vfpi_spmv": (C.c_int, [H, sysp, _f64p, _f64p]),

@@ -1322,3 +1322,38 @@ int vfpi_augment(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augmented* o
   out->nnz = o.nnz;
   return VFPI_OK;
 }
+
+// ---- step-pipeline primitives (device pointers, caller stream) --------------
+int vfpi_fem_rhs_device(vfpi_handle* h, int64_t n, const int64_t* k_indptr, const int32_t* k_indices,
+                        const double* k_data, const double* x, const double* X, const double* v, const double* m,
+                        const double* g, double dt, double* b, void* stream) {
+  if (!h || n < 0) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::launch_fem_rhs(n, k_indptr, k_indices, k_data, x, X, v, m, g, 2.0 / dt, b, st);
+  h->launches += n > 0;
+  CK(cudaGetLastError());
+  return VFPI_OK;
+}
+
+int vfpi_csr_matvec_device(vfpi_handle* h, int64_t rows, const int32_t* indptr, const int32_t* indices,
+                           const double* data, const double* x, double* y, void* stream) {
+  if (!h || rows < 0) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::launch_csr_matvec(rows, indptr, indices, data, x, y, st);
+  h->launches += rows > 0;
+  CK(cudaGetLastError());
+  return VFPI_OK;
+}
+
+int vfpi_advance_device(vfpi_handle* h, int64_t n, double dt, const double* v_hat, double* x, double* v,
+                        void* stream) {
+  if (!h || n < 0) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::launch_fem_advance(n, dt, v_hat, x, v, nullptr, st);
+  h->launches += n > 0;
+  CK(cudaGetLastError());
+  return VFPI_OK;
+}

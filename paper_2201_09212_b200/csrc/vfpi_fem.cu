@@ -124,7 +124,19 @@ __global__ void k_fem_advance(int64_t n, double dt, const double* __restrict__ v
   const double h = vh[i];
   x[i] = dadd(x[i], dmul(dt, h));
   v[i] = dsub(dmul(2.0, h), v[i]);
-  warm[i] = h;
+  if (warm) warm[i] = h;
+}
+
+// y = J x with J in CSR, each row summed from 0 in stored order (scipy's
+// csr_matvec; explicit zeros included): the warm-start extension
+// v0[n_o:] = J_v v0[:n_o] of harness._warm_velocity (harness.py:502-512)
+__global__ void k_csr_matvec(int64_t rows, const int* __restrict__ rp, const int* __restrict__ ci,
+                             const double* __restrict__ cx, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (int e = rp[r]; e < rp[r + 1]; ++e) s = dadd(s, dmul(cx[e], x[ci[e]]));
+  y[r] = s;
 }
 
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -169,6 +181,11 @@ void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int
 
 void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st) {
   if (n > 0) k_fem_advance<<<nb(n), 256, 0, st>>>(n, dt, vh, x, v, warm);
+}
+
+void launch_csr_matvec(int64_t rows, const int* rp, const int* ci, const double* cx, const double* x, double* y,
+                       cudaStream_t st) {
+  if (rows > 0) k_csr_matvec<<<nb(rows), 256, 0, st>>>(rows, rp, ci, cx, x, y);
 }
 
 }  // namespace vfpi

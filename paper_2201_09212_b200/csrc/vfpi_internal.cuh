@@ -273,5 +273,7 @@ void launch_fem_contacts(int64_t nodes, const int* flag, const int* pos, const d
                          int* cj, double* frames, double* muv, double* mu2v, double* phi, cudaStream_t st);
 void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int* pos, int* cts, cudaStream_t st);
 void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st);
+void launch_csr_matvec(int64_t rows, const int* rp, const int* ci, const double* cx, const double* x, double* y,
+                       cudaStream_t st);
 
 }  // namespace vfpi

@@ -1,0 +1,411 @@
+"""configs[4]: a pile of deformable cubes with node-to-face contacts
+(SURVEY §8(f) items 2-3).
+
+The reference has no FEM and no face-side contacts: ``detect_contacts``
+(``contacts.py:159-227``) pairs sphere proxies through a KD-tree and
+``_slot_and_jv`` (``:242-268``) resolves only ``node`` and ``rigid`` sides.
+This module keeps the reference's pipeline and adds the missing pieces the
+way the reference would write them:
+
+* **geometry** -- ``n_x x n_y x layers`` copies of the ``scenes.FemCube``
+  linear-tet cube (configs[0] material), placed on a grid with seeded jitter;
+  A_o, K, M are block diagonal (one block per cube, the cube's own arrays);
+* **broad phase** -- a spatial hash: every surface triangle is entered in the
+  cells (edge ``2h``) its bounding box, grown by the search distance, overlaps;
+  every surface node looks up its own cell (sort + binary search, no Python
+  loop over contacts);
+* **narrow phase** -- node ``p`` of cube A against triangle ``(a, b, c)`` of
+  cube B != A: signed distance ``d = (p - a).n`` along B's outward normal,
+  ``-h/2 < d < margin`` and the projection inside the triangle (barycentric
+  weights ``w >= 0``); one contact per node, the candidate with the largest
+  ``d``; ground contacts (plane ``z = 0``) as in ``scenes.FemCube``;
+* **nodalize** -- ``contacts.py:271-321`` with a third side kind, ``face``:
+  a virtual node tied to the triangle's three nodes by ``J_v = [w0 I, w1 I,
+  w2 I]`` (three 3x3 blocks, stored entry by entry as ``nodalize`` stores its
+  blocks); a node's second contact moves to an identity virtual node
+  (``contacts.py:249-255``); plane contacts come first, as in
+  ``detect_contacts``; frames ``contact_frame(n)``, ``phi`` from
+  ``stabilization_term`` (``:230-239``);
+* **augmentation** -- ``augment.augment_arrays`` (device, bit-identical to the
+  reference's ``augment_dynamics``).
+
+``CubePile.system()`` returns the augmented system of the current
+state; ``advance`` integrates (midpoint, ``dynamics.py:237-255``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from .scenes import FemCube, _tets
+from .system import PackedSystem, make_packed
+
+
+def surface_triangles(nx: int, X: np.ndarray) -> np.ndarray:
+    """Boundary faces of the 5-tet hex split, oriented outward (T, 3)."""
+    tets = _tets(nx)
+    faces = np.concatenate([tets[:, [1, 2, 3]], tets[:, [0, 2, 3]], tets[:, [0, 1, 3]], tets[:, [0, 1, 2]]])
+    opp = np.concatenate([tets[:, 0], tets[:, 1], tets[:, 2], tets[:, 3]])
+    key = np.sort(faces, axis=1)
+    _, inv, cnt = np.unique(key, axis=0, return_inverse=True, return_counts=True)
+    bnd = cnt[inv.ravel()] == 1
+    f, o = faces[bnd].copy(), opp[bnd]
+    nrm = np.cross(X[f[:, 1]] - X[f[:, 0]], X[f[:, 2]] - X[f[:, 0]])
+    inward = np.einsum("ij,ij->i", nrm, X[o] - X[f[:, 0]]) > 0
+    f[inward, 1], f[inward, 2] = f[inward, 2], f[inward, 1].copy()
+    return f
+
+
+def contact_frames(normals: np.ndarray) -> np.ndarray:
+    """``contact_frame`` (``contacts.py:131-149``) for many normals at once."""
+    n = np.asarray(normals, dtype=float)
+    norm = np.sqrt(np.einsum("ij,ij->i", n, n))
+    fix = np.abs(norm - 1.0) > 1e-9
+    n = np.where(fix[:, None], n / norm[:, None], n)
+    e = np.zeros_like(n)
+    e[np.arange(n.shape[0]), np.argmin(np.abs(n), axis=1)] = 1.0
+    t1 = np.cross(np.cross(n, e), n)
+    t1 /= np.sqrt(np.einsum("ij,ij->i", t1, t1))[:, None]
+    return np.stack([n, t1, np.cross(n, t1)], axis=1)
+
+
+@dataclass
+class PileContacts:
+    """Nodalized contacts of one step (``NodalContactSet`` in flat arrays)."""
+
+    col_i: np.ndarray
+    col_j: np.ndarray
+    frames: np.ndarray  # (n_c, 3, 3)
+    phi: np.ndarray
+    mu: np.ndarray
+    jv: sp.csr_matrix   # (3 n_virtual, n_o)
+    n_ground: int
+    n_face: int
+
+    @property
+    def n_c(self) -> int:
+        return int(self.col_i.shape[0])
+
+    @property
+    def n_virtual(self) -> int:
+        return int(self.jv.shape[0]) // 3
+
+
+class CubePile:
+    """``nx_cubes x ny_cubes x layers`` FEM cubes of ``nodes^3`` nodes (configs[4]:
+    8 x 8 x 4, 16^3, mu 0.6, dt 5e-4; small sizes for parity tests)."""
+
+    def __init__(self, nx_cubes=8, ny_cubes=8, layers=4, nodes=16, side=0.1, gap=0.005, jitter=0.002, seed=0,
+                 E=1e5, nu=0.3, rho=1000.0, dt=5e-4, mu=0.6, gravity=-9.81, margin=1e-4, beta_err=0.2,
+                 e_rest=0.0, rest_threshold=0.01, k_v=1e5):
+        self.dt, self.mu, self.margin, self.k_v = dt, mu, margin, k_v
+        self.beta, self.e_rest, self.thr = beta_err, e_rest, rest_threshold
+        self.h = side / (nodes - 1)
+        cube = FemCube(nx=nodes, side=side, E=E, nu=nu, rho=rho, drop=0.0, dt=dt, mu=mu, gravity=gravity,
+                       margin=margin, beta_err=beta_err, e_rest=e_rest, rest_threshold=rest_threshold)
+        self.cube = cube
+        nc = nx_cubes * ny_cubes * layers
+        self.n_cubes, self.nn_cube = nc, nodes ** 3
+        rng = np.random.default_rng(seed)
+        pitch = side + gap
+        ix, iy, iz = np.meshgrid(np.arange(nx_cubes), np.arange(ny_cubes), np.arange(layers), indexing="ij")
+        base = np.stack([ix.ravel() * pitch, iy.ravel() * pitch, gap + iz.ravel() * pitch], axis=1)
+        order = np.lexsort((base[:, 0], base[:, 1], base[:, 2]))  # layer-major cube order
+        base = base[order] + rng.uniform(-jitter, jitter, (nc, 3))
+        Xt = cube.X - np.array([0.0, 0.0, 0.0])
+        self.X = (Xt[None, :, :] + base[:, None, :]).reshape(-1, 3)
+        self.x = self.X.copy()
+        self.v = np.zeros_like(self.X)
+        self.n = 3 * self.X.shape[0]
+        self.node_cube = np.repeat(np.arange(nc), self.nn_cube)
+        tri_t = surface_triangles(nodes, cube.X)
+        self.tris = (tri_t[None, :, :] + (self.nn_cube * np.arange(nc))[:, None, None]).reshape(-1, 3)
+        self.tri_cube = np.repeat(np.arange(nc), tri_t.shape[0])
+        surf_t = np.unique(tri_t)
+        self.surf = (surf_t[None, :] + (self.nn_cube * np.arange(nc))[:, None]).ravel()
+        self.m = np.tile(cube.m, nc)
+        self.gravity = np.tile(cube.gravity, nc)
+        A, K = cube.A, cube.K.tocsr()
+        K.sort_indices()
+        self.a_indptr, self.a_indices, self.a_data = _tile_compressed(A, nc)
+        self.k_indptr, self.k_indices, self.k_data = _tile_compressed(K, nc)
+
+    # ---- host right-hand side (the restatement the device path matches) ----
+    def rhs(self) -> np.ndarray:
+        """b = (2/dt) M v - K (x - X) + M g (scenes.FemCube.system), per row in
+        increasing column order (scipy's CSC/CSR matvec order)."""
+        K = sp.csr_matrix((self.k_data, self.k_indices, self.k_indptr), shape=(self.n, self.n))
+        u = (self.x - self.X).ravel()
+        return (2.0 / self.dt) * self.m * self.v.ravel() - K @ u + self.m * self.gravity
+
+    # ---- detection ----------------------------------------------------------
+    def detect(self):
+        """Raw contacts of the current state: plane contacts (all nodes with
+        z < margin, node order), then node-to-face contacts (node order)."""
+        x = self.x
+        ground = np.nonzero(x[:, 2] < self.margin)[0]
+        reach = max(0.5 * self.h, self.margin)
+        cell = 2.0 * self.h
+        tri = self.tris
+        P = x[tri]                                    # (T, 3, 3)
+        lo = np.floor((P.min(axis=1) - reach) / cell).astype(np.int64)
+        hi = np.floor((P.max(axis=1) + reach) / cell).astype(np.int64)
+        span = hi - lo
+        if span.max(initial=0) > 2:
+            raise ValueError("pile: a surface triangle spans more than 3 hash cells (mesh too deformed)")
+        keys, owner = [], []
+        for dx in range(3):
+            for dy in range(3):
+                for dz in range(3):
+                    ok = (dx <= span[:, 0]) & (dy <= span[:, 1]) & (dz <= span[:, 2])
+                    c = lo[ok] + np.array([dx, dy, dz])
+                    keys.append(_cell_key(c))
+                    owner.append(np.nonzero(ok)[0])
+        keys, owner = np.concatenate(keys), np.concatenate(owner)
+        o = np.argsort(keys, kind="stable")
+        keys, owner = keys[o], owner[o]
+        s = self.surf
+        nk = _cell_key(np.floor(x[s] / cell).astype(np.int64))
+        beg, end = np.searchsorted(keys, nk, "left"), np.searchsorted(keys, nk, "right")
+        cnt = end - beg
+        pn = np.repeat(s, cnt)
+        pt = owner[np.repeat(beg, cnt) + _ragged_arange(cnt)]
+        keep = self.node_cube[pn] != self.tri_cube[pt]
+        pn, pt = pn[keep], pt[keep]
+        p = x[pn]
+        a, b, c = x[tri[pt, 0]], x[tri[pt, 1]], x[tri[pt, 2]]
+        nrm = np.cross(b - a, c - a)
+        nrm /= np.sqrt(np.einsum("ij,ij->i", nrm, nrm))[:, None]
+        d = np.einsum("ij,ij->i", p - a, nrm)
+        keep = (d > -0.5 * self.h) & (d < self.margin)
+        pn, pt, p, a, b, c, nrm, d = pn[keep], pt[keep], p[keep], a[keep], b[keep], c[keep], nrm[keep], d[keep]
+        q = p - d[:, None] * nrm
+        v0, v1, v2 = b - a, c - a, q - a
+        d00 = np.einsum("ij,ij->i", v0, v0)
+        d01 = np.einsum("ij,ij->i", v0, v1)
+        d11 = np.einsum("ij,ij->i", v1, v1)
+        d20 = np.einsum("ij,ij->i", v2, v0)
+        d21 = np.einsum("ij,ij->i", v2, v1)
+        den = d00 * d11 - d01 * d01
+        w1 = (d11 * d20 - d01 * d21) / den
+        w2 = (d00 * d21 - d01 * d20) / den
+        w0 = 1.0 - w1 - w2
+        keep = (w0 >= 0.0) & (w1 >= 0.0) & (w2 >= 0.0)
+        pn, pt, nrm, d = pn[keep], pt[keep], nrm[keep], d[keep]
+        w = np.stack([w0[keep], w1[keep], w2[keep]], axis=1)
+        o = np.lexsort((pt, -d, pn))                  # per node: largest d, then lowest triangle
+        pn, pt, nrm, d, w = pn[o], pt[o], nrm[o], d[o], w[o]
+        first = np.ones(pn.shape[0], dtype=bool)
+        first[1:] = pn[1:] != pn[:-1]
+        face = dict(node=pn[first], tri=tri[pt[first]], w=w[first], normal=nrm[first],
+                    depth=np.maximum(0.0, -d[first]))
+        return ground, face
+
+    # ---- nodalize (contacts.py:271-321 with face sides) ----------------------
+    def nodalize(self, ground, face) -> PileContacts:
+        n_o = self.n
+        ng, nf = ground.shape[0], face["node"].shape[0]
+        first_node = np.concatenate([ground, face["node"]])
+        n_c = ng + nf
+        # a node's first contact takes its own slot, later ones an identity virtual node
+        _, first_idx = np.unique(first_node, return_index=True)
+        own = np.zeros(n_c, dtype=bool)
+        own[first_idx] = True
+        needs = np.zeros((n_c, 2), dtype=bool)        # processing order: first side, second side
+        needs[:, 0] = ~own
+        needs[ng:, 1] = True
+        vidx = (np.cumsum(needs.ravel()) - 1).reshape(n_c, 2)
+        n_virtual = int(needs.sum())
+        col_i = np.where(own, 3 * first_node, n_o + 3 * vidx[:, 0])
+        col_j = np.full(n_c, -1, dtype=np.int64)
+        col_j[ng:] = n_o + 3 * vidx[ng:, 1]
+        # J_v blocks, every block entry stored (contacts.py:311-320)
+        eye = np.eye(3).ravel()
+        rr = np.repeat(np.arange(3), 3)
+        cc = np.tile(np.arange(3), 3)
+        ident = np.nonzero(~own)[0]
+        r_id = (3 * vidx[ident, 0])[:, None] + rr[None, :]
+        c_id = (3 * first_node[ident])[:, None] + cc[None, :]
+        v_id = np.broadcast_to(eye, r_id.shape)
+        fv = vidx[ng:, 1]
+        r_f = (3 * fv)[:, None, None] + rr[None, None, :] + np.zeros((1, 3, 1), dtype=np.int64)
+        c_f = (3 * face["tri"])[:, :, None] + cc[None, None, :]
+        v_f = face["w"][:, :, None] * eye[None, None, :]
+        rows = np.concatenate([r_id.ravel(), r_f.ravel()])
+        cols = np.concatenate([c_id.ravel(), c_f.ravel()])
+        vals = np.concatenate([np.asarray(v_id).ravel(), v_f.ravel()])
+        jv = sp.csr_matrix((vals, (rows, cols)), shape=(3 * n_virtual, n_o))
+        normals = np.concatenate([np.tile([0.0, 0.0, 1.0], (ng, 1)), face["normal"]])
+        frames = contact_frames(normals) if n_c else np.zeros((0, 3, 3))
+        depth = np.concatenate([np.maximum(0.0, -self.x[ground, 2]), face["depth"]])
+        vel = self.v
+        v_rel = vel[first_node].copy()
+        if nf:
+            v_rel[ng:] -= np.einsum("fk,fkj->fj", face["w"], vel[face["tri"]])
+        vn = np.einsum("ij,ij->i", frames[:, 0, :], v_rel) if n_c else np.zeros(0)
+        phi = -(self.beta / self.dt) * depth                 # stabilization_term (contacts.py:230-239)
+        phi = np.where(np.abs(vn) > self.thr, phi + self.e_rest * np.minimum(0.0, vn), phi)
+        return PileContacts(col_i, col_j, frames, phi, np.full(n_c, self.mu), jv, ng, nf)
+
+    def contacts(self) -> PileContacts:
+        return self.nodalize(*self.detect())
+
+    # ---- the augmented system -------------------------------------------------
+    def system(self, pc: PileContacts | None = None, b_o=None) -> PackedSystem:
+        """The augmented system (A on the device via ``vfpi_augment``)."""
+        from .augment import augment_arrays
+
+        pc = pc if pc is not None else self.contacts()
+        b_o = self.rhs() if b_o is None else b_o
+        nv3 = pc.jv.shape[0]
+        ip, ix, dx = augment_arrays(self.n, self.a_indptr, self.a_indices, self.a_data, pc.jv, self.k_v)
+        b = np.concatenate([b_o, np.zeros(nv3)])
+        return make_packed(self.n + nv3, ip, ix, dx, b, pc.col_i, pc.col_j, pc.frames.reshape(-1), pc.mu, pc.mu,
+                           pc.phi)
+
+    def warm(self, prev_vhat, pc: PileContacts) -> np.ndarray:
+        """``harness._warm_velocity`` (``harness.py:502-512``)."""
+        n_o = self.n
+        v0 = np.zeros(n_o + pc.jv.shape[0])
+        if prev_vhat is None:
+            return v0
+        v0[:n_o] = prev_vhat[:n_o]
+        if pc.jv.shape[0]:
+            v0[n_o:] = pc.jv @ v0[:n_o]
+        return v0
+
+    def advance(self, v_hat):
+        """Midpoint integration (``dynamics.py:237-255``)."""
+        vh = np.asarray(v_hat)[: self.n].reshape(-1, 3)
+        self.x = self.x + self.dt * vh
+        self.v = 2.0 * vh - self.v
+
+
+def _tile_compressed(m, copies: int):
+    """Compressed arrays of ``copies`` diagonal copies of ``m`` (int32 indices)."""
+    nnz, dim = m.nnz, m.shape[0]
+    if copies * nnz >= 2 ** 31:
+        raise ValueError("pile: more than 2^31 stored entries")
+    ptr = (m.indptr[1:][None, :].astype(np.int64) + nnz * np.arange(copies, dtype=np.int64)[:, None]).ravel()
+    ptr = np.concatenate([[0], ptr]).astype(np.int32)
+    idx = (m.indices[None, :].astype(np.int32) + (dim * np.arange(copies, dtype=np.int32))[:, None]).ravel()
+    return ptr, idx, np.tile(m.data, copies)
+
+
+def _cell_key(c: np.ndarray) -> np.ndarray:
+    c = c + (1 << 20)
+    return (c[:, 0] << 42) | (c[:, 1] << 21) | c[:, 2]
+
+
+def _ragged_arange(cnt: np.ndarray) -> np.ndarray:
+    """concatenate(arange(k) for k in cnt)."""
+    tot = int(cnt.sum())
+    if tot == 0:
+        return np.zeros(0, dtype=np.int64)
+    starts = np.cumsum(cnt) - cnt
+    return np.arange(tot) - np.repeat(starts, cnt)
+
+
+class PileStepper:
+    """A ``CubePile`` stepped with its state in device memory (configs[4]).
+
+    Per step: contact detection + nodalization on the host from a copy of
+    (x, v) (the only host work), then on the device: b (``vfpi_fem_rhs_device``),
+    the augmented matrix (``vfpi_augment_device``), the warm start
+    (``vfpi_csr_matvec_device``, ``harness._warm_velocity``), the V-FPI solve
+    (``vfpi_solve_device``) and the midpoint integration (``vfpi_advance_device``).
+    A_o and K stay resident; torch tensors are plain device memory here."""
+
+    def __init__(self, pile: CubePile, device: int = 0):
+        import torch
+
+        from . import _lib
+
+        self.pile, self.device = pile, device
+        self.h = _lib.handle(device)
+        self.dev = torch.device("cuda", device)
+        up = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.dev)  # noqa: E731
+        self.a = (up(pile.a_indptr, np.int32), up(pile.a_indices, np.int32), up(pile.a_data, np.float64))
+        self.k = (up(pile.k_indptr, np.int64), up(pile.k_indices, np.int32), up(pile.k_data, np.float64))
+        self.m, self.g = up(pile.m, np.float64), up(pile.gravity, np.float64)
+        self.X = up(pile.X.ravel(), np.float64)
+        self.x = up(pile.x.ravel(), np.float64)
+        self.v = up(pile.v.ravel(), np.float64)
+        self.prev = None
+        self.steps = 0
+
+    def _p(self, t):
+        import ctypes as C
+
+        return C.c_void_p(t.data_ptr())
+
+    def step(self, cfg) -> dict:
+        import ctypes as C
+        import time
+
+        import torch
+
+        from . import _lib
+        from ._lib import VfpiAugmented, VfpiAugmentInput, VfpiResult, VfpiSystem
+        from .solver import _c_config, _raise_for
+
+        pile, h, dev, P = self.pile, self.h, self.dev, self._p
+        st = torch.cuda.current_stream(self.device)
+        sp_ = C.c_void_p(st.cuda_stream if st.cuda_stream else 1)
+        t0 = time.perf_counter()
+        pile.x = self.x.cpu().numpy().reshape(-1, 3)
+        pile.v = self.v.cpu().numpy().reshape(-1, 3)
+        pc = pile.contacts()
+        t_detect = time.perf_counter() - t0
+        n_o, nv3 = pile.n, pc.jv.shape[0]
+        n = n_o + nv3
+        up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev, non_blocking=False)  # noqa: E731
+        b = torch.zeros(n, dtype=torch.float64, device=dev)
+        _raise_for(h.L.vfpi_fem_rhs_device(h.h, n_o, P(self.k[0]), P(self.k[1]), P(self.k[2]), P(self.x), P(self.X),
+                                           P(self.v), P(self.m), P(self.g), pile.dt, P(b), sp_), h)
+        jv = pc.jv
+        jp, ji, jx = up(jv.indptr, np.int32), up(jv.indices, np.int32), up(jv.data, np.float64)
+        inp = VfpiAugmentInput(n_o, nv3, int(pile.a_data.shape[0]), C.cast(P(self.a[0]), _lib._i32p),
+                               C.cast(P(self.a[1]), _lib._i32p), C.cast(P(self.a[2]), _lib._f64p), int(jv.nnz),
+                               C.cast(P(jp), _lib._i32p), C.cast(P(ji), _lib._i32p), C.cast(P(jx), _lib._f64p),
+                               float(pile.k_v))
+        out = VfpiAugmented()
+        _raise_for(h.L.vfpi_augment_device(h.h, C.byref(inp), C.byref(out), sp_), h)
+        warm = torch.zeros(n, dtype=torch.float64, device=dev)
+        if self.prev is not None:
+            warm[:n_o] = self.prev
+            if nv3:
+                _raise_for(h.L.vfpi_csr_matvec_device(h.h, nv3, P(jp), P(ji), P(jx), P(warm), P(warm[n_o:]), sp_), h)
+        n_c = pc.n_c
+        ci, cj = up(pc.col_i, np.int32), up(pc.col_j, np.int32)
+        fr, mu, phi = up(pc.frames.reshape(-1), np.float64), up(pc.mu, np.float64), up(pc.phi, np.float64)
+        s = VfpiSystem()
+        s.n, s.n_c, s.nnz = n, n_c, int(out.nnz)
+        s.indptr, s.indices, s.data = out.indptr, out.indices, out.data
+        s.b = C.cast(P(b), _lib._f64p)
+        s.col_i, s.col_j = C.cast(P(ci), _lib._i32p), C.cast(P(cj), _lib._i32p)
+        s.frames, s.mu, s.mu2, s.phi = (C.cast(P(t), _lib._f64p) for t in (fr, mu, mu, phi))
+        vh = torch.empty(n, dtype=torch.float64, device=dev)
+        lam = torch.empty(max(3 * n_c, 1), dtype=torch.float64, device=dev)
+        trace = torch.empty(max(cfg.max_iters, 1), dtype=torch.float64, device=dev)
+        res = VfpiResult()
+        res.v, res.lam, res.residual_trace = (C.cast(P(t), _lib._f64p) for t in (vh, lam, trace))
+        res.scc, res.w = None, None
+        code = h.L.vfpi_solve_device(h.h, C.byref(s), _c_config(cfg), C.cast(P(warm), _lib._f64p), None, C.byref(res),
+                                     sp_)
+        _raise_for(code, h)
+        code = h.L.vfpi_wait(h.h, C.byref(res))
+        if code not in (_lib.OK, _lib.DIVERGED):
+            _raise_for(code, h)
+        _raise_for(h.L.vfpi_advance_device(h.h, n_o, pile.dt, P(vh), P(self.x), P(self.v), sp_), h)
+        self.prev = vh[:n_o].clone()
+        st.synchronize()
+        self.steps += 1
+        self.last = dict(v_hat=vh, lam=lam[: 3 * n_c], contacts=pc)
+        return dict(n_c=n_c, n_ground=pc.n_ground, n_face=pc.n_face, n_virtual=pc.n_virtual, n=n, nnz=int(out.nnz),
+                    iterations=int(res.iterations), converged=bool(res.converged), diverged=code == _lib.DIVERGED,
+                    setup_ms=float(res.setup_ms), loop_ms=float(res.loop_ms), detect_s=t_detect,
+                    wall_s=time.perf_counter() - t0)
