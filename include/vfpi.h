@@ -284,6 +284,48 @@ int vfpi_csr_matvec_device(vfpi_handle* h, int64_t rows, const int32_t* indptr, 
 int vfpi_advance_device(vfpi_handle* h, int64_t n, double dt, const double* v_hat, double* x, double* v,
                         void* stream);
 
+/* ---- cube-pile contacts (configs[4]) -------------- */
+/* Plane z = 0 and node-to-face contacts of deformable bodies, detected with a
+ * spatial hash and nodalized on the device -- the reference's
+ * detect_contacts + nodalize (contacts.py:159-321) extended with a face side
+ * (virtual node tied to a triangle by J_v = [w0 I, w1 I, w2 I]); restates
+ * paper_2201_09212_b200.pile.CubePile.detect/nodalize bit for bit. */
+typedef struct vfpi_pile_geometry {
+  int64_t nodes;               /* all nodes (3 DOF each) */
+  int64_t n_surf;              /* surface nodes */
+  int64_t n_tris;              /* surface triangles */
+  const int32_t* surf;         /* [n_surf] ascending node ids */
+  const int32_t* tris;         /* [n_tris*3] outward-oriented node ids */
+  const int32_t* node_body;    /* [nodes] body of every node */
+  const int32_t* tri_body;     /* [n_tris] body of every triangle */
+  double reach;                /* bounding-box growth (max(h/2, margin)) */
+  double cell;                 /* hash cell edge (2h) */
+  double neg_half_h;           /* deepest signed distance accepted (-h/2) */
+  double margin;               /* contact margin (contacts.py:28) */
+  double mu;                   /* friction coefficient of every contact */
+  double neg_beta_dt;          /* -(beta_err / dt) (stabilization_term) */
+  double e_rest;
+  double rest_threshold;
+} vfpi_pile_geometry;
+
+typedef struct vfpi_pile_contacts {  /* device buffers owned by the handle */
+  int64_t n_c, n_ground, n_face, n_virtual, jv_nnz;
+  int32_t* col_i;
+  int32_t* col_j;
+  double* frames;      /* [n_c*9] */
+  double* mu;          /* [n_c] */
+  double* phi;         /* [n_c] */
+  int32_t* jv_indptr;  /* [3 n_virtual + 1] canonical CSR of J_v */
+  int32_t* jv_indices;
+  double* jv_data;
+} vfpi_pile_contacts;
+
+/* x, v: device state [3*nodes]; outputs valid until the next call on h. */
+int vfpi_pile_contacts_device(vfpi_handle* h, const vfpi_pile_geometry* g, const double* x, const double* v,
+                              vfpi_pile_contacts* out, void* stream);
+/* synchronous device-to-device copy (reading handle-owned outputs into caller buffers) */
+int vfpi_memcpy_d2d(void* dst, const void* src, int64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,6 +59,23 @@ class VfpiAugmented(C.Structure):
     _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("indptr", _i32p), ("indices", _i32p), ("data", _f64p)]
 
 
+class VfpiPileGeometry(C.Structure):
+    _fields_ = [
+        ("nodes", C.c_int64), ("n_surf", C.c_int64), ("n_tris", C.c_int64),
+        ("surf", C.c_void_p), ("tris", C.c_void_p), ("node_body", C.c_void_p), ("tri_body", C.c_void_p),
+        ("reach", C.c_double), ("cell", C.c_double), ("neg_half_h", C.c_double), ("margin", C.c_double),
+        ("mu", C.c_double), ("neg_beta_dt", C.c_double), ("e_rest", C.c_double), ("rest_threshold", C.c_double),
+    ]
+
+
+class VfpiPileContacts(C.Structure):
+    _fields_ = [
+        ("n_c", C.c_int64), ("n_ground", C.c_int64), ("n_face", C.c_int64), ("n_virtual", C.c_int64),
+        ("jv_nnz", C.c_int64), ("col_i", _i32p), ("col_j", _i32p), ("frames", _f64p), ("mu", _f64p),
+        ("phi", _f64p), ("jv_indptr", _i32p), ("jv_indices", _i32p), ("jv_data", _f64p),
+    ]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -99,6 +116,9 @@ def lib() -> C.CDLL:
                                                   C.c_void_p, C.c_void_p]),
                 "vfpi_csr_matvec_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                      C.c_void_p, C.c_void_p]),
+                "vfpi_pile_contacts_device": (C.c_int, [H, C.POINTER(VfpiPileGeometry), C.c_void_p, C.c_void_p,
+                                                        C.POINTER(VfpiPileContacts), C.c_void_p]),
+                "vfpi_memcpy_d2d": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
                 "vfpi_advance_device": (C.c_int, [H, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                                   C.c_void_p]),
                 "vfpi_host_alloc": (C.c_void_p, [C.c_int64]),

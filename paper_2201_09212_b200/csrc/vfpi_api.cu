@@ -57,6 +57,7 @@ struct vfpi_handle {
   int bar_mode = 0;     // resident grid barrier (IterParams::bar_mode)
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
+  vfpi::PileWork pile;
   int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
@@ -232,6 +233,7 @@ int vfpi_create(int device, vfpi_handle** out) {
   cudaMallocHost(&h->ws.h_status, sizeof(vfpi::SolveStatus));
   cudaMallocHost(&h->h_flags, 16);
   cudaMallocHost(&h->aug.h_small, 2 * sizeof(int64_t));
+  cudaMallocHost(&h->pile.h_small, 4 * sizeof(int64_t));
   *out = h;
   return VFPI_OK;
 }
@@ -266,6 +268,12 @@ void vfpi_destroy(vfpi_handle* h) {
                             &aw.t_val, &aw.cs, &aw.ccnt, &aw.cptr, &aw.out_p, &aw.out_i, &aw.out_x})
     if (b->p) cudaFree(b->p);
   if (aw.h_small) cudaFreeHost(aw.h_small);
+  vfpi::PileWork& pw = h->pile;
+  for (Workspace::Buf* b : {&pw.tcnt, &pw.toff, &pw.flag, &pw.key, &pw.key2, &pw.own, &pw.own2, &pw.btri, &pw.best,
+                            &pw.gflag, &pw.gpos, &pw.fflag, &pw.fpos, &pw.nvirt, &pw.vpos, &pw.njv, &pw.jpos, &pw.ci,
+                            &pw.cj, &pw.fr, &pw.mu, &pw.phi, &pw.jrp, &pw.jci, &pw.jcx, &pw.tmp})
+    if (b->p) cudaFree(b->p);
+  if (pw.h_small) cudaFreeHost(pw.h_small);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
   for (SetupGraph* g : {&h->graph_layout, &h->graph_pack})
@@ -1356,4 +1364,53 @@ int vfpi_advance_device(vfpi_handle* h, int64_t n, double dt, const double* v_ha
   h->launches += n > 0;
   CK(cudaGetLastError());
   return VFPI_OK;
+}
+
+int vfpi_pile_contacts_device(vfpi_handle* h, const vfpi_pile_geometry* g, const double* x, const double* v,
+                              vfpi_pile_contacts* out, void* stream) {
+  if (!h || !g || !out || g->nodes < 0 || g->n_surf < 0 || g->n_tris < 0 || 3 * g->nodes > INT32_MAX ||
+      !(g->cell > 0.0))
+    return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::PileGeometry pg;
+  pg.nodes = g->nodes;
+  pg.n_surf = g->n_surf;
+  pg.n_tris = g->n_tris;
+  pg.n_o = (int)(3 * g->nodes);
+  pg.surf = g->surf;
+  pg.tris = g->tris;
+  pg.node_body = g->node_body;
+  pg.tri_body = g->tri_body;
+  pg.reach = g->reach;
+  pg.cell = g->cell;
+  pg.neg_half_h = g->neg_half_h;
+  pg.margin = g->margin;
+  pg.mu = g->mu;
+  pg.neg_beta_dt = g->neg_beta_dt;
+  pg.e_rest = g->e_rest;
+  pg.rest_threshold = g->rest_threshold;
+  vfpi::PileContactsOut o;
+  const int rc = vfpi::pile_contacts_device(h->pile, pg, x, v, st, o, h->err, h->launches);
+  if (rc != VFPI_OK) return rc;
+  out->n_c = o.n_ground + o.n_face;
+  out->n_ground = o.n_ground;
+  out->n_face = o.n_face;
+  out->n_virtual = o.n_virtual;
+  out->jv_nnz = o.jv_nnz;
+  out->col_i = o.col_i;
+  out->col_j = o.col_j;
+  out->frames = o.frames;
+  out->mu = o.mu;
+  out->phi = o.phi;
+  out->jv_indptr = o.jv_indptr;
+  out->jv_indices = o.jv_indices;
+  out->jv_data = o.jv_data;
+  return VFPI_OK;
+}
+
+int vfpi_memcpy_d2d(void* dst, const void* src, int64_t bytes) {
+  if (bytes < 0) return VFPI_BAD_ARGUMENT;
+  if (bytes == 0) return VFPI_OK;
+  return cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice) == cudaSuccess ? VFPI_OK : VFPI_CUDA_ERROR;
 }

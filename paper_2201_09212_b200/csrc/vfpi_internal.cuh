@@ -258,6 +258,36 @@ struct AugmentWork {
 int augment_device(AugmentWork& w, const AugmentIn& in, cudaStream_t st, AugmentOut& out, std::string& err,
                    int64_t& launches);
 
+// ---- cube-pile contacts (vfpi_pile.cu) ---------------------------------------
+struct PileGeometry {
+  int64_t nodes = 0, n_surf = 0, n_tris = 0;
+  int n_o = 0;                   // 3 * nodes
+  const int* surf = nullptr;     // [n_surf] ascending
+  const int* tris = nullptr;     // [n_tris*3] outward
+  const int* node_body = nullptr;
+  const int* tri_body = nullptr;
+  double reach = 0, cell = 0, neg_half_h = 0, margin = 0;
+  double mu = 0, neg_beta_dt = 0, e_rest = 0, rest_threshold = 0;
+};
+struct PileContactsOut {
+  int n_ground = 0, n_face = 0, n_virtual = 0, jv_nnz = 0;
+  int* col_i = nullptr;
+  int* col_j = nullptr;
+  double* frames = nullptr;
+  double* mu = nullptr;
+  double* phi = nullptr;
+  int* jv_indptr = nullptr;
+  int* jv_indices = nullptr;
+  double* jv_data = nullptr;
+};
+struct PileWork {
+  Workspace::Buf tcnt, toff, flag, key, key2, own, own2, btri, best, gflag, gpos, fflag, fpos, nvirt, vpos, njv,
+      jpos, ci, cj, fr, mu, phi, jrp, jci, jcx, tmp;
+  int64_t* h_small = nullptr;  // pinned [4]
+};
+int pile_contacts_device(PileWork& w, const PileGeometry& g, const double* x, const double* v, cudaStream_t st,
+                         PileContactsOut& out, std::string& err, int64_t& launches);
+
 // ---- FEM scene-batch step pipeline (vfpi_fem.cu) ----------------------------
 void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,
                     const double* v, const double* m, const double* g, double twodt, double* b, cudaStream_t st);

@@ -59,17 +59,29 @@ def surface_triangles(nx: int, X: np.ndarray) -> np.ndarray:
     return f
 
 
+# Row-wise 3-vector products with their evaluation order spelled out (the
+# device kernels in csrc/vfpi_pile.cu use exactly these expressions).
+def _dot3(a, b):
+    return a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1] + a[:, 2] * b[:, 2]
+
+
+def _cross3(a, b):
+    return np.stack([a[:, 1] * b[:, 2] - a[:, 2] * b[:, 1],
+                     a[:, 2] * b[:, 0] - a[:, 0] * b[:, 2],
+                     a[:, 0] * b[:, 1] - a[:, 1] * b[:, 0]], axis=1)
+
+
 def contact_frames(normals: np.ndarray) -> np.ndarray:
     """``contact_frame`` (``contacts.py:131-149``) for many normals at once."""
-    n = np.asarray(normals, dtype=float)
-    norm = np.sqrt(np.einsum("ij,ij->i", n, n))
+    n = np.asarray(normals, dtype=float).reshape(-1, 3)
+    norm = np.sqrt(_dot3(n, n))
     fix = np.abs(norm - 1.0) > 1e-9
     n = np.where(fix[:, None], n / norm[:, None], n)
     e = np.zeros_like(n)
     e[np.arange(n.shape[0]), np.argmin(np.abs(n), axis=1)] = 1.0
-    t1 = np.cross(np.cross(n, e), n)
-    t1 /= np.sqrt(np.einsum("ij,ij->i", t1, t1))[:, None]
-    return np.stack([n, t1, np.cross(n, t1)], axis=1)
+    t1 = _cross3(_cross3(n, e), n)
+    t1 = t1 / np.sqrt(_dot3(t1, t1))[:, None]
+    return np.stack([n, t1, _cross3(n, t1)], axis=1)
 
 
 @dataclass
@@ -133,6 +145,9 @@ class CubePile:
         self.a_indptr, self.a_indices, self.a_data = _tile_compressed(A, nc)
         self.k_indptr, self.k_indices, self.k_data = _tile_compressed(K, nc)
 
+    def node_body_i32(self):
+        return self.node_cube.astype(np.int32)
+
     # ---- host right-hand side (the restatement the device path matches) ----
     def rhs(self) -> np.ndarray:
         """b = (2/dt) M v - K (x - X) + M g (scenes.FemCube.system), per row in
@@ -177,18 +192,15 @@ class CubePile:
         pn, pt = pn[keep], pt[keep]
         p = x[pn]
         a, b, c = x[tri[pt, 0]], x[tri[pt, 1]], x[tri[pt, 2]]
-        nrm = np.cross(b - a, c - a)
-        nrm /= np.sqrt(np.einsum("ij,ij->i", nrm, nrm))[:, None]
-        d = np.einsum("ij,ij->i", p - a, nrm)
+        nrm = _cross3(b - a, c - a)
+        nrm = nrm / np.sqrt(_dot3(nrm, nrm))[:, None]
+        d = _dot3(p - a, nrm)
         keep = (d > -0.5 * self.h) & (d < self.margin)
         pn, pt, p, a, b, c, nrm, d = pn[keep], pt[keep], p[keep], a[keep], b[keep], c[keep], nrm[keep], d[keep]
         q = p - d[:, None] * nrm
         v0, v1, v2 = b - a, c - a, q - a
-        d00 = np.einsum("ij,ij->i", v0, v0)
-        d01 = np.einsum("ij,ij->i", v0, v1)
-        d11 = np.einsum("ij,ij->i", v1, v1)
-        d20 = np.einsum("ij,ij->i", v2, v0)
-        d21 = np.einsum("ij,ij->i", v2, v1)
+        d00, d01, d11 = _dot3(v0, v0), _dot3(v0, v1), _dot3(v1, v1)
+        d20, d21 = _dot3(v2, v0), _dot3(v2, v1)
         den = d00 * d11 - d01 * d01
         w1 = (d11 * d20 - d01 * d21) / den
         w2 = (d00 * d21 - d01 * d20) / den
@@ -244,8 +256,9 @@ class CubePile:
         vel = self.v
         v_rel = vel[first_node].copy()
         if nf:
-            v_rel[ng:] -= np.einsum("fk,fkj->fj", face["w"], vel[face["tri"]])
-        vn = np.einsum("ij,ij->i", frames[:, 0, :], v_rel) if n_c else np.zeros(0)
+            w, vt = face["w"], vel[face["tri"]]
+            v_rel[ng:] -= w[:, 0:1] * vt[:, 0] + w[:, 1:2] * vt[:, 1] + w[:, 2:3] * vt[:, 2]
+        vn = _dot3(frames[:, 0, :], v_rel) if n_c else np.zeros(0)
         phi = -(self.beta / self.dt) * depth                 # stabilization_term (contacts.py:230-239)
         phi = np.where(np.abs(vn) > self.thr, phi + self.e_rest * np.minimum(0.0, vn), phi)
         return PileContacts(col_i, col_j, frames, phi, np.full(n_c, self.mu), jv, ng, nf)
@@ -284,6 +297,16 @@ class CubePile:
         self.v = 2.0 * vh - self.v
 
 
+def _lib_cuda_copy(t, src_ptr, n, dt):
+    """Copy n elements of a device pointer into tensor t (device to device)."""
+    import ctypes as C
+
+    from . import _lib
+
+    nbytes = n * t.element_size()
+    _lib.lib().vfpi_memcpy_d2d(C.c_void_p(t.data_ptr()), C.cast(src_ptr, C.c_void_p), C.c_int64(nbytes))
+
+
 def _tile_compressed(m, copies: int):
     """Compressed arrays of ``copies`` diagonal copies of ``m`` (int32 indices)."""
     nnz, dim = m.nnz, m.shape[0]
@@ -312,19 +335,20 @@ def _ragged_arange(cnt: np.ndarray) -> np.ndarray:
 class PileStepper:
     """A ``CubePile`` stepped with its state in device memory (configs[4]).
 
-    Per step: contact detection + nodalization on the host from a copy of
-    (x, v) (the only host work), then on the device: b (``vfpi_fem_rhs_device``),
+    Per step, on the device: contact detection + nodalization
+    (``vfpi_pile_contacts_device``; ``detect="host"`` runs ``CubePile.detect`` /
+    ``nodalize`` on a copy of (x, v) instead), b (``vfpi_fem_rhs_device``),
     the augmented matrix (``vfpi_augment_device``), the warm start
     (``vfpi_csr_matvec_device``, ``harness._warm_velocity``), the V-FPI solve
     (``vfpi_solve_device``) and the midpoint integration (``vfpi_advance_device``).
     A_o and K stay resident; torch tensors are plain device memory here."""
 
-    def __init__(self, pile: CubePile, device: int = 0):
+    def __init__(self, pile: CubePile, device: int = 0, detect: str = "device"):
         import torch
 
         from . import _lib
 
-        self.pile, self.device = pile, device
+        self.pile, self.device, self.detect = pile, device, detect
         self.h = _lib.handle(device)
         self.dev = torch.device("cuda", device)
         up = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.dev)  # noqa: E731
@@ -336,6 +360,49 @@ class PileStepper:
         self.v = up(pile.v.ravel(), np.float64)
         self.prev = None
         self.steps = 0
+        self.geo_t = (up(pile.surf, np.int32), up(pile.tris.ravel(), np.int32), up(pile.node_body_i32(), np.int32),
+                      up(pile.tri_cube, np.int32))
+        g = _lib.VfpiPileGeometry()
+        g.nodes, g.n_surf, g.n_tris = pile.n // 3, pile.surf.shape[0], pile.tris.shape[0]
+        g.surf, g.tris, g.node_body, g.tri_body = (t.data_ptr() for t in self.geo_t)
+        g.reach, g.cell, g.neg_half_h = max(0.5 * pile.h, pile.margin), 2.0 * pile.h, -0.5 * pile.h
+        g.margin, g.mu = pile.margin, pile.mu
+        g.neg_beta_dt, g.e_rest, g.rest_threshold = -(pile.beta / pile.dt), pile.e_rest, pile.thr
+        self.geo = g
+
+    def device_contacts(self) -> PileContacts:
+        """Device detection + nodalization of the current device state, copied
+        to the host (for checks; the step keeps them on the device)."""
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+        from .solver import _raise_for
+
+        h = self.h
+        oc = _lib.VfpiPileContacts()
+        st = torch.cuda.current_stream(self.device)
+        sp_ = C.c_void_p(st.cuda_stream if st.cuda_stream else 1)
+        _raise_for(h.L.vfpi_pile_contacts_device(h.h, C.byref(self.geo), self._p(self.x), self._p(self.v),
+                                                 C.byref(oc), sp_), h)
+        st.synchronize()
+        n_c, nv3, nj = int(oc.n_c), 3 * int(oc.n_virtual), int(oc.jv_nnz)
+
+        def d2h(p, n, dt):
+            t = torch.empty(n, dtype=dt, device=self.dev)
+            if n:
+                torch.cuda.synchronize(self.device)
+                _lib_cuda_copy(t, p, n, dt)
+            return t.cpu().numpy()
+
+        i32, f64 = torch.int32, torch.float64
+        ci, cj = d2h(oc.col_i, n_c, i32), d2h(oc.col_j, n_c, i32)
+        fr, mu, phi = d2h(oc.frames, 9 * n_c, f64), d2h(oc.mu, n_c, f64), d2h(oc.phi, n_c, f64)
+        jp, ji, jx = d2h(oc.jv_indptr, nv3 + 1, i32), d2h(oc.jv_indices, nj, i32), d2h(oc.jv_data, nj, f64)
+        jv = sp.csr_matrix((jx, ji, jp), shape=(nv3, self.pile.n))
+        return PileContacts(ci.astype(np.int64), cj.astype(np.int64), fr.reshape(-1, 3, 3), phi, mu, jv,
+                            int(oc.n_ground), int(oc.n_face))
 
     def _p(self, t):
         import ctypes as C
@@ -356,21 +423,36 @@ class PileStepper:
         st = torch.cuda.current_stream(self.device)
         sp_ = C.c_void_p(st.cuda_stream if st.cuda_stream else 1)
         t0 = time.perf_counter()
-        pile.x = self.x.cpu().numpy().reshape(-1, 3)
-        pile.v = self.v.cpu().numpy().reshape(-1, 3)
-        pc = pile.contacts()
-        t_detect = time.perf_counter() - t0
-        n_o, nv3 = pile.n, pc.jv.shape[0]
-        n = n_o + nv3
+        n_o = pile.n
         up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev, non_blocking=False)  # noqa: E731
+        i32, f64 = _lib._i32p, _lib._f64p
+        if self.detect == "device":
+            oc = _lib.VfpiPileContacts()
+            _raise_for(h.L.vfpi_pile_contacts_device(h.h, C.byref(self.geo), P(self.x), P(self.v), C.byref(oc), sp_), h)
+            pc = None
+            n_c, nv3, jnnz = int(oc.n_c), 3 * int(oc.n_virtual), int(oc.jv_nnz)
+            counts = dict(n_ground=int(oc.n_ground), n_face=int(oc.n_face), n_virtual=int(oc.n_virtual))
+            jp_, ji_, jx_ = oc.jv_indptr, oc.jv_indices, oc.jv_data
+            cptr = (oc.col_i, oc.col_j, oc.frames, oc.mu, oc.phi)
+        else:
+            pile.x = self.x.cpu().numpy().reshape(-1, 3)
+            pile.v = self.v.cpu().numpy().reshape(-1, 3)
+            pc = pile.contacts()
+            n_c, nv3, jnnz = pc.n_c, pc.jv.shape[0], int(pc.jv.nnz)
+            counts = dict(n_ground=pc.n_ground, n_face=pc.n_face, n_virtual=pc.n_virtual)
+            keep = (up(pc.jv.indptr, np.int32), up(pc.jv.indices, np.int32), up(pc.jv.data, np.float64),
+                    up(pc.col_i, np.int32), up(pc.col_j, np.int32), up(pc.frames.reshape(-1), np.float64),
+                    up(pc.mu, np.float64), up(pc.phi, np.float64))
+            self._keep = keep
+            jp_, ji_, jx_ = (C.cast(P(t), typ) for t, typ in zip(keep[:3], (i32, i32, f64)))
+            cptr = tuple(C.cast(P(t), typ) for t, typ in zip(keep[3:], (i32, i32, f64, f64, f64)))
+        t_detect = time.perf_counter() - t0
+        n = n_o + nv3
         b = torch.zeros(n, dtype=torch.float64, device=dev)
         _raise_for(h.L.vfpi_fem_rhs_device(h.h, n_o, P(self.k[0]), P(self.k[1]), P(self.k[2]), P(self.x), P(self.X),
                                            P(self.v), P(self.m), P(self.g), pile.dt, P(b), sp_), h)
-        jv = pc.jv
-        jp, ji, jx = up(jv.indptr, np.int32), up(jv.indices, np.int32), up(jv.data, np.float64)
-        inp = VfpiAugmentInput(n_o, nv3, int(pile.a_data.shape[0]), C.cast(P(self.a[0]), _lib._i32p),
-                               C.cast(P(self.a[1]), _lib._i32p), C.cast(P(self.a[2]), _lib._f64p), int(jv.nnz),
-                               C.cast(P(jp), _lib._i32p), C.cast(P(ji), _lib._i32p), C.cast(P(jx), _lib._f64p),
+        inp = VfpiAugmentInput(n_o, nv3, int(pile.a_data.shape[0]), C.cast(P(self.a[0]), i32),
+                               C.cast(P(self.a[1]), i32), C.cast(P(self.a[2]), f64), jnnz, jp_, ji_, jx_,
                                float(pile.k_v))
         out = VfpiAugmented()
         _raise_for(h.L.vfpi_augment_device(h.h, C.byref(inp), C.byref(out), sp_), h)
@@ -378,16 +460,15 @@ class PileStepper:
         if self.prev is not None:
             warm[:n_o] = self.prev
             if nv3:
-                _raise_for(h.L.vfpi_csr_matvec_device(h.h, nv3, P(jp), P(ji), P(jx), P(warm), P(warm[n_o:]), sp_), h)
-        n_c = pc.n_c
-        ci, cj = up(pc.col_i, np.int32), up(pc.col_j, np.int32)
-        fr, mu, phi = up(pc.frames.reshape(-1), np.float64), up(pc.mu, np.float64), up(pc.phi, np.float64)
+                vp = C.c_void_p
+                _raise_for(h.L.vfpi_csr_matvec_device(h.h, nv3, C.cast(jp_, vp), C.cast(ji_, vp), C.cast(jx_, vp),
+                                                      P(warm), P(warm[n_o:]), sp_), h)
         s = VfpiSystem()
         s.n, s.n_c, s.nnz = n, n_c, int(out.nnz)
         s.indptr, s.indices, s.data = out.indptr, out.indices, out.data
-        s.b = C.cast(P(b), _lib._f64p)
-        s.col_i, s.col_j = C.cast(P(ci), _lib._i32p), C.cast(P(cj), _lib._i32p)
-        s.frames, s.mu, s.mu2, s.phi = (C.cast(P(t), _lib._f64p) for t in (fr, mu, mu, phi))
+        s.b = C.cast(P(b), f64)
+        s.col_i, s.col_j, s.frames, s.mu, s.phi = cptr
+        s.mu2 = cptr[3]
         vh = torch.empty(n, dtype=torch.float64, device=dev)
         lam = torch.empty(max(3 * n_c, 1), dtype=torch.float64, device=dev)
         trace = torch.empty(max(cfg.max_iters, 1), dtype=torch.float64, device=dev)
@@ -405,7 +486,7 @@ class PileStepper:
         st.synchronize()
         self.steps += 1
         self.last = dict(v_hat=vh, lam=lam[: 3 * n_c], contacts=pc)
-        return dict(n_c=n_c, n_ground=pc.n_ground, n_face=pc.n_face, n_virtual=pc.n_virtual, n=n, nnz=int(out.nnz),
+        return dict(n_c=n_c, **counts, n=n, nnz=int(out.nnz),
                     iterations=int(res.iterations), converged=bool(res.converged), diverged=code == _lib.DIVERGED,
                     setup_ms=float(res.setup_ms), loop_ms=float(res.loop_ms), detect_s=t_detect,
                     wall_s=time.perf_counter() - t0)

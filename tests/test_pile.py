@@ -107,7 +107,8 @@ def test_gpu_pile_lockstep_with_oracle():
 
 
 @pytest.mark.gpu
-def test_gpu_pile_stepper_matches_host_pipeline():
+@pytest.mark.parametrize("detect", ["device", "host"])
+def test_gpu_pile_stepper_matches_host_pipeline(detect):
     """The device step pipeline (b, augmentation, warm start, solve,
     integration on the GPU) against the host pipeline driven by the oracle:
     same contacts and iterations every step, states bit-equal."""
@@ -115,7 +116,7 @@ def test_gpu_pile_stepper_matches_host_pipeline():
     from paper_2201_09212_b200.solver import SolverConfig
 
     host = small_pile()
-    dev = PileStepper(small_pile())
+    dev = PileStepper(small_pile(), detect=detect)
     prev = None
     for step in range(6):
         pc, _, _, _, vo, lo, ro = _oracle_step(host, prev, 200)
@@ -127,3 +128,25 @@ def test_gpu_pile_stepper_matches_host_pipeline():
         assert np.array_equal(dev.x.cpu().numpy(), host.x.ravel()), step
         assert np.array_equal(dev.v.cpu().numpy(), host.v.ravel()), step
         assert np.array_equal(dev.last["lam"].cpu().numpy().reshape(-1, 3), lo), step
+
+
+@pytest.mark.gpu
+def test_gpu_pile_contacts_equal_host_detection():
+    """Device spatial hash + narrow phase + nodalization vs CubePile.detect /
+    nodalize on the same (deformed, moving) state: every array bit-equal."""
+    from paper_2201_09212_b200.pile import PileStepper
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    dev = PileStepper(small_pile(nx_cubes=2, ny_cubes=2, layers=2, seed=9))
+    for _ in range(3):
+        dev.step(SolverConfig(residual_tol=1e-8, max_iters=100))
+    pile = dev.pile
+    pile.x = dev.x.cpu().numpy().reshape(-1, 3)
+    pile.v = dev.v.cpu().numpy().reshape(-1, 3)
+    hc, dc = pile.contacts(), dev.device_contacts()
+    assert (hc.n_ground, hc.n_face, hc.n_virtual) == (dc.n_ground, dc.n_face, dc.n_virtual)
+    assert hc.n_face > 0 and hc.n_virtual > hc.n_face
+    for name in ("col_i", "col_j", "frames", "phi", "mu"):
+        assert np.array_equal(getattr(hc, name), getattr(dc, name)), name
+    for name in ("indptr", "indices", "data"):
+        assert np.array_equal(getattr(hc.jv, name), getattr(dc.jv, name)), name
