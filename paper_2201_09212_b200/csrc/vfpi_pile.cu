@@ -54,7 +54,7 @@ __global__ void k_tri_count(int64_t T, const int* __restrict__ tris, const doubl
     const double p2 = x[3 * (int64_t)tris[3 * t + 2] + a];
     const double mn = fmin(fmin(p0, p1), p2), mx = fmax(fmax(p0, p1), p2);
     const long long lo = cell_of(dsub(mn, reach), cell), hi = cell_of(dadd(mx, reach), cell);
-    if (hi - lo > 2) atomicExch(bad, 1);
+    if (hi - lo > 7) atomicExch(bad, 1);
     span *= (hi - lo + 1);
   }
   cnt[t] = span;
@@ -71,7 +71,7 @@ __global__ void k_tri_fill(int64_t T, const int* __restrict__ tris, const double
     const double p2 = x[3 * (int64_t)tris[3 * t + 2] + a];
     const double mn = fmin(fmin(p0, p1), p2), mx = fmax(fmax(p0, p1), p2);
     lo[a] = cell_of(dsub(mn, reach), cell);
-    hi[a] = min(cell_of(dadd(mx, reach), cell), lo[a] + 2);
+    hi[a] = min(cell_of(dadd(mx, reach), cell), lo[a] + 7);
   }
   int64_t o = off[t];
   for (long long cx = lo[0]; cx <= hi[0]; ++cx)
@@ -105,7 +105,7 @@ __global__ void k_node_query(int64_t S, const int* __restrict__ surf, const doub
   double bd = 0.0, bw[3] = {0, 0, 0}, bn[3] = {0, 0, 0};
   for (int64_t e = lo; e < E && key[e] == k; ++e) {
     const int t = owner[e];
-    if (tri_body[t] == body) continue;
+    if (tri_body[t] >= body) continue;  // one pass: later body's nodes on earlier body's faces
     const int ia = tris[3 * (int64_t)t], ib = tris[3 * (int64_t)t + 1], ic = tris[3 * (int64_t)t + 2];
     double a[3], b[3], c[3];
     for (int q = 0; q < 3; ++q) {
@@ -331,7 +331,7 @@ int pile_contacts_device(PileWork& w, const PileGeometry& g, const double* x, co
   PK(cudaStreamSynchronize(st));
   const int64_t E = w.h_small[0];
   if (reinterpret_cast<int*>(w.h_small + 1)[0]) {
-    err = "pile contacts: a surface triangle spans more than 3 hash cells (mesh too deformed)";
+    err = "pile contacts: a surface triangle spans more than 8 hash cells (mesh too deformed)";
     return VFPI_BAD_ARGUMENT;
   }
   PK(ensure(w.key, sizeof(unsigned long long) * (size_t)std::max<int64_t>(E, 1)));

@@ -14,8 +14,10 @@ way the reference would write them:
   cells (edge ``2h``) its bounding box, grown by the search distance, overlaps;
   every surface node looks up its own cell (sort + binary search, no Python
   loop over contacts);
-* **narrow phase** -- node ``p`` of cube A against triangle ``(a, b, c)`` of
-  cube B != A: signed distance ``d = (p - a).n`` along B's outward normal,
+* **narrow phase** -- one pass (the classic slave-node / master-face split,
+  so two coincident surfaces are never constrained from both sides): node
+  ``p`` of cube A against triangle ``(a, b, c)`` of cube B < A (cubes are
+  numbered layer by layer, so upper nodes meet lower faces): signed distance ``d = (p - a).n`` along B's outward normal,
   ``-h/2 < d < margin`` and the projection inside the triangle (barycentric
   weights ``w >= 0``); one contact per node, the candidate with the largest
   ``d``; ground contacts (plane ``z = 0``) as in ``scenes.FemCube``;
@@ -112,7 +114,10 @@ class CubePile:
 
     def __init__(self, nx_cubes=8, ny_cubes=8, layers=4, nodes=16, side=0.1, gap=0.005, jitter=0.002, seed=0,
                  E=1e5, nu=0.3, rho=1000.0, dt=5e-4, mu=0.6, gravity=-9.81, margin=1e-4, beta_err=0.2,
-                 e_rest=0.0, rest_threshold=0.01, k_v=1e5):
+                 e_rest=0.0, rest_threshold=0.01, k_v=1e5, gap_z=None, jitter_z=None):
+        """``gap`` / ``jitter``: lateral spacing and U[-jitter, jitter] offsets in
+        x and y; ``gap_z`` / ``jitter_z`` (default: the lateral values) the same
+        between layers and above the plane."""
         self.dt, self.mu, self.margin, self.k_v = dt, mu, margin, k_v
         self.beta, self.e_rest, self.thr = beta_err, e_rest, rest_threshold
         self.h = side / (nodes - 1)
@@ -122,11 +127,14 @@ class CubePile:
         nc = nx_cubes * ny_cubes * layers
         self.n_cubes, self.nn_cube = nc, nodes ** 3
         rng = np.random.default_rng(seed)
+        gz = gap if gap_z is None else gap_z
+        jz = jitter if jitter_z is None else jitter_z
         pitch = side + gap
         ix, iy, iz = np.meshgrid(np.arange(nx_cubes), np.arange(ny_cubes), np.arange(layers), indexing="ij")
-        base = np.stack([ix.ravel() * pitch, iy.ravel() * pitch, gap + iz.ravel() * pitch], axis=1)
+        base = np.stack([ix.ravel() * pitch, iy.ravel() * pitch, gz + iz.ravel() * (side + gz)], axis=1)
         order = np.lexsort((base[:, 0], base[:, 1], base[:, 2]))  # layer-major cube order
-        base = base[order] + rng.uniform(-jitter, jitter, (nc, 3))
+        jit = rng.uniform(-1.0, 1.0, (nc, 3)) * np.array([jitter, jitter, jz])
+        base = base[order] + jit
         Xt = cube.X - np.array([0.0, 0.0, 0.0])
         self.X = (Xt[None, :, :] + base[:, None, :]).reshape(-1, 3)
         self.x = self.X.copy()
@@ -169,12 +177,13 @@ class CubePile:
         lo = np.floor((P.min(axis=1) - reach) / cell).astype(np.int64)
         hi = np.floor((P.max(axis=1) + reach) / cell).astype(np.int64)
         span = hi - lo
-        if span.max(initial=0) > 2:
-            raise ValueError("pile: a surface triangle spans more than 3 hash cells (mesh too deformed)")
+        smax = int(span.max(initial=0))
+        if smax > 7:
+            raise ValueError("pile: a surface triangle spans more than 8 hash cells (mesh too deformed)")
         keys, owner = [], []
-        for dx in range(3):
-            for dy in range(3):
-                for dz in range(3):
+        for dx in range(smax + 1):
+            for dy in range(smax + 1):
+                for dz in range(smax + 1):
                     ok = (dx <= span[:, 0]) & (dy <= span[:, 1]) & (dz <= span[:, 2])
                     c = lo[ok] + np.array([dx, dy, dz])
                     keys.append(_cell_key(c))
@@ -188,7 +197,7 @@ class CubePile:
         cnt = end - beg
         pn = np.repeat(s, cnt)
         pt = owner[np.repeat(beg, cnt) + _ragged_arange(cnt)]
-        keep = self.node_cube[pn] != self.tri_cube[pt]
+        keep = self.node_cube[pn] > self.tri_cube[pt]  # one pass: nodes of the later body on faces of the earlier
         pn, pt = pn[keep], pt[keep]
         p = x[pn]
         a, b, c = x[tri[pt, 0]], x[tri[pt, 1]], x[tri[pt, 2]]

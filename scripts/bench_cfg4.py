@@ -1,0 +1,146 @@
+"""configs[4] measurement: a pile of 8x8x4 deformable 16^3-node cubes
+(3,145,728 DOF per scene) stepped entirely on one GPU by PileStepper
+(device contact detection + nodalization, right-hand side, augmentation,
+V-FPI solve, integration), with per-step timings, the streaming kernel's
+algorithmic-byte roofline, and a bounded CPU-oracle sample of the last
+step's augmented system. Prints one JSON line.
+
+Scene parameters BASELINE leaves open (recorded in the output): side 0.1 m
+(configs[0]'s cube), lateral gap 5 mm with jitter U[-2,2] mm in x and y,
+layers and the bottom layer 0.5 mm apart (no z jitter: stacked cubes would
+otherwise start interpenetrating), tol 1e-8, max_iters 500, k_v 1e2 (SURVEY's
+1e5 comes from unit-mass rigid bodies; against 16^3-node FEM cubes, whose
+node mass term (2/dt) m is about 1, k_v = 1e5 makes the non-converged
+V-FPI impulses pump energy into the pile until the mesh tears; 1e3 already
+does so at this resolution, 1e2 stays bounded -- scripts/pile_trace.py).
+
+usage: python scripts/bench_cfg4.py [--steps 120] [--kv 100] [--scenes 1] [--max-iters 500] [--cpu-iters 2]
+       [--nodes 16] [--cubes 8 8 4]
+Under torchrun the scenes shard across ranks (contiguous blocks, no data-path
+collective; counters all-reduced and the wall time max-reduced at the end)."""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def b_iter(n, nnz_num, n_c):
+    return 12 * nnz_num + 4 * (n + 1) + 32 * n + 128 * n_c
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=120)
+    ap.add_argument("--scenes", type=int, default=1)
+    ap.add_argument("--max-iters", type=int, default=500)
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--nodes", type=int, default=16)
+    ap.add_argument("--cubes", type=int, nargs=3, default=[8, 8, 4])
+    ap.add_argument("--kv", type=float, default=100.0)
+    a = ap.parse_args()
+    import torch
+
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    dev = torch.cuda.current_device()
+    from paper_2201_09212_b200 import _lib
+    from paper_2201_09212_b200.pile import CubePile, PileStepper
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    peak = 6650.0
+    try:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        peak = float(json.load(open(os.path.join(root, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=a.max_iters)
+    mine = list(range(rank * a.scenes // world, (rank + 1) * a.scenes // world))
+    h = _lib.handle(dev)
+    totals = dict(steps=0, contact_iterations=0, iterations=0, bytes=0.0, loop_s=0.0, setup_s=0.0)
+    rows = []
+    last = None
+    torch.cuda.synchronize()
+    t_all = time.perf_counter()
+    t_build = 0.0
+    for sc in mine:
+        tb = time.perf_counter()
+        pile = CubePile(*a.cubes, nodes=a.nodes, gap=0.005, jitter=0.002, gap_z=0.0005, jitter_z=0.0, seed=sc,
+                        k_v=a.kv)
+        stp = PileStepper(pile, device=dev)
+        t_build += time.perf_counter() - tb
+        for k in range(a.steps):
+            r = stp.step(cfg)
+            nnz_num = r["nnz"]  # the augmented matrix keeps only numeric entries in its top-left block
+            bi = b_iter(r["n"], nnz_num, r["n_c"])
+            totals["steps"] += 1
+            totals["contact_iterations"] += r["n_c"] * r["iterations"]
+            totals["iterations"] += r["iterations"]
+            totals["bytes"] += bi * r["iterations"]
+            totals["loop_s"] += r["loop_ms"] * 1e-3
+            totals["setup_s"] += r["setup_ms"] * 1e-3
+            if sc == mine[0]:
+                rows.append({k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in r.items()})
+        last = stp
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_all - t_build
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([totals["steps"], totals["contact_iterations"], totals["iterations"], totals["bytes"]],
+                         dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        w = torch.tensor([wall, totals["loop_s"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        totals["steps"], totals["contact_iterations"], totals["iterations"], totals["bytes"] = t.tolist()
+        wall = float(w[0])
+    if rank == 0:
+        ctc = [r for r in rows if r["n_c"] > 0]
+        loop_gbs = totals["bytes"] / totals["loop_s"] / 1e9 if totals["loop_s"] > 0 else 0.0
+        out = {"workload": f"configs[4] cube pile {a.cubes[0]}x{a.cubes[1]}x{a.cubes[2]} cubes of {a.nodes}^3 nodes",
+               "scenes": a.scenes, "n_gpus": world, "steps_per_scene": a.steps, "n_orig": last.pile.n,
+               "nnz_A_o": int(last.pile.a_data.shape[0]), "dt": last.pile.dt, "mu": last.pile.mu, "k_v": last.pile.k_v,
+               "tol": cfg.residual_tol, "max_iters": cfg.max_iters, "operator": "strict", "chebyshev": False,
+               "wall_s": wall, "scene_steps_per_s": totals["steps"] / wall,
+               "contact_iter_per_s": totals["contact_iterations"] / wall,
+               "loop": {"iterations": totals["iterations"], "loop_s": totals["loop_s"], "setup_s": totals["setup_s"],
+                        "achieved_gbs": loop_gbs, "peak_gbs": peak, "frac": loop_gbs / peak,
+                        "bytes_rule": "12 nnz + 4 (n+1) + 32 n + 128 n_c per iteration (SURVEY 8(d))"},
+               "contact_steps": len(ctc),
+               "mean_contacts": float(np.mean([r["n_c"] for r in ctc])) if ctc else 0.0,
+               "mean_iterations_contact_steps": float(np.mean([r["iterations"] for r in ctc])) if ctc else 0.0,
+               "per_step_first_scene": rows[-5:]}
+        if a.cpu_iters > 0:
+            from oracle import vfpi_oracle as O  # CPU baseline only
+
+            pile = last.pile
+            pile.x = last.x.cpu().numpy().reshape(-1, 3)
+            pile.v = last.v.cpu().numpy().reshape(-1, 3)
+            pc = pile.contacts()
+            b_o = pile.rhs()
+            t1 = time.perf_counter()
+            p, i, x, b = O.augment(pile.n, pile.a_indptr, pile.a_indices, pile.a_data, b_o, pc.jv, pile.k_v)
+            s = O.System(pile.n + pc.jv.shape[0], p, i, x, b, pc.col_i, pc.col_j, pc.frames, pc.mu, pc.mu, pc.phi)
+            O.solve(s, O.Config(residual_tol=0.0, max_iters=a.cpu_iters), np.zeros(s.n))
+            dt = time.perf_counter() - t1
+            out["cpu_baseline"] = {"kind": "port", "cores": 1, "seconds": dt, "n_c": pc.n_c,
+                                   "sample": f"final state: augmentation + oracle solve capped at {a.cpu_iters} "
+                                             "iterations (setup included); detection and b not timed",
+                                   "contact_iter_per_s": pc.n_c * a.cpu_iters / dt}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
