@@ -433,6 +433,7 @@ class PileStepper:
         sp_ = C.c_void_p(st.cuda_stream if st.cuda_stream else 1)
         t0 = time.perf_counter()
         n_o = pile.n
+        max_pen = max(0.0, -float(self.x.view(-1, 3)[:, 2].min()))
         up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev, non_blocking=False)  # noqa: E731
         i32, f64 = _lib._i32p, _lib._f64p
         if self.detect == "device":
@@ -495,7 +496,20 @@ class PileStepper:
         st.synchronize()
         self.steps += 1
         self.last = dict(v_hat=vh, lam=lam[: 3 * n_c], contacts=pc)
+        it = int(res.iterations)
+        resid = float(trace[it - 1]) if it > 0 else 0.0
         return dict(n_c=n_c, **counts, n=n, nnz=int(out.nnz),
                     iterations=int(res.iterations), converged=bool(res.converged), diverged=code == _lib.DIVERGED,
                     setup_ms=float(res.setup_ms), loop_ms=float(res.loop_ms), detect_s=t_detect,
-                    wall_s=time.perf_counter() - t0)
+                    residual=resid, max_pen_m=max_pen, wall_s=time.perf_counter() - t0)
+
+    def metrics_row(self, step: int, r: dict):
+        """``harness.MetricsRow`` of one step result (``harness.py:598-611``):
+        dyn_ms = detection + nodalization, solve_ms = setup + loop, ke_J of the
+        integrated state, max_pen_m = deepest plane penetration at the start of
+        the step (face-contact depths are not included)."""
+        from .metrics import MetricsRow, kinetic_energy
+
+        return MetricsRow(step=step, dyn_ms=1e3 * r["detect_s"], solve_ms=r["setup_ms"] + r["loop_ms"],
+                          iters=r["iterations"], residual=r["residual"], max_pen_m=r["max_pen_m"], contacts=r["n_c"],
+                          ke_J=kinetic_energy(self.m, self.v), diverged=r["diverged"], converged=r["converged"])

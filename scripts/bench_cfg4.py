@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--nodes", type=int, default=16)
     ap.add_argument("--cubes", type=int, nargs=3, default=[8, 8, 4])
     ap.add_argument("--kv", type=float, default=100.0)
+    ap.add_argument("--csv", default="", help="write scene 0's per-step metrics in the reference CSV format")
     a = ap.parse_args()
     import torch
 
@@ -66,7 +67,7 @@ def main():
     mine = list(range(rank * a.scenes // world, (rank + 1) * a.scenes // world))
     h = _lib.handle(dev)
     totals = dict(steps=0, contact_iterations=0, iterations=0, bytes=0.0, loop_s=0.0, setup_s=0.0)
-    rows = []
+    rows, csv_rows = [], []
     last = None
     torch.cuda.synchronize()
     t_all = time.perf_counter()
@@ -89,6 +90,8 @@ def main():
             totals["setup_s"] += r["setup_ms"] * 1e-3
             if sc == mine[0]:
                 rows.append({k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in r.items()})
+                if a.csv:
+                    csv_rows.append(stp.metrics_row(k, r))
         last = stp
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_all - t_build
@@ -102,6 +105,10 @@ def main():
         dist.all_reduce(w, op=dist.ReduceOp.MAX)
         totals["steps"], totals["contact_iterations"], totals["iterations"], totals["bytes"] = t.tolist()
         wall = float(w[0])
+    if a.csv and csv_rows:
+        from paper_2201_09212_b200.metrics import report_csv
+
+        report_csv(csv_rows, a.csv if world == 1 else f"{a.csv}.rank{rank}")
     if rank == 0:
         ctc = [r for r in rows if r["n_c"] > 0]
         loop_gbs = totals["bytes"] / totals["loop_s"] / 1e9 if totals["loop_s"] > 0 else 0.0

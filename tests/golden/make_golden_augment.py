@@ -16,7 +16,8 @@ and stores its input (A_o CSC arrays, b_o, J_v CSR arrays, k_v) and output
   (blocks ``w_k I`` on three nodes; some ``w_k`` exactly 0) and identity
   virtual nodes (a node's second contact, ``contacts.py:249-255``), J_v built
   the way ``nodalize`` builds it (COO of every block entry -> CSR);
-* ``aug_none``: no virtual node (A_o returned unchanged, explicit zeros kept).
+* ``aug_none``: no virtual node (A_o returned unchanged, explicit zeros kept);
+* ``metrics_ref.csv``: rows written by the reference's ``report_csv`` (harness.py:651-697).
 """
 
 from __future__ import annotations
@@ -124,7 +125,18 @@ def face_case(rng, k_v=1e5):
     return a_o, b_o, NodalContactSet([], nv, jv, k_v)
 
 
+def metrics_csv():
+    """A CSV written by the reference's report_csv (harness.py:651-697)."""
+    from condsim.harness import MetricsRow, report_csv
+
+    rows = [MetricsRow(0, 0.123456789, 1.5, 12, 3.2e-9, 0.0, 0, 0.0),
+            MetricsRow(1, 10.0, 0.1, 500, 1e-300, 1.4e-3, 60349, 1234.5678901234567, diverged=True),
+            MetricsRow(2, 1.0 / 3.0, 2.0 ** -40, 7, 5e-324, 2.5e-17, 7, 1e22)]
+    report_csv(rows, os.path.join(HERE, "metrics_ref.csv"))
+
+
 def main():
+    metrics_csv()
     rng = np.random.default_rng(91)
     a_o, b_o, nodal = rigid_case(rng)
     save("aug_rigid", a_o, b_o, nodal.jv, nodal.k_v, augment_dynamics(a_o, b_o, nodal))
