@@ -286,7 +286,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     if (WC > nw - 1 && R > CR) WC = nw - 1;
     if (WC > nw) WC = nw;
   }
-  if (C > 0 && WC < nw && p.tune_wc > 0) WC = p.tune_wc < nw ? p.tune_wc : nw - 1;
+  if (C > 0 && WC < nw && p.tune_wc > 0) {  // tuning aid: never fewer warps than one lane per contact needs
+    WC = p.tune_wc < nw ? p.tune_wc : nw - 1;
+    if (WC < (C + 31) / 32) WC = (C + 31) / 32 < nw ? (C + 31) / 32 : nw - 1;
+  }
   double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
   const double u = p.under_relax;
   const double omu = dsub(1.0, u);
