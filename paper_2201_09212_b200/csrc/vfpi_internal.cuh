@@ -94,6 +94,7 @@ struct IterParams {
   int* bar_flags;           // [G] epoch flags of the flag barrier
   long long* prof;          // optional [G][4][8] phase timestamps (NULL = off)
   int tune_wc;              // > 0: force the number of contact warps (tuning aid)
+  int tune_fw;              // > 0: resident kernel free-row warp count (tuning aid)
   int bar_mode;             // resident grid barrier: 0 one counter, 1/2 CTA pairs (clusters of 2) + counter
   const double* diag;       // [n] diagonal of A (per-scene fixed-alpha default)
   int fixed_alpha_default;  // fixed-alpha strategy with fixed_alpha = None
@@ -167,7 +168,10 @@ int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes);
 // shared-memory resident variant (whole CTA partition of A on chip)
 int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, size_t smem_bytes, cudaStream_t st,
                             std::string& err);
-constexpr int kResThreads = 512;
+#ifndef VFPI_RES_THREADS
+#define VFPI_RES_THREADS 512
+#endif
+constexpr int kResThreads = VFPI_RES_THREADS;
 int launch_scc_final(const IterParams& p, double* scc, cudaStream_t st);
 // independent scenes, one CTA each (layout with one CTA range per scene)
 int launch_iterate_scenes(const IterParams& p, int op, bool cheb, bool bb, int smem_bytes, cudaStream_t st,

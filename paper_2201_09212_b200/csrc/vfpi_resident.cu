@@ -524,8 +524,11 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     if (warp >= WC || WC == nw) {
       // ---- free rows: v_new = v* (+ w * 0 when contacts exist) ------------
       const int t0 = (WC == nw) ? tid : tid - WC * 32;
-      const int TT = (WC == nw) ? T : T - WC * 32;
-      for (int q = CR + t0; q < R; q += TT) {
+      const int TTall = (WC == nw) ? T : T - WC * 32;
+      // tune_fw > 0: only that many free-row warps (fewer issue slots taken
+      // from the contact lanes' one-shot chains)
+      const int TT = (p.tune_fw > 0 && WC < nw && p.tune_fw * 32 < TTall) ? p.tune_fw * 32 : TTall;
+      for (int q = CR + t0; t0 < TT && q < R; q += TT) {
         const double r = residual(q);
         if (!check_only) {
           const double wr = use_alpha ? alpha : ws[q];
