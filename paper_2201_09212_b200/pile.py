@@ -379,6 +379,10 @@ class PileStepper:
         g.neg_beta_dt, g.e_rest, g.rest_threshold = -(pile.beta / pile.dt), pile.e_rest, pile.thr
         self.geo = g
 
+    def state(self):
+        """(x, v) of the device state as host arrays (n_nodes, 3)."""
+        return self.x.cpu().numpy().reshape(-1, 3), self.v.cpu().numpy().reshape(-1, 3)
+
     def device_contacts(self) -> PileContacts:
         """Device detection + nodalization of the current device state, copied
         to the host (for checks; the step keeps them on the device)."""
@@ -501,15 +505,79 @@ class PileStepper:
         return dict(n_c=n_c, **counts, n=n, nnz=int(out.nnz),
                     iterations=int(res.iterations), converged=bool(res.converged), diverged=code == _lib.DIVERGED,
                     setup_ms=float(res.setup_ms), loop_ms=float(res.loop_ms), detect_s=t_detect,
-                    residual=resid, max_pen_m=max_pen, wall_s=time.perf_counter() - t0)
+                    residual=resid, max_pen_m=max_pen, ke_J=float(0.5 * torch.dot(self.m * self.v, self.v)),
+                    wall_s=time.perf_counter() - t0)
 
     def metrics_row(self, step: int, r: dict):
         """``harness.MetricsRow`` of one step result (``harness.py:598-611``):
         dyn_ms = detection + nodalization, solve_ms = setup + loop, ke_J of the
         integrated state, max_pen_m = deepest plane penetration at the start of
         the step (face-contact depths are not included)."""
-        from .metrics import MetricsRow, kinetic_energy
+        return step_metrics_row(step, r)
 
-        return MetricsRow(step=step, dyn_ms=1e3 * r["detect_s"], solve_ms=r["setup_ms"] + r["loop_ms"],
-                          iters=r["iterations"], residual=r["residual"], max_pen_m=r["max_pen_m"], contacts=r["n_c"],
-                          ke_J=kinetic_energy(self.m, self.v), diverged=r["diverged"], converged=r["converged"])
+
+def step_metrics_row(step: int, r: dict):
+    """``harness.MetricsRow`` (``harness.py:598-611``) of a ``PileStepper.step`` result."""
+    from .metrics import MetricsRow
+
+    return MetricsRow(step=step, dyn_ms=1e3 * r["detect_s"], solve_ms=r["setup_ms"] + r["loop_ms"],
+                      iters=r["iterations"], residual=r["residual"], max_pen_m=r["max_pen_m"], contacts=r["n_c"],
+                      ke_J=r["ke_J"], diverged=r["diverged"], converged=r["converged"])
+
+
+def run_piles_sharded(n_scenes: int, steps: int, cfg, make_pile, stepper=None, group=None, keep_rows=True):
+    """configs[4] scene variants sharded over ranks: every rank
+    builds and steps its contiguous block of scenes (``batch.shard_bounds``)
+    with no data-path collective; at the end the counters are sum-reduced, the
+    wall time max-reduced, and rank 0 gathers every scene's final (x, v) and
+    per-step rows in scene order.
+
+    ``make_pile(scene) -> CubePile``; ``stepper(pile) -> obj`` with
+    ``.step(cfg) -> dict`` and ``.state() -> (x, v)`` (default: ``PileStepper``
+    on the current CUDA device). Returns (per-scene results on rank 0 else
+    None, totals)."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from .batch import shard_bounds
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = shard_bounds(n_scenes, world, rank)
+    if stepper is None:
+        stepper = lambda p: PileStepper(p, device=torch.cuda.current_device())  # noqa: E731
+    local, ci, its, nsteps = [], 0, 0, 0
+    build_s = 0.0
+    t0 = time.perf_counter()
+    for sc in range(lo, hi):
+        tb = time.perf_counter()
+        st = stepper(make_pile(sc))
+        build_s += time.perf_counter() - tb
+        rows = []
+        for _ in range(steps):
+            r = st.step(cfg)
+            ci += r["n_c"] * r["iterations"]
+            its += r["iterations"]
+            nsteps += 1
+            if keep_rows:
+                rows.append(dict(r))
+        x, v = st.state()
+        local.append(dict(scene=sc, x=np.asarray(x), v=np.asarray(v), rows=rows))
+    wall = time.perf_counter() - t0 - build_s
+    totals = {"contact_iterations": ci, "iterations": its, "scene_steps": nsteps, "wall_s": wall}
+    if world == 1:
+        return local, totals
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else None
+    t = torch.tensor([float(ci), float(its), float(nsteps)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    w = torch.tensor([wall], dtype=torch.float64, device=dev)
+    dist.all_reduce(w, op=dist.ReduceOp.MAX, group=group)
+    totals = {"contact_iterations": int(t[0].item()), "iterations": int(t[1].item()), "scene_steps": int(t[2].item()),
+              "wall_s": float(w[0].item())}
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object(local, gathered, dst=0, group=group)
+    if rank != 0:
+        return None, totals
+    return [s for part in gathered for s in part], totals

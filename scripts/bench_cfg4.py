@@ -64,52 +64,35 @@ def main():
     except Exception:
         pass
     cfg = SolverConfig(residual_tol=1e-8, max_iters=a.max_iters)
-    mine = list(range(rank * a.scenes // world, (rank + 1) * a.scenes // world))
-    h = _lib.handle(dev)
-    totals = dict(steps=0, contact_iterations=0, iterations=0, bytes=0.0, loop_s=0.0, setup_s=0.0)
-    rows, csv_rows = [], []
-    last = None
-    torch.cuda.synchronize()
-    t_all = time.perf_counter()
-    t_build = 0.0
-    for sc in mine:
-        tb = time.perf_counter()
-        pile = CubePile(*a.cubes, nodes=a.nodes, gap=0.005, jitter=0.002, gap_z=0.0005, jitter_z=0.0, seed=sc,
+    from paper_2201_09212_b200.pile import run_piles_sharded
+
+    last = {}
+
+    def make_pile(sc):
+        return CubePile(*a.cubes, nodes=a.nodes, gap=0.005, jitter=0.002, gap_z=0.0005, jitter_z=0.0, seed=sc,
                         k_v=a.kv)
-        stp = PileStepper(pile, device=dev)
-        t_build += time.perf_counter() - tb
-        for k in range(a.steps):
-            r = stp.step(cfg)
-            nnz_num = r["nnz"]  # the augmented matrix keeps only numeric entries in its top-left block
-            bi = b_iter(r["n"], nnz_num, r["n_c"])
-            totals["steps"] += 1
-            totals["contact_iterations"] += r["n_c"] * r["iterations"]
-            totals["iterations"] += r["iterations"]
-            totals["bytes"] += bi * r["iterations"]
-            totals["loop_s"] += r["loop_ms"] * 1e-3
-            totals["setup_s"] += r["setup_ms"] * 1e-3
-            if sc == mine[0]:
-                rows.append({k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in r.items()})
-                if a.csv:
-                    csv_rows.append(stp.metrics_row(k, r))
-        last = stp
+
+    def stepper(pile):
+        last["st"] = PileStepper(pile, device=dev)
+        return last["st"]
+
     torch.cuda.synchronize()
-    wall = time.perf_counter() - t_all - t_build
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([totals["steps"], totals["contact_iterations"], totals["iterations"], totals["bytes"]],
-                         dtype=torch.float64, device="cuda")
-        dist.all_reduce(t)
-        w = torch.tensor([wall, totals["loop_s"]], dtype=torch.float64, device="cuda")
-        dist.all_reduce(w, op=dist.ReduceOp.MAX)
-        totals["steps"], totals["contact_iterations"], totals["iterations"], totals["bytes"] = t.tolist()
-        wall = float(w[0])
-    if a.csv and csv_rows:
-        from paper_2201_09212_b200.metrics import report_csv
-
-        report_csv(csv_rows, a.csv if world == 1 else f"{a.csv}.rank{rank}")
+    res, tot = run_piles_sharded(a.scenes, a.steps, cfg, make_pile, stepper=stepper)
+    wall = tot["wall_s"]
     if rank == 0:
+        allrows = [r for sc in res for r in sc["rows"]]
+        rows = [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in r.items()} for r in res[0]["rows"]]
+        totals = dict(steps=tot["scene_steps"], contact_iterations=tot["contact_iterations"],
+                      iterations=tot["iterations"],
+                      bytes=sum(b_iter(r["n"], r["nnz"], r["n_c"]) * r["iterations"] for r in allrows),
+                      loop_s=sum(r["loop_ms"] for r in allrows) * 1e-3,
+                      setup_s=sum(r["setup_ms"] for r in allrows) * 1e-3)
+        if a.csv:
+            from paper_2201_09212_b200.metrics import report_csv
+            from paper_2201_09212_b200.pile import step_metrics_row
+
+            report_csv([step_metrics_row(k, r) for k, r in enumerate(res[0]["rows"])], a.csv)
+        last = last["st"]
         ctc = [r for r in rows if r["n_c"] > 0]
         loop_gbs = totals["bytes"] / totals["loop_s"] / 1e9 if totals["loop_s"] > 0 else 0.0
         out = {"workload": f"configs[4] cube pile {a.cubes[0]}x{a.cubes[1]}x{a.cubes[2]} cubes of {a.nodes}^3 nodes",
