@@ -628,7 +628,7 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
   if (rc) return rc;
   const int max_ct = refresh_max_ct < 0 ? hs->max_ct_per_blk : refresh_max_ct;
   const int smem = 2 * vfpi::kSlotsPerContact * 8 * max_ct;
-  if (vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem) <= 0) {
+  if (vfpi::iterate_max_blocks_per_sm(cfg->op, cheb, bb, smem, true) <= 0) {
     h->err = "a scene has too many contacts for one CTA";
     return VFPI_UNSUPPORTED;
   }

@@ -164,7 +164,7 @@ int setup_step_matrix(Workspace& ws, const vfpi_system& dsys, const vfpi_config&
 // ---- iteration (vfpi_solve.cu) ---------------------------------------------
 int launch_iterate(const IterParams& p, int op, bool cheb, bool bb, int smem_bytes, cudaStream_t st,
                    std::string& err);
-int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes);
+int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes, bool scenes = false);
 // shared-memory resident variant (whole CTA partition of A on chip)
 int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, size_t smem_bytes, cudaStream_t st,
                             std::string& err);

@@ -31,6 +31,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef VFPI_SWEEP_RING
+#define VFPI_SWEEP_RING 1  // scene batches: SELL stream through a TMA-fed shared-memory ring (see SellRing)
+#endif
+
 namespace vfpi {
 
 namespace {
@@ -109,7 +113,10 @@ __device__ __forceinline__ void grid_totals(const double* __restrict__ part, int
 #define VFPI_SELL_UNROLL 8
 #endif
 #ifndef VFPI_SC_MIN_BLOCKS
-#define VFPI_SC_MIN_BLOCKS 4
+#define VFPI_SC_MIN_BLOCKS 4  // single-system kernel: 4 CTAs/SM (64 registers)
+#endif
+#ifndef VFPI_RING_MIN_BLOCKS
+#define VFPI_RING_MIN_BLOCKS 3  // scene-batch kernel with the SELL ring: 3 CTAs/SM
 #endif
 
 template <class X>
@@ -141,12 +148,145 @@ __device__ __forceinline__ double sell_row(const double* __restrict__ sv, const 
   return acc;
 }
 
+// ---- SELL stream through a per-warp shared-memory ring (TMA bulk copies) ----
+// Scene-batch kernels (SC; VFPI_SWEEP_RING): every warp streams its own SELL slices, in a fixed
+// cyclic order that repeats every iteration (A does not change during a
+// solve), as chunks of kRingChunk k-steps (32 rows x kRingChunk entries:
+// 2 KB of values + 1 KB of columns) into kRingStages shared-memory stages
+// with cp.async.bulk + mbarrier complete_tx. The copy engine keeps
+// kRingStages chunks per warp in flight while the lanes gather x for the
+// chunk they consume, so HBM streaming no longer waits on the gather
+// latency, and the in-flight bytes cost no registers. Lane 0 refills a stage
+// as soon as the warp has consumed it, including across the contact phase
+// and the barrier (the next iteration's first chunks arrive early).
+// Measured (B200): configs[2]-shaped batch 0.69 -> 0.74 of HBM peak with 2
+// stages of 8 k-steps at 3 CTAs/SM; the single-system kernel keeps 4 CTAs/SM
+// of register-fed loads, which the ring's smem cost would halve (configs[3]
+// 0.65 -> 0.52-0.55, configs[4] 0.57 -> 0.54-0.58), so it streams directly.
+#ifndef VFPI_RING_CHUNK
+#define VFPI_RING_CHUNK 8
+#endif
+#ifndef VFPI_RING_STAGES
+#define VFPI_RING_STAGES 2
+#endif
+constexpr int kRingChunk = VFPI_RING_CHUNK;
+constexpr int kRingStages = VFPI_RING_STAGES;
+constexpr int kRingChunkElems = kRingChunk * 32;
+constexpr int kRingStageBytes = kRingChunkElems * 12;
+constexpr int kRingBytes = VFPI_SWEEP_RING ? (kThreads / 32) * kRingStages * kRingStageBytes + 128 : 0;
+
+__device__ __forceinline__ bool mbar_try_wait(unsigned addr, unsigned parity) {
+  unsigned done;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done)
+               : "r"(addr), "r"(parity)
+               : "memory");
+  return done != 0;
+}
+
+struct SellRing {
+  double* val;     // [kRingStages][kRingChunkElems]
+  int* col;        // [kRingStages][kRingChunkElems]
+  unsigned bar0;   // shared address of this warp's first stage barrier
+  int s_first;     // first slice of the warp (s0 + warp)
+  int ps, pc;      // producer cursor: slice, chunk within the slice
+  unsigned issued, consumed;
+  bool work;       // the warp owns at least one non-empty slice
+};
+
+// lane 0: issue the chunk at the producer cursor into stage issued % kRingStages
+// (every lane then advances its copy of `issued`)
+__device__ __forceinline__ void ring_issue(SellRing& r, const IterParams& p, int s1, int nw, uint64_t pol) {
+  int64_t off;
+  int W;
+  for (;;) {  // skip empty slices (r.work guarantees termination)
+    off = p.slice_off[r.ps];
+    W = (int)((p.slice_off[r.ps + 1] - off) >> 5);
+    if (W > 0) break;
+    r.ps += nw;
+    if (r.ps >= s1) r.ps = r.s_first;
+  }
+  const int k0 = r.pc * kRingChunk;
+  const int kk = min(kRingChunk, W - k0);
+  const int stage = (int)(r.issued % kRingStages);
+  const unsigned bar = r.bar0 + 8u * (unsigned)stage;
+  const unsigned dv = (unsigned)__cvta_generic_to_shared(r.val + (size_t)stage * kRingChunkElems);
+  const unsigned dc = (unsigned)__cvta_generic_to_shared(r.col + (size_t)stage * kRingChunkElems);
+  const unsigned bv = (unsigned)kk * 32u * 8u, bc = (unsigned)kk * 32u * 4u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bv + bc) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(dv), "l"(p.sell_val + off + 32 * (int64_t)k0), "r"(bv), "r"(bar), "l"(pol)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(dc), "l"(p.sell_col + off + 32 * (int64_t)k0), "r"(bc), "r"(bar), "l"(pol)
+      : "memory");
+  ++r.pc;
+  if (r.pc * kRingChunk >= W) {
+    r.pc = 0;
+    r.ps += nw;
+    if (r.ps >= s1) r.ps = r.s_first;
+  }
+}
+
+// sequential row sum of the warp's next slice (width W) out of the ring,
+// same order and operations as sell_row
+template <class X>
+__device__ __forceinline__ double ring_row(SellRing& r, const IterParams& p, int W, int lane, int s1, int nw,
+                                           uint64_t pol, X x) {
+  double acc = 0.0;
+  for (int k0 = 0; k0 < W; k0 += kRingChunk) {
+    const int kk = min(kRingChunk, W - k0);
+    const int stage = (int)(r.consumed % kRingStages);
+    const unsigned bar = r.bar0 + 8u * (unsigned)stage;
+    const unsigned par = (r.consumed / kRingStages) & 1u;
+    while (!mbar_try_wait(bar, par)) {
+    }
+    const double* vs = r.val + (size_t)stage * kRingChunkElems + lane;
+    const int* cs = r.col + (size_t)stage * kRingChunkElems + lane;
+    if (kk == kRingChunk) {
+      int c[kRingChunk];
+      double a[kRingChunk], xv[kRingChunk];
+#pragma unroll
+      for (int u = 0; u < kRingChunk; ++u) {
+        c[u] = cs[32 * u];
+        a[u] = vs[32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < kRingChunk; ++u) xv[u] = c[u] >= 0 ? x(c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kRingChunk; ++u)
+        if (c[u] >= 0) acc = dadd(acc, dmul(a[u], xv[u]));
+    } else {
+      for (int u = 0; u < kk; ++u) {
+        const int c = cs[32 * u];
+        if (c >= 0) acc = dadd(acc, dmul(vs[32 * u], x(c)));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      ring_issue(r, p, s1, nw, pol);
+    }
+    ++r.issued;
+    ++r.consumed;
+  }
+  return acc;
+}
+
 // SC = false: one system over a cooperative grid (grid barrier per iteration).
 // SC = true : a batch of independent scenes, one CTA per scene (CTA b owns
 //             scene b's rows and contacts); every CTA runs its own iteration
 //             loop, reductions and termination with CTA barriers only.
+template <bool SC>
+constexpr bool kUseRing = SC && VFPI_SWEEP_RING;
+template <bool SC>
+constexpr int kRingSmem = kUseRing<SC> ? kRingBytes : 0;
+
 template <int OP, bool CHEB, bool BB, bool HASC, bool SC>
-__global__ void __launch_bounds__(kThreads, VFPI_SC_MIN_BLOCKS) k_iterate(IterParams p) {
+__global__ void __launch_bounds__(kThreads, kUseRing<SC> ? VFPI_RING_MIN_BLOCKS : VFPI_SC_MIN_BLOCKS)
+    k_iterate(IterParams p) {
   extern __shared__ double smem[];
   __shared__ double sm_warp[3 * (kThreads / 32)];
   __shared__ double sm_tot[4];
@@ -162,6 +302,37 @@ __global__ void __launch_bounds__(kThreads, VFPI_SC_MIN_BLOCKS) k_iterate(IterPa
   double* jt_s = smem + kSlotsPerContact * nct;  // J_c^T lam_{l-1} rows   [6*nct]
 
   for (int t = threadIdx.x; t < kSlotsPerContact * nct; t += blockDim.x) jt_s[t] = 0.0;
+  __shared__ __align__(8) uint64_t ring_bar[kUseRing<SC> ? kThreads / 32 : 1][kRingStages];
+  uint64_t pol = 0;
+  SellRing ring{};
+  if constexpr (kUseRing<SC>) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const size_t cbytes = (size_t)2 * kSlotsPerContact * nct * sizeof(double);
+    unsigned char* base = reinterpret_cast<unsigned char*>(smem) + ((cbytes + 127) & ~(size_t)127);
+    unsigned char* mine = base + (size_t)warp * kRingStages * kRingStageBytes;
+    ring.val = reinterpret_cast<double*>(mine);
+    ring.col = reinterpret_cast<int*>(mine + (size_t)kRingStages * kRingChunkElems * sizeof(double));
+    ring.bar0 = (unsigned)__cvta_generic_to_shared(&ring_bar[warp][0]);
+    ring.s_first = s0 + warp;
+    ring.ps = ring.s_first;
+    ring.pc = 0;
+    ring.issued = ring.consumed = 0;
+    bool w = false;
+    for (int s = s0 + warp; s < s1 && !w; s += nwarps) w = p.slice_off[s + 1] > p.slice_off[s];
+    ring.work = w;
+    if (lane == 0) {
+      for (int st = 0; st < kRingStages; ++st)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ring.bar0 + 8u * (unsigned)st) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (w)
+        for (int st = 0; st < kRingStages; ++st) {
+          ring_issue(ring, p, s1, nwarps, pol);
+          ++ring.issued;
+        }
+    }
+    __syncwarp();
+    ring.issued = w ? kRingStages : 0;  // lane 0's count, for every lane
+  }
   __syncthreads();
 
   double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
@@ -291,7 +462,9 @@ __global__ void __launch_bounds__(kThreads, VFPI_SC_MIN_BLOCKS) k_iterate(IterPa
       const int pos = p0 + (s - s0) * 32 + lane;
       const int64_t off = p.slice_off[s];
       const int W = (int)((p.slice_off[s + 1] - off) >> 5);
-      const double y = sell_row(p.sell_val, p.sell_col, off, W, lane, [&](int c) { return vcur[c]; });
+      double y;
+      if constexpr (kUseRing<SC>) y = ring_row(ring, p, W, lane, s1, nwarps, pol, [&](int c) { return vcur[c]; });
+      else y = sell_row(p.sell_val, p.sell_col, off, W, lane, [&](int c) { return vcur[c]; });
       if (pos < p1) {
         const int row = __ldg(p.row_list + pos);
         const int slot = HASC ? __ldg(p.row_slot + pos) : -1;
@@ -409,6 +582,13 @@ __global__ void __launch_bounds__(kThreads, VFPI_SC_MIN_BLOCKS) k_iterate(IterPa
     theta_prev = theta;
   }
 
+  if constexpr (kUseRing<SC>) {  // drain the chunks in flight before the shared memory is released
+    for (unsigned n = ring.consumed; n < ring.issued; ++n) {
+      const unsigned bar = ring.bar0 + 8u * (n % kRingStages);
+      while (!mbar_try_wait(bar, (n / kRingStages) & 1u)) {
+      }
+    }
+  }
   // ---- outputs: each CTA copies its own rows / contacts -------------------
   const double* vfin = vb[final_buf];
   for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
@@ -470,11 +650,12 @@ KernelFn pick(int op, bool cheb, bool bb, bool hasc, bool sc = false) {
 
 }  // namespace
 
-int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes) {
-  KernelFn f = pick(op, cheb, bb, true);
+int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes, bool scenes) {
+  KernelFn f = pick(op, cheb, bb, true, scenes);
   if (ensure_max_dynamic_smem((const void*)f) != cudaSuccess) return 0;
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, smem_bytes) != cudaSuccess) return 0;
+  const int ring = scenes ? kRingSmem<true> : kRingSmem<false>;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kThreads, smem_bytes + ring) != cudaSuccess) return 0;
   return nb;
 }
 
@@ -487,7 +668,8 @@ int launch_iterate(const IterParams& p, int op, bool cheb, bool bb, int smem_byt
   }
   IterParams local = p;
   void* args[] = {&local};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kThreads), args, smem_bytes, st);
+  cudaError_t e =
+      cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kThreads), args, smem_bytes + kRingSmem<false>, st);
   if (e != cudaSuccess) {
     err = std::string("cooperative launch: ") + cudaGetErrorString(e);
     return VFPI_CUDA_ERROR;
@@ -500,7 +682,7 @@ int launch_iterate_scenes(const IterParams& p, int op, bool cheb, bool bb, int s
   KernelFn f = pick(op, cheb, bb, p.n_c > 0, true);
   cudaError_t e = ensure_max_dynamic_smem((const void*)f);
   if (e != cudaSuccess) { err = cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
-  f<<<p.G, kThreads, smem_bytes, st>>>(p);
+  f<<<p.G, kThreads, smem_bytes + kRingSmem<true>, st>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     err = std::string("scene-batch launch: ") + cudaGetErrorString(e);
