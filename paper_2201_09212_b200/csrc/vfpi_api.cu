@@ -39,11 +39,18 @@ struct SetupGraph {
   std::vector<uint64_t> key, last_key;
   cudaGraphExec_t exec = nullptr;
   int64_t launches = 0;
+  uint64_t used = 0;  // LRU tick
+};
+// two graphs per phase: a caller that alternates two input buffers (double-
+// buffered uploads overlapping the previous solve) replays both
+struct SetupGraphSet {
+  SetupGraph slot[2];
+  uint64_t tick = 0;
 };
 
 struct vfpi_handle {
   Workspace ws;
-  SetupGraph graph_layout, graph_pack;
+  SetupGraphSet graph_layout, graph_pack;
   int use_graphs = 1;
   std::string err;
   int64_t launches = 0;
@@ -95,11 +102,17 @@ int choose_blocks_resident(const vfpi_system& s, int num_sms) {
 // Run a setup phase: eagerly the first time a key is seen (this is where the
 // workspace grows), captured into a graph the second time, replayed after.
 template <class F>
-int run_setup_phase(vfpi_handle* h, SetupGraph& g, std::vector<uint64_t> key, cudaStream_t st, F&& body) {
+int run_setup_phase(vfpi_handle* h, SetupGraphSet& gs, std::vector<uint64_t> key, cudaStream_t st, F&& body) {
   const bool capturable = h->use_graphs && st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread;
   key.push_back(vfpi::alloc_generation());
   key.push_back((uint64_t)(uintptr_t)st);
   if (!capturable) return body();
+  int si = -1;
+  for (int i = 0; i < 2 && si < 0; ++i)
+    if (gs.slot[i].key == key || gs.slot[i].last_key == key) si = i;
+  if (si < 0) si = gs.slot[0].used <= gs.slot[1].used ? 0 : 1;
+  SetupGraph& g = gs.slot[si];
+  g.used = ++gs.tick;
   if (g.exec && g.key == key) {
     CK(cudaGraphLaunch(g.exec, st));
     h->launches += g.launches;
@@ -277,8 +290,9 @@ void vfpi_destroy(vfpi_handle* h) {
   if (pw.h_small) cudaFreeHost(pw.h_small);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
-  for (SetupGraph* g : {&h->graph_layout, &h->graph_pack})
-    if (g->exec) cudaGraphExecDestroy(g->exec);
+  for (SetupGraphSet* gs : {&h->graph_layout, &h->graph_pack})
+    for (SetupGraph& g : gs->slot)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
   if (h->ws.stream) cudaStreamDestroy(h->ws.stream);
   if (h->ws.h_summary) cudaFreeHost(h->ws.h_summary);
   if (h->ws.h_status) cudaFreeHost(h->ws.h_status);
