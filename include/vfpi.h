@@ -190,8 +190,7 @@ int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
 /* Tuning knobs. key 0: force the resident kernel's contact-warp count (0 = auto);
  * key 1: order units by their smallest referenced column (default 1; 0 = row order);
  * key 2: sort each CTA's free rows by decreasing length (default 1);
- * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0);
- * key 6: resident grid barrier (0 one counter = default, 1/2 CTA pairs). */
+ * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0). */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

@@ -61,8 +61,6 @@ struct vfpi_handle {
   int kernel_mode = 0;  // 0 auto, 1 force shared-memory resident, 2 force streaming
   int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
   int tune_wc = 0;      // >0: force the contact-warp count of the resident kernel
-  int bar_mode = 0;     // resident grid barrier (IterParams::bar_mode)
-  int tune_fw = 0;      // >0: resident kernel free-row warp count
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
   vfpi::PileWork pile;
@@ -312,8 +310,6 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (key == 3 && value > 0) { h->layout_opt.entry_cost = value; return VFPI_OK; }
   if (key == 4 && value > 0) { h->layout_opt.row_cost = value; return VFPI_OK; }
   if (key == 5 && value >= 0) { h->layout_opt.contact_cost = value; return VFPI_OK; }
-  if (key == 6 && value >= 0 && value <= 2) { h->bar_mode = value; return VFPI_OK; }
-  if (key == 7 && value >= 0) { h->tune_fw = value; return VFPI_OK; }
   return VFPI_BAD_ARGUMENT;
 }
 
@@ -464,8 +460,6 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.prof = nullptr;
   p.prof_iter0 = 0;
   p.tune_wc = h->tune_wc;
-  p.bar_mode = h->bar_mode;
-  p.tune_fw = h->tune_fw;
   p.diag = P<double>(ws.diag);
   p.fixed_alpha_default = 0;
   p.trace_stride = 0;

@@ -94,8 +94,6 @@ struct IterParams {
   int* bar_flags;           // [G] epoch flags of the flag barrier
   long long* prof;          // optional [G][4][8] phase timestamps (NULL = off)
   int tune_wc;              // > 0: force the number of contact warps (tuning aid)
-  int tune_fw;              // > 0: resident kernel free-row warp count (tuning aid)
-  int bar_mode;             // resident grid barrier: 0 one counter, 1/2 CTA pairs (clusters of 2) + counter
   const double* diag;       // [n] diagonal of A (per-scene fixed-alpha default)
   int fixed_alpha_default;  // fixed-alpha strategy with fixed_alpha = None
   size_t trace_stride;      // scene batches: residual_trace row stride per scene

@@ -70,45 +70,23 @@ __device__ __forceinline__ void cta_reduce3(double a, double b, double c, double
   }
 }
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
 // Arrive (publish this CTA's partials, release-add the counter) and wait until
-// all G CTAs arrived at `epoch` (counter never reset).
-//   mode 0: every CTA release-adds the counter (target epoch*G);
-//   mode 1: CTA pairs (clusters of 2) first meet at a cluster barrier, then
-//           only rank 0 of each pair release-adds (target epoch*G/2: half the
-//           serialised same-address reductions) and both CTAs poll;
-//   mode 2: as 1, but only rank 0 polls and a second cluster barrier
-//           releases rank 1.
-// Rank 1's writes reach the other clusters through the cluster-scope
-// release/acquire followed by rank 0's gpu-scope release (cumulativity).
+// all G CTAs arrived at `epoch` (counter target epoch*G, never reset).
 __device__ __forceinline__ void grid_arrive_wait(const double* sm_tot, double* part, int off, unsigned* counter,
-                                                 int G, int epoch, int mode) {
+                                                 int G, int epoch) {
   if (threadIdx.x == 0) {
     double* q = part + (size_t)blockIdx.x * kPartialStride + off;
     q[0] = sm_tot[0];
     q[1] = sm_tot[1];
     q[2] = sm_tot[2];
-  }
-  unsigned rank = 0, arrivals = (unsigned)G;
-  if (mode != 0) {
-    cluster_sync_all();
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    arrivals = (unsigned)G / 2u;
-  }
-  if (threadIdx.x == 0 && (mode != 2 || rank == 0)) {
-    if (rank == 0) red_release_add(counter, 1u);
-    const unsigned target = (unsigned)epoch * arrivals;
+    red_release_add(counter, 1u);
+    const unsigned target = (unsigned)epoch * (unsigned)G;
     const long long t0 = clock64();
     while (ld_acquire_u32(counter) < target) {
       if (clock64() - t0 > (1ll << 36)) __trap();  // ~30 s: never in a healthy run
     }
   }
-  if (mode == 2) cluster_sync_all();
-  else __syncthreads();
+  __syncthreads();
 }
 
 // warp 0: fixed-order sum of the G published partials -> sm_tot[0..2]
@@ -398,7 +376,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       }
       cta_reduce3(sz, ss, zz, sm_warp, sm_tot);
       __syncthreads();
-      grid_arrive_wait(sm_tot, part, 4, counter, G, ++epoch, p.bar_mode);
+      grid_arrive_wait(sm_tot, part, 4, counter, G, ++epoch);
       if (warp == 0) warp0_collect(part, 4, G, sm_tot, false);
       __syncthreads();
       const double tsz = sm_tot[0], tss = sm_tot[1], tzz = sm_tot[2];
@@ -524,11 +502,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     if (warp >= WC || WC == nw) {
       // ---- free rows: v_new = v* (+ w * 0 when contacts exist) ------------
       const int t0 = (WC == nw) ? tid : tid - WC * 32;
-      const int TTall = (WC == nw) ? T : T - WC * 32;
-      // tune_fw > 0: only that many free-row warps (fewer issue slots taken
-      // from the contact lanes' one-shot chains)
-      const int TT = (p.tune_fw > 0 && WC < nw && p.tune_fw * 32 < TTall) ? p.tune_fw * 32 : TTall;
-      for (int q = CR + t0; t0 < TT && q < R; q += TT) {
+      const int TT = (WC == nw) ? T : T - WC * 32;
+      for (int q = CR + t0; q < R; q += TT) {
         const double r = residual(q);
         if (!check_only) {
           const double wr = use_alpha ? alpha : ws[q];
@@ -578,7 +553,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         }
       }
     }
-    grid_arrive_wait(sm_tot, part, 0, counter, G, ++epoch, p.bar_mode);
+    grid_arrive_wait(sm_tot, part, 0, counter, G, ++epoch);
     stamp(5);
   }
 
@@ -631,28 +606,8 @@ int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, siz
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kResThreads, smem_bytes);
   if (e != cudaSuccess || nb < 1) { err = "resident kernel does not fit on an SM"; return VFPI_UNSUPPORTED; }
   IterParams local = p;
-  if (local.bar_mode != 0 && (local.G % 2) != 0) local.bar_mode = 0;  // pairs need an even grid
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(local.G);
-  lc.blockDim = dim3(kResThreads);
-  lc.dynamicSmemBytes = smem_bytes;
-  lc.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = local.bar_mode != 0 ? 2 : 1;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = local.bar_mode != 0 ? 2 : 1;
-  e = cudaLaunchKernelEx(&lc, f, local);
-  if (e != cudaSuccess && local.bar_mode != 0) {  // pairs not co-resident: one-counter barrier
-    (void)cudaGetLastError();
-    local.bar_mode = 0;
-    lc.numAttrs = 1;
-    e = cudaLaunchKernelEx(&lc, f, local);
-  }
+  void* args[] = {&local};
+  e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kResThreads), args, smem_bytes, st);
   if (e != cudaSuccess) {
     err = std::string("cooperative launch (resident): ") + cudaGetErrorString(e);
     return VFPI_CUDA_ERROR;
