@@ -462,19 +462,39 @@ __global__ void __launch_bounds__(kThreads, kUseRing<SC> ? VFPI_RING_MIN_BLOCKS 
       const int pos = p0 + (s - s0) * 32 + lane;
       const int64_t off = p.slice_off[s];
       const int W = (int)((p.slice_off[s + 1] - off) >> 5);
+      // the row's own operands are independent of the row sum. The ring
+      // kernels (registers to spare) issue their two levels of dependent
+      // loads before the sweep so they land while the SELL stream is in
+      // flight (configs[2] batch 0.74 -> 0.77 of HBM peak); the 64-register
+      // single-system kernel loads them afterwards (early loads spill there:
+      // configs[3] 0.65 -> 0.55)
+      const bool live = pos < p1;
+      int row = 0, slot = -1;
+      double bv = 0.0, wv = 0.0, vc = 0.0;
+      auto row_operands = [&] {
+        if (live) {
+          row = __ldg(p.row_list + pos);
+          if (HASC) slot = __ldg(p.row_slot + pos);
+          bv = __ldg(p.b + row);
+          if (!use_alpha) wv = __ldg(p.w + row);
+          vc = vcur[row];
+        }
+      };
       double y;
-      if constexpr (kUseRing<SC>) y = ring_row(ring, p, W, lane, s1, nwarps, pol, [&](int c) { return vcur[c]; });
-      else y = sell_row(p.sell_val, p.sell_col, off, W, lane, [&](int c) { return vcur[c]; });
-      if (pos < p1) {
-        const int row = __ldg(p.row_list + pos);
-        const int slot = HASC ? __ldg(p.row_slot + pos) : -1;
-        const double r = dsub(y, __ldg(p.b + row));
+      if constexpr (kUseRing<SC>) {
+        row_operands();
+        y = ring_row(ring, p, W, lane, s1, nwarps, pol, [&](int c) { return vcur[c]; });
+      } else {
+        y = sell_row(p.sell_val, p.sell_col, off, W, lane, [&](int c) { return vcur[c]; });
+        row_operands();
+      }
+      if (live) {
+        const double r = dsub(y, bv);
         // force residual of the previous iterate (solver.py:437-439)
         const double f = (slot >= 0) ? dsub(r, jt_s[slot]) : dsub(r, 0.0);
         fr = dadd(fr, dmul(f, f));
         if (!check_only) {
-          const double wr = use_alpha ? alpha : __ldg(p.w + row);
-          const double vc = vcur[row];
+          const double wr = use_alpha ? alpha : wv;
           const double vstar = dsub(vc, dmul(wr, r));
           if (slot >= 0) {
             vs_s[slot] = vstar;
