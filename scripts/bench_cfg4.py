@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--nodes", type=int, default=16)
     ap.add_argument("--cubes", type=int, nargs=3, default=[8, 8, 4])
     ap.add_argument("--kv", type=float, default=100.0)
+    ap.add_argument("--chebyshev", action="store_true")
     ap.add_argument("--csv", default="", help="write scene 0's per-step metrics in the reference CSV format")
     a = ap.parse_args()
     import torch
@@ -63,7 +64,7 @@ def main():
         peak = float(json.load(open(os.path.join(root, "MEASURED_PEAKS.json")))["hbm_gbs"])
     except Exception:
         pass
-    cfg = SolverConfig(residual_tol=1e-8, max_iters=a.max_iters)
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=a.max_iters, chebyshev=a.chebyshev)
     from paper_2201_09212_b200.pile import run_piles_sharded
 
     last = {}
@@ -84,7 +85,8 @@ def main():
         rows = [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in r.items()} for r in res[0]["rows"]]
         totals = dict(steps=tot["scene_steps"], contact_iterations=tot["contact_iterations"],
                       iterations=tot["iterations"],
-                      bytes=sum(b_iter(r["n"], r["nnz"], r["n_c"]) * r["iterations"] for r in allrows),
+                      bytes=sum((b_iter(r["n"], r["nnz"], r["n_c"]) + (8 * r["n"] if a.chebyshev else 0)) * r["iterations"]
+                                for r in allrows),
                       loop_s=sum(r["loop_ms"] for r in allrows) * 1e-3,
                       setup_s=sum(r["setup_ms"] for r in allrows) * 1e-3)
         if a.csv:
@@ -98,7 +100,7 @@ def main():
         out = {"workload": f"configs[4] cube pile {a.cubes[0]}x{a.cubes[1]}x{a.cubes[2]} cubes of {a.nodes}^3 nodes",
                "scenes": a.scenes, "n_gpus": world, "steps_per_scene": a.steps, "n_orig": last.pile.n,
                "nnz_A_o": int(last.pile.a_data.shape[0]), "dt": last.pile.dt, "mu": last.pile.mu, "k_v": last.pile.k_v,
-               "tol": cfg.residual_tol, "max_iters": cfg.max_iters, "operator": "strict", "chebyshev": False,
+               "tol": cfg.residual_tol, "max_iters": cfg.max_iters, "operator": "strict", "chebyshev": a.chebyshev,
                "wall_s": wall, "scene_steps_per_s": totals["steps"] / wall,
                "contact_iter_per_s": totals["contact_iterations"] / wall,
                "loop": {"iterations": totals["iterations"], "loop_s": totals["loop_s"], "setup_s": totals["setup_s"],
