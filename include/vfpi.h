@@ -322,6 +322,46 @@ typedef struct vfpi_pile_contacts {  /* device buffers owned by the handle */
 /* x, v: device state [3*nodes]; outputs valid until the next call on h. */
 int vfpi_pile_contacts_device(vfpi_handle* h, const vfpi_pile_geometry* g, const double* x, const double* v,
                               vfpi_pile_contacts* out, void* stream);
+/* ---- nodalization ------------------------------- */
+/* condsim.contacts.nodalize (contacts.py:271-321) on the device: raw contacts
+ * (sides: 0 node with ref = velocity offset, 1 rigid with ref = body index,
+ * -1 static for the second side) -> nodal contacts (slots as augmented
+ * columns, virtual nodes, J_v canonical CSR with every block entry stored),
+ * frames (contact_frame, :131-149) and phi (stabilization_term, :230-239),
+ * bit-identical to the reference. Device pointers in; outputs are device
+ * buffers owned by the handle, valid until the next call. mu2 = NaN: None. */
+typedef struct vfpi_nodalize_input {
+  int64_t n_c;
+  int64_t n_o;                 /* velocity dimension (columns of J_v) */
+  const int32_t* first_kind;
+  const int32_t* first_ref;
+  const int32_t* second_kind;
+  const int32_t* second_ref;
+  const double* point;         /* [n_c*3] */
+  const double* normal;        /* [n_c*3] (normalised inside, as contact_frame does) */
+  const double* depth;         /* [n_c] */
+  const double* q;             /* generalized coordinates (rigid: position + quaternion) */
+  const double* v;             /* [n_o] velocities */
+  const int32_t* body_q;       /* per body: coordinate offset (Body.q_offset) */
+  const int32_t* body_v;       /* per body: velocity offset (Body.v_offset) */
+  double mu, mu2, beta_err, dt, e_rest, rest_threshold;
+} vfpi_nodalize_input;
+
+typedef struct vfpi_nodal_contacts {
+  int64_t n_c, n_virtual, jv_nnz;
+  int32_t* col_i;       /* augmented column of side i */
+  int32_t* col_j;       /* augmented column of side j, -1 for S contacts */
+  double* frames;       /* [n_c*9] */
+  double* phi;
+  double* mu;
+  double* mu2;
+  int32_t* jv_indptr;   /* [3 n_virtual + 1] */
+  int32_t* jv_indices;
+  double* jv_data;
+} vfpi_nodal_contacts;
+
+int vfpi_nodalize_device(vfpi_handle* h, const vfpi_nodalize_input* in, vfpi_nodal_contacts* out, void* stream);
+
 /* synchronous device-to-device copy (reading handle-owned outputs into caller buffers) */
 int vfpi_memcpy_d2d(void* dst, const void* src, int64_t bytes);
 

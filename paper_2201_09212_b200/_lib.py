@@ -76,6 +76,26 @@ class VfpiPileContacts(C.Structure):
     ]
 
 
+class VfpiNodalizeInput(C.Structure):
+    _fields_ = [
+        ("n_c", C.c_int64), ("n_o", C.c_int64),
+        ("first_kind", C.c_void_p), ("first_ref", C.c_void_p), ("second_kind", C.c_void_p),
+        ("second_ref", C.c_void_p), ("point", C.c_void_p), ("normal", C.c_void_p), ("depth", C.c_void_p),
+        ("q", C.c_void_p), ("v", C.c_void_p), ("body_q", C.c_void_p), ("body_v", C.c_void_p),
+        ("mu", C.c_double), ("mu2", C.c_double), ("beta_err", C.c_double), ("dt", C.c_double),
+        ("e_rest", C.c_double), ("rest_threshold", C.c_double),
+    ]
+
+
+class VfpiNodalContacts(C.Structure):
+    _fields_ = [
+        ("n_c", C.c_int64), ("n_virtual", C.c_int64), ("jv_nnz", C.c_int64),
+        ("col_i", C.c_void_p), ("col_j", C.c_void_p), ("frames", C.c_void_p), ("phi", C.c_void_p),
+        ("mu", C.c_void_p), ("mu2", C.c_void_p), ("jv_indptr", C.c_void_p), ("jv_indices", C.c_void_p),
+        ("jv_data", C.c_void_p),
+    ]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -119,6 +139,8 @@ def lib() -> C.CDLL:
                 "vfpi_pile_contacts_device": (C.c_int, [H, C.POINTER(VfpiPileGeometry), C.c_void_p, C.c_void_p,
                                                         C.POINTER(VfpiPileContacts), C.c_void_p]),
                 "vfpi_memcpy_d2d": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+                "vfpi_nodalize_device": (C.c_int, [H, C.POINTER(VfpiNodalizeInput), C.POINTER(VfpiNodalContacts),
+                                                   C.c_void_p]),
                 "vfpi_advance_device": (C.c_int, [H, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                                   C.c_void_p]),
                 "vfpi_host_alloc": (C.c_void_p, [C.c_int64]),
@@ -209,3 +231,18 @@ def as_i32(a) -> np.ndarray:
 
 def as_f64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a), dtype=np.float64)
+
+
+def device_to_numpy(src, count: int, dtype, device: int = 0) -> np.ndarray:
+    """Copy ``count`` elements at a device pointer (e.g. a handle-owned output
+    buffer) into a new host array."""
+    import torch
+
+    tdt = {np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64}[np.dtype(dtype)]
+    t = torch.empty(max(int(count), 1), dtype=tdt, device=torch.device("cuda", device))
+    if count:
+        nbytes = int(count) * t.element_size()
+        rc = lib().vfpi_memcpy_d2d(C.c_void_p(t.data_ptr()), C.cast(src, C.c_void_p), C.c_int64(nbytes))
+        if rc != OK:
+            raise RuntimeError(f"device copy failed with code {rc}")
+    return t.cpu().numpy()[: int(count)]

@@ -64,6 +64,7 @@ struct vfpi_handle {
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
   vfpi::PileWork pile;
+  vfpi::NodalizeWork nod;
   int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
@@ -246,6 +247,7 @@ int vfpi_create(int device, vfpi_handle** out) {
   cudaMallocHost(&h->h_flags, 16);
   cudaMallocHost(&h->aug.h_small, 2 * sizeof(int64_t));
   cudaMallocHost(&h->pile.h_small, 4 * sizeof(int64_t));
+  cudaMallocHost(&h->nod.h_small, 2 * sizeof(int64_t));
   *out = h;
   return VFPI_OK;
 }
@@ -286,6 +288,11 @@ void vfpi_destroy(vfpi_handle* h) {
                             &pw.cj, &pw.fr, &pw.mu, &pw.phi, &pw.jrp, &pw.jci, &pw.jcx, &pw.tmp})
     if (b->p) cudaFree(b->p);
   if (pw.h_small) cudaFreeHost(pw.h_small);
+  vfpi::NodalizeWork& nw = h->nod;
+  for (Workspace::Buf* b : {&nw.first, &nw.vflag, &nw.vpos, &nw.jcnt, &nw.jpos, &nw.flag, &nw.tmp, &nw.ci, &nw.cj,
+                            &nw.fr, &nw.phi, &nw.mu, &nw.mu2, &nw.jrp, &nw.jci, &nw.jcx})
+    if (b->p) cudaFree(b->p);
+  if (nw.h_small) cudaFreeHost(nw.h_small);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
   for (SetupGraphSet* gs : {&h->graph_layout, &h->graph_pack})
@@ -1424,4 +1431,46 @@ int vfpi_memcpy_d2d(void* dst, const void* src, int64_t bytes) {
   if (bytes < 0) return VFPI_BAD_ARGUMENT;
   if (bytes == 0) return VFPI_OK;
   return cudaMemcpy(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice) == cudaSuccess ? VFPI_OK : VFPI_CUDA_ERROR;
+}
+
+int vfpi_nodalize_device(vfpi_handle* h, const vfpi_nodalize_input* in, vfpi_nodal_contacts* out, void* stream) {
+  if (!h || !in || !out || in->n_c < 0 || in->n_c > INT32_MAX / 2 || in->n_o < 0 || in->n_o > INT32_MAX / 2)
+    return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::NodalizeIn ni;
+  ni.n_c = in->n_c;
+  ni.n_o = (int)in->n_o;
+  ni.first_kind = in->first_kind;
+  ni.first_ref = in->first_ref;
+  ni.second_kind = in->second_kind;
+  ni.second_ref = in->second_ref;
+  ni.point = in->point;
+  ni.normal = in->normal;
+  ni.depth = in->depth;
+  ni.q = in->q;
+  ni.v = in->v;
+  ni.body_q = in->body_q;
+  ni.body_v = in->body_v;
+  ni.mu = in->mu;
+  ni.mu2 = std::isnan(in->mu2) ? in->mu : in->mu2;
+  ni.neg_beta_dt = -(in->beta_err / in->dt);
+  ni.e_rest = in->e_rest;
+  ni.rest_threshold = in->rest_threshold;
+  vfpi::NodalizeOut o;
+  const int rc = vfpi::nodalize_device(h->nod, ni, st, o, h->err, h->launches);
+  if (rc != VFPI_OK) return rc;
+  out->n_c = in->n_c;
+  out->n_virtual = o.n_virtual;
+  out->jv_nnz = o.jv_nnz;
+  out->col_i = o.col_i;
+  out->col_j = o.col_j;
+  out->frames = o.frames;
+  out->phi = o.phi;
+  out->mu = o.mu;
+  out->mu2 = o.mu2;
+  out->jv_indptr = o.jv_indptr;
+  out->jv_indices = o.jv_indices;
+  out->jv_data = o.jv_data;
+  return VFPI_OK;
 }

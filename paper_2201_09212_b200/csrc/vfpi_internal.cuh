@@ -290,6 +290,42 @@ struct PileWork {
 int pile_contacts_device(PileWork& w, const PileGeometry& g, const double* x, const double* v, cudaStream_t st,
                          PileContactsOut& out, std::string& err, int64_t& launches);
 
+// ---- nodalization (vfpi_nodalize.cu) -----------------------------------------
+struct NodalizeIn {
+  int64_t n_c = 0;
+  int n_o = 0;  // velocity dimension
+  const int* first_kind = nullptr;   // 0 node (ref = velocity offset), 1 rigid (ref = body)
+  const int* first_ref = nullptr;
+  const int* second_kind = nullptr;  // -1 static, 0 node, 1 rigid
+  const int* second_ref = nullptr;
+  const double* point = nullptr;     // [n_c*3]
+  const double* normal = nullptr;    // [n_c*3]
+  const double* depth = nullptr;     // [n_c]
+  const double* q = nullptr;         // generalized coordinates
+  const double* v = nullptr;         // velocities [n_o]
+  const int* body_q = nullptr;       // per body: coordinate offset
+  const int* body_v = nullptr;       // per body: velocity offset
+  double mu = 0, mu2 = 0, neg_beta_dt = 0, e_rest = 0, rest_threshold = 0;
+};
+struct NodalizeOut {
+  int n_virtual = 0, jv_nnz = 0;
+  int* col_i = nullptr;
+  int* col_j = nullptr;
+  double* frames = nullptr;
+  double* phi = nullptr;
+  double* mu = nullptr;
+  double* mu2 = nullptr;
+  int* jv_indptr = nullptr;
+  int* jv_indices = nullptr;
+  double* jv_data = nullptr;
+};
+struct NodalizeWork {
+  Workspace::Buf first, vflag, vpos, jcnt, jpos, flag, tmp, ci, cj, fr, phi, mu, mu2, jrp, jci, jcx;
+  int64_t* h_small = nullptr;  // pinned [2]
+};
+int nodalize_device(NodalizeWork& w, const NodalizeIn& in, cudaStream_t st, NodalizeOut& out, std::string& err,
+                    int64_t& launches);
+
 // ---- FEM scene-batch step pipeline (vfpi_fem.cu) ----------------------------
 void launch_fem_rhs(int64_t n, const int64_t* krp, const int* kc, const double* kv, const double* x, const double* X,
                     const double* v, const double* m, const double* g, double twodt, double* b, cudaStream_t st);

@@ -67,6 +67,8 @@ class Contact:
     phi_n: float = 0.0
     slot_j: tuple | None = None
     mu2: float | None = None
+    warm_impulse: np.ndarray | None = None
+    key: tuple | None = None  # provenance (first side, second side)
 
 
 @dataclass

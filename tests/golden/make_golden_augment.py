@@ -17,7 +17,9 @@ and stores its input (A_o CSC arrays, b_o, J_v CSR arrays, k_v) and output
   virtual nodes (a node's second contact, ``contacts.py:249-255``), J_v built
   the way ``nodalize`` builds it (COO of every block entry -> CSR);
 * ``aug_none``: no virtual node (A_o returned unchanged, explicit zeros kept);
-* ``metrics_ref.csv``: rows written by the reference's ``report_csv`` (harness.py:651-697).
+* ``metrics_ref.csv``: rows written by the reference's ``report_csv`` (harness.py:651-697);
+* ``nodalize_mixed``: the reference ``nodalize`` (contacts.py:271-321) on mixed
+  rigid / node / static sides with moving bodies and restitution.
 """
 
 from __future__ import annotations
@@ -146,5 +148,78 @@ def main():
     save("aug_none", a_o2, b_o2, None, 1e5, augment_dynamics(a_o2, b_o2, NodalContactSet([], 0, None, 1e5)))
 
 
+
+def nodalize_case(rng):
+    """Mixed raw contacts through the reference ``nodalize`` (contacts.py:271-321):
+    rigid-rigid, rigid-static, node-static, node-node, node-rigid, and nodes
+    carrying a second contact (identity virtual nodes); moving bodies and a
+    nonzero restitution so phi takes the v_n branch of stabilization_term."""
+    from condsim.contacts import StabilizationParams
+
+    n_rigid, n_part = 10, 14
+    bodies, q, v = [], [], []
+    qo = vo = 0
+    for k in range(n_rigid):
+        quat = rng.standard_normal(4)
+        quat /= np.linalg.norm(quat)
+        bodies.append(Body("rigid6", 1.0, qo, vo, np.eye(3)))
+        q += [rng.uniform(-1, 1, 3), quat]
+        v += [rng.standard_normal(6)]
+        qo += 7
+        vo += 6
+    for k in range(n_part):
+        bodies.append(Body("particle3", 0.1, qo, vo))
+        q += [rng.uniform(-1, 1, 3)]
+        v += [rng.standard_normal(3) * 0.05]
+        qo += 3
+        vo += 3
+    state = SystemState(np.concatenate(q), np.concatenate(v), 0, 1e-3)
+    node = lambda k: ("node", bodies[n_rigid + k].v_offset)  # noqa: E731
+    raw = []
+    for m in range(60):
+        kind = m % 5
+        if kind == 0:
+            i, j = rng.choice(n_rigid, 2, replace=False)
+            first, second = ("rigid", int(i), m), ("rigid", int(j), m)
+        elif kind == 1:
+            first, second = ("rigid", int(rng.integers(n_rigid)), m), ("static",)
+        elif kind == 2:
+            first, second = node(int(rng.integers(n_part))), ("static",)
+        elif kind == 3:
+            i, j = rng.choice(n_part, 2, replace=False)
+            first, second = node(int(i)), node(int(j))
+        else:
+            first, second = node(int(rng.integers(n_part))), ("rigid", int(rng.integers(n_rigid)), m)
+        nrm = rng.standard_normal(3)
+        if m % 7 == 0:
+            nrm = np.array([0.0, 0.0, 2.5])  # not unit: normalised inside contact_frame
+        raw.append(RawContact(point=rng.uniform(-1, 1, 3), normal=nrm, depth=float(abs(rng.normal(0, 1e-3))),
+                              first=first, second=second))
+    stab = StabilizationParams(beta_err=0.2, e_rest=0.3, dt=1e-3, v_rest_threshold=0.01)
+    nodal = nodalize(raw, state, bodies, 1e5, 0.45, 0.3, stab)
+    slot = lambda s: -1 if s is None else (s[1] if s[0] == "orig" else state.v.shape[0] + 3 * s[1])  # noqa: E731
+    kinds = {"node": 0, "rigid": 1, "static": -1}
+    jv = sp.csr_matrix(nodal.jv)
+    np.savez_compressed(
+        os.path.join(HERE, "nodalize_mixed.npz"),
+        q=state.q, v=state.v, body_q=np.array([b.q_offset for b in bodies], np.int32),
+        body_v=np.array([b.v_offset for b in bodies], np.int32),
+        first_kind=np.array([kinds[r.first[0]] for r in raw], np.int32),
+        first_ref=np.array([r.first[1] for r in raw], np.int32),
+        second_kind=np.array([kinds[r.second[0]] for r in raw], np.int32),
+        second_ref=np.array([r.second[1] if len(r.second) > 1 else -1 for r in raw], np.int32),
+        point=np.array([r.point for r in raw]), normal=np.array([r.normal for r in raw]),
+        depth=np.array([r.depth for r in raw]), k_v=1e5, mu=0.45, mu2=0.3, beta=0.2, e_rest=0.3, dt=1e-3,
+        thr=0.01, out_col_i=np.array([slot(c.slot_i) for c in nodal.contacts], np.int32),
+        out_col_j=np.array([slot(c.slot_j) for c in nodal.contacts], np.int32),
+        out_frames=np.array([c.frame for c in nodal.contacts]).reshape(-1),
+        out_phi=np.array([c.phi_n for c in nodal.contacts]), out_mu=np.array([c.mu for c in nodal.contacts]),
+        out_mu2=np.array([c.mu2 for c in nodal.contacts]), out_n_virtual=np.int64(nodal.n_virtual),
+        out_jv_indptr=jv.indptr.astype(np.int32), out_jv_indices=jv.indices.astype(np.int32),
+        out_jv_data=jv.data)
+    print("nodalize_mixed n_c", len(nodal.contacts), "n_virtual", nodal.n_virtual, "jv nnz", jv.nnz)
+
+
 if __name__ == "__main__":
     main()
+    nodalize_case(np.random.default_rng(5))

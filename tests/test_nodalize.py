@@ -1,0 +1,124 @@
+"""Nodalization (reference ``nodalize``, contacts.py:271-321): the oracle
+restatement against the reference's own output on mixed rigid / node / static
+sides (CPU), and the device nodalization ``vfpi_nodalize_device`` against the
+same golden (-m gpu) -- slots, virtual nodes, J_v (pattern, values, explicit
+zeros), frames and phi bit for bit."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import vfpi_oracle as O
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "nodalize_mixed.npz")
+
+
+def load():
+    return dict(np.load(GOLD))
+
+
+def _check(d, col_i, col_j, frames, phi, mu, mu2, jv, nv):
+    assert nv == int(d["out_n_virtual"])
+    assert np.array_equal(col_i, d["out_col_i"]) and np.array_equal(col_j, d["out_col_j"])
+    assert np.array_equal(np.asarray(frames).reshape(-1), d["out_frames"])
+    assert np.array_equal(phi, d["out_phi"])
+    assert np.array_equal(mu, d["out_mu"]) and np.array_equal(mu2, d["out_mu2"])
+    assert np.array_equal(jv.indptr, d["out_jv_indptr"]) and np.array_equal(jv.indices, d["out_jv_indices"])
+    assert np.array_equal(jv.data, d["out_jv_data"])
+    assert np.array_equal(np.signbit(jv.data), np.signbit(d["out_jv_data"]))
+
+
+def test_oracle_nodalize_matches_reference():
+    d = load()
+    out = O.nodalize(d["first_kind"], d["first_ref"], d["second_kind"], d["second_ref"], d["point"], d["normal"],
+                     d["depth"], d["q"], d["v"], d["body_q"], d["body_v"], d["v"].shape[0], float(d["mu"]),
+                     float(d["mu2"]), float(d["beta"]), float(d["dt"]), float(d["e_rest"]), float(d["thr"]))
+    _check(d, *out)
+
+
+def test_golden_exercises_every_side_kind():
+    d = load()
+    assert set(d["first_kind"].tolist()) == {0, 1} and set(d["second_kind"].tolist()) == {-1, 0, 1}
+    # more virtual nodes than rigid sides: some nodes carry a second contact
+    rigid_sides = int((d["first_kind"] == 1).sum() + (d["second_kind"] == 1).sum())
+    assert int(d["out_n_virtual"]) > rigid_sides
+    # restitution branch taken somewhere
+    assert not np.array_equal(d["out_phi"], -(float(d["beta"]) / float(d["dt"])) * d["depth"])
+
+
+@pytest.mark.gpu
+def test_device_nodalize_matches_reference():
+    from paper_2201_09212_b200.nodalize import nodalize_arrays
+
+    d = load()
+    out = nodalize_arrays(d["first_kind"], d["first_ref"], d["second_kind"], d["second_ref"], d["point"],
+                          d["normal"], d["depth"], d["q"], d["v"], d["body_q"], d["body_v"], float(d["mu"]),
+                          float(d["mu2"]), float(d["beta"]), float(d["dt"]), float(d["e_rest"]), float(d["thr"]))
+    _check(d, out["col_i"], out["col_j"], out["frames"], out["phi"], out["mu"], out["mu2"], out["jv"],
+           out["n_virtual"])
+
+
+def _raw_from_golden(d):
+    from collections import namedtuple
+
+    Raw = namedtuple("Raw", "point normal depth first second")
+    names = {0: "node", 1: "rigid", -1: "static"}
+    out = []
+    for m in range(d["first_kind"].shape[0]):
+        def side(kind, ref):
+            if kind == -1:
+                return ("static",)
+            return ("node", int(ref)) if kind == 0 else ("rigid", int(ref), m)
+        out.append(Raw(d["point"][m], d["normal"][m], float(d["depth"][m]), side(int(d["first_kind"][m]),
+                   d["first_ref"][m]), side(int(d["second_kind"][m]), d["second_ref"][m])))
+        assert names[int(d["first_kind"][m])] == out[-1].first[0]
+    return out
+
+
+@pytest.mark.gpu
+def test_device_chain_nodalize_augment_solve():
+    """Reference per-step restructuring on the device: nodalize (drop-in API,
+    reference objects in) -> augment_dynamics -> solve_vfpi, against the oracle
+    chain on the same inputs; bit-equal v and lam."""
+    from collections import namedtuple
+
+    import scipy.sparse as sp
+
+    from paper_2201_09212_b200.augment import augment_dynamics
+    from paper_2201_09212_b200.nodalize import nodalize
+    from paper_2201_09212_b200.solver import SolverConfig, solve_vfpi
+    from paper_2201_09212_b200.system import SparseSymmetric
+
+    d = load()
+    State = namedtuple("State", "q v dt")
+    BodyT = namedtuple("BodyT", "q_offset v_offset")
+    Stab = namedtuple("Stab", "beta_err e_rest v_rest_threshold dt")
+    bodies = [BodyT(int(a), int(b)) for a, b in zip(d["body_q"], d["body_v"])]
+    state = State(d["q"], d["v"], float(d["dt"]))
+    stab = Stab(float(d["beta"]), float(d["e_rest"]), float(d["thr"]), float(d["dt"]))
+    nodal = nodalize(_raw_from_golden(d), state, bodies, float(d["k_v"]), float(d["mu"]), float(d["mu2"]), stab)
+    assert nodal.n_virtual == int(d["out_n_virtual"])
+    assert np.array_equal(np.array([c.phi_n for c in nodal.contacts]), d["out_phi"])
+    n_o = d["v"].shape[0]
+    rng = np.random.default_rng(3)
+    blocks = []
+    for k in range(0, n_o, 3):
+        m = rng.standard_normal((3, 3))
+        blocks.append(m @ m.T + 3.0 * np.eye(3))
+    a_o = SparseSymmetric.from_scipy(sp.block_diag([sp.csc_matrix(bk) for bk in blocks], format="csc"))
+    b_o = rng.standard_normal(n_o)
+    aug = augment_dynamics(a_o, b_o, nodal)
+    cfg = SolverConfig(residual_tol=1e-10, max_iters=80)
+    v, lam, rep = solve_vfpi(aug, cfg, np.zeros(aug.n))
+    # oracle chain
+    oc = O.nodalize(d["first_kind"], d["first_ref"], d["second_kind"], d["second_ref"], d["point"], d["normal"],
+                    d["depth"], d["q"], d["v"], d["body_q"], d["body_v"], n_o, float(d["mu"]), float(d["mu2"]),
+                    float(d["beta"]), float(d["dt"]), float(d["e_rest"]), float(d["thr"]))
+    col_i, col_j, frames, phi, mu, mu2, jv, nv = oc
+    p, i, x, b = O.augment(n_o, a_o.indptr, a_o.indices, a_o.data, b_o, jv, float(d["k_v"]))
+    s = O.System(n_o + 3 * nv, p, i, x, b, col_i, col_j, frames, mu, mu2, phi)
+    vo, lo, ro = O.solve(s, O.Config(residual_tol=1e-10, max_iters=80), np.zeros(n_o + 3 * nv))
+    assert np.array_equal(aug.a.data, x) and np.array_equal(aug.a.indices, i)
+    assert rep.iterations == ro.iterations
+    assert np.array_equal(v, vo) and np.array_equal(lam, lo)
