@@ -122,3 +122,20 @@ def test_device_chain_nodalize_augment_solve():
     assert np.array_equal(aug.a.data, x) and np.array_equal(aug.a.indices, i)
     assert rep.iterations == ro.iterations
     assert np.array_equal(v, vo) and np.array_equal(lam, lo)
+
+
+@pytest.mark.gpu
+def test_device_nodalize_edge_cases():
+    """No contacts; a zero normal raises like contact_frame (contacts.py:139-140)."""
+    from paper_2201_09212_b200.errors import DeviceError
+    from paper_2201_09212_b200.nodalize import nodalize_arrays
+
+    d = load()
+    e = np.zeros(0, np.int32)
+    out = nodalize_arrays(e, e, e, e, np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0), d["q"], d["v"], d["body_q"],
+                          d["body_v"])
+    assert out["n_virtual"] == 0 and out["col_i"].size == 0 and out["jv"].shape == (0, d["v"].shape[0])
+    with pytest.raises((ValueError, DeviceError)):
+        nodalize_arrays(np.array([0], np.int32), np.array([0], np.int32), np.array([-1], np.int32),
+                        np.array([-1], np.int32), np.zeros((1, 3)), np.zeros((1, 3)), np.zeros(1), d["q"], d["v"],
+                        d["body_q"], d["body_v"])
