@@ -220,9 +220,12 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   double* vown2 = reinterpret_cast<double*>(smraw + Lo.o_v1);  // own rows of v^(l)
   int* cm = reinterpret_cast<int*>(smraw + Lo.o_cm);
   int* cq = reinterpret_cast<int*>(smraw + Lo.o_cq);
-  double* cfr = reinterpret_cast<double*>(smraw + Lo.o_fr);
-  double* cpar = reinterpret_cast<double*>(smraw + Lo.o_par);  // mu, mu2, phi, gamma
-  double* lam_s = reinterpret_cast<double*>(smraw + Lo.o_lam); // [2][3C]
+  // contact data component-major ([t][C]): the lane that owns contact k reads
+  // consecutive words with its neighbours (no bank conflicts; a [k][t] layout
+  // strides 72 B / 32 B / 24 B across lanes)
+  double* cfr = reinterpret_cast<double*>(smraw + Lo.o_fr);    // [9][C]
+  double* cpar = reinterpret_cast<double*>(smraw + Lo.o_par);  // [4][C]: mu, mu2, phi, gamma
+  double* lam_s = reinterpret_cast<double*>(smraw + Lo.o_lam); // [2][3][C]
   double* jt_s = reinterpret_cast<double*>(smraw + Lo.o_jt);   // [CR]
   unsigned* counter = reinterpret_cast<unsigned*>(p.bar_flags);
 
@@ -246,11 +249,11 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     cm[k] = m;
     cq[k] = __ldg(p.cont_q + c0 + k) | (__ldg(p.col_j + m) >= 0 ? (1 << 30) : 0);
 #pragma unroll
-    for (int t = 0; t < 9; ++t) cfr[9 * k + t] = __ldg(p.frames + 9 * (size_t)m + t);
-    cpar[4 * k + 0] = __ldg(p.mu + m);
-    cpar[4 * k + 1] = __ldg(p.mu2 + m);
-    cpar[4 * k + 2] = __ldg(p.phi + m);
-    cpar[4 * k + 3] = __ldg(p.gamma + m);
+    for (int t = 0; t < 9; ++t) cfr[t * C + k] = __ldg(p.frames + 9 * (size_t)m + t);
+    cpar[0 * C + k] = __ldg(p.mu + m);
+    cpar[1 * C + k] = __ldg(p.mu2 + m);
+    cpar[2 * C + k] = __ldg(p.phi + m);
+    cpar[3 * C + k] = __ldg(p.gamma + m);
   }
   for (int t = tid; t < 6 * C; t += T) lam_s[t] = 0.0;
   for (int t = tid; t < CR; t += T) jt_s[t] = 0.0;
@@ -464,18 +467,20 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         if (profl) { __syncwarp(); if (lane == 0) atomicMax(&sm_role_end[2], (unsigned long long)clock64()); }
         if (!act || !HASC || check_only) continue;
         // (2) gather + (3) one-shot projection (solver.py:262-281)
-        const double* R9 = cfr + 9 * k;
+        double R9[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) R9[t] = cfr[t * C + k];
         double rel[3], eta[3], lam[3], wv[3];
 #pragma unroll
         for (int t = 0; t < 3; ++t) rel[t] = dj ? dsub(vsr[t], vsr[3 + t]) : vsr[t];
         frame_apply(R9, rel, eta);
         double g;
         if (use_alpha) g = dj ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
-        else g = cpar[4 * k + 3];
-        trial_impulse(eta, cpar[4 * k + 2], g, lam);
-        project(OP, lam, cpar[4 * k + 0], cpar[4 * k + 1]);
+        else g = cpar[3 * C + k];
+        trial_impulse(eta, cpar[2 * C + k], g, lam);
+        project(OP, lam, cpar[0 * C + k], cpar[1 * C + k]);
 #pragma unroll
-        for (int t = 0; t < 3; ++t) lam_out[3 * k + t] = lam[t];
+        for (int t = 0; t < 3; ++t) lam_out[t * C + k] = lam[t];
         // (2') scatter J_c^T lam and v_new = v* + w J_c^T lam
         frame_apply_t(R9, lam, wv);
 #pragma unroll
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   for (int k = tid; k < C; k += T) {
     const int m = cm[k];
 #pragma unroll
-    for (int t = 0; t < 3; ++t) p.out_lam[3 * (size_t)m + t] = lfin[3 * k + t];
+    for (int t = 0; t < 3; ++t) p.out_lam[3 * (size_t)m + t] = lfin[t * C + k];
   }
   if (b == 0 && tid == 0) {
     p.status->iterations = iters;

@@ -14,3 +14,4 @@ for i in 1 2; do
 for lib in paper_2201_09212_b200/libvfpi.so exp/libvfpi_oldres.so; do
   echo "== $lib"; VFPI_LIB=$lib timeout 200 python /tmp/ab.py 2>&1 | tail -1
 done; done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py -q -x 2>&1 | tail -2
