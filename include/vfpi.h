@@ -274,6 +274,18 @@ int vfpi_augment(vfpi_handle* h, const vfpi_augment_input* in, vfpi_augmented* o
 int vfpi_fem_rhs_device(vfpi_handle* h, int64_t n, const int64_t* k_indptr, const int32_t* k_indices,
                         const double* k_data, const double* x, const double* X, const double* v, const double* m,
                         const double* g, double dt, double* b, void* stream);
+/* The same right-hand side with K packed once as SELL-32 (slices of 32 rows,
+ * entry k of row r at slice_off[r/32] + 32 k + r%32, padding column -1):
+ * coalesced streaming of K, identical bits. vfpi_sell_layout_device fills
+ * slice_off [ceil(n/32)+1] and returns the element count; the caller
+ * allocates sell_val/sell_col and calls vfpi_sell_pack_device. */
+int vfpi_sell_layout_device(vfpi_handle* h, int64_t n, const int64_t* k_indptr, int64_t* slice_off,
+                            int64_t* elems);
+int vfpi_sell_pack_device(vfpi_handle* h, int64_t n, const int64_t* k_indptr, const int32_t* k_indices,
+                          const double* k_data, const int64_t* slice_off, double* sell_val, int32_t* sell_col);
+int vfpi_fem_rhs_sell_device(vfpi_handle* h, int64_t n, const int64_t* slice_off, const double* sell_val,
+                             const int32_t* sell_col, const double* x, const double* X, const double* v,
+                             const double* m, const double* g, double dt, double* b, void* stream);
 /* y = J x, J in CSR (scipy csr_matvec order): the warm start's virtual-node
  * extension v0[n_o:] = J_v v0[:n_o] (harness._warm_velocity, harness.py:502-512). */
 int vfpi_csr_matvec_device(vfpi_handle* h, int64_t rows, const int32_t* indptr, const int32_t* indices,

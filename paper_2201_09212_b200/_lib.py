@@ -139,6 +139,13 @@ def lib() -> C.CDLL:
                 "vfpi_pile_contacts_device": (C.c_int, [H, C.POINTER(VfpiPileGeometry), C.c_void_p, C.c_void_p,
                                                         C.POINTER(VfpiPileContacts), C.c_void_p]),
                 "vfpi_memcpy_d2d": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+                "vfpi_sell_layout_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p,
+                                                      C.POINTER(C.c_int64)]),
+                "vfpi_sell_pack_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                    C.c_void_p, C.c_void_p]),
+                "vfpi_fem_rhs_sell_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                                       C.c_void_p, C.c_void_p]),
                 "vfpi_nodalize_device": (C.c_int, [H, C.POINTER(VfpiNodalizeInput), C.POINTER(VfpiNodalContacts),
                                                    C.c_void_p]),
                 "vfpi_advance_device": (C.c_int, [H, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -1474,3 +1474,45 @@ int vfpi_nodalize_device(vfpi_handle* h, const vfpi_nodalize_input* in, vfpi_nod
   out->jv_data = o.jv_data;
   return VFPI_OK;
 }
+
+// ---- SELL-32 packing of a CSR matrix (step-pipeline right-hand sides) -------
+int vfpi_sell_layout_device(vfpi_handle* h, int64_t n, const int64_t* k_indptr, int64_t* slice_off,
+                            int64_t* elems) {
+  if (!h || n < 0 || !elems) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = h->ws.stream;
+  const int64_t nsl = (n + 31) / 32;
+  CK(vfpi::ensure(h->ws.y, 8 * (size_t)(nsl + 1)));
+  vfpi::launch_fem_sell_width(n, k_indptr, P<int64_t>(h->ws.y), st);
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, P<int64_t>(h->ws.y), slice_off, (int)(nsl + 1), st));
+  CK(vfpi::ensure(h->ws.cub_tmp, tb));
+  CK(cub::DeviceScan::ExclusiveSum(h->ws.cub_tmp.p, tb, P<int64_t>(h->ws.y), slice_off, (int)(nsl + 1), st));
+  CK(cudaMemcpyAsync(elems, slice_off + nsl, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->launches += 2;
+  return VFPI_OK;
+}
+
+int vfpi_sell_pack_device(vfpi_handle* h, int64_t n, const int64_t* k_indptr, const int32_t* k_indices,
+                          const double* k_data, const int64_t* slice_off, double* sell_val, int32_t* sell_col) {
+  if (!h || n < 0) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = h->ws.stream;
+  vfpi::launch_fem_sell_pack(n, k_indptr, k_indices, k_data, slice_off, sell_val, sell_col, st);
+  CK(cudaStreamSynchronize(st));
+  h->launches += n > 0;
+  return VFPI_OK;
+}
+
+int vfpi_fem_rhs_sell_device(vfpi_handle* h, int64_t n, const int64_t* slice_off, const double* sell_val,
+                             const int32_t* sell_col, const double* x, const double* X, const double* v,
+                             const double* m, const double* g, double dt, double* b, void* stream) {
+  if (!h || n < 0) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::launch_fem_rhs_sell(n, slice_off, sell_val, sell_col, x, X, v, m, g, 2.0 / dt, b, st);
+  h->launches += n > 0;
+  CK(cudaGetLastError());
+  return VFPI_OK;
+}

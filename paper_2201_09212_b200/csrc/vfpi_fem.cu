@@ -65,13 +65,31 @@ __global__ void k_fem_rhs_sell(int64_t n, const int64_t* __restrict__ off, const
   if (i >= n) return;
   const int64_t o = off[i >> 5] + (i & 31);
   const int W = (int)((off[(i >> 5) + 1] - off[i >> 5]) >> 5);
+  // row operands first, then the K row in batches of 8 independent loads
+  // (same sequential accumulation order)
+  const double mi = m[i], vi = v[i], gi = g[i];
   double ku = 0.0;
-  for (int k = 0; k < W; ++k) {
-    const int j = __ldcs(sc + o + 32 * (int64_t)k);
-    if (j >= 0) ku = dadd(ku, dmul(__ldcs(sv + o + 32 * (int64_t)k), dsub(x[j], X[j])));
+  int k = 0;
+  for (; k + 8 <= W; k += 8) {
+    int j[8];
+    double a[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      j[u] = __ldcs(sc + o + 32 * (int64_t)(k + u));
+      a[u] = __ldcs(sv + o + 32 * (int64_t)(k + u));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = j[u] >= 0 ? dsub(x[j[u]], X[j[u]]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j[u] >= 0) ku = dadd(ku, dmul(a[u], xv[u]));
   }
-  const double t1 = dmul(dmul(twodt, m[i]), v[i]);
-  b[i] = dadd(dsub(t1, ku), dmul(m[i], g[i]));
+  for (; k < W; ++k) {
+    const int jj = __ldcs(sc + o + 32 * (int64_t)k);
+    if (jj >= 0) ku = dadd(ku, dmul(__ldcs(sv + o + 32 * (int64_t)k), dsub(x[jj], X[jj])));
+  }
+  const double t1 = dmul(dmul(twodt, mi), vi);
+  b[i] = dadd(dsub(t1, ku), dmul(mi, gi));
 }
 
 // node below the margin of the plane z = 0 (FemCube.contacts)

@@ -346,7 +346,8 @@ class PileStepper:
 
     Per step, on the device: contact detection + nodalization
     (``vfpi_pile_contacts_device``; ``detect="host"`` runs ``CubePile.detect`` /
-    ``nodalize`` on a copy of (x, v) instead), b (``vfpi_fem_rhs_device``),
+    ``nodalize`` on a copy of (x, v) instead), b (``vfpi_fem_rhs_sell_device``,
+    K packed once as SELL-32),
     the augmented matrix (``vfpi_augment_device``), the warm start
     (``vfpi_csr_matvec_device``, ``harness._warm_velocity``), the V-FPI solve
     (``vfpi_solve_device``) and the midpoint integration (``vfpi_advance_device``).
@@ -363,6 +364,22 @@ class PileStepper:
         up = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.dev)  # noqa: E731
         self.a = (up(pile.a_indptr, np.int32), up(pile.a_indices, np.int32), up(pile.a_data, np.float64))
         self.k = (up(pile.k_indptr, np.int64), up(pile.k_indices, np.int32), up(pile.k_data, np.float64))
+        # K packed once as SELL-32 for the per-step right-hand side (coalesced stream)
+        import ctypes as C
+
+        from .solver import _raise_for
+
+        nsl = (pile.n + 31) // 32
+        self.k_off = torch.empty(nsl + 1, dtype=torch.int64, device=self.dev)
+        elems = C.c_int64(0)
+        _raise_for(self.h.L.vfpi_sell_layout_device(self.h.h, pile.n, self.k[0].data_ptr(), self.k_off.data_ptr(),
+                                                    C.byref(elems)), self.h)
+        self.k_val = torch.empty(max(elems.value, 1), dtype=torch.float64, device=self.dev)
+        self.k_col = torch.empty(max(elems.value, 1), dtype=torch.int32, device=self.dev)
+        _raise_for(self.h.L.vfpi_sell_pack_device(self.h.h, pile.n, self.k[0].data_ptr(), self.k[1].data_ptr(),
+                                                  self.k[2].data_ptr(), self.k_off.data_ptr(),
+                                                  self.k_val.data_ptr(), self.k_col.data_ptr()), self.h)
+        self.k = None  # the CSR copy is no longer needed on the device
         self.m, self.g = up(pile.m, np.float64), up(pile.gravity, np.float64)
         self.X = up(pile.X.ravel(), np.float64)
         self.x = up(pile.x.ravel(), np.float64)
@@ -463,8 +480,8 @@ class PileStepper:
         t_detect = time.perf_counter() - t0
         n = n_o + nv3
         b = torch.zeros(n, dtype=torch.float64, device=dev)
-        _raise_for(h.L.vfpi_fem_rhs_device(h.h, n_o, P(self.k[0]), P(self.k[1]), P(self.k[2]), P(self.x), P(self.X),
-                                           P(self.v), P(self.m), P(self.g), pile.dt, P(b), sp_), h)
+        _raise_for(h.L.vfpi_fem_rhs_sell_device(h.h, n_o, P(self.k_off), P(self.k_val), P(self.k_col), P(self.x),
+                                                P(self.X), P(self.v), P(self.m), P(self.g), pile.dt, P(b), sp_), h)
         inp = VfpiAugmentInput(n_o, nv3, int(pile.a_data.shape[0]), C.cast(P(self.a[0]), i32),
                                C.cast(P(self.a[1]), i32), C.cast(P(self.a[2]), f64), jnnz, jp_, ji_, jx_,
                                float(pile.k_v))
