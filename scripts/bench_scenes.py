@@ -22,6 +22,47 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+def _cpu_scene(args):
+    """One configs[2] scene stepped on the host with the oracle solver (CPU baseline worker)."""
+    E, drop, yaw, nx, steps = args
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import vfpi_oracle as O  # CPU baseline only
+    from paper_2201_09212_b200.scenes import FemCube
+
+    cube = FemCube(nx=nx, E=E, drop=drop, yaw=yaw)
+    prev = None
+    ci = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ps = cube.system()
+        s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64), ps.col_j.astype(np.int64),
+                     ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
+        v, lam, rep = O.solve(s, O.Config(residual_tol=1e-8, max_iters=500), np.zeros(ps.n) if prev is None else prev)
+        ci += ps.n_c * rep.iterations
+        cube.advance(v)
+        prev = v
+    return ci, time.perf_counter() - t0
+
+
+def cpu_baseline(E, drop, yaw, nx, steps):
+    """a process pool of P = len(sched_getaffinity) workers, one scene
+    per task; the sample is the first P scenes of the batch, all their steps."""
+    import multiprocessing as mp
+
+    P = len(os.sched_getaffinity(0))
+    work = [(float(E[k]), float(drop[k]), float(yaw[k]), nx, steps) for k in range(min(P, len(E)))]
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(P) as pool:
+        res = pool.map(_cpu_scene, work)
+    wall = time.perf_counter() - t0
+    ci = sum(r[0] for r in res)
+    return {"value": ci / wall, "unit": "contact-iter/s", "cores": P, "kind": "port",
+            "scene_steps_per_s": len(work) * steps / wall, "wall_s": wall,
+            "sample": f"the first {len(work)} scenes x {steps} steps, one process per core (host FemCube assembly + "
+                      "numpy/scipy oracle restating solve_vfpi), pool start-up included"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scenes", type=int, default=1024)
@@ -29,6 +70,7 @@ def main():
     ap.add_argument("--nx", type=int, default=10)
     ap.add_argument("--seed", type=int, default=2022)
     ap.add_argument("--chebyshev", action="store_true")
+    ap.add_argument("--cpu-baseline", action="store_true", help="time the host CPU path on a bounded sample")
     ap.add_argument("--solve-only-steps", type=int, default=0,
                     help="time only the last K steps (earlier steps still run)")
     ap.add_argument("--host-pipeline", action="store_true",
@@ -148,6 +190,12 @@ def device_pipeline(args, cubes, cfg, t_build, rank, world, dist, torch):
                 "wall_s": wall_max, "mean_iters": it_all / (args.scenes * args.steps), "contact_iterations": ci_all,
                 "host_build_s": t_build, "chebyshev": args.chebyshev,
                 "scaling": "strong (fixed scene count split over ranks)"}
+        if args.cpu_baseline and world == 1:
+            g = np.random.default_rng(args.seed)
+            E = g.uniform(5e4, 2e5, args.scenes)
+            drop = g.uniform(0.02, 0.1, args.scenes)
+            yaw = g.uniform(0, 2 * np.pi, args.scenes)
+            line["cpu_baseline"] = cpu_baseline(E, drop, yaw, args.nx, args.steps)
         print(json.dumps(line), flush=True)
     for fb in chunks:
         fb.close()
