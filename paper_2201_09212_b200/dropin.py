@@ -6,14 +6,19 @@
     dropin.install()          # condsim.solve_vfpi & friends now run on the GPU
 
 ``solve_vfpi`` is imported *by name* in ``condsim.harness`` (harness.py:47)
-and re-exported from ``condsim/__init__.py:18``, so every alias is patched.
+and re-exported from ``condsim/__init__.py:18``, so every alias is patched;
+``nodalize`` and ``augment_dynamics`` (imported by name in the harness,
+harness.py:22-31) are patched too, so a harness step's contact restructuring
+runs on the GPU as well.
 """
 
 from __future__ import annotations
 
 import sys
 
+from . import augment as _augment
 from . import contacts as _contacts
+from . import nodalize as _nodalize
 from . import solver as _solver
 from . import sparse as _sparse
 
@@ -30,9 +35,12 @@ _PATCH = {
         "spmv": _sparse.spmv,
         "row_norms_sq": _sparse.row_norms_sq,
     },
-    "condsim.harness": {"solve_vfpi": _solver.solve_vfpi},
+    # harness.run's per-step restructuring (harness.py:545-546) and solve (:557)
+    "condsim.harness": {"solve_vfpi": _solver.solve_vfpi, "nodalize": _nodalize.nodalize,
+                        "augment_dynamics": _augment.augment_dynamics},
     "condsim": {"solve_vfpi": _solver.solve_vfpi},
-    "condsim.contacts": {"apply_jc": _contacts.apply_jc, "apply_jc_t": _contacts.apply_jc_t},
+    "condsim.contacts": {"apply_jc": _contacts.apply_jc, "apply_jc_t": _contacts.apply_jc_t,
+                         "nodalize": _nodalize.nodalize, "augment_dynamics": _augment.augment_dynamics},
     "condsim.sparse": {"spmv": _sparse.spmv, "row_norms_sq": _sparse.row_norms_sq},
 }
 
