@@ -3,6 +3,8 @@ few iterations only, so the whole file takes about two minutes):
 
 * configs[3]: the 64^3-node heightfield block (786,432 DOF, 24.6M entries,
   4,096 contacts), 4 plain V-FPI iterations, GPU == oracle bit for bit;
+* configs[2]: a 1024-scene batch in contact, every distinct scene bit-equal
+  to its oracle solve (iterations, v, lam);
 * configs[4]: the 8x8x4 pile of 16^3-node cubes stacked in contact
   (3.1M DOF + 43k virtual nodes, 82M entries, 60k contacts): device
   detection/nodalization == host restatement, device augmentation == the
@@ -57,3 +59,32 @@ def test_cfg4_full_size_pipeline_bitwise():
     vo, lo, ro = _oracle_solve(ps, 2)
     assert rep.iterations == ro.iterations == 2
     assert np.array_equal(v, vo) and np.array_equal(lam, lo)
+
+
+@pytest.mark.gpu
+def test_cfg2_full_batch_bitwise():
+    """configs[2]: a batch of 1024 FEM scenes (16 distinct cubes pressed into
+    the plane and moving down, replicated) in one scene-batch solve; every
+    distinct scene equals its oracle solve bit for bit with the same iteration
+    count, and every replica equals its class."""
+    from paper_2201_09212_b200.batch import solve_scenes
+    from paper_2201_09212_b200.scenes import FemCube
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    g = np.random.default_rng(7)
+    base = []
+    for _ in range(16):
+        c = FemCube(E=float(g.uniform(5e4, 2e5)), drop=0.0, yaw=float(g.uniform(0, 2 * np.pi)))
+        c.x = c.X.copy()
+        c.x[:, 2] -= 5e-4
+        c.v[:, 2] = -0.3
+        base.append(c.system())
+    scenes = [base[k % 16] for k in range(1024)]
+    res, rep = solve_scenes(scenes, SolverConfig(residual_tol=1e-8, max_iters=500))
+    for k in range(16):
+        vo, lo, ro = _oracle_solve(base[k], 500)
+        v, lam, r = res[k]
+        assert r.iterations == ro.iterations and r.converged == ro.converged, k
+        assert np.array_equal(v, vo) and np.array_equal(lam, lo), k
+    for k in range(16, 1024):
+        assert np.array_equal(res[k][0], res[k % 16][0]) and res[k][2].iterations == res[k % 16][2].iterations
