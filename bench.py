@@ -130,6 +130,17 @@ def cpu_oracle_solve(ps, max_iters):
     return ps.n_c * rep.iterations, dt, rep.iterations
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -170,7 +181,7 @@ def run_reference(args):
         "config": {"workload": "configs[1] rigid-body contact system", "bodies": N_BODIES, "contacts": N_CONTACTS,
                    "n": ps.n, "k_v": KV, "operator": "strict", "chebyshev": False, "tol": TOL,
                    "sample_iters_per_step": sample_iters},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{sample_iters} V-FPI iterations of the full configs[1] system per step, the "
                                    f"per-solve setup ({setup:.3f} s, measured in warm-up) amortised over "
                                    f"{MAX_ITERS} iterations (numpy/scipy oracle restating "
@@ -313,7 +324,7 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         ci, dt, it = cpu_oracle_solve(ps, args.cpu_iters)
-        cpu = {"value": ci / dt, "unit": UNIT, "cores": 1, "kind": "port",
+        cpu = {"value": ci / dt, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"one solve of the full configs[1] system capped at {it} iterations "
                          "(numpy/scipy oracle restating condsim.solver.solve_vfpi, setup included)"}
     clocks = sampler.summary()
