@@ -126,21 +126,28 @@ __device__ __forceinline__ void warp0_collect(const double* part, int off, int G
 
 // sequential (scipy-order) dot of one row with x: SELL element i = base + 32k,
 // x from the staged sectors or from the CTA's own rows
+#ifndef VFPI_ROW_UNROLL
+#define VFPI_ROW_UNROLL 8  // free rows: 8 entries' loads in flight (measured best of 2/4/8/16)
+#endif
+#ifndef VFPI_ROW3_UNROLL
+#define VFPI_ROW3_UNROLL 4
+#endif
 __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const unsigned* __restrict__ mp, int base,
                                           int len, const double* __restrict__ xs) {
+  constexpr int U = VFPI_ROW_UNROLL;
   double acc = 0.0;
   int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    double a[4], x[4];
+  for (; k + U <= len; k += U) {
+    double a[U], x[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int i = base + 32 * (k + u);
       const unsigned m = mp[i];
       a[u] = sv[i];
       x[u] = xs[m];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc = dadd(acc, dmul(a[u], x[u]));
+    for (int u = 0; u < U; ++u) acc = dadd(acc, dmul(a[u], x[u]));
   }
   for (; k < len; ++k) {
     const int i = base + 32 * k;
@@ -165,11 +172,11 @@ __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const un
   double acc[3] = {0.0, 0.0, 0.0};
   // branch-free: every lane loads (a row past its end re-reads its last
   // element) and only adds while k < len, so the three chains interleave
-  for (int k = 0; k < L; k += 4) {  // 12 independent loads per step (rows of <= 4 entries: one step)
-    double pr[4][3];
-    bool ok[4][3];
+  for (int k = 0; k < L; k += VFPI_ROW3_UNROLL) {  // 12 independent loads per step (rows of <= 4 entries: one step)
+    double pr[VFPI_ROW3_UNROLL][3];
+    bool ok[VFPI_ROW3_UNROLL][3];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < VFPI_ROW3_UNROLL; ++u)
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const int kk = k + u;
@@ -179,7 +186,7 @@ __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const un
         pr[u][a] = dmul(sv[i], xs[m]);
       }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < VFPI_ROW3_UNROLL; ++u)
 #pragma unroll
       for (int a = 0; a < 3; ++a) acc[a] = ok[u][a] ? dadd(acc[a], pr[u][a]) : acc[a];
   }
