@@ -167,7 +167,7 @@ int iterate_max_blocks_per_sm(int op, bool cheb, bool bb, int smem_bytes, bool s
 int launch_iterate_resident(const IterParams& p, int op, bool cheb, bool bb, size_t smem_bytes, cudaStream_t st,
                             std::string& err);
 #ifndef VFPI_RES_THREADS
-#define VFPI_RES_THREADS 512
+#define VFPI_RES_THREADS 480  // 15 warps: measured best of 384-1024 with the 8-deep free-row sums
 #endif
 constexpr int kResThreads = VFPI_RES_THREADS;
 int launch_scc_final(const IterParams& p, double* scc, cudaStream_t st);
