@@ -190,7 +190,8 @@ int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
 /* Tuning knobs. key 0: force the resident kernel's contact-warp count (0 = auto);
  * key 1: order units by their smallest referenced column (default 1; 0 = row order);
  * key 2: sort each CTA's free rows by decreasing length (default 1);
- * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0). */
+ * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0; the
+ * shared-memory-resident layout uses row cost 20 unless key 4 sets both). */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

@@ -315,7 +315,10 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (key == 1) { h->layout_opt.anchor_order = value != 0; return VFPI_OK; }
   if (key == 2) { h->layout_opt.length_sort = value != 0; return VFPI_OK; }
   if (key == 3 && value > 0) { h->layout_opt.entry_cost = value; return VFPI_OK; }
-  if (key == 4 && value > 0) { h->layout_opt.row_cost = value; return VFPI_OK; }
+  if (key == 4 && value > 0) {
+    h->layout_opt.row_cost = h->layout_opt.res_row_cost = value;
+    return VFPI_OK;
+  }
   if (key == 5 && value >= 0) { h->layout_opt.contact_cost = value; return VFPI_OK; }
   return VFPI_BAD_ARGUMENT;
 }
@@ -381,12 +384,14 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   int G = choose_blocks_resident(*d, ws.num_sms);
   {
     std::vector<uint64_t> key = system_key(*d, G);
-    const vfpi::LayoutOptions& o = h->layout_opt;
+    vfpi::LayoutOptions res_opt = h->layout_opt;
+    res_opt.row_cost = res_opt.res_row_cost;
+    const vfpi::LayoutOptions& o = res_opt;
     for (uint64_t x : {(uint64_t)o.anchor_order, (uint64_t)o.length_sort, (uint64_t)o.entry_cost,
                        (uint64_t)o.row_cost, (uint64_t)o.contact_cost})
       key.push_back(x);
     rc = run_setup_phase(h, h->graph_layout, key, st, [&] {
-      return vfpi::setup_layout_async(ws, *d, G, st, h->err, h->launches, h->layout_opt);
+      return vfpi::setup_layout_async(ws, *d, G, st, h->err, h->launches, res_opt);
     });
     if (rc) return rc;
     rc = vfpi::setup_layout_finish(ws, st, hs, h->err);

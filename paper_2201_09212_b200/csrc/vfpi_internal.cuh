@@ -135,6 +135,7 @@ struct LayoutOptions {
   bool anchor_order = true;   // order units by their smallest referenced column
   bool length_sort = true;    // free rows of a CTA by decreasing length
   int entry_cost = 24, row_cost = 40, contact_cost = 0;  // partition cost model
+  int res_row_cost = 20;  // row cost of the shared-memory-resident attempt (configs[1]: best of 0-80)
   // scene batches: CTA b = scene b (device arrays, G+1 entries each); contacts
   // must be grouped by scene and never couple two scenes
   const int* scene_row_ptr = nullptr;
