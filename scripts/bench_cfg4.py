@@ -14,7 +14,7 @@ node mass term (2/dt) m is about 1, k_v = 1e5 makes the non-converged
 V-FPI impulses pump energy into the pile until the mesh tears; 1e3 already
 does so at this resolution, 1e2 stays bounded -- scripts/pile_trace.py).
 
-usage: python scripts/bench_cfg4.py [--steps 120] [--kv 100] [--scenes 1] [--max-iters 500] [--cpu-iters 2]
+usage: python scripts/bench_cfg4.py [--steps 400] [--kv 100] [--scenes 1] [--max-iters 500] [--cpu-iters 2]
        [--nodes 16] [--cubes 8 8 4]
 Under torchrun the scenes shard across ranks (contiguous blocks, no data-path
 collective; counters all-reduced and the wall time max-reduced at the end)."""
@@ -35,7 +35,7 @@ def b_iter(n, nnz_num, n_c):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=120)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--scenes", type=int, default=1)
     ap.add_argument("--max-iters", type=int, default=500)
     ap.add_argument("--cpu-iters", type=int, default=2)

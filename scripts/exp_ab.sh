@@ -10,6 +10,6 @@ best = min(solve_packed(ps, cfg, np.zeros(ps.n))[2].timings["loop_s"] for _ in r
 print("loop %.3f ms" % (best * 1e3))
 PY
 for i in 1 2; do
-for lib in exp/libvfpi_t448.so exp/libvfpi_t384.so exp/libvfpi_t416.so exp/libvfpi_t480.so; do
+for lib in exp/libvfpi_ru8.so exp/libvfpi_ru6.so exp/libvfpi_ru10.so exp/libvfpi_ru12.so; do
   echo "== $lib"; VFPI_LIB=$lib timeout 200 python /tmp/ab.py 2>&1 | tail -1
 done; done
