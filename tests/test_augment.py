@@ -97,3 +97,30 @@ def test_device_augment_configs1_size():
     assert np.array_equal(host.indptr, dev.indptr)
     assert np.array_equal(host.indices, dev.indices)
     assert np.array_equal(host.data, dev.data)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_device_augment_random_systems(seed):
+    """Random A_o (explicit zeros included) and random J_v (random widths, exact
+    zeros, exact cancellations, duplicate COO entries summed by the shim) --
+    device augmentation == the reference expression, bit for bit."""
+    from paper_2201_09212_b200.augment import augment_arrays
+
+    g = np.random.default_rng(1000 + seed)
+    n_o = int(g.integers(6, 90))
+    a = sp.random(n_o, n_o, density=float(g.uniform(0.05, 0.4)), random_state=g, format="csc")
+    a = (a + a.T + sp.identity(n_o)).tocsc()
+    if seed % 3 == 0:  # explicit zeros in A_o
+        a.data[g.random(a.nnz) < 0.2] = 0.0
+    a.sort_indices()
+    rows = int(g.integers(1, 30)) * 3
+    nnz = int(g.integers(1, rows * 6))
+    r = g.integers(0, rows, nnz)
+    c = g.integers(0, n_o, nnz)
+    v = np.where(g.random(nnz) < 0.2, 0.0, np.round(g.standard_normal(nnz) * 4) / 4)  # exact sums and zeros
+    jv = sp.csr_matrix((v, (r, c)), shape=(rows, n_o))  # duplicates summed here, like nodalize's COO -> CSR
+    kv = float(g.choice([1e5, 1e2, 3.0]))
+    p, i, x = augment_arrays(n_o, a.indptr, a.indices, a.data, jv, kv)
+    po, io, xo, _ = O.augment(n_o, a.indptr, a.indices, a.data, np.zeros(n_o), jv, kv)
+    assert np.array_equal(p, po) and np.array_equal(i, io) and np.array_equal(x, xo)

@@ -139,3 +139,52 @@ def test_device_nodalize_edge_cases():
         nodalize_arrays(np.array([0], np.int32), np.array([0], np.int32), np.array([-1], np.int32),
                         np.array([-1], np.int32), np.zeros((1, 3)), np.zeros((1, 3)), np.zeros(1), d["q"], d["v"],
                         d["body_q"], d["body_v"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(8))
+def test_device_nodalize_random_contacts(seed):
+    """Random raw contact sets (every side kind, repeated nodes, moving bodies,
+    restitution on) -- device nodalization == the oracle restatement bit for bit."""
+    from paper_2201_09212_b200.nodalize import nodalize_arrays
+
+    g = np.random.default_rng(500 + seed)
+    n_rigid, n_part = int(g.integers(1, 8)), int(g.integers(2, 12))
+    body_q, body_v, q, v = [], [], [], []
+    qo = vo = 0
+    for _ in range(n_rigid):
+        body_q.append(qo)
+        body_v.append(vo)
+        quat = g.standard_normal(4)
+        q += list(g.uniform(-1, 1, 3)) + list(quat / np.linalg.norm(quat))
+        v += list(g.standard_normal(6))
+        qo += 7
+        vo += 6
+    for _ in range(n_part):
+        body_q.append(qo)
+        body_v.append(vo)
+        q += list(g.uniform(-1, 1, 3))
+        v += list(g.standard_normal(3) * 0.1)
+        qo += 3
+        vo += 3
+    q, v = np.array(q), np.array(v)
+    n_c = int(g.integers(1, 50))
+    fk = g.integers(0, 2, n_c).astype(np.int32)
+    sk = g.integers(-1, 2, n_c).astype(np.int32)
+    fr = np.where(fk == 0, [body_v[n_rigid + int(g.integers(n_part))] for _ in range(n_c)],
+                  g.integers(0, n_rigid, n_c)).astype(np.int32)
+    sr = np.where(sk == 0, [body_v[n_rigid + int(g.integers(n_part))] for _ in range(n_c)],
+                  np.where(sk == 1, g.integers(0, n_rigid, n_c), -1)).astype(np.int32)
+    pt = g.uniform(-1, 1, (n_c, 3))
+    nrm = g.standard_normal((n_c, 3)) * g.choice([1.0, 3.0], (n_c, 1))
+    depth = np.abs(g.normal(0, 1e-3, n_c))
+    args = (fk, fr, sk, sr, pt, nrm, depth, q, v, np.array(body_q, np.int32), np.array(body_v, np.int32))
+    prm = (0.4, None if seed % 2 else 0.25, 0.2, 1e-3, 0.5, 0.01)
+    out = nodalize_arrays(*args, *prm)
+    ci, cj, frames, phi, mu, mu2, jv, nv = O.nodalize(*args, v.shape[0], *prm)
+    assert out["n_virtual"] == nv
+    assert np.array_equal(out["col_i"], ci) and np.array_equal(out["col_j"], cj)
+    assert np.array_equal(out["frames"], frames) and np.array_equal(out["phi"], phi)
+    assert np.array_equal(out["mu"], mu) and np.array_equal(out["mu2"], mu2)
+    assert np.array_equal(out["jv"].indptr, jv.indptr) and np.array_equal(out["jv"].indices, jv.indices)
+    assert np.array_equal(out["jv"].data, jv.data) and np.array_equal(np.signbit(out["jv"].data), np.signbit(jv.data))
