@@ -18,6 +18,8 @@ and stores its input (A_o CSC arrays, b_o, J_v CSR arrays, k_v) and output
   the way ``nodalize`` builds it (COO of every block entry -> CSR);
 * ``aug_none``: no virtual node (A_o returned unchanged, explicit zeros kept);
 * ``metrics_ref.csv``: rows written by the reference's ``report_csv`` (harness.py:651-697);
+* ``oneshot_aniso``: the reference strict-anisotropic one-shot with mu2 != mu
+  (ellipse bisection, ``solver.py:103-141``);
 * ``nodalize_mixed``: the reference ``nodalize`` (contacts.py:271-321) on mixed
   rigid / node / static sides with moving bodies and restitution.
 """
@@ -220,6 +222,27 @@ def nodalize_case(rng):
     print("nodalize_mixed n_c", len(nodal.contacts), "n_virtual", nodal.n_virtual, "jv nnz", jv.nnz)
 
 
+def oneshot_aniso_case():
+    """The reference one-shot with the strict-anisotropic operator and mu2 != mu
+    (the ellipse bisection of solver.py:103-126, np.hypot included)."""
+    from condsim.solver import SurrogateDelassus, contact_solve_oneshot
+
+    g = np.random.default_rng(77)
+    n = 3000
+    eta = g.standard_normal((n, 3)) * 3.0
+    eta[::17, 1:] *= 1e-6  # near-zero tangential parts
+    gam = g.uniform(0.5, 2.0, n)
+    phi = g.uniform(-1.0, 0.0, n)
+    mu = g.uniform(0.1, 0.9, n)
+    mu2 = g.uniform(0.1, 0.9, n)
+    mu2[::11] = mu[::11]  # circle cases too
+    lam = contact_solve_oneshot(SurrogateDelassus(gam), eta, phi, mu, "strict-anisotropic", mu2)
+    np.savez_compressed(os.path.join(HERE, "oneshot_aniso.npz"), eta=eta, gamma=gam, phi=phi, mu=mu, mu2=mu2,
+                        out_lam=np.asarray(lam))
+    print("oneshot_aniso", n)
+
+
 if __name__ == "__main__":
     main()
     nodalize_case(np.random.default_rng(5))
+    oneshot_aniso_case()
