@@ -75,3 +75,30 @@ def test_random_config_parity(seed, mode):
         assert np.array_equal(v, vo) and np.array_equal(lam, lo), kw
     else:
         assert _rel(v, vo) <= 1e-9 and _rel(lam, lo) <= 1e-9, kw
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_random_scene_batch_parity(seed):
+    """A batch of random independent systems (different sizes and contact
+    counts) in one scene-batch launch, random plain/Chebyshev configs: every
+    scene equals its own oracle solve (iterations; bits for plain)."""
+    from paper_2201_09212_b200.batch import solve_scenes
+
+    g = np.random.default_rng(7000 + seed)
+    scenes = [rigid_contact_system(int(g.integers(4, 40)), int(g.integers(1, 60)), seed=int(g.integers(1 << 30)),
+                                   k_v=float(g.choice([1e2, 1e5]))) for _ in range(int(g.integers(2, 24)))]
+    op = str(g.choice(["strict", "proximal", "strict-anisotropic"]))
+    kw = dict(operator=op, residual_tol=1e-8, max_iters=int(g.integers(5, 150)),
+              chebyshev=bool(seed % 2), cheby_start=int(g.integers(2, 10)))
+    res, _ = solve_scenes(scenes, SolverConfig(**kw))
+    for ps, r in zip(scenes, res):
+        s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64), ps.col_j.astype(np.int64),
+                     ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
+        vo, lo, ro = O.solve(s, O.Config(**kw), np.zeros(ps.n))
+        v, lam, rep = r
+        assert rep.iterations == ro.iterations, kw
+        if not kw["chebyshev"]:
+            assert np.array_equal(v, vo) and np.array_equal(lam, lo), kw
+        else:
+            assert _rel(v, vo) <= 1e-9 and _rel(lam, lo) <= 1e-9, kw
