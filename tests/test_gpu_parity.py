@@ -119,5 +119,8 @@ def test_per_op_entry_points(name):
         got = GS.contact_solve_oneshot(gam, eta, ps.phi, ps.mu, o, ps.mu2).ravel()
         assert np.array_equal(got, d["op_oneshot_" + o], equal_nan=True), o
     got = GS.contact_solve_oneshot(gam, eta, ps.phi, ps.mu, "strict-anisotropic", ps.mu2).ravel()
+    # the reference squares with Python's ``**`` (glibc pow, not correctly rounded: ~0.1% of
+    # squares differ from x*x in the last bit); where that flips a bisection step of the
+    # ellipse projection the result moves by ~1e-12 relative (1 of 1024 contacts here)
     assert np.allclose(got, d["op_oneshot_strict_anisotropic"], rtol=1e-9, atol=1e-12, equal_nan=True)
     assert np.array_equal(GS.inverse_contact(ps, x, 1e-3).ravel(), d["op_inverse"])

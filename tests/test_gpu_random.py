@@ -102,3 +102,53 @@ def test_random_scene_batch_parity(seed):
             assert np.array_equal(v, vo) and np.array_equal(lam, lo), kw
         else:
             assert _rel(v, vo) <= 1e-9 and _rel(lam, lo) <= 1e-9, kw
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_random_wide_columns_per_op(seed):
+    """Random symmetric matrices with columns of up to several hundred entries
+    (numpy's pairwise blocking in row_norms_sq: 8 accumulators, 128-entry
+    blocks) and random contacts: spmv, row norms, diagonal, Frobenius W (both
+    tie rules), gamma, J_c / J_c^T, one-shots, inverse_contact -- bit for bit."""
+    import scipy.sparse as sp
+
+    from paper_2201_09212_b200 import contacts as GC
+    from paper_2201_09212_b200 import solver as GS
+    from paper_2201_09212_b200 import sparse as GP
+    from paper_2201_09212_b200.system import SparseSymmetric, make_packed
+
+    g = np.random.default_rng(3100 + seed)
+    n = 3 * int(g.integers(40, 200))
+    dens = float(g.uniform(0.05, 0.9))
+    m = sp.random(n, n, density=dens, random_state=g, format="csc")
+    m = (m + m.T + sp.identity(n) * n).tocsc()
+    m.sort_indices()
+    a = SparseSymmetric(n, m.indptr, m.indices, m.data)
+    nodes = g.permutation(n // 3)
+    n_c = int(g.integers(1, n // 6))
+    ci = 3 * nodes[:n_c]
+    cj = np.where(g.random(n_c) < 0.5, 3 * nodes[n_c:2 * n_c], -1)
+    frames = np.stack([O.contact_frame(v) for v in g.standard_normal((n_c, 3))])
+    mu, mu2 = g.uniform(0.1, 0.9, n_c), g.uniform(0.1, 0.9, n_c)
+    phi = g.uniform(-1, 0, n_c)
+    ps = make_packed(n, m.indptr, m.indices, m.data, g.standard_normal(n), ci, cj, frames.ravel(), mu, mu2, phi)
+    s = O.System(n, m.indptr, m.indices, m.data, ps.b, ci.astype(np.int64), cj.astype(np.int64), frames, mu, mu2,
+                 phi)
+    x = g.standard_normal(n)
+    assert np.array_equal(GP.spmv(a, x), O.spmv(s, x))
+    assert np.array_equal(GP.row_norms_sq(a), O.row_norms_sq(s))
+    assert np.array_equal(GP.diagonal(a), O.diagonal(s))
+    for tie in (False, True):
+        assert np.array_equal(GS.step_matrix_frobenius(a, ps, tie).w, O.step_matrix_frobenius(s, tie))
+    w = O.step_matrix_frobenius(s, False)
+    gam = GS.surrogate_gamma(GS.StepMatrix(w), ps, 1e-3)
+    assert np.array_equal(gam.gamma, O.surrogate_gamma(s, w, 1e-3))
+    assert np.array_equal(GC.apply_jc(ps, x), O.apply_jc(s, x))
+    lam = g.standard_normal((n_c, 3))
+    assert np.array_equal(GC.apply_jc_t(ps, lam), O.apply_jc_t(s, lam))
+    eta = g.standard_normal((n_c, 3)) * 3
+    for op in ("strict", "proximal", "strict-anisotropic"):
+        got = GS.contact_solve_oneshot(gam, eta, phi, mu, op, mu2)
+        assert np.array_equal(got, O.oneshot(gam.gamma, eta, phi, mu, mu2, op)), op
+    assert np.array_equal(GS.inverse_contact(ps, x, 1e-3), O.inverse_contact(s, x, 1e-3, "proximal"))
