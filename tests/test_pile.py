@@ -150,3 +150,32 @@ def test_gpu_pile_contacts_equal_host_detection():
         assert np.array_equal(getattr(hc, name), getattr(dc, name)), name
     for name in ("indptr", "indices", "data"):
         assert np.array_equal(getattr(hc.jv, name), getattr(dc.jv, name)), name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(4))
+def test_gpu_pile_random_geometries(seed):
+    """Random small piles (grid shape, resolution, gaps, jitter incl. z): the
+    device step pipeline equals the host/oracle pipeline bit for bit over 4 steps."""
+    from paper_2201_09212_b200.pile import PileStepper
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    g = np.random.default_rng(40 + seed)
+    kw = dict(nx_cubes=int(g.integers(1, 3)), ny_cubes=int(g.integers(1, 3)), layers=int(g.integers(2, 4)),
+              nodes=int(g.integers(3, 6)), gap=float(g.choice([0.0, 1e-4])), jitter=float(g.choice([0.0, 5e-5, 2e-4])),
+              gap_z=0.0, jitter_z=float(g.choice([0.0, 3e-5])), seed=int(g.integers(1000)), dt=5e-4,
+              k_v=float(g.choice([1e2, 1e5])), mu=float(g.uniform(0.2, 0.8)))
+    host = CubePile(**kw)
+    dev = PileStepper(CubePile(**kw))
+    prev = None
+    faces = 0
+    for step in range(4):
+        pc, _, _, _, vo, lo, ro = _oracle_step(host, prev, 60)
+        st = dev.step(SolverConfig(residual_tol=1e-8, max_iters=60))
+        faces += pc.n_face
+        assert (st["n_c"], st["n_face"], st["iterations"]) == (pc.n_c, pc.n_face, ro.iterations), (kw, step)
+        host.advance(vo)
+        prev = vo
+        assert np.array_equal(dev.x.cpu().numpy(), host.x.ravel()), (kw, step)
+        assert np.array_equal(dev.last["lam"].cpu().numpy().reshape(-1, 3), lo), (kw, step)
+    assert faces > 0
