@@ -175,7 +175,8 @@ def test_config1_full_size_matches_oracle_prefix(mode):
 
 def test_config1_full_run_properties():
     """1000 iterations at configs[1]: never converges at k_v=1e5,
-    finite, deterministic, impulses inside the friction cone."""
+    finite, deterministic, impulses inside the friction cone, and bit-equal
+    to the CPU oracle over the whole solve."""
     from paper_2201_09212_b200.solver import SolverConfig, solve_packed
 
     ps = _rigid(4096, 16384, seed=2201)
@@ -188,3 +189,11 @@ def test_config1_full_run_properties():
     assert np.all(tn <= ps.mu * lam[:, 0] * (1 + 1e-12) + 1e-300)
     v2, lam2, rep2 = solve_packed(ps, cfg, np.zeros(ps.n))
     assert np.array_equal(v, v2)
+    # and the whole 1000-iteration solve equals the CPU oracle bit for bit
+    from oracle import vfpi_oracle as O
+
+    s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64), ps.col_j.astype(np.int64),
+                 ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
+    vo, lo, ro = O.solve(s, O.Config(residual_tol=1e-8, max_iters=1000), np.zeros(ps.n))
+    assert ro.iterations == 1000
+    assert np.array_equal(v, vo) and np.array_equal(lam, lo)
