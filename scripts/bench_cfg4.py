@@ -77,6 +77,12 @@ def main():
         last["st"] = PileStepper(pile, device=dev)
         return last["st"]
 
+    # warm-up on a throwaway two-cube pile in contact (loads the lazily-loaded
+    # kernels of every stage outside the timed run)
+    wp = PileStepper(CubePile(1, 1, 2, nodes=4, gap=0.0, jitter=0.0, gap_z=0.0, jitter_z=0.0, k_v=a.kv), device=dev)
+    for _ in range(3):
+        wp.step(cfg)
+    del wp
     torch.cuda.synchronize()
     res, tot = run_piles_sharded(a.scenes, a.steps, cfg, make_pile, stepper=stepper)
     wall = tot["wall_s"]
