@@ -156,10 +156,10 @@ std::vector<uint64_t> system_key(const vfpi_system& d, int G) {
           (uint64_t)(uintptr_t)d.mu, (uint64_t)(uintptr_t)d.mu2, (uint64_t)(uintptr_t)d.phi};
 }
 
-int upload(vfpi_handle* h, Workspace::Buf& b, const void* src, size_t bytes) {
+int upload(vfpi_handle* h, Workspace::Buf& b, const void* src, size_t bytes, cudaStream_t st = nullptr) {
   if (bytes == 0) return VFPI_OK;
   CK(vfpi::ensure(b, bytes));
-  CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, h->ws.stream));
+  CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st ? st : h->ws.stream));
   return VFPI_OK;
 }
 
@@ -174,22 +174,40 @@ int check_system(vfpi_handle* h, const vfpi_system* s) {
   return VFPI_OK;
 }
 
-// copy a host system into the handle's device input buffers
-int stage_system(vfpi_handle* h, const vfpi_system* s, vfpi_system* d) {
+// copy a host system into the handle's device input buffers. With
+// `overlap`, the arrays the layout setup does not read (b, frames, mu, mu2,
+// phi) go on the side stream after the others, so they cross PCIe while the
+// setup kernels run (the solve waits for them before its first use).
+int stage_system(vfpi_handle* h, const vfpi_system* s, vfpi_system* d, bool overlap = false) {
   Workspace& ws = h->ws;
   const size_t n = (size_t)s->n, nc = (size_t)s->n_c, nnz = (size_t)s->nnz;
   int rc;
+  // allocate everything first (ensure may free/realloc and synchronise)
+  for (auto& pr : {std::make_pair(&ws.b_indptr, 4 * (n + 1)), std::make_pair(&ws.b_indices, 4 * nnz),
+                   std::make_pair(&ws.b_data, 8 * nnz), std::make_pair(&ws.b_b, 8 * n),
+                   std::make_pair(&ws.b_ci, 4 * nc), std::make_pair(&ws.b_cj, 4 * nc),
+                   std::make_pair(&ws.b_frames, 72 * nc), std::make_pair(&ws.b_mu, 8 * nc),
+                   std::make_pair(&ws.b_mu2, 8 * nc), std::make_pair(&ws.b_phi, 8 * nc)})
+    if (pr.second) CK(vfpi::ensure(*pr.first, pr.second));
   if ((rc = upload(h, ws.b_indptr, s->indptr, 4 * (n + 1)))) return rc;
   if ((rc = upload(h, ws.b_indices, s->indices, 4 * nnz))) return rc;
   if ((rc = upload(h, ws.b_data, s->data, 8 * nnz))) return rc;
-  if (s->b && (rc = upload(h, ws.b_b, s->b, 8 * n))) return rc;
   if (nc) {
     if ((rc = upload(h, ws.b_ci, s->col_i, 4 * nc))) return rc;
     if ((rc = upload(h, ws.b_cj, s->col_j, 4 * nc))) return rc;
-    if ((rc = upload(h, ws.b_frames, s->frames, 72 * nc))) return rc;
-    if (s->mu && (rc = upload(h, ws.b_mu, s->mu, 8 * nc))) return rc;
-    if (s->mu2 && (rc = upload(h, ws.b_mu2, s->mu2, 8 * nc))) return rc;
-    if (s->phi && (rc = upload(h, ws.b_phi, s->phi, 8 * nc))) return rc;
+  }
+  cudaStream_t late = ws.stream;
+  if (overlap) {
+    CK(cudaEventRecord(ws.ev_main_h2d, ws.stream));
+    CK(cudaStreamWaitEvent(ws.side, ws.ev_main_h2d, 0));
+    late = ws.side;
+  }
+  if (s->b && (rc = upload(h, ws.b_b, s->b, 8 * n, late))) return rc;
+  if (nc) {
+    if ((rc = upload(h, ws.b_frames, s->frames, 72 * nc, late))) return rc;
+    if (s->mu && (rc = upload(h, ws.b_mu, s->mu, 8 * nc, late))) return rc;
+    if (s->mu2 && (rc = upload(h, ws.b_mu2, s->mu2, 8 * nc, late))) return rc;
+    if (s->phi && (rc = upload(h, ws.b_phi, s->phi, 8 * nc, late))) return rc;
   }
   *d = *s;
   d->indptr = P<int32_t>(ws.b_indptr);
@@ -242,6 +260,9 @@ int vfpi_create(int device, vfpi_handle** out) {
   cudaDeviceGetAttribute(&h->ws.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (cudaStreamCreateWithFlags(&h->ws.stream, cudaStreamNonBlocking) != cudaSuccess) { delete h; return VFPI_CUDA_ERROR; }
   for (auto& e : h->ws.ev) cudaEventCreate(&e);
+  cudaStreamCreateWithFlags(&h->ws.side, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&h->ws.ev_main_h2d, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->ws.ev_side, cudaEventDisableTiming);
   cudaMallocHost(&h->ws.h_summary, sizeof(vfpi::SetupSummary));
   cudaMallocHost(&h->ws.h_status, sizeof(vfpi::SolveStatus));
   cudaMallocHost(&h->h_flags, 16);
@@ -299,6 +320,9 @@ void vfpi_destroy(vfpi_handle* h) {
     for (SetupGraph& g : gs->slot)
       if (g.exec) cudaGraphExecDestroy(g.exec);
   if (h->ws.stream) cudaStreamDestroy(h->ws.stream);
+  if (h->ws.side) cudaStreamDestroy(h->ws.side);
+  if (h->ws.ev_main_h2d) cudaEventDestroy(h->ws.ev_main_h2d);
+  if (h->ws.ev_side) cudaEventDestroy(h->ws.ev_side);
   if (h->ws.h_summary) cudaFreeHost(h->ws.h_summary);
   if (h->ws.h_status) cudaFreeHost(h->ws.h_status);
   if (h->h_flags) cudaFreeHost(h->h_flags);
@@ -434,6 +458,10 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   // resident kernel stages whole 32-byte sectors
   const size_t npad = (((size_t)std::max(n, 1) + 3) / 4) * 4 + 4;
   CK(vfpi::ensure(ws.vbuf, 3 * 8 * npad));
+  if (ws.side_pending) {  // host-buffer solve: b, frames, mu, mu2, phi, warm came on the side stream
+    CK(cudaStreamWaitEvent(st, ws.ev_side, 0));
+    ws.side_pending = false;
+  }
   CK(cudaMemsetAsync(ws.vbuf.p, 0, 3 * 8 * npad, st));
   CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)std::max(n_c, 1)));
   CK(vfpi::ensure(ws.partials, 2 * 8 * (size_t)G * vfpi::kPartialStride));
@@ -564,10 +592,12 @@ int vfpi_solve(vfpi_handle* h, const vfpi_system* s, const vfpi_config* cfg, con
   if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
   Workspace& ws = h->ws;
   vfpi_system d;
-  if ((rc = stage_system(h, s, &d))) return rc;
   const size_t n = (size_t)s->n, nc = (size_t)s->n_c;
-  if ((rc = upload(h, ws.b_warm, warm, 8 * n))) return rc;
-  CK(vfpi::ensure(ws.b_warm, 8 * n));
+  CK(vfpi::ensure(ws.b_warm, 8 * std::max<size_t>(n, 1)));
+  if ((rc = stage_system(h, s, &d, true))) return rc;
+  if ((rc = upload(h, ws.b_warm, warm, 8 * n, ws.side))) return rc;
+  CK(cudaEventRecord(ws.ev_side, ws.side));
+  ws.side_pending = true;
   const double* dwc = nullptr;
   if (w_cached) {
     if ((rc = upload(h, ws.b_wc, w_cached, 8 * n))) return rc;
@@ -587,7 +617,9 @@ int vfpi_solve(vfpi_handle* h, const vfpi_system* s, const vfpi_config* cfg, con
   dres.w = res->w ? P<double>(ws.b_w_out) : nullptr;
   rc = vfpi_solve_device(h, &d, cfg, P<double>(ws.b_warm), dwc, &dres, ws.stream);
   if (rc) {
+    cudaStreamSynchronize(ws.side);
     cudaStreamSynchronize(ws.stream);
+    ws.side_pending = false;
     return rc;
   }
   if (n) CK(cudaMemcpyAsync(res->v, dres.v, 8 * n, cudaMemcpyDeviceToHost, ws.stream));

@@ -211,6 +211,11 @@ struct Workspace {
   Buf prof;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // host-buffer solves: the inputs the layout setup does not read (b, frames,
+  // mu, mu2, phi, warm) are uploaded on a side stream while the setup runs
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_main_h2d = nullptr, ev_side = nullptr;
+  bool side_pending = false;
   SetupSummary* h_summary = nullptr;  // pinned
   SolveStatus* h_status = nullptr;    // pinned
   int num_sms = 148;
