@@ -454,7 +454,7 @@ class PileStepper:
         sp_ = C.c_void_p(st.cuda_stream if st.cuda_stream else 1)
         t0 = time.perf_counter()
         n_o = pile.n
-        max_pen = max(0.0, -float(self.x.view(-1, 3)[:, 2].min()))
+        zmin = self.x.view(-1, 3)[:, 2].min()  # read after the step's final sync (no extra round trip)
         up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev, non_blocking=False)  # noqa: E731
         i32, f64 = _lib._i32p, _lib._f64p
         if self.detect == "device":
@@ -514,15 +514,17 @@ class PileStepper:
             _raise_for(code, h)
         _raise_for(h.L.vfpi_advance_device(h.h, n_o, pile.dt, P(vh), P(self.x), P(self.v), sp_), h)
         self.prev = vh[:n_o].clone()
-        st.synchronize()
+        it = int(res.iterations)
+        scalars = torch.stack([zmin, 0.5 * torch.dot(self.m * self.v, self.v),
+                               trace[it - 1] if it > 0 else torch.zeros((), dtype=torch.float64, device=dev)])
+        zmin_h, ke, resid = scalars.tolist()  # the step's one closing synchronisation
+        max_pen = max(0.0, -zmin_h)
         self.steps += 1
         self.last = dict(v_hat=vh, lam=lam[: 3 * n_c], contacts=pc)
-        it = int(res.iterations)
-        resid = float(trace[it - 1]) if it > 0 else 0.0
         return dict(n_c=n_c, **counts, n=n, nnz=int(out.nnz),
                     iterations=int(res.iterations), converged=bool(res.converged), diverged=code == _lib.DIVERGED,
                     setup_ms=float(res.setup_ms), loop_ms=float(res.loop_ms), detect_s=t_detect,
-                    residual=resid, max_pen_m=max_pen, ke_J=float(0.5 * torch.dot(self.m * self.v, self.v)),
+                    residual=resid, max_pen_m=max_pen, ke_J=ke,
                     wall_s=time.perf_counter() - t0)
 
     def metrics_row(self, step: int, r: dict):
