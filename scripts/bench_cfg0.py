@@ -66,7 +66,23 @@ def main():
     single = {"wall_s": swall, "sim_steps_per_s": a.steps / swall, "contact_iter_per_s": sci / swall,
               "loop_ms": sloop, "final_state_max_abs_diff_vs_batch_path":
                   float(np.abs(pst.state()[0] - x_dev.reshape(-1, 3)).max())}
+    # roofline of the solve loops against the algorithmic bytes:
+    # B_iter = 12 nnz_num + 4 (n+1) + 32 n (+8 n Chebyshev) + 128 n_c per iteration
+    cube0 = FemCube()
+    nnz_num = int(np.count_nonzero(cube0.A.data))
+    n0 = cube0.n
+    bytes_tot = sum((12 * nnz_num + 4 * (n0 + 1) + 32 * n0 + (8 * n0 if a.chebyshev else 0) + 128 * c) * i
+                    for c, i in per)
+    peak = 6650.0
+    try:
+        peak = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                 "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    gbs = bytes_tot / (loop_ms * 1e-3) / 1e9 if loop_ms > 0 else 0.0
     out = {"workload": "configs[0] single FEM cube 10^3 nodes, 200 steps", "steps": a.steps,
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                        "note": "one-CTA scene kernel on a 1 MB system: latency-bound, cache-resident"},
            "chebyshev": a.chebyshev, "tol": 1e-8, "max_iters": 500, "wall_s": wall,
            "sim_steps_per_s": a.steps / wall, "contact_iter_per_s": ci / wall, "contact_iterations": ci,
            "iterations": its, "loop_ms": loop_ms, "setup_ms": setup_ms,
