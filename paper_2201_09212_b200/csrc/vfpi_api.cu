@@ -404,9 +404,13 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
 
   CK(cudaEventRecord(ws.ev[0], st));
   vfpi::SetupSummary* hs = ws.h_summary;
-  // first choice: the whole partition of every CTA resident in shared memory
+  // first choice: the whole partition of every CTA resident in shared memory.
+  // Skipped when it cannot fit: every valid row needs >= 52 B on chip (40 B of
+  // row state + one numeric entry of 12 B; a row without one is a zero row)
   int G = choose_blocks_resident(*d, ws.num_sms);
-  {
+  const bool maybe_resident =
+      h->kernel_mode == 1 || (int64_t)n * 52 <= (int64_t)ws.max_smem_optin * (int64_t)ws.num_sms;
+  if (maybe_resident) {
     std::vector<uint64_t> key = system_key(*d, G);
     vfpi::LayoutOptions res_opt = h->layout_opt;
     res_opt.row_cost = res_opt.res_row_cost;
@@ -421,8 +425,9 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
     rc = vfpi::setup_layout_finish(ws, st, hs, h->err);
     if (rc) return rc;
   }
-  const size_t smem_res = (size_t)hs->max_res_bytes;
-  const bool fits = hs->max_ent_per_blk < (1 << 24) && smem_res + 2048 <= (size_t)ws.max_smem_optin && G <= 256;
+  const size_t smem_res = maybe_resident ? (size_t)hs->max_res_bytes : 0;
+  const bool fits = maybe_resident && hs->max_ent_per_blk < (1 << 24) &&
+                    smem_res + 2048 <= (size_t)ws.max_smem_optin && G <= 256;
   if (h->kernel_mode == 1 && !fits) { h->err = "partition does not fit in shared memory"; return VFPI_UNSUPPORTED; }
   bool resident = fits && h->kernel_mode != 2;
   int smem = 0;
