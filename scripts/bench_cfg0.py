@@ -83,7 +83,8 @@ def main():
     out = {"workload": "configs[0] single FEM cube 10^3 nodes, 200 steps", "steps": a.steps,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "note": "one-CTA scene kernel on a 1 MB system: latency-bound, cache-resident"},
-           "chebyshev": a.chebyshev, "tol": 1e-8, "max_iters": 500, "wall_s": wall,
+           "chebyshev": a.chebyshev, "tol": 1e-8, "max_iters": 500, "operator": "strict", "mu": 0.5, "dt": 1e-3,
+           "E": 1e5, "nu": 0.3, "drop_m": 0.05, "wall_s": wall,
            "sim_steps_per_s": a.steps / wall, "contact_iter_per_s": ci / wall, "contact_iterations": ci,
            "iterations": its, "loop_ms": loop_ms, "setup_ms": setup_ms,
            "contact_steps": sum(1 for c, _ in per if c > 0), "max_contacts": max(c for c, _ in per),

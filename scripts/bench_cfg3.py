@@ -40,6 +40,8 @@ def main():
     except Exception:
         pass
     out = {"workload": f"configs[3] heightfield block {a.nx}^3 nodes", "n": ps.n, "n_c": ps.n_c,
+           "tol": 1e-8, "max_iters": a.max_iters, "operator": "strict", "E": 1e6, "nu": 0.35, "mu": 0.4, "dt": 1e-3,
+           "side_m": 0.1, "press": "bottom conformed 0.1 mm into the heightfield + 50 N on the top face",
            "nnz_stored": ps.nnz, "nnz_numeric": nnz_num, "build_s": t_build, "variants": []}
     h = _lib.handle(0)
     for cheb in (False, True):

@@ -107,6 +107,8 @@ def main():
                "scenes": a.scenes, "n_gpus": world, "steps_per_scene": a.steps, "n_orig": last.pile.n,
                "nnz_A_o": int(last.pile.a_data.shape[0]), "dt": last.pile.dt, "mu": last.pile.mu, "k_v": last.pile.k_v,
                "tol": cfg.residual_tol, "max_iters": cfg.max_iters, "operator": "strict", "chebyshev": a.chebyshev,
+               "seeds": "scene k uses default_rng(k) for its jitter", "gap_m": 0.005, "gap_z_m": 0.0005,
+               "jitter_m": 0.002,
                "wall_s": wall, "scene_steps_per_s": totals["steps"] / wall,
                "contact_iter_per_s": totals["contact_iterations"] / wall,
                "loop": {"iterations": totals["iterations"], "loop_s": totals["loop_s"], "setup_s": totals["setup_s"],

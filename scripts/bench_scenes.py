@@ -201,6 +201,8 @@ def device_pipeline(args, cubes, cfg, t_build, rank, world, dist, torch):
                 "device_step_ms_total": step_max, "device_setup_ms_rank0": setup_ms, "device_loop_ms_rank0": loop_ms,
                 "wall_s": wall_max, "mean_iters": it_all / (args.scenes * args.steps), "contact_iterations": ci_all,
                 "host_build_s": t_build, "chebyshev": args.chebyshev,
+                "seed": args.seed, "operator": cfg.operator, "tol": cfg.residual_tol, "max_iters": cfg.max_iters,
+                "scene_params": "E ~ U[5e4, 2e5], drop ~ U[0.02, 0.1] m, yaw ~ U[0, 2pi) from default_rng(seed)",
                 "scaling": "strong (fixed scene count split over ranks)"}
         if args.cpu_baseline and world == 1:
             g = np.random.default_rng(args.seed)
