@@ -342,7 +342,8 @@ int vfpi_pile_contacts_device(vfpi_handle* h, const vfpi_pile_geometry* g, const
  * columns, virtual nodes, J_v canonical CSR with every block entry stored),
  * frames (contact_frame, :131-149) and phi (stabilization_term, :230-239),
  * bit-identical to the reference. Device pointers in; outputs are device
- * buffers owned by the handle, valid until the next call. mu2 = NaN: None. */
+ * buffers owned by the handle, valid until the next call. mu2 = NaN: None.
+ * Side kinds, node offsets and body ids are checked (VFPI_BAD_ARGUMENT). */
 typedef struct vfpi_nodalize_input {
   int64_t n_c;
   int64_t n_o;                 /* velocity dimension (columns of J_v) */
@@ -358,6 +359,7 @@ typedef struct vfpi_nodalize_input {
   const int32_t* body_q;       /* per body: coordinate offset (Body.q_offset) */
   const int32_t* body_v;       /* per body: velocity offset (Body.v_offset) */
   double mu, mu2, beta_err, dt, e_rest, rest_threshold;
+  int64_t n_bodies;            /* entries of body_q / body_v (rigid side ids are checked against it) */
 } vfpi_nodalize_input;
 
 typedef struct vfpi_nodal_contacts {

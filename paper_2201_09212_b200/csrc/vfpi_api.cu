@@ -1483,6 +1483,7 @@ int vfpi_nodalize_device(vfpi_handle* h, const vfpi_nodalize_input* in, vfpi_nod
   vfpi::NodalizeIn ni;
   ni.n_c = in->n_c;
   ni.n_o = (int)in->n_o;
+  ni.n_bodies = (int)in->n_bodies;
   ni.first_kind = in->first_kind;
   ni.first_ref = in->first_ref;
   ni.second_kind = in->second_kind;

@@ -43,15 +43,24 @@ constexpr int kT = 256;
 inline unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + kT - 1) / kT); }
 
 // nonzero entries per J_v row -> products per row (count^2)
-__global__ void k_aug_prod_count(int rows, const int* __restrict__ jp, const double* __restrict__ jx,
-                                 int64_t* __restrict__ cnt) {
+// (also validates J_v: columns inside [0, n_o), strictly increasing per row)
+__global__ void k_aug_prod_count(int rows, int n_o, const int* __restrict__ jp, const int* __restrict__ jc,
+                                 const double* __restrict__ jx, int64_t* __restrict__ cnt, int* __restrict__ bad) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r > rows) return;
   if (r == rows) { cnt[r] = 0; return; }
   int64_t c = 0;
-  for (int e = jp[r]; e < jp[r + 1]; ++e) c += (jx[e] != 0.0);
+  int prev = -1;
+  for (int e = jp[r]; e < jp[r + 1]; ++e) {
+    c += (jx[e] != 0.0);
+    const int col = jc[e];
+    if (col <= prev || col >= n_o) atomicExch(bad, 1);
+    prev = col;
+  }
   cnt[r] = c * c;
 }
+
+__global__ void k_aug_zero(int* p) { *p = 0; }
 
 // products of row r in (i-entry, j-entry) order; key = (j << 32) | i
 __global__ void k_aug_prod_fill(int rows, const int* __restrict__ jp, const int* __restrict__ jc,
@@ -253,14 +262,22 @@ int augment_device(AugmentWork& w, const AugmentIn& in, cudaStream_t st, Augment
   // 1. products
   AK(ensure(w.pcnt, sizeof(int64_t) * (size_t)(rows + 1)));
   AK(ensure(w.poff, sizeof(int64_t) * (size_t)(rows + 1)));
-  k_aug_prod_count<<<grid_for(rows + 1), kT, 0, st>>>(rows, in.jv_indptr, in.jv_data, B<int64_t>(w.pcnt));
+  AK(ensure(w.cs, sizeof(int64_t) * (size_t)(n_o + 1)));  // its first word doubles as the validation flag
+  k_aug_zero<<<1, 1, 0, st>>>(B<int>(w.cs));
+  k_aug_prod_count<<<grid_for(rows + 1), kT, 0, st>>>(rows, n_o, in.jv_indptr, in.jv_indices, in.jv_data,
+                                                      B<int64_t>(w.pcnt), B<int>(w.cs));
   size_t tb = 0;
   AK(cub::DeviceScan::ExclusiveSum(nullptr, tb, B<int64_t>(w.pcnt), B<int64_t>(w.poff), rows + 1, st));
   AK(ensure(w.tmp, tb));
   AK(cub::DeviceScan::ExclusiveSum(w.tmp.p, tb, B<int64_t>(w.pcnt), B<int64_t>(w.poff), rows + 1, st));
   AK(cudaMemcpyAsync(w.h_small, B<int64_t>(w.poff) + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  AK(cudaMemcpyAsync(&w.h_small[1], B<int>(w.cs), sizeof(int), cudaMemcpyDeviceToHost, st));
   AK(cudaStreamSynchronize(st));
   const int64_t m = w.h_small[0];
+  if (reinterpret_cast<int*>(&w.h_small[1])[0]) {
+    err = "augment: J_v is not canonical CSR with columns in [0, n_o)";
+    return VFPI_BAD_ARGUMENT;
+  }
   launches += 2;
   AK(ensure(w.pkey, sizeof(unsigned long long) * (size_t)m));
   AK(ensure(w.pkey2, sizeof(unsigned long long) * (size_t)m));

@@ -44,16 +44,27 @@ __global__ void k_nod_fill_int(int64_t n, int* __restrict__ p, int v) {
 }
 
 // first use of every node offset (processing order 2m + side)
-__global__ void k_nod_first_use(int64_t n_c, const int* __restrict__ fk, const int* __restrict__ fr,
-                                const int* __restrict__ sk, const int* __restrict__ sr, int* __restrict__ first) {
+// (also validates the sides: kinds, node offsets inside [0, n_o - 3], body ids
+// inside [0, n_bodies); a static first side is not a contact)
+__global__ void k_nod_first_use(int64_t n_c, int n_o, int n_bodies, const int* __restrict__ fk,
+                                const int* __restrict__ fr, const int* __restrict__ sk, const int* __restrict__ sr,
+                                int* __restrict__ first, int* __restrict__ bad) {
   const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (m >= n_c) return;
-  if (fk[m] == 0) atomicMin(first + fr[m], (int)(2 * m));
-  if (sk[m] == 0) atomicMin(first + sr[m], (int)(2 * m + 1));
+  for (int s = 0; s < 2; ++s) {
+    const int kind = s ? sk[m] : fk[m], ref = s ? sr[m] : fr[m];
+    const bool ok = (kind == 0 && ref >= 0 && ref <= n_o - 3) || (kind == 1 && ref >= 0 && ref < n_bodies) ||
+                    (kind == -1 && s == 1);
+    if (!ok) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    if (kind == 0) atomicMin(first + ref, (int)(2 * m + s));
+  }
 }
 
 // per (contact, side): 1 if it needs a virtual node; its J_v entry count
-__global__ void k_nod_virtual_flags(int64_t n_c, const int* __restrict__ fk, const int* __restrict__ fr,
+__global__ void k_nod_virtual_flags(int64_t n_c, int n_o, const int* __restrict__ fk, const int* __restrict__ fr,
                                     const int* __restrict__ sk, const int* __restrict__ sr,
                                     const int* __restrict__ first, int* __restrict__ vflag, int* __restrict__ jcnt) {
   const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -64,7 +75,7 @@ __global__ void k_nod_virtual_flags(int64_t n_c, const int* __restrict__ fk, con
   const int ref = (o & 1) ? sr[m] : fr[m];
   int f = 0, c = 0;
   if (kind == 1) { f = 1; c = 18; }                            // rigid: [I, -[r]x]
-  else if (kind == 0 && first[ref] != (int)o) { f = 1; c = 9; }  // node, second use: identity
+  else if (kind == 0 && ref >= 0 && ref <= n_o - 3 && first[ref] != (int)o) { f = 1; c = 9; }  // node, later use
   vflag[o] = f;
   jcnt[o] = c;
 }
@@ -199,9 +210,9 @@ int nodalize_device(NodalizeWork& w, const NodalizeIn& in, cudaStream_t st, Noda
   NK(ensure(w.flag, sizeof(int)));
   k_nod_fill_int<<<gridn(in.n_o), kT, 0, st>>>(in.n_o, Bn<int>(w.first), INT_MAX);
   k_nod_set<<<1, 1, 0, st>>>(Bn<int>(w.flag), 0);
-  k_nod_first_use<<<gridn(n_c), kT, 0, st>>>(n_c, in.first_kind, in.first_ref, in.second_kind, in.second_ref,
-                                              Bn<int>(w.first));
-  k_nod_virtual_flags<<<gridn(S + 1), kT, 0, st>>>(n_c, in.first_kind, in.first_ref, in.second_kind, in.second_ref,
+  k_nod_first_use<<<gridn(n_c), kT, 0, st>>>(n_c, in.n_o, in.n_bodies, in.first_kind, in.first_ref, in.second_kind,
+                                              in.second_ref, Bn<int>(w.first), Bn<int>(w.flag));
+  k_nod_virtual_flags<<<gridn(S + 1), kT, 0, st>>>(n_c, in.n_o, in.first_kind, in.first_ref, in.second_kind, in.second_ref,
                                                    Bn<int>(w.first), Bn<int>(w.vflag), Bn<int>(w.jcnt));
   size_t tb = 0;
   NK(cub::DeviceScan::ExclusiveSum(nullptr, tb, Bn<int>(w.vflag), Bn<int>(w.vpos), S + 1, st));
@@ -211,7 +222,12 @@ int nodalize_device(NodalizeWork& w, const NodalizeIn& in, cudaStream_t st, Noda
   int* hs = reinterpret_cast<int*>(w.h_small);
   NK(cudaMemcpyAsync(hs, Bn<int>(w.vpos) + S, sizeof(int), cudaMemcpyDeviceToHost, st));
   NK(cudaMemcpyAsync(hs + 1, Bn<int>(w.jpos) + S, sizeof(int), cudaMemcpyDeviceToHost, st));
+  NK(cudaMemcpyAsync(hs + 2, Bn<int>(w.flag), sizeof(int), cudaMemcpyDeviceToHost, st));
   NK(cudaStreamSynchronize(st));
+  if (hs[2]) {
+    err = "nodalize: bad contact side (kind, node offset or body index out of range)";
+    return VFPI_BAD_ARGUMENT;
+  }
   const int nv = hs[0], nj = hs[1];
   NK(ensure(w.ci, sizeof(int) * (size_t)std::max<int64_t>(n_c, 1)));
   NK(ensure(w.cj, sizeof(int) * (size_t)std::max<int64_t>(n_c, 1)));

@@ -124,3 +124,26 @@ def test_device_augment_random_systems(seed):
     p, i, x = augment_arrays(n_o, a.indptr, a.indices, a.data, jv, kv)
     po, io, xo, _ = O.augment(n_o, a.indptr, a.indices, a.data, np.zeros(n_o), jv, kv)
     assert np.array_equal(p, po) and np.array_equal(i, io) and np.array_equal(x, xo)
+
+
+@pytest.mark.gpu
+def test_device_augment_rejects_non_canonical_jv():
+    """vfpi_augment_device validates J_v (columns in range, increasing per row)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2201_09212_b200 import _lib
+
+    n_o = 6
+    a = sp.identity(n_o, format="csc")
+    up = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).cuda()  # noqa: E731
+    ap, ai, ax = up(a.indptr, np.int32), up(a.indices, np.int32), up(a.data, np.float64)
+    for cols in ([0, 7, 1], [2, 1, 3]):  # out of range / not increasing
+        jp, ji, jx = up([0, 3, 3, 3], np.int32), up(cols, np.int32), up([1.0, 1.0, 1.0], np.float64)
+        h = _lib.handle(0)
+        inp = _lib.VfpiAugmentInput(n_o, 3, a.nnz, C.cast(ap.data_ptr(), _lib._i32p), C.cast(ai.data_ptr(), _lib._i32p),
+                                    C.cast(ax.data_ptr(), _lib._f64p), 3, C.cast(jp.data_ptr(), _lib._i32p),
+                                    C.cast(ji.data_ptr(), _lib._i32p), C.cast(jx.data_ptr(), _lib._f64p), 1e5)
+        out = _lib.VfpiAugmented()
+        assert h.L.vfpi_augment_device(h.h, C.byref(inp), C.byref(out), None) == _lib.BAD_ARGUMENT

@@ -188,3 +188,19 @@ def test_device_nodalize_random_contacts(seed):
     assert np.array_equal(out["mu"], mu) and np.array_equal(out["mu2"], mu2)
     assert np.array_equal(out["jv"].indptr, jv.indptr) and np.array_equal(out["jv"].indices, jv.indices)
     assert np.array_equal(out["jv"].data, jv.data) and np.array_equal(np.signbit(out["jv"].data), np.signbit(jv.data))
+
+
+@pytest.mark.gpu
+def test_device_nodalize_rejects_bad_sides():
+    """Out-of-range node offsets / body ids and a static first side are refused
+    before any output is written."""
+    from paper_2201_09212_b200.nodalize import nodalize_arrays
+
+    d = load()
+    base = dict(point=np.zeros((1, 3)), normal=np.array([[0.0, 0.0, 1.0]]), depth=np.zeros(1))
+    for fk, fr, sk, sr in ((0, d["v"].shape[0], -1, -1), (1, len(d["body_q"]), -1, -1), (-1, 0, -1, -1),
+                           (0, 0, 1, -5)):
+        with pytest.raises(ValueError):
+            nodalize_arrays(np.array([fk], np.int32), np.array([fr], np.int32), np.array([sk], np.int32),
+                            np.array([sr], np.int32), base["point"], base["normal"], base["depth"], d["q"], d["v"],
+                            d["body_q"], d["body_v"])
