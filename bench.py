@@ -1,24 +1,35 @@
-"""Benchmark of the V-FPI hot path (BASELINE.json configs[1]).
+"""Benchmark of the V-FPI hot path on BASELINE.json configs[2].
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (configs[1]): 4096 rigid bodies, 16,384 D-contacts nodalized onto
-32,768 virtual nodes (n = 122,880 DOF), seeded synthetic system built exactly
-as the reference's nodalize/augment_dynamics would (paper_2201_09212_b200.
-scenes), strict operator, Frobenius W, no Chebyshev (the parity-gated
-setting), tol 1e-8, max 1000 iterations. At k_v = 1e5 it never converges, so
-every step is exactly 1000 iterations = 16,384,000 contact-iterations.
+Workload (configs[2], the largest BASELINE config that runs on one GPU and
+the one north_star shards over 1/2/4/8 GPUs): 1024 independent FEM cubes
+(configs[0]: 10x10x10 nodes, 5 linear tets per hex, nu 0.3, rho 1000, side
+0.1 m, mu 0.5, dt 1e-3) with seeded per-scene E ~ U[5e4, 2e5] Pa, drop height
+~ U[0.02, 0.1] m and yaw ~ U[0, 2 pi), stepped 200 times through the whole
+device step pipeline (right-hand side, node-plane detection, V-FPI solve
+strict / tol 1e-8 / 500 iterations, contact-free CG fallback on divergence,
+midpoint integration; ``fembatch.FemBatch`` / ``vfpi_fem_step``).
 
-A "step" is one complete solve_vfpi (per-solve setup + 1000 iterations +
-post-loop SCC). `value` is measured with the system already in HBM; L2 (126 MB)
-is flushed before every timed step by writing a 256 MB buffer, because the
-working set (~17 MB) would otherwise stay cache resident across steps.
-`e2e` is the same metric through the C-ABI `vfpi_solve` with pinned HOST
-buffers: host->device copy of all inputs and device->host copy of v, lam,
-trace and SCC residuals are inside the timed region.
+A bench "step" is one complete configs[2] run: the 1024 scenes reset to
+their initial state (device to device) and advanced 200 simulation steps,
+ending with the NCCL all-reduce of the counters and the gather of every
+scene's final node positions to rank 0 (N > 1). Scenes are sharded in
+contiguous blocks over the N ranks (strong scaling: the 1024 scenes are
+fixed). The working set (A and K of 1024 scenes, ~2.3 GB) is far larger than
+L2, so no flush is needed between steps.
 
-N > 1: configs[1] is one system, so ranks run independent replicas (weak
-scaling, no data-path collective); timing is the max over ranks.
+``value`` = contact-iterations (sum over scenes and simulation steps of
+contacts x V-FPI iterations) / device time (CUDA events on the pipeline's
+stream, max over ranks), inputs resident in HBM. ``e2e`` = the same through
+the public API from pinned HOST buffers: ``FemBatch`` creation (upload of A,
+K and the state), the 200 steps and the download of the final x and v.
+
+``--impl reference`` runs the reference's own CPU path of the same pipeline
+(``condsim`` from ``baseline/_ref``: ``detect_contacts`` / ``nodalize`` /
+``augment_dynamics`` / ``solve_vfpi`` / the harness's CG fallback, with this
+repo's FEM matrices, since the reference has no FEM) on all host cores, one
+scene per process.
 """
 
 from __future__ import annotations
@@ -26,6 +37,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,14 +49,25 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_BODIES, N_CONTACTS, SEED, KV = 4096, 16384, 2201, 1e5
-MAX_ITERS, TOL = 1000, 1e-8
 METRIC, UNIT = "contact-iterations/sec", "contact-iter/s"
+SCENES, SIM_STEPS, NX, SEED = 1024, 200, 10, 2022
+TOL, MAX_ITERS = 1e-8, 500
+CHUNK = 1024  # scenes per FemBatch (one CTA per scene)
 
 
-def algorithmic_bytes_per_iter(n, nnz_num, n_c, cheb=False):
-    """B_iter = 12 nnz_num + 4 (n+1) + 32 n (+8 n Chebyshev) + 128 n_c."""
-    return 12 * nnz_num + 4 * (n + 1) + 32 * n + (8 * n if cheb else 0) + 128 * n_c
+def scene_params(n=SCENES, seed=SEED):
+    """configs[2]'s seeded per-scene parameters (E, drop, yaw)."""
+    g = np.random.default_rng(seed)
+    E = g.uniform(5e4, 2e5, n)
+    drop = g.uniform(0.02, 0.1, n)
+    yaw = g.uniform(0, 2 * np.pi, n)
+    return E, drop, yaw
+
+
+def bytes_per_scene_iter(nnz_num, n):
+    """SURVEY §8(d) per scene and iteration without the contact term:
+    12 nnz_num + 4 (n+1) + 32 n (the 128 n_c term is added per contact-iteration)."""
+    return 12 * nnz_num + 4 * (n + 1) + 32 * n
 
 
 def peaks():
@@ -52,9 +75,9 @@ def peaks():
     try:
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -77,8 +100,7 @@ class ClockSampler:
         except Exception:
             self.proc = None
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
+        threading.Thread(target=self._read, daemon=True).start()
 
     def _read(self):
         for line in self.proc.stdout:
@@ -106,30 +128,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(under)}
 
 
-def dist_setup(n_gpus):
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=None)
-        pg = dist
-    return rank, world, local, pg
-
-
-def cpu_oracle_solve(ps, max_iters):
-    from oracle import vfpi_oracle as O
-
-    s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64), ps.col_j.astype(np.int64),
-                 ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
-    t0 = time.perf_counter()
-    v, lam, rep = O.solve(s, O.Config(residual_tol=TOL, max_iters=max_iters), np.zeros(ps.n))
-    dt = time.perf_counter() - t0
-    return ps.n_c * rep.iterations, dt, rep.iterations
-
-
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -148,79 +146,243 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-def run_reference(args):
-    """--impl reference: the reference algorithm on the host CPU (oracle port)."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from paper_2201_09212_b200.scenes import rigid_contact_system
+# ---------------------------------------------------------------------------
+# the reference CPU path (one scene per worker process)
+# ---------------------------------------------------------------------------
 
-    ps = rigid_contact_system(N_BODIES, N_CONTACTS, SEED, KV)
-    sample_iters = 60
-    # per-solve setup (Frobenius W with tie groups, gamma, the check pass) measured
-    # in warm-up and amortised over the workload's MAX_ITERS iterations, so a
-    # 60-iteration sample stands for the full solve's rate instead of being
-    # dominated by a setup the full solve pays once
-    setups = []
-    for _ in range(max(args.warmup, 1)):
-        setups.append(cpu_oracle_solve(ps, 0)[1])
-        cpu_oracle_solve(ps, sample_iters)
-    setup = float(np.median(setups))
-    tot_ci, tot_t = 0, 0.0
-    for _ in range(args.steps):
-        ci, dt, _ = cpu_oracle_solve(ps, sample_iters)
+def reference_available() -> bool:
+    return os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "condsim"))
+
+
+def _cpu_scene_worker(job):
+    """One configs[2] scene stepped ``steps`` times on the host. kind
+    'reference': the reference condsim pipeline (baseline/_ref) around this
+    repo's FEM matrices; kind 'port': the oracle restatement. Returns
+    (contact-iterations, sim steps, seconds)."""
+    E, drop, yaw, steps, kind = job
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    sys.path.insert(0, ROOT)
+    if kind == "reference":
+        sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    from oracle import fem_host  # the checker's host restatement (bench CPU leg only)
+    from paper_2201_09212_b200.scenes import FemCube
+
+    cube = FemCube(nx=NX, E=E, drop=drop, yaw=yaw)
+    run = fem_host.reference_steps if kind == "reference" else fem_host.oracle_steps
+    t0 = time.perf_counter()
+    ci = run(cube, steps, residual_tol=TOL, max_iters=MAX_ITERS)
+    return ci, steps, time.perf_counter() - t0
+
+
+class CpuPool:
+    def __init__(self, procs):
+        import multiprocessing as mp
+
+        self.procs = procs
+        self.pool = mp.get_context("spawn").Pool(procs)
+
+    def sample(self, first_scene, steps, kind):
+        E, drop, yaw = scene_params()
+        jobs = [(float(E[k % SCENES]), float(drop[k % SCENES]), float(yaw[k % SCENES]), steps, kind)
+                for k in range(first_scene, first_scene + self.procs)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_scene_worker, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+        return sum(r[0] for r in res), sum(r[1] for r in res), wall
+
+    def close(self):
+        self.pool.terminate()
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path on the host cores (rank 0 only)."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    kind = "reference" if reference_available() else "port"
+    procs = host_threads()
+    pool = CpuPool(procs)
+    for w in range(args.warmup):
+        pool.sample(w * procs, 5, kind)  # process start-up, imports, first-call costs
+    tot_ci = tot_steps = 0
+    tot_t = 0.0
+    for k in range(args.steps):
+        ci, st, wall = pool.sample(k * procs, SIM_STEPS, kind)
         tot_ci += ci
-        tot_t += max(dt - setup, 0.0) + setup * sample_iters / MAX_ITERS
+        tot_steps += st
+        tot_t += wall
+    pool.close()
     val = tot_ci / tot_t
-    cores = 1  # scipy's CSC matvec and numpy's elementwise work run on one thread
+    sample = (f"per step: {procs} scenes of the configs[2] batch (scene k*{procs} onwards, cycling), one per "
+              f"process, each advanced all {SIM_STEPS} simulation steps through "
+              + ("the reference condsim pipeline from baseline/_ref (detect_contacts, nodalize, augment_dynamics, "
+                 "solve_vfpi, harness CG fallback) around this repo's FEM assembly" if kind == "reference" else
+                 "the oracle restatement of solve_vfpi (condsim not installed in baseline/_ref)"))
     line = {
         "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded configs[1])",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded configs[2])",
         "impl": "reference",
-        "config": {"workload": "configs[1] rigid-body contact system", "bodies": N_BODIES, "contacts": N_CONTACTS,
-                   "n": ps.n, "k_v": KV, "operator": "strict", "chebyshev": False, "tol": TOL,
-                   "sample_iters_per_step": sample_iters},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
-                         "sample": f"{sample_iters} V-FPI iterations of the full configs[1] system per step, the "
-                                   f"per-solve setup ({setup:.3f} s, measured in warm-up) amortised over "
-                                   f"{MAX_ITERS} iterations (numpy/scipy oracle restating "
-                                   "condsim.solver.solve_vfpi; single-threaded path)"},
+        "config": {"workload": "configs[2] batched FEM scenes (1024 x 200 steps)", "scenes": SCENES,
+                   "sim_steps": SIM_STEPS, "nodes_per_scene": NX ** 3, "seed": SEED, "operator": "strict",
+                   "tol": TOL, "max_iters": MAX_ITERS, "chebyshev": False},
+        "scene_steps_per_s": tot_steps / tot_t,
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_distributed(n):
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+class Shard:
+    """One rank's contiguous block of configs[2] scenes as device FemBatches."""
+
+    def __init__(self, rank, world, device, pinned=False):
+        from paper_2201_09212_b200.batch import shard_bounds
+        from paper_2201_09212_b200.fembatch import fem_batch_arrays
+        from paper_2201_09212_b200.scenes import fem_assemble
+
+        E, drop, yaw = scene_params()
+        self.lo, self.hi = shard_bounds(SCENES, world, rank)
+        t0 = time.perf_counter()
+        self.arrays, self.costs = [], []
+        for a in range(self.lo, self.hi, CHUNK):
+            b = min(a + CHUNK, self.hi)
+            plan, X, kd, ad, m3 = fem_assemble(NX, E[a:b], drop[a:b], yaw[a:b])
+            arr = fem_batch_arrays(plan, X, kd, ad, m3)
+            nnz = np.count_nonzero(ad, axis=1)  # A stores no zeros: nnz_num = stored entries
+            self.costs.append(bytes_per_scene_iter(nnz, plan["n"]).astype(np.float64))
+            self.arrays.append(arr)
+        self.build_s = time.perf_counter() - t0
+        self.device = device
+        self.n_scene = 3 * NX ** 3
+
+    def pin(self):
+        """Pinned host copies of every array vfpi_fem_create uploads (e2e leg)."""
+        import torch
+
+        def pin(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            return t, t.numpy()
+
+        self._pins, self.pinned = [], []
+        for (S, n, A, K, m, g, X, x, v, prm) in self.arrays:
+            ps = [pin(a) for a in (*A, *K, m, g, X, x, v)]
+            self._pins.append(ps)
+            arr = [p[1] for p in ps]
+            self.pinned.append((S, n, tuple(arr[0:3]), tuple(arr[3:6]), arr[6], arr[7], arr[8], arr[9], arr[10], prm))
+
+    def batches(self, arrays=None):
+        from paper_2201_09212_b200.fembatch import FemBatch
+
+        return [FemBatch(None, device=self.device, _arrays=a) for a in (arrays or self.arrays)]
+
+
+def dry_run(args):
+    """--dry-run: the rank/device/shard plan of `--gpus N` without touching a GPU
+    (gloo); rank 0 prints every rank's assignment (tests/test_bench_launch.py)."""
+    import torch.distributed as dist
+
+    from paper_2201_09212_b200 import _lib
+    from paper_2201_09212_b200.batch import shard_bounds
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    lo, hi = shard_bounds(SCENES, world, rank)
+    me = {"rank": rank, "local_rank": local, "device": _lib.default_device(), "scenes": [lo, hi], "pid": os.getpid()}
+    if world > 1:
+        dist.init_process_group("gloo")
+        allp = [None] * world
+        dist.all_gather_object(allp, me)
+        dist.destroy_process_group()
+    else:
+        allp = [me]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": allp}), flush=True)
+
+
 def run_ours(args):
     import torch
 
-    rank, world, local, dist = dist_setup(args.gpus)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
     from paper_2201_09212_b200 import _lib
-    from paper_2201_09212_b200.device import DeviceSystem
-    from paper_2201_09212_b200.scenes import rigid_contact_system
     from paper_2201_09212_b200.solver import SolverConfig
 
-    ps = rigid_contact_system(N_BODIES, N_CONTACTS, SEED, KV)
-    nnz_num = int(np.count_nonzero(ps.data))
     cfg = SolverConfig(operator="strict", residual_tol=TOL, max_iters=MAX_ITERS, chebyshev=False)
-    ds = DeviceSystem(ps, local)
-    warm = torch.zeros(ps.n, dtype=torch.float64, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.Stream(local)  # the solve and the timing events share this stream
-    torch.cuda.set_stream(stream)
-    h = _lib.handle(local)
+    h = _lib.handle()  # the rank's own device (torch's current device)
+    assert h.device == local, (h.device, local)
+    shard = Shard(rank, world, local)
+    batches = shard.batches()
+    stream = h.torch_stream()  # the pipeline's stream: events and collectives go here
+    n_scene = shard.n_scene
+    xs_local = torch.empty((shard.hi - shard.lo) * n_scene, dtype=torch.float64, device=dev)
+    gather_buf = [torch.empty_like(xs_local) for _ in range(world)] if (dist and rank == 0) else None
 
-    def one_step():
-        ds.enqueue(cfg, warm, stream)
+    def finish_run(counters):
+        """End of one configs[2] run: counters all-reduced, final x gathered to rank 0."""
+        with torch.cuda.stream(stream):
+            off = 0
+            for fb in batches:
+                xp, _ = fb.state_device_ptrs()
+                nb = fb.S * n_scene
+                _lib.lib().vfpi_memcpy_d2d(xs_local[off:off + nb].data_ptr(), xp, 8 * nb)
+                off += nb
+            if dist:
+                dist.all_reduce(counters, op=dist.ReduceOp.SUM)
+                dist.gather(xs_local, gather_buf, dst=0)
 
-    # warm-up (also grows the device workspace once)
+    def one_run(record=None):
+        ci = its = 0
+        loop_ms = setup_ms = kbytes = 0.0
+        max_it = div = 0
+        for fb in batches:
+            fb.reset()
+        for _ in range(SIM_STEPS):
+            for fb, cost in zip(batches, shard.costs):
+                st = fb.step(cfg, per_scene=True)
+                ci += st["contact_iterations"]
+                its += st["iterations"]
+                loop_ms += st["loop_ms"]
+                setup_ms += st["setup_ms"]
+                max_it = max(max_it, st["max_iterations"])
+                div += st["diverged_scenes"]
+                kbytes += float(np.dot(cost, st["iterations_per_scene"])) + 128.0 * st["contact_iterations"]
+        counters = torch.tensor([float(ci), float(its), float(div)], dtype=torch.float64, device=dev)
+        finish_run(counters)
+        return dict(ci=ci, its=its, loop_ms=loop_ms, setup_ms=setup_ms, kbytes=kbytes, max_it=max_it, div=div,
+                    counters=counters)
+
     for _ in range(args.warmup):
-        flush.fill_(1.0)
-        one_step()
-        ds.finish()
-    layout = h.last_layout()
+        one_run()
+    torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -229,146 +391,207 @@ def run_ours(args):
     torch.cuda.synchronize()
     sampler.active = True
     launches0 = h.launches()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    iters, loop_ms = [], []
-    for k in range(args.steps):
-        flush.fill_(1.0)  # evict L2 between timed steps (not timed)
-        ev[k][0].record(stream)
-        one_step()
-        ev[k][1].record(stream)
-        res = ds.finish()
-        iters.append(int(res.iterations))
-        loop_ms.append(float(res.loop_ms))
+    runs, step_ms = [], []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = one_run()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        runs.append(r)
     torch.cuda.synchronize()
-    launches = h.launches() - launches0
     if dist:
         dist.barrier()
     sampler.active = False
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    t_total = sum(step_ms) / 1e3
-    loop_avg_ms = sum(loop_ms) / len(loop_ms)
+    launches = h.launches() - launches0
 
-    # e2e through the C-ABI with pinned host buffers
-    e2e_steps = max(3, min(args.steps, 20))
-    pin = {}
-    for k in ("indptr", "indices", "data", "b", "col_i", "col_j", "frames", "mu", "mu2", "phi"):
-        a = getattr(ps, k)
-        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        pin[k] = t
-    from paper_2201_09212_b200.system import PackedSystem
-
-    pps = PackedSystem(ps.n, *[pin[k].numpy() for k in ("indptr", "indices", "data", "b", "col_i", "col_j",
-                                                         "frames", "mu", "mu2", "phi")])
-    h2d = sum(int(t.numel() * t.element_size()) for t in pin.values()) + 8 * ps.n  # + warm
-    warm_h = torch.zeros(ps.n, dtype=torch.float64).pin_memory().numpy()
-    out_v = torch.empty(ps.n, dtype=torch.float64).pin_memory().numpy()
-    out_l = torch.empty(3 * ps.n_c, dtype=torch.float64).pin_memory().numpy()
-    out_t = torch.empty(MAX_ITERS, dtype=torch.float64).pin_memory().numpy()
-    out_s = torch.empty(ps.n_c, dtype=torch.float64).pin_memory().numpy()
-    d2h = 8 * (out_v.size + out_l.size + out_t.size + out_s.size)
-    from paper_2201_09212_b200._lib import VfpiResult, ptr
-
-    def e2e_once():
-        res = VfpiResult()
-        res.v, res.lam, res.residual_trace, res.scc, res.w = ptr(out_v), ptr(out_l), ptr(out_t), ptr(out_s), None
-        code = h.L.vfpi_solve(h.h, pps.c_struct(), _c_cfg, ptr(warm_h), None, res)
-        assert code == 0, (code, h.error())
-        return res
-
-    from paper_2201_09212_b200.solver import _c_config
-
-    _c_cfg = _c_config(cfg)
-    e2e_once()
-    if dist:
-        dist.barrier()
-    e2e_t = 0.0
-    e2e_ci = 0
+    # e2e: the public API from pinned host buffers (creation uploads A, K and the
+    # state; 200 steps; final x and v downloaded), wall clock, max over ranks
+    shard.pin()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    for fb in batches:
+        fb.close()
+    e2e_t, e2e_ci = 0.0, 0
+    h2d = d2h = 0
+    xh = torch.empty(xs_local.numel(), dtype=torch.float64).pin_memory()
+    vh = torch.empty(xs_local.numel(), dtype=torch.float64).pin_memory()
     for _ in range(e2e_steps):
-        flush.fill_(1.0)
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = e2e_once()
+        batches = shard.batches(shard.pinned)
+        h2d = sum(fb.h2d_bytes for fb in batches)
+        r = one_run()
+        off = 0
+        for fb in batches:
+            nb = fb.S * n_scene
+            fb.state_into(xh.numpy()[off:off + nb], vh.numpy()[off:off + nb])
+            off += nb
+        d2h = 2 * 8 * off
         e2e_t += time.perf_counter() - t0
-        e2e_ci += ps.n_c * r.iterations
+        e2e_ci += r["ci"]
+        for fb in batches:
+            fb.close()
     sampler.stop()
 
-    ci_local = ps.n_c * sum(iters)
-    vals = torch.tensor([t_total, float(ci_local), e2e_t, float(e2e_ci), loop_avg_ms], dtype=torch.float64,
-                        device=dev)
+    ci_local = sum(r["ci"] for r in runs)
+    t_local = sum(step_ms) / 1e3
+    loop_local = sum(r["loop_ms"] for r in runs)
+    kbytes_local = sum(r["kbytes"] for r in runs)
+    vals = torch.tensor([t_local, float(ci_local), e2e_t, float(e2e_ci), loop_local, kbytes_local,
+                         float(sum(r["its"] for r in runs)), float(max(r["max_it"] for r in runs)),
+                         float(sum(r["div"] for r in runs)), max(step_ms)], dtype=torch.float64, device=dev)
     if dist:
-        mx = vals.clone()
+        mx, sm = vals.clone(), vals.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vals.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        t_max, ci_all, e2e_tmax, e2e_ci_all, loop_max = mx[0].item(), sm[1].item(), mx[2].item(), sm[3].item(), \
-            mx[4].item()
     else:
-        t_max, ci_all, e2e_tmax, e2e_ci_all, loop_max = t_total, ci_local, e2e_t, e2e_ci, loop_avg_ms
-
+        mx = sm = vals
+    t_max, ci_all, e2e_tmax, e2e_ci_all = mx[0].item(), sm[1].item(), mx[2].item(), sm[3].item()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
+    # roofline of the dominant kernel (the scene-batch V-FPI iteration kernel), rank 0's
+    # launches: algorithmic bytes of every launch / summed launch time (CUDA events
+    # around each launch on the pipeline stream)
     peak, peak_kind = peaks()
-    b_iter = algorithmic_bytes_per_iter(ps.n, nnz_num, ps.n_c)
-    mean_iters = sum(iters) / len(iters)
-    achieved = b_iter * mean_iters / (loop_max * 1e-3) / 1e9
+    achieved = kbytes_local / (loop_local * 1e-3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    prof = os.path.join(ROOT, "profiles", "r02_cfg2_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    launches_per_run = SIM_STEPS * len(shard.arrays)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        ci, dt, it = cpu_oracle_solve(ps, args.cpu_iters)
-        cpu = {"value": ci / dt, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
-               "sample": f"one solve of the full configs[1] system capped at {it} iterations "
-                         "(numpy/scipy oracle restating condsim.solver.solve_vfpi, setup included)"}
-    clocks = sampler.summary()
+        kind = "reference" if reference_available() else "port"
+        procs = host_threads()
+        pool = CpuPool(procs)
+        pool.sample(0, 2, kind)
+        ci_c, st_c, wall_c = pool.sample(0, SIM_STEPS, kind)
+        pool.close()
+        cpu = {"value": ci_c / wall_c, "unit": UNIT, "cores": procs, "kind": kind, "cpu_model": cpu_model(),
+               "scene_steps_per_s": st_c / wall_c,
+               "sample": f"the first {procs} scenes of the batch, one per process, all {SIM_STEPS} steps through "
+                         + ("the reference condsim pipeline (baseline/_ref) around this repo's FEM assembly"
+                            if kind == "reference" else "the oracle restatement")}
+    sub = {}
+    if not args.no_subrecords:
+        try:
+            sub["configs[1]"] = config1_subrecord(h, dev, peak)
+        except Exception as e:  # a sub-record never sinks the headline line
+            sub["configs[1]"] = {"error": repr(e)}
+    mean_its = sm[6].item() / (SCENES * SIM_STEPS * args.steps)
     line = {
         "metric": METRIC, "value": ci_all / t_max, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded configs[1])",
-        "config": {"workload": "configs[1] rigid-body contact system", "bodies": N_BODIES, "contacts": N_CONTACTS,
-                   "n": ps.n, "nnz_stored": ps.nnz, "nnz_numeric": nnz_num, "k_v": KV, "seed": SEED,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded configs[2])",
+        "config": {"workload": "configs[2] batched FEM scenes (1024 x 200 steps)", "scenes": SCENES,
+                   "scenes_per_rank": shard.hi - shard.lo, "sim_steps": SIM_STEPS, "nodes_per_scene": NX ** 3,
+                   "seed": SEED, "scene_params": "E ~ U[5e4, 2e5] Pa, drop ~ U[0.02, 0.1] m, yaw ~ U[0, 2 pi) "
+                                                 "from default_rng(2022)",
                    "operator": "strict", "step_strategy": "frobenius", "chebyshev": False, "tol": TOL,
-                   "max_iters": MAX_ITERS, "iterations_per_step": mean_iters,
-                   "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}"},
-        "roofline": {"bound": "hbm",
-                     "kernel": ("k_iterate_res (persistent, partition resident in shared memory)" if layout["resident"]
-                                else "k_iterate (persistent, SELL-32 streamed from global memory)"),
-                     "ctas": layout["ctas"],
+                   "max_iters": MAX_ITERS, "mean_vfpi_iterations_per_scene_step": mean_its,
+                   "max_vfpi_iterations": int(mx[7].item()), "diverged_scene_steps": int(sm[8].item()),
+                   "l2": "inputs larger than L2 (A + K of 1024 scenes ~2.3 GB), no flush",
+                   "parallelism": f"scene shards x{world} (contiguous blocks, no data-path collective; "
+                                  "NCCL all-reduce of counters + gather of final positions per run)",
+                   "host_build_s": shard.build_s},
+        "scene_steps_per_s": SCENES * SIM_STEPS * args.steps / t_max,
+        "roofline": {"bound": "hbm", "kernel": "k_iterate<scene batch> (one CTA per scene, TMA-ring SELL stream)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "bytes_per_iter": b_iter, "kernel_ms_per_launch": loop_max,
-                     "note": "A (9.4 MB numeric) + vectors stay L2-resident across the 1000 iterations of one "
-                             "launch: cache-resident working set, so frac can exceed what HBM alone allows"},
-        "e2e": {"value": e2e_ci_all / e2e_tmax, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                     "bytes_per_launch": kbytes_local / (launches_per_run * args.steps),
+                     "kernel_ms_per_launch": loop_local / (launches_per_run * args.steps),
+                     "launches_timed": launches_per_run * args.steps,
+                     "note": "algorithmic bytes per launch = sum over scenes of iterations x (12 nnz_num + 4 (n+1) "
+                             "+ 32 n) + 128 x contact-iterations (SURVEY §8(d)); time = CUDA events around each "
+                             "launch on the pipeline stream"},
+        "e2e": {"value": e2e_ci_all / e2e_tmax, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                "path": "FemBatch(pinned host arrays) -> 200 x FemBatch.step -> FemBatch.state (x, v to host)"},
         "gpu_launches": launches,
-        "clocks": clocks,
+        "clocks": sampler.summary(),
         "cpu_baseline": cpu,
+        "sub": sub,
     }
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
+def config1_subrecord(h, dev, peak):
+    """configs[1] (one coupled rigid-body system, 1000 iterations) as a nested record."""
+    import torch
+
+    from paper_2201_09212_b200.device import DeviceSystem
+    from paper_2201_09212_b200.scenes import rigid_contact_system
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    ps = rigid_contact_system(4096, 16384, 2201, 1e5)
+    nnz_num = int(np.count_nonzero(ps.data))
+    cfg = SolverConfig(operator="strict", residual_tol=1e-8, max_iters=1000, chebyshev=False)
+    ds = DeviceSystem(ps, h.device)
+    warm = torch.zeros(ps.n, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    for _ in range(3):
+        flush.fill_(1.0)
+        ds.enqueue(cfg, warm, stream)
+        ds.finish()
+    ms, loop, its = [], [], []
+    for _ in range(10):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ds.enqueue(cfg, warm, stream)
+        e1.record(stream)
+        res = ds.finish()
+        ms.append(e0.elapsed_time(e1))
+        loop.append(float(res.loop_ms))
+        its.append(int(res.iterations))
+    b_iter = 12 * nnz_num + 4 * (ps.n + 1) + 32 * ps.n + 128 * ps.n_c
+    lay = h.last_layout()
+    return {"workload": "configs[1] 4096 rigid bodies / 16,384 D-contacts, one 1000-iteration solve per step",
+            "value": ps.n_c * sum(its) / (sum(ms) * 1e-3), "unit": UNIT, "steps": len(ms),
+            "ms_per_step": sum(ms) / len(ms), "kernel_ms_per_launch": sum(loop) / len(loop),
+            "us_per_iteration": 1e3 * sum(loop) / sum(its),
+            "kernel": "k_iterate_res (persistent, partition resident in shared memory)" if lay["resident"]
+            else "k_iterate (streaming)",
+            "roofline": {"bound": "latency (working set on chip / in L2)",
+                         "algorithmic_GBps": b_iter * sum(its) / (sum(loop) * 1e-3) / 1e9,
+                         "frac_of_hbm_peak_if_streamed": b_iter * sum(its) / (sum(loop) * 1e-3) / 1e9 / peak,
+                         "note": "A is read from HBM once per solve; the per-iteration cost is L2 latency + one "
+                                 "grid barrier, so this is not an HBM fraction"},
+            "l2": "flushed (256 MB write) before every step"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-iters", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-subrecords", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="print the rank/device/shard plan only (no GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_distributed(args.gpus))
+    if args.dry_run:
+        dry_run(args)
+        return
+    run_ours(args)
 
 
 if __name__ == "__main__":

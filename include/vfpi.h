@@ -152,6 +152,10 @@ int vfpi_solve_scenes(vfpi_handle* h, const vfpi_system* sys, int32_t num_scenes
  * vfpi_fem_step assembles b, detects node-plane contacts (z < margin, frame
  * `frame9` for every contact), solves all scenes with vfpi_solve_scenes
  * semantics (warm start = the previous step's solution) and integrates.
+ * A scene whose solve diverges takes the reference's flagged contact-free
+ * step instead (harness.py:586-593): v_hat = CG(A, b, rtol 1e-10, maxiter
+ * 10 n) of that scene on the device, lam = 0; it is counted in
+ * diverged_scenes (the harness's any_diverged).
  * The handle is borrowed and must outlive the batch. */
 typedef struct vfpi_fem_batch vfpi_fem_batch;
 typedef struct vfpi_fem_params {
@@ -172,7 +176,26 @@ int vfpi_fem_create(vfpi_handle* h, int32_t num_scenes, int32_t nodes_per_scene,
 int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stats* stats,
                   int32_t* iterations_per_scene /* optional [num_scenes] */);
 int vfpi_fem_state(vfpi_fem_batch* fb, double* x, double* v);
+/* Restore the state the batch was created with (x, v; zero warm start),
+ * enqueued on the handle's stream: device-to-device, no host traffic. */
+int vfpi_fem_reset(vfpi_fem_batch* fb);
+/* Device pointers of the batch state x, v (n doubles each, scene-major),
+ * valid until vfpi_fem_destroy; ordered after work on the handle's stream. */
+int vfpi_fem_state_device(vfpi_fem_batch* fb, const double** x, const double** v);
 void vfpi_fem_destroy(vfpi_fem_batch* fb);
+
+/* Contact-free fallback step of a diverged solve (harness.py:586-593):
+ * x = CG(A, b, rtol, maxiter) from x0 = 0 with scipy.sparse.linalg.cg's
+ * recurrence, on device CSC arrays of the contact-free n x n system (read as
+ * rows), one cooperative grid, enqueued on `stream` (NULL = handle stream);
+ * returns after the solve with the iteration count in *iterations. */
+int vfpi_cg_device(vfpi_handle* h, int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
+                   const double* b, double* x, double rtol, int64_t maxiter, int32_t* iterations, void* stream);
+
+/* The handle's own CUDA stream (cudaStream_t): calls that take NULL for
+ * `stream`, and the FEM batch pipeline, enqueue their kernels here, so callers
+ * can time them with events recorded on it. */
+void* vfpi_stream(vfpi_handle* h);
 
 /* Number of kernels this library launched on the handle since creation. */
 int64_t vfpi_launch_count(const vfpi_handle* h);

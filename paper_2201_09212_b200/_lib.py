@@ -123,6 +123,9 @@ def lib() -> C.CDLL:
                 "vfpi_solve_device": (C.c_int, [H, sysp, cfgp, _f64p, _f64p, resp, C.c_void_p]),
                 "vfpi_wait": (C.c_int, [H, resp]),
                 "vfpi_launch_count": (C.c_int64, [H]),
+                "vfpi_stream": (C.c_void_p, [H]),
+                "vfpi_cg_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_double, C.c_int64, C.POINTER(C.c_int32), C.c_void_p]),
                 "vfpi_last_layout": (C.c_int, [H, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
                 "vfpi_set_kernel": (C.c_int, [H, C.c_int]),
                 "vfpi_set_profile": (C.c_int, [H, C.c_int]),
@@ -197,6 +200,16 @@ class Handle:
     def launches(self) -> int:
         return int(self.L.vfpi_launch_count(self.h))
 
+    def stream_ptr(self) -> int:
+        """The handle's own cudaStream_t (the FEM batch pipeline and NULL-stream
+        calls enqueue there): record timing events on it."""
+        return int(self.L.vfpi_stream(self.h) or 0)
+
+    def torch_stream(self):
+        import torch
+
+        return torch.cuda.ExternalStream(self.stream_ptr(), device=torch.device("cuda", self.device))
+
     def set_kernel(self, mode: str):
         """'auto' | 'resident' | 'streaming' for later solves on this handle."""
         code = {"auto": 0, "resident": 1, "streaming": 2}[mode]
@@ -219,10 +232,31 @@ class Handle:
 _tls = threading.local()
 
 
+def default_device() -> int:
+    """The device a handle binds to when none is given: torch's current CUDA
+    device when torch is imported and sees a GPU (a rank that called
+    ``torch.cuda.set_device(local_rank)``), else ``VFPI_DEVICE``, else
+    ``LOCAL_RANK`` (one process per GPU under torchrun), else 0."""
+    import sys
+
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized() or torch.cuda.is_available():
+                return int(torch.cuda.current_device())
+        except Exception:
+            pass
+    for var in ("VFPI_DEVICE", "LOCAL_RANK"):
+        val = os.environ.get(var)
+        if val not in (None, ""):
+            return int(val)
+    return 0
+
+
 def handle(device: int | None = None) -> Handle:
-    """Thread-local handle for ``device`` (default: current torch device or 0)."""
+    """Thread-local handle for ``device`` (default: ``default_device()``)."""
     if device is None:
-        device = int(os.environ.get("VFPI_DEVICE", "0"))
+        device = default_device()
     hs = getattr(_tls, "handles", None)
     if hs is None:
         hs = _tls.handles = {}

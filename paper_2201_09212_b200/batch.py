@@ -148,7 +148,7 @@ def shard_bounds(num_scenes: int, world: int, rank: int) -> tuple[int, int]:
     return lo, hi
 
 
-def solve_scenes_sharded(scenes: list, cfg: SolverConfig, warms=None, group=None, solver=None):
+def solve_scenes_sharded(scenes: list, cfg: SolverConfig, warms=None, group=None, solver=None, device=None):
     """Multi-rank scene batch. Every rank passes the same scene list; rank r
     solves its contiguous block with ``solver`` (default: the GPU
     ``solve_scenes`` on the rank's device) and rank 0 receives every scene's
@@ -165,7 +165,9 @@ def solve_scenes_sharded(scenes: list, cfg: SolverConfig, warms=None, group=None
     my_w = None if warms is None else warms[lo:hi]
     t0 = time.perf_counter()
     if solver is None:
-        local, _ = solve_scenes(mine, cfg, my_w) if mine else ([], None)
+        if device is None:
+            device = _lib.default_device()  # the rank's own GPU (torch's current device / LOCAL_RANK)
+        local, _ = solve_scenes(mine, cfg, my_w, device=device) if mine else ([], None)
     else:
         local = [solver(s, cfg, None if my_w is None else my_w[k]) for k, s in enumerate(mine)]
     dt = time.perf_counter() - t0

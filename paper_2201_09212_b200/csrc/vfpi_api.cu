@@ -294,7 +294,7 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.uval, &h->ws.uorder, &h->ws.row_list2, &h->ws.row_slot2, &h->ws.rowblk,
                             &h->ws.scene_rows, &h->ws.scene_cts, &h->ws.vbuf,
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
-                            &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof};
+                            &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof, &h->ws.cg_vec, &h->ws.cg_part};
   for (auto* b : bufs)
     if (b->p) cudaFree(b->p);
   vfpi::AugmentWork& aw = h->aug;
@@ -332,6 +332,35 @@ void vfpi_destroy(vfpi_handle* h) {
 const char* vfpi_last_error(const vfpi_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 int64_t vfpi_launch_count(const vfpi_handle* h) { return h ? h->launches : 0; }
+
+void* vfpi_stream(vfpi_handle* h) { return h ? (void*)h->ws.stream : nullptr; }
+
+int vfpi_cg_device(vfpi_handle* h, int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
+                   const double* b, double* x, double rtol, int64_t maxiter, int32_t* iterations, void* stream) {
+  if (!h || n < 0 || (n > 0 && (!indptr || !indices || !data || !b || !x))) return VFPI_BAD_ARGUMENT;
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  if (n == 0) {
+    if (iterations) *iterations = 0;
+    return VFPI_OK;
+  }
+  Workspace& ws = h->ws;
+  const int G = vfpi::cg_grid_partials(ws.device);
+  CK(vfpi::ensure(ws.cg_vec, 8 * 3 * (size_t)n));
+  CK(vfpi::ensure(ws.cg_part, 8 * 2 * (size_t)G + 8));
+  double* r = P<double>(ws.cg_vec);
+  if (vfpi::launch_cg_grid(G, n, indptr, indices, data, b, x, r, r + n, r + 2 * n, P<double>(ws.cg_part), rtol,
+                           maxiter, P<int32_t>(ws.cg_part) + 4 * G, st)) {
+    h->err = "fallback CG launch failed";
+    return VFPI_CUDA_ERROR;
+  }
+  ++h->launches;
+  int32_t it = 0;
+  CK(cudaMemcpyAsync(&it, P<int32_t>(ws.cg_part) + 4 * G, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (iterations) *iterations = it;
+  return VFPI_OK;
+}
 
 int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (!h) return VFPI_BAD_ARGUMENT;
@@ -1068,6 +1097,8 @@ struct vfpi_fem_batch {
   std::vector<vfpi::SolveStatus> stat;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   Workspace::Buf zero_cts, ks_off, ks_val, ks_col;  // K in SELL-32
+  Workspace::Buf cg_r, cg_p, cg_q, cg_list;        // contact-free fallback of diverged scenes
+  Workspace::Buf x0, v0;                           // initial state (vfpi_fem_reset)
   uint64_t layout_epoch = ~0ull;  // the handle workspace holds our contact-free layout
 };
 
@@ -1113,6 +1144,10 @@ int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a,
       (rc = fem_upload(h, fb->X, rest_x, 8 * n)) || (rc = fem_upload(h, fb->x, x, 8 * n)) ||
       (rc = fem_upload(h, fb->v, v, 8 * n)) || (rc = fem_upload(h, fb->frame, frame9, 72)))
     return fail(rc);
+  if (vfpi::ensure(fb->x0, 8 * n) || vfpi::ensure(fb->v0, 8 * n) ||
+      cudaMemcpy(fb->x0.p, fb->x.p, 8 * n, cudaMemcpyDeviceToDevice) ||
+      cudaMemcpy(fb->v0.p, fb->v.p, 8 * n, cudaMemcpyDeviceToDevice))
+    return fail(VFPI_CUDA_ERROR);
   for (Workspace::Buf* bb : {&fb->warm, &fb->vhat, &fb->b}) {
     if (vfpi::ensure(*bb, 8 * n) != cudaSuccess) return fail(VFPI_CUDA_ERROR);
   }
@@ -1242,6 +1277,34 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
                             nullptr, P<double>(fb->vhat), P<double>(fb->lam), nullptr, nullptr, fb->stat.data(), st,
                             &su, &lo, max_ct);
   if (rc) return rc;
+  // (3b) diverged scenes take the flagged contact-free step (harness.py:586-593):
+  // v_hat = cg(A, b, rtol=1e-10, maxiter=10 n) of the scene, lam = 0
+  {
+    std::vector<int32_t> div;
+    for (int k = 0; k < fb->S; ++k)
+      if (fb->stat[k].diverged) div.push_back(k);
+    if (!div.empty()) {
+      const size_t n = (size_t)fb->n;
+      CK(vfpi::ensure(fb->cg_r, 8 * n));
+      CK(vfpi::ensure(fb->cg_p, 8 * n));
+      CK(vfpi::ensure(fb->cg_q, 8 * n));
+      CK(vfpi::ensure(fb->cg_list, 4 * (size_t)fb->S));
+      CK(cudaMemcpyAsync(fb->cg_list.p, div.data(), 4 * div.size(), cudaMemcpyHostToDevice, st));
+      const int64_t ns = 3 * (int64_t)fb->Nn;
+      if (vfpi::launch_cg_scenes((int)div.size(), P<int32_t>(fb->cg_list), ns, fb->A.indptr, fb->A.indices,
+                                 fb->A.data, P<double>(fb->b), P<double>(fb->vhat), P<double>(fb->cg_r),
+                                 P<double>(fb->cg_p), P<double>(fb->cg_q), 1e-10, 10 * ns, nullptr, st)) {
+        h->err = "fallback CG launch failed";
+        return VFPI_CUDA_ERROR;
+      }
+      ++h->launches;
+      for (int k : div) {
+        const int c0 = fb->h_cts[k], c1 = fb->h_cts[k + 1];
+        if (c1 > c0) CK(cudaMemsetAsync(P<double>(fb->lam) + 3 * (size_t)c0, 0, 24 * (size_t)(c1 - c0), st));
+      }
+      CK(cudaStreamSynchronize(st));  // `div` is a host buffer of the async copy
+    }
+  }
   // (4) midpoint integration; the solution warm-starts the next step
   vfpi::launch_fem_advance(fb->n, q.dt, P<double>(fb->vhat), P<double>(fb->x), P<double>(fb->v),
                            P<double>(fb->warm), st);
@@ -1272,6 +1335,25 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   return VFPI_OK;
 }
 
+int vfpi_fem_reset(vfpi_fem_batch* fb) {
+  if (!fb) return VFPI_BAD_ARGUMENT;
+  vfpi_handle* h = fb->h;
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  cudaStream_t st = h->ws.stream;
+  const size_t n = (size_t)fb->n;
+  CK(cudaMemcpyAsync(fb->x.p, fb->x0.p, 8 * n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(fb->v.p, fb->v0.p, 8 * n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(fb->warm.p, 0, 8 * n, st));
+  return VFPI_OK;
+}
+
+int vfpi_fem_state_device(vfpi_fem_batch* fb, const double** x, const double** v) {
+  if (!fb) return VFPI_BAD_ARGUMENT;
+  if (x) *x = (const double*)fb->x.p;
+  if (v) *v = (const double*)fb->v.p;
+  return VFPI_OK;
+}
+
 int vfpi_fem_state(vfpi_fem_batch* fb, double* x, double* v) {
   if (!fb) return VFPI_BAD_ARGUMENT;
   vfpi_handle* h = fb->h;
@@ -1288,7 +1370,8 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
   for (Workspace::Buf* b : {&fb->a_indptr, &fb->a_indices, &fb->a_data, &fb->krp, &fb->kc, &fb->kv, &fb->m, &fb->g,
                             &fb->X, &fb->x, &fb->v, &fb->warm, &fb->vhat, &fb->lam, &fb->b, &fb->ci, &fb->cj,
                             &fb->frames, &fb->mu, &fb->mu2, &fb->phi, &fb->flag, &fb->pos, &fb->cts, &fb->rows,
-                            &fb->frame, &fb->tmp, &fb->zero_cts, &fb->ks_off, &fb->ks_val, &fb->ks_col})
+                            &fb->frame, &fb->tmp, &fb->zero_cts, &fb->ks_off, &fb->ks_val, &fb->ks_col, &fb->cg_r,
+                            &fb->cg_p, &fb->cg_q, &fb->cg_list, &fb->x0, &fb->v0})
     if (b->p) cudaFree(b->p);
   if (fb->e0) cudaEventDestroy(fb->e0);
   if (fb->e1) cudaEventDestroy(fb->e1);

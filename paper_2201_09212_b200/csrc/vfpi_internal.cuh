@@ -208,6 +208,7 @@ struct Workspace {
   Buf rowmin, ukey, ukey_s, uval, uorder, row_list2, row_slot2, rowblk, scene_rows, scene_cts;
   Buf vbuf, lambuf, partials, status, summary, flags, cub_tmp;
   Buf x, y;  // scratch for per-op entry points
+  Buf cg_vec, cg_part;  // contact-free CG fallback (vfpi_cg_device)
   Buf prof;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -350,5 +351,14 @@ void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int
 void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st);
 void launch_csr_matvec(int64_t rows, const int* rp, const int* ci, const double* cx, const double* x, double* y,
                        cudaStream_t st);
+
+// ---- contact-free CG fallback of a diverged solve (vfpi_cg.cu) --------------
+int launch_cg_scenes(int num, const int32_t* scene_list, int64_t rows_per_scene, const int32_t* indptr,
+                     const int32_t* indices, const double* data, const double* b, double* x, double* r, double* p,
+                     double* q, double rtol, int64_t maxiter, int32_t* iters_out, cudaStream_t st);
+int cg_grid_partials(int device);
+int launch_cg_grid(int G, int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
+                   const double* b, double* x, double* r, double* p, double* q, double* partial, double rtol,
+                   int64_t maxiter, int32_t* iters_out, cudaStream_t st);
 
 }  // namespace vfpi

@@ -43,6 +43,10 @@ def _bind():
         L.vfpi_fem_step.argtypes = [C.c_void_p, C.POINTER(VfpiConfig), C.POINTER(_Stats), _lib._i32p]
         L.vfpi_fem_state.restype = C.c_int
         L.vfpi_fem_state.argtypes = [C.c_void_p, _lib._f64p, _lib._f64p]
+        L.vfpi_fem_reset.restype = C.c_int
+        L.vfpi_fem_reset.argtypes = [C.c_void_p]
+        L.vfpi_fem_state_device.restype = C.c_int
+        L.vfpi_fem_state_device.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
         L.vfpi_fem_destroy.restype = None
         L.vfpi_fem_destroy.argtypes = [C.c_void_p]
         L._fem_bound = True
@@ -64,31 +68,73 @@ def _block_diag(mats):
     return np.concatenate(ptrs), np.concatenate(idx), np.concatenate(val)
 
 
-class FemBatch:
-    """Device-resident batch of FemCube scenes (same node count, same dt/margin/mu)."""
+def fem_batch_arrays(plan, X, kd, ad, m3, dt=1e-3, margin=1e-4, beta_err=0.2, e_rest=0.0, rest_threshold=0.01,
+                     mu=0.5, gravity=-9.81, x=None, v=None):
+    """The host arrays ``vfpi_fem_create`` uploads, in their final dtypes, built
+    from ``scenes.fem_assemble``'s batched output without per-scene objects: A
+    drops exact zeros per scene like the scipy sum ``FemCube`` uses; K is
+    bitwise symmetric, so its CSC arrays are its CSR arrays."""
+    S, nk = kd.shape
+    n = plan["n"]
+    keep = ad != 0
+    cnt = np.add.reduceat(keep.astype(np.int64), plan["indptr"][:-1], axis=1)     # (S, n)
+    a_ptr = np.zeros(S * n + 1, dtype=np.int64)
+    np.cumsum(cnt.ravel(), out=a_ptr[1:])
+    if a_ptr[-1] >= 2 ** 31 or S * nk >= 2 ** 31:
+        raise ValueError("FemBatch: more than 2^31 stored entries; split the batch")
+    off = (n * np.arange(S, dtype=np.int64))[:, None]
+    a_idx = (plan["indices"][None, :] + off)[keep].astype(np.int32)
+    a_val = ad[keep]
+    k_ptr = (plan["indptr"][None, :-1] + nk * np.arange(S, dtype=np.int64)[:, None]).ravel()
+    k_ptr = np.concatenate([k_ptr, [S * nk]])
+    k_idx = (plan["indices"][None, :] + off).ravel().astype(np.int32)
+    grav = np.zeros((S, n))
+    grav[:, 2::3] = gravity
+    Xf = np.ascontiguousarray(X.reshape(-1))
+    prm = _Params(dt, margin, beta_err, e_rest, rest_threshold, mu)
+    return (S, n, (a_ptr.astype(np.int32), a_idx, a_val), (k_ptr, k_idx, kd.reshape(-1)), m3.reshape(-1),
+            grav.reshape(-1), Xf, Xf.copy() if x is None else x.reshape(-1),
+            np.zeros(S * n) if v is None else v.reshape(-1), prm)
 
-    def __init__(self, cubes, device=None):
-        c0 = cubes[0]
-        for c in cubes:
-            if (c.n, c.dt, c.margin, c.beta, c.e_rest, c.thr, c.mu) != (c0.n, c0.dt, c0.margin, c0.beta, c0.e_rest,
-                                                                        c0.thr, c0.mu):
-                raise ValueError("scenes of a FemBatch share node count, dt, margin and contact parameters")
-        self.S, self.n_scene = len(cubes), c0.n
+
+class FemBatch:
+    """Device-resident batch of FemCube scenes (same node count, same dt/margin/mu).
+
+    ``FemBatch(cubes, device)`` takes ``scenes.FemCube`` objects;
+    ``FemBatch.assembled(...)`` takes ``scenes.fem_assemble``'s batched arrays
+    directly (configs[2]'s 1024 scenes without per-scene objects)."""
+
+    def __init__(self, cubes, device=None, _arrays=None):
+        if _arrays is None:
+            c0 = cubes[0]
+            for c in cubes:
+                if (c.n, c.dt, c.margin, c.beta, c.e_rest, c.thr, c.mu) != (c0.n, c0.dt, c0.margin, c0.beta,
+                                                                            c0.e_rest, c0.thr, c0.mu):
+                    raise ValueError("scenes of a FemBatch share node count, dt, margin and contact parameters")
+            a_ptr, a_idx, a_val = _block_diag([c.A for c in cubes])
+            ks = [c.K.tocsr() for c in cubes]
+            for km in ks:
+                km.sort_indices()
+            k_ptr, k_idx, k_val = _block_diag(ks)
+            cat = lambda f: as_f64(np.concatenate([np.asarray(f(c), float).ravel() for c in cubes]))  # noqa: E731
+            m, g, X, x, v = (cat(lambda c: c.m), cat(lambda c: c.gravity), cat(lambda c: c.X), cat(lambda c: c.x),
+                             cat(lambda c: c.v))
+            S, n_scene = len(cubes), c0.n
+            prm = _Params(c0.dt, c0.margin, c0.beta, c0.e_rest, c0.thr, c0.mu)
+        else:
+            S, n_scene, (a_ptr, a_idx, a_val), (k_ptr, k_idx, k_val), m, g, X, x, v, prm = _arrays
+        self.S, self.n_scene = S, n_scene
         self.h = _lib.handle(device)
+        self.device = self.h.device
         self.L = _bind()
-        a_ptr, a_idx, a_val = _block_diag([c.A for c in cubes])
-        ks = [c.K.tocsr() for c in cubes]
-        for km in ks:
-            km.sort_indices()
-        k_ptr, k_idx, k_val = _block_diag(ks)
         ntot = self.S * self.n_scene
         self._a = make_packed(ntot, a_ptr, a_idx, a_val, np.zeros(ntot), [], [], [], [])
         self._k = (np.ascontiguousarray(k_ptr, dtype=np.int64), as_i32(k_idx), as_f64(k_val))
-        cat = lambda f: as_f64(np.concatenate([np.asarray(f(c), float).ravel() for c in cubes]))  # noqa: E731
-        self._m, self._g, self._X = cat(lambda c: c.m), cat(lambda c: c.gravity), cat(lambda c: c.X)
-        x, v = cat(lambda c: c.x), cat(lambda c: c.v)
+        self._m, self._g, self._X = as_f64(m), as_f64(g), as_f64(X)
+        x, v = as_f64(x), as_f64(v)
+        self.h2d_bytes = int(sum(a.nbytes for a in (self._a.indptr, self._a.indices, self._a.data, *self._k, self._m,
+                                                     self._g, self._X, x, v)))
         frame = as_f64(contact_frame(np.array([0.0, 0.0, 1.0])).ravel())
-        prm = _Params(c0.dt, c0.margin, c0.beta, c0.e_rest, c0.thr, c0.mu)
         out = C.c_void_p()
         i64p = C.POINTER(C.c_int64)
         code = self.L.vfpi_fem_create(self.h.h, self.S, self.n_scene // 3, self._a.c_struct(), ptr(self._k[0], i64p),
@@ -96,6 +142,22 @@ class FemBatch:
                                       ptr(self._X), ptr(x), ptr(v), ptr(frame), C.byref(prm), C.byref(out))
         _raise_for(code, self.h)
         self.fb = out
+
+    @classmethod
+    def assembled(cls, plan, X, kd, ad, m3, device=None, **params):
+        """Batch straight from ``scenes.fem_assemble(nx, Es, drops, yaws)``: scene k is
+        bit-identical to ``FemCube.batch(...)[k]``."""
+        return cls(None, device=device, _arrays=fem_batch_arrays(plan, X, kd, ad, m3, **params))
+
+    def reset(self):
+        """Back to the creation state (device to device, on the handle's stream)."""
+        _raise_for(self.L.vfpi_fem_reset(self.fb), self.h)
+
+    def state_device_ptrs(self):
+        """(x, v) device pointers of the batch state (scene-major, n doubles each)."""
+        x, v = C.c_void_p(), C.c_void_p()
+        _raise_for(self.L.vfpi_fem_state_device(self.fb, C.byref(x), C.byref(v)), self.h)
+        return int(x.value), int(v.value)
 
     def step(self, cfg: SolverConfig, per_scene=False):
         st = _Stats()
@@ -113,6 +175,10 @@ class FemBatch:
         v = np.empty(self.S * self.n_scene)
         _raise_for(self.L.vfpi_fem_state(self.fb, ptr(x), ptr(v)), self.h)
         return x.reshape(self.S, -1, 3), v.reshape(self.S, -1, 3)
+
+    def state_into(self, x: np.ndarray, v: np.ndarray):
+        """Copy the device state into caller-owned (e.g. pinned) float64 host arrays."""
+        _raise_for(self.L.vfpi_fem_state(self.fb, ptr(x), ptr(v)), self.h)
 
     def close(self):
         if getattr(self, "fb", None):

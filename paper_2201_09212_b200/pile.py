@@ -353,14 +353,14 @@ class PileStepper:
     (``vfpi_solve_device``) and the midpoint integration (``vfpi_advance_device``).
     A_o and K stay resident; torch tensors are plain device memory here."""
 
-    def __init__(self, pile: CubePile, device: int = 0, detect: str = "device"):
+    def __init__(self, pile: CubePile, device: int | None = None, detect: str = "device"):
         import torch
 
         from . import _lib
 
-        self.pile, self.device, self.detect = pile, device, detect
         self.h = _lib.handle(device)
-        self.dev = torch.device("cuda", device)
+        self.pile, self.device, self.detect = pile, self.h.device, detect
+        self.dev = torch.device("cuda", self.device)
         up = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.dev)  # noqa: E731
         self.a = (up(pile.a_indptr, np.int32), up(pile.a_indices, np.int32), up(pile.a_data, np.float64))
         self.k = (up(pile.k_indptr, np.int64), up(pile.k_indices, np.int32), up(pile.k_data, np.float64))
@@ -512,17 +512,31 @@ class PileStepper:
         code = h.L.vfpi_wait(h.h, C.byref(res))
         if code not in (_lib.OK, _lib.DIVERGED):
             _raise_for(code, h)
+        diverged = code == _lib.DIVERGED
+        if diverged:
+            # the reference's flagged contact-free step (harness.py:586-593):
+            # v_hat = cg(A_o, b_o, rtol=1e-10, maxiter=10 n_o), virtual rows 0, lam = 0
+            cg_it = C.c_int32(0)
+            _raise_for(h.L.vfpi_cg_device(h.h, n_o, P(self.a[0]), P(self.a[1]), P(self.a[2]), P(b), P(vh), 1e-10,
+                                          10 * n_o, C.byref(cg_it), sp_), h)
+            vh[n_o:] = 0.0
+            lam.zero_()
         _raise_for(h.L.vfpi_advance_device(h.h, n_o, pile.dt, P(vh), P(self.x), P(self.v), sp_), h)
         self.prev = vh[:n_o].clone()
         it = int(res.iterations)
         scalars = torch.stack([zmin, 0.5 * torch.dot(self.m * self.v, self.v),
-                               trace[it - 1] if it > 0 else torch.zeros((), dtype=torch.float64, device=dev)])
+                               trace[it - 1] if it > 0 and not diverged else
+                               torch.zeros((), dtype=torch.float64, device=dev)])
         zmin_h, ke, resid = scalars.tolist()  # the step's one closing synchronisation
         max_pen = max(0.0, -zmin_h)
         self.steps += 1
         self.last = dict(v_hat=vh, lam=lam[: 3 * n_c], contacts=pc)
-        return dict(n_c=n_c, **counts, n=n, nnz=int(out.nnz),
-                    iterations=int(res.iterations), converged=bool(res.converged), diverged=code == _lib.DIVERGED,
+        # a diverged step reports iters 0 / residual 0 like the harness row
+        # (harness.py:549-553, the exception skips their assignment);
+        # vfpi_iterations is the V-FPI work the device did either way
+        return dict(n_c=n_c, **counts, n=n, nnz=int(out.nnz), vfpi_iterations=it,
+                    iterations=0 if diverged else it, converged=bool(res.converged) and not diverged,
+                    diverged=diverged,
                     setup_ms=float(res.setup_ms), loop_ms=float(res.loop_ms), detect_s=t_detect,
                     residual=resid, max_pen_m=max_pen, ke_J=ke,
                     wall_s=time.perf_counter() - t0)
@@ -577,8 +591,8 @@ def run_piles_sharded(n_scenes: int, steps: int, cfg, make_pile, stepper=None, g
         rows = []
         for _ in range(steps):
             r = st.step(cfg)
-            ci += r["n_c"] * r["iterations"]
-            its += r["iterations"]
+            ci += r["n_c"] * r.get("vfpi_iterations", r["iterations"])
+            its += r.get("vfpi_iterations", r["iterations"])
             nsteps += 1
             if keep_rows:
                 rows.append(dict(r))

@@ -112,94 +112,202 @@ def rigid_contact_parts(n_bodies: int = 4096, n_contacts: int = 16384, seed: int
 # ---------------------------------------------------------------------------
 # The reference has no FEM; this is the linear small-strain
 # assembly the SURVEY probe describes (Appendix C): 5 tets per hex with
-# alternating parity, K_e = V B^T C B, lumped mass rho V / 4 per tet node,
+# alternating parity, lumped mass rho V / 4 per tet node,
 # A = (2/dt) M + (dt/2) K, b = (2/dt) M v - K (x - X) + m g (Eq. 10 with the
 # elastic potential). Node-plane contacts follow the reference's
 # detect_contacts (contacts.py:159-200, NodeProxy radius 0, margin 1e-4) and
 # nodalize (contacts.py:271-321): one S-contact per node below the margin,
 # frame contact_frame(+z), phi = -(beta/dt) depth (+ restitution).
+#
+# The element stiffness is the isotropic closed form of V B^T C B,
+#   K_ab[p, q] = V (lam g_a[p] g_b[q] + mu (g_a[q] g_b[p] + delta_pq g_a . g_b)),
+# with g_a the barycentric gradients (rows of D^-1 from explicit cross
+# products), written as elementwise numpy only (no LAPACK/BLAS, whose kernels
+# differ between hosts), so every host produces the same bits; duplicates are
+# summed in element order into K's (column, row)-sorted pattern (np.add.at).
+# The plan depends only on nx, so a batch of scenes (configs[2]) assembles all
+# of them at once: ``fem_assemble`` vectorises over scenes and threads over
+# scene chunks, and a single cube is the batch of one.
 
 _EVEN = ((0, 1, 2, 4), (1, 3, 2, 7), (1, 4, 5, 7), (2, 4, 6, 7), (1, 2, 4, 7))
 _ODD = ((1, 0, 3, 5), (0, 2, 3, 6), (0, 4, 5, 6), (3, 5, 6, 7), (0, 3, 5, 6))
 
 
 def _tets(nx: int):
-    tets = []
-    idx = lambda i, j, k: i + nx * (j + nx * k)  # noqa: E731
-    for k in range(nx - 1):
-        for j in range(nx - 1):
-            for i in range(nx - 1):
-                c = [idx(i + (v & 1), j + ((v >> 1) & 1), k + ((v >> 2) & 1)) for v in range(8)]
-                for t in (_EVEN if (i + j + k) % 2 == 0 else _ODD):
-                    tets.append([c[a] for a in t])
-    return np.array(tets, dtype=np.int64)
+    """Tet connectivity of an nx^3-node grid, 5 tets per cell, parity-alternating split."""
+    i, j, k = np.meshgrid(np.arange(nx - 1), np.arange(nx - 1), np.arange(nx - 1), indexing="ij")
+    i, j, k = (a.transpose(2, 1, 0).ravel() for a in (i, j, k))  # i fastest, then j, then k
+    v = np.arange(8)
+    corners = ((i[:, None] + (v & 1)) + nx * ((j[:, None] + ((v >> 1) & 1)) + nx * (k[:, None] + ((v >> 2) & 1))))
+    even = ((i + j + k) % 2 == 0)[:, None, None]
+    loc = np.where(even, np.array(_EVEN)[None], np.array(_ODD)[None])  # (cells, 5, 4)
+    return np.take_along_axis(corners[:, None, :], loc, axis=2).reshape(-1, 4).astype(np.int64)
 
 
 def _elasticity(E, nu):
     lam = E * nu / ((1 + nu) * (1 - 2 * nu))
     mu = E / (2 * (1 + nu))
-    C = np.zeros((6, 6))
-    C[:3, :3] = lam
-    C[np.arange(3), np.arange(3)] += 2 * mu
-    C[np.arange(3, 6), np.arange(3, 6)] = mu
-    return C
+    return lam, mu
+
+
+_PLANS: dict = {}
+
+
+def _fem_plan(nx: int):
+    """Sparsity plan of the nx^3 cube (cached): tets, K's CSC pattern (sorted
+    by column, then row) and the slot of every element entry in it."""
+    plan = _PLANS.get(nx)
+    if plan is not None:
+        return plan
+    tets = _tets(nx)
+    T = tets.shape[0]
+    n = 3 * nx ** 3
+    dof = (3 * tets[:, :, None] + np.arange(3)).reshape(T, 12)
+    rows = np.broadcast_to(dof[:, :, None], (T, 12, 12)).ravel()
+    cols = np.broadcast_to(dof[:, None, :], (T, 12, 12)).ravel()
+    key = cols * n + rows
+    uk, slot = np.unique(key, return_inverse=True)
+    indices = (uk % n).astype(np.int32)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(indptr, (uk // n) + 1, 1)
+    indptr = np.cumsum(indptr)
+    diag = (uk % n) == (uk // n)
+    plan = dict(tets=tets, slot=slot.astype(np.int32).reshape(T, 144), indices=indices, indptr=indptr, diag=diag,
+                n=n, nnz=int(uk.shape[0]))
+    _PLANS[nx] = plan
+    return plan
+
+
+def fem_rest_positions(nx, side, drops, yaws):
+    """(S, nx^3, 3) rest positions: grid centred in x/y, bottom at z = 0, yawed
+    by ``yaws`` about z, lifted by ``drops``."""
+    h = side / (nx - 1)
+    g = np.arange(nx) * h - side / 2
+    z, y, x = np.meshgrid(g, g, g, indexing="ij")
+    x, y, z = x.ravel(), y.ravel(), z.ravel() + side / 2
+    cy = np.cos(np.asarray(yaws, dtype=np.float64))[:, None]
+    sy = np.sin(np.asarray(yaws, dtype=np.float64))[:, None]
+    drops = np.asarray(drops, dtype=np.float64)[:, None]
+    X = np.empty((cy.shape[0], x.shape[0], 3))
+    X[:, :, 0] = cy * x - sy * y
+    X[:, :, 1] = sy * x + cy * y
+    X[:, :, 2] = z[None, :] + drops
+    return X
+
+
+def _element_stiffness(X, tets, E, nu):
+    """Element matrices (S, T, 144) (rows 3a+p, columns 3b+q) and volumes (S, T)."""
+    S = X.shape[0]
+    P = X[:, tets]                                            # (S, T, 4, 3)
+    c0, c1, c2 = P[:, :, 1] - P[:, :, 0], P[:, :, 2] - P[:, :, 0], P[:, :, 3] - P[:, :, 0]
+
+    def cross(a, b):
+        return np.stack([a[..., 1] * b[..., 2] - a[..., 2] * b[..., 1],
+                         a[..., 2] * b[..., 0] - a[..., 0] * b[..., 2],
+                         a[..., 0] * b[..., 1] - a[..., 1] * b[..., 0]], axis=-1)
+
+    x12, x20, x01 = cross(c1, c2), cross(c2, c0), cross(c0, c1)
+    det = (c0[..., 0] * x12[..., 0] + c0[..., 1] * x12[..., 1]) + c0[..., 2] * x12[..., 2]
+    V = np.abs(det) / 6.0
+    r = np.stack([x12, x20, x01], axis=2) / det[..., None, None]   # rows of D^-1: grad lambda_1..3
+    g = np.concatenate([-((r[:, :, 0:1] + r[:, :, 1:2]) + r[:, :, 2:3]), r], axis=2)  # (S, T, 4, 3)
+    lam, mu = _elasticity(np.asarray(E, dtype=np.float64), nu)
+    lam = lam.reshape(S, 1, 1, 1, 1, 1)
+    mu = mu.reshape(S, 1, 1, 1, 1, 1)
+    gg = g[:, :, :, None, :, None] * g[:, :, None, :, None, :]           # [a, b, p, q] = g_a[p] g_b[q]
+    dot = (gg[..., 0, 0] + gg[..., 1, 1]) + gg[..., 2, 2]                # g_a . g_b
+    tr = gg.swapaxes(-1, -2).copy()                                      # g_a[q] g_b[p]
+    idx = np.arange(3)
+    tr[..., idx, idx] += dot[..., None]
+    ke = V[:, :, None, None, None, None] * (lam * gg + mu * tr)          # (S, T, a, b, p, q)
+    return ke.transpose(0, 1, 2, 4, 3, 5).reshape(S, tets.shape[0], 144), V
+
+
+def _assemble_chunk(X, E, nu, rho, plan, tet_block=1 << 17):
+    """K values (S, nnz_K) on the plan's pattern and lumped nodal masses
+    (S, nodes): element entries added into their slots with ``np.add.at``
+    (unbuffered, in element order -- the sum order is the tet order whatever
+    the blocking)."""
+    tets, slot, nk = plan["tets"], plan["slot"], plan["nnz"]
+    S, nn = X.shape[0], X.shape[1]
+    kd = np.zeros(S * nk)
+    mass = np.zeros(S * nn)
+    soff = (nk * np.arange(S, dtype=np.int64))[:, None, None]
+    noff = (nn * np.arange(S, dtype=np.int64))[:, None, None]
+    step = max(1, tet_block // S)
+    for t0 in range(0, tets.shape[0], step):
+        t1 = min(t0 + step, tets.shape[0])
+        ke, V = _element_stiffness(X, tets[t0:t1], E, nu)
+        np.add.at(kd, (slot[None, t0:t1] + soff).ravel(), ke.ravel())
+        np.add.at(mass, (tets[None, t0:t1] + noff).ravel(), np.repeat((rho * V / 4.0).ravel(), 4))
+    return kd.reshape(S, nk), mass.reshape(S, nn)
+
+
+def fem_assemble(nx, Es, drops, yaws, side=0.1, nu=0.3, rho=1000.0, dt=1e-3, chunk=8, threads=None):
+    """Batched assembly of ``len(Es)`` cubes sharing nx: returns the plan, rest
+    positions (S, nodes, 3), K values (S, nnz_K), A values on K's pattern
+    (S, nnz_K; exact zeros are dropped per scene, as scipy's sparse sum does),
+    masses (S, n). Threads over scene chunks (numpy releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    plan = _fem_plan(nx)
+    Es = np.atleast_1d(np.asarray(Es, dtype=np.float64))
+    S = Es.shape[0]
+    X = fem_rest_positions(nx, side, np.broadcast_to(drops, (S,)), np.broadcast_to(yaws, (S,)))
+    kd = np.empty((S, plan["nnz"]))
+    mass = np.empty((S, X.shape[1]))
+
+    def work(a):
+        b = min(a + chunk, S)
+        kd[a:b], mass[a:b] = _assemble_chunk(X[a:b], Es[a:b], nu, rho, plan)
+
+    starts = list(range(0, S, chunk))
+    if len(starts) == 1:
+        work(0)
+    else:
+        import os
+
+        with ThreadPoolExecutor(threads or min(len(starts), len(os.sched_getaffinity(0)))) as ex:
+            list(ex.map(work, starts))
+    m3 = np.repeat(mass, 3, axis=1)
+    # A = diags((2/dt) m) + (dt/2) K, as scipy's sparse sum forms it (entrywise a + b)
+    ad = (dt / 2.0) * kd
+    ad[:, plan["diag"]] = (2.0 / dt) * m3 + ad[:, plan["diag"]]
+    return plan, X, kd, ad, m3
 
 
 class FemCube:
     """One deformable cube (configs[0] defaults; configs[2] varies E, drop, yaw)."""
 
     def __init__(self, nx=10, side=0.1, E=1e5, nu=0.3, rho=1000.0, drop=0.05, yaw=0.0, dt=1e-3, mu=0.5,
-                 gravity=-9.81, margin=1e-4, beta_err=0.2, e_rest=0.0, rest_threshold=0.01):
+                 gravity=-9.81, margin=1e-4, beta_err=0.2, e_rest=0.0, rest_threshold=0.01, _parts=None):
         self.nx, self.dt, self.mu = nx, dt, mu
         self.margin, self.beta, self.e_rest, self.thr = margin, beta_err, e_rest, rest_threshold
-        h = side / (nx - 1)
-        g = np.arange(nx) * h - side / 2
-        z, y, x = np.meshgrid(g, g, g, indexing="ij")
-        X = np.stack([x.ravel(), y.ravel(), z.ravel() + side / 2], axis=1)
-        cy, sy = np.cos(yaw), np.sin(yaw)
-        X = X @ np.array([[cy, -sy, 0.0], [sy, cy, 0.0], [0.0, 0.0, 1.0]]).T
-        X[:, 2] += drop
+        if _parts is None:
+            plan, X, kd, ad, m3 = fem_assemble(nx, [E], [drop], [yaw], side=side, nu=nu, rho=rho, dt=dt)
+            _parts = (plan, X[0], kd[0], ad[0], m3[0])
+        plan, X, kd, ad, m3 = _parts
+        n = plan["n"]
         self.X = X
         self.x = X.copy()
         self.v = np.zeros_like(X)
-        tets = _tets(nx)
-        C = _elasticity(E, nu)
-        nn = X.shape[0]
-        # all tets at once: D = [P1-P0, P2-P0, P3-P0] (columns), grad lambda_1..3 = rows of D^-1
-        P = X[tets]                                   # (T, 4, 3)
-        D = np.stack([P[:, 1] - P[:, 0], P[:, 2] - P[:, 0], P[:, 3] - P[:, 0]], axis=2)
-        V = np.abs(np.linalg.det(D)) / 6.0
-        Gi = np.linalg.inv(D)                         # (T, 3, 3)
-        grads = np.concatenate([-Gi.sum(axis=1, keepdims=True), Gi], axis=1)  # (T, 4, 3)
-        T = tets.shape[0]
-        B = np.zeros((T, 6, 12))
-        for a in range(4):
-            gx, gy, gz = grads[:, a, 0], grads[:, a, 1], grads[:, a, 2]
-            c0 = 3 * a
-            B[:, 0, c0], B[:, 1, c0 + 1], B[:, 2, c0 + 2] = gx, gy, gz
-            B[:, 3, c0], B[:, 3, c0 + 1] = gy, gx
-            B[:, 4, c0 + 1], B[:, 4, c0 + 2] = gz, gy
-            B[:, 5, c0], B[:, 5, c0 + 2] = gz, gx
-        Ke = V[:, None, None] * np.einsum("tji,jk,tkl->til", B, C, B)
-        dof = (3 * tets[:, :, None] + np.arange(3)).reshape(T, 12)
-        rows = [np.broadcast_to(dof[:, :, None], (T, 12, 12)).ravel()]
-        cols = [np.broadcast_to(dof[:, None, :], (T, 12, 12)).ravel()]
-        vals = [Ke.ravel()]
-        mass = np.zeros(nn)
-        np.add.at(mass, tets.ravel(), np.repeat(rho * V / 4.0, 4))
-        n = 3 * nn
-        K = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n)).tocsc()
-        K.sum_duplicates()
-        self.K = K
-        self.m = np.repeat(mass, 3)
+        self.K = sp.csc_matrix((kd, plan["indices"], plan["indptr"]), shape=(n, n))
+        keep = ad != 0  # the sparse sum drops exact zeros
+        cnt = np.zeros(n + 1, dtype=np.int64)
+        cnt[1:] = np.add.reduceat(keep.astype(np.int64), plan["indptr"][:-1])
+        self.A = sp.csc_matrix((ad[keep], plan["indices"][keep], np.cumsum(cnt)), shape=(n, n))
+        self.m = m3
         self.gravity = np.zeros(n)
         self.gravity[2::3] = gravity
-        A = sp.diags((2.0 / dt) * self.m, format="csc") + (dt / 2.0) * K
-        A = sp.csc_matrix(A)
-        A.sum_duplicates()
-        A.sort_indices()
-        self.A = A
         self.n = n
+
+    @classmethod
+    def batch(cls, nx, Es, drops, yaws, side=0.1, nu=0.3, rho=1000.0, dt=1e-3, **kw):
+        """configs[2]: many cubes assembled in one vectorised pass (``fem_assemble``);
+        cube k is bit-identical to ``FemCube(nx, E=Es[k], drop=drops[k], yaw=yaws[k])``."""
+        plan, X, kd, ad, m3 = fem_assemble(nx, Es, drops, yaws, side=side, nu=nu, rho=rho, dt=dt)
+        return [cls(nx=nx, side=side, nu=nu, rho=rho, dt=dt, _parts=(plan, X[k], kd[k], ad[k], m3[k]), **kw)
+                for k in range(len(Es))]
 
     def contacts(self):
         """Node-plane contacts of the current configuration (reference detect + nodalize)."""
@@ -213,8 +321,12 @@ class FemCube:
         frame = contact_frame(np.array([0.0, 0.0, 1.0]))
         return nodes, phi, depth, frame
 
+    def rhs(self) -> np.ndarray:
+        """b = (2/dt) M v - K (x - X) + M g (per row in increasing column order)."""
+        return (2.0 / self.dt) * self.m * self.v.ravel() - self.K @ (self.x - self.X).ravel() + self.m * self.gravity
+
     def system(self) -> PackedSystem:
-        b = (2.0 / self.dt) * self.m * self.v.ravel() - self.K @ (self.x - self.X).ravel() + self.m * self.gravity
+        b = self.rhs()
         nodes, phi, depth, frame = self.contacts()
         n_c = nodes.shape[0]
         mu = np.full(n_c, self.mu)
