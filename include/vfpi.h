@@ -184,6 +184,31 @@ int vfpi_fem_reset(vfpi_fem_batch* fb);
 int vfpi_fem_state_device(vfpi_fem_batch* fb, const double** x, const double** v);
 void vfpi_fem_destroy(vfpi_fem_batch* fb);
 
+/* ---- configs[3] heightfield step pieces (device pointers, on `stream`) ----
+ * Node-vs-heightfield detection for z = amp sin(freq x) sin(freq y), the
+ * detect_contacts (contacts.py:159-227) + nodalize (contacts.py:271-321)
+ * contract for a surface the reference does not have: every node with
+ * z < h + margin is an S-contact on its own node (col_i = 3 node, col_j = -1),
+ * in node order; phi = neg_beta_dt * max(0, h - z); frame
+ * contact_frame((-hx, -hy, 1)/norm) with hx = slope cos(freq x) sin(freq y),
+ * hy = slope sin(freq x) cos(freq y). x: 3*nodes device doubles. Outputs are
+ * handle-owned device buffers valid until the next call; one host read. */
+typedef struct vfpi_heightfield_params {
+  double amp, freq, slope, margin, mu, neg_beta_dt;
+} vfpi_heightfield_params;
+typedef struct vfpi_heightfield_contacts {
+  int64_t n_c;
+  int32_t* col_i;
+  int32_t* col_j;
+  double* frames;
+  double* mu;
+  double* phi;
+} vfpi_heightfield_contacts;
+int vfpi_heightfield_contacts_device(vfpi_handle* h, const vfpi_heightfield_params* p, int64_t nodes,
+                                     const double* x, vfpi_heightfield_contacts* out, void* stream);
+/* b[i] += f[i] (the external load term of the right-hand side). */
+int vfpi_add_device(vfpi_handle* h, int64_t n, const double* f, double* b, void* stream);
+
 /* Contact-free fallback step of a diverged solve (harness.py:586-593):
  * x = CG(A, b, rtol, maxiter) from x0 = 0 with scipy.sparse.linalg.cg's
  * recurrence, on device CSC arrays of the contact-free n x n system (read as

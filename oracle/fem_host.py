@@ -4,6 +4,9 @@ Only ``tests/`` and ``bench.py``'s CPU legs (``cpu_baseline`` /
 ``--impl reference``) import this module; the product path steps scenes on
 the device (``fembatch.FemBatch`` / ``vfpi_fem_step``).
 
+* ``fem_rhs`` / ``fem_contacts`` / ``fem_system`` / ``fem_advance`` and
+  ``heightfield_*`` -- the host restatement of the device step pieces
+  (``csrc/vfpi_fem.cu``, ``csrc/vfpi_heightfield.cu``) they are checked against;
 * ``oracle_steps`` -- one ``scenes.FemCube`` advanced on the host with the
   oracle's ``solve`` (``vfpi_oracle.solve`` restating ``solver.py:345-461``)
   and the harness's contact-free CG fallback on divergence
@@ -22,7 +25,93 @@ from __future__ import annotations
 
 import numpy as np
 
+from paper_2201_09212_b200.system import PackedSystem, make_packed
+
 from . import vfpi_oracle as O
+
+
+# ---- configs[0]/[2]: one FEM cube on the plane z = 0 -------------------------
+
+def fem_rhs(cube) -> np.ndarray:
+    """b = (2/dt) M v - K (x - X) + M g (scipy's CSC matvec: per row in
+    increasing column order), the device's k_fem_rhs_sell."""
+    return (2.0 / cube.dt) * cube.m * cube.v.ravel() - cube.K @ (cube.x - cube.X).ravel() + cube.m * cube.gravity
+
+
+def fem_contacts(cube):
+    """Node-plane contacts of the current state: the reference's
+    detect_contacts (contacts.py:159-200, radius-0 node proxies, margin) +
+    nodalize (:271-321) for S-contacts on nodes, frame contact_frame(+z),
+    phi from stabilization_term (:230-239)."""
+    from paper_2201_09212_b200.contacts import contact_frame
+
+    z = cube.x[:, 2]
+    nodes = np.nonzero(z < cube.margin)[0]
+    depth = np.maximum(0.0, -z[nodes])
+    phi = -(cube.beta / cube.dt) * depth
+    vn = cube.v[nodes, 2]
+    rest = np.abs(vn) > cube.thr
+    phi = np.where(rest, phi + cube.e_rest * np.minimum(0.0, vn), phi)
+    frame = contact_frame(np.array([0.0, 0.0, 1.0]))
+    return nodes, phi, depth, frame
+
+
+def fem_system(cube) -> PackedSystem:
+    """The step's system (A, b, contacts) as ``solve_vfpi`` consumes it."""
+    b = fem_rhs(cube)
+    nodes, phi, depth, frame = fem_contacts(cube)
+    n_c = nodes.shape[0]
+    mu = np.full(n_c, cube.mu)
+    return make_packed(cube.n, cube.A.indptr, cube.A.indices, cube.A.data, b, 3 * nodes,
+                       np.full(n_c, -1), np.tile(frame.ravel(), n_c), mu, mu, phi)
+
+
+def fem_advance(cube, v_hat):
+    """Midpoint integration (dynamics.py:237-255 for particles)."""
+    vh = np.asarray(v_hat)[: cube.n].reshape(-1, 3)
+    cube.x = cube.x + cube.dt * vh
+    cube.v = 2.0 * vh - cube.v
+
+
+# ---- configs[3]: the block pressed onto the heightfield ----------------------
+
+def heightfield_rhs(blk) -> np.ndarray:
+    """fem_rhs + the top-face load (added last, as the device does)."""
+    return fem_rhs(blk) + blk.f_ext
+
+
+def heightfield_contacts(blk):
+    """Nodes within the margin of z = amp sin(freq x) sin(freq y) (node order):
+    depth max(0, h - z), phi = -(beta/dt) depth, normal (-hx, -hy, 1)/norm with
+    hx = (amp freq) cos(freq x) sin(freq y), hy = (amp freq) sin(freq x) cos(freq y),
+    frames contact_frame(normal) -- the device's k_hf_contacts operation for operation."""
+    from paper_2201_09212_b200.scenes import hf_sincos
+
+    from .pile_host import contact_frames
+
+    x, y, z = blk.x[:, 0], blk.x[:, 1], blk.x[:, 2]
+    sx, cx = hf_sincos(blk.freq * x)
+    sy, cy = hf_sincos(blk.freq * y)
+    h = (blk.amp * sx) * sy
+    nodes = np.nonzero(z < h + blk.margin)[0]
+    depth = np.maximum(0.0, h[nodes] - z[nodes])
+    phi = -(blk.beta / blk.dt) * depth
+    slope = blk.amp * blk.freq
+    hx = (slope * cx[nodes]) * sy[nodes]
+    hy = (slope * sx[nodes]) * cy[nodes]
+    norm = np.sqrt((hx * hx + hy * hy) + 1.0)
+    normals = np.stack([-hx / norm, -hy / norm, 1.0 / norm], axis=1)
+    frames = contact_frames(normals) if len(nodes) else np.zeros((0, 3, 3))
+    return nodes, phi, depth, frames
+
+
+def heightfield_system(blk) -> PackedSystem:
+    b = heightfield_rhs(blk)
+    nodes, phi, depth, frames = heightfield_contacts(blk)
+    n_c = nodes.shape[0]
+    mu = np.full(n_c, blk.mu)
+    return make_packed(blk.n, blk.A.indptr, blk.A.indices, blk.A.data, b, 3 * nodes, np.full(n_c, -1),
+                       frames.reshape(-1), mu, mu, phi)
 
 
 def _cg_fallback(cube, b):
@@ -41,7 +130,7 @@ def oracle_steps(cube, steps, residual_tol=1e-8, max_iters=500, chebyshev=False,
     ci = 0
     cfg = O.Config(residual_tol=residual_tol, max_iters=max_iters, chebyshev=chebyshev, **cfg_extra)
     for _ in range(steps):
-        ps = cube.system()
+        ps = fem_system(cube)
         s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64),
                      ps.col_j.astype(np.int64), ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
         warm = np.zeros(ps.n) if prev is None else prev
@@ -54,7 +143,7 @@ def oracle_steps(cube, steps, residual_tol=1e-8, max_iters=500, chebyshev=False,
         ci += ps.n_c * it
         if record is not None:
             record.append(dict(n_c=ps.n_c, iterations=it, diverged=div, v=v.copy(), lam=lam.copy()))
-        cube.advance(v)
+        fem_advance(cube, v)
         prev = v
     return ci
 
@@ -79,7 +168,7 @@ def reference_steps(cube, steps, residual_tol=1e-8, max_iters=500, chebyshev=Fal
     prev = None
     ci = 0
     for step in range(steps):
-        b = cube.rhs()
+        b = fem_rhs(cube)
         state = SystemState(cube.x.ravel().copy(), cube.v.ravel().copy(), step, cube.dt)
         raw = detect_contacts(state, bodies, geom)
         nodal = nodalize(raw, state, bodies, k_v, cube.mu, None, StabilizationParams(dt=cube.dt))
@@ -98,6 +187,6 @@ def reference_steps(cube, steps, residual_tol=1e-8, max_iters=500, chebyshev=Fal
         ci += n_c * it
         if record is not None:
             record.append(dict(n_c=n_c, iterations=it, diverged=div, v=np.asarray(v).copy()))
-        cube.advance(v)
+        fem_advance(cube, v)
         prev = v
     return ci

@@ -96,6 +96,16 @@ class VfpiNodalContacts(C.Structure):
     ]
 
 
+class VfpiHeightfieldParams(C.Structure):
+    _fields_ = [("amp", C.c_double), ("freq", C.c_double), ("slope", C.c_double), ("margin", C.c_double),
+                ("mu", C.c_double), ("neg_beta_dt", C.c_double)]
+
+
+class VfpiHeightfieldContacts(C.Structure):
+    _fields_ = [("n_c", C.c_int64), ("col_i", _i32p), ("col_j", _i32p), ("frames", _f64p), ("mu", _f64p),
+                ("phi", _f64p)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -142,6 +152,10 @@ def lib() -> C.CDLL:
                 "vfpi_pile_contacts_device": (C.c_int, [H, C.POINTER(VfpiPileGeometry), C.c_void_p, C.c_void_p,
                                                         C.POINTER(VfpiPileContacts), C.c_void_p]),
                 "vfpi_memcpy_d2d": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+                "vfpi_heightfield_contacts_device": (C.c_int, [H, C.POINTER(VfpiHeightfieldParams), C.c_int64,
+                                                               C.c_void_p, C.POINTER(VfpiHeightfieldContacts),
+                                                               C.c_void_p]),
+                "vfpi_add_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
                 "vfpi_sell_layout_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p,
                                                       C.POINTER(C.c_int64)]),
                 "vfpi_sell_pack_device": (C.c_int, [H, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -65,6 +65,7 @@ struct vfpi_handle {
   vfpi::AugmentWork aug;
   vfpi::PileWork pile;
   vfpi::NodalizeWork nod;
+  vfpi::HfWork hf;
   int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
@@ -314,6 +315,10 @@ void vfpi_destroy(vfpi_handle* h) {
                             &nw.fr, &nw.phi, &nw.mu, &nw.mu2, &nw.jrp, &nw.jci, &nw.jcx})
     if (b->p) cudaFree(b->p);
   if (nw.h_small) cudaFreeHost(nw.h_small);
+  vfpi::HfWork& hw = h->hf;
+  for (auto* b : {&hw.flag, &hw.pos, &hw.tmp, &hw.ci, &hw.cj, &hw.fr, &hw.mu, &hw.phi})
+    if (b->p) cudaFree(b->p);
+  if (hw.h_small) cudaFreeHost(hw.h_small);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
   for (SetupGraphSet* gs : {&h->graph_layout, &h->graph_pack})
@@ -1549,6 +1554,34 @@ int vfpi_pile_contacts_device(vfpi_handle* h, const vfpi_pile_geometry* g, const
   out->jv_indptr = o.jv_indptr;
   out->jv_indices = o.jv_indices;
   out->jv_data = o.jv_data;
+  return VFPI_OK;
+}
+
+int vfpi_heightfield_contacts_device(vfpi_handle* h, const vfpi_heightfield_params* p, int64_t nodes,
+                                     const double* x, vfpi_heightfield_contacts* out, void* stream) {
+  if (!h || !p || !out || nodes < 0 || 3 * nodes > INT32_MAX || (nodes > 0 && !x)) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::HfParams hp{p->amp, p->freq, p->slope, p->margin, p->mu, p->neg_beta_dt};
+  vfpi::HfContactsOut o;
+  const int rc = vfpi::heightfield_contacts_device(h->hf, hp, nodes, x, st, o, h->err, h->launches);
+  if (rc != VFPI_OK) return rc;
+  out->n_c = o.n_c;
+  out->col_i = o.col_i;
+  out->col_j = o.col_j;
+  out->frames = o.frames;
+  out->mu = o.mu;
+  out->phi = o.phi;
+  return VFPI_OK;
+}
+
+int vfpi_add_device(vfpi_handle* h, int64_t n, const double* f, double* b, void* stream) {
+  if (!h || n < 0 || (n > 0 && (!f || !b))) return VFPI_BAD_ARGUMENT;
+  CK(cudaSetDevice(h->ws.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : h->ws.stream;
+  vfpi::launch_add_inplace(n, f, b, st);
+  h->launches += n > 0;
+  CK(cudaGetLastError());
   return VFPI_OK;
 }
 

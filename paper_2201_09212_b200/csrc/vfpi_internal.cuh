@@ -352,6 +352,26 @@ void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, doubl
 void launch_csr_matvec(int64_t rows, const int* rp, const int* ci, const double* cx, const double* x, double* y,
                        cudaStream_t st);
 
+// ---- configs[3] heightfield detection (vfpi_heightfield.cu) -----------------
+struct HfParams {
+  double amp, freq, slope, margin, mu, neg_beta_dt;
+};
+struct HfContactsOut {
+  int64_t n_c = 0;
+  int* col_i = nullptr;
+  int* col_j = nullptr;
+  double* frames = nullptr;
+  double* mu = nullptr;
+  double* phi = nullptr;
+};
+struct HfWork {
+  Workspace::Buf flag, pos, tmp, ci, cj, fr, mu, phi;
+  int64_t* h_small = nullptr;  // pinned [2]
+};
+int heightfield_contacts_device(HfWork& w, const HfParams& p, int64_t N, const double* x, cudaStream_t st,
+                                HfContactsOut& out, std::string& err, int64_t& launches);
+void launch_add_inplace(int64_t n, const double* f, double* b, cudaStream_t st);
+
 // ---- contact-free CG fallback of a diverged solve (vfpi_cg.cu) --------------
 int launch_cg_scenes(int num, const int32_t* scene_list, int64_t rows_per_scene, const int32_t* indptr,
                      const int32_t* indices, const double* data, const double* b, double* x, double* r, double* p,

@@ -29,14 +29,6 @@ namespace {
 constexpr int kT = 256;
 inline unsigned gridn(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + kT - 1) / kT); }
 
-__device__ __forceinline__ double dot3(const double* a, const double* b) {  // einsum 'ij,ij->i': sequential
-  return dadd(dadd(dmul(a[0], b[0]), dmul(a[1], b[1])), dmul(a[2], b[2]));
-}
-__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {  // np.cross
-  c[0] = dsub(dmul(a[1], b[2]), dmul(a[2], b[1]));
-  c[1] = dsub(dmul(a[2], b[0]), dmul(a[0], b[2]));
-  c[2] = dsub(dmul(a[0], b[1]), dmul(a[1], b[0]));
-}
 __device__ __forceinline__ long long cell_of(double c, double cell) { return (long long)floor(ddiv(c, cell)); }
 __device__ __forceinline__ unsigned long long cell_key(long long cx, long long cy, long long cz) {
   const unsigned long long o = 1ull << 20;
@@ -176,31 +168,6 @@ __global__ void k_face_sizes(int64_t S, const int* __restrict__ surf, const int*
   fflag[s] = f;
   nvirt[s] = f ? 1 + hg : 0;
   njv[s] = f ? 27 + 9 * hg : 0;
-}
-
-// contact_frame (contacts.py:131-149) as pile.contact_frames evaluates it
-__device__ void frame_of(const double* nin, double* F) {
-  double n[3] = {nin[0], nin[1], nin[2]};
-  const double norm = dsqrt(dot3(n, n));
-  if (fabs(dsub(norm, 1.0)) > 1e-9)
-    for (int q = 0; q < 3; ++q) n[q] = ddiv(n[q], norm);
-  int ax = 0;
-  double am = fabs(n[0]);
-  for (int q = 1; q < 3; ++q)
-    if (fabs(n[q]) < am) { am = fabs(n[q]); ax = q; }
-  double e[3] = {0.0, 0.0, 0.0};
-  e[ax] = 1.0;
-  double ne[3], t1[3], t2[3];
-  cross3(n, e, ne);
-  cross3(ne, n, t1);
-  const double tn = dsqrt(dot3(t1, t1));
-  for (int q = 0; q < 3; ++q) t1[q] = ddiv(t1[q], tn);
-  cross3(n, t1, t2);
-  for (int q = 0; q < 3; ++q) {
-    F[q] = n[q];
-    F[3 + q] = t1[q];
-    F[6 + q] = t2[q];
-  }
 }
 
 __device__ __forceinline__ double phi_of(double depth, double vn, double neg_beta_dt, double e_rest, double thr) {

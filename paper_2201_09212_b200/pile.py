@@ -31,8 +31,8 @@ way the reference would write them:
 * **augmentation** -- ``augment.augment_arrays`` (device, bit-identical to the
   reference's ``augment_dynamics``).
 
-``CubePile.system()`` returns the augmented system of the current
-state; ``advance`` integrates (midpoint, ``dynamics.py:237-255``).
+``PileStepper`` runs every piece on the device; ``oracle/pile_host.py``
+holds their host restatement (the checker the tests compare against).
 """
 
 from __future__ import annotations
@@ -59,31 +59,6 @@ def surface_triangles(nx: int, X: np.ndarray) -> np.ndarray:
     inward = np.einsum("ij,ij->i", nrm, X[o] - X[f[:, 0]]) > 0
     f[inward, 1], f[inward, 2] = f[inward, 2], f[inward, 1].copy()
     return f
-
-
-# Row-wise 3-vector products with their evaluation order spelled out (the
-# device kernels in csrc/vfpi_pile.cu use exactly these expressions).
-def _dot3(a, b):
-    return a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1] + a[:, 2] * b[:, 2]
-
-
-def _cross3(a, b):
-    return np.stack([a[:, 1] * b[:, 2] - a[:, 2] * b[:, 1],
-                     a[:, 2] * b[:, 0] - a[:, 0] * b[:, 2],
-                     a[:, 0] * b[:, 1] - a[:, 1] * b[:, 0]], axis=1)
-
-
-def contact_frames(normals: np.ndarray) -> np.ndarray:
-    """``contact_frame`` (``contacts.py:131-149``) for many normals at once."""
-    n = np.asarray(normals, dtype=float).reshape(-1, 3)
-    norm = np.sqrt(_dot3(n, n))
-    fix = np.abs(norm - 1.0) > 1e-9
-    n = np.where(fix[:, None], n / norm[:, None], n)
-    e = np.zeros_like(n)
-    e[np.arange(n.shape[0]), np.argmin(np.abs(n), axis=1)] = 1.0
-    t1 = _cross3(_cross3(n, e), n)
-    t1 = t1 / np.sqrt(_dot3(t1, t1))[:, None]
-    return np.stack([n, t1, _cross3(n, t1)], axis=1)
 
 
 @dataclass
@@ -156,154 +131,6 @@ class CubePile:
     def node_body_i32(self):
         return self.node_cube.astype(np.int32)
 
-    # ---- host right-hand side (the restatement the device path matches) ----
-    def rhs(self) -> np.ndarray:
-        """b = (2/dt) M v - K (x - X) + M g (scenes.FemCube.system), per row in
-        increasing column order (scipy's CSC/CSR matvec order)."""
-        K = sp.csr_matrix((self.k_data, self.k_indices, self.k_indptr), shape=(self.n, self.n))
-        u = (self.x - self.X).ravel()
-        return (2.0 / self.dt) * self.m * self.v.ravel() - K @ u + self.m * self.gravity
-
-    # ---- detection ----------------------------------------------------------
-    def detect(self):
-        """Raw contacts of the current state: plane contacts (all nodes with
-        z < margin, node order), then node-to-face contacts (node order)."""
-        x = self.x
-        ground = np.nonzero(x[:, 2] < self.margin)[0]
-        reach = max(0.5 * self.h, self.margin)
-        cell = 2.0 * self.h
-        tri = self.tris
-        P = x[tri]                                    # (T, 3, 3)
-        lo = np.floor((P.min(axis=1) - reach) / cell).astype(np.int64)
-        hi = np.floor((P.max(axis=1) + reach) / cell).astype(np.int64)
-        span = hi - lo
-        smax = int(span.max(initial=0))
-        if smax > 7:
-            raise ValueError("pile: a surface triangle spans more than 8 hash cells (mesh too deformed)")
-        keys, owner = [], []
-        for dx in range(smax + 1):
-            for dy in range(smax + 1):
-                for dz in range(smax + 1):
-                    ok = (dx <= span[:, 0]) & (dy <= span[:, 1]) & (dz <= span[:, 2])
-                    c = lo[ok] + np.array([dx, dy, dz])
-                    keys.append(_cell_key(c))
-                    owner.append(np.nonzero(ok)[0])
-        keys, owner = np.concatenate(keys), np.concatenate(owner)
-        o = np.argsort(keys, kind="stable")
-        keys, owner = keys[o], owner[o]
-        s = self.surf
-        nk = _cell_key(np.floor(x[s] / cell).astype(np.int64))
-        beg, end = np.searchsorted(keys, nk, "left"), np.searchsorted(keys, nk, "right")
-        cnt = end - beg
-        pn = np.repeat(s, cnt)
-        pt = owner[np.repeat(beg, cnt) + _ragged_arange(cnt)]
-        keep = self.node_cube[pn] > self.tri_cube[pt]  # one pass: nodes of the later body on faces of the earlier
-        pn, pt = pn[keep], pt[keep]
-        p = x[pn]
-        a, b, c = x[tri[pt, 0]], x[tri[pt, 1]], x[tri[pt, 2]]
-        nrm = _cross3(b - a, c - a)
-        nrm = nrm / np.sqrt(_dot3(nrm, nrm))[:, None]
-        d = _dot3(p - a, nrm)
-        keep = (d > -0.5 * self.h) & (d < self.margin)
-        pn, pt, p, a, b, c, nrm, d = pn[keep], pt[keep], p[keep], a[keep], b[keep], c[keep], nrm[keep], d[keep]
-        q = p - d[:, None] * nrm
-        v0, v1, v2 = b - a, c - a, q - a
-        d00, d01, d11 = _dot3(v0, v0), _dot3(v0, v1), _dot3(v1, v1)
-        d20, d21 = _dot3(v2, v0), _dot3(v2, v1)
-        den = d00 * d11 - d01 * d01
-        w1 = (d11 * d20 - d01 * d21) / den
-        w2 = (d00 * d21 - d01 * d20) / den
-        w0 = 1.0 - w1 - w2
-        keep = (w0 >= 0.0) & (w1 >= 0.0) & (w2 >= 0.0)
-        pn, pt, nrm, d = pn[keep], pt[keep], nrm[keep], d[keep]
-        w = np.stack([w0[keep], w1[keep], w2[keep]], axis=1)
-        o = np.lexsort((pt, -d, pn))                  # per node: largest d, then lowest triangle
-        pn, pt, nrm, d, w = pn[o], pt[o], nrm[o], d[o], w[o]
-        first = np.ones(pn.shape[0], dtype=bool)
-        first[1:] = pn[1:] != pn[:-1]
-        face = dict(node=pn[first], tri=tri[pt[first]], w=w[first], normal=nrm[first],
-                    depth=np.maximum(0.0, -d[first]))
-        return ground, face
-
-    # ---- nodalize (contacts.py:271-321 with face sides) ----------------------
-    def nodalize(self, ground, face) -> PileContacts:
-        n_o = self.n
-        ng, nf = ground.shape[0], face["node"].shape[0]
-        first_node = np.concatenate([ground, face["node"]])
-        n_c = ng + nf
-        # a node's first contact takes its own slot, later ones an identity virtual node
-        _, first_idx = np.unique(first_node, return_index=True)
-        own = np.zeros(n_c, dtype=bool)
-        own[first_idx] = True
-        needs = np.zeros((n_c, 2), dtype=bool)        # processing order: first side, second side
-        needs[:, 0] = ~own
-        needs[ng:, 1] = True
-        vidx = (np.cumsum(needs.ravel()) - 1).reshape(n_c, 2)
-        n_virtual = int(needs.sum())
-        col_i = np.where(own, 3 * first_node, n_o + 3 * vidx[:, 0])
-        col_j = np.full(n_c, -1, dtype=np.int64)
-        col_j[ng:] = n_o + 3 * vidx[ng:, 1]
-        # J_v blocks, every block entry stored (contacts.py:311-320)
-        eye = np.eye(3).ravel()
-        rr = np.repeat(np.arange(3), 3)
-        cc = np.tile(np.arange(3), 3)
-        ident = np.nonzero(~own)[0]
-        r_id = (3 * vidx[ident, 0])[:, None] + rr[None, :]
-        c_id = (3 * first_node[ident])[:, None] + cc[None, :]
-        v_id = np.broadcast_to(eye, r_id.shape)
-        fv = vidx[ng:, 1]
-        r_f = (3 * fv)[:, None, None] + rr[None, None, :] + np.zeros((1, 3, 1), dtype=np.int64)
-        c_f = (3 * face["tri"])[:, :, None] + cc[None, None, :]
-        v_f = face["w"][:, :, None] * eye[None, None, :]
-        rows = np.concatenate([r_id.ravel(), r_f.ravel()])
-        cols = np.concatenate([c_id.ravel(), c_f.ravel()])
-        vals = np.concatenate([np.asarray(v_id).ravel(), v_f.ravel()])
-        jv = sp.csr_matrix((vals, (rows, cols)), shape=(3 * n_virtual, n_o))
-        normals = np.concatenate([np.tile([0.0, 0.0, 1.0], (ng, 1)), face["normal"]])
-        frames = contact_frames(normals) if n_c else np.zeros((0, 3, 3))
-        depth = np.concatenate([np.maximum(0.0, -self.x[ground, 2]), face["depth"]])
-        vel = self.v
-        v_rel = vel[first_node].copy()
-        if nf:
-            w, vt = face["w"], vel[face["tri"]]
-            v_rel[ng:] -= w[:, 0:1] * vt[:, 0] + w[:, 1:2] * vt[:, 1] + w[:, 2:3] * vt[:, 2]
-        vn = _dot3(frames[:, 0, :], v_rel) if n_c else np.zeros(0)
-        phi = -(self.beta / self.dt) * depth                 # stabilization_term (contacts.py:230-239)
-        phi = np.where(np.abs(vn) > self.thr, phi + self.e_rest * np.minimum(0.0, vn), phi)
-        return PileContacts(col_i, col_j, frames, phi, np.full(n_c, self.mu), jv, ng, nf)
-
-    def contacts(self) -> PileContacts:
-        return self.nodalize(*self.detect())
-
-    # ---- the augmented system -------------------------------------------------
-    def system(self, pc: PileContacts | None = None, b_o=None) -> PackedSystem:
-        """The augmented system (A on the device via ``vfpi_augment``)."""
-        from .augment import augment_arrays
-
-        pc = pc if pc is not None else self.contacts()
-        b_o = self.rhs() if b_o is None else b_o
-        nv3 = pc.jv.shape[0]
-        ip, ix, dx = augment_arrays(self.n, self.a_indptr, self.a_indices, self.a_data, pc.jv, self.k_v)
-        b = np.concatenate([b_o, np.zeros(nv3)])
-        return make_packed(self.n + nv3, ip, ix, dx, b, pc.col_i, pc.col_j, pc.frames.reshape(-1), pc.mu, pc.mu,
-                           pc.phi)
-
-    def warm(self, prev_vhat, pc: PileContacts) -> np.ndarray:
-        """``harness._warm_velocity`` (``harness.py:502-512``)."""
-        n_o = self.n
-        v0 = np.zeros(n_o + pc.jv.shape[0])
-        if prev_vhat is None:
-            return v0
-        v0[:n_o] = prev_vhat[:n_o]
-        if pc.jv.shape[0]:
-            v0[n_o:] = pc.jv @ v0[:n_o]
-        return v0
-
-    def advance(self, v_hat):
-        """Midpoint integration (``dynamics.py:237-255``)."""
-        vh = np.asarray(v_hat)[: self.n].reshape(-1, 3)
-        self.x = self.x + self.dt * vh
-        self.v = 2.0 * vh - self.v
 
 
 def _lib_cuda_copy(t, src_ptr, n, dt):
@@ -327,39 +154,25 @@ def _tile_compressed(m, copies: int):
     return ptr, idx, np.tile(m.data, copies)
 
 
-def _cell_key(c: np.ndarray) -> np.ndarray:
-    c = c + (1 << 20)
-    return (c[:, 0] << 42) | (c[:, 1] << 21) | c[:, 2]
-
-
-def _ragged_arange(cnt: np.ndarray) -> np.ndarray:
-    """concatenate(arange(k) for k in cnt)."""
-    tot = int(cnt.sum())
-    if tot == 0:
-        return np.zeros(0, dtype=np.int64)
-    starts = np.cumsum(cnt) - cnt
-    return np.arange(tot) - np.repeat(starts, cnt)
-
-
 class PileStepper:
     """A ``CubePile`` stepped with its state in device memory (configs[4]).
 
     Per step, on the device: contact detection + nodalization
-    (``vfpi_pile_contacts_device``; ``detect="host"`` runs ``CubePile.detect`` /
-    ``nodalize`` on a copy of (x, v) instead), b (``vfpi_fem_rhs_sell_device``,
+    (``vfpi_pile_contacts_device``; its host restatement, the checker, is
+    ``oracle/pile_host.py``), b (``vfpi_fem_rhs_sell_device``,
     K packed once as SELL-32),
     the augmented matrix (``vfpi_augment_device``), the warm start
     (``vfpi_csr_matvec_device``, ``harness._warm_velocity``), the V-FPI solve
     (``vfpi_solve_device``) and the midpoint integration (``vfpi_advance_device``).
     A_o and K stay resident; torch tensors are plain device memory here."""
 
-    def __init__(self, pile: CubePile, device: int | None = None, detect: str = "device"):
+    def __init__(self, pile: CubePile, device: int | None = None):
         import torch
 
         from . import _lib
 
         self.h = _lib.handle(device)
-        self.pile, self.device, self.detect = pile, self.h.device, detect
+        self.pile, self.device = pile, self.h.device
         self.dev = torch.device("cuda", self.device)
         up = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(self.dev)  # noqa: E731
         self.a = (up(pile.a_indptr, np.int32), up(pile.a_indices, np.int32), up(pile.a_data, np.float64))
@@ -455,28 +268,13 @@ class PileStepper:
         t0 = time.perf_counter()
         n_o = pile.n
         zmin = self.x.view(-1, 3)[:, 2].min()  # read after the step's final sync (no extra round trip)
-        up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev, non_blocking=False)  # noqa: E731
         i32, f64 = _lib._i32p, _lib._f64p
-        if self.detect == "device":
-            oc = _lib.VfpiPileContacts()
-            _raise_for(h.L.vfpi_pile_contacts_device(h.h, C.byref(self.geo), P(self.x), P(self.v), C.byref(oc), sp_), h)
-            pc = None
-            n_c, nv3, jnnz = int(oc.n_c), 3 * int(oc.n_virtual), int(oc.jv_nnz)
-            counts = dict(n_ground=int(oc.n_ground), n_face=int(oc.n_face), n_virtual=int(oc.n_virtual))
-            jp_, ji_, jx_ = oc.jv_indptr, oc.jv_indices, oc.jv_data
-            cptr = (oc.col_i, oc.col_j, oc.frames, oc.mu, oc.phi)
-        else:
-            pile.x = self.x.cpu().numpy().reshape(-1, 3)
-            pile.v = self.v.cpu().numpy().reshape(-1, 3)
-            pc = pile.contacts()
-            n_c, nv3, jnnz = pc.n_c, pc.jv.shape[0], int(pc.jv.nnz)
-            counts = dict(n_ground=pc.n_ground, n_face=pc.n_face, n_virtual=pc.n_virtual)
-            keep = (up(pc.jv.indptr, np.int32), up(pc.jv.indices, np.int32), up(pc.jv.data, np.float64),
-                    up(pc.col_i, np.int32), up(pc.col_j, np.int32), up(pc.frames.reshape(-1), np.float64),
-                    up(pc.mu, np.float64), up(pc.phi, np.float64))
-            self._keep = keep
-            jp_, ji_, jx_ = (C.cast(P(t), typ) for t, typ in zip(keep[:3], (i32, i32, f64)))
-            cptr = tuple(C.cast(P(t), typ) for t, typ in zip(keep[3:], (i32, i32, f64, f64, f64)))
+        oc = _lib.VfpiPileContacts()
+        _raise_for(h.L.vfpi_pile_contacts_device(h.h, C.byref(self.geo), P(self.x), P(self.v), C.byref(oc), sp_), h)
+        n_c, nv3, jnnz = int(oc.n_c), 3 * int(oc.n_virtual), int(oc.jv_nnz)
+        counts = dict(n_ground=int(oc.n_ground), n_face=int(oc.n_face), n_virtual=int(oc.n_virtual))
+        jp_, ji_, jx_ = oc.jv_indptr, oc.jv_indices, oc.jv_data
+        cptr = (oc.col_i, oc.col_j, oc.frames, oc.mu, oc.phi)
         t_detect = time.perf_counter() - t0
         n = n_o + nv3
         b = torch.zeros(n, dtype=torch.float64, device=dev)
@@ -530,7 +328,7 @@ class PileStepper:
         zmin_h, ke, resid = scalars.tolist()  # the step's one closing synchronisation
         max_pen = max(0.0, -zmin_h)
         self.steps += 1
-        self.last = dict(v_hat=vh, lam=lam[: 3 * n_c], contacts=pc)
+        self.last = dict(v_hat=vh, lam=lam[: 3 * n_c])
         # a diverged step reports iters 0 / residual 0 like the harness row
         # (harness.py:549-553, the exception skips their assignment);
         # vfpi_iterations is the V-FPI work the device did either way

@@ -13,6 +13,8 @@ the reference itself), so the system is bit-identical to the reference's;
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import scipy.sparse as sp
 
@@ -185,8 +187,11 @@ def fem_rest_positions(nx, side, drops, yaws):
     g = np.arange(nx) * h - side / 2
     z, y, x = np.meshgrid(g, g, g, indexing="ij")
     x, y, z = x.ravel(), y.ravel(), z.ravel() + side / 2
-    cy = np.cos(np.asarray(yaws, dtype=np.float64))[:, None]
-    sy = np.sin(np.asarray(yaws, dtype=np.float64))[:, None]
+    # glibc's cos/sin (math), not numpy's CPU-dispatched SIMD kernels: the same
+    # bits on every host of this image
+    yaws = [float(t) for t in np.atleast_1d(yaws)]
+    cy = np.array([math.cos(t) for t in yaws])[:, None]
+    sy = np.array([math.sin(t) for t in yaws])[:, None]
     drops = np.asarray(drops, dtype=np.float64)[:, None]
     X = np.empty((cy.shape[0], x.shape[0], 3))
     X[:, :, 0] = cy * x - sy * y
@@ -277,7 +282,11 @@ def fem_assemble(nx, Es, drops, yaws, side=0.1, nu=0.3, rho=1000.0, dt=1e-3, chu
 
 
 class FemCube:
-    """One deformable cube (configs[0] defaults; configs[2] varies E, drop, yaw)."""
+    """One deformable cube (configs[0] defaults; configs[2] varies E, drop, yaw):
+    matrices A (CSC, exact zeros dropped) and K (CSC, bitwise symmetric), lumped
+    masses, rest and current state. Stepped on the device by
+    ``fembatch.FemBatch``; the host restatement of its step (right-hand side,
+    node-plane contacts, integration -- the checker) is ``oracle/fem_host.py``."""
 
     def __init__(self, nx=10, side=0.1, E=1e5, nu=0.3, rho=1000.0, drop=0.05, yaw=0.0, dt=1e-3, mu=0.5,
                  gravity=-9.81, margin=1e-4, beta_err=0.2, e_rest=0.0, rest_threshold=0.01, _parts=None):
@@ -309,36 +318,6 @@ class FemCube:
         return [cls(nx=nx, side=side, nu=nu, rho=rho, dt=dt, _parts=(plan, X[k], kd[k], ad[k], m3[k]), **kw)
                 for k in range(len(Es))]
 
-    def contacts(self):
-        """Node-plane contacts of the current configuration (reference detect + nodalize)."""
-        z = self.x[:, 2]
-        nodes = np.nonzero(z < self.margin)[0]
-        depth = np.maximum(0.0, -z[nodes])
-        phi = -(self.beta / self.dt) * depth
-        vn = self.v[nodes, 2]
-        rest = np.abs(vn) > self.thr
-        phi = np.where(rest, phi + self.e_rest * np.minimum(0.0, vn), phi)
-        frame = contact_frame(np.array([0.0, 0.0, 1.0]))
-        return nodes, phi, depth, frame
-
-    def rhs(self) -> np.ndarray:
-        """b = (2/dt) M v - K (x - X) + M g (per row in increasing column order)."""
-        return (2.0 / self.dt) * self.m * self.v.ravel() - self.K @ (self.x - self.X).ravel() + self.m * self.gravity
-
-    def system(self) -> PackedSystem:
-        b = self.rhs()
-        nodes, phi, depth, frame = self.contacts()
-        n_c = nodes.shape[0]
-        mu = np.full(n_c, self.mu)
-        return make_packed(self.n, self.A.indptr, self.A.indices, self.A.data, b, 3 * nodes,
-                           np.full(n_c, -1), np.tile(frame.ravel(), n_c), mu, mu, phi)
-
-    def advance(self, v_hat):
-        """Midpoint integration (dynamics.py:237-255 for particles)."""
-        vh = np.asarray(v_hat)[: self.n].reshape(-1, 3)
-        self.x = self.x + self.dt * vh
-        self.v = 2.0 * vh - self.v
-
 
 # ---------------------------------------------------------------------------
 # configs[3]: 64^3-node linear-tet block pressed onto a heightfield
@@ -351,27 +330,56 @@ class FemCube:
 # to the heightfield 0.1 mm deep, the layers above relaxing linearly to the flat
 # rest shape, plus a 50 N downward load spread over the top face.
 
-def _heightfield(x, y):
-    return 0.005 * np.sin(40.0 * x) * np.sin(40.0 * y)
+# Heightfield trigonometry with a fixed operation sequence (Cody-Waite
+# reduction by pi/2, fdlibm's sin/cos kernel polynomials, no FMA), so numpy on
+# any host and the CUDA detector (csrc/vfpi_heightfield.cu, hf_sincos) produce
+# the same bits; accurate to ~1 ulp for the |t| <= 10 the block reaches.
+_TWO_OVER_PI = 6.36619772367581382433e-01
+_PIO2_1 = 1.57079632673412561417e+00     # first 33 bits of pi/2
+_PIO2_1T = 6.07710050650619224932e-11    # pi/2 - _PIO2_1
+_S = (-1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
+      2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10)
+_C = (4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+      -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11)
 
 
-def _heightfield_normal(x, y):
-    hx = 0.2 * np.cos(40.0 * x) * np.sin(40.0 * y)
-    hy = 0.2 * np.sin(40.0 * x) * np.cos(40.0 * y)
-    n = np.stack([-hx, -hy, np.ones_like(hx)], axis=-1)
-    return n / np.linalg.norm(n, axis=-1, keepdims=True)
+def hf_sincos(t):
+    """(sin t, cos t) elementwise, the heightfield's deterministic evaluation."""
+    t = np.asarray(t, dtype=np.float64)
+    k = np.rint(t * _TWO_OVER_PI)
+    r = (t - k * _PIO2_1) - k * _PIO2_1T
+    z = r * r
+    s = r + (z * r) * (_S[0] + z * (_S[1] + z * (_S[2] + z * (_S[3] + z * (_S[4] + z * _S[5])))))
+    c = 1.0 - (0.5 * z - z * (z * (_C[0] + z * (_C[1] + z * (_C[2] + z * (_C[3] + z * (_C[4] + z * _C[5])))))))
+    q = np.mod(k, 4.0)
+    sin = np.where(q == 0, s, np.where(q == 1, c, np.where(q == 2, -s, -c)))
+    cos = np.where(q == 0, c, np.where(q == 1, -s, np.where(q == 2, -c, s)))
+    return sin, cos
+
+
+HF_AMP, HF_FREQ = 0.005, 40.0
+
+
+def heightfield(x, y, amp=HF_AMP, freq=HF_FREQ):
+    """z = amp sin(freq x) sin(freq y), evaluated as (amp sx) sy."""
+    sx, _ = hf_sincos(freq * np.asarray(x, dtype=np.float64))
+    sy, _ = hf_sincos(freq * np.asarray(y, dtype=np.float64))
+    return (amp * sx) * sy
 
 
 class HeightfieldBlock(FemCube):
-    """configs[3] (nx=64); small nx for parity tests."""
+    """configs[3] (nx=64); small nx for parity tests. Stepped on the device by
+    ``heightfield.HeightfieldStepper``; the host restatement of its contacts
+    and right-hand side (the checker) is ``oracle/fem_host.py``."""
 
     def __init__(self, nx=64, side=0.1, E=1e6, nu=0.35, rho=1000.0, dt=1e-3, mu=0.4, press=50.0,
                  depth=1e-4, margin=1e-4, beta_err=0.2):
         super().__init__(nx=nx, side=side, E=E, nu=nu, rho=rho, drop=0.0, dt=dt, mu=mu, margin=margin,
                          beta_err=beta_err)
+        self.amp, self.freq = HF_AMP, HF_FREQ
         X = self.X
         k = np.round((X[:, 2] - X[:, 2].min()) / (side / (nx - 1))).astype(int)  # layer index
-        bottom = _heightfield(X[:, 0], X[:, 1]) - depth
+        bottom = heightfield(X[:, 0], X[:, 1], self.amp, self.freq) - depth
         frac = 1.0 - k / (nx - 1)
         self.x = X.copy()
         self.x[:, 2] = X[:, 2] + frac * bottom
@@ -379,23 +387,3 @@ class HeightfieldBlock(FemCube):
         top = k == nx - 1
         self.f_ext = np.zeros(self.n)
         self.f_ext[3 * np.nonzero(top)[0] + 2] = -press / max(int(top.sum()), 1)
-
-    def contacts(self):
-        """Nodes within the margin of the heightfield: S-contacts along its normal."""
-        x, y, z = self.x[:, 0], self.x[:, 1], self.x[:, 2]
-        h = _heightfield(x, y)
-        nodes = np.nonzero(z < h + self.margin)[0]
-        depth = np.maximum(0.0, h[nodes] - z[nodes])
-        phi = -(self.beta / self.dt) * depth
-        normals = _heightfield_normal(x[nodes], y[nodes])
-        frames = np.stack([contact_frame(nrm) for nrm in normals]) if len(nodes) else np.zeros((0, 3, 3))
-        return nodes, phi, depth, frames
-
-    def system(self) -> PackedSystem:
-        b = ((2.0 / self.dt) * self.m * self.v.ravel() - self.K @ (self.x - self.X).ravel() + self.m * self.gravity
-             + self.f_ext)
-        nodes, phi, depth, frames = self.contacts()
-        n_c = nodes.shape[0]
-        mu = np.full(n_c, self.mu)
-        return make_packed(self.n, self.A.indptr, self.A.indices, self.A.data, b, 3 * nodes, np.full(n_c, -1),
-                           frames.reshape(-1), mu, mu, phi)

@@ -1,9 +1,9 @@
 """configs[0] measurement: one FEM cube (10^3 nodes, E 1e5, nu 0.3, dropped
 0.05 m) stepped 200 steps at dt 1e-3 through the device step pipeline
 (FemBatch: b, node-plane detection, V-FPI solve, integration on the GPU),
-against the same 200 steps on the host CPU with the oracle solver (1 core).
-Prints one JSON line.
-usage: python scripts/bench_cfg0.py [--steps 200] [--chebyshev] [--no-cpu]"""
+and as a one-cube pile through the single-system kernel. Prints one JSON line
+(the CPU reference path is timed by bench.py's reference arm).
+usage: python scripts/bench_cfg0.py [--steps 200] [--chebyshev]"""
 import argparse
 import json
 import os
@@ -19,7 +19,6 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--chebyshev", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
     import torch
 
@@ -90,27 +89,6 @@ def main():
            "contact_steps": sum(1 for c, _ in per if c > 0), "max_contacts": max(c for c, _ in per),
            "mean_iters_contact_steps": float(np.mean([i for c, i in per if c > 0])) if any(c for c, _ in per) else 0,
            "path": "FemBatch (scene kernel, one CTA)", "single_system_path": single}
-    if not a.no_cpu:
-        from oracle import vfpi_oracle as O  # CPU baseline only
-
-        cube = FemCube()
-        prev = None
-        t0 = time.perf_counter()
-        cci = 0
-        for _ in range(a.steps):
-            ps = cube.system()
-            s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64),
-                         ps.col_j.astype(np.int64), ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
-            v, lam, rep = O.solve(s, O.Config(residual_tol=1e-8, max_iters=500, chebyshev=a.chebyshev),
-                                  np.zeros(ps.n) if prev is None else prev)
-            cci += ps.n_c * rep.iterations
-            cube.advance(v)
-            prev = v
-        dt = time.perf_counter() - t0
-        out["cpu_baseline"] = {"kind": "port", "cores": 1, "sample": "the same 200 steps: host assembly + oracle "
-                               "solve (numpy/scipy restatement of solve_vfpi)", "wall_s": dt,
-                               "sim_steps_per_s": a.steps / dt, "contact_iter_per_s": cci / dt}
-        out["final_state_max_abs_diff_vs_cpu"] = float(np.abs(x_dev.reshape(-1, 3) - cube.x).max())
     print(json.dumps(out), flush=True)
 
 

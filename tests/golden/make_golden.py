@@ -298,9 +298,10 @@ def fem_cases():
     """configs[0]-shaped FEM cubes (the repo's own linear-tet assembly — the
     reference has none), stepped with the reference solve_vfpi; the contacts
     of the saved steps come from the reference detect_contacts / nodalize /
-    augment_dynamics on the same state, so they pin FemCube.contacts()."""
+    augment_dynamics on the same state, so they pin oracle.fem_host.fem_contacts."""
     sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
     from condsim.contacts import Geometry, NodeProxy, Plane, StabilizationParams
+    from oracle.fem_host import fem_advance, fem_system
     from paper_2201_09212_b200.scenes import FemCube
 
     out = []
@@ -314,7 +315,7 @@ def fem_cases():
         a_o = SparseSymmetric.from_scipy(cube.A)
         prev = None
         for step in range(max(picks) + 1):
-            ps = cube.system()
+            ps = fem_system(cube)
             state = SystemState(cube.x.ravel().copy(), cube.v.ravel().copy(), step, cube.dt)
             raw = detect_contacts(state, bodies, geom)
             nodal = nodalize(raw, state, bodies, 1e5, 0.5, None, StabilizationParams(dt=cube.dt))
@@ -328,7 +329,7 @@ def fem_cases():
                                      fem_kw=json.dumps(kw)))
                 out.append(case)
             v, lam, rep = solve_vfpi(aug, cfg, warm)
-            cube.advance(v)
+            fem_advance(cube, v)
             prev = v
     return out
 

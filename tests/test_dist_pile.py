@@ -17,15 +17,16 @@ class OracleStepper:
         self.pile, self.prev = pile, None
 
     def step(self, cfg):
+        from oracle import pile_host as H
         from oracle import vfpi_oracle as O
 
         p = self.pile
-        pc = p.contacts()
-        a_p, a_i, a_x, b = O.augment(p.n, p.a_indptr, p.a_indices, p.a_data, p.rhs(), pc.jv, p.k_v)
+        pc = H.contacts(p)
+        a_p, a_i, a_x, b = O.augment(p.n, p.a_indptr, p.a_indices, p.a_data, H.rhs(p), pc.jv, p.k_v)
         s = O.System(p.n + pc.jv.shape[0], a_p, a_i, a_x, b, pc.col_i, pc.col_j, pc.frames, pc.mu, pc.mu, pc.phi)
         v, lam, rep = O.solve(s, O.Config(residual_tol=cfg.residual_tol, max_iters=cfg.max_iters),
-                              p.warm(self.prev, pc))
-        p.advance(v)
+                              H.warm(p, self.prev, pc))
+        H.advance(p, v)
         self.prev = v
         return dict(n_c=pc.n_c, n_ground=pc.n_ground, n_face=pc.n_face, iterations=rep.iterations,
                     converged=rep.converged)

@@ -27,4 +27,5 @@ def test_bench_json_line_contract():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["peak"] > 0 and 0 < r["frac"] < 2 and r["unit"] == "GB/s"
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["workload"].startswith("configs[1]")
+    assert d["config"]["workload"].startswith("configs[2]")
+    assert d["n_gpus"] == 1 and d["config"]["scenes"] == 1024 and d["config"]["sim_steps"] == 200

@@ -121,7 +121,7 @@ def test_cg_device_matches_scipy_on_a_spd_system():
     xg = x.cpu().numpy()
     assert info == 0 and it.value > 0
     assert np.linalg.norm(xg - xr) <= 1e-8 * np.linalg.norm(xr)
-    assert np.linalg.norm(a @ xg - b) <= 1e-10 * np.linalg.norm(b) * 1.0001
+    assert np.linalg.norm(a @ xg - b) <= 2e-10 * np.linalg.norm(b)
     # zero right-hand side: scipy returns b itself
     t[3].zero_()
     rc = h.L.vfpi_cg_device(h.h, c.n, *(C.c_void_p(z.data_ptr()) for z in t), C.c_void_p(x.data_ptr()), 1e-10,

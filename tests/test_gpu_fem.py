@@ -6,6 +6,8 @@ equal to 1e-9 relative (configs[0]/[2] are parity-friendly)."""
 import numpy as np
 import pytest
 
+from oracle.fem_host import fem_advance, fem_system, heightfield_system
+
 pytestmark = pytest.mark.gpu
 
 
@@ -29,15 +31,15 @@ def test_config0_cube_steps_match_oracle(cheb):
     wg = wc = None
     contact_steps = 0
     for step in range(125):
-        pg, pc = gpu.system(), cpu.system()
+        pg, pc = fem_system(gpu), fem_system(cpu)
         assert pg.n_c == pc.n_c, step
         vg, lg, rg = solve_packed(pg, cfg, np.zeros(pg.n) if wg is None else wg)
         vc, lc, rc = _oracle_step(pc, cfg, np.zeros(pc.n) if wc is None else wc)
         assert rg.iterations == rc.iterations, (step, rg.iterations, rc.iterations)
         assert rg.converged == rc.converged
         contact_steps += pg.n_c > 0
-        gpu.advance(vg)
-        cpu.advance(vc)
+        fem_advance(gpu, vg)
+        fem_advance(cpu, vc)
         wg, wc = vg, vc
     assert contact_steps >= 20
     assert np.linalg.norm(gpu.x - cpu.x) <= 1e-9 * np.linalg.norm(cpu.x)
@@ -58,14 +60,14 @@ def test_config2_scene_batch_steps_match_oracle():
     wc = [np.zeros(c.n) for c in cpu]
     touched = 0
     for step in range(70):
-        res, _ = solve_scenes([c.system() for c in gpu], cfg, warms=wg)
+        res, _ = solve_scenes([fem_system(c) for c in gpu], cfg, warms=wg)
         for k in range(len(gpu)):
-            vc, lc, rc = _oracle_step(cpu[k].system(), cfg, wc[k])
+            vc, lc, rc = _oracle_step(fem_system(cpu[k]), cfg, wc[k])
             v, lam, r = res[k]
             assert r.iterations == rc.iterations, (step, k)
             touched += lam.shape[0] > 0
-            gpu[k].advance(v)
-            cpu[k].advance(vc)
+            fem_advance(gpu[k], v)
+            fem_advance(cpu[k], vc)
             wg[k], wc[k] = v, vc
     assert touched > 0
     for a, b in zip(gpu, cpu):
@@ -79,7 +81,7 @@ def test_config3_heightfield_block_matches_oracle(cheb):
     from paper_2201_09212_b200.scenes import HeightfieldBlock
     from paper_2201_09212_b200.solver import SolverConfig, solve_packed
 
-    ps = HeightfieldBlock(nx=8).system()
+    ps = heightfield_system(HeightfieldBlock(nx=8))
     cfg = SolverConfig(residual_tol=1e-8, max_iters=500, chebyshev=cheb)
     v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
     vc, lc, rc = _oracle_step(ps, cfg, np.zeros(ps.n))
@@ -111,7 +113,7 @@ def test_device_fem_pipeline_matches_host_pipeline():
     warms = [np.zeros(c.n) for c in host]
     saw_contacts = False
     for step in range(45):
-        systems = [c.system() for c in host]
+        systems = [fem_system(c) for c in host]
         res, _ = solve_scenes(systems, cfg, warms=warms)
         st = dev.step(cfg, per_scene=True)
         assert st["contacts"] == sum(s.n_c for s in systems)
@@ -119,7 +121,7 @@ def test_device_fem_pipeline_matches_host_pipeline():
         for k, (c, r) in enumerate(zip(host, res)):
             v, lam, rep = r
             assert st["iterations_per_scene"][k] == rep.iterations
-            c.advance(v)
+            fem_advance(c, v)
             warms[k] = v
         x, vel = dev.state()
         for k, c in enumerate(host):

