@@ -176,6 +176,17 @@ int vfpi_fem_create(vfpi_handle* h, int32_t num_scenes, int32_t nodes_per_scene,
 int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stats* stats,
                   int32_t* iterations_per_scene /* optional [num_scenes] */);
 int vfpi_fem_state(vfpi_fem_batch* fb, double* x, double* v);
+/* Node-block SELL layout for the batch's iteration kernel (csrc/vfpi_nodes.cu):
+ * one lane per node, 3x3 blocks (descriptor + 9 values) instead of entries,
+ * the same template for every scene: `order` (nodes_per_scene) = node
+ * positions (32 per slice), `slice_off` (n_slices + 1, n_slices =
+ * ceil(nodes/32)) = k-step offsets, `block_cols` (32 * slice_off[n_slices])
+ * = [k][lane] block column of the lane's k-th block (ascending per node),
+ * -1 = padding. A must be symmetric with every stored entry inside the
+ * template (VFPI_UNSUPPORTED otherwise). Later steps then use the node-block
+ * kernel (identical v and lam; not for Barzilai-Borwein steps). */
+int vfpi_fem_set_node_layout(vfpi_fem_batch* fb, int32_t nodes_per_scene, const int32_t* order, int32_t n_slices,
+                             const int64_t* slice_off, const int32_t* block_cols);
 /* Restore the state the batch was created with (x, v; zero warm start),
  * enqueued on the handle's stream: device-to-device, no host traffic. */
 int vfpi_fem_reset(vfpi_fem_batch* fb);
@@ -239,7 +250,10 @@ int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
  * key 1: order units by their smallest referenced column (default 1; 0 = row order);
  * key 2: sort each CTA's free rows by decreasing length (default 1);
  * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0; the
- * shared-memory-resident layout uses row cost 20 unless key 4 sets both). */
+ * shared-memory-resident layout uses row cost 20 unless key 4 sets both);
+ * key 6: FEM batches use the node-block kernel when a node layout is set
+ * (default 1); key 7 (query, value ignored): 1 if the last scene-batch solve
+ * ran the node-block kernel. */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

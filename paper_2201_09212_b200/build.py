@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvfpi.so")
-SOURCES = ["vfpi_setup.cu", "vfpi_cg.cu", "vfpi_solve.cu", "vfpi_resident.cu", "vfpi_ops.cu", "vfpi_fem.cu", "vfpi_augment.cu", "vfpi_pile.cu", "vfpi_heightfield.cu", "vfpi_nodalize.cu", "vfpi_api.cu"]
+SOURCES = ["vfpi_setup.cu", "vfpi_cg.cu", "vfpi_solve.cu", "vfpi_nodes.cu", "vfpi_resident.cu", "vfpi_ops.cu", "vfpi_fem.cu", "vfpi_augment.cu", "vfpi_pile.cu", "vfpi_heightfield.cu", "vfpi_nodalize.cu", "vfpi_api.cu"]
 HEADERS = ["vfpi_internal.cuh", "vfpi_math.cuh", os.path.join("..", "..", "include", "vfpi.h")]
 
 NVCC_FLAGS = [

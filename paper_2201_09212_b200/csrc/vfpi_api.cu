@@ -61,6 +61,8 @@ struct vfpi_handle {
   int kernel_mode = 0;  // 0 auto, 1 force shared-memory resident, 2 force streaming
   int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
   int tune_wc = 0;      // >0: force the contact-warp count of the resident kernel
+  int node_kernel = 1;  // FEM batches: node-block SELL kernel when a node layout is set (tuning key 6)
+  int last_node_kernel = 0;
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
   vfpi::PileWork pile;
@@ -378,6 +380,8 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
     return VFPI_OK;
   }
   if (key == 5 && value >= 0) { h->layout_opt.contact_cost = value; return VFPI_OK; }
+  if (key == 6) { h->node_kernel = value != 0; return VFPI_OK; }
+  if (key == 7) return h->last_node_kernel;  // query: did the last scene solve use the node-block kernel
   return VFPI_BAD_ARGUMENT;
 }
 
@@ -689,7 +693,8 @@ int vfpi_solve(vfpi_handle* h, const vfpi_system* s, const vfpi_config* cfg, con
 int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t* d_scene_rows,
                      const int32_t* d_scene_cts, const vfpi_config* cfg, const double* d_warm, const double* d_wc,
                      double* d_out_v, double* d_out_lam, double* d_trace, double* d_scc, vfpi::SolveStatus* h_stat,
-                     cudaStream_t st, float* setup_ms, float* loop_ms, int refresh_max_ct = -1) {
+                     cudaStream_t st, float* setup_ms, float* loop_ms, int refresh_max_ct = -1,
+                     const vfpi::NodeLayoutDev* nodes = nullptr) {
   // refresh_max_ct >= 0: the workspace holds this batch's contact-free row
   // layout (FEM pipeline); only the contact marks are rebuilt, and
   // refresh_max_ct is the largest per-scene contact count
@@ -784,9 +789,22 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
   p.under_relax = cfg->under_relax;
   p.omega = cfg->omega;
   p.cfactor = cfg->consistency_factor;
-  rc = vfpi::launch_iterate_scenes(p, cfg->op, cheb, bb, smem, st, h->err);
+  const bool use_nodes = nodes && !bb && h->node_kernel &&
+                         vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, std::max(max_ct, 1)) > 0;
+  if (use_nodes) {
+    if (vfpi::node_slots_refresh(*nodes, S, n_c, d.col_i, d.col_j, d_scene_cts, st)) {
+      h->err = "node slot refresh failed";
+      return VFPI_CUDA_ERROR;
+    }
+    ++h->launches;
+    CK(cudaEventRecord(ws.ev[1], st));  // the loop timing covers the iteration kernel only
+    rc = vfpi::launch_iterate_nodes(p, *nodes, cfg->op, cheb, std::max(max_ct, 1), st, h->err);
+  } else {
+    rc = vfpi::launch_iterate_scenes(p, cfg->op, cheb, bb, smem, st, h->err);
+  }
   if (rc) return rc;
   ++h->launches;
+  h->last_node_kernel = use_nodes ? 1 : 0;
   CK(cudaEventRecord(ws.ev[2], st));
   if (d_scc && n_c > 0) {
     rc = vfpi::launch_scc_final(p, d_scc, st);
@@ -1104,6 +1122,9 @@ struct vfpi_fem_batch {
   Workspace::Buf zero_cts, ks_off, ks_val, ks_col;  // K in SELL-32
   Workspace::Buf cg_r, cg_p, cg_q, cg_list;        // contact-free fallback of diverged scenes
   Workspace::Buf x0, v0;                           // initial state (vfpi_fem_reset)
+  vfpi::NodeLayoutHost nbh;                        // node-block SELL layout (vfpi_fem_set_node_layout)
+  vfpi::NodeLayoutDev nbd;
+  bool nb_ready = false;
   uint64_t layout_epoch = ~0ull;  // the handle workspace holds our contact-free layout
 };
 
@@ -1280,7 +1301,7 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   float su = 0.f, lo = 0.f;
   int rc = vfpi_scenes_core(h, d, fb->S, P<int32_t>(fb->rows), P<int32_t>(fb->cts), cfg, P<double>(fb->warm),
                             nullptr, P<double>(fb->vhat), P<double>(fb->lam), nullptr, nullptr, fb->stat.data(), st,
-                            &su, &lo, max_ct);
+                            &su, &lo, max_ct, fb->nb_ready ? &fb->nbd : nullptr);
   if (rc) return rc;
   // (3b) diverged scenes take the flagged contact-free step (harness.py:586-593):
   // v_hat = cg(A, b, rtol=1e-10, maxiter=10 n) of the scene, lam = 0
@@ -1340,6 +1361,62 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   return VFPI_OK;
 }
 
+int vfpi_fem_set_node_layout(vfpi_fem_batch* fb, int32_t nodes_per_scene, const int32_t* order, int32_t n_slices,
+                             const int64_t* slice_off, const int32_t* block_cols) {
+  if (!fb || !order || !slice_off || !block_cols || nodes_per_scene != fb->Nn || n_slices != (fb->Nn + 31) / 32)
+    return VFPI_BAD_ARGUMENT;
+  vfpi_handle* h = fb->h;
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  if (slice_off[0] != 0) return VFPI_BAD_ARGUMENT;
+  for (int t = 0; t < n_slices; ++t)
+    if (slice_off[t + 1] < slice_off[t] || slice_off[t + 1] - slice_off[t] > 32) {
+      h->err = "node layout: slice widths must be 0..32 blocks";
+      return VFPI_BAD_ARGUMENT;
+    }
+  std::vector<char> seen((size_t)fb->Nn, 0);
+  for (int i = 0; i < fb->Nn; ++i) {
+    if (order[i] < 0 || order[i] >= fb->Nn || seen[(size_t)order[i]]) {
+      h->err = "node layout: order must be a permutation of the scene's nodes";
+      return VFPI_BAD_ARGUMENT;
+    }
+    seen[(size_t)order[i]] = 1;
+  }
+  const int64_t K = slice_off[n_slices];
+  for (int64_t e = 0; e < 32 * K; ++e)
+    if (block_cols[e] < -1 || block_cols[e] >= fb->Nn) {
+      h->err = "node layout: block column out of range";
+      return VFPI_BAD_ARGUMENT;
+    }
+  if ((int64_t)fb->S * K * 32 * 9 >= ((int64_t)1 << 40)) return VFPI_UNSUPPORTED;
+  vfpi::NodeLayoutHost& L = fb->nbh;
+  L.nn = fb->Nn;
+  L.nsl = n_slices;
+  L.k_scene = K;
+  int rc;
+  if ((rc = fem_upload(h, L.t_order, order, 4 * (size_t)fb->Nn)) ||
+      (rc = fem_upload(h, L.t_off, slice_off, 8 * ((size_t)n_slices + 1))) ||
+      (rc = fem_upload(h, L.t_bcol, block_cols, 4 * 32 * (size_t)std::max<int64_t>(K, 1))))
+    return rc;
+  cudaStream_t st = h->ws.stream;
+  CK(vfpi::ensure(h->ws.flags, 16));
+  CK(cudaMemsetAsync(h->ws.flags.p, 0, 16, st));
+  if (vfpi::node_layout_build(L, fb->S, fb->A.indptr, fb->A.indices, fb->A.data, fb->nbd, (int*)h->ws.flags.p, st)) {
+    h->err = "node layout build failed";
+    return VFPI_CUDA_ERROR;
+  }
+  h->launches += 2;
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, h->ws.flags.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (flag) {
+    h->err = "node layout: A has entries outside the block template";
+    fb->nb_ready = false;
+    return VFPI_UNSUPPORTED;
+  }
+  fb->nb_ready = true;
+  return VFPI_OK;
+}
+
 int vfpi_fem_reset(vfpi_fem_batch* fb) {
   if (!fb) return VFPI_BAD_ARGUMENT;
   vfpi_handle* h = fb->h;
@@ -1376,7 +1453,9 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
                             &fb->X, &fb->x, &fb->v, &fb->warm, &fb->vhat, &fb->lam, &fb->b, &fb->ci, &fb->cj,
                             &fb->frames, &fb->mu, &fb->mu2, &fb->phi, &fb->flag, &fb->pos, &fb->cts, &fb->rows,
                             &fb->frame, &fb->tmp, &fb->zero_cts, &fb->ks_off, &fb->ks_val, &fb->ks_col, &fb->cg_r,
-                            &fb->cg_p, &fb->cg_q, &fb->cg_list, &fb->x0, &fb->v0})
+                            &fb->cg_p, &fb->cg_q, &fb->cg_list, &fb->x0, &fb->v0, &fb->nbh.t_order,
+                            &fb->nbh.t_off, &fb->nbh.t_bcol, &fb->nbh.desc, &fb->nbh.val, &fb->nbh.slice_off,
+                            &fb->nbh.node_list, &fb->nbh.node_slot})
     if (b->p) cudaFree(b->p);
   if (fb->e0) cudaEventDestroy(fb->e0);
   if (fb->e1) cudaEventDestroy(fb->e1);

@@ -381,4 +381,27 @@ int launch_cg_grid(int G, int64_t n, const int32_t* indptr, const int32_t* indic
                    const double* b, double* x, double* r, double* p, double* q, double* partial, double rtol,
                    int64_t maxiter, int32_t* iters_out, cudaStream_t st);
 
+// ---- node-block SELL scene kernel (vfpi_nodes.cu; FEM batches) ---------------
+struct NodeLayoutDev {
+  int nn = 0, nsl = 0;                 // nodes and node slices per scene (every scene the same template)
+  const int* node_list = nullptr;      // [S*nn] position -> global node
+  int* node_slot = nullptr;            // [S*nn] global node -> contact slot base (6 per contact) or -1
+  const int64_t* slice_off = nullptr;  // [S*nsl+1] k-step offset of every slice
+  const unsigned* desc = nullptr;      // [k][lane]: block column | mask << 23
+  const double* val = nullptr;         // [k][9][lane]
+};
+struct NodeLayoutHost {
+  int nn = 0, nsl = 0;
+  int64_t k_scene = 0;                 // k-steps per scene
+  Workspace::Buf t_order, t_off, t_bcol, desc, val, slice_off, node_list, node_slot;
+};
+int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
+                      NodeLayoutDev& out, int* d_flags, cudaStream_t st);
+int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
+                       cudaStream_t st);
+int node_kernel_smem(int max_ct);
+int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct);
+int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bool cheb, int max_ct, cudaStream_t st,
+                         std::string& err);
+
 }  // namespace vfpi

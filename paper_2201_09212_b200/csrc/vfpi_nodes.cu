@@ -1,0 +1,606 @@
+// Scene-batch V-FPI iteration over a NODE-BLOCK SELL layout (FEM batches).
+//
+// Same iteration as k_iterate<..., SC=true> (vfpi_solve.cu; reference loop
+// solver.py:388-446): one CTA per scene, the scene's own loop, reductions and
+// termination with CTA barriers only. What changes is how the surrogate sweep
+// r = A v - b (sparse.py:97-102, solver.py:402-403) streams A:
+//
+//   * one lane per FEM NODE (its 3 rows), 32 nodes per slice, nodes of a scene
+//     ordered by decreasing block count so slices are dense;
+//   * the k-th entry of a lane is a 3x3 BLOCK: one 32-bit descriptor (global
+//     block column | 9-bit mask of the entries A actually stores) and the 9
+//     values row-major (zeros where absent), stored [k][lane] and
+//     [k][9][lane] per slice, so a warp's k-step is one 128 B + nine 256 B
+//     coalesced lines;
+//   * the slice stream goes through a per-warp shared-memory ring fed by TMA
+//     bulk copies (cp.async.bulk + mbarrier complete_tx, evict-first), as in
+//     the row-SELL ring of the scene kernel.
+//
+// Row p of node i sums its present entries block by block in increasing block
+// column and, inside a block, in increasing column: exactly increasing column
+// order, sequential, FMA-free from 0 -- the same bits as scipy's CSC matvec.
+// A block moves 4 + 72 B for up to 9 stored entries (8.4 B per entry when
+// full) instead of 12 B per entry of the row layout, the three x values of a
+// block column are gathered once for three rows, and three row sums per lane
+// are independent chains. Contacts (S-contacts on node rows, FEM) are handled
+// exactly as in k_iterate: v* of a contact node's rows is staged in shared
+// memory, then one thread per contact gathers, projects and scatters.
+//
+// Only the fixed-order reductions of theta and the force residual visit rows
+// in a different order than the row kernel (both are the GPU's own fixed
+// order; the reference's are OpenBLAS dots), so v and lam are bit-identical
+// to the row kernel's for the same iteration count.
+#include "vfpi_internal.cuh"
+#include "vfpi_math.cuh"
+
+#ifndef VFPI_NB_CHUNK
+#define VFPI_NB_CHUNK 2  // k-steps (node blocks) per ring stage
+#endif
+#ifndef VFPI_NB_STAGES
+#define VFPI_NB_STAGES 2
+#endif
+#ifndef VFPI_NB_WARPS
+#define VFPI_NB_WARPS 8
+#endif
+#ifndef VFPI_NB_MIN_BLOCKS
+#define VFPI_NB_MIN_BLOCKS 2
+#endif
+
+namespace vfpi {
+
+namespace {
+
+constexpr int kNbThreads = 32 * VFPI_NB_WARPS;
+constexpr int kNbChunk = VFPI_NB_CHUNK;
+constexpr int kNbStages = VFPI_NB_STAGES;
+constexpr int kDescBytes = 32 * 4;          // one k-step of descriptors
+constexpr int kValBytes = 9 * 32 * 8;       // one k-step of block values
+constexpr int kNbStageBytes = kNbChunk * (kDescBytes + kValBytes);
+constexpr int kNbRingBytes = VFPI_NB_WARPS * kNbStages * kNbStageBytes + 128;
+constexpr unsigned kMaskShift = 23;
+constexpr unsigned kColMask = (1u << kMaskShift) - 1u;
+
+__device__ __forceinline__ bool nb_try_wait(unsigned addr, unsigned parity) {
+  unsigned done;
+  asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done)
+               : "r"(addr), "r"(parity)
+               : "memory");
+  return done != 0;
+}
+
+__device__ __forceinline__ void cta_sum3(double a, double b, double c, double* sm_warp, double* sm_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = dadd(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = dadd(b, __shfl_xor_sync(0xffffffffu, b, o));
+    c = dadd(c, __shfl_xor_sync(0xffffffffu, c, o));
+  }
+  if (lane == 0) {
+    sm_warp[3 * warp + 0] = a;
+    sm_warp[3 * warp + 1] = b;
+    sm_warp[3 * warp + 2] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0, z = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      x = dadd(x, sm_warp[3 * w + 0]);
+      y = dadd(y, sm_warp[3 * w + 1]);
+      z = dadd(z, sm_warp[3 * w + 2]);
+    }
+    sm_out[0] = x;
+    sm_out[1] = y;
+    sm_out[2] = z;
+  }
+  __syncthreads();
+}
+
+struct NbRing {
+  unsigned char* base;  // this warp's stages
+  unsigned bar0;
+  int s_first, s_end, nw;  // the warp's slices: s_first, s_first + nw, ... < s_end
+  int ps, pc;              // producer cursor
+  unsigned issued, consumed;
+  bool work;
+};
+
+__device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint64_t pol) {
+  int64_t off;
+  int W;
+  for (;;) {
+    off = L.slice_off[r.ps];
+    W = (int)(L.slice_off[r.ps + 1] - off);
+    if (W > 0) break;
+    r.ps += r.nw;
+    if (r.ps >= r.s_end) r.ps = r.s_first;
+  }
+  const int k0 = r.pc * kNbChunk;
+  const int kk = min(kNbChunk, W - k0);
+  const int stage = (int)(r.issued % kNbStages);
+  const unsigned bar = r.bar0 + 8u * (unsigned)stage;
+  unsigned char* sb = r.base + (size_t)stage * kNbStageBytes;
+  const unsigned dd = (unsigned)__cvta_generic_to_shared(sb);
+  const unsigned dv = (unsigned)__cvta_generic_to_shared(sb + kNbChunk * kDescBytes);
+  const unsigned bd = (unsigned)kk * kDescBytes, bv = (unsigned)kk * kValBytes;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bd + bv) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(dd), "l"(L.desc + (off + k0) * 32), "r"(bd), "r"(bar), "l"(pol)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(dv), "l"(L.val + (off + k0) * (9 * 32)), "r"(bv), "r"(bar), "l"(pol)
+      : "memory");
+  ++r.pc;
+  if (r.pc * kNbChunk >= W) {
+    r.pc = 0;
+    r.ps += r.nw;
+    if (r.ps >= r.s_end) r.ps = r.s_first;
+  }
+}
+
+// the three row sums of this lane's node over its slice (width W) out of the ring
+template <class X>
+__device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W, int lane, uint64_t pol, X x,
+                                        double& y0, double& y1, double& y2) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int k0 = 0; k0 < W; k0 += kNbChunk) {
+    const int kk = min(kNbChunk, W - k0);
+    const int stage = (int)(r.consumed % kNbStages);
+    const unsigned bar = r.bar0 + 8u * (unsigned)stage;
+    const unsigned par = (r.consumed / kNbStages) & 1u;
+    while (!nb_try_wait(bar, par)) {
+    }
+    const unsigned char* sb = r.base + (size_t)stage * kNbStageBytes;
+    const unsigned* ds = reinterpret_cast<const unsigned*>(sb) + lane;
+    const double* vs = reinterpret_cast<const double*>(sb + kNbChunk * kDescBytes) + lane;
+#pragma unroll
+    for (int u = 0; u < kNbChunk; ++u) {
+      if (u < kk) {
+        const unsigned d = ds[32 * u];
+        const unsigned m = d >> kMaskShift;
+        if (m) {
+          const int c = 3 * (int)(d & kColMask);
+          const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
+          const double* v = vs + 9 * 32 * u;
+          if (m & 0x001) a0 = dadd(a0, dmul(v[32 * 0], x0));
+          if (m & 0x002) a0 = dadd(a0, dmul(v[32 * 1], x1));
+          if (m & 0x004) a0 = dadd(a0, dmul(v[32 * 2], x2));
+          if (m & 0x008) a1 = dadd(a1, dmul(v[32 * 3], x0));
+          if (m & 0x010) a1 = dadd(a1, dmul(v[32 * 4], x1));
+          if (m & 0x020) a1 = dadd(a1, dmul(v[32 * 5], x2));
+          if (m & 0x040) a2 = dadd(a2, dmul(v[32 * 6], x0));
+          if (m & 0x080) a2 = dadd(a2, dmul(v[32 * 7], x1));
+          if (m & 0x100) a2 = dadd(a2, dmul(v[32 * 8], x2));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      nb_issue(r, L, pol);
+    }
+    ++r.issued;
+    ++r.consumed;
+  }
+  y0 = a0;
+  y1 = a1;
+  y2 = a2;
+}
+
+template <int OP, bool CHEB, bool HASC>
+__global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_nodes(IterParams p, NodeLayoutDev L) {
+  extern __shared__ double smem[];
+  __shared__ double sm_warp[3 * (kNbThreads / 32)];
+  __shared__ double sm_tot[4];
+  __shared__ __align__(8) uint64_t ring_bar[kNbThreads / 32][kNbStages];
+
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int np0 = b * L.nn, np1 = np0 + L.nn;          // node positions of the scene
+  const int s0 = b * L.nsl, s1 = s0 + L.nsl;          // node slices of the scene
+  const int c0 = p.blk_ct[b], c1 = p.blk_ct[b + 1];
+  const int nct = c1 - c0;
+  double* vs_s = smem;                                // v* of contact rows    [6*nct]
+  double* jt_s = smem + kSlotsPerContact * nct;       // J_c^T lam_{l-1} rows  [6*nct]
+  for (int t = threadIdx.x; t < kSlotsPerContact * nct; t += blockDim.x) jt_s[t] = 0.0;
+
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  NbRing ring{};
+  {
+    const size_t cbytes = (size_t)2 * kSlotsPerContact * nct * sizeof(double);
+    unsigned char* base = reinterpret_cast<unsigned char*>(smem) + ((cbytes + 127) & ~(size_t)127);
+    ring.base = base + (size_t)warp * kNbStages * kNbStageBytes;
+    ring.bar0 = (unsigned)__cvta_generic_to_shared(&ring_bar[warp][0]);
+    ring.s_first = s0 + warp;
+    ring.s_end = s1;
+    ring.nw = nwarps;
+    ring.ps = ring.s_first;
+    bool w = false;
+    for (int s = s0 + warp; s < s1 && !w; s += nwarps) w = L.slice_off[s + 1] > L.slice_off[s];
+    ring.work = w;
+    if (lane == 0) {
+      for (int st = 0; st < kNbStages; ++st)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ring.bar0 + 8u * (unsigned)st) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (w)
+        for (int st = 0; st < kNbStages; ++st) {
+          nb_issue(ring, L, pol);
+          ++ring.issued;
+        }
+    }
+    __syncwarp();
+    ring.issued = w ? kNbStages : 0;
+  }
+  __syncthreads();
+
+  double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
+  double* lb[2] = {p.lam0, p.lam1};
+  const double u = p.under_relax;
+  const double omu = dsub(1.0, u);
+  double rho = 0.0, nu = 1.0, theta_prev = 0.0;
+  double alpha = 0.0;
+  bool use_alpha = false;
+  if (p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
+    // fixed-alpha default 1 / max|diag| of this scene (solver.py:368)
+    double mx = -INFINITY, nanf = 0.0;
+    for (int r = 3 * np0 + threadIdx.x; r < 3 * np1; r += blockDim.x) {
+      const double a = fabs(__ldg(p.diag + r));
+      if (isnan(a)) nanf = 1.0;
+      mx = a > mx ? a : mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = t > mx ? t : mx;
+    }
+    cta_sum3(0.0, 0.0, nanf, sm_warp, sm_tot);
+    const double anynan = sm_tot[2];
+    __syncthreads();
+    if (lane == 0) sm_warp[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = -INFINITY;
+      for (int w2 = 0; w2 < nwarps; ++w2) m = sm_warp[w2] > m ? sm_warp[w2] : m;
+      sm_tot[3] = m;
+    }
+    __syncthreads();
+    alpha = ddiv(1.0, anynan > 0.0 ? NAN : sm_tot[3]);
+    use_alpha = true;
+    __syncthreads();
+  }
+  double* trace = p.trace + (size_t)b * p.trace_stride;
+  SolveStatus* status = p.status + b;
+  bool pending = false;
+  int final_buf = 0, final_lam = 0, iters = 0, conv = 0, div = 0;
+  double consistency = NAN;
+
+  for (int l = 1;; ++l) {
+    const bool check_only = (l == p.max_iters + 1);
+    const double* vcur = vb[(l - 1) % 3];
+    const double* vprev = vb[(l + 1) % 3];
+    double* vnext = vb[l % 3];
+    double* __restrict__ lam_out = lb[l & 1];
+
+    if (CHEB && !check_only) {
+      if (l < p.cheby_start) nu = 1.0;
+      else if (l == p.cheby_start) nu = ddiv(2.0, dsub(2.0, dmul(rho, rho)));
+      else nu = ddiv(4.0, dsub(4.0, dmul(dmul(rho, rho), nu)));
+    }
+
+    double th = 0.0, fr = 0.0, nf = 0.0;
+    auto finish_row = [&](int row, double vnew, double vc) {
+      double vn = vnew;
+      if (CHEB) {
+        const double vss = dadd(dmul(u, vnew), dmul(omu, vc));
+        if (l > 1) {
+          const double vp = vprev[row];
+          vn = dadd(dmul(nu, dsub(vss, vp)), vp);
+        } else {
+          vn = vss;
+        }
+      }
+      const double d = dsub(vn, vc);
+      th = dadd(th, dmul(d, d));
+      if (!isfinite(vn)) nf = dadd(nf, 1.0);
+      vnext[row] = vn;
+    };
+
+    // ---- (1) surrogate sweep, one lane per node -------------------------
+    for (int s = s0 + warp; s < s1; s += nwarps) {
+      const int pos = np0 + (s - s0) * 32 + lane;
+      const int64_t off = L.slice_off[s];
+      const int W = (int)(L.slice_off[s + 1] - off);
+      const bool live = pos < np1;
+      int node = 0, slot = -1;
+      double bv[3] = {0.0, 0.0, 0.0}, wv[3] = {0.0, 0.0, 0.0}, vc[3] = {0.0, 0.0, 0.0};
+      if (live) {
+        node = __ldg(L.node_list + pos);
+        if (HASC) slot = L.node_slot[node];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          bv[q] = __ldg(p.b + 3 * node + q);
+          if (!use_alpha) wv[q] = __ldg(p.w + 3 * node + q);
+          vc[q] = vcur[3 * node + q];
+        }
+      }
+      double y[3];
+      if (W > 0) nb_rows(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2]);
+      else y[0] = y[1] = y[2] = 0.0;
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double r = dsub(y[q], bv[q]);
+          const double f = (slot >= 0) ? dsub(r, jt_s[slot + q]) : dsub(r, 0.0);
+          fr = dadd(fr, dmul(f, f));
+          if (!check_only) {
+            const double wr = use_alpha ? alpha : wv[q];
+            const double vstar = dsub(vc[q], dmul(wr, r));
+            if (slot >= 0) {
+              vs_s[slot + q] = vstar;
+            } else {
+              const double vnew = HASC ? dadd(vstar, dmul(wr, 0.0)) : vstar;
+              finish_row(3 * node + q, vnew, vc[q]);
+            }
+          }
+        }
+      }
+    }
+
+    // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter -------
+    if (HASC && !check_only) {
+      __syncthreads();
+      for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+        const int m = __ldg(p.cont_list + k);
+        const int loc = (k - c0) * kSlotsPerContact;
+        const int ci = __ldg(p.col_i + m), cj = __ldg(p.col_j + m);
+        double R[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) R[t] = __ldg(p.frames + 9 * (size_t)m + t);
+        double vi[3], vj[3] = {0.0, 0.0, 0.0}, rel[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) vi[t] = vs_s[loc + t];
+        if (cj >= 0) {
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            vj[t] = vs_s[loc + 3 + t];
+            rel[t] = dsub(vi[t], vj[t]);
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 3; ++t) rel[t] = vi[t];
+        }
+        double eta[3], lam[3], world[3];
+        frame_apply(R, rel, eta);
+        double g;
+        if (use_alpha) g = (cj >= 0) ? dadd(dadd(alpha, alpha), p.omega) : dadd(alpha, p.omega);
+        else g = __ldg(p.gamma + m);
+        trial_impulse(eta, __ldg(p.phi + m), g, lam);
+        project(OP, lam, __ldg(p.mu + m), __ldg(p.mu2 + m));
+#pragma unroll
+        for (int t = 0; t < 3; ++t) lam_out[3 * (size_t)m + t] = lam[t];
+        frame_apply_t(R, lam, world);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int row = ci + t;
+          const double oi = dadd(0.0, world[t]);
+          jt_s[loc + t] = oi;
+          const double wr = use_alpha ? alpha : __ldg(p.w + row);
+          finish_row(row, dadd(vi[t], dmul(wr, oi)), vcur[row]);
+        }
+        if (cj >= 0) {
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int row = cj + t;
+            const double oj = dsub(0.0, world[t]);
+            jt_s[loc + 3 + t] = oj;
+            const double wr = use_alpha ? alpha : __ldg(p.w + row);
+            finish_row(row, dadd(vj[t], dmul(wr, oj)), vcur[row]);
+          }
+        }
+      }
+    }
+
+    // ---- (4) residual reduction + decision -------------------------------
+    cta_sum3(th, fr, nf, sm_warp, sm_tot);
+    const double theta = dsqrt(sm_tot[0]);
+    const double fres = dsqrt(sm_tot[1]);
+    const bool nonfinite = sm_tot[2] > 0.0;
+    if (pending) {
+      consistency = fres;
+      if (fres <= dmul(p.cfactor, p.tol)) {
+        iters = l - 1; conv = 1;
+        final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
+        break;
+      }
+    }
+    if (check_only) {
+      iters = p.max_iters;
+      consistency = fres;
+      final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
+      break;
+    }
+    if (threadIdx.x == 0) trace[l - 1] = theta;
+    if (nonfinite) {
+      iters = l; div = 1;
+      final_buf = l % 3; final_lam = l & 1;
+      break;
+    }
+    pending = theta < p.tol;
+    if (CHEB) rho = (theta_prev <= 0.0) ? rho : py_min(ddiv(theta, theta_prev), 1.0);
+    theta_prev = theta;
+  }
+
+  for (unsigned n = ring.consumed; n < ring.issued; ++n) {  // drain the chunks in flight
+    const unsigned bar = ring.bar0 + 8u * (n % kNbStages);
+    while (!nb_try_wait(bar, (n / kNbStages) & 1u)) {
+    }
+  }
+  const double* vfin = vb[final_buf];
+  for (int r = 3 * np0 + threadIdx.x; r < 3 * np1; r += blockDim.x) p.out_v[r] = vfin[r];
+  const double* lfin = lb[final_lam];
+  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const int m = __ldg(p.cont_list + k);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) p.out_lam[3 * (size_t)m + t] = lfin[3 * (size_t)m + t];
+  }
+  if (threadIdx.x == 0) {
+    status->iterations = iters;
+    status->converged = conv;
+    status->diverged = div;
+    status->final_vbuf = final_buf;
+    status->consistency = consistency;
+  }
+}
+
+// ---- layout construction ---------------------------------------------------
+
+// per (scene, node position): gather the node's 3 rows (CSC columns of the
+// symmetric A) into its template block slots: values + 9-bit masks
+__global__ void k_nb_fill(int S, int nn, int nsl, const int* __restrict__ t_order,
+                          const int64_t* __restrict__ t_off, const int* __restrict__ t_bcol,
+                          const int* __restrict__ a_ptr, const int* __restrict__ a_idx, const double* __restrict__ a_val,
+                          int64_t k_scene, unsigned* __restrict__ desc, double* __restrict__ val,
+                          int* __restrict__ flags) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)S * nn) return;
+  const int s = (int)(gid / nn), pos = (int)(gid % nn);
+  const int sl = pos >> 5, lane = pos & 31;
+  const int64_t toff = t_off[sl];
+  const int W = (int)(t_off[sl + 1] - toff);
+  const int64_t goff = (int64_t)s * k_scene + toff;  // global k-step offset of the slice
+  const int lnode = t_order[pos];
+  const int node = s * nn + lnode;
+  unsigned mask[32];  // W <= 32 blocks per node (checked on the host)
+  for (int k = 0; k < W; ++k) mask[k] = 0u;
+  for (int p = 0; p < 3; ++p) {
+    const int r = 3 * node + p;
+    int k = 0;
+    for (int e = a_ptr[r]; e < a_ptr[r + 1]; ++e) {
+      const int j = a_idx[e];
+      const int lb = j / 3 - s * nn;
+      while (k < W && t_bcol[toff * 32 + 32 * k + lane] != lb) ++k;
+      if (k >= W) {  // an entry outside the template (A not on the K pattern)
+        atomicOr(flags, 1);
+        return;
+      }
+      const int t = 3 * p + (j % 3);
+      val[(goff * 9 + 9 * k + t) * 32 + lane] = a_val[e];
+      mask[k] |= 1u << t;
+    }
+  }
+  for (int k = 0; k < W; ++k) {
+    const int lb = t_bcol[toff * 32 + 32 * k + lane];
+    desc[(goff + k) * 32 + lane] = (lb >= 0 && mask[k]) ? ((mask[k] << kMaskShift) | (unsigned)(s * nn + lb)) : 0u;
+  }
+}
+
+__global__ void k_nb_slice_off(int S, int nsl, const int64_t* __restrict__ t_off, int64_t k_scene, int nn,
+                               int64_t* __restrict__ off, int* __restrict__ node_list, const int* __restrict__ t_order) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid < (int64_t)S * nsl) {
+    const int s = (int)(gid / nsl), t = (int)(gid % nsl);
+    off[gid] = (int64_t)s * k_scene + t_off[t];
+  }
+  if (gid == 0) off[(int64_t)S * nsl] = (int64_t)S * k_scene;
+  if (gid < (int64_t)S * nn) node_list[gid] = (int)(gid / nn) * nn + t_order[gid % nn];
+}
+
+__global__ void k_nb_node_slots(int n_c, int G, const int* __restrict__ ci, const int* __restrict__ cj,
+                                const int* __restrict__ ct, int* __restrict__ node_slot) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_c) return;
+  int lo = 0, hi = G;  // owner scene: ct[b] <= k < ct[b+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (ct[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  const int loc = (k - ct[lo]) * kSlotsPerContact;
+  node_slot[ci[k] / 3] = loc;
+  if (cj[k] >= 0) node_slot[cj[k] / 3] = loc + 3;
+}
+
+using NbFn = void (*)(IterParams, NodeLayoutDev);
+
+template <int OP>
+NbFn nb_pick2(bool cheb, bool hasc) {
+  if (cheb) return hasc ? k_iterate_nodes<OP, true, true> : k_iterate_nodes<OP, true, false>;
+  return hasc ? k_iterate_nodes<OP, false, true> : k_iterate_nodes<OP, false, false>;
+}
+
+NbFn nb_pick(int op, bool cheb, bool hasc) {
+  if (op == OP_PROXIMAL) return nb_pick2<OP_PROXIMAL>(cheb, hasc);
+  if (op == OP_ANISO) return nb_pick2<OP_ANISO>(cheb, hasc);
+  return nb_pick2<OP_STRICT>(cheb, hasc);
+}
+
+}  // namespace
+
+int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
+                      NodeLayoutDev& out, int* d_flags, cudaStream_t st) {
+  cudaError_t e;
+  const int nn = h.nn, nsl = h.nsl;
+  const int64_t ks = h.k_scene;
+  if ((e = ensure(h.desc, 4 * 32 * (size_t)std::max<int64_t>(S * ks, 1))) ||
+      (e = ensure(h.val, 8 * 9 * 32 * (size_t)std::max<int64_t>(S * ks, 1))) ||
+      (e = ensure(h.slice_off, 8 * ((size_t)S * nsl + 1))) || (e = ensure(h.node_list, 4 * (size_t)S * nn)) ||
+      (e = ensure(h.node_slot, 4 * (size_t)S * nn)))
+    return 1;
+  if ((e = cudaMemsetAsync(h.val.p, 0, 8 * 9 * 32 * (size_t)S * ks, st))) return 1;
+  const int64_t nt = std::max<int64_t>((int64_t)S * nsl, (int64_t)S * nn) + 1;
+  k_nb_slice_off<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(S, nsl, (const int64_t*)h.t_off.p, ks, nn,
+                                                                (int64_t*)h.slice_off.p, (int*)h.node_list.p,
+                                                                (const int*)h.t_order.p);
+  const int64_t nf = (int64_t)S * nn;
+  k_nb_fill<<<(unsigned)((nf + 127) / 128), 128, 0, st>>>(S, nn, nsl, (const int*)h.t_order.p,
+                                                           (const int64_t*)h.t_off.p, (const int*)h.t_bcol.p, d_a_ptr,
+                                                           d_a_idx, d_a_val, ks, (unsigned*)h.desc.p,
+                                                           (double*)h.val.p, d_flags);
+  if ((e = cudaGetLastError())) return 1;
+  out.nn = nn;
+  out.nsl = nsl;
+  out.node_list = (const int*)h.node_list.p;
+  out.node_slot = (int*)h.node_slot.p;
+  out.slice_off = (const int64_t*)h.slice_off.p;
+  out.desc = (const unsigned*)h.desc.p;
+  out.val = (const double*)h.val.p;
+  return 0;
+}
+
+int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
+                       cudaStream_t st) {
+  if (cudaMemsetAsync(L.node_slot, 0xff, 4 * (size_t)S * L.nn, st) != cudaSuccess) return 1;
+  if (n_c > 0) k_nb_node_slots<<<(n_c + 255) / 256, 256, 0, st>>>(n_c, S, ci, cj, d_ct, L.node_slot);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int node_kernel_smem(int max_ct) { return 2 * kSlotsPerContact * 8 * max_ct + kNbRingBytes + 128; }
+
+int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct) {
+  NbFn f = nb_pick(op, cheb, true);
+  if (ensure_max_dynamic_smem((const void*)f) != cudaSuccess) return 0;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kNbThreads, node_kernel_smem(max_ct)) != cudaSuccess)
+    return 0;
+  return nb;
+}
+
+int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bool cheb, int max_ct, cudaStream_t st,
+                         std::string& err) {
+  NbFn f = nb_pick(op, cheb, p.n_c > 0);
+  cudaError_t e = ensure_max_dynamic_smem((const void*)f);
+  if (e != cudaSuccess) { err = cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
+  f<<<p.G, kNbThreads, node_kernel_smem(max_ct), st>>>(p, L);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("node-block scene launch: ") + cudaGetErrorString(e);
+    return VFPI_CUDA_ERROR;
+  }
+  return VFPI_OK;
+}
+
+}  // namespace vfpi

@@ -43,6 +43,9 @@ def _bind():
         L.vfpi_fem_step.argtypes = [C.c_void_p, C.POINTER(VfpiConfig), C.POINTER(_Stats), _lib._i32p]
         L.vfpi_fem_state.restype = C.c_int
         L.vfpi_fem_state.argtypes = [C.c_void_p, _lib._f64p, _lib._f64p]
+        L.vfpi_fem_set_node_layout.restype = C.c_int
+        L.vfpi_fem_set_node_layout.argtypes = [C.c_void_p, C.c_int32, _lib._i32p, C.c_int32, C.POINTER(C.c_int64),
+                                               _lib._i32p]
         L.vfpi_fem_reset.restype = C.c_int
         L.vfpi_fem_reset.argtypes = [C.c_void_p]
         L.vfpi_fem_state_device.restype = C.c_int
@@ -66,6 +69,35 @@ def _block_diag(mats):
         nnz += m.nnz
         off += m.shape[0]
     return np.concatenate(ptrs), np.concatenate(idx), np.concatenate(val)
+
+
+def node_block_template(indptr, indices, n):
+    """Node-block SELL template of one scene (``vfpi_fem_set_node_layout``) from
+    the CSC pattern of its K (every scene of a batch shares it): per node the
+    ascending list of 3x3 block columns its rows touch, nodes ordered by
+    decreasing block count (stable) in slices of 32, each slice as wide as its
+    busiest node. Returns (order, slice_off, block_cols)."""
+    nn = n // 3
+    indptr = np.asarray(indptr, dtype=np.int64)
+    col = np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr))
+    key = np.unique((col // 3) * nn + np.asarray(indices, dtype=np.int64) // 3)  # (node, block column), sorted
+    node, bcol = key // nn, key % nn
+    cnt = np.bincount(node, minlength=nn)
+    order = np.argsort(-cnt, kind="stable").astype(np.int32)
+    nsl = (nn + 31) // 32
+    pcnt = np.zeros(nsl * 32, dtype=np.int64)
+    pcnt[:nn] = cnt[order]
+    width = pcnt.reshape(nsl, 32).max(axis=1)
+    slice_off = np.zeros(nsl + 1, dtype=np.int64)
+    np.cumsum(width, out=slice_off[1:])
+    pos = np.empty(nn, dtype=np.int64)
+    pos[order] = np.arange(nn)
+    start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+    k = np.arange(key.shape[0]) - start[node]
+    p = pos[node]
+    block_cols = np.full(32 * slice_off[-1], -1, dtype=np.int32)
+    block_cols[32 * slice_off[p // 32] + 32 * k + p % 32] = bcol
+    return order, slice_off, block_cols
 
 
 def fem_batch_arrays(plan, X, kd, ad, m3, dt=1e-3, margin=1e-4, beta_err=0.2, e_rest=0.0, rest_threshold=0.01,
@@ -104,7 +136,7 @@ class FemBatch:
     ``FemBatch.assembled(...)`` takes ``scenes.fem_assemble``'s batched arrays
     directly (configs[2]'s 1024 scenes without per-scene objects)."""
 
-    def __init__(self, cubes, device=None, _arrays=None):
+    def __init__(self, cubes, device=None, _arrays=None, node_layout=True):
         if _arrays is None:
             c0 = cubes[0]
             for c in cubes:
@@ -142,12 +174,25 @@ class FemBatch:
                                       ptr(self._X), ptr(x), ptr(v), ptr(frame), C.byref(prm), C.byref(out))
         _raise_for(code, self.h)
         self.fb = out
+        self.node_kernel = False
+        if node_layout:
+            # K's CSC pattern of scene 0 (all scenes share it)
+            kp = self._k[0]
+            n0 = self.n_scene
+            order, soff, bcols = node_block_template(kp[: n0 + 1], self._k[1][: kp[n0]], n0)
+            if soff.shape[0] > 1 and int(np.diff(soff).max(initial=0)) <= 32:
+                rc = self.L.vfpi_fem_set_node_layout(self.fb, n0 // 3, ptr(order, _lib._i32p), soff.shape[0] - 1,
+                                                     ptr(soff, C.POINTER(C.c_int64)), ptr(bcols, _lib._i32p))
+                if rc not in (_lib.OK, _lib.UNSUPPORTED):
+                    _raise_for(rc, self.h)
+                self.node_kernel = rc == _lib.OK
 
     @classmethod
-    def assembled(cls, plan, X, kd, ad, m3, device=None, **params):
+    def assembled(cls, plan, X, kd, ad, m3, device=None, node_layout=True, **params):
         """Batch straight from ``scenes.fem_assemble(nx, Es, drops, yaws)``: scene k is
         bit-identical to ``FemCube.batch(...)[k]``."""
-        return cls(None, device=device, _arrays=fem_batch_arrays(plan, X, kd, ad, m3, **params))
+        return cls(None, device=device, _arrays=fem_batch_arrays(plan, X, kd, ad, m3, **params),
+                   node_layout=node_layout)
 
     def reset(self):
         """Back to the creation state (device to device, on the handle's stream)."""
@@ -160,12 +205,15 @@ class FemBatch:
         return int(x.value), int(v.value)
 
     def step(self, cfg: SolverConfig, per_scene=False):
+        """One step of every scene; ``node_kernel`` in the result says whether the
+        node-block iteration kernel ran (vs the row-SELL scene kernel)."""
         st = _Stats()
         its = np.zeros(self.S, dtype=np.int32) if per_scene else None
         code = self.L.vfpi_fem_step(self.fb, _c_config(cfg), C.byref(st),
                                     ptr(its, _lib._i32p) if its is not None else None)
         _raise_for(code, self.h)
         out = {f: getattr(st, f) for f, _ in _Stats._fields_}
+        out["node_kernel"] = bool(self.L.vfpi_set_tuning(self.h.h, 7, 0))
         if its is not None:
             out["iterations_per_scene"] = its
         return out

@@ -73,12 +73,13 @@ def test_fem_batch_without_divergence_is_unchanged():
 def test_pile_stepper_diverged_step_takes_contact_free_cg_step():
     import scipy.sparse as sp
 
+    from oracle import pile_host as H
     from paper_2201_09212_b200.pile import CubePile, PileStepper
     from paper_2201_09212_b200.solver import SolverConfig
 
     pile = CubePile(nx_cubes=2, ny_cubes=1, layers=2, nodes=4, seed=3, gap=0.0, jitter=0.0, gap_z=-1e-4)
     x0, v0 = pile.x.copy(), pile.v.copy()
-    b_o = pile.rhs()
+    b_o = H.rhs(pile)
     a_o = sp.csc_matrix((pile.a_data, pile.a_indices, pile.a_indptr), shape=(pile.n, pile.n))
     st = PileStepper(pile)
     r = st.step(SolverConfig(residual_tol=1e-8, max_iters=100, step_strategy="fixed-alpha", fixed_alpha=1e3))
