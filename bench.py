@@ -361,7 +361,7 @@ def run_ours(args):
 
     def one_run(record=None):
         ci = its = 0
-        loop_ms = setup_ms = kbytes = 0.0
+        loop_ms = setup_ms = kbytes = lbytes = 0.0
         max_it = div = 0
         for fb in batches:
             fb.reset()
@@ -375,10 +375,13 @@ def run_ours(args):
                 max_it = max(max_it, st["max_iterations"])
                 div += st["diverged_scenes"]
                 kbytes += float(np.dot(cost, st["iterations_per_scene"])) + 128.0 * st["contact_iterations"]
+                if fb.layout_bytes_per_scene_iter:
+                    lbytes += (float(st["iterations_per_scene"].sum()) * fb.layout_bytes_per_scene_iter
+                               + 128.0 * st["contact_iterations"])
         counters = torch.tensor([float(ci), float(its), float(div)], dtype=torch.float64, device=dev)
         finish_run(counters)
-        return dict(ci=ci, its=its, loop_ms=loop_ms, setup_ms=setup_ms, kbytes=kbytes, max_it=max_it, div=div,
-                    counters=counters)
+        return dict(ci=ci, its=its, loop_ms=loop_ms, setup_ms=setup_ms, kbytes=kbytes, lbytes=lbytes,
+                    max_it=max_it, div=div, counters=counters, node_kernel=all(fb.node_kernel for fb in batches))
 
     for _ in range(args.warmup):
         one_run()
@@ -440,6 +443,8 @@ def run_ours(args):
     t_local = sum(step_ms) / 1e3
     loop_local = sum(r["loop_ms"] for r in runs)
     kbytes_local = sum(r["kbytes"] for r in runs)
+    lbytes_local = sum(r["lbytes"] for r in runs)
+    node_kernel = all(r["node_kernel"] for r in runs)
     vals = torch.tensor([t_local, float(ci_local), e2e_t, float(e2e_ci), loop_local, kbytes_local,
                          float(sum(r["its"] for r in runs)), float(max(r["max_it"] for r in runs)),
                          float(sum(r["div"] for r in runs)), max(step_ms)], dtype=torch.float64, device=dev)
@@ -504,15 +509,22 @@ def run_ours(args):
                                   "NCCL all-reduce of counters + gather of final positions per run)",
                    "host_build_s": shard.build_s},
         "scene_steps_per_s": SCENES * SIM_STEPS * args.steps / t_max,
-        "roofline": {"bound": "hbm", "kernel": "k_iterate<scene batch> (one CTA per scene, TMA-ring SELL stream)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k_iterate_nodes (one CTA per scene, node-block SELL through a TMA ring)" if node_kernel
+                                else "k_iterate<scene batch> (one CTA per scene, row-SELL through a TMA ring)"),
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "layout_bytes_per_launch": (lbytes_local / (launches_per_run * args.steps)) if lbytes_local else None,
+                     "layout_frac": (lbytes_local / (loop_local * 1e-3) / 1e9 / peak) if lbytes_local else None,
                      "bytes_per_launch": kbytes_local / (launches_per_run * args.steps),
                      "kernel_ms_per_launch": loop_local / (launches_per_run * args.steps),
                      "launches_timed": launches_per_run * args.steps,
-                     "note": "algorithmic bytes per launch = sum over scenes of iterations x (12 nnz_num + 4 (n+1) "
-                             "+ 32 n) + 128 x contact-iterations (SURVEY §8(d)); time = CUDA events around each "
-                             "launch on the pipeline stream"},
+                     "note": "achieved/frac: algorithmic bytes per launch = sum over scenes of iterations x "
+                             "(12 nnz_num + 4 (n+1) + 32 n) + 128 x contact-iterations (SURVEY §8(d)), i.e. 12 B per "
+                             "stored entry; the node-block layout streams 3x3 blocks (4 B descriptor + 72 B values "
+                             "for up to 9 entries), ~25% fewer bytes, so frac can exceed 1; layout_frac counts the "
+                             "bytes the layout actually streams (the physical HBM fraction); time = CUDA events "
+                             "around each launch on the pipeline stream"},
         "e2e": {"value": e2e_ci_all / e2e_tmax, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "path": "FemBatch(pinned host arrays) -> 200 x FemBatch.step -> FemBatch.state (x, v to host)"},

@@ -46,6 +46,18 @@
 #define VFPI_NB_MIN_BLOCKS 2
 #endif
 
+#ifdef VFPI_NB_DEBUG
+#define NB_CHECK(cond, fmt, ...)                                                             \
+  do {                                                                                       \
+    if (!(cond)) printf("NB_CHECK %s:%d b=%d t=%d " fmt "\n", __FILE__, __LINE__, (int)blockIdx.x, \
+                        (int)threadIdx.x, __VA_ARGS__);                                      \
+  } while (0)
+#else
+#define NB_CHECK(cond, fmt, ...) \
+  do {                           \
+  } while (0)
+#endif
+
 namespace vfpi {
 
 namespace {
@@ -144,7 +156,7 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
 // the three row sums of this lane's node over its slice (width W) out of the ring
 template <class X>
 __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W, int lane, uint64_t pol, X x,
-                                        double& y0, double& y1, double& y2) {
+                                        double& y0, double& y1, double& y2, int nrows_dbg) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int k0 = 0; k0 < W; k0 += kNbChunk) {
     const int kk = min(kNbChunk, W - k0);
@@ -163,6 +175,7 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
         const unsigned m = d >> kMaskShift;
         if (m) {
           const int c = 3 * (int)(d & kColMask);
+          NB_CHECK(c + 2 < nrows_dbg, "gather c=%d n=%d d=%u", c, nrows_dbg, d);
           const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
           const double* v = vs + 9 * 32 * u;
           if (m & 0x001) a0 = dadd(a0, dmul(v[32 * 0], x0));
@@ -319,7 +332,9 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       double bv[3] = {0.0, 0.0, 0.0}, wv[3] = {0.0, 0.0, 0.0}, vc[3] = {0.0, 0.0, 0.0};
       if (live) {
         node = __ldg(L.node_list + pos);
+        NB_CHECK(node >= np0 && node < np1, "node=%d np0=%d np1=%d pos=%d", node, np0, np1, pos);
         if (HASC) slot = L.node_slot[node];
+        NB_CHECK(slot < 0 || slot + 2 < kSlotsPerContact * nct, "slot=%d nct=%d node=%d", slot, nct, node);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           bv[q] = __ldg(p.b + 3 * node + q);
@@ -328,7 +343,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
         }
       }
       double y[3];
-      if (W > 0) nb_rows(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2]);
+      if (W > 0) nb_rows(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n);
       else y[0] = y[1] = y[2] = 0.0;
       if (live) {
 #pragma unroll
@@ -357,6 +372,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
         const int m = __ldg(p.cont_list + k);
         const int loc = (k - c0) * kSlotsPerContact;
         const int ci = __ldg(p.col_i + m), cj = __ldg(p.col_j + m);
+        NB_CHECK(ci >= 3 * np0 && ci + 2 < 3 * np1 && m >= 0 && m < p.n_c, "contact m=%d ci=%d k=%d", m, ci, k);
         double R[9];
 #pragma unroll
         for (int t = 0; t < 9; ++t) R[t] = __ldg(p.frames + 9 * (size_t)m + t);

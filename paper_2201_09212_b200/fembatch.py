@@ -175,6 +175,9 @@ class FemBatch:
         _raise_for(code, self.h)
         self.fb = out
         self.node_kernel = False
+        # bytes one iteration of one scene streams with the row-SELL layout: 12 per
+        # stored entry + the row operands (the SURVEY §8(d) per-iteration count)
+        self.layout_bytes_per_scene_iter = None
         if node_layout:
             # K's CSC pattern of scene 0 (all scenes share it)
             kp = self._k[0]
@@ -186,6 +189,10 @@ class FemBatch:
                 if rc not in (_lib.OK, _lib.UNSUPPORTED):
                     _raise_for(rc, self.h)
                 self.node_kernel = rc == _lib.OK
+                if self.node_kernel:
+                    # node-block layout: 32 lanes x (4 B descriptor + 9 x 8 B values) per k-step,
+                    # + per row b, w, v_cur, v_next (32 B) + per node list and slot (8 B)
+                    self.layout_bytes_per_scene_iter = int(32 * 76 * soff[-1] + 32 * n0 + 8 * (n0 // 3))
 
     @classmethod
     def assembled(cls, plan, X, kd, ad, m3, device=None, node_layout=True, **params):

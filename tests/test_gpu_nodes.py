@@ -1,0 +1,88 @@
+"""The node-block SELL scene kernel (csrc/vfpi_nodes.cu) against the row-SELL
+scene kernel and the CPU oracle: FEM batches stepped through contact with
+either kernel end in bit-identical states with the same iteration counts,
+for every operator, Chebyshev, and the fixed-alpha step."""
+
+import numpy as np
+import pytest
+
+from oracle import fem_host as F
+
+pytestmark = pytest.mark.gpu
+
+
+def _cubes(nx, n, seed):
+    from paper_2201_09212_b200.scenes import FemCube
+
+    g = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        c = FemCube(nx=nx, E=float(g.uniform(5e4, 2e5)), drop=float(g.uniform(0.0005, 0.004)),
+                    yaw=float(g.uniform(0, 2 * np.pi)))
+        out.append(c)
+    return out
+
+
+def test_node_template_covers_every_block():
+    from paper_2201_09212_b200.fembatch import node_block_template
+    from paper_2201_09212_b200.scenes import FemCube
+
+    c = FemCube(nx=7, yaw=0.3)
+    order, soff, bcols = node_block_template(c.K.indptr, c.K.indices, c.n)
+    assert sorted(order.tolist()) == list(range(c.n // 3))
+    nb = int((bcols >= 0).sum())
+    K = c.K.tocoo()
+    assert nb == np.unique((K.row // 3) * (c.n // 3) + K.col // 3).size
+    w = np.diff(soff)
+    assert (w[:-1] >= w[1:]).all()  # decreasing block counts -> decreasing slice widths
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(chebyshev=True), dict(operator="proximal"),
+                                dict(operator="strict-anisotropic"), dict(step_strategy="fixed-alpha")])
+def test_node_kernel_equals_row_kernel(kw):
+    from paper_2201_09212_b200.fembatch import FemBatch
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=400, **kw)
+    a = FemBatch(_cubes(6, 12, 3), node_layout=True)
+    b = FemBatch(_cubes(6, 12, 3), node_layout=False)
+    assert a.node_kernel and not b.node_kernel
+    contacts = 0
+    for step in range(40):
+        sa, sb = a.step(cfg, per_scene=True), b.step(cfg, per_scene=True)
+        assert sa["node_kernel"] and not sb["node_kernel"]
+        assert sa["contacts"] == sb["contacts"], step
+        contacts += sa["contacts"]
+        assert np.array_equal(sa["iterations_per_scene"], sb["iterations_per_scene"]), step
+        assert sa["diverged_scenes"] == sb["diverged_scenes"]
+    assert contacts > 0
+    xa, va = a.state()
+    xb, vb = b.state()
+    if kw.get("chebyshev"):
+        # Chebyshev's rho = theta_l / theta_{l-1} depends on the reduction order
+        # of theta (the kernels visit rows in different orders; the reference's
+        # is an OpenBLAS dot): last-bit differences in nu, so tolerance-equal
+        assert np.linalg.norm(xa - xb) <= 1e-12 * np.linalg.norm(xb)
+        assert np.linalg.norm(va - vb) <= 1e-9 * np.linalg.norm(vb)
+    else:
+        assert np.array_equal(xa, xb) and np.array_equal(va, vb)
+    a.close()
+    b.close()
+
+
+def test_node_kernel_matches_oracle_pipeline():
+    from paper_2201_09212_b200.fembatch import FemBatch
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    steps = 30
+    fb = FemBatch(_cubes(5, 6, 11))
+    assert fb.node_kernel
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=500)
+    its = [fb.step(cfg, per_scene=True)["iterations_per_scene"].tolist() for _ in range(steps)]
+    x, v = fb.state()
+    for k, c in enumerate(_cubes(5, 6, 11)):
+        rec = []
+        F.oracle_steps(c, steps, residual_tol=1e-8, max_iters=500, record=rec)
+        assert [r["iterations"] for r in rec] == [row[k] for row in its], k
+        assert sum(r["n_c"] for r in rec) > 0
+        assert np.array_equal(x[k], c.x) and np.array_equal(v[k], c.v), k
