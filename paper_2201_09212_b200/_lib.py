@@ -225,14 +225,21 @@ class Handle:
         return torch.cuda.ExternalStream(self.stream_ptr(), device=torch.device("cuda", self.device))
 
     def set_kernel(self, mode: str):
-        """'auto' | 'resident' | 'streaming' for later solves on this handle."""
+        """'auto' | 'resident' | 'streaming' for later solves on this handle
+        ('streaming' = a global-memory kernel: node-block when eligible, see
+        ``set_node_kernel``, else row-SELL)."""
         code = {"auto": 0, "resident": 1, "streaming": 2}[mode]
         self.L.vfpi_set_kernel(self.h, code)
 
     def last_layout(self):
         r, g = C.c_int(), C.c_int()
         self.L.vfpi_last_layout(self.h, C.byref(r), C.byref(g))
-        return {"resident": bool(r.value), "ctas": int(g.value)}
+        return {"resident": bool(r.value), "ctas": int(g.value),
+                "node_kernel": bool(self.L.vfpi_set_tuning(self.h, 7, 0))}
+
+    def set_node_kernel(self, on: bool):
+        """Use the node-block kernels (FEM batches, single systems) when eligible (default on)."""
+        self.L.vfpi_set_tuning(self.h, 6, 1 if on else 0)
 
     def __del__(self):
         try:

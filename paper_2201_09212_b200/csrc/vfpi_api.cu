@@ -68,6 +68,7 @@ struct vfpi_handle {
   vfpi::PileWork pile;
   vfpi::NodalizeWork nod;
   vfpi::HfWork hf;
+  vfpi::NodeGridWork ngw;  // node-block layout of the last single-system solve
   int last_G = 0;
   int* h_flags = nullptr;  // pinned
 };
@@ -321,6 +322,11 @@ void vfpi_destroy(vfpi_handle* h) {
   for (auto* b : {&hw.flag, &hw.pos, &hw.tmp, &hw.ci, &hw.cj, &hw.fr, &hw.mu, &hw.phi})
     if (b->p) cudaFree(b->p);
   if (hw.h_small) cudaFreeHost(hw.h_small);
+  vfpi::NodeGridWork& gw = h->ngw;
+  for (auto* b : {&gw.blk_pos, &gw.blk_slice, &gw.key, &gw.key2, &gw.val_i, &gw.node_list, &gw.cnt, &gw.node_slot,
+                  &gw.width, &gw.slice_off, &gw.flags, &gw.vs, &gw.jt, &gw.tmp, &gw.desc, &gw.val})
+    if (b->p) cudaFree(b->p);
+  if (gw.h_small) cudaFreeHost(gw.h_small);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
   for (SetupGraphSet* gs : {&h->graph_layout, &h->graph_pack})
@@ -492,6 +498,22 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
     rc = vfpi::setup_pack(ws, *d, G, false, *hs, st, h->err, h->launches);
   }
   if (rc) return rc;
+  // single systems that do not fit on chip: the node-block streaming kernel
+  // (csrc/vfpi_nodes.cu) when every contact column is node aligned and the
+  // step is not Barzilai-Borwein; otherwise the row-SELL streaming kernel
+  bool use_nodes = false;
+  int G_nodes = 0;
+  vfpi::NodeLayoutDev nl;
+  if (!resident && h->node_kernel && !bb && n % 3 == 0) {
+    const int bps = vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, 0, true);
+    if (bps > 0) {
+      G_nodes = bps * ws.num_sms;
+      rc = vfpi::node_grid_build(h->ngw, *d, G_nodes, P<int64_t>(ws.row_ptr), P<int>(ws.rowcnt), P<int>(ws.perm),
+                                 P<int>(ws.colof), st, nl, h->err, h->launches);
+      if (rc == VFPI_OK) use_nodes = true;
+      else if (rc != VFPI_UNSUPPORTED) return rc;
+    }
+  }
   const size_t smem_res_full = smem_res;
   rc = vfpi::setup_step_matrix(ws, *d, *cfg, w_cached, st, h->err, h->launches);
   if (rc) return rc;
@@ -507,6 +529,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   }
   CK(cudaMemsetAsync(ws.vbuf.p, 0, 3 * 8 * npad, st));
   CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)std::max(n_c, 1)));
+  if (use_nodes) G = G_nodes;
   CK(vfpi::ensure(ws.partials, 2 * 8 * (size_t)G * vfpi::kPartialStride));
   CK(vfpi::ensure(ws.status, sizeof(vfpi::SolveStatus)));
   CK(vfpi::ensure(ws.bar_flags, 4 * (size_t)G));
@@ -581,9 +604,14 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.omega = cfg->omega;
   p.cfactor = cfg->consistency_factor;
   (void)tr;
-  rc = resident ? vfpi::launch_iterate_resident(p, cfg->op, cheb, bb, smem_res_full, st, h->err)
-                : vfpi::launch_iterate(p, cfg->op, cheb, bb, smem, st, h->err);
+  if (use_nodes) {
+    rc = vfpi::launch_iterate_nodes(p, nl, cfg->op, cheb, 0, st, h->err, true);
+  } else {
+    rc = resident ? vfpi::launch_iterate_resident(p, cfg->op, cheb, bb, smem_res_full, st, h->err)
+                  : vfpi::launch_iterate(p, cfg->op, cheb, bb, smem, st, h->err);
+  }
   if (rc) return rc;
+  h->last_node_kernel = use_nodes ? 1 : 0;
   h->last_resident = resident ? 1 : 0;
   h->last_G = G;
   ++h->launches;

@@ -383,7 +383,11 @@ int launch_cg_grid(int G, int64_t n, const int32_t* indptr, const int32_t* indic
 
 // ---- node-block SELL scene kernel (vfpi_nodes.cu; FEM batches) ---------------
 struct NodeLayoutDev {
-  int nn = 0, nsl = 0;                 // nodes and node slices per scene (every scene the same template)
+  int nn = 0, nsl = 0;                 // nodes and node slices (per scene for batches, of the system for grids)
+  const int* blk_slice = nullptr;      // [G+1] node slices of every CTA
+  const int* blk_pos = nullptr;        // [G+1] node positions of every CTA
+  double* vs_g = nullptr;              // grid mode: v* of contact rows [6 n_c]
+  double* jt_g = nullptr;              // grid mode: J_c^T lam of contact rows [6 n_c]
   const int* node_list = nullptr;      // [S*nn] position -> global node
   int* node_slot = nullptr;            // [S*nn] global node -> contact slot base (6 per contact) or -1
   const int64_t* slice_off = nullptr;  // [S*nsl+1] k-step offset of every slice
@@ -393,15 +397,24 @@ struct NodeLayoutDev {
 struct NodeLayoutHost {
   int nn = 0, nsl = 0;
   int64_t k_scene = 0;                 // k-steps per scene
-  Workspace::Buf t_order, t_off, t_bcol, desc, val, slice_off, node_list, node_slot;
+  Workspace::Buf t_order, t_off, t_bcol, desc, val, slice_off, node_list, node_slot, blk_slice, blk_pos;
 };
+struct NodeGridWork {  // single-system node-block layout (rebuilt per solve)
+  Workspace::Buf blk_pos, blk_slice, key, key2, val_i, node_list, cnt, node_slot, width, slice_off, flags, vs, jt,
+      tmp, desc, val;
+  int64_t* h_small = nullptr;  // pinned [2]
+  int64_t k_total = 0;
+};
+int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t* row_ptr, const int* rowcnt,
+                    const int* perm, const int* colof, cudaStream_t st, NodeLayoutDev& out, std::string& err,
+                    int64_t& launches);
 int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
                       NodeLayoutDev& out, int* d_flags, cudaStream_t st);
 int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
                        cudaStream_t st);
 int node_kernel_smem(int max_ct);
-int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct);
+int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, bool grid = false);
 int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bool cheb, int max_ct, cudaStream_t st,
-                         std::string& err);
+                         std::string& err, bool grid = false);
 
 }  // namespace vfpi

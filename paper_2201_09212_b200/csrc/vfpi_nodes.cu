@@ -30,8 +30,17 @@
 // in a different order than the row kernel (both are the GPU's own fixed
 // order; the reference's are OpenBLAS dots), so v and lam are bit-identical
 // to the row kernel's for the same iteration count.
+#include <cooperative_groups.h>
+
+#include <climits>
+#include <vector>
+
+#include <cub/cub.cuh>
+
 #include "vfpi_internal.cuh"
 #include "vfpi_math.cuh"
+
+namespace cg = cooperative_groups;
 
 #ifndef VFPI_NB_CHUNK
 #define VFPI_NB_CHUNK 2  // k-steps (node blocks) per ring stage
@@ -203,7 +212,52 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
   y2 = a2;
 }
 
-template <int OP, bool CHEB, bool HASC>
+// every CTA reduces all G partials in the same fixed order (warp 0)
+__device__ __forceinline__ void nb_grid_totals(const double* __restrict__ part, int G, double* sm_tot) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int g0 = lane; g0 < G; g0 += 32 * 4) {
+      double x[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int g = g0 + 32 * u;
+        const double* q = part + (size_t)g * kPartialStride;
+        x[u][0] = g < G ? __ldcg(q + 0) : 0.0;
+        x[u][1] = g < G ? __ldcg(q + 1) : 0.0;
+        x[u][2] = g < G ? __ldcg(q + 2) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (g0 + 32 * u < G) {
+          a = dadd(a, x[u][0]);
+          b = dadd(b, x[u][1]);
+          c = dadd(c, x[u][2]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = dadd(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = dadd(b, __shfl_xor_sync(0xffffffffu, b, o));
+      c = dadd(c, __shfl_xor_sync(0xffffffffu, c, o));
+    }
+    if (lane == 0) {
+      sm_tot[0] = a;
+      sm_tot[1] = b;
+      sm_tot[2] = c;
+    }
+  }
+  __syncthreads();
+}
+
+// GRID = false: a batch of independent scenes, CTA b = scene b (its own loop,
+//               contacts staged in shared memory, CTA barriers only);
+// GRID = true : one system over a cooperative grid, CTA b owns a range of node
+//               slices; v* / J_c^T lam of contact rows go through global
+//               arrays, so an iteration is sweep | grid barrier | contacts |
+//               grid barrier (reductions), and every CTA takes the same
+//               decision from the same fixed-order totals.
+template <int OP, bool CHEB, bool HASC, bool GRID>
 __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_nodes(IterParams p, NodeLayoutDev L) {
   extern __shared__ double smem[];
   __shared__ double sm_warp[3 * (kNbThreads / 32)];
@@ -212,13 +266,14 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
 
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int np0 = b * L.nn, np1 = np0 + L.nn;          // node positions of the scene
-  const int s0 = b * L.nsl, s1 = s0 + L.nsl;          // node slices of the scene
-  const int c0 = p.blk_ct[b], c1 = p.blk_ct[b + 1];
-  const int nct = c1 - c0;
-  double* vs_s = smem;                                // v* of contact rows    [6*nct]
-  double* jt_s = smem + kSlotsPerContact * nct;       // J_c^T lam_{l-1} rows  [6*nct]
-  for (int t = threadIdx.x; t < kSlotsPerContact * nct; t += blockDim.x) jt_s[t] = 0.0;
+  const int np0 = L.blk_pos[b], np1 = L.blk_pos[b + 1];      // node positions of the CTA
+  const int s0 = L.blk_slice[b], s1 = L.blk_slice[b + 1];    // node slices of the CTA
+  const int c0 = GRID ? 0 : p.blk_ct[b], c1 = GRID ? p.n_c : p.blk_ct[b + 1];
+  const int nct = GRID ? 0 : c1 - c0;
+  double* vs_s = GRID ? L.vs_g : smem;                       // v* of contact rows    [6*contacts]
+  double* jt_s = GRID ? L.jt_g : smem + kSlotsPerContact * nct;  // J_c^T lam_{l-1} rows
+  if (!GRID)
+    for (int t = threadIdx.x; t < kSlotsPerContact * nct; t += blockDim.x) jt_s[t] = 0.0;
 
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -257,8 +312,9 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   double rho = 0.0, nu = 1.0, theta_prev = 0.0;
   double alpha = 0.0;
   bool use_alpha = false;
-  if (p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
-    // fixed-alpha default 1 / max|diag| of this scene (solver.py:368)
+  if (!GRID && p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
+    // scene batches: fixed-alpha default 1 / max|diag| of this scene (solver.py:368);
+    // a single system gets it from the setup (w filled with alpha)
     double mx = -INFINITY, nanf = 0.0;
     for (int r = 3 * np0 + threadIdx.x; r < 3 * np1; r += blockDim.x) {
       const double a = fabs(__ldg(p.diag + r));
@@ -285,8 +341,9 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     use_alpha = true;
     __syncthreads();
   }
-  double* trace = p.trace + (size_t)b * p.trace_stride;
-  SolveStatus* status = p.status + b;
+  double* trace = GRID ? p.trace : p.trace + (size_t)b * p.trace_stride;
+  SolveStatus* status = GRID ? p.status : p.status + b;
+  const bool writer = GRID ? (b == 0) : true;  // the CTA that writes trace / status
   bool pending = false;
   int final_buf = 0, final_lam = 0, iters = 0, conv = 0, div = 0;
   double consistency = NAN;
@@ -297,6 +354,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     const double* vprev = vb[(l + 1) % 3];
     double* vnext = vb[l % 3];
     double* __restrict__ lam_out = lb[l & 1];
+    double* part = p.partials + (size_t)(l & 1) * p.G * kPartialStride;
 
     if (CHEB && !check_only) {
       if (l < p.cheby_start) nu = 1.0;
@@ -332,9 +390,9 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       double bv[3] = {0.0, 0.0, 0.0}, wv[3] = {0.0, 0.0, 0.0}, vc[3] = {0.0, 0.0, 0.0};
       if (live) {
         node = __ldg(L.node_list + pos);
-        NB_CHECK(node >= np0 && node < np1, "node=%d np0=%d np1=%d pos=%d", node, np0, np1, pos);
+        NB_CHECK(node >= 0 && 3 * node + 2 < p.n, "node=%d np0=%d np1=%d pos=%d", node, np0, np1, pos);
         if (HASC) slot = L.node_slot[node];
-        NB_CHECK(slot < 0 || slot + 2 < kSlotsPerContact * nct, "slot=%d nct=%d node=%d", slot, nct, node);
+        NB_CHECK(slot < 0 || GRID || slot + 2 < kSlotsPerContact * nct, "slot=%d nct=%d node=%d", slot, nct, node);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           bv[q] = __ldg(p.b + 3 * node + q);
@@ -367,12 +425,14 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
 
     // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter -------
     if (HASC && !check_only) {
-      __syncthreads();
-      for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-        const int m = __ldg(p.cont_list + k);
+      if constexpr (GRID) cg::this_grid().sync();
+      else __syncthreads();
+      const int kstep = GRID ? (int)(gridDim.x * blockDim.x) : (int)blockDim.x;
+      for (int k = c0 + (GRID ? (int)(b * blockDim.x) : 0) + threadIdx.x; k < c1; k += kstep) {
+        const int m = GRID ? k : __ldg(p.cont_list + k);
         const int loc = (k - c0) * kSlotsPerContact;
         const int ci = __ldg(p.col_i + m), cj = __ldg(p.col_j + m);
-        NB_CHECK(ci >= 3 * np0 && ci + 2 < 3 * np1 && m >= 0 && m < p.n_c, "contact m=%d ci=%d k=%d", m, ci, k);
+        NB_CHECK(ci >= 0 && ci + 2 < p.n && m >= 0 && m < p.n_c, "contact m=%d ci=%d k=%d", m, ci, k);
         double R[9];
 #pragma unroll
         for (int t = 0; t < 9; ++t) R[t] = __ldg(p.frames + 9 * (size_t)m + t);
@@ -422,6 +482,15 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
 
     // ---- (4) residual reduction + decision -------------------------------
     cta_sum3(th, fr, nf, sm_warp, sm_tot);
+    if constexpr (GRID) {
+      if (threadIdx.x == 0) {
+        part[(size_t)b * kPartialStride + 0] = sm_tot[0];
+        part[(size_t)b * kPartialStride + 1] = sm_tot[1];
+        part[(size_t)b * kPartialStride + 2] = sm_tot[2];
+      }
+      cg::this_grid().sync();
+      nb_grid_totals(part, p.G, sm_tot);
+    }
     const double theta = dsqrt(sm_tot[0]);
     const double fres = dsqrt(sm_tot[1]);
     const bool nonfinite = sm_tot[2] > 0.0;
@@ -439,7 +508,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       final_buf = (l - 1) % 3; final_lam = (l - 1) & 1;
       break;
     }
-    if (threadIdx.x == 0) trace[l - 1] = theta;
+    if (writer && threadIdx.x == 0) trace[l - 1] = theta;
     if (nonfinite) {
       iters = l; div = 1;
       final_buf = l % 3; final_lam = l & 1;
@@ -456,14 +525,19 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     }
   }
   const double* vfin = vb[final_buf];
-  for (int r = 3 * np0 + threadIdx.x; r < 3 * np1; r += blockDim.x) p.out_v[r] = vfin[r];
+  for (int pos = np0 + threadIdx.x; pos < np1; pos += blockDim.x) {
+    const int node = __ldg(L.node_list + pos);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) p.out_v[3 * node + q] = vfin[3 * node + q];
+  }
   const double* lfin = lb[final_lam];
-  for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
-    const int m = __ldg(p.cont_list + k);
+  const int kstep = GRID ? (int)(gridDim.x * blockDim.x) : (int)blockDim.x;
+  for (int k = c0 + (GRID ? (int)(b * blockDim.x) : 0) + threadIdx.x; k < c1; k += kstep) {
+    const int m = GRID ? k : __ldg(p.cont_list + k);
 #pragma unroll
     for (int t = 0; t < 3; ++t) p.out_lam[3 * (size_t)m + t] = lfin[3 * (size_t)m + t];
   }
-  if (threadIdx.x == 0) {
+  if (writer && threadIdx.x == 0) {
     status->iterations = iters;
     status->converged = conv;
     status->diverged = div;
@@ -515,7 +589,8 @@ __global__ void k_nb_fill(int S, int nn, int nsl, const int* __restrict__ t_orde
 }
 
 __global__ void k_nb_slice_off(int S, int nsl, const int64_t* __restrict__ t_off, int64_t k_scene, int nn,
-                               int64_t* __restrict__ off, int* __restrict__ node_list, const int* __restrict__ t_order) {
+                               int64_t* __restrict__ off, int* __restrict__ node_list, const int* __restrict__ t_order,
+                               int* __restrict__ blk_slice, int* __restrict__ blk_pos) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid < (int64_t)S * nsl) {
     const int s = (int)(gid / nsl), t = (int)(gid % nsl);
@@ -523,6 +598,10 @@ __global__ void k_nb_slice_off(int S, int nsl, const int64_t* __restrict__ t_off
   }
   if (gid == 0) off[(int64_t)S * nsl] = (int64_t)S * k_scene;
   if (gid < (int64_t)S * nn) node_list[gid] = (int)(gid / nn) * nn + t_order[gid % nn];
+  if (gid <= S) {
+    blk_slice[gid] = (int)gid * nsl;
+    blk_pos[gid] = (int)gid * nn;
+  }
 }
 
 __global__ void k_nb_node_slots(int n_c, int G, const int* __restrict__ ci, const int* __restrict__ cj,
@@ -540,80 +619,297 @@ __global__ void k_nb_node_slots(int n_c, int G, const int* __restrict__ ci, cons
   if (cj[k] >= 0) node_slot[cj[k] / 3] = loc + 3;
 }
 
+// ---- single-system (grid) layout, built per solve from the row-sorted entries --
+// (setup_pack: perm[row_ptr[r] + k] = CSC index of the k-th numeric entry of
+// row r in increasing column order, colof = its column)
+
+__device__ __forceinline__ int ng_owner(const int* __restrict__ blk_pos, int G, int pos) {
+  int lo = 0, hi = G;  // blk_pos[lo] <= pos < blk_pos[lo + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (blk_pos[mid] <= pos) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// distinct block columns of a node's three rows (3-way merge); key sorts the
+// CTA's nodes by decreasing count
+__global__ void k_ng_count(int nn, int G, const int* __restrict__ blk_pos, const int64_t* __restrict__ row_ptr,
+                           const int* __restrict__ rowcnt, const int* __restrict__ perm, const int* __restrict__ colof,
+                           unsigned* __restrict__ key, int* __restrict__ val, int* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  int64_t e[3], end[3];
+  for (int q = 0; q < 3; ++q) {
+    e[q] = row_ptr[3 * i + q];
+    end[q] = e[q] + rowcnt[3 * i + q];
+  }
+  int c = 0;
+  for (;;) {
+    int bc = INT_MAX;
+    for (int q = 0; q < 3; ++q)
+      if (e[q] < end[q]) bc = min(bc, colof[perm[e[q]]] / 3);
+    if (bc == INT_MAX) break;
+    ++c;
+    for (int q = 0; q < 3; ++q)
+      while (e[q] < end[q] && colof[perm[e[q]]] / 3 == bc) ++e[q];
+  }
+  cnt[i] = c;
+  const int g = ng_owner(blk_pos, G, i);
+  key[i] = ((unsigned)g << 12) | (unsigned)(4095 - min(c, 4095));
+  val[i] = i;
+}
+
+__global__ void k_ng_widths(int nsl, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_pos,
+                            const int* __restrict__ node_list, const int* __restrict__ cnt, int64_t* __restrict__ w) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > nsl) return;
+  if (s == nsl) { w[s] = 0; return; }
+  int lo = 0, hi = G;  // owner CTA of slice s
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (blk_slice[mid] <= s) lo = mid;
+    else hi = mid;
+  }
+  const int pos = blk_pos[lo] + 32 * (s - blk_slice[lo]);  // its first (busiest) node
+  w[s] = pos < blk_pos[lo + 1] ? cnt[node_list[pos]] : 0;
+}
+
+__global__ void k_ng_fill(int nn, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_pos,
+                          const int* __restrict__ node_list, const int64_t* __restrict__ slice_off,
+                          const int64_t* __restrict__ row_ptr, const int* __restrict__ rowcnt,
+                          const int* __restrict__ perm, const int* __restrict__ colof, const double* __restrict__ data,
+                          unsigned* __restrict__ desc, double* __restrict__ val) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= nn) return;
+  const int g = ng_owner(blk_pos, G, pos);
+  const int loc = pos - blk_pos[g];
+  const int s = blk_slice[g] + (loc >> 5), lane = loc & 31;
+  const int64_t off = slice_off[s];
+  const int W = (int)(slice_off[s + 1] - off);
+  const int i = node_list[pos];
+  int64_t e[3], end[3];
+  for (int q = 0; q < 3; ++q) {
+    e[q] = row_ptr[3 * i + q];
+    end[q] = e[q] + rowcnt[3 * i + q];
+  }
+  int k = 0;
+  for (;;) {
+    int bc = INT_MAX;
+    for (int q = 0; q < 3; ++q)
+      if (e[q] < end[q]) bc = min(bc, colof[perm[e[q]]] / 3);
+    if (bc == INT_MAX || k >= W) break;
+    unsigned mask = 0u;
+    for (int q = 0; q < 3; ++q)
+      while (e[q] < end[q]) {
+        const int ent = perm[e[q]];
+        const int col = colof[ent];
+        if (col / 3 != bc) break;
+        const int t = 3 * q + col % 3;
+        val[((off + k) * 9 + t) * 32 + lane] = data[ent];
+        mask |= 1u << t;
+        ++e[q];
+      }
+    desc[(off + k) * 32 + lane] = (mask << kMaskShift) | (unsigned)bc;
+    ++k;
+  }
+  for (; k < W; ++k) desc[(off + k) * 32 + lane] = 0u;
+}
+
+__global__ void k_ng_contact_check(int n_c, const int* __restrict__ ci, const int* __restrict__ cj,
+                                   int* __restrict__ bad) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n_c && (ci[k] % 3 != 0 || (cj[k] >= 0 && cj[k] % 3 != 0))) atomicOr(bad, 1);
+}
+
+__global__ void k_ng_node_slots(int n_c, const int* __restrict__ ci, const int* __restrict__ cj,
+                                int* __restrict__ node_slot) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_c) return;
+  node_slot[ci[k] / 3] = kSlotsPerContact * k;
+  if (cj[k] >= 0) node_slot[cj[k] / 3] = kSlotsPerContact * k + 3;
+}
+
 using NbFn = void (*)(IterParams, NodeLayoutDev);
 
-template <int OP>
+template <int OP, bool GRID>
 NbFn nb_pick2(bool cheb, bool hasc) {
-  if (cheb) return hasc ? k_iterate_nodes<OP, true, true> : k_iterate_nodes<OP, true, false>;
-  return hasc ? k_iterate_nodes<OP, false, true> : k_iterate_nodes<OP, false, false>;
+  if (cheb) return hasc ? k_iterate_nodes<OP, true, true, GRID> : k_iterate_nodes<OP, true, false, GRID>;
+  return hasc ? k_iterate_nodes<OP, false, true, GRID> : k_iterate_nodes<OP, false, false, GRID>;
 }
 
-NbFn nb_pick(int op, bool cheb, bool hasc) {
-  if (op == OP_PROXIMAL) return nb_pick2<OP_PROXIMAL>(cheb, hasc);
-  if (op == OP_ANISO) return nb_pick2<OP_ANISO>(cheb, hasc);
-  return nb_pick2<OP_STRICT>(cheb, hasc);
+NbFn nb_pick(int op, bool cheb, bool hasc, bool grid) {
+  if (grid) {
+    if (op == OP_PROXIMAL) return nb_pick2<OP_PROXIMAL, true>(cheb, hasc);
+    if (op == OP_ANISO) return nb_pick2<OP_ANISO, true>(cheb, hasc);
+    return nb_pick2<OP_STRICT, true>(cheb, hasc);
+  }
+  if (op == OP_PROXIMAL) return nb_pick2<OP_PROXIMAL, false>(cheb, hasc);
+  if (op == OP_ANISO) return nb_pick2<OP_ANISO, false>(cheb, hasc);
+  return nb_pick2<OP_STRICT, false>(cheb, hasc);
 }
+
+inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
 }  // namespace
 
 int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
                       NodeLayoutDev& out, int* d_flags, cudaStream_t st) {
-  cudaError_t e;
   const int nn = h.nn, nsl = h.nsl;
   const int64_t ks = h.k_scene;
-  if ((e = ensure(h.desc, 4 * 32 * (size_t)std::max<int64_t>(S * ks, 1))) ||
-      (e = ensure(h.val, 8 * 9 * 32 * (size_t)std::max<int64_t>(S * ks, 1))) ||
-      (e = ensure(h.slice_off, 8 * ((size_t)S * nsl + 1))) || (e = ensure(h.node_list, 4 * (size_t)S * nn)) ||
-      (e = ensure(h.node_slot, 4 * (size_t)S * nn)))
+  if (ensure(h.desc, 4 * 32 * (size_t)std::max<int64_t>(S * ks, 1)) ||
+      ensure(h.val, 8 * 9 * 32 * (size_t)std::max<int64_t>(S * ks, 1)) ||
+      ensure(h.slice_off, 8 * ((size_t)S * nsl + 1)) || ensure(h.node_list, 4 * (size_t)S * nn) ||
+      ensure(h.node_slot, 4 * (size_t)S * nn) || ensure(h.blk_slice, 4 * ((size_t)S + 1)) ||
+      ensure(h.blk_pos, 4 * ((size_t)S + 1)))
     return 1;
-  if ((e = cudaMemsetAsync(h.val.p, 0, 8 * 9 * 32 * (size_t)S * ks, st))) return 1;
+  // padding lanes (positions past the scene's last node) are never filled:
+  // their descriptors must read as empty
+  if (cudaMemsetAsync(h.val.p, 0, 8 * 9 * 32 * (size_t)S * ks, st) ||
+      cudaMemsetAsync(h.desc.p, 0, 4 * 32 * (size_t)S * ks, st))
+    return 1;
   const int64_t nt = std::max<int64_t>((int64_t)S * nsl, (int64_t)S * nn) + 1;
-  k_nb_slice_off<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(S, nsl, (const int64_t*)h.t_off.p, ks, nn,
-                                                                (int64_t*)h.slice_off.p, (int*)h.node_list.p,
-                                                                (const int*)h.t_order.p);
+  k_nb_slice_off<<<nblk(nt), 256, 0, st>>>(S, nsl, (const int64_t*)h.t_off.p, ks, nn, (int64_t*)h.slice_off.p,
+                                           (int*)h.node_list.p, (const int*)h.t_order.p, (int*)h.blk_slice.p,
+                                           (int*)h.blk_pos.p);
   const int64_t nf = (int64_t)S * nn;
-  k_nb_fill<<<(unsigned)((nf + 127) / 128), 128, 0, st>>>(S, nn, nsl, (const int*)h.t_order.p,
-                                                           (const int64_t*)h.t_off.p, (const int*)h.t_bcol.p, d_a_ptr,
-                                                           d_a_idx, d_a_val, ks, (unsigned*)h.desc.p,
-                                                           (double*)h.val.p, d_flags);
-  if ((e = cudaGetLastError())) return 1;
+  k_nb_fill<<<nblk(nf, 128), 128, 0, st>>>(S, nn, nsl, (const int*)h.t_order.p, (const int64_t*)h.t_off.p,
+                                           (const int*)h.t_bcol.p, d_a_ptr, d_a_idx, d_a_val, ks, (unsigned*)h.desc.p,
+                                           (double*)h.val.p, d_flags);
+  if (cudaGetLastError() != cudaSuccess) return 1;
   out.nn = nn;
   out.nsl = nsl;
+  out.blk_slice = (const int*)h.blk_slice.p;
+  out.blk_pos = (const int*)h.blk_pos.p;
   out.node_list = (const int*)h.node_list.p;
   out.node_slot = (int*)h.node_slot.p;
   out.slice_off = (const int64_t*)h.slice_off.p;
   out.desc = (const unsigned*)h.desc.p;
   out.val = (const double*)h.val.p;
+  out.vs_g = out.jt_g = nullptr;
   return 0;
 }
 
 int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
                        cudaStream_t st) {
   if (cudaMemsetAsync(L.node_slot, 0xff, 4 * (size_t)S * L.nn, st) != cudaSuccess) return 1;
-  if (n_c > 0) k_nb_node_slots<<<(n_c + 255) / 256, 256, 0, st>>>(n_c, S, ci, cj, d_ct, L.node_slot);
+  if (n_c > 0) k_nb_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, S, ci, cj, d_ct, L.node_slot);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t* row_ptr, const int* rowcnt,
+                    const int* perm, const int* colof, cudaStream_t st, NodeLayoutDev& out, std::string& err,
+                    int64_t& launches) {
+  auto fail = [&](const char* what) {
+    err = std::string("node-block layout: ") + what;
+    return VFPI_CUDA_ERROR;
+  };
+  const int n = (int)d.n, n_c = (int)d.n_c;
+  if (n % 3 != 0 || n <= 0) return VFPI_UNSUPPORTED;
+  const int nn = n / 3;
+  if (nn >= (1 << 23)) return VFPI_UNSUPPORTED;
+  // CTA g owns node positions [floor(nn g / G), floor(nn (g+1) / G)) and their ceil(count / 32) slices
+  std::vector<int> bpos((size_t)G + 1), bsl((size_t)G + 1);
+  for (int g = 0; g <= G; ++g) bpos[g] = (int)((int64_t)nn * g / G);
+  bsl[0] = 0;
+  for (int g = 0; g < G; ++g) bsl[g + 1] = bsl[g] + (bpos[g + 1] - bpos[g] + 31) / 32;
+  const int nsl = bsl[G];
+  if (ensure(w.blk_pos, 4 * ((size_t)G + 1)) || ensure(w.blk_slice, 4 * ((size_t)G + 1)) ||
+      ensure(w.key, 4 * (size_t)nn) || ensure(w.key2, 4 * (size_t)nn) || ensure(w.val_i, 4 * (size_t)nn) ||
+      ensure(w.node_list, 4 * (size_t)nn) || ensure(w.cnt, 4 * (size_t)nn) || ensure(w.node_slot, 4 * (size_t)nn) ||
+      ensure(w.width, 8 * ((size_t)nsl + 1)) || ensure(w.slice_off, 8 * ((size_t)nsl + 1)) ||
+      ensure(w.flags, 16) || ensure(w.vs, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1)) ||
+      ensure(w.jt, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1)))
+    return fail("allocation");
+  if (!w.h_small && cudaMallocHost(&w.h_small, 16) != cudaSuccess) return fail("pinned allocation");
+  if (cudaMemcpyAsync(w.blk_pos.p, bpos.data(), 4 * ((size_t)G + 1), cudaMemcpyHostToDevice, st) ||
+      cudaMemcpyAsync(w.blk_slice.p, bsl.data(), 4 * ((size_t)G + 1), cudaMemcpyHostToDevice, st) ||
+      cudaMemsetAsync(w.flags.p, 0, 16, st))
+    return fail("upload");
+  k_ng_count<<<nblk(nn), 256, 0, st>>>(nn, G, (const int*)w.blk_pos.p, row_ptr, rowcnt, perm, colof,
+                                       (unsigned*)w.key.p, (int*)w.val_i.p, (int*)w.cnt.p);
+  if (n_c > 0) k_ng_contact_check<<<nblk(n_c), 256, 0, st>>>(n_c, d.col_i, d.col_j, (int*)w.flags.p);
+  int eb = 12;
+  while ((1 << (eb - 12)) <= G) ++eb;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned*)w.key.p, (unsigned*)w.key2.p, (int*)w.val_i.p,
+                                  (int*)w.node_list.p, nn, 0, eb, st);
+  size_t ts = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, ts, (int64_t*)w.width.p, (int64_t*)w.slice_off.p, nsl + 1, st);
+  if (ensure(w.tmp, std::max(tb, ts))) return fail("allocation");
+  tb = w.tmp.cap;
+  if (cub::DeviceRadixSort::SortPairs(w.tmp.p, tb, (unsigned*)w.key.p, (unsigned*)w.key2.p, (int*)w.val_i.p,
+                                      (int*)w.node_list.p, nn, 0, eb, st))
+    return fail("sort");
+  k_ng_widths<<<nblk(nsl + 1), 256, 0, st>>>(nsl, G, (const int*)w.blk_slice.p, (const int*)w.blk_pos.p,
+                                             (const int*)w.node_list.p, (const int*)w.cnt.p, (int64_t*)w.width.p);
+  ts = w.tmp.cap;
+  if (cub::DeviceScan::ExclusiveSum(w.tmp.p, ts, (int64_t*)w.width.p, (int64_t*)w.slice_off.p, nsl + 1, st))
+    return fail("scan");
+  launches += 6 + (n_c > 0);
+  if (cudaMemcpyAsync(w.h_small, (int64_t*)w.slice_off.p + nsl, 8, cudaMemcpyDeviceToHost, st) ||
+      cudaMemcpyAsync((int*)(w.h_small + 1), w.flags.p, 4, cudaMemcpyDeviceToHost, st) ||
+      cudaStreamSynchronize(st))
+    return fail("host read");
+  if (((int*)(w.h_small + 1))[0]) return VFPI_UNSUPPORTED;  // a contact column is not node aligned
+  const int64_t K = w.h_small[0];
+  if (ensure(w.desc, 4 * 32 * (size_t)std::max<int64_t>(K, 1)) ||
+      ensure(w.val, 8 * 9 * 32 * (size_t)std::max<int64_t>(K, 1)))
+    return fail("allocation");
+  if (cudaMemsetAsync(w.val.p, 0, 8 * 9 * 32 * (size_t)K, st) || cudaMemsetAsync(w.desc.p, 0, 4 * 32 * (size_t)K, st))
+    return fail("memset");  // padding lanes past a CTA's last node are never filled
+  k_ng_fill<<<nblk(nn, 128), 128, 0, st>>>(nn, G, (const int*)w.blk_slice.p, (const int*)w.blk_pos.p,
+                                           (const int*)w.node_list.p, (const int64_t*)w.slice_off.p, row_ptr, rowcnt,
+                                           perm, colof, d.data, (unsigned*)w.desc.p, (double*)w.val.p);
+  if (cudaMemsetAsync(w.node_slot.p, 0xff, 4 * (size_t)nn, st)) return fail("memset");
+  if (n_c > 0) k_ng_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, d.col_i, d.col_j, (int*)w.node_slot.p);
+  if (cudaMemsetAsync(w.jt.p, 0, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1), st)) return fail("memset");
+  launches += 1 + (n_c > 0);
+  if (cudaGetLastError() != cudaSuccess) return fail("launch");
+  w.k_total = K;
+  out.nn = nn;
+  out.nsl = nsl;
+  out.blk_slice = (const int*)w.blk_slice.p;
+  out.blk_pos = (const int*)w.blk_pos.p;
+  out.node_list = (const int*)w.node_list.p;
+  out.node_slot = (int*)w.node_slot.p;
+  out.slice_off = (const int64_t*)w.slice_off.p;
+  out.desc = (const unsigned*)w.desc.p;
+  out.val = (const double*)w.val.p;
+  out.vs_g = (double*)w.vs.p;
+  out.jt_g = (double*)w.jt.p;
+  return VFPI_OK;
 }
 
 int node_kernel_smem(int max_ct) { return 2 * kSlotsPerContact * 8 * max_ct + kNbRingBytes + 128; }
 
-int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct) {
-  NbFn f = nb_pick(op, cheb, true);
+int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, bool grid) {
+  NbFn f = nb_pick(op, cheb, true, grid);
   if (ensure_max_dynamic_smem((const void*)f) != cudaSuccess) return 0;
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kNbThreads, node_kernel_smem(max_ct)) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kNbThreads, node_kernel_smem(grid ? 0 : max_ct)) !=
+      cudaSuccess)
     return 0;
   return nb;
 }
 
 int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bool cheb, int max_ct, cudaStream_t st,
-                         std::string& err) {
-  NbFn f = nb_pick(op, cheb, p.n_c > 0);
+                         std::string& err, bool grid) {
+  NbFn f = nb_pick(op, cheb, p.n_c > 0, grid);
   cudaError_t e = ensure_max_dynamic_smem((const void*)f);
   if (e != cudaSuccess) { err = cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
-  f<<<p.G, kNbThreads, node_kernel_smem(max_ct), st>>>(p, L);
-  e = cudaGetLastError();
+  if (grid) {
+    IterParams lp = p;
+    NodeLayoutDev ll = L;
+    void* args[] = {&lp, &ll};
+    e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kNbThreads), args, node_kernel_smem(0), st);
+  } else {
+    f<<<p.G, kNbThreads, node_kernel_smem(max_ct), st>>>(p, L);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) {
-    err = std::string("node-block scene launch: ") + cudaGetErrorString(e);
+    err = std::string("node-block launch: ") + cudaGetErrorString(e);
     return VFPI_CUDA_ERROR;
   }
   return VFPI_OK;
