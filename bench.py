@@ -492,6 +492,11 @@ def run_ours(args):
             sub["configs[1]"] = config1_subrecord(h, dev, peak)
         except Exception as e:  # a sub-record never sinks the headline line
             sub["configs[1]"] = {"error": repr(e)}
+        if reference_available():
+            try:
+                sub["configs[1] drop-in e2e"] = config1_dropin_subrecord()
+            except Exception as e:
+                sub["configs[1] drop-in e2e"] = {"error": repr(e)}
     mean_its = sm[6].item() / (SCENES * SIM_STEPS * args.steps)
     line = {
         "metric": METRIC, "value": ci_all / t_max, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -582,6 +587,44 @@ def config1_subrecord(h, dev, peak):
                          "note": "A is read from HBM once per solve; the per-iteration cost is L2 latency + one "
                                  "grid barrier, so this is not an HBM fraction"},
             "l2": "flushed (256 MB write) before every step"}
+
+
+def config1_dropin_subrecord():
+    """configs[1] through the call the reference's harness makes,
+    ``condsim.solver.solve_vfpi(aug, cfg, warm)`` as ``dropin.install()`` binds it:
+    a reference-typed ``AugmentedDynamics`` (condsim from baseline/_ref) with
+    pageable numpy arrays in, numpy v / lam / report out, wall clock per call."""
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    from condsim.contacts import AugmentedDynamics, Contact, NodalContactSet
+    from condsim.solver import SolverConfig as RefConfig
+    from condsim.sparse import SparseSymmetric
+
+    from paper_2201_09212_b200 import solver as S
+    from paper_2201_09212_b200.scenes import rigid_contact_system
+
+    ps = rigid_contact_system(4096, 16384, 2201, 1e5)
+    fr = ps.frames.reshape(-1, 3, 3)
+    n_o = ps.n - 6 * ps.n_c
+    cons = [Contact(kind="D", slot_i=("virt", 2 * m), frame=fr[m], mu=float(ps.mu[m]), depth=0.0,
+                    phi_n=float(ps.phi[m]), slot_j=("virt", 2 * m + 1)) for m in range(ps.n_c)]
+    aug = AugmentedDynamics(a=SparseSymmetric(ps.n, ps.indptr.copy(), ps.indices.copy(), ps.data.copy()),
+                            b=ps.b.copy(), n=ps.n, n_orig=n_o,
+                            contacts=NodalContactSet(cons, 2 * ps.n_c, None, 1e5),
+                            col_i=ps.col_i.astype(np.int64), col_j=ps.col_j.astype(np.int64), frames=fr.copy())
+    cfg = RefConfig(operator="strict", residual_tol=1e-8, max_iters=1000, chebyshev=False)
+    warm = np.zeros(ps.n)
+    for _ in range(2):
+        S.solve_vfpi(aug, cfg, warm)
+    t, ci = [], 0
+    for _ in range(5):
+        t0 = time.perf_counter()
+        v, lam, rep = S.solve_vfpi(aug, cfg, warm)
+        t.append(time.perf_counter() - t0)
+        ci += ps.n_c * rep.iterations
+    return {"workload": "configs[1] through solve_vfpi(aug, cfg, warm) with a condsim AugmentedDynamics "
+                        "(pageable numpy in/out, the drop-in's call)",
+            "value": ci / sum(t), "unit": UNIT, "ms_per_call": 1e3 * sum(t) / len(t), "calls": len(t),
+            "iterations": int(rep.iterations)}
 
 
 def main():

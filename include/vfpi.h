@@ -422,6 +422,7 @@ typedef struct vfpi_nodalize_input {
   const int32_t* body_v;       /* per body: velocity offset (Body.v_offset) */
   double mu, mu2, beta_err, dt, e_rest, rest_threshold;
   int64_t n_bodies;            /* entries of body_q / body_v (rigid side ids are checked against it) */
+  int64_t n_q;                 /* entries of q: a rigid side needs body_q + 3 <= n_q and body_v + 6 <= n_o */
 } vfpi_nodalize_input;
 
 typedef struct vfpi_nodal_contacts {

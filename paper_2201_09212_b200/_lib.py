@@ -83,7 +83,7 @@ class VfpiNodalizeInput(C.Structure):
         ("second_ref", C.c_void_p), ("point", C.c_void_p), ("normal", C.c_void_p), ("depth", C.c_void_p),
         ("q", C.c_void_p), ("v", C.c_void_p), ("body_q", C.c_void_p), ("body_v", C.c_void_p),
         ("mu", C.c_double), ("mu2", C.c_double), ("beta_err", C.c_double), ("dt", C.c_double),
-        ("e_rest", C.c_double), ("rest_threshold", C.c_double), ("n_bodies", C.c_int64),
+        ("e_rest", C.c_double), ("rest_threshold", C.c_double), ("n_bodies", C.c_int64), ("n_q", C.c_int64),
     ]
 
 

@@ -1707,6 +1707,7 @@ int vfpi_nodalize_device(vfpi_handle* h, const vfpi_nodalize_input* in, vfpi_nod
   ni.n_c = in->n_c;
   ni.n_o = (int)in->n_o;
   ni.n_bodies = (int)in->n_bodies;
+  ni.n_q = in->n_q;
   ni.first_kind = in->first_kind;
   ni.first_ref = in->first_ref;
   ni.second_kind = in->second_kind;

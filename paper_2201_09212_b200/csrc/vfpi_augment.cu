@@ -44,11 +44,21 @@ inline unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, (n +
 
 // nonzero entries per J_v row -> products per row (count^2)
 // (also validates J_v: columns inside [0, n_o), strictly increasing per row)
-__global__ void k_aug_prod_count(int rows, int n_o, const int* __restrict__ jp, const int* __restrict__ jc,
-                                 const double* __restrict__ jx, int64_t* __restrict__ cnt, int* __restrict__ bad) {
+__global__ void k_aug_prod_count(int rows, int n_o, int64_t jnnz, const int* __restrict__ jp,
+                                 const int* __restrict__ jc, const double* __restrict__ jx, int64_t* __restrict__ cnt,
+                                 int* __restrict__ bad) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r > rows) return;
-  if (r == rows) { cnt[r] = 0; return; }
+  if (r == rows) {
+    cnt[r] = 0;
+    if (jp[0] != 0 || jp[rows] != jnnz) atomicExch(bad, 1);
+    return;
+  }
+  if (jp[r] < 0 || jp[r] > jp[r + 1] || jp[r + 1] > jnnz) {  // not a CSR row pointer: do not walk it
+    atomicExch(bad, 1);
+    cnt[r] = 0;
+    return;
+  }
   int64_t c = 0;
   int prev = -1;
   for (int e = jp[r]; e < jp[r + 1]; ++e) {
@@ -61,6 +71,25 @@ __global__ void k_aug_prod_count(int rows, int n_o, const int* __restrict__ jp, 
 }
 
 __global__ void k_aug_zero(int* p) { *p = 0; }
+
+// A_o must be CSC with strictly increasing row indices in [0, n_o) per column
+__global__ void k_aug_check_a(int n_o, int64_t nnz, const int* __restrict__ ap, const int* __restrict__ ai,
+                              int* __restrict__ bad) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > n_o) return;
+  if (c == n_o) {
+    if (ap[0] != 0 || ap[n_o] != nnz) atomicExch(bad, 1);
+    return;
+  }
+  const int e0 = ap[c], e1 = ap[c + 1];
+  if (e0 < 0 || e0 > e1 || e1 > nnz) { atomicExch(bad, 1); return; }
+  int prev = -1;
+  for (int e = e0; e < e1; ++e) {
+    const int r = ai[e];
+    if (r <= prev || r >= n_o) { atomicExch(bad, 1); return; }
+    prev = r;
+  }
+}
 
 // products of row r in (i-entry, j-entry) order; key = (j << 32) | i
 __global__ void k_aug_prod_fill(int rows, const int* __restrict__ jp, const int* __restrict__ jc,
@@ -264,8 +293,9 @@ int augment_device(AugmentWork& w, const AugmentIn& in, cudaStream_t st, Augment
   AK(ensure(w.poff, sizeof(int64_t) * (size_t)(rows + 1)));
   AK(ensure(w.cs, sizeof(int64_t) * (size_t)(n_o + 1)));  // its first word doubles as the validation flag
   k_aug_zero<<<1, 1, 0, st>>>(B<int>(w.cs));
-  k_aug_prod_count<<<grid_for(rows + 1), kT, 0, st>>>(rows, n_o, in.jv_indptr, in.jv_indices, in.jv_data,
+  k_aug_prod_count<<<grid_for(rows + 1), kT, 0, st>>>(rows, n_o, jnnz, in.jv_indptr, in.jv_indices, in.jv_data,
                                                       B<int64_t>(w.pcnt), B<int>(w.cs));
+  k_aug_check_a<<<grid_for(n_o + 1), kT, 0, st>>>(n_o, in.a_nnz, in.a_indptr, in.a_indices, B<int>(w.cs));
   size_t tb = 0;
   AK(cub::DeviceScan::ExclusiveSum(nullptr, tb, B<int64_t>(w.pcnt), B<int64_t>(w.poff), rows + 1, st));
   AK(ensure(w.tmp, tb));
@@ -275,7 +305,7 @@ int augment_device(AugmentWork& w, const AugmentIn& in, cudaStream_t st, Augment
   AK(cudaStreamSynchronize(st));
   const int64_t m = w.h_small[0];
   if (reinterpret_cast<int*>(&w.h_small[1])[0]) {
-    err = "augment: J_v is not canonical CSR with columns in [0, n_o)";
+    err = "augment: J_v is not canonical CSR with columns in [0, n_o), or A_o not canonical CSC";
     return VFPI_BAD_ARGUMENT;
   }
   launches += 2;

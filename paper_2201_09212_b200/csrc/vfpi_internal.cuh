@@ -302,6 +302,7 @@ struct NodalizeIn {
   int64_t n_c = 0;
   int n_o = 0;  // velocity dimension
   int n_bodies = 0;
+  int64_t n_q = 0;                   // entries of q
   const int* first_kind = nullptr;   // 0 node (ref = velocity offset), 1 rigid (ref = body)
   const int* first_ref = nullptr;
   const int* second_kind = nullptr;  // -1 static, 0 node, 1 rigid

@@ -46,15 +46,18 @@ __global__ void k_nod_fill_int(int64_t n, int* __restrict__ p, int v) {
 // first use of every node offset (processing order 2m + side)
 // (also validates the sides: kinds, node offsets inside [0, n_o - 3], body ids
 // inside [0, n_bodies); a static first side is not a contact)
-__global__ void k_nod_first_use(int64_t n_c, int n_o, int n_bodies, const int* __restrict__ fk,
+__global__ void k_nod_first_use(int64_t n_c, int n_o, int n_bodies, int64_t n_q, const int* __restrict__ fk,
                                 const int* __restrict__ fr, const int* __restrict__ sk, const int* __restrict__ sr,
+                                const int* __restrict__ body_q, const int* __restrict__ body_v,
                                 int* __restrict__ first, int* __restrict__ bad) {
   const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (m >= n_c) return;
   for (int s = 0; s < 2; ++s) {
     const int kind = s ? sk[m] : fk[m], ref = s ? sr[m] : fr[m];
-    const bool ok = (kind == 0 && ref >= 0 && ref <= n_o - 3) || (kind == 1 && ref >= 0 && ref < n_bodies) ||
-                    (kind == -1 && s == 1);
+    // a rigid side reads q[body_q .. +2] (position) and writes J_v columns body_v .. +5
+    const bool rigid_ok = kind == 1 && ref >= 0 && ref < n_bodies && body_q[ref] >= 0 &&
+                          (int64_t)body_q[ref] + 3 <= n_q && body_v[ref] >= 0 && body_v[ref] + 6 <= n_o;
+    const bool ok = (kind == 0 && ref >= 0 && ref <= n_o - 3) || rigid_ok || (kind == -1 && s == 1);
     if (!ok) {
       atomicExch(bad, 1);
       continue;
@@ -210,8 +213,9 @@ int nodalize_device(NodalizeWork& w, const NodalizeIn& in, cudaStream_t st, Noda
   NK(ensure(w.flag, sizeof(int)));
   k_nod_fill_int<<<gridn(in.n_o), kT, 0, st>>>(in.n_o, Bn<int>(w.first), INT_MAX);
   k_nod_set<<<1, 1, 0, st>>>(Bn<int>(w.flag), 0);
-  k_nod_first_use<<<gridn(n_c), kT, 0, st>>>(n_c, in.n_o, in.n_bodies, in.first_kind, in.first_ref, in.second_kind,
-                                              in.second_ref, Bn<int>(w.first), Bn<int>(w.flag));
+  k_nod_first_use<<<gridn(n_c), kT, 0, st>>>(n_c, in.n_o, in.n_bodies, in.n_q, in.first_kind, in.first_ref,
+                                              in.second_kind, in.second_ref, in.body_q, in.body_v, Bn<int>(w.first),
+                                              Bn<int>(w.flag));
   k_nod_virtual_flags<<<gridn(S + 1), kT, 0, st>>>(n_c, in.n_o, in.first_kind, in.first_ref, in.second_kind, in.second_ref,
                                                    Bn<int>(w.first), Bn<int>(w.vflag), Bn<int>(w.jcnt));
   size_t tb = 0;
@@ -225,7 +229,7 @@ int nodalize_device(NodalizeWork& w, const NodalizeIn& in, cudaStream_t st, Noda
   NK(cudaMemcpyAsync(hs + 2, Bn<int>(w.flag), sizeof(int), cudaMemcpyDeviceToHost, st));
   NK(cudaStreamSynchronize(st));
   if (hs[2]) {
-    err = "nodalize: bad contact side (kind, node offset or body index out of range)";
+    err = "nodalize: bad contact side (kind, node offset, body index or body q/v offsets out of range)";
     return VFPI_BAD_ARGUMENT;
   }
   const int nv = hs[0], nj = hs[1];

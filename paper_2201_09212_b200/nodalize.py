@@ -43,7 +43,8 @@ def nodalize_arrays(first_kind, first_ref, second_kind, second_ref, point, norma
          up(depth, np.float64), up(q, np.float64), up(v, np.float64), up(body_q, np.int32), up(body_v, np.int32)]
     inp = _lib.VfpiNodalizeInput(n_c, n_o, *[x.data_ptr() for x in t], float(mu),
                                  float("nan") if mu2 is None else float(mu2), float(beta_err), float(dt),
-                                 float(e_rest), float(rest_threshold), int(np.asarray(body_q).shape[0]))
+                                 float(e_rest), float(rest_threshold), int(np.asarray(body_q).shape[0]),
+                                 int(np.asarray(q).shape[0]))
     out = _lib.VfpiNodalContacts()
     _raise_for(h.L.vfpi_nodalize_device(h.h, C.byref(inp), C.byref(out), None), h)
     d2h = lambda p, k, dt_: _lib.device_to_numpy(p, k, dt_, h.device)  # noqa: E731

@@ -86,3 +86,57 @@ def test_node_kernel_matches_oracle_pipeline():
         assert [r["iterations"] for r in rec] == [row[k] for row in its], k
         assert sum(r["n_c"] for r in rec) > 0
         assert np.array_equal(x[k], c.x) and np.array_equal(v[k], c.v), k
+
+
+def _grid_case(case):
+    from oracle import pile_host as H
+    from paper_2201_09212_b200.pile import CubePile
+    from paper_2201_09212_b200.scenes import HeightfieldBlock, rigid_contact_system
+
+    if case == "rigid":
+        return rigid_contact_system(96, 300, seed=4, k_v=1e3)
+    if case == "heightfield":
+        return F.heightfield_system(HeightfieldBlock(nx=10))
+    pile = CubePile(nx_cubes=2, ny_cubes=1, layers=2, nodes=4, gap=0.0, jitter=0.00005, seed=5, dt=5e-4)
+    return H.system(pile)
+
+
+@pytest.mark.parametrize("case", ["rigid", "heightfield", "pile"])
+@pytest.mark.parametrize("cheb", [False, True])
+def test_grid_node_kernel_equals_row_streaming_kernel(case, cheb):
+    """Single systems on the global-memory path: the node-block grid kernel
+    against the row-SELL streaming kernel (and the oracle, plain V-FPI)."""
+    from oracle import vfpi_oracle as O
+    from paper_2201_09212_b200 import _lib
+    from paper_2201_09212_b200.solver import SolverConfig, solve_packed
+
+    ps = _grid_case(case)
+    cfg = SolverConfig(residual_tol=1e-9, max_iters=150, chebyshev=cheb)
+    warm = np.zeros(ps.n)
+    h = _lib.handle()
+    h.set_kernel("streaming")
+    try:
+        h.set_node_kernel(True)
+        v1, l1, r1 = solve_packed(ps, cfg, warm)
+        assert h.last_layout()["node_kernel"]
+        h.set_node_kernel(False)
+        v2, l2, r2 = solve_packed(ps, cfg, warm)
+        assert not h.last_layout()["node_kernel"]
+    finally:
+        h.set_kernel("auto")
+        h.set_node_kernel(True)
+    assert r1.iterations == r2.iterations and r1.converged == r2.converged
+    if cheb:
+        # rho = theta_l / theta_{l-1}: last-bit differences of theta (reduction
+        # order) reach v and lam through nu; stiff virtual-node systems amplify
+        # them (SURVEY §0.7: the reference moves 1e-1 under a 1e-15 input change)
+        tol = 1e-9 if case == "heightfield" else 1e-6
+        assert np.linalg.norm(v1 - v2) <= tol * np.linalg.norm(v2)
+        assert np.linalg.norm(l1 - l2) <= tol * max(np.linalg.norm(l2), 1e-300)
+    else:
+        assert np.array_equal(v1, v2) and np.array_equal(l1, l2)
+        s = O.System(ps.n, ps.indptr, ps.indices, ps.data, ps.b, ps.col_i.astype(np.int64),
+                     ps.col_j.astype(np.int64), ps.frames.reshape(-1, 3, 3), ps.mu, ps.mu2, ps.phi)
+        vo, lo, ro = O.solve(s, O.Config(residual_tol=1e-9, max_iters=150), warm)
+        assert ro.iterations == r1.iterations
+        assert np.array_equal(v1, vo) and np.array_equal(l1, lo)
