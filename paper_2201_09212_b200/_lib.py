@@ -237,6 +237,11 @@ class Handle:
         return {"resident": bool(r.value), "ctas": int(g.value),
                 "node_kernel": bool(self.L.vfpi_set_tuning(self.h, 7, 0))}
 
+    def set_node_cluster(self, on: bool):
+        """FEM batches created afterwards: one thread-block cluster per scene when the
+        batch is too small to fill the GPU (default on)."""
+        self.L.vfpi_set_tuning(self.h, 8, 1 if on else 0)
+
     def set_node_kernel(self, on: bool):
         """Use the node-block kernels (FEM batches, single systems) when eligible (default on)."""
         self.L.vfpi_set_tuning(self.h, 6, 1 if on else 0)

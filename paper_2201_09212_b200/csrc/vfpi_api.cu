@@ -62,6 +62,7 @@ struct vfpi_handle {
   int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
   int tune_wc = 0;      // >0: force the contact-warp count of the resident kernel
   int node_kernel = 1;  // FEM batches: node-block SELL kernel when a node layout is set (tuning key 6)
+  int node_cluster = 1; // small FEM batches: one thread-block cluster per scene (tuning key 8; set before the layout)
   int last_node_kernel = 0;
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
@@ -388,6 +389,7 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (key == 5 && value >= 0) { h->layout_opt.contact_cost = value; return VFPI_OK; }
   if (key == 6) { h->node_kernel = value != 0; return VFPI_OK; }
   if (key == 7) return h->last_node_kernel;  // query: did the last scene solve use the node-block kernel
+  if (key == 8) { h->node_cluster = value != 0; return VFPI_OK; }
   return VFPI_BAD_ARGUMENT;
 }
 
@@ -505,7 +507,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   int G_nodes = 0;
   vfpi::NodeLayoutDev nl;
   if (!resident && h->node_kernel && !bb && n % 3 == 0) {
-    const int bps = vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, 0, true);
+    const int bps = vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, 0, 1);
     if (bps > 0) {
       G_nodes = bps * ws.num_sms;
       rc = vfpi::node_grid_build(h->ngw, *d, G_nodes, P<int64_t>(ws.row_ptr), P<int>(ws.rowcnt), P<int>(ws.perm),
@@ -605,7 +607,7 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.cfactor = cfg->consistency_factor;
   (void)tr;
   if (use_nodes) {
-    rc = vfpi::launch_iterate_nodes(p, nl, cfg->op, cheb, 0, st, h->err, true);
+    rc = vfpi::launch_iterate_nodes(p, nl, cfg->op, cheb, 0, st, h->err, 1);
   } else {
     rc = resident ? vfpi::launch_iterate_resident(p, cfg->op, cheb, bb, smem_res_full, st, h->err)
                   : vfpi::launch_iterate(p, cfg->op, cheb, bb, smem, st, h->err);
@@ -817,8 +819,12 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
   p.under_relax = cfg->under_relax;
   p.omega = cfg->omega;
   p.cfactor = cfg->consistency_factor;
-  const bool use_nodes = nodes && !bb && h->node_kernel &&
-                         vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, std::max(max_ct, 1)) > 0;
+  // one cluster per scene needs the per-scene fixed-alpha default computed
+  // cluster-wide, which only the one-CTA kernel does: that case keeps one CTA
+  const bool fixed_default = cfg->step_strategy == VFPI_STEP_FIXED_ALPHA && std::isnan(cfg->fixed_alpha);
+  const int nmode = (nodes && nodes->cluster > 1 && !fixed_default) ? 2 : 0;
+  const bool use_nodes = nodes && !bb && h->node_kernel && (nmode == 2 || nodes->cluster == 1) &&
+                         vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, std::max(max_ct, 1), nmode) > 0;
   if (use_nodes) {
     if (vfpi::node_slots_refresh(*nodes, S, n_c, d.col_i, d.col_j, d_scene_cts, st)) {
       h->err = "node slot refresh failed";
@@ -826,7 +832,7 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
     }
     ++h->launches;
     CK(cudaEventRecord(ws.ev[1], st));  // the loop timing covers the iteration kernel only
-    rc = vfpi::launch_iterate_nodes(p, *nodes, cfg->op, cheb, std::max(max_ct, 1), st, h->err);
+    rc = vfpi::launch_iterate_nodes(p, *nodes, cfg->op, cheb, std::max(max_ct, 1), st, h->err, nmode);
   } else {
     rc = vfpi::launch_iterate_scenes(p, cfg->op, cheb, bb, smem, st, h->err);
   }
@@ -1428,7 +1434,10 @@ int vfpi_fem_set_node_layout(vfpi_fem_batch* fb, int32_t nodes_per_scene, const 
   cudaStream_t st = h->ws.stream;
   CK(vfpi::ensure(h->ws.flags, 16));
   CK(cudaMemsetAsync(h->ws.flags.p, 0, 16, st));
-  if (vfpi::node_layout_build(L, fb->S, fb->A.indptr, fb->A.indices, fb->A.data, fb->nbd, (int*)h->ws.flags.p, st)) {
+  L.t_off_host.assign(slice_off, slice_off + n_slices + 1);
+  const int cl = h->node_cluster ? vfpi::node_cluster_size(fb->S, n_slices, h->ws.num_sms) : 1;
+  if (vfpi::node_layout_build(L, fb->S, fb->A.indptr, fb->A.indices, fb->A.data, fb->nbd, (int*)h->ws.flags.p, st,
+                              cl, L.t_off_host)) {
     h->err = "node layout build failed";
     return VFPI_CUDA_ERROR;
   }
@@ -1483,7 +1492,8 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
                             &fb->frame, &fb->tmp, &fb->zero_cts, &fb->ks_off, &fb->ks_val, &fb->ks_col, &fb->cg_r,
                             &fb->cg_p, &fb->cg_q, &fb->cg_list, &fb->x0, &fb->v0, &fb->nbh.t_order,
                             &fb->nbh.t_off, &fb->nbh.t_bcol, &fb->nbh.desc, &fb->nbh.val, &fb->nbh.slice_off,
-                            &fb->nbh.node_list, &fb->nbh.node_slot})
+                            &fb->nbh.node_list, &fb->nbh.node_slot, &fb->nbh.blk_slice, &fb->nbh.blk_pos, &fb->nbh.vs,
+                            &fb->nbh.jt})
     if (b->p) cudaFree(b->p);
   if (fb->e0) cudaEventDestroy(fb->e0);
   if (fb->e1) cudaEventDestroy(fb->e1);

@@ -387,7 +387,8 @@ struct NodeLayoutDev {
   int nn = 0, nsl = 0;                 // nodes and node slices (per scene for batches, of the system for grids)
   const int* blk_slice = nullptr;      // [G+1] node slices of every CTA
   const int* blk_pos = nullptr;        // [G+1] node positions of every CTA
-  double* vs_g = nullptr;              // grid mode: v* of contact rows [6 n_c]
+  int cluster = 1;                     // scene batches: CTAs per scene (thread-block cluster) when > 1
+  double* vs_g = nullptr;              // grid / cluster mode: v* of contact rows [6 n_c]
   double* jt_g = nullptr;              // grid mode: J_c^T lam of contact rows [6 n_c]
   const int* node_list = nullptr;      // [S*nn] position -> global node
   int* node_slot = nullptr;            // [S*nn] global node -> contact slot base (6 per contact) or -1
@@ -398,7 +399,8 @@ struct NodeLayoutDev {
 struct NodeLayoutHost {
   int nn = 0, nsl = 0;
   int64_t k_scene = 0;                 // k-steps per scene
-  Workspace::Buf t_order, t_off, t_bcol, desc, val, slice_off, node_list, node_slot, blk_slice, blk_pos;
+  Workspace::Buf t_order, t_off, t_bcol, desc, val, slice_off, node_list, node_slot, blk_slice, blk_pos, vs, jt;
+  std::vector<int64_t> t_off_host;
 };
 struct NodeGridWork {  // single-system node-block layout (rebuilt per solve)
   Workspace::Buf blk_pos, blk_slice, key, key2, val_i, node_list, cnt, node_slot, width, slice_off, flags, vs, jt,
@@ -410,12 +412,15 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
                     const int* perm, const int* colof, cudaStream_t st, NodeLayoutDev& out, std::string& err,
                     int64_t& launches);
 int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
-                      NodeLayoutDev& out, int* d_flags, cudaStream_t st);
+                      NodeLayoutDev& out, int* d_flags, cudaStream_t st, int cluster,
+                      const std::vector<int64_t>& t_off_host);
+int node_cluster_size(int S, int nsl, int num_sms);  // CTAs per scene so a small batch fills the GPU
 int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
                        cudaStream_t st);
 int node_kernel_smem(int max_ct);
-int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, bool grid = false);
+// mode: 0 one CTA per scene, 1 one system over a cooperative grid, 2 one cluster per scene
+int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, int mode = 0);
 int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bool cheb, int max_ct, cudaStream_t st,
-                         std::string& err, bool grid = false);
+                         std::string& err, int mode = 0);
 
 }  // namespace vfpi

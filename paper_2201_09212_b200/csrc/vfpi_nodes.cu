@@ -250,29 +250,41 @@ __device__ __forceinline__ void nb_grid_totals(const double* __restrict__ part, 
   __syncthreads();
 }
 
-// GRID = false: a batch of independent scenes, CTA b = scene b (its own loop,
-//               contacts staged in shared memory, CTA barriers only);
-// GRID = true : one system over a cooperative grid, CTA b owns a range of node
-//               slices; v* / J_c^T lam of contact rows go through global
-//               arrays, so an iteration is sweep | grid barrier | contacts |
-//               grid barrier (reductions), and every CTA takes the same
-//               decision from the same fixed-order totals.
-template <int OP, bool CHEB, bool HASC, bool GRID>
+// MODE kScene  : a batch of independent scenes, CTA b = scene b (its own loop,
+//                contacts staged in shared memory, CTA barriers only);
+// MODE kGrid   : one system over a cooperative grid, CTA b owns a range of node
+//                slices; v* / J_c^T lam of contact rows go through global
+//                arrays, so an iteration is sweep | grid barrier | contacts |
+//                grid barrier (reductions), and every CTA takes the same
+//                decision from the same fixed-order totals;
+// MODE kCluster: a batch of scenes, one thread-block CLUSTER per scene (when
+//                the batch is too small to fill the GPU, e.g. a rank's shard
+//                at 8 GPUs): the scene's node slices split over the cluster's
+//                CTAs, contacts through global slots, cluster barriers, and the
+//                partials summed over distributed shared memory in rank order.
+constexpr int kScene = 0, kGrid = 1, kCluster = 2;
+
+template <int OP, bool CHEB, bool HASC, int MODE>
 __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_nodes(IterParams p, NodeLayoutDev L) {
   extern __shared__ double smem[];
   __shared__ double sm_warp[3 * (kNbThreads / 32)];
   __shared__ double sm_tot[4];
   __shared__ __align__(8) uint64_t ring_bar[kNbThreads / 32][kNbStages];
 
+  constexpr bool GRID = MODE == kGrid, CLUSTER = MODE == kCluster, SHARED_C = MODE == kScene;
+  __shared__ double sm_cpart[2][4];  // cluster mode: this CTA's partials, by iteration parity
   const int b = blockIdx.x;
+  const int crank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
+  const int csize = CLUSTER ? (int)cg::this_cluster().num_blocks() : 1;
+  const int scene = CLUSTER ? b / csize : b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int np0 = L.blk_pos[b], np1 = L.blk_pos[b + 1];      // node positions of the CTA
   const int s0 = L.blk_slice[b], s1 = L.blk_slice[b + 1];    // node slices of the CTA
-  const int c0 = GRID ? 0 : p.blk_ct[b], c1 = GRID ? p.n_c : p.blk_ct[b + 1];
-  const int nct = GRID ? 0 : c1 - c0;
-  double* vs_s = GRID ? L.vs_g : smem;                       // v* of contact rows    [6*contacts]
-  double* jt_s = GRID ? L.jt_g : smem + kSlotsPerContact * nct;  // J_c^T lam_{l-1} rows
-  if (!GRID)
+  const int c0 = GRID ? 0 : p.blk_ct[scene], c1 = GRID ? p.n_c : p.blk_ct[scene + 1];
+  const int nct = SHARED_C ? c1 - c0 : 0;
+  double* vs_s = SHARED_C ? smem : L.vs_g;                       // v* of contact rows    [6*contacts]
+  double* jt_s = SHARED_C ? smem + kSlotsPerContact * nct : L.jt_g;  // J_c^T lam_{l-1} rows
+  if (SHARED_C)
     for (int t = threadIdx.x; t < kSlotsPerContact * nct; t += blockDim.x) jt_s[t] = 0.0;
 
   uint64_t pol;
@@ -312,7 +324,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   double rho = 0.0, nu = 1.0, theta_prev = 0.0;
   double alpha = 0.0;
   bool use_alpha = false;
-  if (!GRID && p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
+  if (SHARED_C && p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
     // scene batches: fixed-alpha default 1 / max|diag| of this scene (solver.py:368);
     // a single system gets it from the setup (w filled with alpha)
     double mx = -INFINITY, nanf = 0.0;
@@ -341,9 +353,9 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     use_alpha = true;
     __syncthreads();
   }
-  double* trace = GRID ? p.trace : p.trace + (size_t)b * p.trace_stride;
-  SolveStatus* status = GRID ? p.status : p.status + b;
-  const bool writer = GRID ? (b == 0) : true;  // the CTA that writes trace / status
+  double* trace = GRID ? p.trace : p.trace + (size_t)scene * p.trace_stride;
+  SolveStatus* status = GRID ? p.status : p.status + scene;
+  const bool writer = GRID ? (b == 0) : crank == 0;  // the CTA that writes trace / status
   bool pending = false;
   int final_buf = 0, final_lam = 0, iters = 0, conv = 0, div = 0;
   double consistency = NAN;
@@ -392,7 +404,8 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
         node = __ldg(L.node_list + pos);
         NB_CHECK(node >= 0 && 3 * node + 2 < p.n, "node=%d np0=%d np1=%d pos=%d", node, np0, np1, pos);
         if (HASC) slot = L.node_slot[node];
-        NB_CHECK(slot < 0 || GRID || slot + 2 < kSlotsPerContact * nct, "slot=%d nct=%d node=%d", slot, nct, node);
+        NB_CHECK(slot < 0 || !SHARED_C || slot + 2 < kSlotsPerContact * nct, "slot=%d nct=%d node=%d", slot, nct,
+                 node);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           bv[q] = __ldg(p.b + 3 * node + q);
@@ -426,11 +439,13 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter -------
     if (HASC && !check_only) {
       if constexpr (GRID) cg::this_grid().sync();
+      else if constexpr (CLUSTER) cg::this_cluster().sync();
       else __syncthreads();
-      const int kstep = GRID ? (int)(gridDim.x * blockDim.x) : (int)blockDim.x;
-      for (int k = c0 + (GRID ? (int)(b * blockDim.x) : 0) + threadIdx.x; k < c1; k += kstep) {
+      const int kstep = GRID ? (int)(gridDim.x * blockDim.x) : csize * (int)blockDim.x;
+      const int kfirst = GRID ? (int)(b * blockDim.x) : crank * (int)blockDim.x;
+      for (int k = c0 + kfirst + threadIdx.x; k < c1; k += kstep) {
         const int m = GRID ? k : __ldg(p.cont_list + k);
-        const int loc = (k - c0) * kSlotsPerContact;
+        const int loc = (SHARED_C ? k - c0 : k) * kSlotsPerContact;
         const int ci = __ldg(p.col_i + m), cj = __ldg(p.col_j + m);
         NB_CHECK(ci >= 0 && ci + 2 < p.n && m >= 0 && m < p.n_c, "contact m=%d ci=%d k=%d", m, ci, k);
         double R[9];
@@ -490,6 +505,24 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       }
       cg::this_grid().sync();
       nb_grid_totals(part, p.G, sm_tot);
+    } else if constexpr (CLUSTER) {
+      // cluster-wide totals: every CTA sums the cluster's partials in rank order
+      if (threadIdx.x == 0)
+        for (int t = 0; t < 3; ++t) sm_cpart[l & 1][t] = sm_tot[t];
+      cg::this_cluster().sync();
+      if (threadIdx.x == 0) {
+        double x = 0.0, y = 0.0, z = 0.0;
+        for (int r = 0; r < csize; ++r) {
+          const double* q = cg::this_cluster().map_shared_rank(&sm_cpart[l & 1][0], r);
+          x = dadd(x, q[0]);
+          y = dadd(y, q[1]);
+          z = dadd(z, q[2]);
+        }
+        sm_tot[0] = x;
+        sm_tot[1] = y;
+        sm_tot[2] = z;
+      }
+      __syncthreads();
     }
     const double theta = dsqrt(sm_tot[0]);
     const double fres = dsqrt(sm_tot[1]);
@@ -531,12 +564,14 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     for (int q = 0; q < 3; ++q) p.out_v[3 * node + q] = vfin[3 * node + q];
   }
   const double* lfin = lb[final_lam];
-  const int kstep = GRID ? (int)(gridDim.x * blockDim.x) : (int)blockDim.x;
-  for (int k = c0 + (GRID ? (int)(b * blockDim.x) : 0) + threadIdx.x; k < c1; k += kstep) {
+  const int kstep = GRID ? (int)(gridDim.x * blockDim.x) : csize * (int)blockDim.x;
+  const int kfirst = GRID ? (int)(b * blockDim.x) : crank * (int)blockDim.x;
+  for (int k = c0 + kfirst + threadIdx.x; k < c1; k += kstep) {
     const int m = GRID ? k : __ldg(p.cont_list + k);
 #pragma unroll
     for (int t = 0; t < 3; ++t) p.out_lam[3 * (size_t)m + t] = lfin[3 * (size_t)m + t];
   }
+  if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA leaves while a peer may read its partials
   if (writer && threadIdx.x == 0) {
     status->iterations = iters;
     status->converged = conv;
@@ -733,21 +768,23 @@ __global__ void k_ng_node_slots(int n_c, const int* __restrict__ ci, const int* 
 
 using NbFn = void (*)(IterParams, NodeLayoutDev);
 
-template <int OP, bool GRID>
+template <int OP, int MODE>
 NbFn nb_pick2(bool cheb, bool hasc) {
-  if (cheb) return hasc ? k_iterate_nodes<OP, true, true, GRID> : k_iterate_nodes<OP, true, false, GRID>;
-  return hasc ? k_iterate_nodes<OP, false, true, GRID> : k_iterate_nodes<OP, false, false, GRID>;
+  if (cheb) return hasc ? k_iterate_nodes<OP, true, true, MODE> : k_iterate_nodes<OP, true, false, MODE>;
+  return hasc ? k_iterate_nodes<OP, false, true, MODE> : k_iterate_nodes<OP, false, false, MODE>;
 }
 
-NbFn nb_pick(int op, bool cheb, bool hasc, bool grid) {
-  if (grid) {
-    if (op == OP_PROXIMAL) return nb_pick2<OP_PROXIMAL, true>(cheb, hasc);
-    if (op == OP_ANISO) return nb_pick2<OP_ANISO, true>(cheb, hasc);
-    return nb_pick2<OP_STRICT, true>(cheb, hasc);
-  }
-  if (op == OP_PROXIMAL) return nb_pick2<OP_PROXIMAL, false>(cheb, hasc);
-  if (op == OP_ANISO) return nb_pick2<OP_ANISO, false>(cheb, hasc);
-  return nb_pick2<OP_STRICT, false>(cheb, hasc);
+template <int MODE>
+NbFn nb_pick_mode(int op, bool cheb, bool hasc) {
+  if (op == OP_PROXIMAL) return nb_pick2<OP_PROXIMAL, MODE>(cheb, hasc);
+  if (op == OP_ANISO) return nb_pick2<OP_ANISO, MODE>(cheb, hasc);
+  return nb_pick2<OP_STRICT, MODE>(cheb, hasc);
+}
+
+NbFn nb_pick(int op, bool cheb, bool hasc, int mode) {
+  if (mode == kGrid) return nb_pick_mode<kGrid>(op, cheb, hasc);
+  if (mode == kCluster) return nb_pick_mode<kCluster>(op, cheb, hasc);
+  return nb_pick_mode<kScene>(op, cheb, hasc);
 }
 
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
@@ -755,14 +792,18 @@ inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t
 }  // namespace
 
 int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
-                      NodeLayoutDev& out, int* d_flags, cudaStream_t st) {
+                      NodeLayoutDev& out, int* d_flags, cudaStream_t st, int cluster,
+                      const std::vector<int64_t>& t_off_host) {
   const int nn = h.nn, nsl = h.nsl;
   const int64_t ks = h.k_scene;
+  const int CL = std::max(1, cluster);
+  const size_t G = (size_t)S * CL;
   if (ensure(h.desc, 4 * 32 * (size_t)std::max<int64_t>(S * ks, 1)) ||
       ensure(h.val, 8 * 9 * 32 * (size_t)std::max<int64_t>(S * ks, 1)) ||
       ensure(h.slice_off, 8 * ((size_t)S * nsl + 1)) || ensure(h.node_list, 4 * (size_t)S * nn) ||
-      ensure(h.node_slot, 4 * (size_t)S * nn) || ensure(h.blk_slice, 4 * ((size_t)S + 1)) ||
-      ensure(h.blk_pos, 4 * ((size_t)S + 1)))
+      ensure(h.node_slot, 4 * (size_t)S * nn) || ensure(h.blk_slice, 4 * (G + 1)) || ensure(h.blk_pos, 4 * (G + 1)))
+    return 1;
+  if (CL > 1 && (ensure(h.vs, 8 * kSlotsPerContact * (size_t)S * nn) || ensure(h.jt, 8 * kSlotsPerContact * (size_t)S * nn)))
     return 1;
   // padding lanes (positions past the scene's last node) are never filled:
   // their descriptors must read as empty
@@ -773,6 +814,29 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   k_nb_slice_off<<<nblk(nt), 256, 0, st>>>(S, nsl, (const int64_t*)h.t_off.p, ks, nn, (int64_t*)h.slice_off.p,
                                            (int*)h.node_list.p, (const int*)h.t_order.p, (int*)h.blk_slice.p,
                                            (int*)h.blk_pos.p);
+  if (CL > 1) {
+    // the scene's slices split over the cluster's CTAs by equal k-step shares
+    std::vector<int> split((size_t)CL + 1, nsl);
+    split[0] = 0;
+    for (int r = 1; r < CL; ++r) {
+      const int64_t want = ks * r / CL;
+      int t = split[r - 1];
+      while (t < nsl && t_off_host[t] < want) ++t;
+      split[r] = std::max(t, split[r - 1] + 1 <= nsl ? split[r - 1] + 1 : nsl);
+    }
+    std::vector<int> bs(G + 1), bp(G + 1);
+    for (int sc = 0; sc < S; ++sc)
+      for (int r = 0; r < CL; ++r) {
+        bs[(size_t)sc * CL + r] = sc * nsl + split[r];
+        bp[(size_t)sc * CL + r] = sc * nn + std::min(nn, 32 * split[r]);
+      }
+    bs[G] = S * nsl;
+    bp[G] = S * nn;
+    if (cudaMemcpyAsync(h.blk_slice.p, bs.data(), 4 * (G + 1), cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(h.blk_pos.p, bp.data(), 4 * (G + 1), cudaMemcpyHostToDevice, st) ||
+        cudaStreamSynchronize(st))  // the host vectors die here
+      return 1;
+  }
   const int64_t nf = (int64_t)S * nn;
   k_nb_fill<<<nblk(nf, 128), 128, 0, st>>>(S, nn, nsl, (const int*)h.t_order.p, (const int64_t*)h.t_off.p,
                                            (const int*)h.t_bcol.p, d_a_ptr, d_a_idx, d_a_val, ks, (unsigned*)h.desc.p,
@@ -780,6 +844,7 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   if (cudaGetLastError() != cudaSuccess) return 1;
   out.nn = nn;
   out.nsl = nsl;
+  out.cluster = CL;
   out.blk_slice = (const int*)h.blk_slice.p;
   out.blk_pos = (const int*)h.blk_pos.p;
   out.node_list = (const int*)h.node_list.p;
@@ -787,14 +852,20 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   out.slice_off = (const int64_t*)h.slice_off.p;
   out.desc = (const unsigned*)h.desc.p;
   out.val = (const double*)h.val.p;
-  out.vs_g = out.jt_g = nullptr;
+  out.vs_g = CL > 1 ? (double*)h.vs.p : nullptr;
+  out.jt_g = CL > 1 ? (double*)h.jt.p : nullptr;
   return 0;
 }
 
 int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
                        cudaStream_t st) {
   if (cudaMemsetAsync(L.node_slot, 0xff, 4 * (size_t)S * L.nn, st) != cudaSuccess) return 1;
-  if (n_c > 0) k_nb_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, S, ci, cj, d_ct, L.node_slot);
+  if (L.cluster > 1) {  // global contact slots; J_c^T lam starts at 0
+    if (n_c > 0) k_ng_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, ci, cj, L.node_slot);
+    if (cudaMemsetAsync(L.jt_g, 0, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1), st) != cudaSuccess) return 1;
+  } else if (n_c > 0) {
+    k_nb_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, S, ci, cj, d_ct, L.node_slot);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -884,26 +955,40 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
 
 int node_kernel_smem(int max_ct) { return 2 * kSlotsPerContact * 8 * max_ct + kNbRingBytes + 128; }
 
-int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, bool grid) {
-  NbFn f = nb_pick(op, cheb, true, grid);
+int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, int mode) {
+  NbFn f = nb_pick(op, cheb, true, mode);
   if (ensure_max_dynamic_smem((const void*)f) != cudaSuccess) return 0;
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kNbThreads, node_kernel_smem(grid ? 0 : max_ct)) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kNbThreads, node_kernel_smem(mode == kScene ? max_ct : 0)) !=
       cudaSuccess)
     return 0;
   return nb;
 }
 
 int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bool cheb, int max_ct, cudaStream_t st,
-                         std::string& err, bool grid) {
-  NbFn f = nb_pick(op, cheb, p.n_c > 0, grid);
+                         std::string& err, int mode) {
+  NbFn f = nb_pick(op, cheb, p.n_c > 0, mode);
   cudaError_t e = ensure_max_dynamic_smem((const void*)f);
   if (e != cudaSuccess) { err = cudaGetErrorString(e); return VFPI_CUDA_ERROR; }
-  if (grid) {
+  if (mode == kGrid) {
     IterParams lp = p;
     NodeLayoutDev ll = L;
     void* args[] = {&lp, &ll};
     e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kNbThreads), args, node_kernel_smem(0), st);
+  } else if (mode == kCluster) {
+    cudaLaunchConfig_t c{};
+    c.gridDim = dim3((unsigned)(p.G * L.cluster));
+    c.blockDim = dim3(kNbThreads);
+    c.dynamicSmemBytes = (size_t)node_kernel_smem(0);
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)L.cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    e = cudaLaunchKernelEx(&c, f, p, L);
   } else {
     f<<<p.G, kNbThreads, node_kernel_smem(max_ct), st>>>(p, L);
     e = cudaGetLastError();
@@ -913,6 +998,12 @@ int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bo
     return VFPI_CUDA_ERROR;
   }
   return VFPI_OK;
+}
+
+int node_cluster_size(int S, int nsl, int num_sms) {
+  int cl = 1;
+  while (cl < 8 && (int64_t)S * cl * 2 <= 2LL * num_sms && cl * 2 <= nsl) cl *= 2;
+  return cl;
 }
 
 }  // namespace vfpi

@@ -140,3 +140,39 @@ def test_grid_node_kernel_equals_row_streaming_kernel(case, cheb):
         vo, lo, ro = O.solve(s, O.Config(residual_tol=1e-9, max_iters=150), warm)
         assert ro.iterations == r1.iterations
         assert np.array_equal(v1, vo) and np.array_equal(l1, lo)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(operator="proximal"), dict(chebyshev=True)])
+def test_cluster_per_scene_equals_one_cta_per_scene(kw):
+    """A small batch (16 scenes) runs one thread-block cluster per scene (the
+    scene's node slices split over the cluster's CTAs, partials summed over
+    distributed shared memory); it must equal the one-CTA-per-scene kernel."""
+    from paper_2201_09212_b200 import _lib
+    from paper_2201_09212_b200.fembatch import FemBatch
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    h = _lib.handle()
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=300, **kw)
+    try:
+        h.set_node_cluster(True)
+        a = FemBatch(_cubes(6, 16, 5))
+        h.set_node_cluster(False)
+        b = FemBatch(_cubes(6, 16, 5))
+    finally:
+        h.set_node_cluster(True)
+    contacts = 0
+    for step in range(30):
+        sa, sb = a.step(cfg, per_scene=True), b.step(cfg, per_scene=True)
+        assert sa["node_kernel"] and sb["node_kernel"]
+        assert sa["contacts"] == sb["contacts"], step
+        contacts += sa["contacts"]
+        assert np.array_equal(sa["iterations_per_scene"], sb["iterations_per_scene"]), step
+    assert contacts > 0
+    xa, va = a.state()
+    xb, vb = b.state()
+    if kw.get("chebyshev"):
+        assert np.linalg.norm(va - vb) <= 1e-9 * np.linalg.norm(vb)
+    else:
+        assert np.array_equal(xa, xb) and np.array_equal(va, vb)
+    a.close()
+    b.close()
