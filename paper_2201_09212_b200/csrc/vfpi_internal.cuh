@@ -388,6 +388,7 @@ struct NodeLayoutDev {
   const int* blk_slice = nullptr;      // [G+1] node slices of every CTA
   const int* blk_pos = nullptr;        // [G+1] node positions of every CTA
   int cluster = 1;                     // scene batches: CTAs per scene (thread-block cluster) when > 1
+  int has_d = 1;                       // any two-node contact (else no contact phase / barrier)
   double* vs_g = nullptr;              // grid / cluster mode: v* of contact rows [6 n_c]
   double* jt_g = nullptr;              // grid mode: J_c^T lam of contact rows [6 n_c]
   const int* node_list = nullptr;      // [S*nn] position -> global node

@@ -417,27 +417,53 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       if (W > 0) nb_rows(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n);
       else y[0] = y[1] = y[2] = 0.0;
       if (live) {
+        double vstar[3], wrq[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           const double r = dsub(y[q], bv[q]);
           const double f = (slot >= 0) ? dsub(r, jt_s[slot + q]) : dsub(r, 0.0);
           fr = dadd(fr, dmul(f, f));
-          if (!check_only) {
-            const double wr = use_alpha ? alpha : wv[q];
-            const double vstar = dsub(vc[q], dmul(wr, r));
-            if (slot >= 0) {
-              vs_s[slot + q] = vstar;
-            } else {
-              const double vnew = HASC ? dadd(vstar, dmul(wr, 0.0)) : vstar;
-              finish_row(3 * node + q, vnew, vc[q]);
+          wrq[q] = use_alpha ? alpha : wv[q];
+          vstar[q] = dsub(vc[q], dmul(wrq[q], r));
+          if (!check_only && slot < 0) {
+            const double vnew = HASC ? dadd(vstar[q], dmul(wrq[q], 0.0)) : vstar[q];
+            finish_row(3 * node + q, vnew, vc[q]);
+          }
+        }
+        if (HASC && !check_only && slot >= 0) {
+          // an S-contact (single node) is solved right here by the node's lane:
+          // its one-shot projection needs only this node's v* (contacts.py:402-423,
+          // solver.py:405-411); two-node contacts are staged for the contact phase
+          const int k = slot / kSlotsPerContact + (SHARED_C ? c0 : 0);
+          const int m = GRID ? k : __ldg(p.cont_list + k);
+          if (slot % kSlotsPerContact == 0 && __ldg(p.col_j + m) < 0) {
+            double R[9];
+#pragma unroll
+            for (int t = 0; t < 9; ++t) R[t] = __ldg(p.frames + 9 * (size_t)m + t);
+            double eta[3], lam[3], world[3];
+            frame_apply(R, vstar, eta);
+            const double g = use_alpha ? dadd(alpha, p.omega) : __ldg(p.gamma + m);
+            trial_impulse(eta, __ldg(p.phi + m), g, lam);
+            project(OP, lam, __ldg(p.mu + m), __ldg(p.mu2 + m));
+#pragma unroll
+            for (int t = 0; t < 3; ++t) lam_out[3 * (size_t)m + t] = lam[t];
+            frame_apply_t(R, lam, world);
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              const double oi = dadd(0.0, world[t]);
+              jt_s[slot + t] = oi;
+              finish_row(3 * node + t, dadd(vstar[t], dmul(wrq[t], oi)), vc[t]);
             }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) vs_s[slot + q] = vstar[q];
           }
         }
       }
     }
 
-    // ---- (2)(3)(2') contacts: gather, one-shot projection, scatter -------
-    if (HASC && !check_only) {
+    // ---- (2)(3)(2') two-node contacts: gather, one-shot projection, scatter
+    if (HASC && L.has_d && !check_only) {
       if constexpr (GRID) cg::this_grid().sync();
       else if constexpr (CLUSTER) cg::this_cluster().sync();
       else __syncthreads();
@@ -447,6 +473,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
         const int m = GRID ? k : __ldg(p.cont_list + k);
         const int loc = (SHARED_C ? k - c0 : k) * kSlotsPerContact;
         const int ci = __ldg(p.col_i + m), cj = __ldg(p.col_j + m);
+        if (cj < 0) continue;  // S-contacts were solved in the sweep
         NB_CHECK(ci >= 0 && ci + 2 < p.n && m >= 0 && m < p.n_c, "contact m=%d ci=%d k=%d", m, ci, k);
         double R[9];
 #pragma unroll
@@ -756,6 +783,7 @@ __global__ void k_ng_contact_check(int n_c, const int* __restrict__ ci, const in
                                    int* __restrict__ bad) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n_c && (ci[k] % 3 != 0 || (cj[k] >= 0 && cj[k] % 3 != 0))) atomicOr(bad, 1);
+  if (k < n_c && cj[k] >= 0) atomicOr(bad + 1, 1);  // a two-node contact: the contact phase runs
 }
 
 __global__ void k_ng_node_slots(int n_c, const int* __restrict__ ci, const int* __restrict__ cj,
@@ -845,6 +873,7 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   out.nn = nn;
   out.nsl = nsl;
   out.cluster = CL;
+  out.has_d = 0;  // FEM batches: node-plane contacts only (col_j = -1)
   out.blk_slice = (const int*)h.blk_slice.p;
   out.blk_pos = (const int*)h.blk_pos.p;
   out.node_list = (const int*)h.node_list.p;
@@ -920,7 +949,7 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
     return fail("scan");
   launches += 6 + (n_c > 0);
   if (cudaMemcpyAsync(w.h_small, (int64_t*)w.slice_off.p + nsl, 8, cudaMemcpyDeviceToHost, st) ||
-      cudaMemcpyAsync((int*)(w.h_small + 1), w.flags.p, 4, cudaMemcpyDeviceToHost, st) ||
+      cudaMemcpyAsync((int*)(w.h_small + 1), w.flags.p, 8, cudaMemcpyDeviceToHost, st) ||
       cudaStreamSynchronize(st))
     return fail("host read");
   if (((int*)(w.h_small + 1))[0]) return VFPI_UNSUPPORTED;  // a contact column is not node aligned
@@ -939,6 +968,7 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   launches += 1 + (n_c > 0);
   if (cudaGetLastError() != cudaSuccess) return fail("launch");
   w.k_total = K;
+  out.has_d = ((int*)(w.h_small + 1))[1] ? 1 : 0;
   out.nn = nn;
   out.nsl = nsl;
   out.blk_slice = (const int*)w.blk_slice.p;
