@@ -317,8 +317,6 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   }
   __syncthreads();
 
-  double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
-  double* lb[2] = {p.lam0, p.lam1};
   const double u = p.under_relax;
   const double omu = dsub(1.0, u);
   double rho = 0.0, nu = 1.0, theta_prev = 0.0;
@@ -362,10 +360,10 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
 
   for (int l = 1;; ++l) {
     const bool check_only = (l == p.max_iters + 1);
-    const double* vcur = vb[(l - 1) % 3];
-    const double* vprev = vb[(l + 1) % 3];
-    double* vnext = vb[l % 3];
-    double* __restrict__ lam_out = lb[l & 1];
+    const double* vcur = ring3(p.vbuf0, p.vbuf1, p.vbuf2, (l - 1) % 3);
+    const double* vprev = ring3(p.vbuf0, p.vbuf1, p.vbuf2, (l + 1) % 3);
+    double* vnext = ring3(p.vbuf0, p.vbuf1, p.vbuf2, l % 3);
+    double* __restrict__ lam_out = ring2(p.lam0, p.lam1, l & 1);
     double* part = p.partials + (size_t)(l & 1) * p.G * kPartialStride;
 
     if (CHEB && !check_only) {
@@ -584,13 +582,13 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     while (!nb_try_wait(bar, (n / kNbStages) & 1u)) {
     }
   }
-  const double* vfin = vb[final_buf];
+  const double* vfin = ring3(p.vbuf0, p.vbuf1, p.vbuf2, final_buf);
   for (int pos = np0 + threadIdx.x; pos < np1; pos += blockDim.x) {
     const int node = __ldg(L.node_list + pos);
 #pragma unroll
     for (int q = 0; q < 3; ++q) p.out_v[3 * node + q] = vfin[3 * node + q];
   }
-  const double* lfin = lb[final_lam];
+  const double* lfin = ring2(p.lam0, p.lam1, final_lam);
   const int kstep = GRID ? (int)(gridDim.x * blockDim.x) : csize * (int)blockDim.x;
   const int kfirst = GRID ? (int)(b * blockDim.x) : crank * (int)blockDim.x;
   for (int k = c0 + kfirst + threadIdx.x; k < c1; k += kstep) {

@@ -278,7 +278,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     WC = p.tune_wc < nw ? p.tune_wc : nw - 1;
     if (WC < (C + 31) / 32) WC = (C + 31) / 32 < nw ? (C + 31) / 32 : nw - 1;
   }
-  double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
   const double u = p.under_relax;
   const double omu = dsub(1.0, u);
   double rho = 0.0, nu = 1.0, theta_prev = 0.0;
@@ -303,9 +302,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       }
     };
     stamp(0);
-    const double* vcur = vb[(l - 1) % 3];   // written by other CTAs: coherent loads only
-    const double* vprev = vb[(l + 1) % 3];  // v^(l-2)
-    double* vnext = vb[l % 3];
+    const double* vcur = ring3(p.vbuf0, p.vbuf1, p.vbuf2, (l - 1) % 3);   // written by other CTAs: coherent loads only
+    const double* vprev = ring3(p.vbuf0, p.vbuf1, p.vbuf2, (l + 1) % 3);  // v^(l-2)
+    double* vnext = ring3(p.vbuf0, p.vbuf1, p.vbuf2, l % 3);
     double* lam_out = lam_s + (l & 1) * 3 * C;
 
     // ---- phase 1: stage the remote sectors of v^(l-1); reduce partials of l-1
@@ -569,7 +568,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     stamp(5);
   }
 
-  const double* vfin = vb[final_buf];
+  const double* vfin = ring3(p.vbuf0, p.vbuf1, p.vbuf2, final_buf);
   for (int q = tid; q < R; q += T) p.out_v[rw[q]] = vfin[rw[q]];
   const double* lfin = lam_s + final_lam * 3 * C;
   for (int k = tid; k < C; k += T) {

@@ -335,8 +335,6 @@ __global__ void __launch_bounds__(kThreads, kUseRing<SC> ? VFPI_RING_MIN_BLOCKS 
   }
   __syncthreads();
 
-  double* vb[3] = {p.vbuf0, p.vbuf1, p.vbuf2};
-  double* lb[2] = {p.lam0, p.lam1};
   const double u = p.under_relax;
   const double omu = dsub(1.0, u);
   double rho = 0.0, nu = 1.0, theta_prev = 0.0;
@@ -390,10 +388,10 @@ __global__ void __launch_bounds__(kThreads, kUseRing<SC> ? VFPI_RING_MIN_BLOCKS 
     const bool check_only = (l == p.max_iters + 1);
     // iterate buffers are written by other CTAs during the launch: plain
     // (coherent) loads only, never the read-only/nc path
-    const double* vcur = vb[(l - 1) % 3];
-    const double* vprev = vb[(l + 1) % 3];  // == v^(l-2)
-    double* vnext = vb[l % 3];
-    double* __restrict__ lam_out = lb[l & 1];
+    const double* vcur = ring3(p.vbuf0, p.vbuf1, p.vbuf2, (l - 1) % 3);
+    const double* vprev = ring3(p.vbuf0, p.vbuf1, p.vbuf2, (l + 1) % 3);  // == v^(l-2)
+    double* vnext = ring3(p.vbuf0, p.vbuf1, p.vbuf2, l % 3);
+    double* __restrict__ lam_out = ring2(p.lam0, p.lam1, l & 1);
     double* part = p.partials + (size_t)(l & 1) * G * kPartialStride;
 
     // ---- Barzilai-Borwein scalar step (solver.py:389-400) ----------------
@@ -610,12 +608,12 @@ __global__ void __launch_bounds__(kThreads, kUseRing<SC> ? VFPI_RING_MIN_BLOCKS 
     }
   }
   // ---- outputs: each CTA copies its own rows / contacts -------------------
-  const double* vfin = vb[final_buf];
+  const double* vfin = ring3(p.vbuf0, p.vbuf1, p.vbuf2, final_buf);
   for (int pos = p0 + threadIdx.x; pos < p1; pos += blockDim.x) {
     const int row = __ldg(p.row_list + pos);
     p.out_v[row] = vfin[row];
   }
-  const double* lfin = lb[final_lam];
+  const double* lfin = ring2(p.lam0, p.lam1, final_lam);
   for (int k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
     const int m = __ldg(p.cont_list + k);
 #pragma unroll
