@@ -819,11 +819,8 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
   p.under_relax = cfg->under_relax;
   p.omega = cfg->omega;
   p.cfactor = cfg->consistency_factor;
-  // one cluster per scene needs the per-scene fixed-alpha default computed
-  // cluster-wide, which only the one-CTA kernel does: that case keeps one CTA
-  const bool fixed_default = cfg->step_strategy == VFPI_STEP_FIXED_ALPHA && std::isnan(cfg->fixed_alpha);
-  const int nmode = (nodes && nodes->cluster > 1 && !fixed_default) ? 2 : 0;
-  const bool use_nodes = nodes && !bb && h->node_kernel && (nmode == 2 || nodes->cluster == 1) &&
+  const int nmode = (nodes && nodes->cluster > 1) ? 2 : 0;  // one CTA or one cluster per scene
+  const bool use_nodes = nodes && !bb && h->node_kernel &&
                          vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, std::max(max_ct, 1), nmode) > 0;
   if (use_nodes) {
     if (vfpi::node_slots_refresh(*nodes, S, n_c, d.col_i, d.col_j, d_scene_cts, st)) {

@@ -322,14 +322,18 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   double rho = 0.0, nu = 1.0, theta_prev = 0.0;
   double alpha = 0.0;
   bool use_alpha = false;
-  if (SHARED_C && p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
-    // scene batches: fixed-alpha default 1 / max|diag| of this scene (solver.py:368);
+  if (!GRID && p.step == VFPI_STEP_FIXED_ALPHA && p.fixed_alpha_default) {
+    // scene batches: fixed-alpha default 1 / max|diag| of the scene (solver.py:368),
+    // over the CTA's nodes and, for a cluster, over the cluster's CTAs;
     // a single system gets it from the setup (w filled with alpha)
     double mx = -INFINITY, nanf = 0.0;
-    for (int r = 3 * np0 + threadIdx.x; r < 3 * np1; r += blockDim.x) {
-      const double a = fabs(__ldg(p.diag + r));
-      if (isnan(a)) nanf = 1.0;
-      mx = a > mx ? a : mx;
+    for (int pos = np0 + threadIdx.x; pos < np1; pos += blockDim.x) {
+      const int node = __ldg(L.node_list + pos);
+      for (int q = 0; q < 3; ++q) {
+        const double a = fabs(__ldg(p.diag + 3 * node + q));
+        if (isnan(a)) nanf = 1.0;
+        mx = a > mx ? a : mx;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -337,17 +341,30 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       mx = t > mx ? t : mx;
     }
     cta_sum3(0.0, 0.0, nanf, sm_warp, sm_tot);
-    const double anynan = sm_tot[2];
+    const double anynan_cta = sm_tot[2];
     __syncthreads();
     if (lane == 0) sm_warp[warp] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
       double m = -INFINITY;
       for (int w2 = 0; w2 < nwarps; ++w2) m = sm_warp[w2] > m ? sm_warp[w2] : m;
-      sm_tot[3] = m;
+      sm_cpart[0][0] = m;
+      sm_cpart[0][1] = anynan_cta;
     }
     __syncthreads();
-    alpha = ddiv(1.0, anynan > 0.0 ? NAN : sm_tot[3]);
+    if constexpr (CLUSTER) cg::this_cluster().sync();
+    double m = sm_cpart[0][0], anynan = sm_cpart[0][1];
+    if constexpr (CLUSTER) {
+      m = -INFINITY;
+      anynan = 0.0;
+      for (int r = 0; r < csize; ++r) {
+        const double* q = cg::this_cluster().map_shared_rank(&sm_cpart[0][0], r);
+        m = q[0] > m ? q[0] : m;
+        anynan = q[1] > anynan ? q[1] : anynan;
+      }
+      cg::this_cluster().sync();  // sm_cpart is reused by the reductions below
+    }
+    alpha = ddiv(1.0, anynan > 0.0 ? NAN : m);
     use_alpha = true;
     __syncthreads();
   }
