@@ -176,6 +176,26 @@ int vfpi_fem_create(vfpi_handle* h, int32_t num_scenes, int32_t nodes_per_scene,
 int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stats* stats,
                   int32_t* iterations_per_scene /* optional [num_scenes] */);
 int vfpi_fem_state(vfpi_fem_batch* fb, double* x, double* v);
+/* `steps` steps of every scene without a host round trip per step: contact
+ * counts, W / gamma sizes, the diverged-scene fallback and the counters stay
+ * on the device (one synchronisation at the end), so the steps run back to
+ * back on the handle's stream. Same results as `steps` calls of vfpi_fem_step.
+ * Needs the node layout (vfpi_fem_set_node_layout) and a non-BB step; falls
+ * back to vfpi_fem_step per step otherwise (host_synced = 1). Optional
+ * outputs: iterations [steps][num_scenes], contacts [steps]. */
+typedef struct vfpi_fem_run_stats {
+  int64_t contacts;            /* sum over steps of the step's contacts */
+  int64_t contact_iterations;  /* sum over steps and scenes of n_c(scene) * iterations(scene) */
+  int64_t iterations;          /* sum over steps and scenes */
+  int32_t max_iterations;
+  int32_t diverged_scene_steps;
+  double loop_ms;              /* summed iteration-kernel time (device events) */
+  double run_ms;               /* the whole run (device events) */
+  int32_t host_synced;
+  int32_t reserved;
+} vfpi_fem_run_stats;
+int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi_fem_run_stats* stats,
+                 int32_t* iterations, int32_t* contacts);
 /* Node-block SELL layout for the batch's iteration kernel (csrc/vfpi_nodes.cu):
  * one lane per node, 3x3 blocks (descriptor + 9 values) instead of entries,
  * the same template for every scene: `order` (nodes_per_scene) = node

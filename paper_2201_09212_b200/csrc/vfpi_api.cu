@@ -823,7 +823,7 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
   const bool use_nodes = nodes && !bb && h->node_kernel &&
                          vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, std::max(max_ct, 1), nmode) > 0;
   if (use_nodes) {
-    if (vfpi::node_slots_refresh(*nodes, S, n_c, d.col_i, d.col_j, d_scene_cts, st)) {
+    if (vfpi::node_slots_refresh(*nodes, S, n_c, d.col_i, d.col_j, nullptr, st)) {
       h->err = "node slot refresh failed";
       return VFPI_CUDA_ERROR;
     }
@@ -1153,6 +1153,8 @@ struct vfpi_fem_batch {
   Workspace::Buf zero_cts, ks_off, ks_val, ks_col;  // K in SELL-32
   Workspace::Buf cg_r, cg_p, cg_q, cg_list;        // contact-free fallback of diverged scenes
   Workspace::Buf x0, v0;                           // initial state (vfpi_fem_reset)
+  Workspace::Buf run_acc, run_its, run_cts;        // device counters of vfpi_fem_run
+  std::vector<cudaEvent_t> run_ev;                 // per-step iteration-kernel events of vfpi_fem_run
   vfpi::NodeLayoutHost nbh;                        // node-block SELL layout (vfpi_fem_set_node_layout)
   vfpi::NodeLayoutDev nbd;
   bool nb_ready = false;
@@ -1260,6 +1262,44 @@ int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a,
   return VFPI_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// A's contact-free row layout + column statistics (diagonal, squared row norms
+// for W), built once per batch and whenever another solve used the workspace
+int fem_contact_free_layout(vfpi_fem_batch* fb) {
+  vfpi_handle* h = fb->h;
+  Workspace& ws = h->ws;
+  cudaStream_t st = ws.stream;
+  vfpi_system d0 = fb->A;
+  d0.n_c = 0;
+  d0.b = P<double>(fb->b);
+  d0.col_i = P<int32_t>(fb->ci);
+  d0.col_j = P<int32_t>(fb->cj);
+  d0.frames = P<double>(fb->frames);
+  d0.mu = P<double>(fb->mu);
+  d0.mu2 = P<double>(fb->mu2);
+  d0.phi = P<double>(fb->phi);
+  vfpi::LayoutOptions opt;
+  opt.anchor_order = false;
+  opt.length_sort = h->layout_opt.length_sort;
+  opt.scene_row_ptr = P<int>(fb->rows);
+  opt.scene_ct_ptr = P<int>(fb->zero_cts);
+  int rc0 = vfpi::setup_layout(ws, d0, fb->S, st, ws.h_summary, h->err, h->launches, opt);
+  if (!rc0) rc0 = vfpi::setup_pack(ws, d0, fb->S, false, *ws.h_summary, st, h->err, h->launches);
+  if (!rc0) rc0 = vfpi::setup_rowpos(ws, (int)fb->n, fb->S, st, h->err);
+  if (rc0) return rc0;
+  CK(vfpi::ensure(ws.cont_list, 4 * (size_t)fb->nodes));  // per-step refresh never grows it
+  CK(cudaStreamSynchronize(st));
+  fb->layout_epoch = ws.layout_epoch;
+  return VFPI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stats* stats,
                   int32_t* iterations_per_scene) {
   if (!fb || !cfg || !stats) return VFPI_BAD_ARGUMENT;
@@ -1296,27 +1336,8 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   // (layout buffers are only (re)allocated inside setup_layout/setup_pack, which
   // bump the epoch; growth of unrelated workspace buffers leaves them intact)
   if (fb->layout_epoch != ws.layout_epoch) {
-    vfpi_system d0 = fb->A;
-    d0.n_c = 0;
-    d0.b = P<double>(fb->b);
-    d0.col_i = P<int32_t>(fb->ci);
-    d0.col_j = P<int32_t>(fb->cj);
-    d0.frames = P<double>(fb->frames);
-    d0.mu = P<double>(fb->mu);
-    d0.mu2 = P<double>(fb->mu2);
-    d0.phi = P<double>(fb->phi);
-    vfpi::LayoutOptions opt;
-    opt.anchor_order = false;
-    opt.length_sort = h->layout_opt.length_sort;
-    opt.scene_row_ptr = P<int>(fb->rows);
-    opt.scene_ct_ptr = P<int>(fb->zero_cts);
-    int rc0 = vfpi::setup_layout(ws, d0, fb->S, st, ws.h_summary, h->err, h->launches, opt);
-    if (!rc0) rc0 = vfpi::setup_pack(ws, d0, fb->S, false, *ws.h_summary, st, h->err, h->launches);
-    if (!rc0) rc0 = vfpi::setup_rowpos(ws, (int)fb->n, fb->S, st, h->err);
+    const int rc0 = fem_contact_free_layout(fb);
     if (rc0) return rc0;
-    CK(vfpi::ensure(ws.cont_list, 4 * (size_t)fb->nodes));  // per-step refresh never grows it
-    CK(cudaStreamSynchronize(st));
-    fb->layout_epoch = ws.layout_epoch;
   }
   int max_ct = 0;
   for (int k = 0; k < fb->S; ++k) max_ct = std::max(max_ct, fb->h_cts[k + 1] - fb->h_cts[k]);
@@ -1389,6 +1410,197 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   stats->setup_ms = su;
   stats->loop_ms = lo;
   stats->step_ms = step;
+  return VFPI_OK;
+}
+
+int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi_fem_run_stats* stats,
+                 int32_t* iterations, int32_t* contacts) {
+  if (!fb || !cfg || !stats || steps < 0) return VFPI_BAD_ARGUMENT;
+  vfpi_handle* h = fb->h;
+  if (cfg->op < 0 || cfg->op > 2 || cfg->step_strategy < 0 || cfg->step_strategy > 4 || cfg->max_iters < 0) {
+    h->err = "bad solver config";
+    return VFPI_BAD_ARGUMENT;
+  }
+  std::memset(stats, 0, sizeof(*stats));
+  const bool cheb = cfg->chebyshev != 0;
+  const bool bb = cfg->step_strategy >= VFPI_STEP_BB1 && cfg->step_strategy <= VFPI_STEP_BB_ALTERNATING;
+  const int nmode = fb->nb_ready && fb->nbd.cluster > 1 ? 2 : 0;
+  if (!fb->nb_ready || bb || !h->node_kernel || vfpi::node_kernel_blocks_per_sm(cfg->op, cheb, 1, nmode) <= 0) {
+    // the per-step path (host reads of the contact counts each step)
+    for (int k = 0; k < steps; ++k) {
+      vfpi_fem_step_stats s{};
+      std::vector<int32_t> its(iterations ? (size_t)fb->S : 0);
+      const int rc = vfpi_fem_step(fb, cfg, &s, iterations ? its.data() : nullptr);
+      if (rc) return rc;
+      if (iterations) std::memcpy(iterations + (size_t)k * fb->S, its.data(), 4 * (size_t)fb->S);
+      if (contacts) contacts[k] = (int32_t)s.contacts;
+      stats->contacts += s.contacts;
+      stats->contact_iterations += s.contact_iterations;
+      stats->iterations += s.iterations;
+      stats->max_iterations = std::max(stats->max_iterations, s.max_iterations);
+      stats->diverged_scene_steps += s.diverged_scenes;
+      stats->loop_ms += s.loop_ms;
+      stats->run_ms += s.step_ms;
+    }
+    stats->host_synced = 1;
+    return VFPI_OK;
+  }
+  if (cudaSetDevice(h->ws.device) != cudaSuccess) return VFPI_CUDA_ERROR;
+  cudaStream_t st = h->ws.stream;
+  Workspace& ws = h->ws;
+  const vfpi_fem_params& q = fb->prm;
+  const int S = fb->S;
+  const int n = (int)fb->n;
+  const int ncmax = (int)fb->nodes;  // every node in contact: the upper bound the run sizes for
+  int rc;
+  if (fb->layout_epoch != ws.layout_epoch && (rc = fem_contact_free_layout(fb))) return rc;
+  // everything the loop touches, sized once (no allocation, no host read inside the loop)
+  const size_t tr = (size_t)std::max(cfg->max_iters, 1);
+  const size_t npad = (((size_t)std::max(n, 1) + 3) / 4) * 4 + 4;
+  CK(vfpi::ensure(ws.vbuf, 3 * 8 * npad));
+  CK(vfpi::ensure(ws.lambuf, 2 * 24 * (size_t)ncmax));
+  CK(vfpi::ensure(ws.status, sizeof(vfpi::SolveStatus) * (size_t)S));
+  CK(vfpi::ensure(ws.b_trace, 8 * tr * (size_t)S));
+  CK(vfpi::ensure(ws.cont_list, 4 * (size_t)ncmax));
+  CK(vfpi::ensure(ws.blk_ct, 4 * ((size_t)S + 1)));
+  CK(vfpi::ensure(ws.w, 8 * (size_t)n));
+  CK(vfpi::ensure(ws.gamma, 8 * (size_t)ncmax));
+  CK(vfpi::ensure(ws.w_mean, 16));
+  CK(vfpi::ensure(ws.partials, 2 * 8 * (size_t)S * vfpi::kPartialStride));
+  CK(vfpi::ensure(fb->cg_r, 8 * (size_t)n));
+  CK(vfpi::ensure(fb->cg_p, 8 * (size_t)n));
+  CK(vfpi::ensure(fb->cg_q, 8 * (size_t)n));
+  CK(vfpi::ensure(fb->run_acc, 8 * 8));
+  if (iterations) CK(vfpi::ensure(fb->run_its, 4 * (size_t)std::max(steps, 1) * S));
+  if (contacts) CK(vfpi::ensure(fb->run_cts, 4 * (size_t)std::max(steps, 1)));
+  while (fb->run_ev.size() < 2 * (size_t)steps + 2) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    fb->run_ev.push_back(e);
+  }
+  CK(cudaMemsetAsync(fb->run_acc.p, 0, 64, st));
+  CK(cudaMemsetAsync(ws.flags.p, 0, 16, st));
+  vfpi::launch_iota_int(ncmax, P<int>(ws.cont_list), st);  // contacts stay in scene order
+  ++h->launches;
+  double* vb = P<double>(ws.vbuf);
+  double* lb = P<double>(ws.lambuf);
+  vfpi_system d = fb->A;
+  d.n_c = ncmax;
+  d.b = P<double>(fb->b);
+  d.col_i = P<int32_t>(fb->ci);
+  d.col_j = P<int32_t>(fb->cj);
+  d.frames = P<double>(fb->frames);
+  d.mu = P<double>(fb->mu);
+  d.mu2 = P<double>(fb->mu2);
+  d.phi = P<double>(fb->phi);
+  const int* d_nc = P<int>(fb->cts) + S;  // the step's contact count, on the device
+  vfpi::IterParams p{};
+  p.n = n;
+  p.n_c = ncmax;  // upper bound; the kernels take each scene's range from blk_ct
+  p.G = S;
+  p.blk_ct = P<int>(ws.blk_ct);
+  p.cont_list = P<int>(ws.cont_list);
+  p.b = d.b;
+  p.w = P<double>(ws.w);
+  p.gamma = P<double>(ws.gamma);
+  p.col_i = d.col_i;
+  p.col_j = d.col_j;
+  p.frames = d.frames;
+  p.mu = d.mu;
+  p.mu2 = d.mu2;
+  p.phi = d.phi;
+  p.w_mean = P<double>(ws.w_mean);
+  p.diag = P<double>(ws.diag);
+  p.fixed_alpha_default = (cfg->step_strategy == VFPI_STEP_FIXED_ALPHA && std::isnan(cfg->fixed_alpha)) ? 1 : 0;
+  p.vbuf0 = vb;
+  p.vbuf1 = vb + npad;
+  p.vbuf2 = vb + 2 * npad;
+  p.lam0 = lb;
+  p.lam1 = lb + 3 * (size_t)ncmax;
+  p.partials = P<double>(ws.partials);
+  p.trace = P<double>(ws.b_trace);
+  p.trace_stride = tr;
+  p.status = P<vfpi::SolveStatus>(ws.status);
+  p.out_v = P<double>(fb->vhat);
+  p.out_lam = P<double>(fb->lam);
+  p.max_iters = cfg->max_iters;
+  p.cheby_start = cfg->cheby_start;
+  p.step = cfg->step_strategy;
+  p.tol = cfg->residual_tol;
+  p.under_relax = cfg->under_relax;
+  p.omega = cfg->omega;
+  p.cfactor = cfg->consistency_factor;
+  CK(cudaEventRecord(fb->run_ev[0], st));
+  for (int k = 0; k < steps; ++k) {
+    // (1) right-hand side, (2) node-plane contacts (as vfpi_fem_step)
+    vfpi::launch_fem_rhs_sell(fb->n, P<int64_t>(fb->ks_off), P<double>(fb->ks_val), P<int>(fb->ks_col),
+                              P<double>(fb->x), P<double>(fb->X), P<double>(fb->v), P<double>(fb->m),
+                              P<double>(fb->g), 2.0 / q.dt, P<double>(fb->b), st);
+    vfpi::launch_fem_flags(fb->nodes, P<double>(fb->x), q.margin, P<int>(fb->flag), st);
+    size_t tb = fb->tmp.cap;
+    CK(cub::DeviceScan::ExclusiveSum(fb->tmp.p, tb, P<int>(fb->flag), P<int>(fb->pos), (int)fb->nodes, st));
+    vfpi::launch_fem_scene_cts(S, fb->Nn, P<int>(fb->flag), P<int>(fb->pos), P<int>(fb->cts), st);
+    vfpi::launch_fem_contacts(fb->nodes, P<int>(fb->flag), P<int>(fb->pos), P<double>(fb->x), P<double>(fb->v),
+                              P<double>(fb->frame), q.mu, -(q.beta_err / q.dt), q.e_rest, q.rest_threshold,
+                              P<int>(fb->ci), P<int>(fb->cj), P<double>(fb->frames), P<double>(fb->mu),
+                              P<double>(fb->mu2), P<double>(fb->phi), st);
+    // (3) W, gamma and the solve of every scene (counts read on the device)
+    CK(cudaMemcpyAsync(ws.blk_ct.p, fb->cts.p, 4 * ((size_t)S + 1), cudaMemcpyDeviceToDevice, st));
+    rc = vfpi::setup_step_matrix(ws, d, *cfg, nullptr, st, h->err, h->launches, d_nc);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(ws.vbuf.p, 0, 3 * 8 * npad, st));
+    CK(cudaMemcpyAsync(vb, fb->warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(vb + 2 * npad, fb->warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(ws.lambuf.p, 0, 2 * 24 * (size_t)ncmax, st));
+    CK(cudaMemsetAsync(ws.status.p, 0, sizeof(vfpi::SolveStatus) * (size_t)S, st));
+    if (vfpi::node_slots_refresh(fb->nbd, S, ncmax, d.col_i, d.col_j, d_nc, st)) {
+      h->err = "node slot refresh failed";
+      return VFPI_CUDA_ERROR;
+    }
+    CK(cudaEventRecord(fb->run_ev[2 + 2 * k], st));
+    rc = vfpi::launch_iterate_nodes(p, fb->nbd, cfg->op, cheb, 1, st, h->err, nmode);
+    if (rc) return rc;
+    CK(cudaEventRecord(fb->run_ev[3 + 2 * k], st));
+    // (3b) diverged scenes: the flagged contact-free CG step, decided on the device
+    const int64_t ns = 3 * (int64_t)fb->Nn;
+    if (vfpi::launch_cg_scenes_status(S, ns, fb->A.indptr, fb->A.indices, fb->A.data, P<double>(fb->b),
+                                      P<double>(fb->vhat), P<double>(fb->cg_r), P<double>(fb->cg_p),
+                                      P<double>(fb->cg_q), 1e-10, 10 * ns, P<vfpi::SolveStatus>(ws.status),
+                                      P<int>(fb->cts), P<double>(fb->lam), st)) {
+      h->err = "fallback CG launch failed";
+      return VFPI_CUDA_ERROR;
+    }
+    // (4) midpoint integration, warm start; (5) counters
+    vfpi::launch_fem_advance(fb->n, q.dt, P<double>(fb->vhat), P<double>(fb->x), P<double>(fb->v),
+                             P<double>(fb->warm), st);
+    vfpi::launch_fem_run_stats(S, P<vfpi::SolveStatus>(ws.status), P<int>(fb->cts), k,
+                               P<unsigned long long>(fb->run_acc), iterations ? P<int>(fb->run_its) : nullptr,
+                               contacts ? P<int>(fb->run_cts) : nullptr, st);
+    h->launches += 14;  // rhs, flags, scan x2, scene pointers, contacts, W/tie/gamma x3, slots, kernel, CG, advance, stats
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(fb->run_ev[1], st));
+  unsigned long long acc[8];
+  CK(cudaMemcpyAsync(acc, fb->run_acc.p, 64, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->h_flags, ws.flags.p, 4, cudaMemcpyDeviceToHost, st));
+  if (iterations && steps) CK(cudaMemcpyAsync(iterations, fb->run_its.p, 4 * (size_t)steps * S, cudaMemcpyDeviceToHost, st));
+  if (contacts && steps) CK(cudaMemcpyAsync(contacts, fb->run_cts.p, 4 * (size_t)steps, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  rc = flags_to_code(h, *h->h_flags);
+  if (rc) return rc;
+  stats->contact_iterations = (int64_t)acc[0];
+  stats->iterations = (int64_t)acc[1];
+  stats->diverged_scene_steps = (int32_t)acc[2];
+  stats->max_iterations = (int32_t)acc[3];
+  stats->contacts = (int64_t)acc[4];
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, fb->run_ev[0], fb->run_ev[1]);
+  stats->run_ms = ms;
+  for (int k = 0; k < steps; ++k) {
+    cudaEventElapsedTime(&ms, fb->run_ev[2 + 2 * k], fb->run_ev[3 + 2 * k]);
+    stats->loop_ms += ms;
+  }
+  h->last_node_kernel = 1;
   return VFPI_OK;
 }
 
@@ -1490,8 +1702,9 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
                             &fb->cg_p, &fb->cg_q, &fb->cg_list, &fb->x0, &fb->v0, &fb->nbh.t_order,
                             &fb->nbh.t_off, &fb->nbh.t_bcol, &fb->nbh.desc, &fb->nbh.val, &fb->nbh.slice_off,
                             &fb->nbh.node_list, &fb->nbh.node_slot, &fb->nbh.blk_slice, &fb->nbh.blk_pos, &fb->nbh.vs,
-                            &fb->nbh.jt})
+                            &fb->nbh.jt, &fb->run_acc, &fb->run_its, &fb->run_cts})
     if (b->p) cudaFree(b->p);
+  for (cudaEvent_t e : fb->run_ev) cudaEventDestroy(e);
   if (fb->e0) cudaEventDestroy(fb->e0);
   if (fb->e1) cudaEventDestroy(fb->e1);
   delete fb;

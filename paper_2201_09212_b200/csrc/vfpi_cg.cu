@@ -38,6 +38,9 @@ struct CgArgs {
   double* partial;     // [2][G] (grid mode)
   int32_t* iters_out;  // per scene (scene mode) or [1] (grid mode)
   const int32_t* scene_list;
+  const SolveStatus* status;  // scene mode without a list: CTA b runs iff scene b diverged
+  const int* cts;             //   its contacts' impulses [cts[b], cts[b+1]) are zeroed
+  double* lam;
   int64_t n;           // rows per scene (scene mode) / of the system (grid mode)
   double rtol;
   int64_t maxiter;
@@ -90,9 +93,16 @@ __global__ void __launch_bounds__(kCgThreads) k_cg(CgArgs a) {
   if (GRID) {
     lo = a.n * blockIdx.x / gridDim.x;
     hi = a.n * (blockIdx.x + 1) / gridDim.x;
-  } else {
+  } else if (a.scene_list) {
     lo = (int64_t)a.scene_list[blockIdx.x] * a.n;
     hi = lo + a.n;
+  } else {  // device-driven: every scene's CTA checks its own status
+    if (!a.status[blockIdx.x].diverged) return;
+    lo = (int64_t)blockIdx.x * a.n;
+    hi = lo + a.n;
+    for (int64_t t = 3 * (int64_t)a.cts[blockIdx.x] + threadIdx.x; t < 3 * (int64_t)a.cts[blockIdx.x + 1];
+         t += blockDim.x)
+      a.lam[t] = 0.0;
   }
   const double* b = a.b;
   double *x = a.x, *r = a.r, *p = a.p, *q = a.q;
@@ -152,8 +162,20 @@ int launch_cg_scenes(int num, const int32_t* scene_list, int64_t rows_per_scene,
                      const int32_t* indices, const double* data, const double* b, double* x, double* r, double* p,
                      double* q, double rtol, int64_t maxiter, int32_t* iters_out, cudaStream_t st) {
   if (num <= 0) return 0;
-  CgArgs a{indptr, indices, data, b, x, r, p, q, nullptr, iters_out, scene_list, rows_per_scene, rtol, maxiter};
+  CgArgs a{indptr, indices, data, b, x, r, p, q, nullptr, iters_out, scene_list, nullptr, nullptr, nullptr,
+           rows_per_scene, rtol, maxiter};
   k_cg<false><<<num, kCgThreads, 0, st>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int launch_cg_scenes_status(int S, int64_t rows_per_scene, const int32_t* indptr, const int32_t* indices,
+                            const double* data, const double* b, double* x, double* r, double* p, double* q,
+                            double rtol, int64_t maxiter, const SolveStatus* status, const int* cts, double* lam,
+                            cudaStream_t st) {
+  if (S <= 0) return 0;
+  CgArgs a{indptr, indices, data, b, x, r, p, q, nullptr, nullptr, nullptr, status, cts, lam, rows_per_scene, rtol,
+           maxiter};
+  k_cg<false><<<S, kCgThreads, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -167,7 +189,8 @@ int cg_grid_partials(int device) {
 int launch_cg_grid(int G, int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
                    const double* b, double* x, double* r, double* p, double* q, double* partial, double rtol,
                    int64_t maxiter, int32_t* iters_out, cudaStream_t st) {
-  CgArgs a{indptr, indices, data, b, x, r, p, q, partial, iters_out, nullptr, n, rtol, maxiter};
+  CgArgs a{indptr, indices, data, b, x, r, p, q, partial, iters_out, nullptr, nullptr, nullptr, nullptr, n, rtol,
+           maxiter};
   void* args[] = {&a};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cg<true>, dim3(G), dim3(kCgThreads), args, 0, st);
   return e == cudaSuccess ? 0 : 1;

@@ -201,6 +201,46 @@ void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, doubl
   if (n > 0) k_fem_advance<<<nb(n), 256, 0, st>>>(n, dt, vh, x, v, warm);
 }
 
+// per-step counters of a device-driven run (vfpi_fem_run): integer sums, so
+// the atomics give exact, order-independent totals
+__global__ void k_fem_run_stats(int S, const SolveStatus* __restrict__ st, const int* __restrict__ cts, int step,
+                                unsigned long long* __restrict__ acc, int* __restrict__ its_out,
+                                int* __restrict__ cts_out) {
+  unsigned long long ci = 0, it = 0, dv = 0;
+  int mx = 0;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int i = st[s].iterations;
+    const int nc = cts[s + 1] - cts[s];
+    ci += (unsigned long long)nc * (unsigned long long)i;
+    it += (unsigned long long)i;
+    dv += st[s].diverged ? 1ull : 0ull;
+    mx = max(mx, i);
+    if (its_out) its_out[(size_t)step * S + s] = i;
+  }
+  atomicAdd(acc + 0, ci);
+  atomicAdd(acc + 1, it);
+  atomicAdd(acc + 2, dv);
+  atomicMax(acc + 3, (unsigned long long)mx);
+  if (threadIdx.x == 0) {
+    atomicAdd(acc + 4, (unsigned long long)cts[S]);
+    if (cts_out) cts_out[step] = cts[S];
+  }
+}
+
+__global__ void k_iota_int(int n, int* v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+void launch_fem_run_stats(int S, const SolveStatus* st, const int* cts, int step, unsigned long long* acc,
+                          int* its_out, int* cts_out, cudaStream_t stream) {
+  k_fem_run_stats<<<1, 1024, 0, stream>>>(S, st, cts, step, acc, its_out, cts_out);
+}
+
+void launch_iota_int(int n, int* v, cudaStream_t st) {
+  if (n > 0) k_iota_int<<<nb(n), 256, 0, st>>>(n, v);
+}
+
 void launch_csr_matvec(int64_t rows, const int* rp, const int* ci, const double* cx, const double* x, double* y,
                        cudaStream_t st) {
   if (rows > 0) k_csr_matvec<<<nb(rows), 256, 0, st>>>(rows, rp, ci, cx, x, y);

@@ -157,8 +157,9 @@ uint64_t alloc_generation();
 // resident = CTA-contiguous CSR (pos_ptr/pk_val/pk_col), else SELL-32.
 int setup_pack(Workspace& ws, const vfpi_system& dsys, int G, bool resident, const SetupSummary& hs,
                cudaStream_t st, std::string& err, int64_t& launches);
+// d_nc != nullptr: dsys.n_c is an upper bound and *d_nc (device) the contact count
 int setup_step_matrix(Workspace& ws, const vfpi_system& dsys, const vfpi_config& cfg, const double* d_w_cached,
-                      cudaStream_t st, std::string& err, int64_t& launches);
+                      cudaStream_t st, std::string& err, int64_t& launches, const int* d_nc = nullptr);
 
 // ---- iteration (vfpi_solve.cu) ---------------------------------------------
 int launch_iterate(const IterParams& p, int op, bool cheb, bool bb, int smem_bytes, cudaStream_t st,
@@ -352,6 +353,9 @@ void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int
 void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st);
 void launch_csr_matvec(int64_t rows, const int* rp, const int* ci, const double* cx, const double* x, double* y,
                        cudaStream_t st);
+void launch_fem_run_stats(int S, const SolveStatus* st, const int* cts, int step, unsigned long long* acc,
+                          int* its_out, int* cts_out, cudaStream_t stream);
+void launch_iota_int(int n, int* v, cudaStream_t st);
 
 // ---- configs[3] heightfield detection (vfpi_heightfield.cu) -----------------
 struct HfParams {
@@ -377,6 +381,11 @@ void launch_add_inplace(int64_t n, const double* f, double* b, cudaStream_t st);
 int launch_cg_scenes(int num, const int32_t* scene_list, int64_t rows_per_scene, const int32_t* indptr,
                      const int32_t* indices, const double* data, const double* b, double* x, double* r, double* p,
                      double* q, double rtol, int64_t maxiter, int32_t* iters_out, cudaStream_t st);
+// device-driven variant: CTA b steps scene b iff status[b].diverged (no host round trip)
+int launch_cg_scenes_status(int S, int64_t rows_per_scene, const int32_t* indptr, const int32_t* indices,
+                            const double* data, const double* b, double* x, double* r, double* p, double* q,
+                            double rtol, int64_t maxiter, const SolveStatus* status, const int* cts, double* lam,
+                            cudaStream_t st);
 int cg_grid_partials(int device);
 int launch_cg_grid(int G, int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
                    const double* b, double* x, double* r, double* p, double* q, double* partial, double rtol,
@@ -416,7 +425,7 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
                       NodeLayoutDev& out, int* d_flags, cudaStream_t st, int cluster,
                       const std::vector<int64_t>& t_off_host);
 int node_cluster_size(int S, int nsl, int num_sms);  // CTAs per scene so a small batch fills the GPU
-int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
+int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_nc,
                        cudaStream_t st);
 int node_kernel_smem(int max_ct);
 // mode: 0 one CTA per scene, 1 one system over a cooperative grid, 2 one cluster per scene

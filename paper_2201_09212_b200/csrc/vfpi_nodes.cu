@@ -271,7 +271,11 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   __shared__ double sm_tot[4];
   __shared__ __align__(8) uint64_t ring_bar[kNbThreads / 32][kNbStages];
 
-  constexpr bool GRID = MODE == kGrid, CLUSTER = MODE == kCluster, SHARED_C = MODE == kScene;
+  // contact slots (v* / J_c^T lam of contact rows, 6 per contact, global index)
+  // live in global memory in every mode: single-node contacts are solved inline
+  // by the node's lane, so the slots see a few doubles per contact and iteration,
+  // and the kernel's shared memory does not depend on the contact count
+  constexpr bool GRID = MODE == kGrid, CLUSTER = MODE == kCluster, SHARED_C = false;
   __shared__ double sm_cpart[2][4];  // cluster mode: this CTA's partials, by iteration parity
   const int b = blockIdx.x;
   const int crank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
@@ -681,21 +685,6 @@ __global__ void k_nb_slice_off(int S, int nsl, const int64_t* __restrict__ t_off
   }
 }
 
-__global__ void k_nb_node_slots(int n_c, int G, const int* __restrict__ ci, const int* __restrict__ cj,
-                                const int* __restrict__ ct, int* __restrict__ node_slot) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_c) return;
-  int lo = 0, hi = G;  // owner scene: ct[b] <= k < ct[b+1]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (ct[mid] <= k) lo = mid;
-    else hi = mid;
-  }
-  const int loc = (k - ct[lo]) * kSlotsPerContact;
-  node_slot[ci[k] / 3] = loc;
-  if (cj[k] >= 0) node_slot[cj[k] / 3] = loc + 3;
-}
-
 // ---- single-system (grid) layout, built per solve from the row-sorted entries --
 // (setup_pack: perm[row_ptr[r] + k] = CSC index of the k-th numeric entry of
 // row r in increasing column order, colof = its column)
@@ -802,9 +791,9 @@ __global__ void k_ng_contact_check(int n_c, const int* __restrict__ ci, const in
 }
 
 __global__ void k_ng_node_slots(int n_c, const int* __restrict__ ci, const int* __restrict__ cj,
-                                int* __restrict__ node_slot) {
+                                int* __restrict__ node_slot, const int* __restrict__ d_nc = nullptr) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_c) return;
+  if (k >= n_c || (d_nc && k >= *d_nc)) return;
   node_slot[ci[k] / 3] = kSlotsPerContact * k;
   if (cj[k] >= 0) node_slot[cj[k] / 3] = kSlotsPerContact * k + 3;
 }
@@ -846,7 +835,7 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
       ensure(h.slice_off, 8 * ((size_t)S * nsl + 1)) || ensure(h.node_list, 4 * (size_t)S * nn) ||
       ensure(h.node_slot, 4 * (size_t)S * nn) || ensure(h.blk_slice, 4 * (G + 1)) || ensure(h.blk_pos, 4 * (G + 1)))
     return 1;
-  if (CL > 1 && (ensure(h.vs, 8 * kSlotsPerContact * (size_t)S * nn) || ensure(h.jt, 8 * kSlotsPerContact * (size_t)S * nn)))
+  if (ensure(h.vs, 8 * kSlotsPerContact * (size_t)S * nn) || ensure(h.jt, 8 * kSlotsPerContact * (size_t)S * nn))
     return 1;
   // padding lanes (positions past the scene's last node) are never filled:
   // their descriptors must read as empty
@@ -896,20 +885,18 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   out.slice_off = (const int64_t*)h.slice_off.p;
   out.desc = (const unsigned*)h.desc.p;
   out.val = (const double*)h.val.p;
-  out.vs_g = CL > 1 ? (double*)h.vs.p : nullptr;
-  out.jt_g = CL > 1 ? (double*)h.jt.p : nullptr;
+  out.vs_g = (double*)h.vs.p;
+  out.jt_g = (double*)h.jt.p;
   return 0;
 }
 
-int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_ct,
+int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_nc,
                        cudaStream_t st) {
+  // global contact slots (6 k); J_c^T lam starts at 0. n_c is the exact count,
+  // or with d_nc != nullptr an upper bound and *d_nc (device) the count
   if (cudaMemsetAsync(L.node_slot, 0xff, 4 * (size_t)S * L.nn, st) != cudaSuccess) return 1;
-  if (L.cluster > 1) {  // global contact slots; J_c^T lam starts at 0
-    if (n_c > 0) k_ng_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, ci, cj, L.node_slot);
-    if (cudaMemsetAsync(L.jt_g, 0, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1), st) != cudaSuccess) return 1;
-  } else if (n_c > 0) {
-    k_nb_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, S, ci, cj, d_ct, L.node_slot);
-  }
+  if (n_c > 0) k_ng_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, ci, cj, L.node_slot, d_nc);
+  if (cudaMemsetAsync(L.jt_g, 0, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1), st) != cudaSuccess) return 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -998,7 +985,10 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   return VFPI_OK;
 }
 
-int node_kernel_smem(int max_ct) { return 2 * kSlotsPerContact * 8 * max_ct + kNbRingBytes + 128; }
+int node_kernel_smem(int max_ct) {
+  (void)max_ct;  // contact slots are global: the ring is the only dynamic shared memory
+  return kNbRingBytes + 128;
+}
 
 int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, int mode) {
   NbFn f = nb_pick(op, cheb, true, mode);

@@ -561,9 +561,10 @@ __global__ void k_w_frob(int n, const double* __restrict__ diag, const double* _
 // the two nodes of a D contact (solver.py:182-213, 366). Groups are disjoint
 // because contact columns do not overlap (checked in k_mark).
 __global__ void k_tie(int n_c, int pair_tie, const int* __restrict__ ci, const int* __restrict__ cj,
-                      const double* __restrict__ diag, const double* __restrict__ rns, double* w) {
+                      const double* __restrict__ diag, const double* __restrict__ rns, double* w,
+                      const int* __restrict__ d_nc) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n_c) return;
+  if (m >= n_c || (d_nc && m >= *d_nc)) return;
   const int i = ci[m], j = cj[m];
   if (pair_tie && j >= 0) {
     double sd = 0.0, sr = 0.0;
@@ -588,9 +589,9 @@ __global__ void k_tie(int n_c, int pair_tie, const int* __restrict__ ci, const i
 }
 
 __global__ void k_gamma(int n_c, const int* __restrict__ ci, const int* __restrict__ cj, const double* __restrict__ w,
-                        double omega, double* gamma, int* flags) {
+                        double omega, double* gamma, int* flags, const int* __restrict__ d_nc) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n_c) return;
+  if (m >= n_c || (d_nc && m >= *d_nc)) return;
   const int i = ci[m], j = cj[m];
   double g = w[i];
   if (!(w[i] == w[i + 1] && w[i] == w[i + 2])) atomicOr(flags, 8);
@@ -946,7 +947,7 @@ int setup_pack(Workspace& ws, const vfpi_system& s, int G, bool resident, const 
 
 // W (frobenius / fixed-alpha / cached) and gamma; flags reported through ws.flags
 int setup_step_matrix(Workspace& ws, const vfpi_system& s, const vfpi_config& cfg, const double* d_w_cached,
-                      cudaStream_t st, std::string& err, int64_t& launches) {
+                      cudaStream_t st, std::string& err, int64_t& launches, const int* d_nc) {
   const int n = (int)s.n, n_c = (int)s.n_c;
   VFPI_CK(ensure(ws.w, 8 * (size_t)n));
   VFPI_CK(ensure(ws.gamma, 8 * (size_t)n_c));
@@ -972,12 +973,13 @@ int setup_step_matrix(Workspace& ws, const vfpi_system& s, const vfpi_config& cf
     }
     if (n_c > 0) {
       k_tie<<<nblk(n_c), 256, 0, st>>>(n_c, cfg.op == VFPI_OP_PROXIMAL ? 1 : 0, s.col_i, s.col_j,
-                                       P<double>(ws.diag), P<double>(ws.rns), w);
+                                       P<double>(ws.diag), P<double>(ws.rns), w, d_nc);
       ++launches;
     }
   }
   if (n_c > 0) {
-    k_gamma<<<nblk(n_c), 256, 0, st>>>(n_c, s.col_i, s.col_j, w, cfg.omega, P<double>(ws.gamma), P<int>(ws.flags));
+    k_gamma<<<nblk(n_c), 256, 0, st>>>(n_c, s.col_i, s.col_j, w, cfg.omega, P<double>(ws.gamma), P<int>(ws.flags),
+                                       d_nc);
     ++launches;
   }
   const bool bb = cfg.step_strategy >= VFPI_STEP_BB1 && cfg.step_strategy <= VFPI_STEP_BB_ALTERNATING;

@@ -31,6 +31,12 @@ class _Stats(C.Structure):
                 ("loop_ms", C.c_double), ("step_ms", C.c_double)]
 
 
+class _RunStats(C.Structure):
+    _fields_ = [("contacts", C.c_int64), ("contact_iterations", C.c_int64), ("iterations", C.c_int64),
+                ("max_iterations", C.c_int32), ("diverged_scene_steps", C.c_int32), ("loop_ms", C.c_double),
+                ("run_ms", C.c_double), ("host_synced", C.c_int32), ("reserved", C.c_int32)]
+
+
 def _bind():
     L = _lib.lib()
     if not hasattr(L, "_fem_bound"):
@@ -46,6 +52,9 @@ def _bind():
         L.vfpi_fem_set_node_layout.restype = C.c_int
         L.vfpi_fem_set_node_layout.argtypes = [C.c_void_p, C.c_int32, _lib._i32p, C.c_int32, C.POINTER(C.c_int64),
                                                _lib._i32p]
+        L.vfpi_fem_run.restype = C.c_int
+        L.vfpi_fem_run.argtypes = [C.c_void_p, C.POINTER(VfpiConfig), C.c_int32, C.POINTER(_RunStats), _lib._i32p,
+                                   _lib._i32p]
         L.vfpi_fem_reset.restype = C.c_int
         L.vfpi_fem_reset.argtypes = [C.c_void_p]
         L.vfpi_fem_state_device.restype = C.c_int
@@ -223,6 +232,25 @@ class FemBatch:
         out["node_kernel"] = bool(self.L.vfpi_set_tuning(self.h.h, 7, 0))
         if its is not None:
             out["iterations_per_scene"] = its
+        return out
+
+    def run(self, cfg: SolverConfig, steps: int, per_step=False):
+        """``steps`` steps of every scene back to back on the device (``vfpi_fem_run``:
+        contact counts, the fallback and the counters stay on the device, one
+        synchronisation at the end); identical results to ``steps`` calls of
+        ``step``. ``per_step``: also the [steps, scenes] iteration counts and the
+        per-step contact counts."""
+        st = _RunStats()
+        its = np.zeros((steps, self.S), dtype=np.int32) if per_step else None
+        cts = np.zeros(steps, dtype=np.int32) if per_step else None
+        code = self.L.vfpi_fem_run(self.fb, _c_config(cfg), int(steps), C.byref(st),
+                                   ptr(its, _lib._i32p) if its is not None else None,
+                                   ptr(cts, _lib._i32p) if cts is not None else None)
+        _raise_for(code, self.h)
+        out = {f: getattr(st, f) for f, _ in _RunStats._fields_ if f != "reserved"}
+        if per_step:
+            out["iterations_per_step"] = its
+            out["contacts_per_step"] = cts
         return out
 
     def state(self):

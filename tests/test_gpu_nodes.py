@@ -176,3 +176,41 @@ def test_cluster_per_scene_equals_one_cta_per_scene(kw):
         assert np.array_equal(xa, xb) and np.array_equal(va, vb)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(chebyshev=True), dict(step_strategy="fixed-alpha", fixed_alpha=1e3)])
+@pytest.mark.parametrize("cluster", [True, False])
+def test_device_run_equals_step_loop(kw, cluster):
+    """FemBatch.run (vfpi_fem_run: no host round trip per step, the diverged-scene
+    fallback decided on the device) equals the same number of FemBatch.step calls."""
+    from paper_2201_09212_b200 import _lib
+    from paper_2201_09212_b200.fembatch import FemBatch
+    from paper_2201_09212_b200.solver import SolverConfig
+
+    h = _lib.handle()
+    cfg = SolverConfig(residual_tol=1e-8, max_iters=200, **kw)
+    steps = 25
+    try:
+        h.set_node_cluster(cluster)
+        a = FemBatch(_cubes(6, 10, 8))
+        b = FemBatch(_cubes(6, 10, 8))
+    finally:
+        h.set_node_cluster(True)
+    r = a.run(cfg, steps, per_step=True)
+    assert r["host_synced"] == 0
+    its, cts, div = [], [], 0
+    for _ in range(steps):
+        st = b.step(cfg, per_scene=True)
+        its.append(st["iterations_per_scene"])
+        cts.append(st["contacts"])
+        div += st["diverged_scenes"]
+    assert np.array_equal(r["iterations_per_step"], np.array(its))
+    assert np.array_equal(r["contacts_per_step"], np.array(cts)) and sum(cts) > 0
+    assert r["diverged_scene_steps"] == div
+    if kw.get("step_strategy") == "fixed-alpha":
+        assert div > 0
+    xa, va = a.state()
+    xb, vb = b.state()
+    assert np.array_equal(xa, xb) and np.array_equal(va, vb)
+    a.close()
+    b.close()
