@@ -266,14 +266,14 @@ int vfpi_set_kernel(vfpi_handle* h, int mode);
  * phase starts 0..5, globaltimer at 7); vfpi_get_profile copies them out. */
 int vfpi_set_profile(vfpi_handle* h, int iter0);
 int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
-/* Tuning knobs. key 0: force the resident kernel's contact-warp count (0 = auto);
- * key 1: order units by their smallest referenced column (default 1; 0 = row order);
+/* Tuning knobs. key 1: order units by their smallest referenced column (default 1; 0 = row order);
  * key 2: sort each CTA's free rows by decreasing length (default 1);
  * keys 3/4/5: partition cost per entry / row / contact (defaults 24 / 40 / 0; the
  * shared-memory-resident layout uses row cost 20 unless key 4 sets both);
  * key 6: FEM batches use the node-block kernel when a node layout is set
  * (default 1); key 7 (query, value ignored): 1 if the last scene-batch solve
- * ran the node-block kernel. */
+ * ran the node-block kernel; key 8: small FEM batches run one thread-block cluster
+ * per scene (default 1). */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

@@ -60,7 +60,6 @@ struct vfpi_handle {
   int last_resident = 0;
   int kernel_mode = 0;  // 0 auto, 1 force shared-memory resident, 2 force streaming
   int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
-  int tune_wc = 0;      // >0: force the contact-warp count of the resident kernel
   int node_kernel = 1;  // FEM batches: node-block SELL kernel when a node layout is set (tuning key 6)
   int node_cluster = 1; // small FEM batches: one thread-block cluster per scene (tuning key 8; set before the layout)
   int last_node_kernel = 0;
@@ -378,7 +377,6 @@ int vfpi_cg_device(vfpi_handle* h, int64_t n, const int32_t* indptr, const int32
 
 int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (!h) return VFPI_BAD_ARGUMENT;
-  if (key == 0) { h->tune_wc = value; return VFPI_OK; }
   if (key == 1) { h->layout_opt.anchor_order = value != 0; return VFPI_OK; }
   if (key == 2) { h->layout_opt.length_sort = value != 0; return VFPI_OK; }
   if (key == 3 && value > 0) { h->layout_opt.entry_cost = value; return VFPI_OK; }
@@ -567,7 +565,6 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
   p.bar_flags = P<int>(ws.bar_flags);
   p.prof = nullptr;
   p.prof_iter0 = 0;
-  p.tune_wc = h->tune_wc;
   p.diag = P<double>(ws.diag);
   p.fixed_alpha_default = 0;
   p.trace_stride = 0;

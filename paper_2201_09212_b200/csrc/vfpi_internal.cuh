@@ -12,6 +12,7 @@ namespace vfpi {
 constexpr int kThreads = 256;      // threads per CTA of the iteration kernel
 constexpr int kSlotsPerContact = 6;  // rows of a contact unit (3 for S, 6 for D)
 constexpr int kPartialStride = 8;  // doubles per CTA per parity in the partials ring
+constexpr unsigned kSecIdMask = 0x3fffffffu;  // staged-sector entries: id | half marks << 30
 
 // Shared-memory layout of one CTA of the resident iteration kernel: EP SELL-32
 // elements (values + gather map) of its R rows (the first CR belong to its C
@@ -93,7 +94,6 @@ struct IterParams {
   const int* cont_q;        // [n_c] rank of a two-sided contact among its CTA's (row a of side j: 3C + a*CD + rank)
   int* bar_flags;           // [G] epoch flags of the flag barrier
   long long* prof;          // optional [G][4][8] phase timestamps (NULL = off)
-  int tune_wc;              // > 0: force the number of contact warps (tuning aid)
   const double* diag;       // [n] diagonal of A (per-scene fixed-alpha default)
   int fixed_alpha_default;  // fixed-alpha strategy with fixed_alpha = None
   size_t trace_stride;      // scene batches: residual_trace row stride per scene

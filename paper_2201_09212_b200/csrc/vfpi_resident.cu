@@ -132,8 +132,17 @@ __device__ __forceinline__ void warp0_collect(const double* part, int off, int G
 #ifndef VFPI_ROW3_UNROLL
 #define VFPI_ROW3_UNROLL 4
 #endif
+#ifndef VFPI_RES_FREE_START
+#define VFPI_RES_FREE_START 1  // free-row warps start: 0 at once, 1 after the contact-row sweep
+#endif
+// x operand at a byte offset of the CTA's shared memory (the gather maps
+// hold byte offsets, so a gather is one load with no index arithmetic)
+__device__ __forceinline__ double xs_at(const unsigned char* sm, unsigned off) {
+  return *reinterpret_cast<const double*>(sm + off);
+}
+
 __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const unsigned* __restrict__ mp, int base,
-                                          int len, const double* __restrict__ xs) {
+                                          int len, const unsigned char* sm) {
   constexpr int U = VFPI_ROW_UNROLL;
   double acc = 0.0;
   int k = 0;
@@ -142,17 +151,15 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const u
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = base + 32 * (k + u);
-      const unsigned m = mp[i];
       a[u] = sv[i];
-      x[u] = xs[m];
+      x[u] = xs_at(sm, mp[i]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) acc = dadd(acc, dmul(a[u], x[u]));
   }
   for (; k < len; ++k) {
     const int i = base + 32 * k;
-    const unsigned m = mp[i];
-    acc = dadd(acc, dmul(sv[i], xs[m]));
+    acc = dadd(acc, dmul(sv[i], xs_at(sm, mp[i])));
   }
   return acc;
 }
@@ -160,7 +167,7 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ sv, const u
 // three independent row sums at once (one contact side), each in scipy order
 __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const unsigned* __restrict__ mp,
                                          const int* __restrict__ sb, const int* __restrict__ rlen,
-                                         const double* __restrict__ xs, int q0, int q1, int q2, double* out) {
+                                         const unsigned char* sm, int q0, int q1, int q2, double* out) {
   const int qq[3] = {q0, q1, q2};
   int base[3], len[3];
 #pragma unroll
@@ -182,8 +189,7 @@ __device__ __forceinline__ void row_dot3(const double* __restrict__ sv, const un
         const int kk = k + u;
         ok[u][a] = kk < len[a];
         const int i = base[a] + 32 * (ok[u][a] ? kk : 0);
-        const unsigned m = mp[i];
-        pr[u][a] = dmul(sv[i], xs[m]);
+        pr[u][a] = dmul(sv[i], xs_at(sm, mp[i]));
       }
 #pragma unroll
     for (int u = 0; u < VFPI_ROW3_UNROLL; ++u)
@@ -265,6 +271,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
   for (int t = tid; t < 6 * C; t += T) lam_s[t] = 0.0;
   for (int t = tid; t < CR; t += T) jt_s[t] = 0.0;
   __syncthreads();
+  // gather map -> byte offsets of the x operands
+  for (int i = tid; i < EP; i += T) mp[i] = (unsigned)Lo.o_xs + 8u * mp[i];
+  __syncthreads();
 
   // split the warps: [0, WC) run one contact per lane (its rows, the one-shot
   // projection and the scatter), [WC, nw) sweep the free rows
@@ -273,10 +282,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     WC = (C + 31) / 32;
     if (WC > nw - 1 && R > CR) WC = nw - 1;
     if (WC > nw) WC = nw;
-  }
-  if (C > 0 && WC < nw && p.tune_wc > 0) {  // tuning aid: never fewer warps than one lane per contact needs
-    WC = p.tune_wc < nw ? p.tune_wc : nw - 1;
-    if (WC < (C + 31) / 32) WC = (C + 31) / 32 < nw ? (C + 31) / 32 : nw - 1;
   }
   const double u = p.under_relax;
   const double omu = dsub(1.0, u);
@@ -316,10 +321,14 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       if (warp > 0) {
         const unsigned xs_sh = (unsigned)__cvta_generic_to_shared(xs);
         for (int j = tid - 32; j < NS; j += TS) {
-          const double* src = vcur + 4 * (size_t)sec[j];
+          // only the 16-byte halves the CTA's entries read (marks from k_sell_map)
+          const unsigned sj = sec[j];
+          const double* src = vcur + 4 * (size_t)(sj & kSecIdMask);
           const unsigned d = xs_sh + 32u * (unsigned)j;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u), "l"(src + 2) : "memory");
+          if (sj & (1u << 30))
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+          if (sj & (1u << 31))
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u), "l"(src + 2) : "memory");
         }
         // own rows of v^(l-1) (written last iteration) join the x array
         if (l > 1)
@@ -374,8 +383,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         double z = 0.0;
         for (int k = 0; k < rlen[q]; ++k) {
           const int i = base + 32 * k;
-          const unsigned m = mp[i];
-          const int g = (m >= 4u * (unsigned)NS) ? rw[m - 4u * (unsigned)NS] : (int)(4u * sec[m >> 2] + (m & 3u));
+          const unsigned m = (mp[i] - (unsigned)Lo.o_xs) >> 3;
+          const int g = (m >= 4u * (unsigned)NS) ? rw[m - 4u * (unsigned)NS]
+                                                 : (int)(4u * (sec[m >> 2] & kSecIdMask) + (m & 3u));
           z = dadd(z, dmul(sv[i], dsub(vcur[g], vprev[g])));
         }
         const double s = dsub(vown[q], vprev[rw[q]]);
@@ -426,7 +436,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
     };
     // r = A v - b of own row q; force residual of the previous iterate (solver.py:437-439)
     auto residual = [&](int q) {
-      const double r = dsub(row_dot(sv, mp, sb[q >> 5] + (q & 31), rlen[q], xs), bs[q]);
+      const double r = dsub(row_dot(sv, mp, sb[q >> 5] + (q & 31), rlen[q], smraw), bs[q]);
       const double f = (q < CR) ? dsub(r, jt_s[q]) : dsub(r, 0.0);
       fr = dadd(fr, dmul(f, f));
       return r;
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && !dj) break;
           double dot[3];
-          row_dot3(sv, mp, sb, rlen, xs, qs[3 * h], qs[3 * h + 1], qs[3 * h + 2], dot);
+          row_dot3(sv, mp, sb, rlen, smraw, qs[3 * h], qs[3 * h + 1], qs[3 * h + 2], dot);
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             const int q = qs[3 * h + a];
@@ -469,7 +479,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
         }
         // the free-row warps start once every contact's rows are swept (they
         // would otherwise take the issue slots the contact lanes' chains need)
-        if (k0 == warp * 32 && WC < nw) asm volatile("bar.arrive 2, %0;" ::"r"(T) : "memory");
+        if (VFPI_RES_FREE_START == 1 && k0 == warp * 32 && WC < nw) asm volatile("bar.arrive 2, %0;" ::"r"(T) : "memory");
         if (profl) { __syncwarp(); if (lane == 0) atomicMax(&sm_role_end[2], (unsigned long long)clock64()); }
         if (!act || !HASC || check_only) continue;
         // (2) gather + (3) one-shot projection (solver.py:262-281)
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_iterate_res(IterParams p) {
       }
       if (profl && lane == 0) atomicMax(&sm_role_end[0], (unsigned long long)clock64());
     }
-    if (warp >= WC && WC > 0 && WC < nw) asm volatile("bar.sync 2, %0;" ::"r"(T) : "memory");
+    if (VFPI_RES_FREE_START == 1 && warp >= WC && WC > 0 && WC < nw) asm volatile("bar.sync 2, %0;" ::"r"(T) : "memory");
     if (warp >= WC || WC == nw) {
       // ---- free rows: v_new = v* (+ w * 0 when contacts exist) ------------
       const int t0 = (WC == nw) ? tid : tid - WC * 32;

@@ -477,8 +477,9 @@ constexpr int kMapSmemSectors = 8192;
 __global__ void __launch_bounds__(1024) k_sell_map(int G, const int* __restrict__ blk_slice,
                                                   const int* __restrict__ blk_row, const int64_t* __restrict__ slice_off,
                                                   const int* __restrict__ sell_col, const int* __restrict__ rowpos,
-                                                  const unsigned* __restrict__ secs, const int* __restrict__ sec_ptr,
+                                                  const unsigned* secs, const int* __restrict__ sec_ptr,
                                                   unsigned* __restrict__ map) {
+  unsigned* secs_w = const_cast<unsigned*>(secs);
   __shared__ unsigned ssec[kMapSmemSectors];
   const int b = blockIdx.x;
   const int p0 = blk_row[b], p1 = blk_row[b + 1];
@@ -499,12 +500,14 @@ __global__ void __launch_bounds__(1024) k_sell_map(int G, const int* __restrict_
         m = 4u * (unsigned)ns + (unsigned)(pc - p0);  // own rows follow the staged sectors
       } else {
         const unsigned sec = (unsigned)c >> 2;
-        int lo = 0, hi = ns;  // first sector >= sec
+        int lo = 0, hi = ns;  // first sector >= sec (bits 30/31 are the half marks set below)
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          if (sl[mid] < sec) lo = mid + 1; else hi = mid;
+          if ((sl[mid] & kSecIdMask) < sec) lo = mid + 1; else hi = mid;
         }
         m = 4u * (unsigned)lo + ((unsigned)c & 3u);
+        // the kernel stages only the 16-byte halves of a sector its entries read
+        atomicOr(secs_w + u0 + lo, 1u << (30 + (((unsigned)c & 3u) >> 1)));
       }
     }
     map[i] = m;

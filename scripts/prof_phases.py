@@ -50,8 +50,3 @@ for b_ in (0, 20, 40, 55, 60, 61, 62, 63, 64, 80, 100, 147):
 arr = a[:, :, 7]
 print("arrival skew (globaltimer ns) per iteration:", (arr.max(0) - arr.min(0)).tolist())
 h.L.vfpi_set_profile(h.h, 0)
-for wc in (2, 4, 6, 8, 10, 12, 14):
-    h.L.vfpi_set_tuning(h.h, 0, wc)
-    v, lam, rep = solve_packed(ps, cfg, np.zeros(ps.n))
-    print(f"WC={wc:2d} loop_ms {rep.timings['loop_s'] * 1e3:.3f}")
-h.L.vfpi_set_tuning(h.h, 0, 0)
