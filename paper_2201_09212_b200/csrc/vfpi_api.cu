@@ -62,6 +62,7 @@ struct vfpi_handle {
   int prof_iter0 = 0;   // >0: record phase timestamps of iterations prof_iter0..+3
   int node_kernel = 1;  // FEM batches: node-block SELL kernel when a node layout is set (tuning key 6)
   int node_cluster = 1; // small FEM batches: one thread-block cluster per scene (tuning key 8; set before the layout)
+  int node_cluster_force = 0;  // > 0: CTAs per scene of FEM batches created afterwards (tuning key 9)
   int last_node_kernel = 0;
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
@@ -388,6 +389,10 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (key == 6) { h->node_kernel = value != 0; return VFPI_OK; }
   if (key == 7) return h->last_node_kernel;  // query: did the last scene solve use the node-block kernel
   if (key == 8) { h->node_cluster = value != 0; return VFPI_OK; }
+  if (key == 9 && (value == 0 || value == 1 || value == 2 || value == 4 || value == 8)) {
+    h->node_cluster_force = value;
+    return VFPI_OK;
+  }
   return VFPI_BAD_ARGUMENT;
 }
 
@@ -827,6 +832,10 @@ int vfpi_scenes_core(vfpi_handle* h, const vfpi_system& d, int S, const int32_t*
     ++h->launches;
     CK(cudaEventRecord(ws.ev[1], st));  // the loop timing covers the iteration kernel only
     rc = vfpi::launch_iterate_nodes(p, *nodes, cfg->op, cheb, std::max(max_ct, 1), st, h->err, nmode);
+    if (rc == VFPI_OK && nodes->scene_perm) {  // next solve: longest predicted scenes first
+      vfpi::launch_scene_order(S, P<vfpi::SolveStatus>(ws.status), const_cast<int*>(nodes->scene_perm), st);
+      ++h->launches;
+    }
   } else {
     rc = vfpi::launch_iterate_scenes(p, cfg->op, cheb, bb, smem, st, h->err);
   }
@@ -1558,6 +1567,10 @@ int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi
     rc = vfpi::launch_iterate_nodes(p, fb->nbd, cfg->op, cheb, 1, st, h->err, nmode);
     if (rc) return rc;
     CK(cudaEventRecord(fb->run_ev[3 + 2 * k], st));
+    if (fb->nbd.scene_perm) {  // next step: longest predicted scenes first
+      vfpi::launch_scene_order(S, P<vfpi::SolveStatus>(ws.status), const_cast<int*>(fb->nbd.scene_perm), st);
+      ++h->launches;
+    }
     // (3b) diverged scenes: the flagged contact-free CG step, decided on the device
     const int64_t ns = 3 * (int64_t)fb->Nn;
     if (vfpi::launch_cg_scenes_status(S, ns, fb->A.indptr, fb->A.indices, fb->A.data, P<double>(fb->b),
@@ -1641,7 +1654,8 @@ int vfpi_fem_set_node_layout(vfpi_fem_batch* fb, int32_t nodes_per_scene, const 
   CK(vfpi::ensure(h->ws.flags, 16));
   CK(cudaMemsetAsync(h->ws.flags.p, 0, 16, st));
   L.t_off_host.assign(slice_off, slice_off + n_slices + 1);
-  const int cl = h->node_cluster ? vfpi::node_cluster_size(fb->S, n_slices, h->ws.num_sms) : 1;
+  int cl = h->node_cluster ? vfpi::node_cluster_size(fb->S, n_slices, h->ws.num_sms) : 1;
+  if (h->node_cluster_force > 0) cl = std::min(h->node_cluster_force, std::max(1, n_slices / 2));
   if (vfpi::node_layout_build(L, fb->S, fb->A.indptr, fb->A.indices, fb->A.data, fb->nbd, (int*)h->ws.flags.p, st,
                               cl, L.t_off_host)) {
     h->err = "node layout build failed";
@@ -1699,7 +1713,7 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
                             &fb->cg_p, &fb->cg_q, &fb->cg_list, &fb->x0, &fb->v0, &fb->nbh.t_order,
                             &fb->nbh.t_off, &fb->nbh.t_bcol, &fb->nbh.desc, &fb->nbh.val, &fb->nbh.slice_off,
                             &fb->nbh.node_list, &fb->nbh.node_slot, &fb->nbh.blk_slice, &fb->nbh.blk_pos, &fb->nbh.vs,
-                            &fb->nbh.jt, &fb->run_acc, &fb->run_its, &fb->run_cts})
+                            &fb->nbh.jt, &fb->nbh.perm, &fb->run_acc, &fb->run_its, &fb->run_cts})
     if (b->p) cudaFree(b->p);
   for (cudaEvent_t e : fb->run_ev) cudaEventDestroy(e);
   if (fb->e0) cudaEventDestroy(fb->e0);

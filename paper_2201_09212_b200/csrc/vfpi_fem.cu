@@ -227,6 +227,25 @@ __global__ void k_fem_run_stats(int S, const SolveStatus* __restrict__ st, const
   }
 }
 
+__global__ void __launch_bounds__(1024) k_scene_order(int S, const SolveStatus* __restrict__ st, int* __restrict__ perm) {
+  __shared__ int its[kMaxOrderedScenes];
+  for (int s = threadIdx.x; s < S; s += blockDim.x) its[s] = st[s].iterations;
+  __syncthreads();
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    const int a = its[i];
+    int r = 0;
+    for (int j = 0; j < S; ++j) {
+      const int c = its[j];
+      r += (c > a) || (c == a && j < i);
+    }
+    perm[r] = i;
+  }
+}
+
+void launch_scene_order(int S, const SolveStatus* st, int* perm, cudaStream_t stream) {
+  if (S > 0 && S <= kMaxOrderedScenes) k_scene_order<<<1, 1024, 0, stream>>>(S, st, perm);
+}
+
 __global__ void k_iota_int(int n, int* v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = i;

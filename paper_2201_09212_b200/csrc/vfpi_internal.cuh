@@ -387,6 +387,12 @@ int launch_cg_scenes_status(int S, int64_t rows_per_scene, const int32_t* indptr
                             double rtol, int64_t maxiter, const SolveStatus* status, const int* cts, double* lam,
                             cudaStream_t st);
 int cg_grid_partials(int device);
+// scene batches: perm = scenes by decreasing iteration count of their last
+// solve (ties by index), so the CTAs the block scheduler dispatches first run
+// the scenes predicted to take longest (counts change by < 1 per step)
+void launch_scene_order(int S, const SolveStatus* st, int* perm, cudaStream_t stream);
+constexpr int kMaxOrderedScenes = 2048;
+
 int launch_cg_grid(int G, int64_t n, const int32_t* indptr, const int32_t* indices, const double* data,
                    const double* b, double* x, double* r, double* p, double* q, double* partial, double rtol,
                    int64_t maxiter, int32_t* iters_out, cudaStream_t st);
@@ -405,11 +411,12 @@ struct NodeLayoutDev {
   const int64_t* slice_off = nullptr;  // [S*nsl+1] k-step offset of every slice
   const unsigned* desc = nullptr;      // [k][lane]: block column | mask << 23
   const double* val = nullptr;         // [k][9][lane]
+  const int* scene_perm = nullptr;     // scene batches: CTA (cluster) c runs scene scene_perm[c] (longest first)
 };
 struct NodeLayoutHost {
   int nn = 0, nsl = 0;
   int64_t k_scene = 0;                 // k-steps per scene
-  Workspace::Buf t_order, t_off, t_bcol, desc, val, slice_off, node_list, node_slot, blk_slice, blk_pos, vs, jt;
+  Workspace::Buf t_order, t_off, t_bcol, desc, val, slice_off, node_list, node_slot, blk_slice, blk_pos, vs, jt, perm;
   std::vector<int64_t> t_off_host;
 };
 struct NodeGridWork {  // single-system node-block layout (rebuilt per solve)

@@ -277,10 +277,13 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   // and the kernel's shared memory does not depend on the contact count
   constexpr bool GRID = MODE == kGrid, CLUSTER = MODE == kCluster, SHARED_C = false;
   __shared__ double sm_cpart[2][4];  // cluster mode: this CTA's partials, by iteration parity
-  const int b = blockIdx.x;
   const int crank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
   const int csize = CLUSTER ? (int)cg::this_cluster().num_blocks() : 1;
-  const int scene = CLUSTER ? b / csize : b;
+  // scene batches: CTA / cluster c runs scene scene_perm[c] (longest predicted
+  // first); b = the layout's CTA index of this CTA's share of that scene
+  const int cid = CLUSTER ? (int)blockIdx.x / csize : (int)blockIdx.x;
+  const int scene = (!GRID && L.scene_perm) ? __ldg(L.scene_perm + cid) : cid;
+  const int b = CLUSTER ? scene * csize + crank : (GRID ? (int)blockIdx.x : scene);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int np0 = L.blk_pos[b], np1 = L.blk_pos[b + 1];      // node positions of the CTA
   const int s0 = L.blk_slice[b], s1 = L.blk_slice[b + 1];    // node slices of the CTA
@@ -628,6 +631,11 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
 }
 
 // ---- layout construction ---------------------------------------------------
+__global__ void k_nb_iota(int n, int* v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
 
 // per (scene, node position): gather the node's 3 rows (CSC columns of the
 // symmetric A) into its template block slots: values + 9-bit masks
@@ -835,7 +843,8 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
       ensure(h.slice_off, 8 * ((size_t)S * nsl + 1)) || ensure(h.node_list, 4 * (size_t)S * nn) ||
       ensure(h.node_slot, 4 * (size_t)S * nn) || ensure(h.blk_slice, 4 * (G + 1)) || ensure(h.blk_pos, 4 * (G + 1)))
     return 1;
-  if (ensure(h.vs, 8 * kSlotsPerContact * (size_t)S * nn) || ensure(h.jt, 8 * kSlotsPerContact * (size_t)S * nn))
+  if (ensure(h.vs, 8 * kSlotsPerContact * (size_t)S * nn) || ensure(h.jt, 8 * kSlotsPerContact * (size_t)S * nn) ||
+      ensure(h.perm, 4 * (size_t)std::max(S, 1)))
     return 1;
   // padding lanes (positions past the scene's last node) are never filled:
   // their descriptors must read as empty
@@ -887,7 +896,10 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   out.val = (const double*)h.val.p;
   out.vs_g = (double*)h.vs.p;
   out.jt_g = (double*)h.jt.p;
-  return 0;
+  // scene order: identity until the first solve's counts are known
+  k_nb_iota<<<nblk(S), 256, 0, st>>>(S, (int*)h.perm.p);
+  out.scene_perm = S <= kMaxOrderedScenes ? (const int*)h.perm.p : nullptr;
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_nc,
@@ -1035,9 +1047,13 @@ int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bo
   return VFPI_OK;
 }
 
+// CTAs per scene: the smallest power of two that gives the batch >= 1.5 waves
+// of the GPU's 2 CTAs per SM (with the longest-first scene order the block
+// scheduler then balances scenes of unequal iteration counts), at most 8 and
+// at most one CTA per two node slices
 int node_cluster_size(int S, int nsl, int num_sms) {
   int cl = 1;
-  while (cl < 8 && (int64_t)S * cl * 2 <= 2LL * num_sms && cl * 2 <= nsl) cl *= 2;
+  while (cl < 8 && (int64_t)S * cl < 3LL * num_sms && cl * 2 <= nsl) cl *= 2;
   return cl;
 }
 

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--ns", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--cluster", type=int, default=0, help="force CTAs per scene (tuning key 9; 0 = automatic)")
     a = ap.parse_args()
     import torch
 
@@ -34,6 +35,8 @@ def main():
 
     cfg = SolverConfig(operator="strict", residual_tol=bench.TOL, max_iters=bench.MAX_ITERS, chebyshev=False)
     h = _lib.handle(0)
+    if a.cluster:
+        h.L.vfpi_set_tuning(h.h, 9, a.cluster)
     stream = h.torch_stream()
     base = None
     for n in a.ns:
