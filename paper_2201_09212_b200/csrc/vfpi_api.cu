@@ -1164,10 +1164,25 @@ struct vfpi_fem_batch {
   vfpi::NodeLayoutHost nbh;                        // node-block SELL layout (vfpi_fem_set_node_layout)
   vfpi::NodeLayoutDev nbd;
   bool nb_ready = false;
+  Workspace::Buf kn_desc, kn_val;  // K on the node-block template (right-hand side)
+  bool kn_ready = false;
   uint64_t layout_epoch = ~0ull;  // the handle workspace holds our contact-free layout
 };
 
 namespace {
+
+// (1) of a FEM step: b = ((2/dt) m) v - K (x - X) + m g, K streamed as node
+// blocks when the batch has its node layout, else as row SELL-32
+void fem_rhs(vfpi_fem_batch* fb, double twodt, cudaStream_t st) {
+  if (fb->nb_ready && fb->kn_ready)
+    vfpi::launch_fem_rhs_nodes(fb->S, fb->Nn, fb->nbd.nsl, fb->nbd.slice_off, fb->nbd.node_list,
+                               P<unsigned>(fb->kn_desc), P<double>(fb->kn_val), P<double>(fb->x), P<double>(fb->X),
+                               P<double>(fb->v), P<double>(fb->m), P<double>(fb->g), twodt, P<double>(fb->b), st);
+  else
+    vfpi::launch_fem_rhs_sell(fb->n, P<int64_t>(fb->ks_off), P<double>(fb->ks_val), P<int>(fb->ks_col),
+                              P<double>(fb->x), P<double>(fb->X), P<double>(fb->v), P<double>(fb->m), P<double>(fb->g),
+                              twodt, P<double>(fb->b), st);
+}
 
 int fem_upload(vfpi_handle* h, Workspace::Buf& b, const void* src, size_t bytes) {
   CK(vfpi::ensure(b, std::max<size_t>(bytes, 8)));
@@ -1319,9 +1334,7 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   const vfpi_fem_params& q = fb->prm;
   CK(cudaEventRecord(fb->e0, st));
   // (1) right-hand side of every scene
-  vfpi::launch_fem_rhs_sell(fb->n, P<int64_t>(fb->ks_off), P<double>(fb->ks_val), P<int>(fb->ks_col),
-                            P<double>(fb->x), P<double>(fb->X), P<double>(fb->v), P<double>(fb->m), P<double>(fb->g),
-                            2.0 / q.dt, P<double>(fb->b), st);
+  fem_rhs(fb, 2.0 / q.dt, st);
   // (2) node-plane contacts: flags, scene-ordered compaction, parameters
   vfpi::launch_fem_flags(fb->nodes, P<double>(fb->x), q.margin, P<int>(fb->flag), st);
   size_t tb = fb->tmp.cap;
@@ -1539,9 +1552,7 @@ int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi
   CK(cudaEventRecord(fb->run_ev[0], st));
   for (int k = 0; k < steps; ++k) {
     // (1) right-hand side, (2) node-plane contacts (as vfpi_fem_step)
-    vfpi::launch_fem_rhs_sell(fb->n, P<int64_t>(fb->ks_off), P<double>(fb->ks_val), P<int>(fb->ks_col),
-                              P<double>(fb->x), P<double>(fb->X), P<double>(fb->v), P<double>(fb->m),
-                              P<double>(fb->g), 2.0 / q.dt, P<double>(fb->b), st);
+    fem_rhs(fb, 2.0 / q.dt, st);
     vfpi::launch_fem_flags(fb->nodes, P<double>(fb->x), q.margin, P<int>(fb->flag), st);
     size_t tb = fb->tmp.cap;
     CK(cub::DeviceScan::ExclusiveSum(fb->tmp.p, tb, P<int>(fb->flag), P<int>(fb->pos), (int)fb->nodes, st));
@@ -1671,6 +1682,15 @@ int vfpi_fem_set_node_layout(vfpi_fem_batch* fb, int32_t nodes_per_scene, const 
     return VFPI_UNSUPPORTED;
   }
   fb->nb_ready = true;
+  // K on the same template: the right-hand side streams node blocks too
+  CK(cudaMemsetAsync(h->ws.flags.p, 0, 16, st));
+  fb->kn_ready = false;
+  if (vfpi::node_fill_matrix(L, fb->S, P<int64_t>(fb->krp), P<int>(fb->kc), P<double>(fb->kv), fb->kn_desc, fb->kn_val,
+                             (int*)h->ws.flags.p, st) == 0) {
+    CK(cudaMemcpyAsync(&flag, h->ws.flags.p, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fb->kn_ready = flag == 0;
+  }
   return VFPI_OK;
 }
 

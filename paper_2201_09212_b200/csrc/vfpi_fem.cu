@@ -92,6 +92,57 @@ __global__ void k_fem_rhs_sell(int64_t n, const int64_t* __restrict__ off, const
   b[i] = dadd(dsub(t1, ku), dmul(mi, gi));
 }
 
+// The same right-hand side with K in the node-block layout of the batch (one
+// warp per node slice, one lane per node: 3 row sums per lane, blocks in
+// increasing block column, entries of a block in increasing column -- each
+// row's sequence of k_fem_rhs; the masks keep K's explicit zeros)
+__global__ void __launch_bounds__(256) k_fem_rhs_nodes(int64_t nslices, int nn, int nsl,
+                                                       const int64_t* __restrict__ slice_off,
+                                                       const int* __restrict__ node_list,
+                                                       const unsigned* __restrict__ kdesc,
+                                                       const double* __restrict__ kval, const double* __restrict__ x,
+                                                       const double* __restrict__ X, const double* __restrict__ v,
+                                                       const double* __restrict__ m, const double* __restrict__ g,
+                                                       double twodt, double* __restrict__ b) {
+  const int64_t gs = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gs >= nslices) return;
+  const int scene = (int)(gs / nsl), sl = (int)(gs % nsl);
+  const int p = sl * 32 + lane;
+  const int64_t off = slice_off[gs];
+  const int W = (int)(slice_off[gs + 1] - off);
+  const bool live = p < nn;
+  const int node = live ? node_list[(int64_t)scene * nn + p] : 0;
+  double k0 = 0.0, k1 = 0.0, k2 = 0.0;
+  for (int k = 0; k < W; ++k) {
+    const unsigned d = __ldcs(kdesc + (off + k) * 32 + lane);
+    const unsigned mk = d >> 23;
+    if (mk) {
+      const int c = 3 * (int)(d & ((1u << 23) - 1u));
+      const double u0 = dsub(x[c], X[c]), u1 = dsub(x[c + 1], X[c + 1]), u2 = dsub(x[c + 2], X[c + 2]);
+      const double* kv = kval + (off + k) * (9 * 32) + lane;
+      if (mk & 0x001) k0 = dadd(k0, dmul(__ldcs(kv + 32 * 0), u0));
+      if (mk & 0x002) k0 = dadd(k0, dmul(__ldcs(kv + 32 * 1), u1));
+      if (mk & 0x004) k0 = dadd(k0, dmul(__ldcs(kv + 32 * 2), u2));
+      if (mk & 0x008) k1 = dadd(k1, dmul(__ldcs(kv + 32 * 3), u0));
+      if (mk & 0x010) k1 = dadd(k1, dmul(__ldcs(kv + 32 * 4), u1));
+      if (mk & 0x020) k1 = dadd(k1, dmul(__ldcs(kv + 32 * 5), u2));
+      if (mk & 0x040) k2 = dadd(k2, dmul(__ldcs(kv + 32 * 6), u0));
+      if (mk & 0x080) k2 = dadd(k2, dmul(__ldcs(kv + 32 * 7), u1));
+      if (mk & 0x100) k2 = dadd(k2, dmul(__ldcs(kv + 32 * 8), u2));
+    }
+  }
+  if (!live) return;
+  const double ku[3] = {k0, k1, k2};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int64_t i = 3 * (int64_t)node + q;
+    const double mi = m[i];
+    const double t1 = dmul(dmul(twodt, mi), v[i]);
+    b[i] = dadd(dsub(t1, ku[q]), dmul(mi, g[i]));
+  }
+}
+
 // node below the margin of the plane z = 0 (FemCube.contacts)
 __global__ void k_fem_flags(int64_t nodes, const double* __restrict__ x, double margin, int* __restrict__ flag) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -240,6 +291,16 @@ __global__ void __launch_bounds__(1024) k_scene_order(int S, const SolveStatus* 
     }
     perm[r] = i;
   }
+}
+
+void launch_fem_rhs_nodes(int S, int nn, int nsl, const int64_t* slice_off, const int* node_list,
+                          const unsigned* kdesc, const double* kval, const double* x, const double* X,
+                          const double* v, const double* m, const double* g, double twodt, double* b,
+                          cudaStream_t st) {
+  const int64_t ns = (int64_t)S * nsl;
+  if (ns > 0)
+    k_fem_rhs_nodes<<<(unsigned)((ns + 7) / 8), 256, 0, st>>>(ns, nn, nsl, slice_off, node_list, kdesc, kval, x, X, v,
+                                                            m, g, twodt, b);
 }
 
 void launch_scene_order(int S, const SolveStatus* st, int* perm, cudaStream_t stream) {

@@ -432,6 +432,16 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
                       NodeLayoutDev& out, int* d_flags, cudaStream_t st, int cluster,
                       const std::vector<int64_t>& t_off_host);
 int node_cluster_size(int S, int nsl, int num_sms);  // CTAs per scene so a small batch fills the GPU
+// a second matrix on the same node-block template (FEM batches: K for the
+// right-hand side), every stored entry kept (explicit zeros included)
+int node_fill_matrix(const NodeLayoutHost& h, int S, const int64_t* d_ptr, const int* d_idx, const double* d_val,
+                     Workspace::Buf& desc, Workspace::Buf& val, int* d_flags, cudaStream_t st);
+// b = ((2/dt) m) v - K (x - X) + m g with K in the node-block layout
+// (slice_off / node_list of the batch's A layout, desc / val of K)
+void launch_fem_rhs_nodes(int S, int nn, int nsl, const int64_t* slice_off, const int* node_list,
+                          const unsigned* kdesc, const double* kval, const double* x, const double* X,
+                          const double* v, const double* m, const double* g, double twodt, double* b,
+                          cudaStream_t st);
 int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_nc,
                        cudaStream_t st);
 int node_kernel_smem(int max_ct);

@@ -639,9 +639,10 @@ __global__ void k_nb_iota(int n, int* v) {
 
 // per (scene, node position): gather the node's 3 rows (CSC columns of the
 // symmetric A) into its template block slots: values + 9-bit masks
+template <class PT>
 __global__ void k_nb_fill(int S, int nn, int nsl, const int* __restrict__ t_order,
                           const int64_t* __restrict__ t_off, const int* __restrict__ t_bcol,
-                          const int* __restrict__ a_ptr, const int* __restrict__ a_idx, const double* __restrict__ a_val,
+                          const PT* __restrict__ a_ptr, const int* __restrict__ a_idx, const double* __restrict__ a_val,
                           int64_t k_scene, unsigned* __restrict__ desc, double* __restrict__ val,
                           int* __restrict__ flags) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -658,7 +659,7 @@ __global__ void k_nb_fill(int S, int nn, int nsl, const int* __restrict__ t_orde
   for (int p = 0; p < 3; ++p) {
     const int r = 3 * node + p;
     int k = 0;
-    for (int e = a_ptr[r]; e < a_ptr[r + 1]; ++e) {
+    for (PT e = a_ptr[r]; e < a_ptr[r + 1]; ++e) {
       const int j = a_idx[e];
       const int lb = j / 3 - s * nn;
       while (k < W && t_bcol[toff * 32 + 32 * k + lane] != lb) ++k;
@@ -879,7 +880,7 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
       return 1;
   }
   const int64_t nf = (int64_t)S * nn;
-  k_nb_fill<<<nblk(nf, 128), 128, 0, st>>>(S, nn, nsl, (const int*)h.t_order.p, (const int64_t*)h.t_off.p,
+  k_nb_fill<int><<<nblk(nf, 128), 128, 0, st>>>(S, nn, nsl, (const int*)h.t_order.p, (const int64_t*)h.t_off.p,
                                            (const int*)h.t_bcol.p, d_a_ptr, d_a_idx, d_a_val, ks, (unsigned*)h.desc.p,
                                            (double*)h.val.p, d_flags);
   if (cudaGetLastError() != cudaSuccess) return 1;
@@ -899,6 +900,21 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   // scene order: identity until the first solve's counts are known
   k_nb_iota<<<nblk(S), 256, 0, st>>>(S, (int*)h.perm.p);
   out.scene_perm = S <= kMaxOrderedScenes ? (const int*)h.perm.p : nullptr;
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int node_fill_matrix(const NodeLayoutHost& h, int S, const int64_t* d_ptr, const int* d_idx, const double* d_val,
+                     Workspace::Buf& desc, Workspace::Buf& val, int* d_flags, cudaStream_t st) {
+  const int64_t ks = h.k_scene;
+  if (ensure(desc, 4 * 32 * (size_t)std::max<int64_t>(S * ks, 1)) ||
+      ensure(val, 8 * 9 * 32 * (size_t)std::max<int64_t>(S * ks, 1)))
+    return 1;
+  if (cudaMemsetAsync(val.p, 0, 8 * 9 * 32 * (size_t)S * ks, st) || cudaMemsetAsync(desc.p, 0, 4 * 32 * (size_t)S * ks, st))
+    return 1;
+  const int64_t nf = (int64_t)S * h.nn;
+  k_nb_fill<int64_t><<<nblk(nf, 128), 128, 0, st>>>(S, h.nn, h.nsl, (const int*)h.t_order.p, (const int64_t*)h.t_off.p,
+                                                    (const int*)h.t_bcol.p, d_ptr, d_idx, d_val, ks, (unsigned*)desc.p,
+                                                    (double*)val.p, d_flags);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
