@@ -37,6 +37,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--scenes", type=int, default=1)
+    ap.add_argument("--first-scene", type=int, default=0,
+                    help="seed of the first variant (e.g. 224 with --scenes 32: the share of rank 7 of 8 of the 256)")
     ap.add_argument("--max-iters", type=int, default=500)
     ap.add_argument("--nodes", type=int, default=16)
     ap.add_argument("--cubes", type=int, nargs=3, default=[8, 8, 4])
@@ -69,8 +71,8 @@ def main():
     last = {}
 
     def make_pile(sc):
-        return CubePile(*a.cubes, nodes=a.nodes, gap=0.005, jitter=0.002, gap_z=0.0005, jitter_z=0.0, seed=sc,
-                        k_v=a.kv)
+        return CubePile(*a.cubes, nodes=a.nodes, gap=0.005, jitter=0.002, gap_z=0.0005, jitter_z=0.0,
+                        seed=a.first_scene + sc, k_v=a.kv)
 
     def stepper(pile):
         last["st"] = PileStepper(pile, device=dev)
@@ -106,7 +108,7 @@ def main():
                "scenes": a.scenes, "n_gpus": world, "steps_per_scene": a.steps, "n_orig": last.pile.n,
                "nnz_A_o": int(last.pile.a_data.shape[0]), "dt": last.pile.dt, "mu": last.pile.mu, "k_v": last.pile.k_v,
                "tol": cfg.residual_tol, "max_iters": cfg.max_iters, "operator": "strict", "chebyshev": a.chebyshev,
-               "seeds": "scene k uses default_rng(k) for its jitter", "gap_m": 0.005, "gap_z_m": 0.0005,
+               "seeds": f"scene k uses default_rng(k) for its jitter, k = {a.first_scene} .. {a.first_scene + a.scenes - 1}", "gap_m": 0.005, "gap_z_m": 0.0005,
                "jitter_m": 0.002,
                "wall_s": wall, "scene_steps_per_s": totals["steps"] / wall,
                "contact_iter_per_s": totals["contact_iterations"] / wall,
