@@ -1235,7 +1235,7 @@ int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a,
   // contact arrays sized for every node in contact
   if (vfpi::ensure(fb->lam, 24 * nodes) || vfpi::ensure(fb->ci, 4 * nodes) || vfpi::ensure(fb->cj, 4 * nodes) ||
       vfpi::ensure(fb->frames, 72 * nodes) || vfpi::ensure(fb->mu, 8 * nodes) || vfpi::ensure(fb->mu2, 8 * nodes) ||
-      vfpi::ensure(fb->phi, 8 * nodes) || vfpi::ensure(fb->flag, 4 * nodes) || vfpi::ensure(fb->pos, 4 * nodes) ||
+      vfpi::ensure(fb->phi, 8 * nodes) || vfpi::ensure(fb->pos, 4 * nodes) ||
       vfpi::ensure(fb->cts, 4 * (size_t)(S + 1)))
     return fail(VFPI_CUDA_ERROR);
   std::vector<int32_t> rows((size_t)S + 1);
@@ -1243,9 +1243,8 @@ int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a,
   if ((rc = fem_upload(h, fb->rows, rows.data(), 4 * (size_t)(S + 1)))) return fail(rc);
   std::vector<int32_t> zeros((size_t)S + 1, 0);
   if ((rc = fem_upload(h, fb->zero_cts, zeros.data(), 4 * (size_t)(S + 1)))) return fail(rc);
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, (int*)fb->flag.p, (int*)fb->pos.p, (int)nodes);
-  if (vfpi::ensure(fb->tmp, tb)) return fail(VFPI_CUDA_ERROR);
+  const size_t tb = vfpi::fem_detect_tmp_bytes((int64_t)nodes);
+  if (vfpi::ensure(fb->tmp, std::max<size_t>(tb, 16))) return fail(VFPI_CUDA_ERROR);
   {  // K -> SELL-32 once (coalesced right-hand-side sums)
     const int64_t nsl = ((int64_t)n + 31) / 32;
     if (vfpi::ensure(fb->ks_off, 8 * (size_t)(nsl + 1))) return fail(VFPI_CUDA_ERROR);
@@ -1336,15 +1335,15 @@ int vfpi_fem_step(vfpi_fem_batch* fb, const vfpi_config* cfg, vfpi_fem_step_stat
   // (1) right-hand side of every scene
   fem_rhs(fb, 2.0 / q.dt, st);
   // (2) node-plane contacts: flags, scene-ordered compaction, parameters
-  vfpi::launch_fem_flags(fb->nodes, P<double>(fb->x), q.margin, P<int>(fb->flag), st);
-  size_t tb = fb->tmp.cap;
-  CK(cub::DeviceScan::ExclusiveSum(fb->tmp.p, tb, P<int>(fb->flag), P<int>(fb->pos), (int)fb->nodes, st));
-  vfpi::launch_fem_scene_cts(fb->S, fb->Nn, P<int>(fb->flag), P<int>(fb->pos), P<int>(fb->cts), st);
-  vfpi::launch_fem_contacts(fb->nodes, P<int>(fb->flag), P<int>(fb->pos), P<double>(fb->x), P<double>(fb->v),
-                            P<double>(fb->frame), q.mu, -(q.beta_err / q.dt), q.e_rest, q.rest_threshold,
-                            P<int>(fb->ci), P<int>(fb->cj), P<double>(fb->frames), P<double>(fb->mu),
-                            P<double>(fb->mu2), P<double>(fb->phi), st);
-  h->launches += 6;  // rhs, flags, scan (init + pass), scene pointers, contacts
+  if (vfpi::launch_fem_detect(fb->nodes, fb->S, fb->Nn, P<double>(fb->x), P<double>(fb->v), q.margin, fb->tmp.p,
+                              fb->tmp.cap, P<int>(fb->pos), P<int>(fb->cts), P<double>(fb->frame), q.mu,
+                              -(q.beta_err / q.dt), q.e_rest, q.rest_threshold, P<int>(fb->ci), P<int>(fb->cj),
+                              P<double>(fb->frames), P<double>(fb->mu), P<double>(fb->mu2), P<double>(fb->phi),
+                              nullptr, nullptr, st)) {
+    h->err = "node-plane detection launch failed";
+    return VFPI_CUDA_ERROR;
+  }
+  h->launches += 4;  // rhs, scan (init + pass), detection
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(fb->h_cts.data(), fb->cts.p, 4 * (size_t)(fb->S + 1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1553,22 +1552,22 @@ int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi
   for (int k = 0; k < steps; ++k) {
     // (1) right-hand side, (2) node-plane contacts (as vfpi_fem_step)
     fem_rhs(fb, 2.0 / q.dt, st);
-    vfpi::launch_fem_flags(fb->nodes, P<double>(fb->x), q.margin, P<int>(fb->flag), st);
-    size_t tb = fb->tmp.cap;
-    CK(cub::DeviceScan::ExclusiveSum(fb->tmp.p, tb, P<int>(fb->flag), P<int>(fb->pos), (int)fb->nodes, st));
-    vfpi::launch_fem_scene_cts(S, fb->Nn, P<int>(fb->flag), P<int>(fb->pos), P<int>(fb->cts), st);
-    vfpi::launch_fem_contacts(fb->nodes, P<int>(fb->flag), P<int>(fb->pos), P<double>(fb->x), P<double>(fb->v),
-                              P<double>(fb->frame), q.mu, -(q.beta_err / q.dt), q.e_rest, q.rest_threshold,
-                              P<int>(fb->ci), P<int>(fb->cj), P<double>(fb->frames), P<double>(fb->mu),
-                              P<double>(fb->mu2), P<double>(fb->phi), st);
+    if (vfpi::launch_fem_detect(fb->nodes, S, fb->Nn, P<double>(fb->x), P<double>(fb->v), q.margin, fb->tmp.p,
+                                fb->tmp.cap, P<int>(fb->pos), P<int>(fb->cts), P<double>(fb->frame), q.mu,
+                                -(q.beta_err / q.dt), q.e_rest, q.rest_threshold, P<int>(fb->ci), P<int>(fb->cj),
+                                P<double>(fb->frames), P<double>(fb->mu), P<double>(fb->mu2), P<double>(fb->phi),
+                                lb, lb + 3 * (size_t)ncmax, st)) {
+      h->err = "node-plane detection launch failed";
+      return VFPI_CUDA_ERROR;
+    }
     // (3) W, gamma and the solve of every scene (counts read on the device)
     CK(cudaMemcpyAsync(ws.blk_ct.p, fb->cts.p, 4 * ((size_t)S + 1), cudaMemcpyDeviceToDevice, st));
     rc = vfpi::setup_step_matrix(ws, d, *cfg, nullptr, st, h->err, h->launches, d_nc);
     if (rc) return rc;
-    CK(cudaMemsetAsync(ws.vbuf.p, 0, 3 * 8 * npad, st));
+    // (v ring: buffers 0 and 2 get the warm start, buffer 1 is written before it is read;
+    // impulses and J_c^T lam slots of the live contacts are zeroed by the contact kernels)
     CK(cudaMemcpyAsync(vb, fb->warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(vb + 2 * npad, fb->warm.p, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemsetAsync(ws.lambuf.p, 0, 2 * 24 * (size_t)ncmax, st));
     CK(cudaMemsetAsync(ws.status.p, 0, sizeof(vfpi::SolveStatus) * (size_t)S, st));
     if (vfpi::node_slots_refresh(fb->nbd, S, ncmax, d.col_i, d.col_j, d_nc, st)) {
       h->err = "node slot refresh failed";
@@ -1578,10 +1577,6 @@ int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi
     rc = vfpi::launch_iterate_nodes(p, fb->nbd, cfg->op, cheb, 1, st, h->err, nmode);
     if (rc) return rc;
     CK(cudaEventRecord(fb->run_ev[3 + 2 * k], st));
-    if (fb->nbd.scene_perm) {  // next step: longest predicted scenes first
-      vfpi::launch_scene_order(S, P<vfpi::SolveStatus>(ws.status), const_cast<int*>(fb->nbd.scene_perm), st);
-      ++h->launches;
-    }
     // (3b) diverged scenes: the flagged contact-free CG step, decided on the device
     const int64_t ns = 3 * (int64_t)fb->Nn;
     if (vfpi::launch_cg_scenes_status(S, ns, fb->A.indptr, fb->A.indices, fb->A.data, P<double>(fb->b),
@@ -1596,8 +1591,9 @@ int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi
                              P<double>(fb->warm), st);
     vfpi::launch_fem_run_stats(S, P<vfpi::SolveStatus>(ws.status), P<int>(fb->cts), k,
                                P<unsigned long long>(fb->run_acc), iterations ? P<int>(fb->run_its) : nullptr,
-                               contacts ? P<int>(fb->run_cts) : nullptr, st);
-    h->launches += 14;  // rhs, flags, scan x2, scene pointers, contacts, W/tie/gamma x3, slots, kernel, CG, advance, stats
+                               contacts ? P<int>(fb->run_cts) : nullptr, st,
+                               const_cast<int*>(fb->nbd.scene_perm));  // + the next step's longest-first order
+    h->launches += 12;  // rhs, scan x2, detection, W/tie/gamma x3, slots, kernel, CG, advance, stats + order
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(fb->run_ev[1], st));

@@ -4,6 +4,10 @@
 // round trips of the state. Every expression follows the host restatement
 // (scenes.FemCube.system / contacts / advance) operation for operation, so
 // the device pipeline and the host pipeline produce identical bits.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
 #include "vfpi_internal.cuh"
 #include "vfpi_math.cuh"
 
@@ -143,27 +147,38 @@ __global__ void __launch_bounds__(256) k_fem_rhs_nodes(int64_t nslices, int nn, 
   }
 }
 
-// node below the margin of the plane z = 0 (FemCube.contacts)
-__global__ void k_fem_flags(int64_t nodes, const double* __restrict__ x, double margin, int* __restrict__ flag) {
+// Node-plane contacts (FemCube.contacts): a node is in contact when it lies
+// below the margin of the plane z = 0. After the exclusive scan of that
+// predicate over all nodes (scene-ordered compaction), one pass writes the
+// scene pointers cts and every contact's parameters; optionally it zeroes
+// both impulse parities of every contact (the run loop's solve start).
+__global__ void k_fem_detect(int64_t nodes, int S, int nodes_per_scene, const int* __restrict__ pos,
+                             const double* __restrict__ x, const double* __restrict__ v, double margin,
+                             const double* __restrict__ frame, double mu, double neg_beta_dt, double e_rest,
+                             double thr, int* __restrict__ cts, int* __restrict__ ci, int* __restrict__ cj,
+                             double* __restrict__ frames, double* __restrict__ muv, double* __restrict__ mu2v,
+                             double* __restrict__ phi, double* __restrict__ lam0, double* __restrict__ lam1) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k < nodes) flag[k] = x[3 * k + 2] < margin ? 1 : 0;
-}
-
-__global__ void k_fem_contacts(int64_t nodes, const int* __restrict__ flag, const int* __restrict__ pos,
-                               const double* __restrict__ x, const double* __restrict__ v,
-                               const double* __restrict__ frame, double mu, double neg_beta_dt, double e_rest,
-                               double thr, int* __restrict__ ci, int* __restrict__ cj, double* __restrict__ frames,
-                               double* __restrict__ muv, double* __restrict__ mu2v, double* __restrict__ phi) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= nodes || !flag[k]) return;
-  const int c = pos[k];
+  if (k >= nodes) return;
   const double z = x[3 * k + 2];
+  const bool in = z < margin;
+  const int c = pos[k];
+  if (k % nodes_per_scene == 0) cts[k / nodes_per_scene] = c;
+  if (k == nodes - 1) cts[S] = c + (in ? 1 : 0);
+  if (!in) return;
   const double depth = np_max(0.0, -z);        // np.maximum(0.0, -z[nodes])
   double ph = dmul(neg_beta_dt, depth);        // -(beta / dt) * depth
   const double vn = v[3 * k + 2];
   if (fabs(vn) > thr) ph = dadd(ph, dmul(e_rest, np_min(0.0, vn)));  // np.where(rest, ...)
   ci[c] = (int)(3 * k);
   cj[c] = -1;
+  if (lam0) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      lam0[3 * (size_t)c + t] = 0.0;
+      lam1[3 * (size_t)c + t] = 0.0;
+    }
+  }
 #pragma unroll
   for (int t = 0; t < 9; ++t) frames[9 * (size_t)c + t] = frame[t];
   muv[c] = mu;
@@ -171,18 +186,12 @@ __global__ void k_fem_contacts(int64_t nodes, const int* __restrict__ flag, cons
   phi[c] = ph;
 }
 
-// contacts of scene s start at the exclusive prefix of the flags at its first node
-__global__ void k_fem_scene_cts(int S, int nodes_per_scene, const int* __restrict__ flag,
-                                const int* __restrict__ pos, int* __restrict__ cts) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s > S) return;
-  if (s < S) {
-    cts[s] = pos[(int64_t)s * nodes_per_scene];
-  } else {
-    const int64_t last = (int64_t)S * nodes_per_scene - 1;
-    cts[S] = pos[last] + flag[last];
-  }
-}
+struct BelowMargin {  // the contact predicate as a scan input
+  const double* x;
+  double margin;
+  __host__ __device__ int operator()(int64_t k) const { return x[3 * k + 2] < margin ? 1 : 0; }
+};
+using FlagIter = thrust::transform_iterator<BelowMargin, thrust::counting_iterator<int64_t>>;
 
 // midpoint integration (FemCube.advance): x += dt v_hat; v = 2 v_hat - v;
 // the solution also warm-starts the next step
@@ -232,20 +241,23 @@ void launch_fem_rhs_sell(int64_t n, const int64_t* off, const double* sv, const 
   if (n > 0) k_fem_rhs_sell<<<nb(n), 256, 0, st>>>(n, off, sv, sc, x, X, v, m, g, twodt, b);
 }
 
-void launch_fem_flags(int64_t nodes, const double* x, double margin, int* flag, cudaStream_t st) {
-  if (nodes > 0) k_fem_flags<<<nb(nodes), 256, 0, st>>>(nodes, x, margin, flag);
+size_t fem_detect_tmp_bytes(int64_t nodes) {
+  size_t tb = 0;
+  FlagIter it(thrust::counting_iterator<int64_t>(0), BelowMargin{nullptr, 0.0});
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, it, (int*)nullptr, (int)nodes);
+  return tb;
 }
 
-void launch_fem_contacts(int64_t nodes, const int* flag, const int* pos, const double* x, const double* v,
-                         const double* frame, double mu, double neg_beta_dt, double e_rest, double thr, int* ci,
-                         int* cj, double* frames, double* muv, double* mu2v, double* phi, cudaStream_t st) {
-  if (nodes > 0)
-    k_fem_contacts<<<nb(nodes), 256, 0, st>>>(nodes, flag, pos, x, v, frame, mu, neg_beta_dt, e_rest, thr, ci, cj,
-                                             frames, muv, mu2v, phi);
-}
-
-void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int* pos, int* cts, cudaStream_t st) {
-  k_fem_scene_cts<<<nb(S + 1), 256, 0, st>>>(S, nodes_per_scene, flag, pos, cts);
+int launch_fem_detect(int64_t nodes, int S, int nodes_per_scene, const double* x, const double* v, double margin,
+                      void* tmp, size_t tmp_bytes, int* pos, int* cts, const double* frame, double mu,
+                      double neg_beta_dt, double e_rest, double thr, int* ci, int* cj, double* frames, double* muv,
+                      double* mu2v, double* phi, double* lam0, double* lam1, cudaStream_t st) {
+  if (nodes <= 0) return 0;
+  FlagIter it(thrust::counting_iterator<int64_t>(0), BelowMargin{x, margin});
+  if (cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, it, pos, (int)nodes, st) != cudaSuccess) return 1;
+  k_fem_detect<<<nb(nodes), 256, 0, st>>>(nodes, S, nodes_per_scene, pos, x, v, margin, frame, mu, neg_beta_dt,
+                                          e_rest, thr, cts, ci, cj, frames, muv, mu2v, phi, lam0, lam1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st) {
@@ -256,7 +268,7 @@ void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, doubl
 // the atomics give exact, order-independent totals
 __global__ void k_fem_run_stats(int S, const SolveStatus* __restrict__ st, const int* __restrict__ cts, int step,
                                 unsigned long long* __restrict__ acc, int* __restrict__ its_out,
-                                int* __restrict__ cts_out) {
+                                int* __restrict__ cts_out, int* __restrict__ perm) {
   unsigned long long ci = 0, it = 0, dv = 0;
   int mx = 0;
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
@@ -275,6 +287,20 @@ __global__ void k_fem_run_stats(int S, const SolveStatus* __restrict__ st, const
   if (threadIdx.x == 0) {
     atomicAdd(acc + 4, (unsigned long long)cts[S]);
     if (cts_out) cts_out[step] = cts[S];
+  }
+  if (perm) {  // the next step's longest-first scene order (k_scene_order)
+    __shared__ int its[kMaxOrderedScenes];
+    for (int s = threadIdx.x; s < S; s += blockDim.x) its[s] = st[s].iterations;
+    __syncthreads();
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      const int a = its[i];
+      int r = 0;
+      for (int j = 0; j < S; ++j) {
+        const int c = its[j];
+        r += (c > a) || (c == a && j < i);
+      }
+      perm[r] = i;
+    }
   }
 }
 
@@ -313,8 +339,9 @@ __global__ void k_iota_int(int n, int* v) {
 }
 
 void launch_fem_run_stats(int S, const SolveStatus* st, const int* cts, int step, unsigned long long* acc,
-                          int* its_out, int* cts_out, cudaStream_t stream) {
-  k_fem_run_stats<<<1, 1024, 0, stream>>>(S, st, cts, step, acc, its_out, cts_out);
+                          int* its_out, int* cts_out, cudaStream_t stream, int* perm) {
+  k_fem_run_stats<<<1, 1024, 0, stream>>>(S, st, cts, step, acc, its_out, cts_out,
+                                          S <= kMaxOrderedScenes ? perm : nullptr);
 }
 
 void launch_iota_int(int n, int* v, cudaStream_t st) {

@@ -345,16 +345,18 @@ void launch_fem_sell_pack(int64_t n, const int64_t* krp, const int* kc, const do
 void launch_fem_rhs_sell(int64_t n, const int64_t* off, const double* sv, const int* sc, const double* x,
                          const double* X, const double* v, const double* m, const double* g, double twodt, double* b,
                          cudaStream_t st);
-void launch_fem_flags(int64_t nodes, const double* x, double margin, int* flag, cudaStream_t st);
-void launch_fem_contacts(int64_t nodes, const int* flag, const int* pos, const double* x, const double* v,
-                         const double* frame, double mu, double neg_beta_dt, double e_rest, double thr, int* ci,
-                         int* cj, double* frames, double* muv, double* mu2v, double* phi, cudaStream_t st);
-void launch_fem_scene_cts(int S, int nodes_per_scene, const int* flag, const int* pos, int* cts, cudaStream_t st);
+// node-plane detection of a FEM batch: scan of the below-margin predicate
+// (cub, 2 launches) + one pass writing scene pointers and contact parameters
+size_t fem_detect_tmp_bytes(int64_t nodes);
+int launch_fem_detect(int64_t nodes, int S, int nodes_per_scene, const double* x, const double* v, double margin,
+                      void* tmp, size_t tmp_bytes, int* pos, int* cts, const double* frame, double mu,
+                      double neg_beta_dt, double e_rest, double thr, int* ci, int* cj, double* frames, double* muv,
+                      double* mu2v, double* phi, double* lam0, double* lam1, cudaStream_t st);
 void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, double* v, double* warm, cudaStream_t st);
 void launch_csr_matvec(int64_t rows, const int* rp, const int* ci, const double* cx, const double* x, double* y,
                        cudaStream_t st);
 void launch_fem_run_stats(int S, const SolveStatus* st, const int* cts, int step, unsigned long long* acc,
-                          int* its_out, int* cts_out, cudaStream_t stream);
+                          int* its_out, int* cts_out, cudaStream_t stream, int* perm = nullptr);
 void launch_iota_int(int n, int* v, cudaStream_t st);
 
 // ---- configs[3] heightfield detection (vfpi_heightfield.cu) -----------------

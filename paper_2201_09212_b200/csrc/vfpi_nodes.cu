@@ -800,11 +800,14 @@ __global__ void k_ng_contact_check(int n_c, const int* __restrict__ ci, const in
 }
 
 __global__ void k_ng_node_slots(int n_c, const int* __restrict__ ci, const int* __restrict__ cj,
-                                int* __restrict__ node_slot, const int* __restrict__ d_nc = nullptr) {
+                                int* __restrict__ node_slot, const int* __restrict__ d_nc = nullptr,
+                                double* __restrict__ jt = nullptr) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_c || (d_nc && k >= *d_nc)) return;
   node_slot[ci[k] / 3] = kSlotsPerContact * k;
   if (cj[k] >= 0) node_slot[cj[k] / 3] = kSlotsPerContact * k + 3;
+  if (jt)  // J_c^T lam of the contact's slots starts at 0 (only live contacts' slots are read)
+    for (int t = 0; t < kSlotsPerContact; ++t) jt[kSlotsPerContact * (size_t)k + t] = 0.0;
 }
 
 using NbFn = void (*)(IterParams, NodeLayoutDev);
@@ -923,6 +926,10 @@ int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, co
   // global contact slots (6 k); J_c^T lam starts at 0. n_c is the exact count,
   // or with d_nc != nullptr an upper bound and *d_nc (device) the count
   if (cudaMemsetAsync(L.node_slot, 0xff, 4 * (size_t)S * L.nn, st) != cudaSuccess) return 1;
+  if (d_nc) {  // n_c is an upper bound: zero the slots of the live contacts only
+    if (n_c > 0) k_ng_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, ci, cj, L.node_slot, d_nc, L.jt_g);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+  }
   if (n_c > 0) k_ng_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, ci, cj, L.node_slot, d_nc);
   if (cudaMemsetAsync(L.jt_g, 0, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1), st) != cudaSuccess) return 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
