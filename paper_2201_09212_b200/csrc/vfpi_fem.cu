@@ -118,22 +118,37 @@ __global__ void __launch_bounds__(256) k_fem_rhs_nodes(int64_t nslices, int nn, 
   const bool live = p < nn;
   const int node = live ? node_list[(int64_t)scene * nn + p] : 0;
   double k0 = 0.0, k1 = 0.0, k2 = 0.0;
-  for (int k = 0; k < W; ++k) {
-    const unsigned d = __ldcs(kdesc + (off + k) * 32 + lane);
-    const unsigned mk = d >> 23;
-    if (mk) {
-      const int c = 3 * (int)(d & ((1u << 23) - 1u));
-      const double u0 = dsub(x[c], X[c]), u1 = dsub(x[c + 1], X[c + 1]), u2 = dsub(x[c + 2], X[c + 2]);
-      const double* kv = kval + (off + k) * (9 * 32) + lane;
-      if (mk & 0x001) k0 = dadd(k0, dmul(__ldcs(kv + 32 * 0), u0));
-      if (mk & 0x002) k0 = dadd(k0, dmul(__ldcs(kv + 32 * 1), u1));
-      if (mk & 0x004) k0 = dadd(k0, dmul(__ldcs(kv + 32 * 2), u2));
-      if (mk & 0x008) k1 = dadd(k1, dmul(__ldcs(kv + 32 * 3), u0));
-      if (mk & 0x010) k1 = dadd(k1, dmul(__ldcs(kv + 32 * 4), u1));
-      if (mk & 0x020) k1 = dadd(k1, dmul(__ldcs(kv + 32 * 5), u2));
-      if (mk & 0x040) k2 = dadd(k2, dmul(__ldcs(kv + 32 * 6), u0));
-      if (mk & 0x080) k2 = dadd(k2, dmul(__ldcs(kv + 32 * 7), u1));
-      if (mk & 0x100) k2 = dadd(k2, dmul(__ldcs(kv + 32 * 8), u2));
+  // two blocks per step with every load issued first (the 9 value slots of a
+  // block share its 2304-byte line set, so loading absent slots costs no DRAM
+  // traffic); absent entries are still skipped, not added as zeros
+  constexpr int U = 2;
+  for (int k = 0; k < W; k += U) {
+    unsigned mk[U];
+    double kv[U][9], u[U][3];
+#pragma unroll
+    for (int e = 0; e < U; ++e) {
+      const bool in = k + e < W;
+      const unsigned d = in ? __ldcs(kdesc + (off + k + e) * 32 + lane) : 0u;
+      mk[e] = d >> 23;
+      const int c = mk[e] ? 3 * (int)(d & ((1u << 23) - 1u)) : 0;
+      const double* vp = kval + (off + (in ? k + e : k)) * (9 * 32) + lane;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) kv[e][t] = __ldcs(vp + 32 * t);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) u[e][q] = dsub(x[c + q], X[c + q]);
+    }
+#pragma unroll
+    for (int e = 0; e < U; ++e) {
+      const unsigned m = mk[e];
+      if (m & 0x001) k0 = dadd(k0, dmul(kv[e][0], u[e][0]));
+      if (m & 0x002) k0 = dadd(k0, dmul(kv[e][1], u[e][1]));
+      if (m & 0x004) k0 = dadd(k0, dmul(kv[e][2], u[e][2]));
+      if (m & 0x008) k1 = dadd(k1, dmul(kv[e][3], u[e][0]));
+      if (m & 0x010) k1 = dadd(k1, dmul(kv[e][4], u[e][1]));
+      if (m & 0x020) k1 = dadd(k1, dmul(kv[e][5], u[e][2]));
+      if (m & 0x040) k2 = dadd(k2, dmul(kv[e][6], u[e][0]));
+      if (m & 0x080) k2 = dadd(k2, dmul(kv[e][7], u[e][1]));
+      if (m & 0x100) k2 = dadd(k2, dmul(kv[e][8], u[e][2]));
     }
   }
   if (!live) return;
@@ -264,9 +279,31 @@ void launch_fem_advance(int64_t n, double dt, const double* vh, double* x, doubl
   if (n > 0) k_fem_advance<<<nb(n), 256, 0, st>>>(n, dt, vh, x, v, warm);
 }
 
+// scenes by decreasing iteration count of their last solve, ties by index,
+// into perm (one CTA of 1024 threads; S <= kMaxOrderedScenes): one block radix
+// sort of the unique keys (inverted count | scene index)
+__device__ __forceinline__ void scene_order_block(int S, const SolveStatus* __restrict__ st, int* __restrict__ perm) {
+  constexpr int IPT = kMaxOrderedScenes / 1024;
+  using Sort = cub::BlockRadixSort<unsigned, 1024, IPT>;
+  __shared__ typename Sort::TempStorage tmp;
+  unsigned key[IPT];
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    const int sc = threadIdx.x * IPT + u;
+    const unsigned it = (unsigned)min(max(sc < S ? st[sc].iterations : 0, 0), (1 << 20) - 1);
+    key[u] = sc < S ? ((((1u << 20) - 1u - it) << 11) | (unsigned)sc) : 0xffffffffu;
+  }
+  Sort(tmp).Sort(key, 0, 32);
+#pragma unroll
+  for (int u = 0; u < IPT; ++u) {
+    const int r = threadIdx.x * IPT + u;  // blocked arrangement: thread t holds ranks t*IPT ..
+    if (r < S) perm[r] = (int)(key[u] & 0x7ffu);
+  }
+}
+
 // per-step counters of a device-driven run (vfpi_fem_run): integer sums, so
 // the atomics give exact, order-independent totals
-__global__ void k_fem_run_stats(int S, const SolveStatus* __restrict__ st, const int* __restrict__ cts, int step,
+__global__ void __launch_bounds__(1024) k_fem_run_stats(int S, const SolveStatus* __restrict__ st, const int* __restrict__ cts, int step,
                                 unsigned long long* __restrict__ acc, int* __restrict__ its_out,
                                 int* __restrict__ cts_out, int* __restrict__ perm) {
   unsigned long long ci = 0, it = 0, dv = 0;
@@ -288,35 +325,11 @@ __global__ void k_fem_run_stats(int S, const SolveStatus* __restrict__ st, const
     atomicAdd(acc + 4, (unsigned long long)cts[S]);
     if (cts_out) cts_out[step] = cts[S];
   }
-  if (perm) {  // the next step's longest-first scene order (k_scene_order)
-    __shared__ int its[kMaxOrderedScenes];
-    for (int s = threadIdx.x; s < S; s += blockDim.x) its[s] = st[s].iterations;
-    __syncthreads();
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-      const int a = its[i];
-      int r = 0;
-      for (int j = 0; j < S; ++j) {
-        const int c = its[j];
-        r += (c > a) || (c == a && j < i);
-      }
-      perm[r] = i;
-    }
-  }
+  if (perm) scene_order_block(S, st, perm);  // the next step's longest-first scene order
 }
 
 __global__ void __launch_bounds__(1024) k_scene_order(int S, const SolveStatus* __restrict__ st, int* __restrict__ perm) {
-  __shared__ int its[kMaxOrderedScenes];
-  for (int s = threadIdx.x; s < S; s += blockDim.x) its[s] = st[s].iterations;
-  __syncthreads();
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    const int a = its[i];
-    int r = 0;
-    for (int j = 0; j < S; ++j) {
-      const int c = its[j];
-      r += (c > a) || (c == a && j < i);
-    }
-    perm[r] = i;
-  }
+  scene_order_block(S, st, perm);
 }
 
 void launch_fem_rhs_nodes(int S, int nn, int nsl, const int64_t* slice_off, const int* node_list,
