@@ -274,7 +274,8 @@ int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
  * (default 1); key 7 (query, value ignored): 1 if the last scene-batch solve
  * ran the node-block kernel; key 8: small FEM batches run one thread-block cluster
  * per scene (default 1); key 9: force the CTAs per scene (1/2/4/8, 0 = automatic) of FEM
- * batches created afterwards. */
+ * batches created afterwards; key 11: partition weight of a single-node contact, in
+ * node blocks, when a single system is split over the grid (default 8). *
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

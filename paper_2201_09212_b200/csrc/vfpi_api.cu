@@ -63,6 +63,7 @@ struct vfpi_handle {
   int node_kernel = 1;  // FEM batches: node-block SELL kernel when a node layout is set (tuning key 6)
   int node_cluster = 1; // small FEM batches: one thread-block cluster per scene (tuning key 8; set before the layout)
   int node_cluster_force = 0;  // > 0: CTAs per scene of FEM batches created afterwards (tuning key 9)
+  int grid_contact_cost = 8;   // single systems: partition weight of a single-node contact in blocks (key 11)
   int last_node_kernel = 0;
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
@@ -389,6 +390,7 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (key == 6) { h->node_kernel = value != 0; return VFPI_OK; }
   if (key == 7) return h->last_node_kernel;  // query: did the last scene solve use the node-block kernel
   if (key == 8) { h->node_cluster = value != 0; return VFPI_OK; }
+  if (key == 11 && value >= 0) { h->grid_contact_cost = value; return VFPI_OK; }
   if (key == 9 && (value == 0 || value == 1 || value == 2 || value == 4 || value == 8)) {
     h->node_cluster_force = value;
     return VFPI_OK;
@@ -514,7 +516,8 @@ int vfpi_solve_device(vfpi_handle* h, const vfpi_system* d, const vfpi_config* c
     if (bps > 0) {
       G_nodes = bps * ws.num_sms;
       rc = vfpi::node_grid_build(h->ngw, *d, G_nodes, P<int64_t>(ws.row_ptr), P<int>(ws.rowcnt), P<int>(ws.perm),
-                                 P<int>(ws.colof), st, nl, h->err, h->launches);
+                                 P<int>(ws.colof), st, nl, h->err, h->launches,
+                                 h->grid_contact_cost);
       if (rc == VFPI_OK) use_nodes = true;
       else if (rc != VFPI_UNSUPPORTED) return rc;
     }

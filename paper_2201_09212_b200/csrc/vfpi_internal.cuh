@@ -423,13 +423,14 @@ struct NodeLayoutHost {
 };
 struct NodeGridWork {  // single-system node-block layout (rebuilt per solve)
   Workspace::Buf blk_pos, blk_slice, key, key2, val_i, node_list, cnt, node_slot, width, slice_off, flags, vs, jt,
-      tmp, desc, val;
+      tmp, desc, val, wt, wpre;
   int64_t* h_small = nullptr;  // pinned [2]
+  std::vector<int> h_bpos;     // CTA split points of the last build
   int64_t k_total = 0;
 };
 int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t* row_ptr, const int* rowcnt,
                     const int* perm, const int* colof, cudaStream_t st, NodeLayoutDev& out, std::string& err,
-                    int64_t& launches);
+                    int64_t& launches, int contact_cost = 8);
 int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
                       NodeLayoutDev& out, int* d_flags, cudaStream_t st, int cluster,
                       const std::vector<int64_t>& t_off_host);

@@ -710,9 +710,45 @@ __device__ __forceinline__ int ng_owner(const int* __restrict__ blk_pos, int G, 
 
 // distinct block columns of a node's three rows (3-way merge); key sorts the
 // CTA's nodes by decreasing count
-__global__ void k_ng_count(int nn, int G, const int* __restrict__ blk_pos, const int64_t* __restrict__ row_ptr,
-                           const int* __restrict__ rowcnt, const int* __restrict__ perm, const int* __restrict__ colof,
-                           unsigned* __restrict__ key, int* __restrict__ val, int* __restrict__ cnt) {
+// nodes carrying a single-node (S) contact: their lane also runs the contact's
+// one-shot projection inline in the sweep
+__global__ void k_ng_smark(int n_c, const int* __restrict__ ci, const int* __restrict__ cj, int* __restrict__ mark) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n_c && cj[k] < 0) mark[ci[k] / 3] = 1;
+}
+
+// CTA split points of the weighted node sequence: CTA g owns the nodes whose
+// exclusive weight prefix lies in [W g / G, W (g+1) / G)
+__global__ void k_ng_split(int G, int nn, const int64_t* __restrict__ excl, int* __restrict__ bpos) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > G) return;
+  if (g == 0) { bpos[0] = 0; return; }
+  if (g == G) { bpos[G] = nn; return; }
+  const int64_t W = excl[nn];
+  int lo = 0, hi = nn;  // first i with excl[i] * G >= W * g
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (excl[mid] * (int64_t)G < W * (int64_t)g) lo = mid + 1;
+    else hi = mid;
+  }
+  bpos[g] = lo;
+}
+
+// sort key of a node: (owner CTA, decreasing block count)
+__global__ void k_ng_key(int nn, int G, const int* __restrict__ blk_pos, const int* __restrict__ cnt,
+                         unsigned* __restrict__ key, int* __restrict__ val) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  const int g = ng_owner(blk_pos, G, i);
+  key[i] = ((unsigned)g << 12) | (unsigned)(4095 - min(cnt[i], 4095));
+  val[i] = i;
+}
+
+// block count of every node (its 3 rows' distinct block columns) and its
+// partition weight: blocks + (single-node contact ? contact cost : 0)
+__global__ void k_ng_count(int nn, const int64_t* __restrict__ row_ptr, const int* __restrict__ rowcnt,
+                           const int* __restrict__ perm, const int* __restrict__ colof, const int* __restrict__ smark,
+                           int contact_cost, int* __restrict__ cnt, int64_t* __restrict__ wt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   int64_t e[3], end[3];
@@ -731,9 +767,7 @@ __global__ void k_ng_count(int nn, int G, const int* __restrict__ blk_pos, const
       while (e[q] < end[q] && colof[perm[e[q]]] / 3 == bc) ++e[q];
   }
   cnt[i] = c;
-  const int g = ng_owner(blk_pos, G, i);
-  key[i] = ((unsigned)g << 12) | (unsigned)(4095 - min(c, 4095));
-  val[i] = i;
+  wt[i] = c + (smark[i] ? contact_cost : 0);
 }
 
 __global__ void k_ng_widths(int nsl, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_pos,
@@ -937,7 +971,7 @@ int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, co
 
 int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t* row_ptr, const int* rowcnt,
                     const int* perm, const int* colof, cudaStream_t st, NodeLayoutDev& out, std::string& err,
-                    int64_t& launches) {
+                    int64_t& launches, int contact_cost) {
   auto fail = [&](const char* what) {
     err = std::string("node-block layout: ") + what;
     return VFPI_CUDA_ERROR;
@@ -946,26 +980,47 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   if (n % 3 != 0 || n <= 0) return VFPI_UNSUPPORTED;
   const int nn = n / 3;
   if (nn >= (1 << 23)) return VFPI_UNSUPPORTED;
-  // CTA g owns node positions [floor(nn g / G), floor(nn (g+1) / G)) and their ceil(count / 32) slices
-  std::vector<int> bpos((size_t)G + 1), bsl((size_t)G + 1);
-  for (int g = 0; g <= G; ++g) bpos[g] = (int)((int64_t)nn * g / G);
-  bsl[0] = 0;
-  for (int g = 0; g < G; ++g) bsl[g + 1] = bsl[g] + (bpos[g + 1] - bpos[g] + 31) / 32;
-  const int nsl = bsl[G];
+  // CTA g owns a contiguous range of node positions of equal weight (block
+  // count + contact_cost per single-node contact: those lanes also run the
+  // contact's one-shot) and their ceil(count / 32) slices
   if (ensure(w.blk_pos, 4 * ((size_t)G + 1)) || ensure(w.blk_slice, 4 * ((size_t)G + 1)) ||
       ensure(w.key, 4 * (size_t)nn) || ensure(w.key2, 4 * (size_t)nn) || ensure(w.val_i, 4 * (size_t)nn) ||
       ensure(w.node_list, 4 * (size_t)nn) || ensure(w.cnt, 4 * (size_t)nn) || ensure(w.node_slot, 4 * (size_t)nn) ||
-      ensure(w.width, 8 * ((size_t)nsl + 1)) || ensure(w.slice_off, 8 * ((size_t)nsl + 1)) ||
-      ensure(w.flags, 16) || ensure(w.vs, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1)) ||
+      ensure(w.wt, 8 * ((size_t)nn + 1)) || ensure(w.wpre, 8 * ((size_t)nn + 1)) || ensure(w.flags, 16) ||
+      ensure(w.vs, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1)) ||
       ensure(w.jt, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1)))
     return fail("allocation");
   if (!w.h_small && cudaMallocHost(&w.h_small, 16) != cudaSuccess) return fail("pinned allocation");
-  if (cudaMemcpyAsync(w.blk_pos.p, bpos.data(), 4 * ((size_t)G + 1), cudaMemcpyHostToDevice, st) ||
-      cudaMemcpyAsync(w.blk_slice.p, bsl.data(), 4 * ((size_t)G + 1), cudaMemcpyHostToDevice, st) ||
-      cudaMemsetAsync(w.flags.p, 0, 16, st))
-    return fail("upload");
-  k_ng_count<<<nblk(nn), 256, 0, st>>>(nn, G, (const int*)w.blk_pos.p, row_ptr, rowcnt, perm, colof,
-                                       (unsigned*)w.key.p, (int*)w.val_i.p, (int*)w.cnt.p);
+  if (!w.h_bpos.empty() && (int)w.h_bpos.size() != G + 1) w.h_bpos.clear();
+  w.h_bpos.resize((size_t)G + 1);
+  if (cudaMemsetAsync(w.flags.p, 0, 16, st) || cudaMemsetAsync(w.node_slot.p, 0, 4 * (size_t)nn, st) ||
+      cudaMemsetAsync((int64_t*)w.wt.p + nn, 0, 8, st))
+    return fail("memset");
+  if (n_c > 0) k_ng_smark<<<nblk(n_c), 256, 0, st>>>(n_c, d.col_i, d.col_j, (int*)w.node_slot.p);
+  k_ng_count<<<nblk(nn), 256, 0, st>>>(nn, row_ptr, rowcnt, perm, colof, (const int*)w.node_slot.p, contact_cost,
+                                       (int*)w.cnt.p, (int64_t*)w.wt.p);
+  {
+    size_t tw = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tw, (int64_t*)w.wt.p, (int64_t*)w.wpre.p, nn + 1, st);
+    if (ensure(w.tmp, tw)) return fail("allocation");
+    tw = w.tmp.cap;
+    if (cub::DeviceScan::ExclusiveSum(w.tmp.p, tw, (int64_t*)w.wt.p, (int64_t*)w.wpre.p, nn + 1, st))
+      return fail("scan");
+  }
+  k_ng_split<<<nblk(G + 1), 256, 0, st>>>(G, nn, (const int64_t*)w.wpre.p, (int*)w.blk_pos.p);
+  if (cudaMemcpyAsync(w.h_bpos.data(), w.blk_pos.p, 4 * ((size_t)G + 1), cudaMemcpyDeviceToHost, st) ||
+      cudaStreamSynchronize(st))
+    return fail("host read");
+  std::vector<int> bsl((size_t)G + 1);
+  bsl[0] = 0;
+  for (int g = 0; g < G; ++g) bsl[g + 1] = bsl[g] + (w.h_bpos[g + 1] - w.h_bpos[g] + 31) / 32;
+  const int nsl = bsl[G];
+  if (ensure(w.width, 8 * ((size_t)nsl + 1)) || ensure(w.slice_off, 8 * ((size_t)nsl + 1)))
+    return fail("allocation");
+  if (cudaMemcpyAsync(w.blk_slice.p, bsl.data(), 4 * ((size_t)G + 1), cudaMemcpyHostToDevice, st)) return fail("upload");
+  k_ng_key<<<nblk(nn), 256, 0, st>>>(nn, G, (const int*)w.blk_pos.p, (const int*)w.cnt.p, (unsigned*)w.key.p,
+                                     (int*)w.val_i.p);
+  launches += 5 + (n_c > 0);
   if (n_c > 0) k_ng_contact_check<<<nblk(n_c), 256, 0, st>>>(n_c, d.col_i, d.col_j, (int*)w.flags.p);
   int eb = 12;
   while ((1 << (eb - 12)) <= G) ++eb;

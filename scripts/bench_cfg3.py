@@ -31,7 +31,13 @@ def main():
     ap.add_argument("--max-iters", type=int, default=500)
     ap.add_argument("--chebyshev", action="store_true")
     ap.add_argument("--csv", default=None)
+    ap.add_argument("--tune", nargs="*", default=[], help="key=value tuning knobs of the handle (vfpi_set_tuning)")
     a = ap.parse_args()
+    from paper_2201_09212_b200 import _lib
+
+    for kv in a.tune:
+        k, v = kv.split("=")
+        _lib.handle().L.vfpi_set_tuning(_lib.handle().h, int(k), int(v))
     t0 = time.perf_counter()
     blk = HeightfieldBlock(nx=a.nx)
     t_build = time.perf_counter() - t0

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--kv", type=float, default=100.0)
     ap.add_argument("--chebyshev", action="store_true")
     ap.add_argument("--csv", default="", help="write scene 0's per-step metrics in the reference CSV format")
+    ap.add_argument("--tune", nargs="*", default=[], help="key=value tuning knobs of the handle (vfpi_set_tuning)")
     a = ap.parse_args()
     import torch
 
@@ -56,6 +57,10 @@ def main():
         dist.init_process_group("nccl")
     dev = torch.cuda.current_device()
     from paper_2201_09212_b200 import _lib
+
+    for kv in a.tune:
+        k, v = kv.split("=")
+        _lib.handle(dev).L.vfpi_set_tuning(_lib.handle(dev).h, int(k), int(v))
     from paper_2201_09212_b200.pile import CubePile, PileStepper
     from paper_2201_09212_b200.solver import SolverConfig
 
