@@ -414,6 +414,7 @@ struct NodeLayoutDev {
   const unsigned* desc = nullptr;      // [k][lane]: block column | mask << 23
   const double* val = nullptr;         // [k][9][lane]
   const int* scene_perm = nullptr;     // scene batches: CTA (cluster) c runs scene scene_perm[c] (longest first)
+  const int64_t* voff = nullptr;       // packed values (single systems): [k] first value slot of k-step k, [K] total
 };
 struct NodeLayoutHost {
   int nn = 0, nsl = 0;
@@ -423,14 +424,14 @@ struct NodeLayoutHost {
 };
 struct NodeGridWork {  // single-system node-block layout (rebuilt per solve)
   Workspace::Buf blk_pos, blk_slice, key, key2, val_i, node_list, cnt, node_slot, width, slice_off, flags, vs, jt,
-      tmp, desc, val, wt, wpre;
+      tmp, desc, val, wt, wpre, hsh, ek, voff, tot;
   int64_t* h_small = nullptr;  // pinned [2]
   std::vector<int> h_bpos;     // CTA split points of the last build
   int64_t k_total = 0;
 };
 int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t* row_ptr, const int* rowcnt,
                     const int* perm, const int* colof, cudaStream_t st, NodeLayoutDev& out, std::string& err,
-                    int64_t& launches, int contact_cost = 8);
+                    int64_t& launches, int contact_cost = 8, int pack_mode = 2);
 int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d_a_idx, const double* d_a_val,
                       NodeLayoutDev& out, int* d_flags, cudaStream_t st, int cluster,
                       const std::vector<int64_t>& t_off_host);

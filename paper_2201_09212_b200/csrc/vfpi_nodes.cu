@@ -120,6 +120,7 @@ __device__ __forceinline__ void cta_sum3(double a, double b, double c, double* s
 
 struct NbRing {
   unsigned char* base;  // this warp's stages
+  unsigned short* e1;   // packed layouts: per stage, value offset (doubles) of the chunk's second k-step
   unsigned bar0;
   int s_first, s_end, nw;  // the warp's slices: s_first, s_first + nw, ... < s_end
   int ps, pc;              // producer cursor
@@ -144,16 +145,28 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
   unsigned char* sb = r.base + (size_t)stage * kNbStageBytes;
   const unsigned dd = (unsigned)__cvta_generic_to_shared(sb);
   const unsigned dv = (unsigned)__cvta_generic_to_shared(sb + kNbChunk * kDescBytes);
-  const unsigned bd = (unsigned)kk * kDescBytes, bv = (unsigned)kk * kValBytes;
+  const unsigned bd = (unsigned)kk * kDescBytes;
+  unsigned bv;
+  const double* vsrc;
+  if (L.voff) {  // packed: the chunk's k-steps hold E_k (<= 9) value slots per lane
+    const int64_t v0 = L.voff[off + k0];
+    bv = (unsigned)(8 * (L.voff[off + k0 + kk] - v0));
+    vsrc = L.val + v0;
+    r.e1[stage] = (unsigned short)(kk > 1 ? L.voff[off + k0 + 1] - v0 : 0);
+  } else {
+    bv = (unsigned)kk * kValBytes;
+    vsrc = L.val + (off + k0) * (9 * 32);
+  }
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bd + bv) : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
           "r"(dd), "l"(L.desc + (off + k0) * 32), "r"(bd), "r"(bar), "l"(pol)
       : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-          "r"(dv), "l"(L.val + (off + k0) * (9 * 32)), "r"(bv), "r"(bar), "l"(pol)
-      : "memory");
+  if (bv > 0)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(dv), "l"(vsrc), "r"(bv), "r"(bar), "l"(pol)
+        : "memory");
   ++r.pc;
   if (r.pc * kNbChunk >= W) {
     r.pc = 0;
@@ -163,9 +176,12 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
 }
 
 // the three row sums of this lane's node over its slice (width W) out of the ring
-template <class X>
+// (PACKED: a block's present entries sit at consecutive value slots, rank order)
+template <bool MAYPACK, class X>
 __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W, int lane, uint64_t pol, X x,
                                         double& y0, double& y1, double& y2, int nrows_dbg) {
+  static_assert(!MAYPACK || kNbChunk <= 2, "packed layouts stash one k-step offset per stage");
+  const bool packed = MAYPACK && L.voff != nullptr;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int k0 = 0; k0 < W; k0 += kNbChunk) {
     const int kk = min(kNbChunk, W - k0);
@@ -186,16 +202,30 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
           const int c = 3 * (int)(d & kColMask);
           NB_CHECK(c + 2 < nrows_dbg, "gather c=%d n=%d d=%u", c, nrows_dbg, d);
           const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
-          const double* v = vs + 9 * 32 * u;
-          if (m & 0x001) a0 = dadd(a0, dmul(v[32 * 0], x0));
-          if (m & 0x002) a0 = dadd(a0, dmul(v[32 * 1], x1));
-          if (m & 0x004) a0 = dadd(a0, dmul(v[32 * 2], x2));
-          if (m & 0x008) a1 = dadd(a1, dmul(v[32 * 3], x0));
-          if (m & 0x010) a1 = dadd(a1, dmul(v[32 * 4], x1));
-          if (m & 0x020) a1 = dadd(a1, dmul(v[32 * 5], x2));
-          if (m & 0x040) a2 = dadd(a2, dmul(v[32 * 6], x0));
-          if (m & 0x080) a2 = dadd(a2, dmul(v[32 * 7], x1));
-          if (m & 0x100) a2 = dadd(a2, dmul(v[32 * 8], x2));
+          if (packed) {
+            const double* v = vs + (u == 0 ? 0 : (int)r.e1[stage]);
+            int q = 0;  // rank of the entry among the block's present entries
+            if (m & 0x001) { a0 = dadd(a0, dmul(v[32 * q], x0)); ++q; }
+            if (m & 0x002) { a0 = dadd(a0, dmul(v[32 * q], x1)); ++q; }
+            if (m & 0x004) { a0 = dadd(a0, dmul(v[32 * q], x2)); ++q; }
+            if (m & 0x008) { a1 = dadd(a1, dmul(v[32 * q], x0)); ++q; }
+            if (m & 0x010) { a1 = dadd(a1, dmul(v[32 * q], x1)); ++q; }
+            if (m & 0x020) { a1 = dadd(a1, dmul(v[32 * q], x2)); ++q; }
+            if (m & 0x040) { a2 = dadd(a2, dmul(v[32 * q], x0)); ++q; }
+            if (m & 0x080) { a2 = dadd(a2, dmul(v[32 * q], x1)); ++q; }
+            if (m & 0x100) a2 = dadd(a2, dmul(v[32 * q], x2));
+          } else {
+            const double* v = vs + 9 * 32 * u;
+            if (m & 0x001) a0 = dadd(a0, dmul(v[32 * 0], x0));
+            if (m & 0x002) a0 = dadd(a0, dmul(v[32 * 1], x1));
+            if (m & 0x004) a0 = dadd(a0, dmul(v[32 * 2], x2));
+            if (m & 0x008) a1 = dadd(a1, dmul(v[32 * 3], x0));
+            if (m & 0x010) a1 = dadd(a1, dmul(v[32 * 4], x1));
+            if (m & 0x020) a1 = dadd(a1, dmul(v[32 * 5], x2));
+            if (m & 0x040) a2 = dadd(a2, dmul(v[32 * 6], x0));
+            if (m & 0x080) a2 = dadd(a2, dmul(v[32 * 7], x1));
+            if (m & 0x100) a2 = dadd(a2, dmul(v[32 * 8], x2));
+          }
         }
       }
     }
@@ -270,6 +300,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   __shared__ double sm_warp[3 * (kNbThreads / 32)];
   __shared__ double sm_tot[4];
   __shared__ __align__(8) uint64_t ring_bar[kNbThreads / 32][kNbStages];
+  __shared__ unsigned short ring_e1[kNbThreads / 32][kNbStages];
 
   // contact slots (v* / J_c^T lam of contact rows, 6 per contact, global index)
   // live in global memory in every mode: single-node contacts are solved inline
@@ -302,6 +333,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     unsigned char* base = reinterpret_cast<unsigned char*>(smem) + ((cbytes + 127) & ~(size_t)127);
     ring.base = base + (size_t)warp * kNbStages * kNbStageBytes;
     ring.bar0 = (unsigned)__cvta_generic_to_shared(&ring_bar[warp][0]);
+    ring.e1 = &ring_e1[warp][0];
     ring.s_first = s0 + warp;
     ring.s_end = s1;
     ring.nw = nwarps;
@@ -436,7 +468,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
         }
       }
       double y[3];
-      if (W > 0) nb_rows(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n);
+      if (W > 0) nb_rows<GRID>(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n);
       else y[0] = y[1] = y[2] = 0.0;
       if (live) {
         double vstar[3], wrq[3];
@@ -734,13 +766,15 @@ __global__ void k_ng_split(int G, int nn, const int64_t* __restrict__ excl, int*
   bpos[g] = lo;
 }
 
-// sort key of a node: (owner CTA, decreasing block count)
+// sort key of a node: (owner CTA, decreasing block count, hash of its block
+// mask sequence) -- nodes with the same masks share slices, so the packed
+// k-steps' slot counts (max over the slice's lanes) waste little
 __global__ void k_ng_key(int nn, int G, const int* __restrict__ blk_pos, const int* __restrict__ cnt,
-                         unsigned* __restrict__ key, int* __restrict__ val) {
+                         const unsigned* __restrict__ hsh, unsigned* __restrict__ key, int* __restrict__ val) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   const int g = ng_owner(blk_pos, G, i);
-  key[i] = ((unsigned)g << 12) | (unsigned)(4095 - min(cnt[i], 4095));
+  key[i] = ((unsigned)g << 18) | ((unsigned)(127 - min(cnt[i], 127)) << 11) | (hsh ? (hsh[i] & 0x7ffu) : 0u);
   val[i] = i;
 }
 
@@ -748,7 +782,8 @@ __global__ void k_ng_key(int nn, int G, const int* __restrict__ blk_pos, const i
 // partition weight: blocks + (single-node contact ? contact cost : 0)
 __global__ void k_ng_count(int nn, const int64_t* __restrict__ row_ptr, const int* __restrict__ rowcnt,
                            const int* __restrict__ perm, const int* __restrict__ colof, const int* __restrict__ smark,
-                           int contact_cost, int* __restrict__ cnt, int64_t* __restrict__ wt) {
+                           int contact_cost, int* __restrict__ cnt, int64_t* __restrict__ wt,
+                           unsigned* __restrict__ hsh, int64_t* __restrict__ tot) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   int64_t e[3], end[3];
@@ -757,15 +792,29 @@ __global__ void k_ng_count(int nn, const int64_t* __restrict__ row_ptr, const in
     end[q] = e[q] + rowcnt[3 * i + q];
   }
   int c = 0;
+  unsigned h = 2166136261u;
   for (;;) {
     int bc = INT_MAX;
     for (int q = 0; q < 3; ++q)
       if (e[q] < end[q]) bc = min(bc, colof[perm[e[q]]] / 3);
     if (bc == INT_MAX) break;
     ++c;
+    unsigned mask = 0u;
     for (int q = 0; q < 3; ++q)
-      while (e[q] < end[q] && colof[perm[e[q]]] / 3 == bc) ++e[q];
+      while (e[q] < end[q]) {
+        const int col = colof[perm[e[q]]];
+        if (col / 3 != bc) break;
+        mask |= 1u << (3 * q + col % 3);
+        ++e[q];
+      }
+    h = (h ^ mask) * 16777619u;
   }
+  hsh[i] = h ^ (h >> 11) ^ (h >> 22);
+  // totals of blocks and stored entries (the packing decision)
+  int ent = 0;
+  for (int q = 0; q < 3; ++q) ent += rowcnt[3 * i + q];
+  atomicAdd(reinterpret_cast<unsigned long long*>(tot), (unsigned long long)c);
+  atomicAdd(reinterpret_cast<unsigned long long*>(tot) + 1, (unsigned long long)ent);
   cnt[i] = c;
   wt[i] = c + (smark[i] ? contact_cost : 0);
 }
@@ -785,11 +834,16 @@ __global__ void k_ng_widths(int nsl, int G, const int* __restrict__ blk_slice, c
   w[s] = pos < blk_pos[lo + 1] ? cnt[node_list[pos]] : 0;
 }
 
+// packed values: VALS = false writes the descriptors (block column | mask);
+// VALS = true writes each block's present entries, in entry order, to the
+// value slots voff[k] + rank * 32 + lane of its k-step (slots past a lane's
+// own count stay unwritten: no lane reads them)
+template <bool VALS>
 __global__ void k_ng_fill(int nn, int G, const int* __restrict__ blk_slice, const int* __restrict__ blk_pos,
                           const int* __restrict__ node_list, const int64_t* __restrict__ slice_off,
                           const int64_t* __restrict__ row_ptr, const int* __restrict__ rowcnt,
                           const int* __restrict__ perm, const int* __restrict__ colof, const double* __restrict__ data,
-                          unsigned* __restrict__ desc, double* __restrict__ val) {
+                          const int64_t* __restrict__ voff, unsigned* __restrict__ desc, double* __restrict__ val) {
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= nn) return;
   const int g = ng_owner(blk_pos, G, pos);
@@ -810,20 +864,44 @@ __global__ void k_ng_fill(int nn, int G, const int* __restrict__ blk_slice, cons
       if (e[q] < end[q]) bc = min(bc, colof[perm[e[q]]] / 3);
     if (bc == INT_MAX || k >= W) break;
     unsigned mask = 0u;
-    for (int q = 0; q < 3; ++q)
+    int64_t b0[3];
+    for (int q = 0; q < 3; ++q) {
+      b0[q] = e[q];
       while (e[q] < end[q]) {
-        const int ent = perm[e[q]];
-        const int col = colof[ent];
+        const int col = colof[perm[e[q]]];
         if (col / 3 != bc) break;
-        const int t = 3 * q + col % 3;
-        val[((off + k) * 9 + t) * 32 + lane] = data[ent];
-        mask |= 1u << t;
+        mask |= 1u << (3 * q + col % 3);
         ++e[q];
       }
-    desc[(off + k) * 32 + lane] = (mask << kMaskShift) | (unsigned)bc;
+    }
+    if constexpr (VALS) {
+      // packed: rank of entry t among the block's present entries = its slot;
+      // unpacked (voff == nullptr): slot t of the block's 9
+      const int64_t v0 = voff ? voff[off + k] : (off + k) * (9 * 32);
+      for (int q = 0; q < 3; ++q)
+        for (int64_t f = b0[q]; f < e[q]; ++f) {
+          const int ent = perm[f];
+          const int t = 3 * q + colof[ent] % 3;
+          val[v0 + 32 * (voff ? __popc(mask & ((1u << t) - 1u)) : t) + lane] = data[ent];
+        }
+    } else {
+      desc[(off + k) * 32 + lane] = (mask << kMaskShift) | (unsigned)bc;
+    }
     ++k;
   }
-  for (; k < W; ++k) desc[(off + k) * 32 + lane] = 0u;
+  if constexpr (!VALS)
+    for (; k < W; ++k) desc[(off + k) * 32 + lane] = 0u;
+}
+
+// value slots of every k-step: 32 x (max stored entries of the 32 lanes' blocks)
+__global__ void k_ng_ek(int64_t K, const unsigned* __restrict__ desc, int64_t* __restrict__ ek) {
+  const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k > K) return;
+  int e = k < K ? __popc(desc[k * 32 + lane] >> kMaskShift) : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+  if (lane == 0) ek[k] = 32 * (int64_t)e;
 }
 
 __global__ void k_ng_contact_check(int n_c, const int* __restrict__ ci, const int* __restrict__ cj,
@@ -971,7 +1049,7 @@ int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, co
 
 int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t* row_ptr, const int* rowcnt,
                     const int* perm, const int* colof, cudaStream_t st, NodeLayoutDev& out, std::string& err,
-                    int64_t& launches, int contact_cost) {
+                    int64_t& launches, int contact_cost, int pack_mode) {
   auto fail = [&](const char* what) {
     err = std::string("node-block layout: ") + what;
     return VFPI_CUDA_ERROR;
@@ -987,6 +1065,7 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
       ensure(w.key, 4 * (size_t)nn) || ensure(w.key2, 4 * (size_t)nn) || ensure(w.val_i, 4 * (size_t)nn) ||
       ensure(w.node_list, 4 * (size_t)nn) || ensure(w.cnt, 4 * (size_t)nn) || ensure(w.node_slot, 4 * (size_t)nn) ||
       ensure(w.wt, 8 * ((size_t)nn + 1)) || ensure(w.wpre, 8 * ((size_t)nn + 1)) || ensure(w.flags, 16) ||
+      ensure(w.hsh, 4 * (size_t)nn) ||
       ensure(w.vs, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1)) ||
       ensure(w.jt, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1)))
     return fail("allocation");
@@ -997,8 +1076,9 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
       cudaMemsetAsync((int64_t*)w.wt.p + nn, 0, 8, st))
     return fail("memset");
   if (n_c > 0) k_ng_smark<<<nblk(n_c), 256, 0, st>>>(n_c, d.col_i, d.col_j, (int*)w.node_slot.p);
+  if (ensure(w.tot, 16) || cudaMemsetAsync(w.tot.p, 0, 16, st)) return fail("allocation");
   k_ng_count<<<nblk(nn), 256, 0, st>>>(nn, row_ptr, rowcnt, perm, colof, (const int*)w.node_slot.p, contact_cost,
-                                       (int*)w.cnt.p, (int64_t*)w.wt.p);
+                                       (int*)w.cnt.p, (int64_t*)w.wt.p, (unsigned*)w.hsh.p, (int64_t*)w.tot.p);
   {
     size_t tw = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tw, (int64_t*)w.wt.p, (int64_t*)w.wpre.p, nn + 1, st);
@@ -1009,8 +1089,13 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   }
   k_ng_split<<<nblk(G + 1), 256, 0, st>>>(G, nn, (const int64_t*)w.wpre.p, (int*)w.blk_pos.p);
   if (cudaMemcpyAsync(w.h_bpos.data(), w.blk_pos.p, 4 * ((size_t)G + 1), cudaMemcpyDeviceToHost, st) ||
-      cudaStreamSynchronize(st))
+      cudaMemcpyAsync(w.h_small, w.tot.p, 16, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st))
     return fail("host read");
+  // packed values pay where blocks store few of their 9 entries (axis-aligned
+  // meshes: exact zeros); mode 2 also groups a CTA's nodes by block-mask
+  // sequence so the slices' slot counts fit tighter (at some x locality)
+  const bool want_pack = pack_mode > 0 && (double)w.h_small[1] <= 7.0 * (double)w.h_small[0];
+  const bool by_masks = want_pack && pack_mode == 2;
   std::vector<int> bsl((size_t)G + 1);
   bsl[0] = 0;
   for (int g = 0; g < G; ++g) bsl[g + 1] = bsl[g] + (w.h_bpos[g + 1] - w.h_bpos[g] + 31) / 32;
@@ -1018,12 +1103,13 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   if (ensure(w.width, 8 * ((size_t)nsl + 1)) || ensure(w.slice_off, 8 * ((size_t)nsl + 1)))
     return fail("allocation");
   if (cudaMemcpyAsync(w.blk_slice.p, bsl.data(), 4 * ((size_t)G + 1), cudaMemcpyHostToDevice, st)) return fail("upload");
-  k_ng_key<<<nblk(nn), 256, 0, st>>>(nn, G, (const int*)w.blk_pos.p, (const int*)w.cnt.p, (unsigned*)w.key.p,
+  k_ng_key<<<nblk(nn), 256, 0, st>>>(nn, G, (const int*)w.blk_pos.p, (const int*)w.cnt.p,
+                                     by_masks ? (const unsigned*)w.hsh.p : nullptr, (unsigned*)w.key.p,
                                      (int*)w.val_i.p);
   launches += 5 + (n_c > 0);
   if (n_c > 0) k_ng_contact_check<<<nblk(n_c), 256, 0, st>>>(n_c, d.col_i, d.col_j, (int*)w.flags.p);
-  int eb = 12;
-  while ((1 << (eb - 12)) <= G) ++eb;
+  int eb = 18;
+  while ((1 << (eb - 18)) <= G) ++eb;
   size_t tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned*)w.key.p, (unsigned*)w.key2.p, (int*)w.val_i.p,
                                   (int*)w.node_list.p, nn, 0, eb, st);
@@ -1046,14 +1132,37 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
     return fail("host read");
   if (((int*)(w.h_small + 1))[0]) return VFPI_UNSUPPORTED;  // a contact column is not node aligned
   const int64_t K = w.h_small[0];
+  // packed values: k-step k keeps 32 x E_k slots (E_k = the most entries any of
+  // its lanes' blocks stores), no zeros for absent entries
   if (ensure(w.desc, 4 * 32 * (size_t)std::max<int64_t>(K, 1)) ||
-      ensure(w.val, 8 * 9 * 32 * (size_t)std::max<int64_t>(K, 1)))
+      ensure(w.val, 8 * 9 * 32 * (size_t)std::max<int64_t>(K, 1)) || ensure(w.ek, 8 * ((size_t)K + 1)) ||
+      ensure(w.voff, 8 * ((size_t)K + 1)))
     return fail("allocation");
-  if (cudaMemsetAsync(w.val.p, 0, 8 * 9 * 32 * (size_t)K, st) || cudaMemsetAsync(w.desc.p, 0, 4 * 32 * (size_t)K, st))
+  if (cudaMemsetAsync(w.desc.p, 0, 4 * 32 * (size_t)K, st))
     return fail("memset");  // padding lanes past a CTA's last node are never filled
-  k_ng_fill<<<nblk(nn, 128), 128, 0, st>>>(nn, G, (const int*)w.blk_slice.p, (const int*)w.blk_pos.p,
-                                           (const int*)w.node_list.p, (const int64_t*)w.slice_off.p, row_ptr, rowcnt,
-                                           perm, colof, d.data, (unsigned*)w.desc.p, (double*)w.val.p);
+  k_ng_fill<false><<<nblk(nn, 128), 128, 0, st>>>(nn, G, (const int*)w.blk_slice.p, (const int*)w.blk_pos.p,
+                                                  (const int*)w.node_list.p, (const int64_t*)w.slice_off.p, row_ptr,
+                                                  rowcnt, perm, colof, d.data, nullptr, (unsigned*)w.desc.p, nullptr);
+  k_ng_ek<<<nblk(32 * (K + 1)), 256, 0, st>>>(K, (const unsigned*)w.desc.p, (int64_t*)w.ek.p);
+  {
+    size_t te = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, te, (int64_t*)w.ek.p, (int64_t*)w.voff.p, K + 1, st);
+    if (ensure(w.tmp, te)) return fail("allocation");
+    te = w.tmp.cap;
+    if (cub::DeviceScan::ExclusiveSum(w.tmp.p, te, (int64_t*)w.ek.p, (int64_t*)w.voff.p, K + 1, st))
+      return fail("scan");
+  }
+  // packed only where it saves a fifth of the value bytes (blocks with exact
+  // zeros, e.g. unrotated meshes); full blocks stream faster unpacked
+  if (cudaMemcpyAsync(w.h_small, (int64_t*)w.voff.p + K, 8, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st))
+    return fail("host read");
+  const bool packed = want_pack && (double)w.h_small[0] <= 0.8 * 288.0 * (double)K;
+  k_ng_fill<true><<<nblk(nn, 128), 128, 0, st>>>(nn, G, (const int*)w.blk_slice.p, (const int*)w.blk_pos.p,
+                                                 (const int*)w.node_list.p, (const int64_t*)w.slice_off.p, row_ptr,
+                                                 rowcnt, perm, colof, d.data,
+                                                 packed ? (const int64_t*)w.voff.p : nullptr, nullptr,
+                                                 (double*)w.val.p);
+  launches += 4;
   if (cudaMemsetAsync(w.node_slot.p, 0xff, 4 * (size_t)nn, st)) return fail("memset");
   if (n_c > 0) k_ng_node_slots<<<nblk(n_c), 256, 0, st>>>(n_c, d.col_i, d.col_j, (int*)w.node_slot.p);
   if (cudaMemsetAsync(w.jt.p, 0, 8 * kSlotsPerContact * (size_t)std::max(n_c, 1), st)) return fail("memset");
@@ -1070,6 +1179,7 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   out.slice_off = (const int64_t*)w.slice_off.p;
   out.desc = (const unsigned*)w.desc.p;
   out.val = (const double*)w.val.p;
+  out.voff = packed ? (const int64_t*)w.voff.p : nullptr;
   out.vs_g = (double*)w.vs.p;
   out.jt_g = (double*)w.jt.p;
   return VFPI_OK;
