@@ -67,3 +67,29 @@ def test_product_path_does_not_import_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+
+
+def _decls_outside_comments():
+    txt = re.sub(r"/\*.*?\*/", " ", open(HEADER).read(), flags=re.S)
+    txt = re.sub(r"//[^\n]*", " ", txt)
+    return sorted(set(re.findall(r"\b(vfpi_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_declarations_are_live_code():
+    # a declaration swallowed by an unterminated comment would vanish here
+    assert _decls_outside_comments() == declared()
+
+
+@pytest.mark.parametrize("lang", ["c", "c++"])
+def test_header_compiles_standalone(lang, tmp_path):
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc" if lang == "c" else "g++")
+    if cc is None:
+        pytest.skip("no host compiler")
+    src = tmp_path / ("t.c" if lang == "c" else "t.cpp")
+    src.write_text('#include "vfpi.h"\nint main(void) { return vfpi_version() == 1 ? 0 : 1; }\n')
+    r = subprocess.run([cc, "-fsyntax-only", "-Wall", "-Werror", "-I", os.path.dirname(HEADER), str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
