@@ -415,6 +415,11 @@ struct NodeLayoutDev {
   const double* val = nullptr;         // [k][9][lane]
   const int* scene_perm = nullptr;     // scene batches: CTA (cluster) c runs scene scene_perm[c] (longest first)
   const int64_t* voff = nullptr;       // packed values (single systems): [k] first value slot of k-step k, [K] total
+  // FEM batches: the template's block columns [k_scene][32] (-1 = padding); the
+  // kernel takes block columns from here instead of streaming descriptors
+  // (absent entries are stored as +0 and added: bit-neutral, see vfpi_nodes.cu)
+  const int* tcol = nullptr;
+  int64_t k_scene = 0;
 };
 struct NodeLayoutHost {
   int nn = 0, nsl = 0;

@@ -121,6 +121,7 @@ __device__ __forceinline__ void cta_sum3(double a, double b, double c, double* s
 struct NbRing {
   unsigned char* base;  // this warp's stages
   unsigned short* e1;   // packed layouts: per stage, value offset (doubles) of the chunk's second k-step
+  bool nodesc;          // block columns come from the FEM template (no descriptor stream)
   unsigned bar0;
   int s_first, s_end, nw;  // the warp's slices: s_first, s_first + nw, ... < s_end
   int ps, pc;              // producer cursor
@@ -145,7 +146,7 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
   unsigned char* sb = r.base + (size_t)stage * kNbStageBytes;
   const unsigned dd = (unsigned)__cvta_generic_to_shared(sb);
   const unsigned dv = (unsigned)__cvta_generic_to_shared(sb + kNbChunk * kDescBytes);
-  const unsigned bd = (unsigned)kk * kDescBytes;
+  const unsigned bd = r.nodesc ? 0u : (unsigned)kk * kDescBytes;  // FEM batches (one CTA per scene): template columns
   unsigned bv;
   const double* vsrc;
   if (L.voff) {  // packed: the chunk's k-steps hold E_k (<= 9) value slots per lane
@@ -158,10 +159,11 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
     vsrc = L.val + (off + k0) * (9 * 32);
   }
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bd + bv) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-          "r"(dd), "l"(L.desc + (off + k0) * 32), "r"(bd), "r"(bar), "l"(pol)
-      : "memory");
+  if (bd > 0)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(dd), "l"(L.desc + (off + k0) * 32), "r"(bd), "r"(bar), "l"(pol)
+        : "memory");
   if (bv > 0)
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
@@ -177,9 +179,16 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
 
 // the three row sums of this lane's node over its slice (width W) out of the ring
 // (PACKED: a block's present entries sit at consecutive value slots, rank order)
+// tcs (FEM batches): the template block columns of this lane's slice (+ lane),
+// node0 the scene's first global node. Every one of the 9 slots of a block is
+// then added: slots A does not store hold +0, and +0 * x (x finite: every
+// iterate the sweep reads is finite, a non-finite one ends the solve first)
+// is a signed zero that leaves a row sum unchanged -- a sum that starts at +0
+// is never -0 under round-to-nearest -- so the bits equal the masked sum.
 template <bool MAYPACK, class X>
 __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W, int lane, uint64_t pol, X x,
-                                        double& y0, double& y1, double& y2, int nrows_dbg) {
+                                        double& y0, double& y1, double& y2, int nrows_dbg,
+                                        const int* __restrict__ tcs = nullptr, int node0 = 0) {
   static_assert(!MAYPACK || kNbChunk <= 2, "packed layouts stash one k-step offset per stage");
   const bool packed = MAYPACK && L.voff != nullptr;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -193,6 +202,26 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
     const unsigned char* sb = r.base + (size_t)stage * kNbStageBytes;
     const unsigned* ds = reinterpret_cast<const unsigned*>(sb) + lane;
     const double* vs = reinterpret_cast<const double*>(sb + kNbChunk * kDescBytes) + lane;
+    if (tcs) {
+#pragma unroll
+      for (int u = 0; u < kNbChunk; ++u) {
+        if (u < kk) {
+          const int bc = __ldg(tcs + 32 * (k0 + u));
+          const int c = 3 * (node0 + (bc < 0 ? 0 : bc));
+          const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
+          const double* v = vs + 9 * 32 * u;
+          a0 = dadd(a0, dmul(v[32 * 0], x0));
+          a0 = dadd(a0, dmul(v[32 * 1], x1));
+          a0 = dadd(a0, dmul(v[32 * 2], x2));
+          a1 = dadd(a1, dmul(v[32 * 3], x0));
+          a1 = dadd(a1, dmul(v[32 * 4], x1));
+          a1 = dadd(a1, dmul(v[32 * 5], x2));
+          a2 = dadd(a2, dmul(v[32 * 6], x0));
+          a2 = dadd(a2, dmul(v[32 * 7], x1));
+          a2 = dadd(a2, dmul(v[32 * 8], x2));
+        }
+      }
+    } else
 #pragma unroll
     for (int u = 0; u < kNbChunk; ++u) {
       if (u < kk) {
@@ -334,6 +363,9 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     ring.base = base + (size_t)warp * kNbStages * kNbStageBytes;
     ring.bar0 = (unsigned)__cvta_generic_to_shared(&ring_bar[warp][0]);
     ring.e1 = &ring_e1[warp][0];
+    // one CTA per scene (HBM-bound batches): template columns instead of descriptors;
+    // clusters (latency-bound small batches) keep the descriptors next to the values
+    ring.nodesc = MODE == kScene && L.tcol != nullptr;
     ring.s_first = s0 + warp;
     ring.s_end = s1;
     ring.nw = nwarps;
@@ -468,7 +500,10 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
         }
       }
       double y[3];
-      if (W > 0) nb_rows<GRID>(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n);
+      if (W > 0)
+        nb_rows<GRID>(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n,
+                      (MODE == kScene && L.tcol) ? L.tcol + (off - (int64_t)scene * L.k_scene) * 32 + lane : nullptr,
+                      scene * L.nn);
       else y[0] = y[1] = y[2] = 0.0;
       if (live) {
         double vstar[3], wrq[3];
@@ -1002,6 +1037,8 @@ int node_layout_build(NodeLayoutHost& h, int S, const int* d_a_ptr, const int* d
   out.nn = nn;
   out.nsl = nsl;
   out.cluster = CL;
+  out.tcol = (const int*)h.t_bcol.p;
+  out.k_scene = ks;
   out.has_d = 0;  // FEM batches: node-plane contacts only (col_j = -1)
   out.blk_slice = (const int*)h.blk_slice.p;
   out.blk_pos = (const int*)h.blk_pos.p;
