@@ -530,10 +530,11 @@ def run_ours(args):
                      "launches_timed": launches_per_run * args.steps,
                      "note": "achieved/frac: algorithmic bytes per launch = sum over scenes of iterations x "
                              "(12 nnz_num + 4 (n+1) + 32 n) + 128 x contact-iterations (SURVEY §8(d)), i.e. 12 B per "
-                             "stored entry; the node-block layout streams 3x3 blocks (4 B descriptor + 72 B values "
-                             "for up to 9 entries), ~25% fewer bytes, so frac can exceed 1; layout_frac counts the "
-                             "bytes the layout actually streams (the physical HBM fraction); time = CUDA events "
-                             "around each launch on the pipeline stream"},
+                             "stored entry; the node-block layout streams 72 B of values per 3x3 block for up to 9 "
+                             "entries (block columns from the batch's template; clusters add a 4 B descriptor), "
+                             "~30% fewer bytes, so frac can exceed 1; layout_frac counts the bytes the layout "
+                             "actually streams (vfpi_fem_layout_info: the physical HBM fraction); time = CUDA "
+                             "events around each launch on the pipeline stream"},
         "e2e": {"value": e2e_ci_all / e2e_tmax, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "path": "FemBatch(pinned host arrays) -> FemBatch.run(200 steps) -> FemBatch.state (x, v to host)"},

@@ -207,6 +207,12 @@ int vfpi_fem_run(vfpi_fem_batch* fb, const vfpi_config* cfg, int32_t steps, vfpi
  * kernel (identical v and lam; not for Barzilai-Borwein steps). */
 int vfpi_fem_set_node_layout(vfpi_fem_batch* fb, int32_t nodes_per_scene, const int32_t* order, int32_t n_slices,
                              const int64_t* slice_off, const int32_t* block_cols);
+/* The node layout the batch's iteration kernel streams: CTAs per scene
+ * (thread-block cluster size) and the bytes one V-FPI iteration of one scene
+ * moves from memory (block values, descriptors where streamed, and the row
+ * operands b, w, v^(l-1), v^(l)); VFPI_UNSUPPORTED before
+ * vfpi_fem_set_node_layout succeeded. */
+int vfpi_fem_layout_info(vfpi_fem_batch* fb, int32_t* cluster, int64_t* bytes_per_scene_iteration);
 /* Restore the state the batch was created with (x, v; zero warm start),
  * enqueued on the handle's stream: device-to-device, no host traffic. */
 int vfpi_fem_reset(vfpi_fem_batch* fb);

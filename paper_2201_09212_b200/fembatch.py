@@ -55,6 +55,8 @@ def _bind():
         L.vfpi_fem_run.restype = C.c_int
         L.vfpi_fem_run.argtypes = [C.c_void_p, C.POINTER(VfpiConfig), C.c_int32, C.POINTER(_RunStats), _lib._i32p,
                                    _lib._i32p]
+        L.vfpi_fem_layout_info.restype = C.c_int
+        L.vfpi_fem_layout_info.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
         L.vfpi_fem_reset.restype = C.c_int
         L.vfpi_fem_reset.argtypes = [C.c_void_p]
         L.vfpi_fem_state_device.restype = C.c_int
@@ -184,6 +186,7 @@ class FemBatch:
         _raise_for(code, self.h)
         self.fb = out
         self.node_kernel = False
+        self.cluster = 1
         # bytes one iteration of one scene streams with the row-SELL layout: 12 per
         # stored entry + the row operands (the SURVEY §8(d) per-iteration count)
         self.layout_bytes_per_scene_iter = None
@@ -199,9 +202,11 @@ class FemBatch:
                     _raise_for(rc, self.h)
                 self.node_kernel = rc == _lib.OK
                 if self.node_kernel:
-                    # node-block layout: 32 lanes x (4 B descriptor + 9 x 8 B values) per k-step,
-                    # + per row b, w, v_cur, v_next (32 B) + per node list and slot (8 B)
-                    self.layout_bytes_per_scene_iter = int(32 * 76 * soff[-1] + 32 * n0 + 8 * (n0 // 3))
+                    # the bytes the layout streams per scene and iteration (vfpi_fem_layout_info)
+                    cl, by = C.c_int32(), C.c_int64()
+                    _raise_for(self.L.vfpi_fem_layout_info(self.fb, C.byref(cl), C.byref(by)), self.h)
+                    self.cluster = int(cl.value)
+                    self.layout_bytes_per_scene_iter = int(by.value)
 
     @classmethod
     def assembled(cls, plan, X, kd, ad, m3, device=None, node_layout=True, **params):
