@@ -72,6 +72,7 @@ for cfg in ("cfg2", "cfg3", "cfg4"):
                    "layout_bytes_same_launch": step.get("layout_bytes"),
                    "note": "dram = ncu dram__bytes_read.sum + dram__bytes_write.sum of one capture; algorithmic = "
                            "SURVEY 8(d) 12 B/entry rule for that launch's iterations; layout = the node-block "
-                           "layout's streamed bytes (4 + 72 B per 3x3 block + row operands)"},
+                           "layout's streamed bytes (vfpi_fem_layout_info: 72 B of values per 3x3 block, "
+                           "+ 4 B descriptor in cluster mode, + row operands)"},
                   open(os.path.join(prof, f"{pre}_cfg2_traffic.json"), "w"), indent=1)
 print(open(os.path.join(prof, f"{pre}_cfg2_launches_summary.txt")).read()[:2500])
