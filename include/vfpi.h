@@ -283,7 +283,9 @@ int vfpi_get_profile(vfpi_handle* h, long long* out, int64_t max_count);
  * batches created afterwards; key 11: partition weight of a single-node contact, in
  * node blocks, when a single system is split over the grid (default 8); key 12: packed
  * block values for single systems whose blocks store <= 7 of 9 entries on average
- * (0 off, 1 on, 2 on + nodes grouped by block-mask sequence; default 2). */
+ * (0 off, 1 on, 2 on + nodes grouped by block-mask sequence, 3 always -- tests; default 2);
+ * key 13 (query):
+ * 1 if the last single-system grid layout packed its block values. */
 int vfpi_set_tuning(vfpi_handle* h, int key, int value);
 
 /* Pinned host memory helpers (cudaMallocHost) for fast host<->device copies. */

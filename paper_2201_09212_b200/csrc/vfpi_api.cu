@@ -64,7 +64,7 @@ struct vfpi_handle {
   int node_cluster = 1; // small FEM batches: one thread-block cluster per scene (tuning key 8; set before the layout)
   int node_cluster_force = 0;  // > 0: CTAs per scene of FEM batches created afterwards (tuning key 9)
   int grid_contact_cost = 8;   // single systems: partition weight of a single-node contact in blocks (key 11)
-  int grid_pack = 2;           // single systems: packed block values (0 off, 1 auto, 2 auto + mask-grouped nodes; key 12)
+  int grid_pack = 2;           // single systems: packed block values (0 off, 1 auto, 2 auto + mask-grouped nodes, 3 always; key 12)
   int last_node_kernel = 0;
   vfpi::LayoutOptions layout_opt;
   vfpi::AugmentWork aug;
@@ -392,7 +392,8 @@ int vfpi_set_tuning(vfpi_handle* h, int key, int value) {
   if (key == 7) return h->last_node_kernel;  // query: did the last scene solve use the node-block kernel
   if (key == 8) { h->node_cluster = value != 0; return VFPI_OK; }
   if (key == 11 && value >= 0) { h->grid_contact_cost = value; return VFPI_OK; }
-  if (key == 12 && value >= 0 && value <= 2) { h->grid_pack = value; return VFPI_OK; }
+  if (key == 12 && value >= 0 && value <= 3) { h->grid_pack = value; return VFPI_OK; }
+  if (key == 13) return h->ngw.packed ? 1 : 0;  // query: did the last single-system grid layout pack its values
   if (key == 9 && (value == 0 || value == 1 || value == 2 || value == 4 || value == 8)) {
     h->node_cluster_force = value;
     return VFPI_OK;

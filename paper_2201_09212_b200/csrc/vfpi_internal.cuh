@@ -432,6 +432,7 @@ struct NodeGridWork {  // single-system node-block layout (rebuilt per solve)
       tmp, desc, val, wt, wpre, hsh, ek, voff, tot;
   int64_t* h_small = nullptr;  // pinned [2]
   std::vector<int> h_bpos;     // CTA split points of the last build
+  bool packed = false;         // the last build packed its block values
   int64_t k_total = 0;
 };
 int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t* row_ptr, const int* rowcnt,

@@ -1131,8 +1131,8 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   // packed values pay where blocks store few of their 9 entries (axis-aligned
   // meshes: exact zeros); mode 2 also groups a CTA's nodes by block-mask
   // sequence so the slices' slot counts fit tighter (at some x locality)
-  const bool want_pack = pack_mode > 0 && (double)w.h_small[1] <= 7.0 * (double)w.h_small[0];
-  const bool by_masks = want_pack && pack_mode == 2;
+  const bool want_pack = pack_mode == 3 || (pack_mode > 0 && (double)w.h_small[1] <= 7.0 * (double)w.h_small[0]);
+  const bool by_masks = want_pack && pack_mode >= 2;
   std::vector<int> bsl((size_t)G + 1);
   bsl[0] = 0;
   for (int g = 0; g < G; ++g) bsl[g + 1] = bsl[g] + (w.h_bpos[g + 1] - w.h_bpos[g] + 31) / 32;
@@ -1193,7 +1193,7 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   // zeros, e.g. unrotated meshes); full blocks stream faster unpacked
   if (cudaMemcpyAsync(w.h_small, (int64_t*)w.voff.p + K, 8, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st))
     return fail("host read");
-  const bool packed = want_pack && (double)w.h_small[0] <= 0.8 * 288.0 * (double)K;
+  const bool packed = want_pack && (pack_mode == 3 || (double)w.h_small[0] <= 0.8 * 288.0 * (double)K);
   k_ng_fill<true><<<nblk(nn, 128), 128, 0, st>>>(nn, G, (const int*)w.blk_slice.p, (const int*)w.blk_pos.p,
                                                  (const int*)w.node_list.p, (const int64_t*)w.slice_off.p, row_ptr,
                                                  rowcnt, perm, colof, d.data,
@@ -1217,6 +1217,7 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   out.desc = (const unsigned*)w.desc.p;
   out.val = (const double*)w.val.p;
   out.voff = packed ? (const int64_t*)w.voff.p : nullptr;
+  w.packed = packed;
   out.vs_g = (double*)w.vs.p;
   out.jt_g = (double*)w.jt.p;
   return VFPI_OK;
