@@ -123,21 +123,32 @@ struct NbRing {
   unsigned short* e1;   // packed layouts: per stage, value offset (doubles) of the chunk's second k-step
   bool nodesc;          // block columns come from the FEM template (no descriptor stream)
   unsigned bar0;
-  int s_first, s_end, nw;  // the warp's slices: s_first, s_first + nw, ... < s_end
-  int ps, pc;              // producer cursor
+  int s0, s_end, nw, w;    // the CTA's slices [s0, s_end); this warp w takes one per round of nw (serpentine)
+  int pr, pc;              // producer cursor: round, chunk within the slice
   unsigned issued, consumed;
   bool work;
 };
 
+// the warp's slice of round k: rounds alternate direction (serpentine), so
+// with slices sorted by decreasing width every warp gets a wide and a narrow
+// one in turn (a CTA barrier waits for its busiest warp)
+__device__ __forceinline__ int nb_slice(int s0, int nw, int w, int k) {
+  return s0 + k * nw + ((k & 1) ? nw - 1 - w : w);
+}
+
 __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint64_t pol) {
   int64_t off;
-  int W;
+  int W, ps;
   for (;;) {
-    off = L.slice_off[r.ps];
-    W = (int)(L.slice_off[r.ps + 1] - off);
+    ps = nb_slice(r.s0, r.nw, r.w, r.pr);
+    if (ps >= r.s_end) {  // past the warp's last slice: wrap to the next iteration's first
+      r.pr = 0;
+      continue;
+    }
+    off = L.slice_off[ps];
+    W = (int)(L.slice_off[ps + 1] - off);
     if (W > 0) break;
-    r.ps += r.nw;
-    if (r.ps >= r.s_end) r.ps = r.s_first;
+    ++r.pr;
   }
   const int k0 = r.pc * kNbChunk;
   const int kk = min(kNbChunk, W - k0);
@@ -172,8 +183,7 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
   ++r.pc;
   if (r.pc * kNbChunk >= W) {
     r.pc = 0;
-    r.ps += r.nw;
-    if (r.ps >= r.s_end) r.ps = r.s_first;
+    ++r.pr;
   }
 }
 
@@ -366,12 +376,14 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     // one CTA per scene (HBM-bound batches): template columns instead of descriptors;
     // clusters (latency-bound small batches) keep the descriptors next to the values
     ring.nodesc = MODE == kScene && L.tcol != nullptr;
-    ring.s_first = s0 + warp;
+    ring.s0 = s0;
     ring.s_end = s1;
     ring.nw = nwarps;
-    ring.ps = ring.s_first;
+    ring.w = warp;
+    ring.pr = 0;
     bool w = false;
-    for (int s = s0 + warp; s < s1 && !w; s += nwarps) w = L.slice_off[s + 1] > L.slice_off[s];
+    for (int k = 0, s = nb_slice(s0, nwarps, warp, 0); s < s1 && !w; s = nb_slice(s0, nwarps, warp, ++k))
+      w = L.slice_off[s + 1] > L.slice_off[s];
     ring.work = w;
     if (lane == 0) {
       for (int st = 0; st < kNbStages; ++st)
@@ -479,7 +491,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     };
 
     // ---- (1) surrogate sweep, one lane per node -------------------------
-    for (int s = s0 + warp; s < s1; s += nwarps) {
+    for (int k = 0, s = nb_slice(s0, nwarps, warp, 0); s < s1; s = nb_slice(s0, nwarps, warp, ++k)) {
       const int pos = np0 + (s - s0) * 32 + lane;
       const int64_t off = L.slice_off[s];
       const int W = (int)(L.slice_off[s + 1] - off);
