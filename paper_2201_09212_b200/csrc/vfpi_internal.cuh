@@ -454,7 +454,7 @@ void launch_fem_rhs_nodes(int S, int nn, int nsl, const int64_t* slice_off, cons
                           cudaStream_t st);
 int node_slots_refresh(const NodeLayoutDev& L, int S, int n_c, const int* ci, const int* cj, const int* d_nc,
                        cudaStream_t st);
-int node_kernel_smem(int max_ct);
+int node_kernel_smem(int max_ct, int mode = 0);
 // mode: 0 one CTA per scene, 1 one system over a cooperative grid, 2 one cluster per scene
 int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, int mode = 0);
 int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bool cheb, int max_ct, cudaStream_t st,

@@ -77,6 +77,18 @@ constexpr int kNbStages = VFPI_NB_STAGES;
 constexpr int kDescBytes = 32 * 4;          // one k-step of descriptors
 constexpr int kValBytes = 9 * 32 * 8;       // one k-step of block values
 constexpr int kNbStageBytes = kNbChunk * (kDescBytes + kValBytes);
+// packed block values (single-system grid layouts): a stage takes as many
+// k-steps (<= kNbPackMax) as its kNbChunk k-steps of value space hold, so
+// sparse blocks put more x gathers in flight per stage wait
+#ifndef VFPI_NB_PACKMAX
+#define VFPI_NB_PACKMAX 3
+#endif
+constexpr int kNbPackMax = VFPI_NB_PACKMAX;
+constexpr int kNbGridStageBytes = kNbPackMax * kDescBytes + kNbChunk * kValBytes;
+template <bool GRID>
+__host__ __device__ constexpr int nb_stage_bytes() { return GRID ? kNbGridStageBytes : kNbStageBytes; }
+template <bool GRID>
+__host__ __device__ constexpr int nb_desc_area() { return GRID ? kNbPackMax * kDescBytes : kNbChunk * kDescBytes; }
 constexpr int kNbRingBytes = VFPI_NB_WARPS * kNbStages * kNbStageBytes + 128;
 constexpr unsigned kMaskShift = 23;
 constexpr unsigned kColMask = (1u << kMaskShift) - 1u;
@@ -120,7 +132,8 @@ __device__ __forceinline__ void cta_sum3(double a, double b, double c, double* s
 
 struct NbRing {
   unsigned char* base;  // this warp's stages
-  unsigned short* e1;   // packed layouts: per stage, value offset (doubles) of the chunk's second k-step
+  unsigned short* e1;   // packed layouts: per stage [kNbPackMax]: k-steps in the stage, then the value
+                        // offset (doubles) of its k-steps 1.. in the stage
   bool nodesc;          // block columns come from the FEM template (no descriptor stream)
   unsigned bar0;
   int s0, s_end, nw, w;    // the CTA's slices [s0, s_end); this warp w takes one per round of nw (serpentine)
@@ -136,6 +149,7 @@ __device__ __forceinline__ int nb_slice(int s0, int nw, int w, int k) {
   return s0 + k * nw + ((k & 1) ? nw - 1 - w : w);
 }
 
+template <bool GRID>
 __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint64_t pol) {
   int64_t off;
   int W, ps;
@@ -150,25 +164,30 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
     if (W > 0) break;
     ++r.pr;
   }
-  const int k0 = r.pc * kNbChunk;
-  const int kk = min(kNbChunk, W - k0);
+  const int k0 = r.pc;  // k-step of the slice the stage starts at
+  int kk = min(kNbChunk, W - k0);
   const int stage = (int)(r.issued % kNbStages);
   const unsigned bar = r.bar0 + 8u * (unsigned)stage;
-  unsigned char* sb = r.base + (size_t)stage * kNbStageBytes;
+  unsigned char* sb = r.base + (size_t)stage * nb_stage_bytes<GRID>();
   const unsigned dd = (unsigned)__cvta_generic_to_shared(sb);
-  const unsigned dv = (unsigned)__cvta_generic_to_shared(sb + kNbChunk * kDescBytes);
-  const unsigned bd = r.nodesc ? 0u : (unsigned)kk * kDescBytes;  // FEM batches (one CTA per scene): template columns
+  const unsigned dv = (unsigned)__cvta_generic_to_shared(sb + nb_desc_area<GRID>());
   unsigned bv;
   const double* vsrc;
-  if (L.voff) {  // packed: the chunk's k-steps hold E_k (<= 9) value slots per lane
+  if (GRID && L.voff) {  // packed: k-step k holds E_k (<= 9) value slots per lane
     const int64_t v0 = L.voff[off + k0];
+    kk = 1;
+    while (kk < kNbPackMax && k0 + kk < W && 8 * (L.voff[off + k0 + kk + 1] - v0) <= kNbChunk * kValBytes) {
+      r.e1[kNbPackMax * stage + kk] = (unsigned short)(L.voff[off + k0 + kk] - v0);
+      ++kk;
+    }
+    r.e1[kNbPackMax * stage] = (unsigned short)kk;
     bv = (unsigned)(8 * (L.voff[off + k0 + kk] - v0));
     vsrc = L.val + v0;
-    r.e1[stage] = (unsigned short)(kk > 1 ? L.voff[off + k0 + 1] - v0 : 0);
   } else {
     bv = (unsigned)kk * kValBytes;
     vsrc = L.val + (off + k0) * (9 * 32);
   }
+  const unsigned bd = r.nodesc ? 0u : (unsigned)kk * kDescBytes;  // FEM batches (one CTA per scene): template columns
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bd + bv) : "memory");
   if (bd > 0)
     asm volatile(
@@ -180,8 +199,8 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
             "r"(dv), "l"(vsrc), "r"(bv), "r"(bar), "l"(pol)
         : "memory");
-  ++r.pc;
-  if (r.pc * kNbChunk >= W) {
+  r.pc += kk;
+  if (r.pc >= W) {
     r.pc = 0;
     ++r.pr;
   }
@@ -199,19 +218,20 @@ template <bool MAYPACK, class X>
 __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W, int lane, uint64_t pol, X x,
                                         double& y0, double& y1, double& y2, int nrows_dbg,
                                         const int* __restrict__ tcs = nullptr, int node0 = 0) {
-  static_assert(!MAYPACK || kNbChunk <= 2, "packed layouts stash one k-step offset per stage");
+  // MAYPACK = grid mode (its stage layout; packed values when L.voff is set)
   const bool packed = MAYPACK && L.voff != nullptr;
+  constexpr int CHM = MAYPACK ? kNbPackMax : kNbChunk;  // k-steps a stage may hold
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int k0 = 0; k0 < W; k0 += kNbChunk) {
-    const int kk = min(kNbChunk, W - k0);
+  for (int k0 = 0, kk = 0; k0 < W; k0 += kk) {
     const int stage = (int)(r.consumed % kNbStages);
     const unsigned bar = r.bar0 + 8u * (unsigned)stage;
     const unsigned par = (r.consumed / kNbStages) & 1u;
     while (!nb_try_wait(bar, par)) {
     }
-    const unsigned char* sb = r.base + (size_t)stage * kNbStageBytes;
+    kk = packed ? (int)r.e1[kNbPackMax * stage] : min(kNbChunk, W - k0);
+    const unsigned char* sb = r.base + (size_t)stage * nb_stage_bytes<MAYPACK>();
     const unsigned* ds = reinterpret_cast<const unsigned*>(sb) + lane;
-    const double* vs = reinterpret_cast<const double*>(sb + kNbChunk * kDescBytes) + lane;
+    const double* vs = reinterpret_cast<const double*>(sb + nb_desc_area<MAYPACK>()) + lane;
     if (tcs) {
 #pragma unroll
       for (int u = 0; u < kNbChunk; ++u) {
@@ -233,7 +253,7 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
       }
     } else
 #pragma unroll
-    for (int u = 0; u < kNbChunk; ++u) {
+    for (int u = 0; u < CHM; ++u) {
       if (u < kk) {
         const unsigned d = ds[32 * u];
         const unsigned m = d >> kMaskShift;
@@ -242,7 +262,7 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
           NB_CHECK(c + 2 < nrows_dbg, "gather c=%d n=%d d=%u", c, nrows_dbg, d);
           const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
           if (packed) {
-            const double* v = vs + (u == 0 ? 0 : (int)r.e1[stage]);
+            const double* v = vs + (u == 0 ? 0 : (int)r.e1[kNbPackMax * stage + u]);
             int q = 0;  // rank of the entry among the block's present entries
             if (m & 0x001) { a0 = dadd(a0, dmul(v[32 * q], x0)); ++q; }
             if (m & 0x002) { a0 = dadd(a0, dmul(v[32 * q], x1)); ++q; }
@@ -271,7 +291,7 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
     __syncwarp();
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      nb_issue(r, L, pol);
+      nb_issue<MAYPACK>(r, L, pol);
     }
     ++r.issued;
     ++r.consumed;
@@ -339,7 +359,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   __shared__ double sm_warp[3 * (kNbThreads / 32)];
   __shared__ double sm_tot[4];
   __shared__ __align__(8) uint64_t ring_bar[kNbThreads / 32][kNbStages];
-  __shared__ unsigned short ring_e1[kNbThreads / 32][kNbStages];
+  __shared__ unsigned short ring_e1[kNbThreads / 32][kNbStages * kNbPackMax];
 
   // contact slots (v* / J_c^T lam of contact rows, 6 per contact, global index)
   // live in global memory in every mode: single-node contacts are solved inline
@@ -370,7 +390,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   {
     const size_t cbytes = (size_t)2 * kSlotsPerContact * nct * sizeof(double);
     unsigned char* base = reinterpret_cast<unsigned char*>(smem) + ((cbytes + 127) & ~(size_t)127);
-    ring.base = base + (size_t)warp * kNbStages * kNbStageBytes;
+    ring.base = base + (size_t)warp * kNbStages * nb_stage_bytes<GRID>();
     ring.bar0 = (unsigned)__cvta_generic_to_shared(&ring_bar[warp][0]);
     ring.e1 = &ring_e1[warp][0];
     // one CTA per scene (HBM-bound batches): template columns instead of descriptors;
@@ -391,7 +411,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       if (w)
         for (int st = 0; st < kNbStages; ++st) {
-          nb_issue(ring, L, pol);
+          nb_issue<GRID>(ring, L, pol);
           ++ring.issued;
         }
     }
@@ -1235,8 +1255,9 @@ int node_grid_build(NodeGridWork& w, const vfpi_system& d, int G, const int64_t*
   return VFPI_OK;
 }
 
-int node_kernel_smem(int max_ct) {
+int node_kernel_smem(int max_ct, int mode) {
   (void)max_ct;  // contact slots are global: the ring is the only dynamic shared memory
+  if (mode == kGrid) return VFPI_NB_WARPS * kNbStages * kNbGridStageBytes + 256;
   return kNbRingBytes + 128;
 }
 
@@ -1244,7 +1265,7 @@ int node_kernel_blocks_per_sm(int op, bool cheb, int max_ct, int mode) {
   NbFn f = nb_pick(op, cheb, true, mode);
   if (ensure_max_dynamic_smem((const void*)f) != cudaSuccess) return 0;
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kNbThreads, node_kernel_smem(mode == kScene ? max_ct : 0)) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kNbThreads, node_kernel_smem(mode == kScene ? max_ct : 0, mode)) !=
       cudaSuccess)
     return 0;
   return nb;
@@ -1259,7 +1280,7 @@ int launch_iterate_nodes(const IterParams& p, const NodeLayoutDev& L, int op, bo
     IterParams lp = p;
     NodeLayoutDev ll = L;
     void* args[] = {&lp, &ll};
-    e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kNbThreads), args, node_kernel_smem(0), st);
+    e = cudaLaunchCooperativeKernel((const void*)f, dim3(p.G), dim3(kNbThreads), args, node_kernel_smem(0, kGrid), st);
   } else if (mode == kCluster) {
     cudaLaunchConfig_t c{};
     c.gridDim = dim3((unsigned)(p.G * L.cluster));
