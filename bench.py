@@ -418,6 +418,7 @@ def run_ours(args):
     for fb in batches:
         fb.close()
     e2e_t, e2e_ci = 0.0, 0
+    e2e_split = []
     h2d = d2h = 0
     xh = torch.empty(xs_local.numel(), dtype=torch.float64).pin_memory()
     vh = torch.empty(xs_local.numel(), dtype=torch.float64).pin_memory()
@@ -428,14 +429,19 @@ def run_ours(args):
         t0 = time.perf_counter()
         batches = shard.batches(shard.pinned)
         h2d = sum(fb.h2d_bytes for fb in batches)
+        t1 = time.perf_counter()
         r = one_run()
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
         off = 0
         for fb in batches:
             nb = fb.S * n_scene
             fb.state_into(xh.numpy()[off:off + nb], vh.numpy()[off:off + nb])
             off += nb
         d2h = 2 * 8 * off
-        e2e_t += time.perf_counter() - t0
+        t3 = time.perf_counter()
+        e2e_t += t3 - t0
+        e2e_split.append({"create_s": round(t1 - t0, 4), "run_s": round(t2 - t1, 4), "download_s": round(t3 - t2, 4)})
         e2e_ci += r["ci"]
         for fb in batches:
             fb.close()
@@ -536,7 +542,7 @@ def run_ours(args):
                              "actually streams (vfpi_fem_layout_info: the physical HBM fraction); time = CUDA "
                              "events around each launch on the pipeline stream"},
         "e2e": {"value": e2e_ci_all / e2e_tmax, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps, "rank0_split": e2e_split,
                 "path": "FemBatch(pinned host arrays) -> FemBatch.run(200 steps) -> FemBatch.state (x, v to host)"},
         "gpu_launches": launches,
         "clocks": sampler.summary(),
@@ -638,7 +644,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-subrecords", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="print the rank/device/shard plan only (no GPU)")

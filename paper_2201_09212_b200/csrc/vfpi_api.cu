@@ -303,32 +303,32 @@ void vfpi_destroy(vfpi_handle* h) {
                             &h->ws.lambuf, &h->ws.partials, &h->ws.status, &h->ws.summary, &h->ws.flags,
                             &h->ws.cub_tmp, &h->ws.x, &h->ws.y, &h->ws.prof, &h->ws.cg_vec, &h->ws.cg_part};
   for (auto* b : bufs)
-    if (b->p) cudaFree(b->p);
+    if (b->p) vfpi::dev_free(b->p);
   vfpi::AugmentWork& aw = h->aug;
   for (Workspace::Buf* b : {&aw.pcnt, &aw.poff, &aw.pkey, &aw.pkey2, &aw.pval, &aw.pval2, &aw.head, &aw.hpos, &aw.tmp,
                             &aw.tmp2, &aw.jrow, &aw.jcol_s, &aw.jidx, &aw.jperm, &aw.jcp, &aw.t_row, &aw.t_col,
                             &aw.t_val, &aw.cs, &aw.ccnt, &aw.cptr, &aw.out_p, &aw.out_i, &aw.out_x})
-    if (b->p) cudaFree(b->p);
+    if (b->p) vfpi::dev_free(b->p);
   if (aw.h_small) cudaFreeHost(aw.h_small);
   vfpi::PileWork& pw = h->pile;
   for (Workspace::Buf* b : {&pw.tcnt, &pw.toff, &pw.flag, &pw.key, &pw.key2, &pw.own, &pw.own2, &pw.btri, &pw.best,
                             &pw.gflag, &pw.gpos, &pw.fflag, &pw.fpos, &pw.nvirt, &pw.vpos, &pw.njv, &pw.jpos, &pw.ci,
                             &pw.cj, &pw.fr, &pw.mu, &pw.phi, &pw.jrp, &pw.jci, &pw.jcx, &pw.tmp})
-    if (b->p) cudaFree(b->p);
+    if (b->p) vfpi::dev_free(b->p);
   if (pw.h_small) cudaFreeHost(pw.h_small);
   vfpi::NodalizeWork& nw = h->nod;
   for (Workspace::Buf* b : {&nw.first, &nw.vflag, &nw.vpos, &nw.jcnt, &nw.jpos, &nw.flag, &nw.tmp, &nw.ci, &nw.cj,
                             &nw.fr, &nw.phi, &nw.mu, &nw.mu2, &nw.jrp, &nw.jci, &nw.jcx})
-    if (b->p) cudaFree(b->p);
+    if (b->p) vfpi::dev_free(b->p);
   if (nw.h_small) cudaFreeHost(nw.h_small);
   vfpi::HfWork& hw = h->hf;
   for (auto* b : {&hw.flag, &hw.pos, &hw.tmp, &hw.ci, &hw.cj, &hw.fr, &hw.mu, &hw.phi})
-    if (b->p) cudaFree(b->p);
+    if (b->p) vfpi::dev_free(b->p);
   if (hw.h_small) cudaFreeHost(hw.h_small);
   vfpi::NodeGridWork& gw = h->ngw;
   for (auto* b : {&gw.blk_pos, &gw.blk_slice, &gw.key, &gw.key2, &gw.val_i, &gw.node_list, &gw.cnt, &gw.node_slot,
                   &gw.width, &gw.slice_off, &gw.flags, &gw.vs, &gw.jt, &gw.tmp, &gw.desc, &gw.val})
-    if (b->p) cudaFree(b->p);
+    if (b->p) vfpi::dev_free(b->p);
   if (gw.h_small) cudaFreeHost(gw.h_small);
   for (auto& e : h->ws.ev)
     if (e) cudaEventDestroy(e);
@@ -1262,14 +1262,14 @@ int vfpi_fem_create(vfpi_handle* h, int32_t S, int32_t Nn, const vfpi_system* a,
     Workspace::Buf tb2;
     if (vfpi::ensure(tb2, t2) ||
         cub::DeviceScan::ExclusiveSum(tb2.p, t2, P<int64_t>(wbuf), P<int64_t>(fb->ks_off), (int)(nsl + 1))) {
-      cudaFree(wbuf.p);
-      cudaFree(tb2.p);
+      vfpi::dev_free(wbuf.p);
+      vfpi::dev_free(tb2.p);
       return fail(VFPI_CUDA_ERROR);
     }
     int64_t elems = 0;
     cudaMemcpy(&elems, P<int64_t>(fb->ks_off) + nsl, 8, cudaMemcpyDeviceToHost);
-    cudaFree(wbuf.p);
-    cudaFree(tb2.p);
+    vfpi::dev_free(wbuf.p);
+    vfpi::dev_free(tb2.p);
     if (vfpi::ensure(fb->ks_val, 8 * (size_t)std::max<int64_t>(elems, 1)) ||
         vfpi::ensure(fb->ks_col, 4 * (size_t)std::max<int64_t>(elems, 1)))
       return fail(VFPI_CUDA_ERROR);
@@ -1747,7 +1747,7 @@ void vfpi_fem_destroy(vfpi_fem_batch* fb) {
                             &fb->nbh.t_off, &fb->nbh.t_bcol, &fb->nbh.desc, &fb->nbh.val, &fb->nbh.slice_off,
                             &fb->nbh.node_list, &fb->nbh.node_slot, &fb->nbh.blk_slice, &fb->nbh.blk_pos, &fb->nbh.vs,
                             &fb->nbh.jt, &fb->nbh.perm, &fb->run_acc, &fb->run_its, &fb->run_cts})
-    if (b->p) cudaFree(b->p);
+    if (b->p) vfpi::dev_free(b->p);
   for (cudaEvent_t e : fb->run_ev) cudaEventDestroy(e);
   if (fb->e0) cudaEventDestroy(fb->e0);
   if (fb->e1) cudaEventDestroy(fb->e1);

@@ -226,6 +226,10 @@ struct Workspace {
 };
 
 cudaError_t ensure(Workspace::Buf& b, size_t bytes);
+// the library's device memory cache (vfpi_setup.cu): every Workspace::Buf is
+// allocated and released through these
+cudaError_t dev_alloc(void** p, size_t bytes, size_t* got);
+void dev_free(void* p);
 // Raise a kernel's dynamic shared-memory limit to the device maximum, once per
 // kernel, under a lock (the attribute is process-wide; concurrent solves on
 // several threads must never shrink it under each other).

@@ -9,6 +9,9 @@
 //   fixed-alpha default          solver.py:367-369
 #include <cub/cub.cuh>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <climits>
 
 #include "vfpi_internal.cuh"
@@ -653,16 +656,105 @@ static std::atomic<uint64_t> g_alloc_gen{0};
 
 uint64_t alloc_generation() { return g_alloc_gen.load(); }
 
+// ---- device memory cache ------------------------------------------------------
+// Every device buffer of the library comes from here: a freed buffer is kept
+// (per device, by size) and handed to the next request of 1 to 1.5 times less
+// size, so batches and handles created again and again (a serving loop, the
+// bench's e2e leg) neither pay cudaMalloc/cudaFree -- cudaFree synchronises the
+// device -- nor see their cost vary run to run. At most kPoolCap bytes stay
+// cached; a failing cudaMalloc first returns the device's cached blocks.
+namespace {
+struct PoolBlock { void* p; size_t bytes; int dev; };
+std::mutex g_pool_mu;
+std::multimap<size_t, PoolBlock> g_pool;                       // cached (free) blocks by size
+std::unordered_map<void*, std::pair<size_t, int>> g_live;    // blocks handed out: size, device
+size_t g_pool_bytes = 0;
+constexpr size_t kPoolCap = (size_t)48 << 30;
+
+void pool_release_dev(int dev) {  // caller holds the lock
+  for (auto it = g_pool.begin(); it != g_pool.end();) {
+    if (it->second.dev == dev) {
+      cudaFree(it->second.p);
+      g_pool_bytes -= it->second.bytes;
+      it = g_pool.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+}  // namespace
+
+cudaError_t dev_alloc(void** p, size_t bytes, size_t* got) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (auto it = g_pool.lower_bound(bytes); it != g_pool.end() && it->first <= bytes + bytes / 2; ++it)
+    if (it->second.dev == dev) {
+      *p = it->second.p;
+      *got = it->second.bytes;
+      g_pool_bytes -= it->second.bytes;
+      g_live[*p] = {it->second.bytes, dev};
+      g_pool.erase(it);
+      return cudaSuccess;
+    }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    pool_release_dev(dev);
+    e = cudaMalloc(p, bytes);
+  }
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    *got = 0;
+    return e;
+  }
+  *got = bytes;
+  g_live[*p] = {bytes, dev};
+  return cudaSuccess;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_live.find(p);
+  if (it == g_live.end()) {  // not ours
+    cudaFree(p);
+    return;
+  }
+  const size_t bytes = it->second.first;
+  const int dev = it->second.second;
+  g_live.erase(it);
+  {  // as cudaFree: work still in flight on the device may use the block
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != dev) cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    if (cur != dev) cudaSetDevice(cur);
+  }
+  g_pool.insert({bytes, PoolBlock{p, bytes, dev}});
+  g_pool_bytes += bytes;
+  while (g_pool_bytes > kPoolCap && !g_pool.empty()) {  // over the cap: drop the largest
+    auto last = std::prev(g_pool.end());
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(last->second.dev);
+    cudaFree(last->second.p);
+    cudaSetDevice(cur);
+    g_pool_bytes -= last->second.bytes;
+    g_pool.erase(last);
+  }
+}
+
 cudaError_t ensure(Workspace::Buf& b, size_t bytes) {
   if (bytes == 0) bytes = 8;
   if (b.cap >= bytes) return cudaSuccess;
   g_alloc_gen.fetch_add(1);  // invalidates captured setup graphs
-  if (b.p) cudaFree(b.p);
+  dev_free(b.p);
   b.p = nullptr;
   b.cap = 0;
-  const size_t want = bytes + bytes / 4;
-  cudaError_t e = cudaMalloc(&b.p, want);
-  if (e == cudaSuccess) b.cap = want;
+  size_t got = 0;
+  cudaError_t e = dev_alloc(&b.p, bytes + bytes / 4, &got);
+  if (e == cudaSuccess) b.cap = got;
   return e;
 }
 

@@ -10,6 +10,7 @@ start = previous solution) and integrates on the GPU through ``vfpi_fem_step``
 from __future__ import annotations
 
 import ctypes as C
+import time
 
 import numpy as np
 
@@ -178,6 +179,7 @@ class FemBatch:
         self.h2d_bytes = int(sum(a.nbytes for a in (self._a.indptr, self._a.indices, self._a.data, *self._k, self._m,
                                                      self._g, self._X, x, v)))
         frame = as_f64(contact_frame(np.array([0.0, 0.0, 1.0])).ravel())
+        t0 = time.perf_counter()
         out = C.c_void_p()
         i64p = C.POINTER(C.c_int64)
         code = self.L.vfpi_fem_create(self.h.h, self.S, self.n_scene // 3, self._a.c_struct(), ptr(self._k[0], i64p),
@@ -185,6 +187,7 @@ class FemBatch:
                                       ptr(self._X), ptr(x), ptr(v), ptr(frame), C.byref(prm), C.byref(out))
         _raise_for(code, self.h)
         self.fb = out
+        t1 = time.perf_counter()
         self.node_kernel = False
         self.cluster = 1
         # bytes one iteration of one scene streams with the row-SELL layout: 12 per
@@ -207,6 +210,9 @@ class FemBatch:
                     _raise_for(self.L.vfpi_fem_layout_info(self.fb, C.byref(cl), C.byref(by)), self.h)
                     self.cluster = int(cl.value)
                     self.layout_bytes_per_scene_iter = int(by.value)
+        # wall-clock split of the construction (vfpi_fem_create: uploads + K's row
+        # SELL; vfpi_fem_set_node_layout with the host template)
+        self.timings = {"create_s": t1 - t0, "node_layout_s": time.perf_counter() - t1}
 
     @classmethod
     def assembled(cls, plan, X, kd, ad, m3, device=None, node_layout=True, **params):

@@ -37,7 +37,8 @@ def main():
         for fb in fbs:
             fb.close()
         out.append({"create_s": t1 - t0, "run_s": t2 - t1, "download_s": t3 - t2, "total_s": t3 - t0,
-                    "h2d_bytes": sum(fb.h2d_bytes for fb in fbs)})
+                    "h2d_bytes": sum(fb.h2d_bytes for fb in fbs), "fem_create_s": fbs[0].timings["create_s"],
+                    "node_layout_s": fbs[0].timings["node_layout_s"]})
     print(json.dumps({"workload": "configs[2] e2e breakdown", "reps": out}), flush=True)
 
 
