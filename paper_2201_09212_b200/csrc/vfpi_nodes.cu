@@ -51,6 +51,9 @@ namespace cg = cooperative_groups;
 #ifndef VFPI_NB_WARPS
 #define VFPI_NB_WARPS 8
 #endif
+#ifndef VFPI_NB_HOIST
+#define VFPI_NB_HOIST 1
+#endif
 #ifndef VFPI_NB_MIN_BLOCKS
 #define VFPI_NB_MIN_BLOCKS 2
 #endif
@@ -251,16 +254,34 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
           a2 = dadd(a2, dmul(v[32 * 8], x2));
         }
       }
-    } else
+    } else {
+    // the stage's x gathers first (all of its k-steps' loads in flight at once:
+    // absent blocks and k-steps past kk gather column 0 and are masked out),
+    // then the sums
+    unsigned dsc[CHM];
+    double xg[CHM][3];
+#pragma unroll
+    for (int u = 0; u < CHM; ++u) {
+      dsc[u] = u < kk ? ds[32 * u] : 0u;
+      const int c = (dsc[u] >> kMaskShift) ? 3 * (int)(dsc[u] & kColMask) : 0;
+      NB_CHECK(c + 2 < nrows_dbg, "gather c=%d n=%d d=%u", c, nrows_dbg, dsc[u]);
+#if VFPI_NB_HOIST
+      xg[u][0] = x(c);
+      xg[u][1] = x(c + 1);
+      xg[u][2] = x(c + 2);
+#endif
+    }
 #pragma unroll
     for (int u = 0; u < CHM; ++u) {
       if (u < kk) {
-        const unsigned d = ds[32 * u];
-        const unsigned m = d >> kMaskShift;
+        const unsigned m = dsc[u] >> kMaskShift;
         if (m) {
-          const int c = 3 * (int)(d & kColMask);
-          NB_CHECK(c + 2 < nrows_dbg, "gather c=%d n=%d d=%u", c, nrows_dbg, d);
+#if VFPI_NB_HOIST
+          const double x0 = xg[u][0], x1 = xg[u][1], x2 = xg[u][2];
+#else
+          const int c = 3 * (int)(dsc[u] & kColMask);
           const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
+#endif
           if (packed) {
             const double* v = vs + (u == 0 ? 0 : (int)r.e1[kNbPackMax * stage + u]);
             int q = 0;  // rank of the entry among the block's present entries
@@ -287,6 +308,7 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
           }
         }
       }
+    }
     }
     __syncwarp();
     if (lane == 0) {
