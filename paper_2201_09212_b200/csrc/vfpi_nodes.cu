@@ -51,9 +51,6 @@ namespace cg = cooperative_groups;
 #ifndef VFPI_NB_WARPS
 #define VFPI_NB_WARPS 8
 #endif
-#ifndef VFPI_NB_HOIST
-#define VFPI_NB_HOIST 1
-#endif
 #ifndef VFPI_NB_MIN_BLOCKS
 #define VFPI_NB_MIN_BLOCKS 2
 #endif
@@ -141,6 +138,8 @@ struct NbRing {
   unsigned bar0;
   int s0, s_end, nw, w;    // the CTA's slices [s0, s_end); this warp w takes one per round of nw (serpentine)
   int pr, pc;              // producer cursor: round, chunk within the slice
+  int64_t p_off;           // the producer slice's k-step offset and width
+  int p_W;
   unsigned issued, consumed;
   bool work;
 };
@@ -154,18 +153,24 @@ __device__ __forceinline__ int nb_slice(int s0, int nw, int w, int k) {
 
 template <bool GRID>
 __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint64_t pol) {
-  int64_t off;
-  int W, ps;
-  for (;;) {
-    ps = nb_slice(r.s0, r.nw, r.w, r.pr);
-    if (ps >= r.s_end) {  // past the warp's last slice: wrap to the next iteration's first
-      r.pr = 0;
-      continue;
+  int64_t off = GRID ? r.p_off : 0;
+  int W = GRID ? r.p_W : 0;
+  if (!GRID || r.pc == 0) {  // grids: only a new slice is looked up (mid-slice stages reuse its offset and width)
+    for (;;) {
+      const int ps = nb_slice(r.s0, r.nw, r.w, r.pr);
+      if (ps >= r.s_end) {  // past the warp's last slice: wrap to the next iteration's first
+        r.pr = 0;
+        continue;
+      }
+      off = L.slice_off[ps];
+      W = (int)(L.slice_off[ps + 1] - off);
+      if (W > 0) break;
+      ++r.pr;
     }
-    off = L.slice_off[ps];
-    W = (int)(L.slice_off[ps + 1] - off);
-    if (W > 0) break;
-    ++r.pr;
+    if (GRID) {
+      r.p_off = off;
+      r.p_W = W;
+    }
   }
   const int k0 = r.pc;  // k-step of the slice the stage starts at
   int kk = min(kNbChunk, W - k0);
@@ -177,14 +182,24 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
   unsigned bv;
   const double* vsrc;
   if (GRID && L.voff) {  // packed: k-step k holds E_k (<= 9) value slots per lane
-    const int64_t v0 = L.voff[off + k0];
+    // the value offsets of the stage's candidate k-steps, loaded together (one
+    // latency on the issuing lane's path instead of one per k-step)
+    int64_t vo[kNbPackMax + 1];
+#pragma unroll
+    for (int j = 0; j <= kNbPackMax; ++j) vo[j] = L.voff[off + min(k0 + j, W)];
+    const int64_t v0 = vo[0];
     kk = 1;
-    while (kk < kNbPackMax && k0 + kk < W && 8 * (L.voff[off + k0 + kk + 1] - v0) <= kNbChunk * kValBytes) {
-      r.e1[kNbPackMax * stage + kk] = (unsigned short)(L.voff[off + k0 + kk] - v0);
-      ++kk;
-    }
+#pragma unroll
+    for (int j = 1; j < kNbPackMax; ++j)
+      if (kk == j && k0 + j < W && 8 * (vo[j + 1] - v0) <= kNbChunk * kValBytes) {
+        r.e1[kNbPackMax * stage + j] = (unsigned short)(vo[j] - v0);
+        kk = j + 1;
+      }
     r.e1[kNbPackMax * stage] = (unsigned short)kk;
-    bv = (unsigned)(8 * (L.voff[off + k0 + kk] - v0));
+    int64_t vend = vo[1];
+#pragma unroll
+    for (int j = 2; j <= kNbPackMax; ++j) vend = kk == j ? vo[j] : vend;
+    bv = (unsigned)(8 * (vend - v0));
     vsrc = L.val + v0;
   } else {
     bv = (unsigned)kk * kValBytes;
@@ -220,7 +235,8 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
 template <bool MAYPACK, class X>
 __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W, int lane, uint64_t pol, X x,
                                         double& y0, double& y1, double& y2, int nrows_dbg,
-                                        const int* __restrict__ tcs = nullptr, int node0 = 0) {
+                                        const int* __restrict__ tcs = nullptr, int node0 = 0,
+                                        const double* xv = nullptr) {
   // MAYPACK = grid mode (its stage layout; packed values when L.voff is set)
   const bool packed = MAYPACK && L.voff != nullptr;
   constexpr int CHM = MAYPACK ? kNbPackMax : kNbChunk;  // k-steps a stage may hold
@@ -265,23 +281,26 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
       dsc[u] = u < kk ? ds[32 * u] : 0u;
       const int c = (dsc[u] >> kMaskShift) ? 3 * (int)(dsc[u] & kColMask) : 0;
       NB_CHECK(c + 2 < nrows_dbg, "gather c=%d n=%d d=%u", c, nrows_dbg, dsc[u]);
-#if VFPI_NB_HOIST
-      xg[u][0] = x(c);
-      xg[u][1] = x(c + 1);
-      xg[u][2] = x(c + 2);
-#endif
+      // the node's three x values as two aligned 16-byte loads (two LSU
+      // requests per block instead of three): doubles [c & ~1, +4) hold
+      // c .. c+2 whatever c's parity; the iterate buffers are 32-byte aligned
+      // and padded past n (vfpi_api.cu npad), so the fourth double exists
+      {
+        const double* xa = xv + (c & ~1);
+        const double2 q0 = *reinterpret_cast<const double2*>(xa);
+        const double2 q1 = *reinterpret_cast<const double2*>(xa + 2);
+        const bool odd = c & 1;
+        xg[u][0] = odd ? q0.y : q0.x;
+        xg[u][1] = odd ? q1.x : q0.y;
+        xg[u][2] = odd ? q1.y : q1.x;
+      }
     }
 #pragma unroll
     for (int u = 0; u < CHM; ++u) {
       if (u < kk) {
         const unsigned m = dsc[u] >> kMaskShift;
         if (m) {
-#if VFPI_NB_HOIST
           const double x0 = xg[u][0], x1 = xg[u][1], x2 = xg[u][2];
-#else
-          const int c = 3 * (int)(dsc[u] & kColMask);
-          const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
-#endif
           if (packed) {
             const double* v = vs + (u == 0 ? 0 : (int)r.e1[kNbPackMax * stage + u]);
             int q = 0;  // rank of the entry among the block's present entries
@@ -533,10 +552,21 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     };
 
     // ---- (1) surrogate sweep, one lane per node -------------------------
+    // grids: the next slice's width is loaded a slice ahead (the sweep of a
+    // slice starts with a wait on its width otherwise)
+    int w_next = 0;
+    if (GRID) {
+      const int sf = nb_slice(s0, nwarps, warp, 0);
+      if (sf < s1) w_next = (int)(L.slice_off[sf + 1] - L.slice_off[sf]);
+    }
     for (int k = 0, s = nb_slice(s0, nwarps, warp, 0); s < s1; s = nb_slice(s0, nwarps, warp, ++k)) {
       const int pos = np0 + (s - s0) * 32 + lane;
-      const int64_t off = L.slice_off[s];
-      const int W = (int)(L.slice_off[s + 1] - off);
+      const int64_t off = GRID ? 0 : L.slice_off[s];
+      const int W = GRID ? w_next : (int)(L.slice_off[s + 1] - off);
+      if (GRID) {
+        const int sn = nb_slice(s0, nwarps, warp, k + 1);
+        w_next = sn < s1 ? (int)(L.slice_off[sn + 1] - L.slice_off[sn]) : 0;
+      }
       const bool live = pos < np1;
       int node = 0, slot = -1;
       double bv[3] = {0.0, 0.0, 0.0}, wv[3] = {0.0, 0.0, 0.0}, vc[3] = {0.0, 0.0, 0.0};
@@ -557,7 +587,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       if (W > 0)
         nb_rows<GRID>(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n,
                       (MODE == kScene && L.tcol) ? L.tcol + (off - (int64_t)scene * L.k_scene) * 32 + lane : nullptr,
-                      scene * L.nn);
+                      scene * L.nn, vcur);
       else y[0] = y[1] = y[2] = 0.0;
       if (live) {
         double vstar[3], wrq[3];
