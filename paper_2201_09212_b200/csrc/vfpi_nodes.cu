@@ -252,12 +252,20 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
     const unsigned* ds = reinterpret_cast<const unsigned*>(sb) + lane;
     const double* vs = reinterpret_cast<const double*>(sb + nb_desc_area<MAYPACK>()) + lane;
     if (tcs) {
+      // the stage's x gathers first (a k-step past kk repeats the last one's)
+      double xt[kNbChunk][3];
+#pragma unroll
+      for (int u = 0; u < kNbChunk; ++u) {
+        const int bc = __ldg(tcs + 32 * (k0 + min(u, kk - 1)));
+        const int c = 3 * (node0 + (bc < 0 ? 0 : bc));
+        xt[u][0] = x(c);
+        xt[u][1] = x(c + 1);
+        xt[u][2] = x(c + 2);
+      }
 #pragma unroll
       for (int u = 0; u < kNbChunk; ++u) {
         if (u < kk) {
-          const int bc = __ldg(tcs + 32 * (k0 + u));
-          const int c = 3 * (node0 + (bc < 0 ? 0 : bc));
-          const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
+          const double x0 = xt[u][0], x1 = xt[u][1], x2 = xt[u][2];
           const double* v = vs + 9 * 32 * u;
           a0 = dadd(a0, dmul(v[32 * 0], x0));
           a0 = dadd(a0, dmul(v[32 * 1], x1));
