@@ -51,6 +51,9 @@ namespace cg = cooperative_groups;
 #ifndef VFPI_NB_WARPS
 #define VFPI_NB_WARPS 8
 #endif
+#ifndef VFPI_NB_TCPRE
+#define VFPI_NB_TCPRE 1
+#endif
 #ifndef VFPI_NB_MIN_BLOCKS
 #define VFPI_NB_MIN_BLOCKS 2
 #endif
@@ -241,7 +244,31 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
   const bool packed = MAYPACK && L.voff != nullptr;
   constexpr int CHM = MAYPACK ? kNbPackMax : kNbChunk;  // k-steps a stage may hold
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  // template columns: the block columns of a stage are loaded a stage ahead,
+  // and its x gathers are issued before the wait for its values (neither
+  // depends on the stream); a k-step past the slice repeats the last one's
+  int bcn[kNbChunk];
+#if VFPI_NB_TCPRE
+  if (!MAYPACK && tcs) {
+#pragma unroll
+    for (int u = 0; u < kNbChunk; ++u) bcn[u] = __ldg(tcs + 32 * min(u, W - 1));
+  }
+#endif
   for (int k0 = 0, kk = 0; k0 < W; k0 += kk) {
+    double xt[kNbChunk][3];
+#if VFPI_NB_TCPRE
+    if (!MAYPACK && tcs) {
+#pragma unroll
+      for (int u = 0; u < kNbChunk; ++u) {
+        const int c = 3 * (node0 + (bcn[u] < 0 ? 0 : bcn[u]));
+        xt[u][0] = x(c);
+        xt[u][1] = x(c + 1);
+        xt[u][2] = x(c + 2);
+      }
+#pragma unroll
+      for (int u = 0; u < kNbChunk; ++u) bcn[u] = __ldg(tcs + 32 * min(k0 + kNbChunk + u, W - 1));
+    }
+#endif
     const int stage = (int)(r.consumed % kNbStages);
     const unsigned bar = r.bar0 + 8u * (unsigned)stage;
     const unsigned par = (r.consumed / kNbStages) & 1u;
@@ -252,8 +279,8 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
     const unsigned* ds = reinterpret_cast<const unsigned*>(sb) + lane;
     const double* vs = reinterpret_cast<const double*>(sb + nb_desc_area<MAYPACK>()) + lane;
     if (tcs) {
+#if !VFPI_NB_TCPRE
       // the stage's x gathers first (a k-step past kk repeats the last one's)
-      double xt[kNbChunk][3];
 #pragma unroll
       for (int u = 0; u < kNbChunk; ++u) {
         const int bc = __ldg(tcs + 32 * (k0 + min(u, kk - 1)));
@@ -262,6 +289,7 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
         xt[u][1] = x(c + 1);
         xt[u][2] = x(c + 2);
       }
+#endif
 #pragma unroll
       for (int u = 0; u < kNbChunk; ++u) {
         if (u < kk) {
