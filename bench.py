@@ -537,7 +537,7 @@ def run_ours(args):
                      "note": "achieved/frac: algorithmic bytes per launch = sum over scenes of iterations x "
                              "(12 nnz_num + 4 (n+1) + 32 n) + 128 x contact-iterations (SURVEY §8(d)), i.e. 12 B per "
                              "stored entry; the node-block layout streams 72 B of values per 3x3 block for up to 9 "
-                             "entries (block columns from the batch's template; clusters add a 4 B descriptor), "
+                             "entries (block columns from the batch's template, for one CTA or one cluster per scene), "
                              "~30% fewer bytes, so frac can exceed 1; layout_frac counts the bytes the layout "
                              "actually streams (vfpi_fem_layout_info: the physical HBM fraction); time = CUDA "
                              "events around each launch on the pipeline stream"},

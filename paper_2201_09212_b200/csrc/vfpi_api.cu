@@ -1700,7 +1700,7 @@ int vfpi_fem_layout_info(vfpi_fem_batch* fb, int32_t* cluster, int64_t* bytes_pe
   if (!fb || !cluster || !bytes_per_scene_iteration) return VFPI_BAD_ARGUMENT;
   if (!fb->nb_ready) return VFPI_UNSUPPORTED;
   const int64_t ks = fb->nbd.k_scene;
-  const bool nodesc = fb->nbd.cluster == 1 && fb->nbd.tcol != nullptr;  // one CTA per scene: template columns
+  const bool nodesc = fb->nbd.tcol != nullptr;  // block columns from the template (no descriptor stream)
   *cluster = fb->nbd.cluster;
   // per k-step 32 lanes x (9 values [+ 1 descriptor]); per row b, w, v^(l-1), v^(l); per node its list entry and slot
   *bytes_per_scene_iteration = 32 * ks * (72 + (nodesc ? 0 : 4)) + 32 * 3 * (int64_t)fb->Nn + 8 * (int64_t)fb->Nn;

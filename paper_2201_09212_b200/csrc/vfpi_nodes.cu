@@ -51,9 +51,6 @@ namespace cg = cooperative_groups;
 #ifndef VFPI_NB_WARPS
 #define VFPI_NB_WARPS 8
 #endif
-#ifndef VFPI_NB_TCPRE
-#define VFPI_NB_TCPRE 1
-#endif
 #ifndef VFPI_NB_MIN_BLOCKS
 #define VFPI_NB_MIN_BLOCKS 2
 #endif
@@ -208,7 +205,7 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
     bv = (unsigned)kk * kValBytes;
     vsrc = L.val + (off + k0) * (9 * 32);
   }
-  const unsigned bd = r.nodesc ? 0u : (unsigned)kk * kDescBytes;  // FEM batches (one CTA per scene): template columns
+  const unsigned bd = r.nodesc ? 0u : (unsigned)kk * kDescBytes;  // FEM batches: template columns
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bd + bv) : "memory");
   if (bd > 0)
     asm volatile(
@@ -248,15 +245,12 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
   // and its x gathers are issued before the wait for its values (neither
   // depends on the stream); a k-step past the slice repeats the last one's
   int bcn[kNbChunk];
-#if VFPI_NB_TCPRE
   if (!MAYPACK && tcs) {
 #pragma unroll
     for (int u = 0; u < kNbChunk; ++u) bcn[u] = __ldg(tcs + 32 * min(u, W - 1));
   }
-#endif
   for (int k0 = 0, kk = 0; k0 < W; k0 += kk) {
     double xt[kNbChunk][3];
-#if VFPI_NB_TCPRE
     if (!MAYPACK && tcs) {
 #pragma unroll
       for (int u = 0; u < kNbChunk; ++u) {
@@ -268,7 +262,6 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
 #pragma unroll
       for (int u = 0; u < kNbChunk; ++u) bcn[u] = __ldg(tcs + 32 * min(k0 + kNbChunk + u, W - 1));
     }
-#endif
     const int stage = (int)(r.consumed % kNbStages);
     const unsigned bar = r.bar0 + 8u * (unsigned)stage;
     const unsigned par = (r.consumed / kNbStages) & 1u;
@@ -279,17 +272,6 @@ __device__ __forceinline__ void nb_rows(NbRing& r, const NodeLayoutDev& L, int W
     const unsigned* ds = reinterpret_cast<const unsigned*>(sb) + lane;
     const double* vs = reinterpret_cast<const double*>(sb + nb_desc_area<MAYPACK>()) + lane;
     if (tcs) {
-#if !VFPI_NB_TCPRE
-      // the stage's x gathers first (a k-step past kk repeats the last one's)
-#pragma unroll
-      for (int u = 0; u < kNbChunk; ++u) {
-        const int bc = __ldg(tcs + 32 * (k0 + min(u, kk - 1)));
-        const int c = 3 * (node0 + (bc < 0 ? 0 : bc));
-        xt[u][0] = x(c);
-        xt[u][1] = x(c + 1);
-        xt[u][2] = x(c + 2);
-      }
-#endif
 #pragma unroll
       for (int u = 0; u < kNbChunk; ++u) {
         if (u < kk) {
@@ -470,9 +452,9 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     ring.base = base + (size_t)warp * kNbStages * nb_stage_bytes<GRID>();
     ring.bar0 = (unsigned)__cvta_generic_to_shared(&ring_bar[warp][0]);
     ring.e1 = &ring_e1[warp][0];
-    // one CTA per scene (HBM-bound batches): template columns instead of descriptors;
-    // clusters (latency-bound small batches) keep the descriptors next to the values
-    ring.nodesc = MODE == kScene && L.tcol != nullptr;
+    // FEM batches (one CTA or one cluster per scene): block columns from the batch's
+    // template, loaded a stage ahead, instead of a streamed descriptor
+    ring.nodesc = !GRID && L.tcol != nullptr;
     ring.s0 = s0;
     ring.s_end = s1;
     ring.nw = nwarps;
@@ -622,7 +604,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       double y[3];
       if (W > 0)
         nb_rows<GRID>(ring, L, W, lane, pol, [&](int c) { return vcur[c]; }, y[0], y[1], y[2], p.n,
-                      (MODE == kScene && L.tcol) ? L.tcol + (off - (int64_t)scene * L.k_scene) * 32 + lane : nullptr,
+                      (!GRID && L.tcol) ? L.tcol + (off - (int64_t)scene * L.k_scene) * 32 + lane : nullptr,
                       scene * L.nn, vcur);
       else y[0] = y[1] = y[2] = 0.0;
       if (live) {
