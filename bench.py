@@ -329,7 +329,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    # VFPI_BENCH_FORCE_DIST=1 (under torchrun with one rank): the N > 1 code path --
+    # NCCL init, the closing all-reduce / gather on the pipeline stream, barriers --
+    # on a box with a single GPU
+    if world > 1 or (os.environ.get("VFPI_BENCH_FORCE_DIST") == "1" and "MASTER_ADDR" in os.environ):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)

@@ -63,8 +63,8 @@ for cfg in ("cfg2", "cfg3", "cfg4"):
     if cfg == "cfg2":
         rd = float(d["dram__bytes_read.sum"][0].replace(",", "")) * {"Gbyte": 1e9, "Mbyte": 1e6}[d["dram__bytes_read.sum"][1]]
         wr = float(d["dram__bytes_write.sum"][0].replace(",", "")) * {"Gbyte": 1e9, "Mbyte": 1e6}[d["dram__bytes_write.sum"][1]]
-        lb = json.load(open(os.path.join(out, f"{tag.replace('j', 'i')}_cfg2_launch_bytes.json"))) if os.path.exists(
-            os.path.join(out, f"{tag.replace('j', 'i')}_cfg2_launch_bytes.json")) else None
+        lb = json.load(open(os.path.join(out, f"{tag}_cfg2_launch_bytes.json"))) if os.path.exists(
+            os.path.join(out, f"{tag}_cfg2_launch_bytes.json")) else None
         step = lb["steps"][150] if lb else {}
         json.dump({"kernel": d["Kernel Name"][0], "launch": "node-block kernel launch 150 (configs[2] step 150)",
                    "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
@@ -73,6 +73,8 @@ for cfg in ("cfg2", "cfg3", "cfg4"):
                    "note": "dram = ncu dram__bytes_read.sum + dram__bytes_write.sum of one capture; algorithmic = "
                            "SURVEY 8(d) 12 B/entry rule for that launch's iterations; layout = the node-block "
                            "layout's streamed bytes (vfpi_fem_layout_info: 72 B of values per 3x3 block, "
-                           "+ 4 B descriptor in cluster mode, + row operands)"},
+                           "block columns from the template, + row operands)",
+                   "gpu_time_ms_under_ncu": float(d["gpu__time_duration.sum"][0].replace(",", "")),
+                   "live_loop_ms_same_launch": step.get("loop_ms")},
                   open(os.path.join(prof, f"{pre}_cfg2_traffic.json"), "w"), indent=1)
 print(open(os.path.join(prof, f"{pre}_cfg2_launches_summary.txt")).read()[:2500])
