@@ -51,6 +51,9 @@ namespace cg = cooperative_groups;
 #ifndef VFPI_NB_WARPS
 #define VFPI_NB_WARPS 8
 #endif
+#ifndef VFPI_NB_NODEPRE
+#define VFPI_NB_NODEPRE 1
+#endif
 #ifndef VFPI_NB_MIN_BLOCKS
 #define VFPI_NB_MIN_BLOCKS 2
 #endif
@@ -572,24 +575,39 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     // ---- (1) surrogate sweep, one lane per node -------------------------
     // grids: the next slice's width is loaded a slice ahead (the sweep of a
     // slice starts with a wait on its width otherwise)
-    int w_next = 0;
-    if (GRID) {
+    // so is the lane's node of the next slice (its b, w, v and contact slot
+    // loads start with a wait on it otherwise)
+    int w_next = 0, node_next = 0;
+    {
       const int sf = nb_slice(s0, nwarps, warp, 0);
-      if (sf < s1) w_next = (int)(L.slice_off[sf + 1] - L.slice_off[sf]);
+      if (GRID && sf < s1) w_next = (int)(L.slice_off[sf + 1] - L.slice_off[sf]);
+#if VFPI_NB_NODEPRE
+      const int pf = np0 + (sf - s0) * 32 + lane;
+      if (sf < s1 && pf < np1) node_next = __ldg(L.node_list + pf);
+#endif
     }
     for (int k = 0, s = nb_slice(s0, nwarps, warp, 0); s < s1; s = nb_slice(s0, nwarps, warp, ++k)) {
       const int pos = np0 + (s - s0) * 32 + lane;
       const int64_t off = GRID ? 0 : L.slice_off[s];
       const int W = GRID ? w_next : (int)(L.slice_off[s + 1] - off);
-      if (GRID) {
-        const int sn = nb_slice(s0, nwarps, warp, k + 1);
-        w_next = sn < s1 ? (int)(L.slice_off[sn + 1] - L.slice_off[sn]) : 0;
-      }
       const bool live = pos < np1;
       int node = 0, slot = -1;
+#if VFPI_NB_NODEPRE
+      if (live) node = node_next;
+#endif
+      {
+        const int sn = nb_slice(s0, nwarps, warp, k + 1);
+        if (GRID) w_next = sn < s1 ? (int)(L.slice_off[sn + 1] - L.slice_off[sn]) : 0;
+#if VFPI_NB_NODEPRE
+        const int pn = np0 + (sn - s0) * 32 + lane;
+        if (sn < s1 && pn < np1) node_next = __ldg(L.node_list + pn);
+#endif
+      }
       double bv[3] = {0.0, 0.0, 0.0}, wv[3] = {0.0, 0.0, 0.0}, vc[3] = {0.0, 0.0, 0.0};
       if (live) {
+#if !VFPI_NB_NODEPRE
         node = __ldg(L.node_list + pos);
+#endif
         NB_CHECK(node >= 0 && 3 * node + 2 < p.n, "node=%d np0=%d np1=%d pos=%d", node, np0, np1, pos);
         if (HASC) slot = L.node_slot[node];
         NB_CHECK(slot < 0 || !SHARED_C || slot + 2 < kSlotsPerContact * nct, "slot=%d nct=%d node=%d", slot, nct,
