@@ -51,6 +51,9 @@ namespace cg = cooperative_groups;
 #ifndef VFPI_NB_WARPS
 #define VFPI_NB_WARPS 8
 #endif
+#ifndef VFPI_NB_VOPRE
+#define VFPI_NB_VOPRE 1
+#endif
 #ifndef VFPI_NB_NODEPRE
 #define VFPI_NB_NODEPRE 1
 #endif
@@ -143,6 +146,7 @@ struct NbRing {
   int pr, pc;              // producer cursor: round, chunk within the slice
   int64_t p_off;           // the producer slice's k-step offset and width
   int p_W;
+  unsigned vo_sa;          // packed grids: shared address of the prefetched value offsets [kNbPackMax + 1]
   unsigned issued, consumed;
   bool work;
 };
@@ -188,8 +192,18 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
     // the value offsets of the stage's candidate k-steps, loaded together (one
     // latency on the issuing lane's path instead of one per k-step)
     int64_t vo[kNbPackMax + 1];
+#if VFPI_NB_VOPRE
+    if (k0 != 0) {  // mid-slice: the previous issue prefetched them into shared memory
+      asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
-    for (int j = 0; j <= kNbPackMax; ++j) vo[j] = L.voff[off + min(k0 + j, W)];
+      for (int j = 0; j <= kNbPackMax; ++j)
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(vo[j]) : "r"(r.vo_sa + 8u * (unsigned)j) : "memory");
+    } else
+#endif
+    {
+#pragma unroll
+      for (int j = 0; j <= kNbPackMax; ++j) vo[j] = L.voff[off + min(k0 + j, W)];
+    }
     const int64_t v0 = vo[0];
     kk = 1;
 #pragma unroll
@@ -225,6 +239,17 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
     r.pc = 0;
     ++r.pr;
   }
+#if VFPI_NB_VOPRE
+  else if (GRID && L.voff) {
+    // packed: the next issue's value offsets (same slice) on their way to
+    // shared memory now, so that issue does not wait for them
+#pragma unroll
+    for (int j = 0; j <= kNbPackMax; ++j)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(r.vo_sa + 8u * (unsigned)j),
+                   "l"(L.voff + off + min(r.pc + j, W))
+                   : "memory");
+  }
+#endif
 }
 
 // the three row sums of this lane's node over its slice (width W) out of the ring
@@ -422,6 +447,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
   __shared__ double sm_tot[4];
   __shared__ __align__(8) uint64_t ring_bar[kNbThreads / 32][kNbStages];
   __shared__ unsigned short ring_e1[kNbThreads / 32][kNbStages * kNbPackMax];
+  __shared__ __align__(16) long long ring_vo[kNbThreads / 32][kNbPackMax + 1];
 
   // contact slots (v* / J_c^T lam of contact rows, 6 per contact, global index)
   // live in global memory in every mode: single-node contacts are solved inline
@@ -455,6 +481,7 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     ring.base = base + (size_t)warp * kNbStages * nb_stage_bytes<GRID>();
     ring.bar0 = (unsigned)__cvta_generic_to_shared(&ring_bar[warp][0]);
     ring.e1 = &ring_e1[warp][0];
+    ring.vo_sa = (unsigned)__cvta_generic_to_shared(&ring_vo[warp][0]);
     // FEM batches (one CTA or one cluster per scene): block columns from the batch's
     // template, loaded a stage ahead, instead of a streamed descriptor
     ring.nodesc = !GRID && L.tcol != nullptr;
