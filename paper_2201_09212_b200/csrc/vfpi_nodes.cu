@@ -51,12 +51,6 @@ namespace cg = cooperative_groups;
 #ifndef VFPI_NB_WARPS
 #define VFPI_NB_WARPS 8
 #endif
-#ifndef VFPI_NB_VOPRE
-#define VFPI_NB_VOPRE 1
-#endif
-#ifndef VFPI_NB_NODEPRE
-#define VFPI_NB_NODEPRE 1
-#endif
 #ifndef VFPI_NB_MIN_BLOCKS
 #define VFPI_NB_MIN_BLOCKS 2
 #endif
@@ -192,15 +186,12 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
     // the value offsets of the stage's candidate k-steps, loaded together (one
     // latency on the issuing lane's path instead of one per k-step)
     int64_t vo[kNbPackMax + 1];
-#if VFPI_NB_VOPRE
     if (k0 != 0) {  // mid-slice: the previous issue prefetched them into shared memory
       asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
       for (int j = 0; j <= kNbPackMax; ++j)
         asm volatile("ld.shared.b64 %0, [%1];" : "=l"(vo[j]) : "r"(r.vo_sa + 8u * (unsigned)j) : "memory");
-    } else
-#endif
-    {
+    } else {
 #pragma unroll
       for (int j = 0; j <= kNbPackMax; ++j) vo[j] = L.voff[off + min(k0 + j, W)];
     }
@@ -239,7 +230,6 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
     r.pc = 0;
     ++r.pr;
   }
-#if VFPI_NB_VOPRE
   else if (GRID && L.voff) {
     // packed: the next issue's value offsets (same slice) on their way to
     // shared memory now, so that issue does not wait for them
@@ -249,7 +239,6 @@ __device__ __forceinline__ void nb_issue(NbRing& r, const NodeLayoutDev& L, uint
                    "l"(L.voff + off + min(r.pc + j, W))
                    : "memory");
   }
-#endif
 }
 
 // the three row sums of this lane's node over its slice (width W) out of the ring
@@ -608,10 +597,8 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
     {
       const int sf = nb_slice(s0, nwarps, warp, 0);
       if (GRID && sf < s1) w_next = (int)(L.slice_off[sf + 1] - L.slice_off[sf]);
-#if VFPI_NB_NODEPRE
       const int pf = np0 + (sf - s0) * 32 + lane;
       if (sf < s1 && pf < np1) node_next = __ldg(L.node_list + pf);
-#endif
     }
     for (int k = 0, s = nb_slice(s0, nwarps, warp, 0); s < s1; s = nb_slice(s0, nwarps, warp, ++k)) {
       const int pos = np0 + (s - s0) * 32 + lane;
@@ -619,22 +606,15 @@ __global__ void __launch_bounds__(kNbThreads, VFPI_NB_MIN_BLOCKS) k_iterate_node
       const int W = GRID ? w_next : (int)(L.slice_off[s + 1] - off);
       const bool live = pos < np1;
       int node = 0, slot = -1;
-#if VFPI_NB_NODEPRE
       if (live) node = node_next;
-#endif
       {
         const int sn = nb_slice(s0, nwarps, warp, k + 1);
         if (GRID) w_next = sn < s1 ? (int)(L.slice_off[sn + 1] - L.slice_off[sn]) : 0;
-#if VFPI_NB_NODEPRE
         const int pn = np0 + (sn - s0) * 32 + lane;
         if (sn < s1 && pn < np1) node_next = __ldg(L.node_list + pn);
-#endif
       }
       double bv[3] = {0.0, 0.0, 0.0}, wv[3] = {0.0, 0.0, 0.0}, vc[3] = {0.0, 0.0, 0.0};
       if (live) {
-#if !VFPI_NB_NODEPRE
-        node = __ldg(L.node_list + pos);
-#endif
         NB_CHECK(node >= 0 && 3 * node + 2 < p.n, "node=%d np0=%d np1=%d pos=%d", node, np0, np1, pos);
         if (HASC) slot = L.node_slot[node];
         NB_CHECK(slot < 0 || !SHARED_C || slot + 2 < kSlotsPerContact * nct, "slot=%d nct=%d node=%d", slot, nct,
