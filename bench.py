@@ -30,6 +30,10 @@ K and the state), the 200 steps and the download of the final x and v.
 ``augment_dynamics`` / ``solve_vfpi`` / the harness's CG fallback, with this
 repo's FEM matrices, since the reference has no FEM) on all host cores, one
 scene per process.
+
+``VFPI_BENCH_FORCE_DIST=1`` under ``torchrun --nproc-per-node 1`` runs the
+N > 1 code path (NCCL init, closing all-reduce / gather, barriers) with one
+rank: how that path was exercised on a single-GPU box (scripts/gpu_r2bh.sh).
 """
 
 from __future__ import annotations
