@@ -100,16 +100,7 @@ __global__ void k_fem_rhs_sell(int64_t n, const int64_t* __restrict__ off, const
 // warp per node slice, one lane per node: 3 row sums per lane, blocks in
 // increasing block column, entries of a block in increasing column -- each
 // row's sequence of k_fem_rhs; the masks keep K's explicit zeros)
-#ifndef VFPI_RHS_U
-#define VFPI_RHS_U 2
-#endif
-#ifndef VFPI_RHS_VOLATILE
-#define VFPI_RHS_VOLATILE 0
-#endif
-#ifndef VFPI_RHS_MINB
-#define VFPI_RHS_MINB 1
-#endif
-__global__ void __launch_bounds__(256, VFPI_RHS_MINB) k_fem_rhs_nodes(int64_t nslices, int nn, int nsl,
+__global__ void __launch_bounds__(256) k_fem_rhs_nodes(int64_t nslices, int nn, int nsl,
                                                        const int64_t* __restrict__ slice_off,
                                                        const int* __restrict__ node_list,
                                                        const unsigned* __restrict__ kdesc,
@@ -130,7 +121,7 @@ __global__ void __launch_bounds__(256, VFPI_RHS_MINB) k_fem_rhs_nodes(int64_t ns
   // two blocks per step with every load issued first (the 9 value slots of a
   // block share its 2304-byte line set, so loading absent slots costs no DRAM
   // traffic); absent entries are still skipped, not added as zeros
-  constexpr int U = VFPI_RHS_U;
+  constexpr int U = 2;
   for (int k = 0; k < W; k += U) {
     unsigned mk[U];
     double kv[U][9], u[U][3];
@@ -142,12 +133,7 @@ __global__ void __launch_bounds__(256, VFPI_RHS_MINB) k_fem_rhs_nodes(int64_t ns
       const int c = mk[e] ? 3 * (int)(d & ((1u << 23) - 1u)) : 0;
       const double* vp = kval + (off + (in ? k + e : k)) * (9 * 32) + lane;
 #pragma unroll
-      for (int t = 0; t < 9; ++t)
-#if VFPI_RHS_VOLATILE
-        asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(kv[e][t]) : "l"(vp + 32 * t));
-#else
-        kv[e][t] = __ldcs(vp + 32 * t);
-#endif
+      for (int t = 0; t < 9; ++t) kv[e][t] = __ldcs(vp + 32 * t);
 #pragma unroll
       for (int q = 0; q < 3; ++q) u[e][q] = dsub(x[c + q], X[c + q]);
     }
