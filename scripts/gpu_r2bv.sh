@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-2 GPU pass bv: e2e construction outliers: 6 e2e steps with the nvidia-smi clock sampler running through the e2e leg vs stopped before it
+# round-2 GPU pass bv: e2e construction outliers: 6 e2e steps with the nvidia-smi clock sampler running through the e2e leg vs stopped before it (used a VFPI_BENCH_E2E_SAMPLER switch bench.py had during that session; removed since)
 cd $GRAFT_REPO_ROOT
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out

@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-2 GPU pass bx: bench with the clock sampler stopped before the e2e leg (3 runs), bench contract test, default bench
+# round-2 GPU pass bx: bench with the clock sampler stopped before the e2e leg (3 runs), bench contract test, default bench (bench.py variant of that session; not kept)
 cd $GRAFT_REPO_ROOT
 export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
