@@ -160,6 +160,11 @@ def test_cluster_per_scene_equals_one_cta_per_scene(kw):
         b = FemBatch(_cubes(6, 16, 5))
     finally:
         h.set_node_cluster(True)
+    # the small batch really runs on clusters, and both layouts take their block
+    # columns from the batch's template: no descriptor stream, the same bytes
+    # per scene iteration (vfpi_fem_layout_info)
+    assert a.cluster > 1 and b.cluster == 1
+    assert a.layout_bytes_per_scene_iter == b.layout_bytes_per_scene_iter > 0
     contacts = 0
     for step in range(30):
         sa, sb = a.step(cfg, per_scene=True), b.step(cfg, per_scene=True)
